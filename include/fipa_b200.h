@@ -1,0 +1,127 @@
+/*
+ * fipa_b200.h -- C ABI of the B200-native FlashIPA layer (libfipa_b200.so).
+ *
+ * This is the drop-in boundary for the reference's FlashIPA hot path.  Every entry point
+ * below replaces one reference interface (paths relative to /root/reference/proj):
+ *
+ *   fipa_config / fipa_config_validate   IpaConfig + validate      include/fipa/ipa.hpp:14-32,
+ *                                                                   src/ipa.cpp:12-21
+ *   fipa_layer_create                    (IpaConfig, IpaWeights) pair held by the Python
+ *                                        Model                      python/bindings.cpp:82-101
+ *   fipa_layer_init_weights              IpaWeights::init(cfg, Rng(seed))
+ *                                                                   src/ipa.cpp:172-193
+ *   fipa_layer_set_weights / _get_weights  IpaWeights fields        include/fipa/ipa.hpp:37-50
+ *   fipa_layer_save_weights              save_weights               src/model_io.cpp:121-141
+ *   fipa_layer_load_weights              load_weights               src/model_io.cpp:143-196
+ *   fipa_layer_forward (device buffers)  flash_ipa_forward          src/flash_ipa.cpp:141-218
+ *   fipa_layer_forward_host (host f64)   Model.flash                python/bindings.cpp:122-135
+ *   fipa_last_error + status codes       ValueError / NumericError / IoError
+ *                                                                   include/fipa/error.hpp:10-28
+ *
+ * Differences from the reference, all additive: a leading batch axis B (each sample is an
+ * independent reference call with its own mask), caller-owned device buffers + a CUDA stream,
+ * and a precision switch: FIPA_PREC_BF16 runs the tcgen05 tensor-core path (bf16 operands, fp32
+ * accumulation), FIPA_PREC_F32 the fp32 SIMT path.  There is no CPU fallback: without a
+ * B200 every compute entry point returns FIPA_ERR_CUDA.
+ *
+ * Threading: a layer handle may be used from several threads on distinct streams for
+ * forward calls (weights are read-only during forward); weight mutation is not thread-safe.
+ */
+#ifndef FIPA_B200_H
+#define FIPA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (0 = success).  fipa_last_error() returns the thread's last message. */
+#define FIPA_OK 0
+#define FIPA_ERR_VALUE 1   /* reference ValueError: bad shapes / config / arguments   */
+#define FIPA_ERR_NUMERIC 2 /* reference NumericError                                  */
+#define FIPA_ERR_IO 3      /* reference IoError: weights file problems                */
+#define FIPA_ERR_CUDA 4    /* CUDA runtime / launch failure, or no usable GPU         */
+#define FIPA_ERR_OTHER 9
+
+#define FIPA_PREC_BF16 0
+#define FIPA_PREC_F32 1
+
+/* Hyper-parameters (IpaConfig).  Names follow the reference: d_in = c_s, d_z = c_z,
+ * c = c_hidden, n_query = qk-points, n_value = v-points, rank = z_factor_rank. */
+typedef struct fipa_config {
+    uint64_t d_in, d_z, heads, c, n_query, n_value, rank;
+    int32_t precision;        /* FIPA_PREC_BF16 | FIPA_PREC_F32                       */
+    int32_t enforce_head_cap; /* reference default 1: max(qk_width, v_width) <= 256   */
+} fipa_config;
+
+/* Host weights in the reference IpaWeights layout, float64, row-major:
+ *   w_q w_k w_v [d_in, H*c]; w_qp w_kp [d_in, H*Nq*3]; w_vp [d_in, H*Nv*3];
+ *   w_bias [H, d_z]; gamma_raw [H]; w_out [H*(d_z+c+4Nv), d_in]; b_out [d_in]. */
+typedef struct fipa_host_weights {
+    const double *w_q, *w_k, *w_v, *w_qp, *w_kp, *w_vp, *w_bias, *gamma_raw, *w_out, *b_out;
+    double w_l, w_c;
+} fipa_host_weights;
+
+typedef struct fipa_layer fipa_layer;
+
+const char* fipa_last_error(void);
+
+int fipa_config_validate(const fipa_config* cfg);
+/* Lifted widths of the reference (IpaConfig::qk_width / v_width). */
+uint64_t fipa_config_qk_width(const fipa_config* cfg);
+uint64_t fipa_config_v_width(const fipa_config* cfg);
+
+/* Creates the layer on the current CUDA device with IpaWeights::init(cfg, Rng(0)). */
+int fipa_layer_create(const fipa_config* cfg, fipa_layer** out);
+void fipa_layer_destroy(fipa_layer* layer);
+
+int fipa_layer_init_weights(fipa_layer* layer, uint64_t seed);
+int fipa_layer_set_weights(fipa_layer* layer, const fipa_host_weights* w);
+/* Copies the master weights out; w[10] point to caller buffers sized as above, scal[2] = {w_l, w_c}. */
+int fipa_layer_get_weights(const fipa_layer* layer, double* const* w, double* scal);
+int fipa_layer_save_weights(const fipa_layer* layer, const char* path);
+int fipa_layer_load_weights(fipa_layer* layer, const char* path);
+
+/* Device workspace needed by fipa_layer_forward for a [B, L] batch. */
+size_t fipa_layer_workspace_size(const fipa_layer* layer, int64_t B, int64_t L);
+
+/* Forward over device buffers (float32 unless noted), enqueued on `stream` (cudaStream_t):
+ *   s [B,L,d_in]  z1,z2 [B,L,rank,d_z]  rot [B,L,3,3] (row-major, y = R x + t)  trans [B,L,3]
+ *   mask [B,L] uint8 (1 = valid) or NULL     out [B,L,d_in]
+ * Masked rows of `out` are zero; a fully masked sample yields all zeros. */
+int fipa_layer_forward(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                       const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                       float* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same forward over HOST float64 buffers (the reference / Python calling convention): copies in,
+ * runs on an internal stream, copies out, synchronises. */
+int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L, const double* s,
+                            const double* z1, const double* z2, const double* rot,
+                            const double* trans, const uint8_t* mask, double* out);
+
+/* Byte offsets of the forward's intermediates inside the workspace (for parity tests and
+ * for a caller-driven backward), -1 when absent for this precision, in the order:
+ *   0 trans_c (recentred translations, f32 [B,L,3])   1 s_bf16 (bf16 [B,L,d_in])
+ *   2 proj (f32 [B,L,n_proj])    3 q_hat   4 k_hat ([B*H,L,dqk_pad])   5 v_hat ([B*H,L,dv_pad])
+ *   6 colbias (f32 [B*H,L])      7 lse (f32 [B*H,L])                  8 feat ([B,L,H*seg])
+ * q/k/v/feat are bf16 for FIPA_PREC_BF16 and f32 for FIPA_PREC_F32.  dims[4] receives
+ * {n_proj, dqk_pad, dv_pad, H*seg}.  Returns the number of offsets written (9). */
+int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
+                                int64_t* dims);
+
+/* Number of kernels fipa_layer_forward launches per call for this configuration. */
+int fipa_layer_forward_launches(const fipa_layer* layer);
+
+/* Optional per-stage device timing (CUDA events on the forward's stream).  After enabling,
+ * every forward records stage times; fipa_layer_stage_times copies up to n values (ms) in the
+ * order recenter, cast, projection, pack, attention, output and returns the count. */
+int fipa_layer_set_timing(fipa_layer* layer, int enable);
+int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FIPA_B200_H */

@@ -1,0 +1,156 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY.
+
+ctypes front end over oracle/_ref/libfipa_ref.so -- the UNMODIFIED reference
+library compiled from /root/reference/proj/src by oracle/Makefile, plus the
+extern "C" shim in oracle/ref_shim.cpp.  Used to (a) generate the golden
+fixtures under tests/golden/, (b) pin the numpy restatement, and (c) time the
+reference CPU path in bench.py's cpu_baseline / --impl reference legs.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .fipa_oracle import WEIGHT_NAMES, IpaConfig, weight_shapes
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libfipa_ref.so")
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise FileNotFoundError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
+        _lib = ctypes.CDLL(LIB_PATH)
+        _lib.ref_last_error.restype = ctypes.c_char_p
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().ref_last_error().decode()
+        raise {1: ValueError, 2: ArithmeticError, 3: IOError}.get(rc, RuntimeError)(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(_D)
+
+
+def _cfg(cfg: IpaConfig):
+    return (ctypes.c_uint64 * 9)(*cfg.as_u64())
+
+
+def _c(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _wptrs(cfg, w):
+    arrs = [_c(w[n]) for n in WEIGHT_NAMES]
+    ptrs = (_D * 10)(*[_dp(a) for a in arrs])
+    scal = np.array([w.get("w_l", 0.0), w.get("w_c", 0.0)], dtype=np.float64)
+    return arrs, ptrs, scal
+
+
+def init_weights(cfg: IpaConfig, seed: int) -> dict:
+    sh = weight_shapes(cfg)
+    w = {n: np.zeros(sh[n]) for n in WEIGHT_NAMES}
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    _check(lib().ref_init_weights(_cfg(cfg), ctypes.c_uint64(seed), ptrs, _dp(scal)))
+    out = {n: a for n, a in zip(WEIGHT_NAMES, arrs)}
+    out["w_l"], out["w_c"] = float(scal[0]), float(scal[1])
+    return out
+
+
+def _mask_ptr(mask, L):
+    if mask is None:
+        return None, None
+    m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(L))
+    return m, m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+
+
+def flash_forward(cfg, w, s, z1, z2, rot, trans, mask=None, tile_rows=64, tile_cols=64, threads=1):
+    L = s.shape[0]
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    s, z1, z2, rot, trans = map(_c, (s, z1, z2, rot, trans))
+    m, mp = _mask_ptr(mask, L)
+    out = np.zeros((L, cfg.d_in))
+    _check(lib().ref_flash_forward(_cfg(cfg), ptrs, _dp(scal), ctypes.c_uint64(L), _dp(s), _dp(z1),
+                                   _dp(z2), _dp(rot), _dp(trans), mp, ctypes.c_uint64(tile_rows),
+                                   ctypes.c_uint64(tile_cols), ctypes.c_int(threads), _dp(out)))
+    return out
+
+
+def reference_forward(cfg, w, s, z1, z2, rot, trans, mask=None):
+    L = s.shape[0]
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    s, z1, z2, rot, trans = map(_c, (s, z1, z2, rot, trans))
+    m, mp = _mask_ptr(mask, L)
+    out = np.zeros((L, cfg.d_in))
+    _check(lib().ref_reference_forward(_cfg(cfg), ptrs, _dp(scal), ctypes.c_uint64(L), _dp(s),
+                                       _dp(z1), _dp(z2), _dp(rot), _dp(trans), mp, _dp(out)))
+    return out
+
+
+def lift(cfg, w, s, z1, z2, rot, trans):
+    L, H = s.shape[0], cfg.heads
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    s, z1, z2, rot, trans = map(_c, (s, z1, z2, rot, trans))
+    q = np.zeros((H, L, cfg.qk_width()))
+    k = np.zeros((H, L, cfg.qk_width()))
+    v = np.zeros((H, L, cfg.v_width()))
+    _check(lib().ref_lift(_cfg(cfg), ptrs, _dp(scal), ctypes.c_uint64(L), _dp(s), _dp(z1), _dp(z2),
+                          _dp(rot), _dp(trans), _dp(q), _dp(k), _dp(v)))
+    return q, k, v
+
+
+def flash_attention(q, k, v, mask=None, tile_rows=64, tile_cols=64, threads=1):
+    q, k, v = map(_c, (q, k, v))
+    H, L, dqk = q.shape
+    dv = v.shape[2]
+    m, mp = _mask_ptr(mask, L)
+    out = np.zeros((H, L, dv))
+    _check(lib().ref_flash_attention(ctypes.c_uint64(H), ctypes.c_uint64(L), ctypes.c_uint64(dqk),
+                                     ctypes.c_uint64(dv), _dp(q), _dp(k), _dp(v), mp,
+                                     ctypes.c_uint64(tile_rows), ctypes.c_uint64(tile_cols),
+                                     ctypes.c_int(threads), _dp(out)))
+    return out
+
+
+def save_weights(cfg, w, path):
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    _check(lib().ref_save_weights(_cfg(cfg), ptrs, _dp(scal), str(path).encode()))
+
+
+def load_weights(cfg, path):
+    sh = weight_shapes(cfg)
+    w = {n: np.zeros(sh[n]) for n in WEIGHT_NAMES}
+    arrs, ptrs, scal = _wptrs(cfg, w)
+    _check(lib().ref_load_weights(_cfg(cfg), str(path).encode(), ptrs, _dp(scal)))
+    out = {n: a for n, a in zip(WEIGHT_NAMES, arrs)}
+    out["w_l"], out["w_c"] = float(scal[0]), float(scal[1])
+    return out
+
+
+def random_frames(seed, L, scale=1.0):
+    rot = np.zeros((L, 3, 3))
+    trans = np.zeros((L, 3))
+    _check(lib().ref_random_frames(ctypes.c_uint64(seed), ctypes.c_uint64(L), ctypes.c_double(scale),
+                                   _dp(rot), _dp(trans)))
+    return rot, trans
+
+
+def gaussian(seed, n, stddev=1.0):
+    out = np.zeros(n)
+    _check(lib().ref_gaussian(ctypes.c_uint64(seed), ctypes.c_uint64(n), ctypes.c_double(stddev), _dp(out)))
+    return out

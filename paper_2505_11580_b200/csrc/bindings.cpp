@@ -1,0 +1,271 @@
+// pybind11 module `_fipa_b200`: the reference Python surface (proj/python/bindings.cpp:171-195,
+// proj/python/fipa/__init__.py) rebuilt over the C ABI in include/fipa_b200.h.  Only C-ABI calls
+// are made from here; numpy arrays are accepted as float64 (other dtypes cast) and results come
+// back as float64, like the reference (bindings.cpp:26-45).
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fipa_b200.h"
+
+namespace py = pybind11;
+
+namespace {
+
+using DArr = py::array_t<double, py::array::c_style | py::array::forcecast>;
+
+struct FipaValueError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct FipaNumericError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct FipaIoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct FipaCudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void check(int rc) {
+    if (rc == FIPA_OK) return;
+    const std::string msg = fipa_last_error();
+    switch (rc) {
+        case FIPA_ERR_VALUE: throw FipaValueError(msg);
+        case FIPA_ERR_NUMERIC: throw FipaNumericError(msg);
+        case FIPA_ERR_IO: throw FipaIoError(msg);
+        case FIPA_ERR_CUDA: throw FipaCudaError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+int parse_precision(const std::string& name) {
+    if (name == "bf16") return FIPA_PREC_BF16;
+    if (name == "f32" || name == "f64") return FIPA_PREC_F32;
+    throw FipaValueError("unknown precision '" + name + "' (expected f32, f64 or bf16)");
+}
+
+const char* kNames[10] = {"w_q", "w_k", "w_v", "w_qp", "w_kp", "w_vp", "w_bias", "gamma_raw", "w_out", "b_out"};
+
+class Model {
+public:
+    Model(uint64_t d_in, uint64_t d_z, uint64_t heads, uint64_t c, uint64_t n_query,
+          uint64_t n_value, uint64_t rank, const std::string& precision, uint64_t seed,
+          bool enforce_head_cap)
+        : precision_name_(precision) {
+        cfg_.d_in = d_in;
+        cfg_.d_z = d_z;
+        cfg_.heads = heads;
+        cfg_.c = c;
+        cfg_.n_query = n_query;
+        cfg_.n_value = n_value;
+        cfg_.rank = rank;
+        cfg_.precision = parse_precision(precision);
+        cfg_.enforce_head_cap = enforce_head_cap ? 1 : 0;
+        check(fipa_config_validate(&cfg_));
+        check(fipa_layer_create(&cfg_, &layer_));
+        check(fipa_layer_init_weights(layer_, seed));
+    }
+    ~Model() { fipa_layer_destroy(layer_); }
+    Model(const Model&) = delete;
+    Model& operator=(const Model&) = delete;
+
+    std::vector<std::vector<size_t>> shapes() const {
+        const size_t seg = cfg_.d_z + cfg_.c + 4 * cfg_.n_value;
+        return {{cfg_.d_in, cfg_.heads * cfg_.c},          {cfg_.d_in, cfg_.heads * cfg_.c},
+                {cfg_.d_in, cfg_.heads * cfg_.c},          {cfg_.d_in, cfg_.heads * cfg_.n_query * 3},
+                {cfg_.d_in, cfg_.heads * cfg_.n_query * 3}, {cfg_.d_in, cfg_.heads * cfg_.n_value * 3},
+                {cfg_.heads, cfg_.d_z},                    {cfg_.heads},
+                {cfg_.heads * seg, cfg_.d_in},             {cfg_.d_in}};
+    }
+
+    // flash(s, z1, z2, rotations, translations, mask=None, tile_rows=64, tile_cols=64, threads=1)
+    // Unbatched [L, ...] inputs return [L, d_in]; a leading batch axis [B, L, ...] is accepted
+    // additively (mask then [B][L]).  Tiling/thread arguments are accepted and ignored: the
+    // GPU result does not depend on them (reference guarantee, attention_kernel.hpp:34-37).
+    py::array_t<double> flash(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
+                              const DArr& translations, const py::object& mask, size_t tile_rows,
+                              size_t tile_cols, int threads) {
+        if (tile_rows == 0 || tile_cols == 0) throw FipaValueError("tile sizes must be positive");
+        (void)threads;
+        const bool batched = s.ndim() == 3;
+        if (s.ndim() != 2 && s.ndim() != 3)
+            throw FipaValueError("single representation must be [L, d_in] or [B, L, d_in]");
+        const int64_t B = batched ? s.shape(0) : 1;
+        const int64_t L = batched ? s.shape(1) : s.shape(0);
+        const int o = batched ? 1 : 0;
+        if (L < 1) throw FipaValueError("empty frame set");
+        if (batched && s.shape(0) < 1) throw FipaValueError("batch must be >= 1");
+        if (s.shape(o + 1) != int64_t(cfg_.d_in))
+            throw FipaValueError("single representation must be [L, " + std::to_string(cfg_.d_in) + "]");
+        auto lead_ok = [&](const DArr& a, int nd) {
+            if (a.ndim() != nd + o) return false;
+            if (batched && a.shape(0) != B) return false;
+            return a.shape(o) == L;
+        };
+        if (!lead_ok(rotations, 3) || rotations.shape(o + 1) != 3 || rotations.shape(o + 2) != 3)
+            throw FipaValueError("rotations must have shape [L, 3, 3]");
+        if (!lead_ok(translations, 2) || translations.shape(o + 1) != 3)
+            throw FipaValueError("translations must have shape [L, 3]");
+        for (const DArr* z : {&z1, &z2}) {
+            if (!lead_ok(*z, 3) || z->shape(o + 1) != int64_t(cfg_.rank) ||
+                z->shape(o + 2) != int64_t(cfg_.d_z))
+                throw FipaValueError("factor shapes disagree with the configuration");
+        }
+        std::vector<uint8_t> m;
+        const uint8_t* mp = nullptr;
+        if (!mask.is_none()) {
+            py::array_t<uint8_t, py::array::c_style | py::array::forcecast> ma(mask);
+            if (ma.size() != B * L) throw FipaValueError("mask length must equal L");
+            m.assign(ma.data(), ma.data() + ma.size());
+            for (auto& v : m) v = v ? 1 : 0;
+            mp = m.data();
+        }
+        std::vector<py::ssize_t> shape = batched ? std::vector<py::ssize_t>{B, L, (py::ssize_t)cfg_.d_in}
+                                                 : std::vector<py::ssize_t>{L, (py::ssize_t)cfg_.d_in};
+        py::array_t<double> out(shape);
+        double* op = out.mutable_data();
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_forward_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                         translations.data(), mp, op);
+        }
+        check(rc);
+        return out;
+    }
+
+    void save(const std::string& path) const { check(fipa_layer_save_weights(layer_, path.c_str())); }
+    void load(const std::string& path) { check(fipa_layer_load_weights(layer_, path.c_str())); }
+
+    py::dict weights() const {
+        const auto sh = shapes();
+        std::vector<py::array_t<double>> arrs;
+        double* ptrs[10];
+        for (int i = 0; i < 10; ++i) {
+            arrs.emplace_back(std::vector<py::ssize_t>(sh[i].begin(), sh[i].end()));
+            ptrs[i] = arrs.back().mutable_data();
+        }
+        double scal[2];
+        check(fipa_layer_get_weights(layer_, ptrs, scal));
+        py::dict d;
+        for (int i = 0; i < 10; ++i) d[kNames[i]] = arrs[i];
+        d["w_l"] = scal[0];
+        d["w_c"] = scal[1];
+        return d;
+    }
+
+    void set_weights(const py::dict& d) {
+        const auto sh = shapes();
+        std::vector<DArr> keep;
+        fipa_host_weights w{};
+        const double** dst[10] = {&w.w_q,  &w.w_k,    &w.w_v,         &w.w_qp,   &w.w_kp,
+                                  &w.w_vp, &w.w_bias, &w.gamma_raw,   &w.w_out,  &w.b_out};
+        for (int i = 0; i < 10; ++i) {
+            DArr a(d[kNames[i]]);
+            size_t n = 1;
+            for (auto v : sh[i]) n *= v;
+            if (size_t(a.size()) != n)
+                throw FipaValueError(std::string("weights tensor '") + kNames[i] + "' has the wrong size");
+            keep.push_back(a);
+            *dst[i] = keep.back().data();
+        }
+        w.w_l = d["w_l"].cast<double>();
+        w.w_c = d["w_c"].cast<double>();
+        check(fipa_layer_set_weights(layer_, &w));
+    }
+
+    size_t workspace_size(int64_t B, int64_t L) const { return fipa_layer_workspace_size(layer_, B, L); }
+
+    // Device-pointer forward for benchmarks / tests that own device memory (e.g. torch tensors).
+    void forward_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                        uintptr_t trans, uintptr_t mask, uintptr_t out, uintptr_t ws, size_t ws_bytes,
+                        uintptr_t stream) {
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_forward(layer_, B, L, reinterpret_cast<const float*>(s),
+                                    reinterpret_cast<const float*>(z1), reinterpret_cast<const float*>(z2),
+                                    reinterpret_cast<const float*>(rot), reinterpret_cast<const float*>(trans),
+                                    reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(out),
+                                    reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+
+    py::tuple workspace_layout(int64_t B, int64_t L) const {
+        int64_t off[9], dims[4];
+        const int n = fipa_layer_workspace_layout(layer_, B, L, off, dims);
+        if (n != 9) throw FipaValueError("invalid batch shape");
+        return py::make_tuple(std::vector<int64_t>(off, off + 9), std::vector<int64_t>(dims, dims + 4));
+    }
+
+    int forward_launches() const { return fipa_layer_forward_launches(layer_); }
+    void set_timing(bool on) { check(fipa_layer_set_timing(layer_, on ? 1 : 0)); }
+    std::vector<float> stage_times() const {
+        std::vector<float> t(16);
+        t.resize(fipa_layer_stage_times(layer_, t.data(), 16));
+        return t;
+    }
+    std::string precision() const { return precision_name_; }
+    py::dict config() const {
+        py::dict d;
+        d["d_in"] = cfg_.d_in;
+        d["d_z"] = cfg_.d_z;
+        d["heads"] = cfg_.heads;
+        d["c"] = cfg_.c;
+        d["n_query"] = cfg_.n_query;
+        d["n_value"] = cfg_.n_value;
+        d["rank"] = cfg_.rank;
+        d["precision"] = precision_name_;
+        d["enforce_head_cap"] = bool(cfg_.enforce_head_cap);
+        return d;
+    }
+
+private:
+    fipa_config cfg_{};
+    fipa_layer* layer_ = nullptr;
+    std::string precision_name_;
+};
+
+}  // namespace
+
+PYBIND11_MODULE(_fipa_b200, m) {
+    m.doc() = "B200-native FlashIPA layer (tcgen05 sm_100a kernels behind the reference fipa.Model API)";
+
+    py::register_exception<FipaValueError>(m, "FipaValueError", PyExc_ValueError);
+    py::register_exception<FipaNumericError>(m, "FipaNumericError", PyExc_ArithmeticError);
+    py::register_exception<FipaIoError>(m, "FipaIoError", PyExc_IOError);
+    py::register_exception<FipaCudaError>(m, "FipaCudaError", PyExc_RuntimeError);
+
+    py::class_<Model>(m, "Model", "One FlashIPA layer: hyper-parameters plus deterministic weights")
+        .def(py::init<uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t,
+                      const std::string&, uint64_t, bool>(),
+             py::arg("d_in") = 32, py::arg("d_z") = 4, py::arg("heads") = 2, py::arg("c") = 8,
+             py::arg("n_query") = 2, py::arg("n_value") = 2, py::arg("rank") = 2,
+             py::arg("precision") = "f64", py::arg("seed") = 0, py::arg("enforce_head_cap") = true)
+        .def("flash", &Model::flash, py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rotations"),
+             py::arg("translations"), py::arg("mask") = py::none(), py::arg("tile_rows") = 64,
+             py::arg("tile_cols") = 64, py::arg("threads") = 1,
+             "Linear-memory FlashIPA forward on the GPU")
+        .def("save", &Model::save, py::arg("path"), "Write weights to a binary file")
+        .def("load", &Model::load, py::arg("path"), "Replace weights from a binary file")
+        .def("weights", &Model::weights, "Master weights as a dict of float64 arrays")
+        .def("set_weights", &Model::set_weights, py::arg("weights"))
+        .def("workspace_size", &Model::workspace_size, py::arg("B"), py::arg("L"))
+        .def("forward_device", &Model::forward_device, py::arg("B"), py::arg("L"), py::arg("s"),
+             py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("workspace_layout", &Model::workspace_layout, py::arg("B"), py::arg("L"))
+        .def("forward_launches", &Model::forward_launches)
+        .def("set_timing", &Model::set_timing, py::arg("enable"))
+        .def("stage_times", &Model::stage_times)
+        .def_property_readonly("precision", &Model::precision)
+        .def_property_readonly("config", &Model::config);
+}

@@ -1,0 +1,228 @@
+// extern "C" boundary (include/fipa_b200.h) over the host C++ layer.  Exceptions never cross
+// the ABI: they become status codes + a thread-local message (reference error taxonomy,
+// proj/include/fipa/error.hpp:10-28).
+#include "../../include/fipa_b200.h"
+
+#include <exception>
+#include <new>
+#include <string>
+
+#include "layer.hpp"
+
+struct fipa_layer {
+    fipa_b200::FlashIpaLayer impl;
+    explicit fipa_layer(const fipa_b200::Config& c) : impl(c) {}
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FIPA_OK;
+    } catch (const fipa_b200::ValueError& e) {
+        g_err = e.what();
+        return FIPA_ERR_VALUE;
+    } catch (const fipa_b200::NumericError& e) {
+        g_err = e.what();
+        return FIPA_ERR_NUMERIC;
+    } catch (const fipa_b200::IoError& e) {
+        g_err = e.what();
+        return FIPA_ERR_IO;
+    } catch (const fipa_b200::CudaError& e) {
+        g_err = e.what();
+        return FIPA_ERR_CUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return FIPA_ERR_VALUE;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return FIPA_ERR_OTHER;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FIPA_ERR_OTHER;
+    }
+}
+
+fipa_b200::Config to_cfg(const fipa_config* c) {
+    if (c == nullptr) throw fipa_b200::ValueError("null fipa_config");
+    fipa_b200::Config cfg;
+    cfg.d_in = c->d_in;
+    cfg.d_z = c->d_z;
+    cfg.heads = c->heads;
+    cfg.c = c->c;
+    cfg.n_query = c->n_query;
+    cfg.n_value = c->n_value;
+    cfg.rank = c->rank;
+    if (c->precision == FIPA_PREC_BF16) {
+        cfg.precision = fipa_b200::Precision::bf16;
+    } else if (c->precision == FIPA_PREC_F32) {
+        cfg.precision = fipa_b200::Precision::f32;
+    } else {
+        throw fipa_b200::ValueError("unknown precision code " + std::to_string(c->precision));
+    }
+    cfg.enforce_head_cap = c->enforce_head_cap != 0;
+    return cfg;
+}
+
+fipa_b200::FlashIpaLayer& L(fipa_layer* l) {
+    if (l == nullptr) throw fipa_b200::ValueError("null fipa_layer");
+    return l->impl;
+}
+const fipa_b200::FlashIpaLayer& L(const fipa_layer* l) {
+    if (l == nullptr) throw fipa_b200::ValueError("null fipa_layer");
+    return l->impl;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fipa_last_error(void) { return g_err.c_str(); }
+
+int fipa_config_validate(const fipa_config* cfg) {
+    return guarded([&] { to_cfg(cfg).validate(); });
+}
+
+uint64_t fipa_config_qk_width(const fipa_config* cfg) {
+    return cfg ? cfg->c + 5 * cfg->n_query + cfg->rank * cfg->d_z : 0;
+}
+
+uint64_t fipa_config_v_width(const fipa_config* cfg) {
+    return cfg ? cfg->c + 3 * cfg->n_value + cfg->rank * cfg->d_z : 0;
+}
+
+int fipa_layer_create(const fipa_config* cfg, fipa_layer** out) {
+    return guarded([&] {
+        if (out == nullptr) throw fipa_b200::ValueError("null output handle");
+        *out = nullptr;
+        *out = new fipa_layer(to_cfg(cfg));
+    });
+}
+
+void fipa_layer_destroy(fipa_layer* layer) { delete layer; }
+
+int fipa_layer_init_weights(fipa_layer* layer, uint64_t seed) {
+    return guarded([&] { L(layer).init_weights(seed); });
+}
+
+int fipa_layer_set_weights(fipa_layer* layer, const fipa_host_weights* w) {
+    return guarded([&] {
+        auto& impl = L(layer);
+        if (w == nullptr) throw fipa_b200::ValueError("null weights");
+        const auto shapes = fipa_b200::weight_shapes(impl.config());
+        const double* src[10] = {w->w_q,  w->w_k,      w->w_v,  w->w_qp, w->w_kp,
+                                 w->w_vp, w->w_bias, w->gamma_raw, w->w_out, w->b_out};
+        fipa_b200::HostWeights hw;
+        for (int i = 0; i < 10; ++i) {
+            if (src[i] == nullptr) throw fipa_b200::ValueError("null weights tensor");
+            std::size_t n = 1;
+            for (auto d : shapes[i]) n *= d;
+            hw.slots[i]->assign(src[i], src[i] + n);
+        }
+        hw.w_l = w->w_l;
+        hw.w_c = w->w_c;
+        hw.stored_f32 = impl.config().precision == fipa_b200::Precision::f32;
+        impl.set_weights(hw);
+    });
+}
+
+int fipa_layer_get_weights(const fipa_layer* layer, double* const* w, double* scal) {
+    return guarded([&] {
+        const auto& impl = L(layer);
+        if (w == nullptr || scal == nullptr) throw fipa_b200::ValueError("null output buffers");
+        const auto& hw = impl.weights();
+        for (int i = 0; i < 10; ++i) {
+            if (w[i] == nullptr) throw fipa_b200::ValueError("null weights buffer");
+            std::copy(hw.slots[i]->begin(), hw.slots[i]->end(), w[i]);
+        }
+        scal[0] = hw.w_l;
+        scal[1] = hw.w_c;
+    });
+}
+
+int fipa_layer_save_weights(const fipa_layer* layer, const char* path) {
+    return guarded([&] {
+        if (path == nullptr) throw fipa_b200::ValueError("null path");
+        L(layer).save(path);
+    });
+}
+
+int fipa_layer_load_weights(fipa_layer* layer, const char* path) {
+    return guarded([&] {
+        if (path == nullptr) throw fipa_b200::ValueError("null path");
+        L(layer).load(path);
+    });
+}
+
+size_t fipa_layer_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_) {
+    if (layer == nullptr || B < 1 || L_ < 1) return 0;
+    return layer->impl.workspace_size(B, L_);
+}
+
+int fipa_layer_forward(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                       const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                       float* out, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        L(layer).forward(B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
+                         static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L_, const double* s,
+                            const double* z1, const double* z2, const double* rot,
+                            const double* trans, const uint8_t* mask, double* out) {
+    return guarded([&] {
+        if (!s || !z1 || !z2 || !rot || !trans || !out) throw fipa_b200::ValueError("null buffer");
+        L(layer).forward_host(B, L_, s, z1, z2, rot, trans, mask, out);
+    });
+}
+
+int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, int64_t* offsets,
+                                int64_t* dims) {
+    if (layer == nullptr || offsets == nullptr || B < 1 || L_ < 1) return 0;
+    const auto w = layer->impl.carve(nullptr, B, L_);
+    // carve(nullptr) yields null-based pointers: offsets are the pointer values themselves.
+    auto off = [](const void* p, bool present) -> int64_t {
+        return present ? static_cast<int64_t>(reinterpret_cast<uintptr_t>(p)) : -1;
+    };
+    const bool bf16 = layer->impl.config().precision == fipa_b200::Precision::bf16;
+    offsets[0] = off(w.trans_c, true);
+    offsets[1] = off(w.s_bf16, bf16);
+    offsets[2] = off(w.proj, true);
+    offsets[3] = off(w.qhat, true);
+    offsets[4] = off(w.khat, true);
+    offsets[5] = off(w.vhat, true);
+    offsets[6] = off(w.colbias, true);
+    offsets[7] = off(w.lse, true);
+    offsets[8] = off(w.feat, true);
+    if (dims != nullptr) {
+        const auto& d = layer->impl.dims();
+        dims[0] = d.n_proj;
+        dims[1] = d.dqk_pad;
+        dims[2] = d.dv_pad;
+        dims[3] = d.feat;
+    }
+    return 9;
+}
+
+int fipa_layer_forward_launches(const fipa_layer* layer) {
+    return layer ? layer->impl.launches_per_forward() : 0;
+}
+
+int fipa_layer_set_timing(fipa_layer* layer, int enable) {
+    return guarded([&] { L(layer).set_timing(enable != 0); });
+}
+
+int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n) {
+    if (layer == nullptr || ms == nullptr) return 0;
+    const auto t = layer->impl.stage_times();
+    int k = 0;
+    for (; k < n && k < int(t.size()); ++k) ms[k] = t[k];
+    return k;
+}
+
+}  // extern "C"

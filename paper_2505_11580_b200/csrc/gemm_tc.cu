@@ -1,0 +1,234 @@
+// Generic bf16 GEMM on 5th-gen tensor cores (tcgen05.mma kind::f16, fp32 accumulators in
+// TMEM), TMA-fed through a STAGES-deep mbarrier ring, warp-specialised:
+//   warp 0      : TMA producer (one elected lane)
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  : epilogue, TMEM -> registers -> global (warp w owns TMEM lanes 32*(w%4)..)
+// One 128 x BN output tile per CTA.  Serves the projection GEMM (reference
+// project_inputs, proj/src/ipa.cpp:201-217 -> linear, proj/src/tensor.cpp:292-317), the
+// output projection (proj/src/flash_ipa.cpp:212) and the backward GEMMs.
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+#include "tma_host.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct EpiParams {
+    void* C;
+    int64_t ldc;
+    int M, N, K;
+    bool out_bf16, accumulate;
+    float alpha;
+    const float* bias;
+    const uint8_t* row_mask;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, EpiParams p) {
+    using Cfg = GemmCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* tiles = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+    uint64_t* empty = full + Cfg::kStages;
+    uint64_t* done = empty + Cfg::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = ptx::warp_id();
+    const int lane = ptx::lane_id();
+    const int m0 = blockIdx.y * BM;
+    const int n0 = blockIdx.x * BN;
+    const int nk = (p.K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&mapA);
+        ptx::tma_prefetch(&mapB);
+        for (int s = 0; s < Cfg::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % Cfg::kStages;
+                if (kb >= Cfg::kStages) ptx::mbar_wait(&empty[s], ((kb / Cfg::kStages) - 1) & 1);
+                uint8_t* sa = tiles + s * Cfg::kStageBytes;
+                uint8_t* sb = sa + Cfg::kABytes;
+                ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
+                if (A_MN) {
+                    for (int mb = 0; mb < BM / 64; ++mb)
+                        ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kb * BK);
+                } else {
+                    ptx::tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
+                }
+                if (B_MN) {
+                    for (int nb = 0; nb < BN / 64; ++nb)
+                        ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kb * BK);
+                } else {
+                    ptx::tma_load_2d(sb, &mapB, &full[s], kb * BK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % Cfg::kStages;
+                ptx::mbar_wait(&full[s], (kb / Cfg::kStages) & 1);
+                ptx::tc_fence_after();
+                const uint32_t sa = ptx::smem_u32(tiles + s * Cfg::kStageBytes);
+                const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk) {
+                    const uint64_t da = A_MN ? ptx::sw128_desc(sa + kk * 2048, 64 * 128, 1024)
+                                             : ptx::sw128_desc(sa + kk * 32, 16, 1024);
+                    const uint64_t db = B_MN ? ptx::sw128_desc(sb + kk * 2048, 64 * 128, 1024)
+                                             : ptx::sw128_desc(sb + kk * 32, 16, 1024);
+                    ptx::mma_ss(tmem, da, db, idesc, (kb | kk) != 0);
+                }
+                ptx::mma_commit(&empty[s]);
+            }
+            ptx::mma_commit(done);
+        }
+    } else {
+        // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
+        const int quad = warp & 3;
+        const int row = m0 + quad * 32 + lane;
+        ptx::mbar_wait(done, 0);
+        ptx::tc_fence_after();
+        const bool row_ok = row < p.M;
+        const bool zero_row = row_ok && p.row_mask != nullptr && p.row_mask[row] == 0;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c0, r);
+            ptx::tmem_wait_ld();
+            if (!row_ok) continue;
+            const int col0 = n0 + c0;
+            if (col0 >= p.N) continue;
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float x = __uint_as_float(r[i]) * p.alpha;
+                const int col = col0 + i;
+                if (p.bias != nullptr && col < p.N) x += p.bias[col];
+                v[i] = zero_row ? 0.0f : x;
+            }
+            const bool full_chunk = col0 + 32 <= p.N;
+            if (p.out_bf16) {
+                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + int64_t(row) * p.ldc + col0;
+                if (full_chunk) {
+                    uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        o4[q] = w;
+                    }
+                } else {
+                    for (int i = 0; i < 32 && col0 + i < p.N; ++i) out[i] = __float2bfloat16_rn(v[i]);
+                }
+            } else {
+                float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
+                if (full_chunk) {
+                    float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        if (p.accumulate) {
+                            const float4 o = o4[q];
+                            w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+                        }
+                        o4[q] = w;
+                    }
+                } else {
+                    for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+                        out[i] = p.accumulate ? out[i] + v[i] : v[i];
+                }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+void launch_impl(const GemmArgs& a, cudaStream_t stream) {
+    using Cfg = GemmCfg<BN>;
+    // TMA maps: K-major operands are [rows=M|N, cols=K] with box {64, rows-per-tile};
+    // MN-major operands are [rows=K, cols=M|N] with box {64, BK}.
+    const CUtensorMap mapA = A_MN ? make_map_2d_bf16(a.A, a.K, a.M, a.lda, 64, BK)
+                                  : make_map_2d_bf16(a.A, a.M, a.K, a.lda, 64, BM);
+    const CUtensorMap mapB = B_MN ? make_map_2d_bf16(a.B, a.K, a.N, a.ldb, 64, BK)
+                                  : make_map_2d_bf16(a.B, a.N, a.K, a.ldb, 64, BN);
+    EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, a.alpha, a.bias, a.row_mask};
+    auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        configured = true;
+    }
+    dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
+    kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, p);
+}
+
+}  // namespace
+
+void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0) return;
+    if (a.K % 16 != 0) throw std::invalid_argument("gemm: K must be a multiple of 16");
+    if (a.accumulate && a.out_bf16) throw std::invalid_argument("gemm: accumulate needs fp32 C");
+    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512);
+    const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);
+    if (wide) {
+        switch (sel) {
+            case 0: return launch_impl<256, false, false>(a, stream);
+            case 1: return launch_impl<256, true, false>(a, stream);
+            case 2: return launch_impl<256, false, true>(a, stream);
+            default: return launch_impl<256, true, true>(a, stream);
+        }
+    }
+    switch (sel) {
+        case 0: return launch_impl<128, false, false>(a, stream);
+        case 1: return launch_impl<128, true, false>(a, stream);
+        case 2: return launch_impl<128, false, true>(a, stream);
+        default: return launch_impl<128, true, true>(a, stream);
+    }
+}
+
+}  // namespace fipa_b200

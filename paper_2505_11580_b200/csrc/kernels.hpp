@@ -1,0 +1,105 @@
+// Launch entry points of every sm_100a kernel in the library (host-callable).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fipa_b200 {
+
+// ------------------------------------------------------------------ GEMM
+// C[M,N] = alpha * A[M,K] . B[K,N] (+ bias[N]) (+ beta*C), rows with row_mask==0 zeroed.
+//   a_mn_major = false: A stored row-major [M, K] (lda >= K)
+//   a_mn_major = true : A stored row-major [K, M] (lda >= M)      (i.e. A^T given)
+//   b_mn_major = false: B stored row-major [N, K] (ldb >= K)      (i.e. B^T given, "K-major")
+//   b_mn_major = true : B stored row-major [K, N] (ldb >= N)
+// bf16 operands, fp32 accumulation in TMEM (tcgen05.mma kind::f16), TMA-fed.
+struct GemmArgs {
+    const __nv_bfloat16* A = nullptr;
+    const __nv_bfloat16* B = nullptr;
+    void* C = nullptr;
+    int64_t lda = 0, ldb = 0, ldc = 0;
+    int M = 0, N = 0, K = 0;
+    bool a_mn_major = false;
+    bool b_mn_major = false;
+    bool out_bf16 = false;
+    bool accumulate = false;  // C += result (fp32 output only)
+    float alpha = 1.0f;
+    const float* bias = nullptr;        // [N] or null
+    const uint8_t* row_mask = nullptr;  // [M] or null: rows with 0 are written as 0
+};
+void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
+
+// ------------------------------------------------------- FlashIPA layer
+// Sizes of one layer configuration (host side, shared with the kernels).
+struct LayerDims {
+    int d_in, d_z, heads, c, n_query, n_value, rank;
+    int n_proj;      // H*(3c + 6Nq + 3Nv): fused projection width
+    int dqk_used;    // c + 3Nq + r*d_z           (lifted query/key width, norms/ones dropped)
+    int dqk_pad;     // dqk_used rounded up to 16
+    int dv_used;     // c + r*d_z + 3Nv + 6       (v | z2 | R v_p | t_hi | t_lo)
+    int dv_pad;      // dv_used rounded up to 16
+    int seg;         // d_z + c + 4Nv             (per-head feature block)
+    int feat;        // H*seg
+};
+
+struct PackArgs {
+    const float* proj;     // [BL, n_proj]  s . W_fused (reference column order)
+    const float* z1;       // [BL, r, d_z]
+    const float* z2;       // [BL, r, d_z]
+    const float* rot;      // [BL, 9] row-major
+    const float* trans;    // [BL, 3] (already recentred per sample)
+    const uint8_t* mask;   // [BL] or null
+    const float* head_g;   // [H]  gamma_h * w_l * w_c
+    const float* wl_bias;  // [H, d_z]  w_l * w_bias
+    float k_scale;         // w_l / sqrt(c)
+    void* qhat;            // [B*H, L, dqk_pad]
+    void* khat;            // [B*H, L, dqk_pad]
+    void* vhat;            // [B*H, L, dv_pad]
+    float* colbias;        // [B*H, L]  -g/2 * sum_p |T_j k_p|^2, -inf for masked keys
+    int B, L;
+    bool out_f32;          // write fp32 rows (SIMT f32 path) instead of bf16
+};
+void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream);
+
+struct AttnArgs {
+    const __nv_bfloat16* qhat;
+    const __nv_bfloat16* khat;
+    const __nv_bfloat16* vhat;
+    const float* colbias;
+    const float* z1;
+    const float* rot;
+    const float* trans;
+    __nv_bfloat16* feat;   // [BL, feat]
+    float* lse;            // [B*H, L] natural-log LSE of the shifted logits
+    int B, L;
+};
+// tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
+// inverse frame / norms) writing bf16 features.
+void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
+
+// Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
+void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);
+// Subtract each sample's translation centroid (exact: the layer is invariant to it).
+void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
+                     cudaStream_t stream);
+
+// ------------------------------------------------------ SIMT fp32 path
+void launch_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K,
+                     const float* bias, const uint8_t* row_mask, cudaStream_t stream);
+struct AttnF32Args {
+    const float* qhat;
+    const float* khat;
+    const float* vhat;
+    const float* colbias;
+    const float* z1;
+    const float* rot;
+    const float* trans;
+    float* feat;  // [BL, feat] fp32
+    float* lse;
+    int B, L;
+};
+void launch_attn_fwd_f32(const LayerDims& d, const AttnF32Args& a, cudaStream_t stream);
+
+}  // namespace fipa_b200

@@ -1,0 +1,637 @@
+// Host orchestration of the B200 FlashIPA layer.  See layer.hpp.
+#include "layer.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <sstream>
+
+namespace fipa_b200 {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+namespace {
+
+template <class... P>
+std::string cat(P&&... parts) {
+    std::ostringstream os;
+    (os << ... << parts);
+    return os.str();
+}
+
+#define REQUIRE(cond, ...)                                      \
+    do {                                                        \
+        if (!(cond)) throw ::fipa_b200::ValueError(cat(__VA_ARGS__)); \
+    } while (0)
+
+std::size_t round_up(std::size_t x, std::size_t m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------------ Rng
+// Counter-based splitmix64 + Box-Muller, bit-identical to the reference generator
+// (proj/src/rng.cpp:11-41): draw n = mix64(seed + n*golden), uniform in (0,1].
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : seed_(seed) {}
+    std::uint64_t next_u64() {
+        counter_ += 1;
+        std::uint64_t z = seed_ + counter_ * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    double uniform() { return static_cast<double>((next_u64() >> 11) + 1) * 0x1.0p-53; }
+    double gaussian() {
+        if (have_spare_) {
+            have_spare_ = false;
+            return spare_;
+        }
+        const double u1 = uniform();
+        const double u2 = uniform();
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        const double angle = 2.0 * std::numbers::pi * u2;
+        spare_ = radius * std::sin(angle);
+        have_spare_ = true;
+        return radius * std::cos(angle);
+    }
+
+private:
+    std::uint64_t seed_;
+    std::uint64_t counter_ = 0;
+    double spare_ = 0.0;
+    bool have_spare_ = false;
+};
+
+std::size_t numel(const std::vector<std::size_t>& s) {
+    std::size_t n = 1;
+    for (auto d : s) n *= d;
+    return n;
+}
+
+constexpr double kGammaRawUnit = 0.5413248546129181;  // ln(e - 1), proj/src/ipa.cpp:30
+
+double softplus(double x) {  // proj/src/ipa.cpp:25-27
+    return x > 0.0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Config
+void Config::validate() const {
+    REQUIRE(d_in > 0 && d_z > 0 && heads > 0 && c > 0 && n_query > 0 && n_value > 0 && rank > 0,
+            "all IpaConfig dimensions must be positive");
+    if (enforce_head_cap) {
+        const std::size_t widest = std::max(qk_width(), v_width());
+        REQUIRE(widest <= head_cap, "lifted head width ", widest, " exceeds the cap of ", head_cap,
+                "; shrink c/N/r*d_z or set enforce_head_cap=false");
+    }
+}
+
+LayerDims Config::dims() const {
+    LayerDims d{};
+    d.d_in = int(d_in);
+    d.d_z = int(d_z);
+    d.heads = int(heads);
+    d.c = int(c);
+    d.n_query = int(n_query);
+    d.n_value = int(n_value);
+    d.rank = int(rank);
+    d.n_proj = int(heads * (3 * c + 6 * n_query + 3 * n_value));
+    d.dqk_used = int(c + 3 * n_query + rank * d_z);
+    d.dqk_pad = int(round_up(d.dqk_used, 16));
+    d.dv_used = int(c + rank * d_z + 3 * n_value + 6);
+    d.dv_pad = int(round_up(d.dv_used, 16));
+    d.seg = int(d_z + c + 4 * n_value);
+    d.feat = int(heads) * d.seg;
+    return d;
+}
+
+HostWeights& HostWeights::operator=(const HostWeights& o) {
+    for (int i = 0; i < 10; ++i) *slots[i] = *o.slots[i];
+    w_l = o.w_l;
+    w_c = o.w_c;
+    stored_f32 = o.stored_f32;
+    return *this;
+}
+
+std::vector<std::vector<std::size_t>> weight_shapes(const Config& c) {
+    const std::size_t seg = c.d_z + c.c + 4 * c.n_value;
+    return {{c.d_in, c.heads * c.c},           {c.d_in, c.heads * c.c},
+            {c.d_in, c.heads * c.c},           {c.d_in, c.heads * c.n_query * 3},
+            {c.d_in, c.heads * c.n_query * 3}, {c.d_in, c.heads * c.n_value * 3},
+            {c.heads, c.d_z},                  {c.heads},
+            {c.heads * seg, c.d_in},           {c.d_in}};
+}
+
+const char* const* weight_names() {
+    static const char* names[10] = {"w_q",    "w_k",       "w_v",   "w_qp",  "w_kp",
+                                    "w_vp",   "w_bias",    "gamma_raw", "w_out", "b_out"};
+    return names;
+}
+
+// IpaWeights::init (proj/src/ipa.cpp:172-193): draw order w_q w_k w_v w_qp w_kp w_vp
+// (sigma 1/sqrt(d_in)), w_bias (1/sqrt(d_z)), w_out (1/sqrt(H*seg)); gamma_raw = ln(e-1),
+// b_out = 0, w_l = sqrt(1/3), w_c = sqrt(2/(9 Nq)).  round_f32 mirrors f32 storage.
+HostWeights init_weights(const Config& cfg, std::uint64_t seed, bool round_f32) {
+    cfg.validate();
+    const auto shapes = weight_shapes(cfg);
+    Rng rng(seed);
+    HostWeights w;
+    auto draw = [&](std::vector<double>& dst, const std::vector<std::size_t>& shape, double sd) {
+        dst.resize(numel(shape));
+        for (auto& v : dst) {
+            v = sd * rng.gaussian();
+            if (round_f32) v = static_cast<double>(static_cast<float>(v));
+        }
+    };
+    const double s_in = 1.0 / std::sqrt(static_cast<double>(cfg.d_in));
+    for (int i = 0; i < 6; ++i) draw(*w.slots[i], shapes[i], s_in);
+    draw(w.w_bias, shapes[6], 1.0 / std::sqrt(static_cast<double>(cfg.d_z)));
+    w.gamma_raw.assign(cfg.heads, round_f32 ? double(float(kGammaRawUnit)) : kGammaRawUnit);
+    draw(w.w_out, shapes[8], 1.0 / std::sqrt(static_cast<double>(shapes[8][0])));
+    w.b_out.assign(cfg.d_in, 0.0);
+    w.w_l = std::sqrt(1.0 / 3.0);
+    w.w_c = std::sqrt(2.0 / (9.0 * static_cast<double>(cfg.n_query)));
+    w.stored_f32 = round_f32;
+    return w;
+}
+
+// ------------------------------------------------------------ weights file
+// Layout (proj/include/fipa/model_io.hpp:15-21, README "Weights file format"):
+//   "FIPA" | u16 version=1 | u16 count | entries
+//   entry: u16 name_len | name | u8 precision (0 f32, 1 f64) | u8 rank | u64 dims[rank] | payload
+// w_l / w_c travel as 1-element f64 tensors.  Bit-exact round trips.
+namespace {
+
+void put_u16(std::string& o, std::uint16_t v) {
+    o.push_back(char(v & 0xff));
+    o.push_back(char(v >> 8));
+}
+void put_u64(std::string& o, std::uint64_t v) {
+    for (int i = 0; i < 8; ++i) o.push_back(char((v >> (8 * i)) & 0xff));
+}
+void put_entry(std::string& o, const std::string& name, const std::vector<double>& vals,
+               const std::vector<std::size_t>& shape, bool f32) {
+    put_u16(o, static_cast<std::uint16_t>(name.size()));
+    o.append(name);
+    o.push_back(char(f32 ? 0 : 1));
+    o.push_back(char(shape.size()));
+    for (auto d : shape) put_u64(o, d);
+    for (double v : vals) {
+        if (f32) {
+            const auto bits = std::bit_cast<std::uint32_t>(static_cast<float>(v));
+            for (int b = 0; b < 4; ++b) o.push_back(char((bits >> (8 * b)) & 0xff));
+        } else {
+            put_u64(o, std::bit_cast<std::uint64_t>(v));
+        }
+    }
+}
+
+struct Cursor {
+    const std::string& buf;
+    std::size_t pos = 0;
+    void need(std::size_t n) const {
+        if (pos + n > buf.size()) throw IoError("weights file: truncated payload");
+    }
+    std::uint8_t u8() {
+        need(1);
+        return static_cast<std::uint8_t>(buf[pos++]);
+    }
+    std::uint16_t u16() {
+        need(2);
+        const std::uint16_t v = std::uint16_t(std::uint8_t(buf[pos])) |
+                                std::uint16_t(std::uint16_t(std::uint8_t(buf[pos + 1])) << 8);
+        pos += 2;
+        return v;
+    }
+    std::uint64_t u64() {
+        need(8);
+        std::uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= std::uint64_t(std::uint8_t(buf[pos + i])) << (8 * i);
+        pos += 8;
+        return v;
+    }
+    std::string bytes(std::size_t n) {
+        need(n);
+        std::string s = buf.substr(pos, n);
+        pos += n;
+        return s;
+    }
+};
+
+struct Entry {
+    bool f32 = false;
+    std::vector<std::size_t> shape;
+    std::vector<double> vals;
+};
+
+}  // namespace
+
+void save_weights_file(const HostWeights& w, const std::vector<std::vector<std::size_t>>& shapes,
+                       const std::string& path) {
+    std::string buf("FIPA");
+    put_u16(buf, 1);
+    put_u16(buf, 12);
+    for (int i = 0; i < 10; ++i) put_entry(buf, weight_names()[i], *w.slots[i], shapes[i], w.stored_f32);
+    put_entry(buf, "w_l", {w.w_l}, {1}, false);
+    put_entry(buf, "w_c", {w.w_c}, {1}, false);
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw IoError("cannot open '" + path + "' for writing");
+    out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+    if (!out) throw IoError("short write to '" + path + "'");
+}
+
+HostWeights load_weights_file(const std::string& path,
+                              const std::vector<std::vector<std::size_t>>& shapes) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open '" + path + "' for reading");
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    const std::string buf = ss.str();
+    Cursor cur{buf};
+    if (cur.bytes(4) != "FIPA") throw IoError("weights file: bad magic");
+    const std::uint16_t version = cur.u16();
+    if (version != 1) throw IoError(cat("weights file: version ", version, ", expected 1"));
+    const std::uint16_t count = cur.u16();
+    std::map<std::string, Entry> table;
+    for (std::uint16_t e = 0; e < count; ++e) {
+        const std::uint16_t nl = cur.u16();
+        std::string name = cur.bytes(nl);
+        Entry ent;
+        const std::uint8_t tag = cur.u8();
+        if (tag > 1) throw IoError("weights file: unknown precision tag");
+        ent.f32 = tag == 0;
+        const std::uint8_t rank = cur.u8();
+        if (rank == 0) throw IoError("weights file: rank-0 tensor entry");
+        std::size_t n = 1;
+        for (int r = 0; r < rank; ++r) {
+            const std::uint64_t d = cur.u64();
+            if (d == 0) throw IoError("weights file: zero dimension");
+            ent.shape.push_back(d);
+            n *= d;
+        }
+        cur.need(n * (ent.f32 ? 4 : 8));
+        ent.vals.resize(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            if (ent.f32) {
+                std::uint32_t bits = 0;
+                for (int b = 0; b < 4; ++b)
+                    bits |= std::uint32_t(std::uint8_t(buf[cur.pos + b])) << (8 * b);
+                cur.pos += 4;
+                ent.vals[i] = static_cast<double>(std::bit_cast<float>(bits));
+            } else {
+                ent.vals[i] = std::bit_cast<double>(cur.u64());
+            }
+        }
+        if (!table.emplace(std::move(name), std::move(ent)).second)
+            throw IoError("weights file: duplicate tensor entry");
+    }
+    if (cur.pos != buf.size()) throw IoError("weights file: trailing bytes");
+    auto take = [&](const char* name) {
+        auto it = table.find(name);
+        if (it == table.end()) throw IoError(std::string("weights file: missing tensor '") + name + "'");
+        Entry e = std::move(it->second);
+        table.erase(it);
+        return e;
+    };
+    HostWeights w;
+    for (int i = 0; i < 10; ++i) {
+        Entry e = take(weight_names()[i]);
+        if (e.shape != shapes[i])
+            throw ValueError(cat("weights file: tensor '", weight_names()[i],
+                                 "' has a shape that disagrees with the layer configuration"));
+        if (i == 0) w.stored_f32 = e.f32;
+        *w.slots[i] = std::move(e.vals);
+    }
+    w.w_l = take("w_l").vals.at(0);
+    w.w_c = take("w_c").vals.at(0);
+    if (!table.empty()) throw IoError("weights file: unexpected tensor '" + table.begin()->first + "'");
+    return w;
+}
+
+// ------------------------------------------------------------------ layer
+FlashIpaLayer::FlashIpaLayer(const Config& cfg) : cfg_(cfg) {
+    cfg_.validate();
+    dims_ = cfg_.dims();
+    if (cudaGetDevice(&device_) != cudaSuccess) {
+        device_ = 0;
+        cudaGetLastError();
+    }
+    w_ = fipa_b200::init_weights(cfg_, 0, cfg_.precision == Precision::f32);
+    dirty_ = true;  // device copies are made lazily by the first forward
+}
+
+FlashIpaLayer::~FlashIpaLayer() {
+    release_device();
+    if (h_stage_) cudaFreeHost(h_stage_);
+    if (d_stage_) cudaFree(d_stage_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+}
+
+void FlashIpaLayer::release_device() {
+    for (void* p : {static_cast<void*>(d_wproj_t_), static_cast<void*>(d_wout_t_),
+                    static_cast<void*>(d_wproj_), static_cast<void*>(d_wout_),
+                    static_cast<void*>(d_bout_), static_cast<void*>(d_head_g_),
+                    static_cast<void*>(d_wl_bias_)}) {
+        if (p) cudaFree(p);
+    }
+    d_wproj_t_ = d_wout_t_ = nullptr;
+    d_wproj_ = d_wout_ = d_bout_ = d_head_g_ = d_wl_bias_ = nullptr;
+}
+
+void FlashIpaLayer::init_weights(std::uint64_t seed) {
+    w_ = fipa_b200::init_weights(cfg_, seed, cfg_.precision == Precision::f32);
+    dirty_ = true;
+}
+
+void FlashIpaLayer::set_weights(const HostWeights& w) {
+    const auto shapes = weight_shapes(cfg_);
+    for (int i = 0; i < 10; ++i)
+        REQUIRE(w.slots[i]->size() == numel(shapes[i]), "weights tensor '", weight_names()[i],
+                "' has ", w.slots[i]->size(), " elements, expected ", numel(shapes[i]));
+    w_ = w;
+    dirty_ = true;
+}
+
+void FlashIpaLayer::save(const std::string& path) const { save_weights_file(w_, weight_shapes(cfg_), path); }
+
+void FlashIpaLayer::load(const std::string& path) {
+    w_ = load_weights_file(path, weight_shapes(cfg_));
+    dirty_ = true;
+}
+
+// Device copies: fused projection matrix in the reference column order
+// (w_q | w_k | w_v | w_qp | w_kp | w_vp), output projection, per-head scalars.
+void FlashIpaLayer::upload_weights() {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    release_device();
+    const LayerDims& d = dims_;
+    const std::size_t din = cfg_.d_in, np = d.n_proj, feat = d.feat, H = cfg_.heads;
+    std::vector<double> wproj(din * np);  // [d_in, n_proj]
+    std::size_t col0 = 0;
+    for (int i = 0; i < 6; ++i) {
+        const std::vector<double>& src = *w_.slots[i];
+        const std::size_t w = src.size() / din;
+        for (std::size_t r = 0; r < din; ++r)
+            for (std::size_t c = 0; c < w; ++c) wproj[r * np + col0 + c] = src[r * w + c];
+        col0 += w;
+    }
+    auto up = [&](auto** dst, const auto& host) {
+        using T = std::remove_reference_t<decltype(host[0])>;
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(dst), host.size() * sizeof(T)), "cudaMalloc");
+        cuda_check(cudaMemcpy(*dst, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice),
+                   "cudaMemcpy H2D");
+    };
+    if (cfg_.precision == Precision::bf16) {
+        std::vector<__nv_bfloat16> t(np * din);
+        for (std::size_t r = 0; r < din; ++r)
+            for (std::size_t c = 0; c < np; ++c)
+                t[c * din + r] = __float2bfloat16_rn(static_cast<float>(wproj[r * np + c]));
+        up(&d_wproj_t_, t);
+        std::vector<__nv_bfloat16> o(din * feat);
+        for (std::size_t r = 0; r < feat; ++r)
+            for (std::size_t c = 0; c < din; ++c)
+                o[c * feat + r] = __float2bfloat16_rn(static_cast<float>(w_.w_out[r * din + c]));
+        up(&d_wout_t_, o);
+    } else {
+        std::vector<float> t(wproj.begin(), wproj.end());
+        up(&d_wproj_, t);
+        std::vector<float> o(w_.w_out.begin(), w_.w_out.end());
+        up(&d_wout_, o);
+    }
+    std::vector<float> bout(w_.b_out.begin(), w_.b_out.end());
+    up(&d_bout_, bout);
+    std::vector<float> g(H), wlb(H * cfg_.d_z);
+    for (std::size_t h = 0; h < H; ++h) g[h] = static_cast<float>(softplus(w_.gamma_raw[h]) * w_.w_l * w_.w_c);
+    for (std::size_t e = 0; e < wlb.size(); ++e) wlb[e] = static_cast<float>(w_.w_l * w_.w_bias[e]);
+    up(&d_head_g_, g);
+    up(&d_wl_bias_, wlb);
+    k_scale_ = static_cast<float>(w_.w_l / std::sqrt(static_cast<double>(cfg_.c)));
+    dirty_ = false;
+}
+
+FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::int64_t L) const {
+    const LayerDims& d = dims_;
+    const std::size_t BL = std::size_t(B) * L, BHL = BL * d.heads;
+    const std::size_t el = cfg_.precision == Precision::bf16 ? 2 : 4;
+    Workspace w;
+    std::size_t off = 0;
+    auto take = [&](std::size_t bytes) {
+        char* p = reinterpret_cast<char*>(reinterpret_cast<std::uintptr_t>(base) + off);
+        off += round_up(bytes, 256);
+        return p;
+    };
+    w.trans_c = reinterpret_cast<float*>(take(BL * 3 * 4));
+    if (cfg_.precision == Precision::bf16) w.s_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.d_in * 2));
+    w.proj = reinterpret_cast<float*>(take(BL * d.n_proj * 4));
+    w.qhat = take(BHL * d.dqk_pad * el);
+    w.khat = take(BHL * d.dqk_pad * el);
+    w.vhat = take(BHL * d.dv_pad * el);
+    w.colbias = reinterpret_cast<float*>(take(BHL * 4));
+    w.lse = reinterpret_cast<float*>(take(BHL * 4));
+    w.feat = take(BL * d.feat * el);
+    w.bytes = off;
+    return w;
+}
+
+std::size_t FlashIpaLayer::workspace_size(std::int64_t B, std::int64_t L) const {
+    return carve(nullptr, B, L).bytes;
+}
+
+int FlashIpaLayer::launches_per_forward() const {
+    return cfg_.precision == Precision::bf16 ? 6 : 5;
+}
+
+void FlashIpaLayer::set_timing(bool on) {
+    timing_ = on;
+    if (on && !ev_[0]) {
+        for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    }
+}
+
+std::vector<float> FlashIpaLayer::stage_times() const {
+    std::vector<float> out;
+    if (!timed_once_) return out;
+    for (int i = 0; i < kStages; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]) != cudaSuccess) ms = -1.f;
+        out.push_back(ms);
+    }
+    return out;
+}
+
+void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                            const float* z2, const float* rot, const float* trans,
+                            const std::uint8_t* mask, float* out, void* workspace,
+                            std::size_t workspace_bytes, cudaStream_t stream) {
+    REQUIRE(B >= 1, "batch must be >= 1");
+    REQUIRE(L >= 1, "empty frame set");
+    REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
+    const Workspace ws = carve(workspace, B, L);
+    REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "workspace too small: need ",
+            ws.bytes, " bytes, got ", workspace_bytes);
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (dirty_) {
+        std::lock_guard<std::mutex> lk(upload_mu_);
+        if (dirty_) upload_weights();
+    }
+    const LayerDims& d = dims_;
+    const int BL = static_cast<int>(B * L);
+    auto mark = [&](int i) {
+        if (timing_) cuda_check(cudaEventRecord(ev_[i], stream), "cudaEventRecord");
+    };
+    mark(0);
+    launch_recenter(trans, mask, ws.trans_c, int(B), int(L), stream);
+    mark(1);
+    if (cfg_.precision == Precision::bf16) {
+        launch_f32_to_bf16(s, ws.s_bf16, std::int64_t(BL) * d.d_in, stream);
+        mark(2);
+        GemmArgs g;
+        g.A = ws.s_bf16;
+        g.lda = d.d_in;
+        g.B = d_wproj_t_;
+        g.ldb = d.d_in;
+        g.C = ws.proj;
+        g.ldc = d.n_proj;
+        g.M = BL;
+        g.N = d.n_proj;
+        g.K = d.d_in;
+        launch_gemm_bf16(g, stream);
+    } else {
+        mark(2);
+        launch_gemm_f32(s, d_wproj_, ws.proj, BL, d.n_proj, d.d_in, nullptr, nullptr, stream);
+    }
+    mark(3);
+    PackArgs pa{};
+    pa.proj = ws.proj;
+    pa.z1 = z1;
+    pa.z2 = z2;
+    pa.rot = rot;
+    pa.trans = ws.trans_c;
+    pa.mask = mask;
+    pa.head_g = d_head_g_;
+    pa.wl_bias = d_wl_bias_;
+    pa.k_scale = k_scale_;
+    pa.qhat = ws.qhat;
+    pa.khat = ws.khat;
+    pa.vhat = ws.vhat;
+    pa.colbias = ws.colbias;
+    pa.B = int(B);
+    pa.L = int(L);
+    pa.out_f32 = cfg_.precision == Precision::f32;
+    launch_pack(d, pa, stream);
+    mark(4);
+    if (cfg_.precision == Precision::bf16) {
+        AttnArgs aa{};
+        aa.qhat = static_cast<const __nv_bfloat16*>(ws.qhat);
+        aa.khat = static_cast<const __nv_bfloat16*>(ws.khat);
+        aa.vhat = static_cast<const __nv_bfloat16*>(ws.vhat);
+        aa.colbias = ws.colbias;
+        aa.z1 = z1;
+        aa.rot = rot;
+        aa.trans = ws.trans_c;
+        aa.feat = static_cast<__nv_bfloat16*>(ws.feat);
+        aa.lse = ws.lse;
+        aa.B = int(B);
+        aa.L = int(L);
+        launch_attn_fwd_tc(d, aa, stream);
+        mark(5);
+        GemmArgs g;
+        g.A = static_cast<const __nv_bfloat16*>(ws.feat);
+        g.lda = d.feat;
+        g.B = d_wout_t_;
+        g.ldb = d.feat;
+        g.C = out;
+        g.ldc = d.d_in;
+        g.M = BL;
+        g.N = d.d_in;
+        g.K = d.feat;
+        g.bias = d_bout_;
+        g.row_mask = mask;
+        launch_gemm_bf16(g, stream);
+    } else {
+        AttnF32Args aa{};
+        aa.qhat = static_cast<const float*>(ws.qhat);
+        aa.khat = static_cast<const float*>(ws.khat);
+        aa.vhat = static_cast<const float*>(ws.vhat);
+        aa.colbias = ws.colbias;
+        aa.z1 = z1;
+        aa.rot = rot;
+        aa.trans = ws.trans_c;
+        aa.feat = static_cast<float*>(ws.feat);
+        aa.lse = ws.lse;
+        aa.B = int(B);
+        aa.L = int(L);
+        launch_attn_fwd_f32(d, aa, stream);
+        mark(5);
+        launch_gemm_f32(static_cast<const float*>(ws.feat), d_wout_, out, BL, d.d_in, d.feat, d_bout_,
+                        mask, stream);
+    }
+    mark(6);
+    if (timing_) timed_once_ = true;
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
+                                 const double* z2, const double* rot, const double* trans,
+                                 const std::uint8_t* mask, double* out) {
+    REQUIRE(B >= 1, "batch must be >= 1");
+    REQUIRE(L >= 1, "empty frame set");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");
+    const std::size_t BL = std::size_t(B) * L;
+    const std::size_t rdz = cfg_.rank * cfg_.d_z;
+    const std::size_t n_s = BL * cfg_.d_in, n_z = BL * rdz, n_r = BL * 9, n_t = BL * 3;
+    const std::size_t n_in = n_s + 2 * n_z + n_r + n_t, n_out = BL * cfg_.d_in;
+    const std::size_t io_bytes = round_up((n_in + n_out) * 4 + BL, 256);
+    const std::size_t ws_bytes = workspace_size(B, L);
+    if (h_stage_bytes_ < io_bytes) {
+        if (h_stage_) cudaFreeHost(h_stage_);
+        h_stage_ = nullptr;
+        cuda_check(cudaMallocHost(&h_stage_, io_bytes), "cudaMallocHost");
+        h_stage_bytes_ = io_bytes;
+    }
+    if (d_stage_bytes_ < io_bytes + ws_bytes) {
+        if (d_stage_) cudaFree(d_stage_);
+        d_stage_ = nullptr;
+        cuda_check(cudaMalloc(&d_stage_, io_bytes + ws_bytes), "cudaMalloc");
+        d_stage_bytes_ = io_bytes + ws_bytes;
+    }
+    float* h = static_cast<float*>(h_stage_);
+    auto cvt = [](float* dst, const double* src, std::size_t n) {
+        for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<float>(src[i]);
+    };
+    cvt(h, s, n_s);
+    cvt(h + n_s, z1, n_z);
+    cvt(h + n_s + n_z, z2, n_z);
+    cvt(h + n_s + 2 * n_z, rot, n_r);
+    cvt(h + n_s + 2 * n_z + n_r, trans, n_t);
+    std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
+    if (mask) std::memcpy(hmask, mask, BL);
+    float* dbase = static_cast<float*>(d_stage_);
+    std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
+    cuda_check(cudaMemcpyAsync(dbase, h, n_in * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
+    if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
+    void* ws = static_cast<char*>(d_stage_) + io_bytes;
+    forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
+            dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
+            own_stream_);
+    cuda_check(cudaMemcpyAsync(h + n_in, dbase + n_in, n_out * 4, cudaMemcpyDeviceToHost, own_stream_),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(own_stream_), "forward");
+    for (std::size_t i = 0; i < n_out; ++i) out[i] = static_cast<double>(h[n_in + i]);
+}
+
+}  // namespace fipa_b200

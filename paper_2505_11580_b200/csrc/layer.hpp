@@ -1,0 +1,151 @@
+// Host C++ side of the B200 FlashIPA layer: configuration, weights (init / file IO / device
+// upload), workspace planning and the forward orchestration that launches the sm_100a kernels.
+//
+// Mirrors the reference layer API: IpaConfig (proj/include/fipa/ipa.hpp:14-32), IpaWeights
+// (ipa.hpp:37-50), flash_ipa_forward (proj/include/fipa/flash_ipa.hpp:55-57) and the weights
+// file (proj/include/fipa/model_io.hpp:15-26).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace fipa_b200 {
+
+// Error taxonomy of the reference (proj/include/fipa/error.hpp:10-28) plus CUDA failures.
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ValueError : Error {
+    using Error::Error;
+};
+struct NumericError : Error {
+    using Error::Error;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+struct CudaError : Error {
+    using Error::Error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+enum class Precision { bf16 = 0, f32 = 1 };
+
+struct Config {
+    std::size_t d_in = 32, d_z = 4, heads = 2, c = 8, n_query = 2, n_value = 2, rank = 2;
+    Precision precision = Precision::bf16;
+    bool enforce_head_cap = true;
+
+    std::size_t qk_width() const { return c + 5 * n_query + rank * d_z; }  // ipa.hpp:27
+    std::size_t v_width() const { return c + 3 * n_value + rank * d_z; }   // ipa.hpp:28
+    static constexpr std::size_t head_cap = 256;
+    void validate() const;  // ipa.cpp:12-21
+    LayerDims dims() const;
+};
+
+// Master weights in the reference layout, kept in float64 on the host.
+struct HostWeights {
+    std::vector<double> w_q, w_k, w_v, w_qp, w_kp, w_vp, w_bias, gamma_raw, w_out, b_out;
+    double w_l = 0.0, w_c = 0.0;
+    bool stored_f32 = false;  // precision tag written by save (0 = f32, 1 = f64)
+
+    std::vector<double>* slots[10] = {&w_q, &w_k, &w_v, &w_qp, &w_kp, &w_vp,
+                                      &w_bias, &gamma_raw, &w_out, &b_out};
+    HostWeights() = default;
+    HostWeights(const HostWeights& o) { *this = o; }
+    HostWeights& operator=(const HostWeights& o);
+};
+
+std::vector<std::vector<std::size_t>> weight_shapes(const Config& cfg);
+const char* const* weight_names();  // 10 names, reference order
+
+HostWeights init_weights(const Config& cfg, std::uint64_t seed, bool round_f32);
+void save_weights_file(const HostWeights& w, const std::vector<std::vector<std::size_t>>& shapes,
+                       const std::string& path);
+HostWeights load_weights_file(const std::string& path,
+                              const std::vector<std::vector<std::size_t>>& shapes);
+
+class FlashIpaLayer {
+public:
+    explicit FlashIpaLayer(const Config& cfg);
+    ~FlashIpaLayer();
+    FlashIpaLayer(const FlashIpaLayer&) = delete;
+    FlashIpaLayer& operator=(const FlashIpaLayer&) = delete;
+
+    const Config& config() const { return cfg_; }
+    const LayerDims& dims() const { return dims_; }
+    const HostWeights& weights() const { return w_; }
+
+    void init_weights(std::uint64_t seed);
+    void set_weights(const HostWeights& w);
+    void save(const std::string& path) const;
+    void load(const std::string& path);
+
+    std::size_t workspace_size(std::int64_t B, std::int64_t L) const;
+    void forward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                 const float* rot, const float* trans, const std::uint8_t* mask, float* out,
+                 void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+    void forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
+                      const double* z2, const double* rot, const double* trans,
+                      const std::uint8_t* mask, double* out);
+    int launches_per_forward() const;
+
+    void set_timing(bool on);
+    std::vector<float> stage_times() const;
+
+    // Workspace carve-up (device pointers into the caller's buffer).
+    struct Workspace {
+        float* trans_c = nullptr;
+        __nv_bfloat16* s_bf16 = nullptr;
+        float* proj = nullptr;
+        void* qhat = nullptr;
+        void* khat = nullptr;
+        void* vhat = nullptr;
+        float* colbias = nullptr;
+        float* lse = nullptr;
+        void* feat = nullptr;
+        std::size_t bytes = 0;
+    };
+    Workspace carve(void* base, std::int64_t B, std::int64_t L) const;
+
+private:
+    void upload_weights();
+    void release_device();
+
+    Config cfg_;
+    LayerDims dims_{};
+    HostWeights w_;
+    int device_ = 0;
+    // device weights
+    __nv_bfloat16* d_wproj_t_ = nullptr;  // bf16 [n_proj, d_in]  (K-major B operand)
+    __nv_bfloat16* d_wout_t_ = nullptr;   // bf16 [d_in, feat]
+    float* d_wproj_ = nullptr;            // f32  [d_in, n_proj]
+    float* d_wout_ = nullptr;             // f32  [feat, d_in]
+    float* d_bout_ = nullptr;             // [d_in]
+    float* d_head_g_ = nullptr;           // [H]
+    float* d_wl_bias_ = nullptr;          // [H, d_z]
+    float k_scale_ = 0.f;
+    bool dirty_ = true;
+    std::mutex upload_mu_;
+    // host-path staging (forward_host)
+    void* h_stage_ = nullptr;
+    std::size_t h_stage_bytes_ = 0;
+    void* d_stage_ = nullptr;
+    std::size_t d_stage_bytes_ = 0;
+    cudaStream_t own_stream_ = nullptr;
+    // timing
+    bool timing_ = false;
+    static constexpr int kStages = 6;
+    cudaEvent_t ev_[kStages + 1] = {};
+    bool timed_once_ = false;
+};
+
+}  // namespace fipa_b200

@@ -1,0 +1,277 @@
+// Frame application + lifted-row packing (K2) and small helpers.
+//
+// Restates, per residue and head, the reference lifts
+//   lift_queries  proj/src/flash_ipa.cpp:23-55
+//   lift_keys     proj/src/flash_ipa.cpp:57-94
+//   lift_values   proj/src/flash_ipa.cpp:96-126
+//   bias_factors  proj/src/pair_features.cpp:141-163 (w_l folded, flash_ipa.cpp:161-167)
+//   apply         proj/src/geometry.cpp:63-68
+// in the B200 layout:
+//   q_hat = [ q (c) | T_i q_p (3Nq) | z1_i flat (r d_z) | 0 pad ]
+//   k_hat = [ (w_l/sqrt c) k | g_h T_j k_p | w_l w_bias[h] (.) z2_j | 0 pad ]
+//   colbias_j = -g_h/2 sum_p |T_j k_p|^2   (-inf for masked keys)
+//   v_hat = [ v | z2_j flat | R_j v_p (3Nv) | t_j hi (3) | t_j lo (3) | 0 pad ]
+// The reference's |T_i q_p|^2 column (paired with -g/2) is constant along a query row and
+// cancels in the softmax, so it is dropped; its (ones, -g/2) pair becomes the fp32 colbias.
+// Value points are stored as R_j v_p plus a hi/lo split translation column so that the
+// bf16 operands keep the translation exact to ~2^-17 (sum_j p_ij T_j v = sum p R v + sum p t).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void store_pair(T* dst, float a, float b);
+template <>
+__device__ __forceinline__ void store_pair<__nv_bfloat16>(__nv_bfloat16* dst, float a, float b) {
+    *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(a, b);
+}
+template <>
+__device__ __forceinline__ void store_pair<float>(float* dst, float a, float b) {
+    *reinterpret_cast<float2*>(dst) = make_float2(a, b);
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
+    extern __shared__ float sm[];
+    const int H = d.heads, c = d.c, Nq = d.n_query, Nv = d.n_value, rdz = d.rank * d.d_z;
+    float* s_proj = sm;                      // n_proj
+    float* s_z1 = s_proj + d.n_proj;         // rdz
+    float* s_z2 = s_z1 + rdz;                // rdz
+    float* s_gq = s_z2 + rdz;                // H*Nq*3
+    float* s_gk = s_gq + H * Nq * 3;         // H*Nq*3
+    float* s_gv = s_gk + H * Nq * 3;         // H*Nv*3
+    float* s_kn = s_gv + H * Nv * 3;         // H
+
+    const int64_t row = blockIdx.x;  // b*L + i
+    const int b = static_cast<int>(row / a.L);
+    const int i = static_cast<int>(row % a.L);
+    const int tid = threadIdx.x;
+
+    const float* prow = a.proj + row * d.n_proj;
+    for (int e = tid; e < d.n_proj; e += blockDim.x) s_proj[e] = prow[e];
+    for (int e = tid; e < rdz; e += blockDim.x) {
+        s_z1[e] = a.z1[row * rdz + e];
+        s_z2[e] = a.z2[row * rdz + e];
+    }
+    float R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = a.rot[row * 9 + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = a.trans[row * 3 + k];
+    __syncthreads();
+
+    // Column offsets of the fused projection (reference order w_q|w_k|w_v|w_qp|w_kp|w_vp).
+    const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
+    const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
+    const int npts = H * Nq * 2 + H * Nv;
+    for (int e = tid; e < npts; e += blockDim.x) {
+        const float* src;
+        float* dst;
+        bool add_t = true;
+        int idx;
+        if (e < H * Nq) {
+            idx = e;
+            src = s_proj + off_qp + idx * 3;
+            dst = s_gq + idx * 3;
+        } else if (e < 2 * H * Nq) {
+            idx = e - H * Nq;
+            src = s_proj + off_kp + idx * 3;
+            dst = s_gk + idx * 3;
+        } else {
+            idx = e - 2 * H * Nq;
+            src = s_proj + off_vp + idx * 3;
+            dst = s_gv + idx * 3;
+            add_t = false;
+        }
+        const float x = src[0], y = src[1], z = src[2];
+        dst[0] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z)) + (add_t ? t[0] : 0.f);
+        dst[1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z)) + (add_t ? t[1] : 0.f);
+        dst[2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z)) + (add_t ? t[2] : 0.f);
+    }
+    __syncthreads();
+    for (int h = tid; h < H; h += blockDim.x) {
+        float acc = 0.f;
+        for (int e = 0; e < Nq * 3; ++e) {
+            const float g = s_gk[h * Nq * 3 + e];
+            acc = fmaf(g, g, acc);
+        }
+        s_kn[h] = acc;
+    }
+    __syncthreads();
+
+    const bool valid = a.mask == nullptr || a.mask[row] != 0;
+    OutT* qh = static_cast<OutT*>(a.qhat);
+    OutT* kh = static_cast<OutT*>(a.khat);
+    OutT* vh = static_cast<OutT*>(a.vhat);
+    const int qk_geo = c + 3 * Nq, qk_used = d.dqk_used;
+    const int v_pair = c + rdz, v_pts = v_pair + 3 * Nv, v_used = d.dv_used;
+
+    for (int h = 0; h < H; ++h) {
+        const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
+        const float g = a.head_g[h];
+        OutT* q = qh + hrow * d.dqk_pad;
+        OutT* k = kh + hrow * d.dqk_pad;
+        OutT* v = vh + hrow * d.dv_pad;
+        for (int col = 2 * tid; col < d.dqk_pad; col += 2 * blockDim.x) {
+            float qv[2], kv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int cc = col + u;
+                if (cc < c) {
+                    qv[u] = s_proj[off_q + h * c + cc];
+                    kv[u] = a.k_scale * s_proj[off_k + h * c + cc];
+                } else if (cc < qk_geo) {
+                    qv[u] = s_gq[h * Nq * 3 + (cc - c)];
+                    kv[u] = g * s_gk[h * Nq * 3 + (cc - c)];
+                } else if (cc < qk_used) {
+                    const int e = cc - qk_geo;
+                    qv[u] = s_z1[e];
+                    kv[u] = a.wl_bias[h * d.d_z + (e % d.d_z)] * s_z2[e];
+                } else {
+                    qv[u] = 0.f;
+                    kv[u] = 0.f;
+                }
+            }
+            store_pair<OutT>(q + col, qv[0], qv[1]);
+            store_pair<OutT>(k + col, kv[0], kv[1]);
+        }
+        for (int col = 2 * tid; col < d.dv_pad; col += 2 * blockDim.x) {
+            float vv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int cc = col + u;
+                float x;
+                if (cc < c) {
+                    x = s_proj[off_v + h * c + cc];
+                } else if (cc < v_pair + 0 && cc >= c) {
+                    x = s_z2[cc - c];
+                } else if (cc < v_pts) {
+                    x = s_gv[h * Nv * 3 + (cc - v_pair)];
+                } else if (cc < v_pts + 3) {
+                    const float tt = t[cc - v_pts];
+                    x = sizeof(OutT) == 4 ? tt : __bfloat162float(__float2bfloat16_rn(tt));
+                } else if (cc < v_used) {
+                    const float tt = t[cc - v_pts - 3];
+                    x = sizeof(OutT) == 4 ? 0.f : tt - __bfloat162float(__float2bfloat16_rn(tt));
+                } else {
+                    x = 0.f;
+                }
+                vv[u] = x;
+            }
+            store_pair<OutT>(v + col, vv[0], vv[1]);
+        }
+        if (tid == 0) a.colbias[hrow] = valid ? -0.5f * g * s_kn[h] : -INFINITY;
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   int64_t n) {
+    const int64_t n4 = n / 4;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n4;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(in)[e];
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&lo);
+        w.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(out)[e] = w;
+    }
+    for (int64_t e = n4 * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        out[e] = __float2bfloat16_rn(in[e]);
+    }
+}
+
+// One block per sample: subtract the centroid of the valid residues' translations.
+__global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
+                                float* __restrict__ out, int L) {
+    __shared__ float red[4][32];
+    const int b = blockIdx.x;
+    const float* t = trans + int64_t(b) * L * 3;
+    float sx = 0.f, sy = 0.f, sz = 0.f, cnt = 0.f;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const bool ok = mask == nullptr || mask[int64_t(b) * L + i] != 0;
+        if (ok) {
+            sx += t[i * 3 + 0];
+            sy += t[i * 3 + 1];
+            sz += t[i * 3 + 2];
+            cnt += 1.f;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[0][w] = sx;
+        red[1][w] = sy;
+        red[2][w] = sz;
+        red[3][w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int nw = blockDim.x >> 5;
+        float v[4];
+        for (int k = 0; k < 4; ++k) {
+            v[k] = l < nw ? red[k][l] : 0.f;
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        }
+        if (l == 0) {
+            const float n = v[3] > 0.f ? v[3] : 1.f;
+            red[0][0] = v[0] / n;
+            red[1][0] = v[1] / n;
+            red[2][0] = v[2] / n;
+        }
+    }
+    __syncthreads();
+    const float cx = red[0][0], cy = red[1][0], cz = red[2][0];
+    float* o = out + int64_t(b) * L * 3;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        o[i * 3 + 0] = t[i * 3 + 0] - cx;
+        o[i * 3 + 1] = t[i * 3 + 1] - cy;
+        o[i * 3 + 2] = t[i * 3 + 2] - cz;
+    }
+}
+
+}  // namespace
+
+void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream) {
+    const int rdz = d.rank * d.d_z;
+    const size_t smem =
+        sizeof(float) * (d.n_proj + 2 * rdz + d.heads * (d.n_query * 6 + d.n_value * 3) + d.heads);
+    const dim3 grid(static_cast<unsigned>(int64_t(a.B) * a.L));
+    if (a.out_f32) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(pack_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+        pack_kernel<float><<<grid, 256, smem, stream>>>(d, a);
+    } else {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(pack_kernel<__nv_bfloat16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        pack_kernel<__nv_bfloat16><<<grid, 256, smem, stream>>>(d, a);
+    }
+}
+
+void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
+    f32_to_bf16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, n);
+}
+
+void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
+                     cudaStream_t stream) {
+    recenter_kernel<<<B, 256, 0, stream>>>(trans, mask, out, L);
+}
+
+}  // namespace fipa_b200

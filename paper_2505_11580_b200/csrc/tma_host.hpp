@@ -1,0 +1,69 @@
+// Host-side TMA tensor-map construction (cuTensorMapEncodeTiled fetched through the
+// runtime's driver entry point, so the library needs no -lcuda at link time).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace fipa_b200 {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        if (e != cudaSuccess || p == nullptr || q != cudaDriverEntryPointSuccess) {
+            throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+        }
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// Row-major bf16 matrix [rows, cols] (cols contiguous, row stride `ld` elements),
+// box {box_cols (inner, must be 64 for SWIZZLE_128B), box_rows}.
+inline CUtensorMap make_map_2d_bf16(const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                                    uint32_t box_cols, uint32_t box_rows) {
+    CUtensorMap m{};
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(2d) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
+// bf16 tensor [d2, d1, d0] (d0 contiguous, rows of `ld` elements), box {box0, box1, 1}.
+inline CUtensorMap make_map_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                                    uint64_t ld, uint32_t box0, uint32_t box1) {
+    CUtensorMap m{};
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {ld * 2, ld * 2 * d1};
+    cuuint32_t box[3] = {box0, box1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(3d) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
+}  // namespace fipa_b200

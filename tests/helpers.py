@@ -1,0 +1,135 @@
+"""Shared test helpers: problem generation, oracle runs, GPU runs through the C ABI.
+
+The oracle (oracle/fipa_oracle.py) is the checker only; GPU results always come from the
+native library (libfipa_b200.so) through the Model binding.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from oracle import fipa_oracle as fo
+
+MAIN = dict(d_in=256, d_z=128, heads=8, c=128, n_query=8, n_value=12, rank=2)  # north-star shape
+TINY = dict(d_in=32, d_z=4, heads=2, c=8, n_query=2, n_value=2, rank=2)  # reference Model() default
+
+BF16_TOL = 2e-2  # north_star: bf16 inputs, fp32 accumulation
+F32_TOL = 1e-4  # north_star: fp32 path
+
+
+def oracle_cfg(shape: dict, precision="f64") -> fo.IpaConfig:
+    return fo.IpaConfig(**shape, precision=precision, enforce_head_cap=False)
+
+
+def make_batch(shape, B, L, seed, translation_scale=1.0, mask_frac=0.0, bf16=False):
+    """B independent reference-style problems, stacked on a leading axis."""
+    cfg = oracle_cfg(shape)
+    probs = [fo.make_problem(cfg, L, seed + 17 * b, translation_scale, mask_frac) for b in range(B)]
+    out = {k: np.stack([getattr(p, k) for p in probs]) for k in ("s", "z1", "z2", "rot", "trans", "mask")}
+    if bf16:
+        for k in ("s", "z1", "z2"):
+            out[k] = fo.round_bf16(out[k])
+    return out
+
+
+def oracle_weights_for(model, precision):
+    """The weights the GPU path actually computes with, as float64 for the oracle."""
+    w = dict(model.weights())
+    if precision == "bf16":
+        for n in ("w_q", "w_k", "w_v", "w_qp", "w_kp", "w_vp", "w_out"):
+            w[n] = fo.round_bf16(w[n])
+        for n in ("w_bias", "b_out"):
+            w[n] = fo.round_f32(w[n])
+    return w
+
+
+def oracle_forward(shape, w, batch, return_intermediates=False):
+    cfg = oracle_cfg(shape)
+    outs, inters = [], []
+    for b in range(batch["s"].shape[0]):
+        r = fo.flash_ipa_forward(batch["s"][b], batch["z1"][b], batch["z2"][b], batch["rot"][b],
+                                 batch["trans"][b], batch["mask"][b], cfg, w,
+                                 return_intermediates=return_intermediates)
+        if return_intermediates:
+            outs.append(r[0])
+            inters.append(r[1])
+        else:
+            outs.append(r)
+    return (np.stack(outs), inters) if return_intermediates else np.stack(outs)
+
+
+def rel_dev(ref, got):
+    return fo.rel_dev(ref, got)
+
+
+def random_rigid(seed, scale=10.0):
+    rng = fo.Rng(seed)
+    return fo.random_rototranslation(rng, scale)
+
+
+def move_frames(batch, g_rot, g_trans):
+    """Global rigid motion g . T_i for every frame (proj/src/bench.cpp:56-62)."""
+    out = dict(batch)
+    out["rot"] = np.einsum("ab,...bc->...ac", g_rot, batch["rot"])
+    out["trans"] = np.einsum("ab,...b->...a", g_rot, batch["trans"]) + g_trans
+    return out
+
+
+# ------------------------------------------------------------------ GPU side
+def gpu_forward_device(model, batch):
+    """Run fipa_layer_forward over torch-owned device buffers; returns (out, workspace, layout)."""
+    import torch
+
+    dev = torch.device("cuda:0")
+    B, L = batch["s"].shape[:2]
+    t = {k: torch.from_numpy(np.ascontiguousarray(batch[k], dtype=np.float32)).to(dev)
+         for k in ("s", "z1", "z2", "rot", "trans")}
+    mask = torch.from_numpy(np.ascontiguousarray(batch["mask"], dtype=np.uint8)).to(dev)
+    out = torch.empty((B, L, model.config["d_in"]), dtype=torch.float32, device=dev)
+    nbytes = model.workspace_size(B, L)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    model.forward_device(B, L, t["s"].data_ptr(), t["z1"].data_ptr(), t["z2"].data_ptr(),
+                         t["rot"].data_ptr(), t["trans"].data_ptr(), mask.data_ptr(), out.data_ptr(),
+                         ws.data_ptr(), nbytes, stream.cuda_stream)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64), ws, model.workspace_layout(B, L)
+
+
+def ws_view(ws, offset, count, dtype):
+    """Typed float64 numpy copy of `count` elements at byte `offset` of a torch uint8 workspace."""
+    import torch
+
+    nbytes = count * (2 if dtype == "bf16" else 4)
+    raw = ws[offset:offset + nbytes]
+    if dtype == "bf16":
+        return raw.view(torch.bfloat16).float().cpu().numpy().astype(np.float64)
+    return raw.view(torch.float32).cpu().numpy().astype(np.float64)
+
+
+def expected_packed(shape, w, batch, b):
+    """Oracle q_hat/k_hat/v_hat/colbias of sample b in the B200 layout."""
+    cfg = oracle_cfg(shape)
+    s, z1, z2, rot, trans = (batch[k][b] for k in ("s", "z1", "z2", "rot", "trans"))
+    mask = batch["mask"][b]
+    valid = mask.astype(bool)
+    trans_c = trans - (trans[valid].mean(0) if valid.any() else 0.0)
+    q, k, v, qp, kp, vp = fo.project_inputs(s, cfg, w)
+    H, L = cfg.heads, s.shape[0]
+    gamma = fo.softplus(w["gamma_raw"])
+    g = (gamma * w["w_l"] * w["w_c"])[:, None, None]
+    gq = fo.apply(rot[None, :, None], trans_c[None, :, None], qp).reshape(H, L, -1)
+    gk = fo.apply(rot[None, :, None], trans_c[None, :, None], kp)
+    rv = np.einsum("lab,hlpb->hlpa", rot, vp).reshape(H, L, -1)
+    b1 = np.broadcast_to(z1.reshape(1, L, -1), (H, L, cfg.rank * cfg.d_z))
+    b2 = ((w["w_l"] * w["w_bias"])[:, None, None, :] * z2[None]).reshape(H, L, -1)
+    qh = np.concatenate([q, gq, b1], -1)
+    kh = np.concatenate([w["w_l"] / math.sqrt(cfg.c) * k, g * gk.reshape(H, L, -1), b2], -1)
+    z2f = np.broadcast_to(z2.reshape(1, L, -1), (H, L, cfg.rank * cfg.d_z))
+    tt = np.broadcast_to(trans_c[None], (H, L, 3))
+    vh = np.concatenate([v, z2f, rv, tt], -1)
+    cb = -0.5 * g[:, :, 0] * (gk ** 2).sum((-1, -2))
+    cb = np.where(valid[None], cb, -np.inf)
+    return qh, kh, vh, cb
