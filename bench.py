@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""FlashIPA layer benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1] shape): the north-star FlashIPA layer
+(c_s 256, c_z 128, c_hidden 128, 8 heads, 8 qk-points, 12 v-points, z_factor_rank 2) on
+B=8 sequences of L=1024 residues, bf16 operands / fp32 accumulation, random-init weights
+(IpaWeights::init, seed 0), synthetic reference-distribution inputs.
+A step = one layer forward over the batch (see config.pass).
+
+--impl ours (default): libfipa_b200.so through the C ABI; device-timed with CUDA events on the
+   stream the kernels run on, L2 flushed (256 MiB write) before every timed step, max over ranks.
+--impl reference: the reference's own CPU flash_ipa_forward (oracle/_ref, built from
+   /root/reference sources) on the host cores, rank 0 only.
+Multi-GPU (torchrun): samples are independent, every rank runs its own batch (weak scaling,
+no data-path collective); torch.distributed only provides the barrier and the max-over-ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = dict(d_in=256, d_z=128, heads=8, c=128, n_query=8, n_value=12, rank=2)
+METRIC = "FlashIPA layer residues/sec & attn TFLOP/s vs bf16 peak, L=1k-64k, 1-8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--B", type=int, default=8)
+    ap.add_argument("--L", type=int, default=1024)
+    ap.add_argument("--rank", type=int, default=SHAPE["rank"], dest="zrank")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-L", type=int, default=0, help="residues per CPU sample (default L)")
+    return ap.parse_args()
+
+
+def dims(shape):
+    qk = shape["c"] + 5 * shape["n_query"] + shape["rank"] * shape["d_z"]
+    v = shape["c"] + 3 * shape["n_value"] + shape["rank"] * shape["d_z"]
+    return qk, v
+
+
+def attn_flops(shape, B, L):
+    """Algorithmic attention FLOPs: 2*B*H*L^2*(D_qk + D_v) with the reference widths
+    (IpaConfig::qk_width / v_width, proj/include/fipa/ipa.hpp:27-28)."""
+    qk, v = dims(shape)
+    return 2.0 * B * shape["heads"] * L * L * (qk + v)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].strip() == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def synth_inputs(B, L, shape, seed=1234):
+    """Reference-distribution synthetic inputs (proj/tests/test_support.hpp:36-52):
+    s, z1, z2 ~ N(0,1) (bf16-rounded for the bf16 arm), frames = uniform rotation +
+    N(0, 1 A^2) translation."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    s = rng.standard_normal((B, L, shape["d_in"]), dtype=np.float32)
+    z1 = rng.standard_normal((B, L, shape["rank"], shape["d_z"]), dtype=np.float32)
+    z2 = rng.standard_normal((B, L, shape["rank"], shape["d_z"]), dtype=np.float32)
+    q = rng.standard_normal((B, L, 4))
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    w, x, y, z = np.moveaxis(q, -1, 0)
+    rot = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                    2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                    2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)
+    rot = rot.reshape(B, L, 3, 3).astype(np.float32)
+    trans = rng.standard_normal((B, L, 3)).astype(np.float32)
+    mask = np.ones((B, L), dtype=np.uint8)
+    return dict(s=s, z1=z1, z2=z2, rot=rot, trans=trans, mask=mask)
+
+
+def cpu_reference_step(shape, L, threads, seed=7):
+    """One reference flash_ipa_forward (f32 storage) on the host cores; returns (seconds, kind)."""
+    from oracle import fipa_oracle as fo
+
+    cfg = fo.IpaConfig(**shape, precision="f32", enforce_head_cap=False)
+    p = fo.make_problem(cfg, L, seed)
+    try:
+        from oracle import ref
+
+        if ref.available():
+            w = ref.init_weights(cfg, 0)
+            t0 = time.perf_counter()
+            ref.flash_forward(cfg, w, p.s, p.z1, p.z2, p.rot, p.trans, None, 64, 64, threads)
+            return time.perf_counter() - t0, "reference"
+    except Exception:
+        pass
+    w = fo.init_weights(fo.IpaConfig(**shape, enforce_head_cap=False), 0)
+    t0 = time.perf_counter()
+    fo.flash_ipa_forward(p.s, p.z1, p.z2, p.rot, p.trans, None, cfg, w)
+    return time.perf_counter() - t0, "port"
+
+
+def run_reference(args, shape):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    L = args.cpu_sample_L or args.L
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_reference_step(shape, L, threads)
+    times, kind = [], "reference"
+    for _ in range(args.steps):
+        t, kind = cpu_reference_step(shape, L, threads)
+        times.append(t)
+    total = sum(times)
+    value = L * len(times) / total
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "residues/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 storage, f64 accumulation (reference CPU)",
+        "data": "synthetic (reference generators), random-init weights",
+        "config": {"workload": f"layer forward, 1 sequence of L={L} per step (bounded sample of B={args.B})",
+                   "shape": shape, "B": 1, "L": L},
+        "cpu_baseline": {"value": value, "unit": "residues/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.steps} x 1 sequence, L={L}"},
+        "e2e": {"value": value, "unit": "residues/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, shape):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2505_11580_b200 as fipa
+
+    B, L = args.B, args.L
+    dev = torch.device("cuda", local)
+    model = fipa.Model(**shape, precision=args.precision, seed=0, enforce_head_cap=False)
+    host = synth_inputs(B, L, shape, seed=1234 + rank)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in host.items()}
+    out = torch.empty((B, L, shape["d_in"]), dtype=torch.float32, device=dev)
+    ws_bytes = model.workspace_size(B, L)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        model.forward_device(B, L, t["s"].data_ptr(), t["z1"].data_ptr(), t["z2"].data_ptr(),
+                             t["rot"].data_ptr(), t["trans"].data_ptr(), t["mask"].data_ptr(),
+                             out.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def timed_pass(stage_timing):
+        model.set_timing(stage_timing)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        stages = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()  # L2 flush outside the timed window
+            a.record(stream)
+            step()
+            b.record(stream)
+            if stage_timing:
+                b.synchronize()
+                stages.append(model.stage_times())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        model.set_timing(False)
+        return ms, stages
+
+    gpu_index = local
+    with ClockSampler(gpu_index) as clk:
+        ms_total, _ = timed_pass(False)
+    _, stages = timed_pass(True)
+
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_t.item())
+    ms_step = ms_total / args.steps
+    residues = B * L * world * args.steps
+    value = residues / (ms_total / 1e3)
+
+    st = np.array(stages, dtype=np.float64)  # recenter, cast, proj, pack, attn, out
+    st_mean = st.mean(0) if len(st) else np.zeros(6)
+    attn_ms = float(st_mean[4])
+    flops = attn_flops(shape, B, L)
+    achieved = flops / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
+    peak, peak_sus, peak_kind = load_peaks()
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "attn_fwd_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e through the public API: numpy host buffers in, host result out (Model.flash copies
+    # H2D from pinned staging, runs, copies D2H, synchronises).
+    e2e = None
+    if not args.no_e2e:
+        hin = {k: host[k].astype(np.float64) for k in ("s", "z1", "z2", "rot", "trans")}
+        model.flash(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], mask=host["mask"])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(3, min(args.steps, 10))
+        for _ in range(n_e2e):
+            model.flash(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], mask=host["mask"])
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        h2d = 4 * B * L * (shape["d_in"] + 2 * shape["rank"] * shape["d_z"] + 12) + B * L
+        d2h = 4 * B * L * shape["d_in"]
+        e2e = {"value": B * L * world * n_e2e / float(el.item()), "unit": "residues/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "Model.flash (float64 numpy in/out, fipa_layer_forward_host)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        Ls = args.cpu_sample_L or L
+        secs, kind = cpu_reference_step(shape, Ls, threads)
+        n = 1
+        while secs < 10.0 and n < 8:
+            s2, kind = cpu_reference_step(shape, Ls, threads, seed=7 + n)
+            secs += s2
+            n += 1
+        cpu = {"value": Ls * n / secs, "unit": "residues/s", "cores": threads, "kind": kind,
+               "sample": f"{n} x flash_ipa_forward(f32 storage), 1 sequence of L={Ls}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "residues/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic (reference input distribution), random-init weights",
+            "config": {"workload": f"FlashIPA layer forward, B={B} L={L} per GPU (cfg2 shape; backward pending)",
+                       "pass": "fwd", "model": "FlashIPA layer", "global_batch": B * world, "seq_len": L,
+                       "shape": shape, "parallelism": f"dp{world} (independent samples)",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "attn_tflops": achieved,
+            "stage_ms": {k: float(v) for k, v in zip(
+                ["recenter", "cast", "proj_gemm", "pack", "attn_fwd+epilogue", "out_gemm"], st_mean)},
+            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
+                         "traffic": traffic,
+                         "algorithmic": f"2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per launch"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": model.forward_launches() * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    shape = dict(SHAPE, rank=args.zrank)
+    if args.impl == "reference":
+        return run_reference(args, shape)
+    return run_ours(args, shape)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

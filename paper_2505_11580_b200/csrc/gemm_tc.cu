@@ -211,7 +211,10 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
 
 void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return;
-    if (a.K % 16 != 0) throw std::invalid_argument("gemm: K must be a multiple of 16");
+    // K tails need no special case: TMA zero-fills the out-of-range part of the last K block.
+    // TMA does need 16-byte aligned row strides.
+    if ((a.lda * 2) % 16 != 0 || (a.ldb * 2) % 16 != 0)
+        throw std::invalid_argument("gemm: operand row strides must be multiples of 8 elements");
     if (a.accumulate && a.out_bf16) throw std::invalid_argument("gemm: accumulate needs fp32 C");
     const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512);
     const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);

@@ -36,12 +36,16 @@ void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 struct LayerDims {
     int d_in, d_z, heads, c, n_query, n_value, rank;
     int n_proj;      // H*(3c + 6Nq + 3Nv): fused projection width
-    int dqk_used;    // c + 3Nq + r*d_z           (lifted query/key width, norms/ones dropped)
+    int dqk_used;    // c + 3Nq + 20 + r*d_z      (lifted query/key width, see pack.cu)
     int dqk_pad;     // dqk_used rounded up to 16
     int dv_used;     // c + r*d_z + 3Nv + 6       (v | z2 | R v_p | t_hi | t_lo)
     int dv_pad;      // dv_used rounded up to 16
+    int dv_tc;       // value columns accumulated by the tensor cores (multiple of 16, <= 416)
+    int dv_simt;     // dv_used - dv_tc trailing value columns accumulated on CUDA cores
     int seg;         // d_z + c + 4Nv             (per-head feature block)
     int feat;        // H*seg
+    int din_ld;      // d_in rounded up to 8  (row stride of bf16 GEMM operands, TMA needs 16 B)
+    int feat_ld;     // feat rounded up to 8  (row stride of the feature buffer)
 };
 
 struct PackArgs {
@@ -57,7 +61,7 @@ struct PackArgs {
     void* qhat;            // [B*H, L, dqk_pad]
     void* khat;            // [B*H, L, dqk_pad]
     void* vhat;            // [B*H, L, dv_pad]
-    float* colbias;        // [B*H, L]  -g/2 * sum_p |T_j k_p|^2, -inf for masked keys
+    float* colbias;        // [B*H, L]  -g/2 * sum_p |T_j k_p|^2 (natural units), -inf masked
     int B, L;
     bool out_f32;          // write fp32 rows (SIMT f32 path) instead of bf16
 };
@@ -81,12 +85,15 @@ void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stre
 
 // Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);
+// Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
+void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
+                           cudaStream_t stream);
 // Subtract each sample's translation centroid (exact: the layer is invariant to it).
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream);
 
 // ------------------------------------------------------ SIMT fp32 path
-void launch_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K,
+void launch_gemm_f32(const float* A, int lda, const float* B, float* C, int M, int N, int K,
                      const float* bias, const uint8_t* row_mask, cudaStream_t stream);
 struct AttnF32Args {
     const float* qhat;

@@ -107,12 +107,17 @@ LayerDims Config::dims() const {
     d.n_value = int(n_value);
     d.rank = int(rank);
     d.n_proj = int(heads * (3 * c + 6 * n_query + 3 * n_value));
-    d.dqk_used = int(c + 3 * n_query + rank * d_z);
+    d.dqk_used = int(c + 3 * n_query + 20 + rank * d_z);
     d.dqk_pad = int(round_up(d.dqk_used, 16));
     d.dv_used = int(c + rank * d_z + 3 * n_value + 6);
     d.dv_pad = int(round_up(d.dv_used, 16));
+    // TMEM budget of the tcgen05 attention: O (dv_tc) + S (64) + P (32) <= 512 columns.
+    d.dv_tc = std::min(d.dv_pad, 416);
+    d.dv_simt = std::max(0, d.dv_used - d.dv_tc);
     d.seg = int(d_z + c + 4 * n_value);
     d.feat = int(heads) * d.seg;
+    d.din_ld = int(round_up(d_in, 8));
+    d.feat_ld = int(round_up(d.feat, 8));
     return d;
 }
 
@@ -395,15 +400,16 @@ void FlashIpaLayer::upload_weights() {
                    "cudaMemcpy H2D");
     };
     if (cfg_.precision == Precision::bf16) {
-        std::vector<__nv_bfloat16> t(np * din);
+        const std::size_t dld = d.din_ld, fld = d.feat_ld;
+        std::vector<__nv_bfloat16> t(np * dld, __float2bfloat16_rn(0.f));
         for (std::size_t r = 0; r < din; ++r)
             for (std::size_t c = 0; c < np; ++c)
-                t[c * din + r] = __float2bfloat16_rn(static_cast<float>(wproj[r * np + c]));
+                t[c * dld + r] = __float2bfloat16_rn(static_cast<float>(wproj[r * np + c]));
         up(&d_wproj_t_, t);
-        std::vector<__nv_bfloat16> o(din * feat);
+        std::vector<__nv_bfloat16> o(din * fld, __float2bfloat16_rn(0.f));
         for (std::size_t r = 0; r < feat; ++r)
             for (std::size_t c = 0; c < din; ++c)
-                o[c * feat + r] = __float2bfloat16_rn(static_cast<float>(w_.w_out[r * din + c]));
+                o[c * fld + r] = __float2bfloat16_rn(static_cast<float>(w_.w_out[r * din + c]));
         up(&d_wout_t_, o);
     } else {
         std::vector<float> t(wproj.begin(), wproj.end());
@@ -434,14 +440,14 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         return p;
     };
     w.trans_c = reinterpret_cast<float*>(take(BL * 3 * 4));
-    if (cfg_.precision == Precision::bf16) w.s_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.d_in * 2));
+    if (cfg_.precision == Precision::bf16) w.s_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
     w.proj = reinterpret_cast<float*>(take(BL * d.n_proj * 4));
     w.qhat = take(BHL * d.dqk_pad * el);
     w.khat = take(BHL * d.dqk_pad * el);
     w.vhat = take(BHL * d.dv_pad * el);
     w.colbias = reinterpret_cast<float*>(take(BHL * 4));
     w.lse = reinterpret_cast<float*>(take(BHL * 4));
-    w.feat = take(BL * d.feat * el);
+    w.feat = take(BL * d.feat_ld * el);
     w.bytes = off;
     return w;
 }
@@ -496,13 +502,13 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
     launch_recenter(trans, mask, ws.trans_c, int(B), int(L), stream);
     mark(1);
     if (cfg_.precision == Precision::bf16) {
-        launch_f32_to_bf16(s, ws.s_bf16, std::int64_t(BL) * d.d_in, stream);
+        launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
         mark(2);
         GemmArgs g;
         g.A = ws.s_bf16;
-        g.lda = d.d_in;
+        g.lda = d.din_ld;
         g.B = d_wproj_t_;
-        g.ldb = d.d_in;
+        g.ldb = d.din_ld;
         g.C = ws.proj;
         g.ldc = d.n_proj;
         g.M = BL;
@@ -511,7 +517,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         launch_gemm_bf16(g, stream);
     } else {
         mark(2);
-        launch_gemm_f32(s, d_wproj_, ws.proj, BL, d.n_proj, d.d_in, nullptr, nullptr, stream);
+        launch_gemm_f32(s, d.d_in, d_wproj_, ws.proj, BL, d.n_proj, d.d_in, nullptr, nullptr, stream);
     }
     mark(3);
     PackArgs pa{};
@@ -550,9 +556,9 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         mark(5);
         GemmArgs g;
         g.A = static_cast<const __nv_bfloat16*>(ws.feat);
-        g.lda = d.feat;
+        g.lda = d.feat_ld;
         g.B = d_wout_t_;
-        g.ldb = d.feat;
+        g.ldb = d.feat_ld;
         g.C = out;
         g.ldc = d.d_in;
         g.M = BL;
@@ -576,7 +582,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         aa.L = int(L);
         launch_attn_fwd_f32(d, aa, stream);
         mark(5);
-        launch_gemm_f32(static_cast<const float*>(ws.feat), d_wout_, out, BL, d.d_in, d.feat, d_bout_,
+        launch_gemm_f32(static_cast<const float*>(ws.feat), d.feat_ld, d_wout_, out, BL, d.d_in, d.feat, d_bout_,
                         mask, stream);
     }
     mark(6);

@@ -6,18 +6,29 @@
 //   lift_values   proj/src/flash_ipa.cpp:96-126
 //   bias_factors  proj/src/pair_features.cpp:141-163 (w_l folded, flash_ipa.cpp:161-167)
 //   apply         proj/src/geometry.cpp:63-68
-// in the B200 layout:
-//   q_hat = [ q (c) | T_i q_p (3Nq) | z1_i flat (r d_z) | 0 pad ]
-//   k_hat = [ (w_l/sqrt c) k | g_h T_j k_p | w_l w_bias[h] (.) z2_j | 0 pad ]
-//   colbias_j = -g_h/2 sum_p |T_j k_p|^2   (-inf for masked keys)
-//   v_hat = [ v | z2_j flat | R_j v_p (3Nv) | t_j hi (3) | t_j lo (3) | 0 pad ]
+// in the B200 layout.  With A_p = T_i q_p = R_i q_p + t_i and
+// B_p = T_j k_p, the reference point term g*sum_p <A_p, B_p> is expanded exactly as
+//   g*sum_p <R_i q_p, R_j k_p> + g<Qbar_i, t_j> + g<t_i, W_j>,  Qbar_i = sum_p R_i q_p,
+//   W_j = sum_p T_j k_p,
+// so the only large (translation-sized) products sit in two 3-vector dot products that are
+// carried as bf16 hi/lo splits (a.b ~ a_hi.b_hi + a_hi.b_lo + a_lo.b_hi).  This keeps the
+// bf16 logits accurate for protein-scale coordinates (tens of Angstrom), where a plain bf16
+// T_i q_p column loses ~1 logit unit.  Per head (L2E = log2 e, queries pre-scaled so that
+// S = q_hat . k_hat is in log2 units):
+//   q_hat = L2E*[ q | R_i q_p | Qbar hi,hi,lo | t_i hi,lo,hi ] | 1, 1 | L2E*z1_i | 0
+//   k_hat = [ (w_l/sqrt c) k | g R_j k_p | g t_j hi,lo,hi | g W_j hi,hi,lo ] | cb hi, lo |
+//           w_l w_bias[h] (.) z2_j | 0
+//   cb_j  = L2E * (-g/2 sum_p |T_j k_p|^2)   (-1e30 for masked keys, lo = 0)
 // The reference's |T_i q_p|^2 column (paired with -g/2) is constant along a query row and
-// cancels in the softmax, so it is dropped; its (ones, -g/2) pair becomes the fp32 colbias.
-// Value points are stored as R_j v_p plus a hi/lo split translation column so that the
-// bf16 operands keep the translation exact to ~2^-17 (sum_j p_ij T_j v = sum p R v + sum p t).
+// cancels in the softmax, so it is dropped; its (ones, -g/2 |k|^2) pair becomes the folded
+// column bias cb.  Values:
+//   v_hat = [ v | z2_j flat | R_j v_p (3Nv) | t_j hi (3) | t_j lo (3) | 0 ]
+// (sum_j p_ij T_j v_p = sum_j p_ij R_j v_p + sum_j p_ij t_j, translation kept to ~2^-17).
+// For the fp32 path the same layout is written with hi = value, lo = 0.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.hpp"
@@ -25,6 +36,9 @@
 namespace fipa_b200 {
 
 namespace {
+
+constexpr float kL2E = 1.4426950408889634f;
+constexpr float kMaskedBias = -1.0e30f;
 
 template <typename T>
 __device__ __forceinline__ void store_pair(T* dst, float a, float b);
@@ -37,17 +51,26 @@ __device__ __forceinline__ void store_pair<float>(float* dst, float a, float b) 
     *reinterpret_cast<float2*>(dst) = make_float2(a, b);
 }
 
+template <typename T>
+__device__ __forceinline__ float hi_part(float x) {
+    return sizeof(T) == 4 ? x : __bfloat162float(__float2bfloat16_rn(x));
+}
+template <typename T>
+__device__ __forceinline__ float lo_part(float x) {
+    return sizeof(T) == 4 ? 0.f : x - __bfloat162float(__float2bfloat16_rn(x));
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     extern __shared__ float sm[];
     const int H = d.heads, c = d.c, Nq = d.n_query, Nv = d.n_value, rdz = d.rank * d.d_z;
-    float* s_proj = sm;                      // n_proj
-    float* s_z1 = s_proj + d.n_proj;         // rdz
-    float* s_z2 = s_z1 + rdz;                // rdz
-    float* s_gq = s_z2 + rdz;                // H*Nq*3
-    float* s_gk = s_gq + H * Nq * 3;         // H*Nq*3
-    float* s_gv = s_gk + H * Nq * 3;         // H*Nv*3
-    float* s_kn = s_gv + H * Nv * 3;         // H
+    float* s_proj = sm;                  // n_proj
+    float* s_z1 = s_proj + d.n_proj;     // rdz
+    float* s_z2 = s_z1 + rdz;            // rdz
+    float* s_rq = s_z2 + rdz;            // H*Nq*3   R_i q_p
+    float* s_rk = s_rq + H * Nq * 3;     // H*Nq*3   R_j k_p
+    float* s_rv = s_rk + H * Nq * 3;     // H*Nv*3   R_j v_p
+    float* s_hd = s_rv + H * Nv * 3;     // H*8: Qbar(3), W(3), |Tk|^2, pad
 
     const int64_t row = blockIdx.x;  // b*L + i
     const int b = static_cast<int>(row / a.L);
@@ -74,35 +97,41 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     for (int e = tid; e < npts; e += blockDim.x) {
         const float* src;
         float* dst;
-        bool add_t = true;
-        int idx;
         if (e < H * Nq) {
-            idx = e;
-            src = s_proj + off_qp + idx * 3;
-            dst = s_gq + idx * 3;
+            src = s_proj + off_qp + e * 3;
+            dst = s_rq + e * 3;
         } else if (e < 2 * H * Nq) {
-            idx = e - H * Nq;
-            src = s_proj + off_kp + idx * 3;
-            dst = s_gk + idx * 3;
+            src = s_proj + off_kp + (e - H * Nq) * 3;
+            dst = s_rk + (e - H * Nq) * 3;
         } else {
-            idx = e - 2 * H * Nq;
-            src = s_proj + off_vp + idx * 3;
-            dst = s_gv + idx * 3;
-            add_t = false;
+            src = s_proj + off_vp + (e - 2 * H * Nq) * 3;
+            dst = s_rv + (e - 2 * H * Nq) * 3;
         }
         const float x = src[0], y = src[1], z = src[2];
-        dst[0] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z)) + (add_t ? t[0] : 0.f);
-        dst[1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z)) + (add_t ? t[1] : 0.f);
-        dst[2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z)) + (add_t ? t[2] : 0.f);
+        dst[0] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z));
+        dst[1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z));
+        dst[2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z));
     }
     __syncthreads();
     for (int h = tid; h < H; h += blockDim.x) {
-        float acc = 0.f;
-        for (int e = 0; e < Nq * 3; ++e) {
-            const float g = s_gk[h * Nq * 3 + e];
-            acc = fmaf(g, g, acc);
+        float qb[3] = {0.f, 0.f, 0.f}, w[3] = {0.f, 0.f, 0.f}, kn = 0.f;
+        for (int p = 0; p < Nq; ++p) {
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                qb[x] += s_rq[(h * Nq + p) * 3 + x];
+                const float tk = s_rk[(h * Nq + p) * 3 + x] + t[x];
+                w[x] += tk;
+                kn = fmaf(tk, tk, kn);
+            }
         }
-        s_kn[h] = acc;
+        float* hd = s_hd + h * 8;
+        hd[0] = qb[0];
+        hd[1] = qb[1];
+        hd[2] = qb[2];
+        hd[3] = w[0];
+        hd[4] = w[1];
+        hd[5] = w[2];
+        hd[6] = kn;
     }
     __syncthreads();
 
@@ -110,12 +139,16 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     OutT* qh = static_cast<OutT*>(a.qhat);
     OutT* kh = static_cast<OutT*>(a.khat);
     OutT* vh = static_cast<OutT*>(a.vhat);
-    const int qk_geo = c + 3 * Nq, qk_used = d.dqk_used;
+    const int g0 = c + 3 * Nq;        // start of the 20 translation/bias columns
+    const int zq = g0 + 20;           // start of the pair-factor columns
+    const int qk_used = d.dqk_used;
     const int v_pair = c + rdz, v_pts = v_pair + 3 * Nv, v_used = d.dv_used;
 
     for (int h = 0; h < H; ++h) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
         const float g = a.head_g[h];
+        const float* hd = s_hd + h * 8;
+        const float cb = valid ? kL2E * (-0.5f * g * hd[6]) : kMaskedBias;
         OutT* q = qh + hrow * d.dqk_pad;
         OutT* k = kh + hrow * d.dqk_pad;
         OutT* v = vh + hrow * d.dv_pad;
@@ -125,14 +158,29 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
             for (int u = 0; u < 2; ++u) {
                 const int cc = col + u;
                 if (cc < c) {
-                    qv[u] = s_proj[off_q + h * c + cc];
+                    qv[u] = kL2E * s_proj[off_q + h * c + cc];
                     kv[u] = a.k_scale * s_proj[off_k + h * c + cc];
-                } else if (cc < qk_geo) {
-                    qv[u] = s_gq[h * Nq * 3 + (cc - c)];
-                    kv[u] = g * s_gk[h * Nq * 3 + (cc - c)];
+                } else if (cc < g0) {
+                    qv[u] = kL2E * s_rq[h * Nq * 3 + (cc - c)];
+                    kv[u] = g * s_rk[h * Nq * 3 + (cc - c)];
+                } else if (cc < zq) {
+                    const int e = cc - g0;     // 0..19
+                    const int x = e % 3;
+                    if (e < 9) {               // <Qbar_i, g t_j>:  [Qh Qh Ql] . [th tl th]
+                        const float qq = kL2E * hd[x], tt = g * t[x];
+                        qv[u] = e < 6 ? hi_part<OutT>(qq) : lo_part<OutT>(qq);
+                        kv[u] = (e >= 3 && e < 6) ? lo_part<OutT>(tt) : hi_part<OutT>(tt);
+                    } else if (e < 18) {       // <t_i, g W_j>:     [th tl th] . [Wh Wh Wl]
+                        const float tq = kL2E * t[x], ww = g * hd[3 + x];
+                        qv[u] = (e >= 12 && e < 15) ? lo_part<OutT>(tq) : hi_part<OutT>(tq);
+                        kv[u] = e < 15 ? hi_part<OutT>(ww) : lo_part<OutT>(ww);
+                    } else {                   // folded column bias: [1 1] . [cb_hi cb_lo]
+                        qv[u] = 1.0f;
+                        kv[u] = e == 18 ? hi_part<OutT>(cb) : (valid ? lo_part<OutT>(cb) : 0.f);
+                    }
                 } else if (cc < qk_used) {
-                    const int e = cc - qk_geo;
-                    qv[u] = s_z1[e];
+                    const int e = cc - zq;
+                    qv[u] = kL2E * s_z1[e];
                     kv[u] = a.wl_bias[h * d.d_z + (e % d.d_z)] * s_z2[e];
                 } else {
                     qv[u] = 0.f;
@@ -150,16 +198,14 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
                 float x;
                 if (cc < c) {
                     x = s_proj[off_v + h * c + cc];
-                } else if (cc < v_pair + 0 && cc >= c) {
+                } else if (cc < v_pair) {
                     x = s_z2[cc - c];
                 } else if (cc < v_pts) {
-                    x = s_gv[h * Nv * 3 + (cc - v_pair)];
+                    x = s_rv[h * Nv * 3 + (cc - v_pair)];
                 } else if (cc < v_pts + 3) {
-                    const float tt = t[cc - v_pts];
-                    x = sizeof(OutT) == 4 ? tt : __bfloat162float(__float2bfloat16_rn(tt));
+                    x = hi_part<OutT>(t[cc - v_pts]);
                 } else if (cc < v_used) {
-                    const float tt = t[cc - v_pts - 3];
-                    x = sizeof(OutT) == 4 ? 0.f : tt - __bfloat162float(__float2bfloat16_rn(tt));
+                    x = lo_part<OutT>(t[cc - v_pts - 3]);
                 } else {
                     x = 0.f;
                 }
@@ -167,7 +213,7 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
             }
             store_pair<OutT>(v + col, vv[0], vv[1]);
         }
-        if (tid == 0) a.colbias[hrow] = valid ? -0.5f * g * s_kn[h] : -INFINITY;
+        if (tid == 0) a.colbias[hrow] = valid ? -0.5f * g * hd[6] : -INFINITY;
     }
 }
 
@@ -186,6 +232,16 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
     for (int64_t e = n4 * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
          e += int64_t(gridDim.x) * blockDim.x) {
         out[e] = __float2bfloat16_rn(in[e]);
+    }
+}
+
+__global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                      int64_t rows, int cols, int ld_out) {
+    const int64_t n = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols;
+        out[r * ld_out + (e - r * cols)] = __float2bfloat16_rn(in[e]);
     }
 }
 
@@ -248,7 +304,7 @@ __global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* 
 void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
     const size_t smem =
-        sizeof(float) * (d.n_proj + 2 * rdz + d.heads * (d.n_query * 6 + d.n_value * 3) + d.heads);
+        sizeof(float) * (d.n_proj + 2 * rdz + d.heads * (d.n_query * 6 + d.n_value * 3) + 8 * d.heads);
     const dim3 grid(static_cast<unsigned>(int64_t(a.B) * a.L));
     if (a.out_f32) {
         if (smem > 48 * 1024)
@@ -267,6 +323,15 @@ void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStre
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
     f32_to_bf16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, n);
+}
+
+void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
+                           cudaStream_t stream) {
+    if (cols == ld_out) return launch_f32_to_bf16(in, out, rows * cols, stream);
+    const int64_t n = rows * cols;
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    f32_to_bf16_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, rows, cols, ld_out);
 }
 
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,

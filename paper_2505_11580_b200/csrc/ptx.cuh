@@ -15,6 +15,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
+
+// One lane of the (converged) warp returns true.  Issue tcgen05.mma / commit under this so the
+// descriptor arithmetic around it stays warp-uniform (uniform registers, no per-MMA R2UR).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t"
+        "@px mov.s32 %0, 1;\n\t}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
+}
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // ----------------------------------------------------------------- mbarrier

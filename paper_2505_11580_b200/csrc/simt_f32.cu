@@ -20,7 +20,7 @@ constexpr int TM = 64, TN = 64, TK = 16;
 // C[M,N] = A[M,K] (row-major) . B[K,N] (row-major) (+bias) with masked rows zeroed.
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A,
                                                        const float* __restrict__ B,
-                                                       float* __restrict__ C, int M, int N, int K,
+                                                       float* __restrict__ C, int M, int N, int K, int lda,
                                                        const float* __restrict__ bias,
                                                        const uint8_t* __restrict__ row_mask) {
     __shared__ float sA[TK][TM + 4];
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
         for (int e = threadIdx.x; e < TM * TK; e += 256) {
             const int r = e / TK, kk = e % TK;
             const int gm = m0 + r, gk = k0 + kk;
-            sA[kk][r] = (gm < M && gk < K) ? A[int64_t(gm) * K + gk] : 0.f;
+            sA[kk][r] = (gm < M && gk < K) ? A[int64_t(gm) * lda + gk] : 0.f;
         }
         for (int e = threadIdx.x; e < TN * TK; e += 256) {
             const int kk = e / TN, cidx = e % TN;
@@ -95,10 +95,9 @@ __global__ void __launch_bounds__(kWarps * 32) attn_fwd_f32_kernel(AttnF32Args a
     float m = -INFINITY, l = 0.f;
     const float* kb = a.khat + static_cast<int64_t>(bh) * p.L * p.dqk_pad;
     const float* vb = a.vhat + static_cast<int64_t>(bh) * p.L * p.dv_pad;
-    const float* cb = a.colbias + static_cast<int64_t>(bh) * p.L;
+    // S = q_hat . k_hat is already in log2 units and carries the folded column bias
+    // (pack.cu); masked keys hold -1e30 and vanish once any valid key is seen.
     for (int j = 0; j < p.L; ++j) {
-        const float bias = cb[j];
-        if (bias == -INFINITY) continue;  // masked key: exact zero weight
         const float* kr = kb + static_cast<int64_t>(j) * p.dqk_pad;
         float dot = 0.f;
 #pragma unroll
@@ -108,17 +107,17 @@ __global__ void __launch_bounds__(kWarps * 32) attn_fwd_f32_kernel(AttnF32Args a
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-        const float s = dot + bias;
+        const float s = dot;
         float w;
         if (s > m) {
-            const float scale = expf(m - s);  // 0 when m == -inf
+            const float scale = exp2f(m - s);  // 0 when m == -inf
             l *= scale;
 #pragma unroll
             for (int e = 0; e < kMaxChunks; ++e) o[e] *= scale;
             m = s;
             w = 1.f;
         } else {
-            w = expf(s - m);
+            w = exp2f(s - m);
         }
         l += w;
         const float* vr = vb + static_cast<int64_t>(j) * p.dv_pad;
@@ -129,7 +128,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_fwd_f32_kernel(AttnF32Args a
         }
     }
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    if (lane == 0) a.lse[qrow] = l > 0.f ? m + logf(l) : -INFINITY;
+    if (lane == 0) a.lse[qrow] = l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
     float* so = s_o + warp * p.dv_pad;
 #pragma unroll
     for (int e = 0; e < kMaxChunks; ++e) {
@@ -168,17 +167,17 @@ __global__ void __launch_bounds__(kWarps * 32) attn_fwd_f32_kernel(AttnF32Args a
 
 }  // namespace
 
-void launch_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K,
+void launch_gemm_f32(const float* A, int lda, const float* B, float* C, int M, int N, int K,
                      const float* bias, const uint8_t* row_mask, cudaStream_t stream) {
     if (M <= 0 || N <= 0) return;
     dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
-    gemm_f32_kernel<<<grid, 256, 0, stream>>>(A, B, C, M, N, K, bias, row_mask);
+    gemm_f32_kernel<<<grid, 256, 0, stream>>>(A, B, C, M, N, K, lda, bias, row_mask);
 }
 
 void launch_attn_fwd_f32(const LayerDims& d, const AttnF32Args& a, cudaStream_t stream) {
     if (d.dqk_pad > kMaxChunks * 32 || d.dv_pad > kMaxChunks * 32)
         throw std::invalid_argument("f32 attention: lifted width exceeds 768");
-    F32Params p{a.L, d.heads, d.dqk_pad, d.dv_pad, d.c, d.d_z, d.rank, d.n_value, d.seg, d.feat};
+    F32Params p{a.L, d.heads, d.dqk_pad, d.dv_pad, d.c, d.d_z, d.rank, d.n_value, d.seg, d.feat_ld};
     const size_t smem = sizeof(float) * kWarps * d.dv_pad;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(attn_fwd_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -109,27 +109,30 @@ def ws_view(ws, offset, count, dtype):
     return raw.view(torch.float32).cpu().numpy().astype(np.float64)
 
 
-def expected_packed(shape, w, batch, b):
-    """Oracle q_hat/k_hat/v_hat/colbias of sample b in the B200 layout."""
+def expected_lifted(shape, w, batch, b):
+    """Oracle view of sample b in the B200 layout.
+
+    Returns (logits, v_parts, cb):
+      logits [H, L, L]  the reference attention logits <q_hat_i, k_hat_j> (natural units,
+                        masked keys excluded later by the caller),
+      v_parts [H, L, c + r d_z + 3Nv + 3]  [v | z2 | R_j v_p | t_j (recentred)],
+      cb [H, L]  -g/2 sum_p |T_j k_p|^2 with -inf for masked keys.
+    """
     cfg = oracle_cfg(shape)
     s, z1, z2, rot, trans = (batch[k][b] for k in ("s", "z1", "z2", "rot", "trans"))
-    mask = batch["mask"][b]
-    valid = mask.astype(bool)
+    valid = batch["mask"][b].astype(bool)
     trans_c = trans - (trans[valid].mean(0) if valid.any() else 0.0)
+    qh, kh, _ = fo.lift_qkv(s, z1, z2, rot, trans, cfg, w)
+    logits = np.einsum("hid,hjd->hij", qh, kh)
     q, k, v, qp, kp, vp = fo.project_inputs(s, cfg, w)
     H, L = cfg.heads, s.shape[0]
     gamma = fo.softplus(w["gamma_raw"])
-    g = (gamma * w["w_l"] * w["w_c"])[:, None, None]
-    gq = fo.apply(rot[None, :, None], trans_c[None, :, None], qp).reshape(H, L, -1)
+    g = (gamma * w["w_l"] * w["w_c"])[:, None]
     gk = fo.apply(rot[None, :, None], trans_c[None, :, None], kp)
     rv = np.einsum("lab,hlpb->hlpa", rot, vp).reshape(H, L, -1)
-    b1 = np.broadcast_to(z1.reshape(1, L, -1), (H, L, cfg.rank * cfg.d_z))
-    b2 = ((w["w_l"] * w["w_bias"])[:, None, None, :] * z2[None]).reshape(H, L, -1)
-    qh = np.concatenate([q, gq, b1], -1)
-    kh = np.concatenate([w["w_l"] / math.sqrt(cfg.c) * k, g * gk.reshape(H, L, -1), b2], -1)
     z2f = np.broadcast_to(z2.reshape(1, L, -1), (H, L, cfg.rank * cfg.d_z))
     tt = np.broadcast_to(trans_c[None], (H, L, 3))
-    vh = np.concatenate([v, z2f, rv, tt], -1)
-    cb = -0.5 * g[:, :, 0] * (gk ** 2).sum((-1, -2))
+    v_parts = np.concatenate([v, z2f, rv, tt], -1)
+    cb = -0.5 * g * (gk ** 2).sum((-1, -2))
     cb = np.where(valid[None], cb, -np.inf)
-    return qh, kh, vh, cb
+    return logits, v_parts, cb

@@ -8,7 +8,7 @@ proj/tests/test_support.hpp:31-34) <= 2e-2 for bf16 inputs with fp32 accumulatio
 import numpy as np
 import pytest
 
-from helpers import (BF16_TOL, F32_TOL, MAIN, TINY, expected_packed, gpu_forward_device,
+from helpers import (BF16_TOL, F32_TOL, MAIN, TINY, expected_lifted, gpu_forward_device,
                      make_batch, move_frames, oracle_cfg, oracle_forward, oracle_weights_for,
                      random_rigid, rel_dev, ws_view)
 from oracle import fipa_oracle as fo
@@ -45,17 +45,22 @@ def test_stage_by_stage_main_shape(fipa, precision):
     kh = ws_view(ws, off[4], B * H * L * dqk_pad, el).reshape(B, H, L, dqk_pad)
     vh = ws_view(ws, off[5], B * H * L * dv_pad, el).reshape(B, H, L, dv_pad)
     cb = ws_view(ws, off[6], B * H * L, "f32").reshape(B, H, L)
-    pack_tol = 8e-3 if bf else 1e-5
+    L2E = 1.0 / np.log(2.0)
     for b in range(B):
-        eq, ek, ev, ecb = expected_packed(MAIN, w, batch, b)
-        wq = eq.shape[-1]
-        assert rel_dev(eq, qh[b, :, :, :wq]) < pack_tol
-        assert rel_dev(ek, kh[b, :, :, :wq]) < pack_tol
-        assert np.all(qh[b, :, :, wq:] == 0) and np.all(kh[b, :, :, wq:] == 0)
+        elog, ev, ecb = expected_lifted(MAIN, w, batch, b)
+        valid = batch["mask"][b].astype(bool)
+        # q_hat . k_hat must equal log2(e) * (reference logit) up to a per-row constant
+        # (the dropped |T_i q_p|^2 term), and masked keys must sit at <= -1e29.
+        s_gpu = np.einsum("hid,hjd->hij", qh[b], kh[b])
+        assert np.all(s_gpu[:, :, ~valid] < -1e29)
+        d_gpu = s_gpu[:, :, valid] - s_gpu[:, :, valid][:, :, :1]
+        d_ref = L2E * (elog[:, :, valid] - elog[:, :, valid][:, :, :1])
+        assert rel_dev(d_ref, d_gpu) < (4e-3 if bf else 1e-6)
         nv = ev.shape[-1] - 3
-        assert rel_dev(ev[..., :nv], vh[b, :, :, :nv]) < pack_tol
+        assert rel_dev(ev[..., :nv], vh[b, :, :, :nv]) < (8e-3 if bf else 1e-6)
         t_sum = vh[b, :, :, nv:nv + 3] + vh[b, :, :, nv + 3:nv + 6]
         assert rel_dev(ev[..., nv:], t_sum) < (1e-5 if bf else 1e-6)
+        assert np.all(vh[b, :, :, nv + 6:] == 0)
         fin = np.isfinite(ecb)
         assert np.array_equal(fin, np.isfinite(cb[b]))
         assert rel_dev(ecb[fin], cb[b][fin]) < 1e-5

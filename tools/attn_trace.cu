@@ -1,0 +1,73 @@
+// Pipeline trace of the tcgen05 attention kernel: per-tile event timestamps (SM clock) of CTA
+// (0,0) at the north-star shape, B=8 L=1024.  Build with -DFIPA_ATTN_TRACE (see Makefile rule
+// in tools/README or the gpurun command in profiles/).
+#define FIPA_ATTN_TRACE 1
+#include "../paper_2505_11580_b200/csrc/attn_fwd_tc.cu"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+using namespace fipa_b200;
+
+int main(int argc, char** argv) {
+    const int B = argc > 1 ? atoi(argv[1]) : 8;
+    const int L = argc > 2 ? atoi(argv[2]) : 1024;
+    LayerDims d{};
+    d.d_in = 256; d.d_z = 128; d.heads = 8; d.c = 128; d.n_query = 8; d.n_value = 12; d.rank = 2;
+    d.dqk_used = 128 + 24 + 20 + 256; d.dqk_pad = 432;
+    d.dv_used = 128 + 256 + 36 + 6; d.dv_pad = 432; d.dv_tc = 416; d.dv_simt = 10;
+    d.seg = 304; d.feat = 8 * 304; d.feat_ld = d.feat; d.din_ld = 256;
+    const size_t BH = size_t(B) * d.heads, BL = size_t(B) * L;
+    std::vector<__nv_bfloat16> hq(BH * L * d.dqk_pad), hv(BH * L * d.dv_pad);
+    srand(1);
+    for (auto& x : hq) x = __float2bfloat16((rand() / float(RAND_MAX) - 0.5f) * 0.2f);
+    for (auto& x : hv) x = __float2bfloat16((rand() / float(RAND_MAX) - 0.5f));
+    __nv_bfloat16 *q, *k, *v, *feat;
+    float *z1, *rot, *trans, *lse;
+    cudaMalloc(&q, hq.size() * 2);
+    cudaMalloc(&k, hq.size() * 2);
+    cudaMalloc(&v, hv.size() * 2);
+    cudaMalloc(&feat, BL * d.feat * 2);
+    cudaMalloc(&z1, BL * 256 * 4);
+    cudaMalloc(&rot, BL * 9 * 4);
+    cudaMalloc(&trans, BL * 3 * 4);
+    cudaMalloc(&lse, BH * L * 4);
+    cudaMemcpy(q, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(k, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(v, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemset(z1, 0, BL * 256 * 4);
+    cudaMemset(rot, 0, BL * 9 * 4);
+    cudaMemset(trans, 0, BL * 3 * 4);
+    AttnArgs a{q, k, v, nullptr, z1, rot, trans, feat, lse, B, L};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int it = 0; it < 3; ++it) launch_attn_fwd_tc(d, a, 0);
+    cudaEventRecord(e0);
+    const int reps = 10;
+    for (int it = 0; it < reps; ++it) launch_attn_fwd_tc(d, a, 0);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    const double flops = 2.0 * BH * L * double(L) * (424 + 420);
+    printf("status %s  B=%d L=%d  %.3f ms  %.1f TFLOP/s\n", cudaGetErrorString(err), B, L, ms,
+           flops / ms / 1e9);
+    std::vector<long long> t(16 * 256);
+    cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * sizeof(long long));
+    const long long t0 = t[2 * 256 + 0];
+    const char* names[9] = {"Kload", "Vload", "QKiss", "PViss", "Sfull", "PVdone", "Pfull", "SIMTend", "ofull/end"};
+    const int nt = (L + 63) / 64;
+    printf("tile ");
+    for (int e = 0; e < 8; ++e) printf("%9s", names[e]);
+    printf("\n");
+    for (int j = 0; j < nt && j < 40; ++j) {
+        printf("%4d ", j);
+        for (int e = 0; e < 8; ++e) printf("%9lld", t[e * 256 + j] ? t[e * 256 + j] - t0 : -1);
+        printf("\n");
+    }
+    printf("o_full %lld  end %lld\n", t[8 * 256] - t0, t[8 * 256 + 1] - t0);
+    return 0;
+}
