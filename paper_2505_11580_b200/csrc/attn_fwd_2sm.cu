@@ -1,0 +1,557 @@
+// FlashIPA attention forward on a CTA pair (tcgen05 cta_group::2, M = 256), fused epilogue.
+//
+// Replaces the reference's tiled online-softmax kernel
+//   flash_attention -> flash_block   proj/src/attention_kernel.cpp:112-188, 213-243
+// and the per-row epilogue that follows it
+//   split / pair contraction / apply_inverse / norms   proj/src/flash_ipa.cpp:171-210
+//
+// A cluster of two CTAs owns 256 consecutive query rows of one (sample, head); each CTA keeps
+// its 128 rows of Q_hat resident in shared memory and its 128 rows of O in its own TMEM.  The
+// even CTA issues every MMA for the pair:
+//   S_j = Q_hat . K_hat_j^T   M=256 N=64  (each CTA stages 32 of the 64 keys)  -> TMEM [448,512)
+//   P_j = exp2(S_j - m)       softmax warps of both CTAs, bf16 P -> shared memory (K-major)
+//   O  += P_j . V_hat_j       M=256 N=256+176 (each CTA stages half of every N block)
+//                                                                              -> TMEM [0,432)
+// Lifted rows are in log2 units with the column bias folded in (pack.cu) and stored with a
+// 64-element (128-byte) row stride, so Q and each K tile arrive as ONE 4-D TMA box of 128-byte
+// column blocks (the TMA engine costs ~100 cycles per box, so box count matters more than
+// bytes).  K (whole tiles) and V (32-key slices) stream through two-stage rings fed by 2-SM TMA
+// loads whose bytes are counted on the even CTA's barriers; consumption is signalled back to
+// both CTAs by multicast tcgen05.commit.
+// The tensor pipe runs QK_{j+1} while the softmax warps turn S_j into P_j, then PV_j.  The
+// running max moves only when it grows by more than 2^8, so the O rescale is rare.
+// Masked keys carry a -1e30 bias and vanish once any valid key is seen; keys >= L are forced
+// to -inf; rows with no valid key are zeroed by the output projection (flash_ipa.cpp:213-216).
+//
+// Warps (352 threads per CTA): w0 Q/K producer, w1 TMEM alloc (+ MMA issue on the even CTA),
+// w2..w9 softmax (warp w owns TMEM lanes 32*(w%4).. and key half (w-2)/4, thread = query row;
+// all eight also run the epilogue), w10 V producer.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+#include "tma_host.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+constexpr int BM = 128;      // query rows per CTA (256 per pair)
+constexpr int BN = 64;       // keys per tile
+constexpr int kThreads = 352;
+constexpr int kKStages = 2;  // K ring: whole tiles (32 keys per CTA x all 128-byte blocks)
+constexpr int kVStages = 2;  // V ring: 32-key slices x half the value width
+constexpr int kVKeys = 32;
+constexpr int kVBoxBytes = kVKeys * 128;  // one 64-wide MN atom column block of 32 keys
+constexpr uint32_t kSCol = 448;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct Attn2Params {
+    int L, H, dqk_mma, dv_mma, n_qkb, n1, n2, nb1, nb2;
+    int c, d_z, rank, n_value, seg, feat_ld;
+    const float* z1;
+    const float* rot;
+    const float* trans;
+    __nv_bfloat16* feat_out;
+    float* lse;
+};
+
+struct Bars {
+    uint64_t q_full;
+    uint64_t k_full[kKStages], k_empty[kKStages];
+    uint64_t v_full[kVStages], v_empty[kVStages];
+    uint64_t s_full, s_free, p_full, pv_done, o_full;
+    uint32_t tmem_slot;
+};
+
+struct Layout {
+    int q, p, k, v, xch, bars, total, kstage, vstage;
+};
+__host__ __device__ inline Layout smem_layout(int n_qkb, int nb1, int nb2) {
+    Layout l{};
+    l.kstage = n_qkb * 32 * 128;
+    l.vstage = (nb1 + nb2) * kVBoxBytes;
+    l.q = 0;
+    l.p = n_qkb * BM * 128;
+    l.k = l.p + BM * 128;
+    l.v = l.k + kKStages * l.kstage;
+    l.xch = l.v + kVStages * l.vstage;
+    l.bars = l.xch + 2 * 2 * BM * 4;
+    l.total = l.bars + static_cast<int>(sizeof(Bars));
+    return l;
+}
+__host__ __device__ constexpr int epilogue_smem(int seg) {
+    return BM * ((seg + 7) / 8 * 8 + 8) * 2 + BM * 49 * 4;
+}
+
+// Optional per-event timestamps of clusters (0,0) for pipeline analysis (tools/attn_trace2.cu).
+#ifdef FIPA_ATTN_TRACE
+__device__ long long g_attn_trace[2 * 16 * 16 * 128];  // [cta][warp][event][index]
+#define FIPA_TRACE(ev, j)                                                                          \
+    do {                                                                                           \
+        if (blockIdx.x < 2 && blockIdx.y == 0 && (j) < 128)                                         \
+            g_attn_trace[((blockIdx.x * 16 + ptx::warp_id()) * 16 + (ev)) * 128 + (j)] = clock64(); \
+    } while (0)
+#else
+#define FIPA_TRACE(ev, j) \
+    do {                  \
+    } while (0)
+#endif
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Fused output epilogue (proj/src/flash_ipa.cpp:171-210), one thread per query row reading the
+// row's O accumulator straight from TMEM; the two warps of a lane quadrant split the columns:
+//   feat block = [ sum_rho z1[i,rho,:] * O_pair[rho,:] | O_scalar | R_i^T(g_p - t_i) | |.| ]
+// with g_p = agg(R_j v_p) + agg(t_j hi) + agg(t_j lo).  The z1 row chunks are fetched one chunk
+// ahead of their use (the TMEM loads are ordered asm, so the prefetch is explicit).  Rows are
+// assembled as bf16 in shared memory, then the 128 x seg block is written with coalesced
+// 16-byte stores by all 256 epilogue threads.
+__device__ __forceinline__ void load_z16(const float* zp, bool full, int rem, float* z) {
+    if (full) {
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(zp) + v4);
+            z[4 * v4] = f.x;
+            z[4 * v4 + 1] = f.y;
+            z[4 * v4 + 2] = f.z;
+            z[4 * v4 + 3] = f.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) z[e] = e < rem ? __ldg(zp + e) : 0.f;
+    }
+}
+
+__device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl, float inv_l,
+                                               int row, int q0, int bh, uint8_t* smem, int half) {
+    const int seg = p.seg, sst = (seg + 7) / 8 * 8 + 8;
+    __nv_bfloat16* fst = reinterpret_cast<__nv_bfloat16*>(smem);
+    __nv_bfloat16* frow = fst + row * sst;
+    float* pts = reinterpret_cast<float*>(smem + BM * sst * 2) + row * 49;
+    const int H = p.H, b = bh / H, h = bh % H;
+    const int q = q0 + row;
+    const bool ok = q < p.L;
+    const int64_t grow = static_cast<int64_t>(b) * p.L + (ok ? q : 0);
+    const int c = p.c, dz = p.d_z, Nv = p.n_value;
+    const int base = c + p.rank * dz, npt = 3 * Nv + 6;
+
+    // scalar aggregate -> [d_z, d_z + c): 16-column chunks split between the halves
+    const int nsc = (c + 15) / 16;
+    for (int ch = half ? (nsc + 1) / 2 : 0; ch < (half ? nsc : (nsc + 1) / 2); ++ch) {
+        const int c0 = 16 * ch;
+        uint32_t o[16];
+        ptx::tmem_ld16(tl + c0, o);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (c0 + e < c) frow[dz + c0 + e] = __float2bfloat16_rn(__uint_as_float(o[e]) * inv_l);
+    }
+    // pair contraction -> [0, d_z), z1 chunks prefetched one (chunk, rho) step ahead
+    const float* z1r = p.z1 + grow * (p.rank * dz);
+    const bool vec = (reinterpret_cast<uintptr_t>(z1r) & 15) == 0 && dz % 16 == 0;
+    const int npc = (dz + 15) / 16;
+    const int pc0 = half ? (npc + 1) / 2 : 0, pc1 = half ? npc : (npc + 1) / 2;
+    const int nsteps = (pc1 - pc0) * p.rank;
+    float zc[16], zn[16];
+    if (nsteps > 0) load_z16(z1r + 16 * pc0, vec, dz - 16 * pc0, zc);
+    float acc[16];
+    for (int st = 0; st < nsteps; ++st) {
+        const int ch = pc0 + st / p.rank, rho = st % p.rank;
+        const int d0 = 16 * ch;
+        if (st + 1 < nsteps) {
+            const int ch2 = pc0 + (st + 1) / p.rank, rho2 = (st + 1) % p.rank;
+            load_z16(z1r + rho2 * dz + 16 * ch2, vec, dz - 16 * ch2, zn);
+        }
+        if (rho == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+        }
+        uint32_t o[16];
+        ptx::tmem_ld16(tl + c + rho * dz + d0, o);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = fmaf(zc[e], __uint_as_float(o[e]), acc[e]);
+        if (rho == p.rank - 1) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if (d0 + e < dz) frow[d0 + e] = __float2bfloat16_rn(acc[e] * inv_l);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) zc[e] = zn[e];
+    }
+    // points (half 0): point block [base, base + npt) of O_hat -> per-row scratch -> local frame
+    if (half == 0) {
+        for (int c0 = 0; c0 < npt; c0 += 16) {
+            uint32_t o[16];
+            ptx::tmem_ld16(tl + base + c0, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if (c0 + e < npt) pts[c0 + e] = __uint_as_float(o[e]) * inv_l;
+        }
+        if (ok) {
+            const float* R = p.rot + grow * 9;
+            const float* t = p.trans + grow * 3;
+            float Rm[9], tg[3];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Rm[k] = __ldg(R + k);
+#pragma unroll
+            for (int y = 0; y < 3; ++y) tg[y] = pts[3 * Nv + y] + pts[3 * Nv + 3 + y] - __ldg(t + y);
+            __nv_bfloat16* fp = frow + dz + c;
+            for (int pt = 0; pt < Nv; ++pt) {
+                const float gx = pts[3 * pt] + tg[0], gy = pts[3 * pt + 1] + tg[1], gz = pts[3 * pt + 2] + tg[2];
+                // apply_inverse: R^T g   (proj/src/geometry.cpp:70-76)
+                const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
+                const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));
+                const float lz = fmaf(Rm[2], gx, fmaf(Rm[5], gy, Rm[8] * gz));
+                fp[3 * pt] = __float2bfloat16_rn(lx);
+                fp[3 * pt + 1] = __float2bfloat16_rn(ly);
+                fp[3 * pt + 2] = __float2bfloat16_rn(lz);
+                fp[3 * Nv + pt] = __float2bfloat16_rn(sqrtf(lx * lx + ly * ly + lz * lz));
+            }
+        }
+    }
+    named_bar_sync(1, 256);
+    const int tid = threadIdx.x - 64;  // 0..255 over warps 2..9
+    const int rows = min(BM, p.L - q0);
+    if (rows <= 0) return;
+    __nv_bfloat16* gout = p.feat_out + (static_cast<int64_t>(b) * p.L + q0) * p.feat_ld + h * seg;
+    if (seg % 8 == 0 && p.feat_ld % 8 == 0 && ((h * seg) % 8) == 0) {
+        const int per_row = seg / 8;
+        for (int e = tid; e < rows * per_row; e += 256) {
+            const int r = e / per_row, k = e - r * per_row;
+            *reinterpret_cast<uint4*>(gout + static_cast<int64_t>(r) * p.feat_ld + 8 * k) =
+                *reinterpret_cast<const uint4*>(fst + r * sst + 8 * k);
+        }
+    } else {
+        for (int e = tid; e < rows * seg; e += 256) {
+            const int r = e / seg, k = e - r * seg;
+            gout[static_cast<int64_t>(r) * p.feat_ld + k] = fst[r * sst + k];
+        }
+    }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap mapQ,
+                        const __grid_constant__ CUtensorMap mapK,
+                        const __grid_constant__ CUtensorMap mapV, Attn2Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const Layout lay = smem_layout(p.n_qkb, p.nb1, p.nb2);
+    uint8_t* sQ = smem + lay.q;
+    uint8_t* sP = smem + lay.p;
+    uint8_t* sK = smem + lay.k;
+    uint8_t* sV = smem + lay.v;
+    Bars* bars = reinterpret_cast<Bars*>(smem + lay.bars);
+
+    const int warp = ptx::warp_id();
+    const int lane = ptx::lane_id();
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int bh = blockIdx.y;
+    const int q0 = blockIdx.x * BM;
+    const int ntiles = (p.L + BN - 1) / BN;
+    const int qk_steps = p.dqk_mma / 16;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&mapQ);
+        ptx::tma_prefetch(&mapK);
+        ptx::tma_prefetch(&mapV);
+        ptx::mbar_init(&bars->q_full, 1);
+        for (int s = 0; s < kKStages; ++s) {
+            ptx::mbar_init(&bars->k_full[s], 1);
+            ptx::mbar_init(&bars->k_empty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            ptx::mbar_init(&bars->v_full[s], 1);
+            ptx::mbar_init(&bars->v_empty[s], 1);
+        }
+        ptx::mbar_init(&bars->s_full, 1);
+        ptx::mbar_init(&bars->s_free, 16);
+        ptx::mbar_init(&bars->p_full, 16);
+        ptx::mbar_init(&bars->pv_done, 1);
+        ptx::mbar_init(&bars->o_full, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm(&bars->tmem_slot, 512);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // barrier inits + TMEM address visible to the pair
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_slot, 0);
+
+    if (warp == 0) {
+        // --------------------------------------------------------- Q / K producer
+        if (lane == 0) {
+            if (leader) ptx::mbar_expect_tx(&bars->q_full, 2 * p.n_qkb * BM * 128);
+            ptx::tma_load_4d_2sm(sQ, &mapQ, &bars->q_full, 0, q0, 0, bh);
+            for (int j = 0; j < ntiles; ++j) {
+                const int s = j % kKStages;
+                if (j >= kKStages) ptx::mbar_wait(&bars->k_empty[s], ((j / kKStages) - 1) & 1);
+                FIPA_TRACE(5, j);
+                if (leader) ptx::mbar_expect_tx(&bars->k_full[s], 2 * lay.kstage);
+                ptx::tma_load_4d_2sm(sK + s * lay.kstage, &mapK, &bars->k_full[s], 0,
+                                     j * BN + 32 * static_cast<int>(rank), 0, bh);
+            }
+        }
+    } else if (warp == 10) {
+        // --------------------------------------------------------------- V producer
+        if (lane == 0) {
+            const int half1 = p.n1 / 2, half2 = p.n2 / 2;
+            const int nslices = ntiles * (BN / kVKeys);
+            for (int n = 0; n < nslices; ++n) {
+                const int s = n % kVStages;
+                if (n >= kVStages) ptx::mbar_wait(&bars->v_empty[s], ((n / kVStages) - 1) & 1);
+                FIPA_TRACE(6, n);
+                if (leader) ptx::mbar_expect_tx(&bars->v_full[s], 2 * lay.vstage);
+                uint8_t* dst = sV + s * lay.vstage;
+                const int key = n * kVKeys;
+                for (int x = 0; x < p.nb1; ++x)
+                    ptx::tma_load_3d_2sm(dst + x * kVBoxBytes, &mapV, &bars->v_full[s],
+                                         half1 * static_cast<int>(rank) + 64 * x, key, bh);
+                for (int x = 0; x < p.nb2; ++x)
+                    ptx::tma_load_3d_2sm(dst + (p.nb1 + x) * kVBoxBytes, &mapV, &bars->v_full[s],
+                                         p.n1 + half2 * static_cast<int>(rank) + 64 * x, key, bh);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issue (even CTA only)
+        if (leader) {
+            const uint32_t idesc_qk = ptx::idesc_bf16(256, BN, false, false);
+            const uint32_t idesc_pv1 = ptx::idesc_bf16(256, p.n1, false, true);
+            const uint32_t idesc_pv2 = ptx::idesc_bf16(256, p.n2 > 0 ? p.n2 : 16, false, true);
+            const uint32_t q_base = ptx::smem_u32(sQ);
+            const uint32_t p_base = ptx::smem_u32(sP);
+            const uint32_t k_base = ptx::smem_u32(sK);
+            const uint32_t v_base = ptx::smem_u32(sV);
+            ptx::mbar_wait(&bars->q_full, 0);
+            for (int j = 0; j <= ntiles; ++j) {
+                if (j < ntiles) {
+                    if (j > 0) ptx::mbar_wait_cluster(&bars->s_free, (j - 1) & 1);
+                    if (lane == 0) FIPA_TRACE(7, j);
+                    const int ks = j % kKStages;
+                    ptx::mbar_wait(&bars->k_full[ks], (j / kKStages) & 1);
+                    if (lane == 0) FIPA_TRACE(0, j);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t kb = k_base + ks * lay.kstage;
+                        for (int kk = 0; kk < qk_steps; ++kk) {
+                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
+                            const uint64_t da = ptx::sw128_desc(q_base + blk * (BM * 128) + sub, 16, 1024);
+                            const uint64_t db = ptx::sw128_desc(kb + blk * (32 * 128) + sub, 16, 1024);
+                            ptx::mma2_ss(tmem + kSCol, da, db, idesc_qk, kk != 0);
+                        }
+                        ptx::mma_commit_2sm(&bars->k_empty[ks], 0x3);
+                        ptx::mma_commit_2sm(&bars->s_full, 0x3);
+                    }
+                    __syncwarp();
+                }
+                if (j > 0) {
+                    const int jj = j - 1;
+                    ptx::mbar_wait_cluster(&bars->p_full, jj & 1);
+                    if (lane == 0) FIPA_TRACE(8, jj);
+                    for (int h2 = 0; h2 < BN / kVKeys; ++h2) {
+                        const int n = jj * (BN / kVKeys) + h2;
+                        const int vs = n % kVStages;
+                        ptx::mbar_wait(&bars->v_full[vs], (n / kVStages) & 1);
+                        if (lane == 0 && h2 == 0) FIPA_TRACE(1, jj);
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            for (int kk = 0; kk < kVKeys / 16; ++kk) {
+                                const uint64_t da = ptx::sw128_desc(p_base + (2 * h2 + kk) * 32, 16, 1024);
+                                const uint32_t vb = v_base + vs * lay.vstage + kk * 2048;
+                                const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
+                                ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kVBoxBytes, 1024), idesc_pv1, acc);
+                                if (p.n2 > 0)
+                                    ptx::mma2_ss(tmem + p.n1, da,
+                                                 ptx::sw128_desc(vb + p.nb1 * kVBoxBytes, kVBoxBytes, 1024),
+                                                 idesc_pv2, acc);
+                            }
+                            ptx::mma_commit_2sm(&bars->v_empty[vs], 0x3);
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) FIPA_TRACE(11, jj);
+                    if (ptx::elect_one()) {
+                        ptx::mma_commit_2sm(&bars->pv_done, 0x3);
+                        if (j == ntiles) ptx::mma_commit_2sm(&bars->o_full, 0x3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ softmax
+        // Eight warps: warp w handles TMEM lane quadrant w%4 (its 32 rows) and key half
+        // (w-2)/4 of every S tile; the two warps of a quadrant exchange their row maxima through
+        // shared memory once per tile so both halves of P share one scale.
+        const int sw = warp - 2;
+        const int quad = warp & 3;
+        const int half = sw >> 2;
+        const int row = quad * 32 + lane;
+        const uint32_t tl = tmem + (uint32_t(quad * 32) << 16);
+        const uint32_t s_free_remote = ptx::mapa(&bars->s_free, 0);
+        const uint32_t p_full_remote = ptx::mapa(&bars->p_full, 0);
+        float* xch = reinterpret_cast<float*>(smem + lay.xch);  // [2 parity][2 half][128 rows]
+        uint8_t* prow = sP + row * 128;
+        const int n16 = p.dv_mma / 16;                 // O rescale: 16-column chunks split by half
+        const int c_lo = half ? (n16 + 1) / 2 : 0, c_hi = half ? n16 : (n16 + 1) / 2;
+        float m = -INFINITY;  // running max, log2 units (identical in both halves)
+        float l = 0.f;        // this half's partial denominator
+        for (int j = 0; j < ntiles; ++j) {
+            ptx::mbar_wait(&bars->s_full, j & 1);
+            if (lane == 0) FIPA_TRACE(2, j);
+            ptx::tc_fence_after();
+            uint32_t sr[32];
+            ptx::tmem_ld32(tl + kSCol + 32 * half, sr);
+            ptx::tmem_wait_ld();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(s_free_remote);
+            if (lane == 0) FIPA_TRACE(12, j);
+
+            float x[32];
+            const int kvalid = p.L - j * BN - 32 * half;  // keys >= L are not real
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) x[cc] = cc < kvalid ? __uint_as_float(sr[cc]) : -INFINITY;
+            float mx[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx[k] = fmaxf(fmaxf(x[4 * k], x[4 * k + 1]), fmaxf(x[4 * k + 2], x[4 * k + 3]));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mx[k] = fmaxf(mx[k], mx[k + 4]);
+            float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+            float* xb = xch + (j & 1) * 256;
+            xb[half * 128 + row] = mt;
+            named_bar_sync(2 + quad, 64);
+            mt = fmaxf(mt, xb[(half ^ 1) * 128 + row]);
+            const bool need = mt > m + 8.0f;  // also true on the first finite tile
+            float scale = 1.0f;
+            if (need) {
+                scale = ptx::ex2(m - mt);  // 0 when m == -inf
+                m = mt;
+                l *= scale;
+            }
+            const float mm = m == -INFINITY ? 0.f : m;
+            uint32_t pk[16];
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+                const float p0 = ptx::ex2(x[2 * cc] - mm);
+                const float p1 = ptx::ex2(x[2 * cc + 1] - mm);
+                ls[cc & 3] += p0 + p1;
+                pk[cc] = ptx::pack_bf16x2(p0, p1);
+            }
+            l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            if (lane == 0) FIPA_TRACE(13, j);
+
+            // P_j overwrites P_{j-1} (and O may be rescaled) only once PV_{j-1} is done.
+            if (j > 0) {
+                ptx::mbar_wait(&bars->pv_done, (j - 1) & 1);
+                if (lane == 0) FIPA_TRACE(3, j);
+                ptx::tc_fence_after();
+                if (__any_sync(0xffffffffu, need)) {
+                    for (int ch = c_lo; ch < c_hi; ++ch) {
+                        uint32_t o[16];
+                        ptx::tmem_ld16(tl + 16 * ch, o);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * scale);
+                        ptx::tmem_st16(tl + 16 * ch, o);
+                    }
+                    ptx::tmem_wait_st();
+                }
+            }
+            if (lane == 0) FIPA_TRACE(14, j);
+            // P row half (32 keys, 64 B) in the SWIZZLE_128B K-major layout: 16-byte chunk k of
+            // row r lives at chunk k ^ (r % 8).
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int chunk = 4 * half + k;
+                const uint4 v = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                *reinterpret_cast<uint4*>(prow + ((chunk ^ (row & 7)) << 4)) = v;
+            }
+            ptx::fence_proxy_async_smem();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_remote(p_full_remote);
+            if (lane == 0) FIPA_TRACE(4, j);
+        }
+
+        // -------------------------------------------------------------- epilogue
+        float* lb = xch + (ntiles & 1) * 256;
+        lb[half * 128 + row] = l;
+        named_bar_sync(2 + quad, 64);
+        l += lb[(half ^ 1) * 128 + row];
+        ptx::mbar_wait(&bars->o_full, 0);
+        if (lane == 0) FIPA_TRACE(9, 0);
+        ptx::tc_fence_after();
+        const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+        const int qi = q0 + row;
+        if (half == 0 && qi < p.L)
+            p.lse[static_cast<int64_t>(bh) * p.L + qi] = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half);
+        if (lane == 0) FIPA_TRACE(9, 1);
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) ptx::tmem_dealloc_2sm(tmem, 512);
+}
+
+}  // namespace
+
+bool attn_fwd_2sm_supported(const LayerDims& d) {
+    const int n1 = std::min(d.dv_mma, 256), n2 = d.dv_mma - n1;
+    const int nb1 = (n1 / 2 + 63) / 64, nb2 = (n2 / 2 + 63) / 64;
+    const int n_qkb = (d.dqk_mma + 63) / 64;
+    const Layout lay = smem_layout(n_qkb, nb1, nb2);
+    return d.dv_mma <= 448 && n1 % 16 == 0 && n2 % 16 == 0 && 3 * d.n_value + 6 <= 48 &&
+           d.dqk_pad % 64 == 0 && d.dv_pad % 64 == 0 && n_qkb * 64 <= d.dqk_pad &&
+           lay.total + 1024 <= 232448 && epilogue_smem(d.seg) <= lay.xch;
+}
+
+void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t stream) {
+    if (!attn_fwd_2sm_supported(d))
+        throw std::invalid_argument("tcgen05 attention: lifted widths unsupported (use precision='f32')");
+    Attn2Params p{};
+    p.L = a.L;
+    p.H = d.heads;
+    p.dqk_mma = d.dqk_mma;
+    p.dv_mma = d.dv_mma;
+    p.n_qkb = (d.dqk_mma + 63) / 64;
+    p.n1 = std::min(d.dv_mma, 256);
+    p.n2 = d.dv_mma - p.n1;
+    p.nb1 = (p.n1 / 2 + 63) / 64;
+    p.nb2 = (p.n2 / 2 + 63) / 64;
+    p.c = d.c;
+    p.d_z = d.d_z;
+    p.rank = d.rank;
+    p.n_value = d.n_value;
+    p.seg = d.seg;
+    p.feat_ld = d.feat_ld;
+    p.z1 = a.z1;
+    p.rot = a.rot;
+    p.trans = a.trans;
+    p.feat_out = a.feat;
+    p.lse = a.lse;
+    const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
+    const CUtensorMap mapQ = make_map_blocks_bf16(a.qhat, a.L, BH, d.dqk_pad, BM, p.n_qkb);
+    const CUtensorMap mapK = make_map_blocks_bf16(a.khat, a.L, BH, d.dqk_pad, 32, p.n_qkb);
+    const CUtensorMap mapV = make_map_3d_bf16(a.vhat, d.dv_pad, a.L, BH, d.dv_pad, 64, kVKeys);
+    const Layout lay = smem_layout(p.n_qkb, p.nb1, p.nb2);
+    const int smem = lay.total + 1024;
+    cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int qtiles = (a.L + BM - 1) / BM;
+    dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(BH));
+    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, p);
+}
+
+}  // namespace fipa_b200

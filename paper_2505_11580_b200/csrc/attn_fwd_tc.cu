@@ -48,7 +48,7 @@ constexpr int kMaxSimt = 16;
 constexpr float kLn2 = 0.6931471805599453f;
 
 struct AttnParams {
-    int L, H, dqk_pad, dv_tc, dv_simt, dv_used, n_qkb, n_vb;
+    int L, H, dqk_mma, dv_tc, dv_simt, dv_used, n_qkb, n_vb;
     int c, d_z, rank, n_value, seg, feat_ld;
     const float* z1;
     const float* rot;
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q_base = ptx::smem_u32(sQ);
         const uint32_t k_base = ptx::smem_u32(sK);
         const uint32_t v_base = ptx::smem_u32(sV);
-        const int qk_steps = p.dqk_pad / 16;
+        const int qk_steps = p.dqk_mma / 16;
         ptx::mbar_wait(&bars->q_full, 0);
         for (int j = 0; j <= ntiles; ++j) {
             if (j < ntiles) {
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stream) {
-    if (d.dqk_pad > 448)
+    if (d.dqk_mma > 448)
         throw std::invalid_argument("tcgen05 attention: lifted q/k width exceeds 448 (use precision='f32')");
     if (d.dv_simt > kMaxSimt)
         throw std::invalid_argument("tcgen05 attention: lifted value width exceeds 432 (use precision='f32')");
@@ -459,11 +459,11 @@ void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stre
     AttnParams p{};
     p.L = a.L;
     p.H = d.heads;
-    p.dqk_pad = d.dqk_pad;
+    p.dqk_mma = d.dqk_mma;
     p.dv_tc = d.dv_tc;
     p.dv_simt = d.dv_simt;
     p.dv_used = d.dv_used;
-    p.n_qkb = (d.dqk_pad + 63) / 64;
+    p.n_qkb = (d.dqk_mma + 63) / 64;
     p.n_vb = (d.dv_pad + 63) / 64;
     p.c = d.c;
     p.d_z = d.d_z;

@@ -37,9 +37,11 @@ struct LayerDims {
     int d_in, d_z, heads, c, n_query, n_value, rank;
     int n_proj;      // H*(3c + 6Nq + 3Nv): fused projection width
     int dqk_used;    // c + 3Nq + 20 + r*d_z      (lifted query/key width, see pack.cu)
-    int dqk_pad;     // dqk_used rounded up to 16
+    int dqk_mma;     // dqk_used rounded up to 16  (MMA K extent of Q.K^T)
+    int dqk_pad;     // dqk_used rounded up to 64  (row stride of q_hat / k_hat: 128-byte blocks)
     int dv_used;     // c + r*d_z + 3Nv + 6       (v | z2 | R v_p | t_hi | t_lo)
-    int dv_pad;      // dv_used rounded up to 16
+    int dv_mma;      // dv_used rounded up to 16   (MMA N extent of P.V)
+    int dv_pad;      // dv_used rounded up to 64   (row stride of v_hat)
     int dv_tc;       // value columns accumulated by the tensor cores (multiple of 16, <= 416)
     int dv_simt;     // dv_used - dv_tc trailing value columns accumulated on CUDA cores
     int seg;         // d_z + c + 4Nv             (per-head feature block)
@@ -82,6 +84,9 @@ struct AttnArgs {
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
 // inverse frame / norms) writing bf16 features.
 void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
+// CTA-pair version (tcgen05 cta_group::2, 256 query rows per pair, streamed K/V rings).
+bool attn_fwd_2sm_supported(const LayerDims& d);
+void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
 
 // Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);

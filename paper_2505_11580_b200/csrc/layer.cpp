@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -36,6 +37,13 @@ std::string cat(P&&... parts) {
     } while (0)
 
 std::size_t round_up(std::size_t x, std::size_t m) { return (x + m - 1) / m * m; }
+
+// CTA-pair attention unless FIPA_ATTN_IMPL=1sm forces the single-CTA kernel.
+bool use_2sm_attention(const LayerDims& d) {
+    const char* e = std::getenv("FIPA_ATTN_IMPL");
+    const bool force_1sm = e != nullptr && std::string(e) == "1sm";
+    return !force_1sm && attn_fwd_2sm_supported(d);
+}
 
 // ------------------------------------------------------------------ Rng
 // Counter-based splitmix64 + Box-Muller, bit-identical to the reference generator
@@ -108,11 +116,13 @@ LayerDims Config::dims() const {
     d.rank = int(rank);
     d.n_proj = int(heads * (3 * c + 6 * n_query + 3 * n_value));
     d.dqk_used = int(c + 3 * n_query + 20 + rank * d_z);
-    d.dqk_pad = int(round_up(d.dqk_used, 16));
+    d.dqk_mma = int(round_up(d.dqk_used, 16));
+    d.dqk_pad = int(round_up(d.dqk_used, 64));
     d.dv_used = int(c + rank * d_z + 3 * n_value + 6);
-    d.dv_pad = int(round_up(d.dv_used, 16));
+    d.dv_mma = int(round_up(d.dv_used, 16));
+    d.dv_pad = int(round_up(d.dv_used, 64));
     // TMEM budget of the tcgen05 attention: O (dv_tc) + S (64) + P (32) <= 512 columns.
-    d.dv_tc = std::min(d.dv_pad, 416);
+    d.dv_tc = std::min(d.dv_mma, 416);
     d.dv_simt = std::max(0, d.dv_used - d.dv_tc);
     d.seg = int(d_z + c + 4 * n_value);
     d.feat = int(heads) * d.seg;
@@ -552,7 +562,11 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         aa.lse = ws.lse;
         aa.B = int(B);
         aa.L = int(L);
-        launch_attn_fwd_tc(d, aa, stream);
+        if (use_2sm_attention(d)) {
+            launch_attn_fwd_2sm(d, aa, stream);
+        } else {
+            launch_attn_fwd_tc(d, aa, stream);
+        }
         mark(5);
         GemmArgs g;
         g.A = static_cast<const __nv_bfloat16*>(ws.feat);

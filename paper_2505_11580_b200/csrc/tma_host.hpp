@@ -66,4 +66,25 @@ inline CUtensorMap make_map_3d_bf16(const void* base, uint64_t d0, uint64_t d1, 
     return m;
 }
 
+// bf16 tensor [d2][rows][ld] viewed as 128-byte column blocks: 4-D map
+// {64 elements, rows, ld/64 blocks, d2} with strides {ld*2, 128, rows*ld*2}, so a single box
+// {64, box_rows, nblk, 1} lands in shared memory as nblk consecutive [box_rows][128 B] blocks --
+// exactly the SWIZZLE_128B K-major operand layout -- in ONE TMA instruction.  ld % 64 == 0.
+inline CUtensorMap make_map_blocks_bf16(const void* base, uint64_t rows, uint64_t d2, uint64_t ld,
+                                        uint32_t box_rows, uint32_t nblk) {
+    CUtensorMap m{};
+    cuuint64_t dims[4] = {64, rows, ld / 64, d2};
+    cuuint64_t strides[3] = {ld * 2, 128, rows * ld * 2};
+    cuuint32_t box[4] = {64, box_rows, nblk, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(4d blocks) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 }  // namespace fipa_b200

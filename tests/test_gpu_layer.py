@@ -162,3 +162,16 @@ def test_reference_model_defaults_roundtrip(fipa, tmp_path):
     other = fipa.Model(seed=999)
     other.load(path)
     assert np.array_equal(other.flash(*args), got)
+
+
+@pytest.mark.parametrize("impl", ["1sm", "2sm"])
+def test_attention_kernels_agree(fipa, impl, monkeypatch):
+    """Both tcgen05 attention kernels (single CTA, CTA pair) against the oracle at the
+    north-star shape, ragged L with masked keys (FIPA_ATTN_IMPL selects the kernel)."""
+    monkeypatch.setenv("FIPA_ATTN_IMPL", impl)
+    model = _model(fipa, MAIN, "bf16", seed=21)
+    w = oracle_weights_for(model, "bf16")
+    batch = make_batch(MAIN, 2, 389, seed=4242, mask_frac=0.15, bf16=True)
+    got = model.flash(batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"], mask=batch["mask"])
+    ref = oracle_forward(MAIN, w, batch)
+    assert rel_dev(ref, got) < BF16_TOL

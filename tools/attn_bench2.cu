@@ -1,8 +1,8 @@
-// Pipeline trace of the tcgen05 attention kernel: per-tile event timestamps (SM clock) of CTA
+// Timing harness of the CTA-pair attention kernel (no trace points)
 // (0,0) at the north-star shape, B=8 L=1024.  Build with -DFIPA_ATTN_TRACE (see Makefile rule
 // in tools/README or the gpurun command in profiles/).
-#define FIPA_ATTN_TRACE 1
-#include "../paper_2505_11580_b200/csrc/attn_fwd_tc.cu"
+
+#include "../paper_2505_11580_b200/csrc/attn_fwd_2sm.cu"
 
 #include <cstdio>
 #include <cstdlib>
@@ -43,10 +43,10 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int it = 0; it < 3; ++it) launch_attn_fwd_tc(d, a, 0);
+    for (int it = 0; it < 3; ++it) launch_attn_fwd_2sm(d, a, 0);
     cudaEventRecord(e0);
     const int reps = 10;
-    for (int it = 0; it < reps; ++it) launch_attn_fwd_tc(d, a, 0);
+    for (int it = 0; it < reps; ++it) launch_attn_fwd_2sm(d, a, 0);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0;
@@ -55,19 +55,6 @@ int main(int argc, char** argv) {
     const double flops = 2.0 * BH * L * double(L) * (424 + 420);
     printf("status %s  B=%d L=%d  %.3f ms  %.1f TFLOP/s\n", cudaGetErrorString(err), B, L, ms,
            flops / ms / 1e9);
-    std::vector<long long> t(16 * 256);
-    cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * sizeof(long long));
-    const long long t0 = t[2 * 256 + 0];
-    const char* names[9] = {"Kload", "Vload", "QKiss", "PViss", "Sfull", "PVdone", "Pfull", "SIMTend", "ofull/end"};
-    const int nt = (L + 63) / 64;
-    printf("tile ");
-    for (int e = 0; e < 8; ++e) printf("%9s", names[e]);
-    printf("\n");
-    for (int j = 0; j < nt && j < 40; ++j) {
-        printf("%4d ", j);
-        for (int e = 0; e < 8; ++e) printf("%9lld", t[e * 256 + j] ? t[e * 256 + j] - t0 : -1);
-        printf("\n");
-    }
-    printf("o_full %lld  end %lld\n", t[8 * 256] - t0, t[8 * 256 + 1] - t0);
     return 0;
 }
+

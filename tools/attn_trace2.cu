@@ -1,8 +1,8 @@
-// Pipeline trace of the tcgen05 attention kernel: per-tile event timestamps (SM clock) of CTA
-// (0,0) at the north-star shape, B=8 L=1024.  Build with -DFIPA_ATTN_TRACE (see Makefile rule
-// in tools/README or the gpurun command in profiles/).
+// Pipeline trace of the CTA-pair attention kernel (leader CTA of cluster (0,0)), north-star
+// shape.  Events (SM clock): QK first-block ready, PV first-stage ready, softmax S ready,
+// softmax PV(j-1) done, softmax P published, K/V load issue, MMA s_free / p_full observed.
 #define FIPA_ATTN_TRACE 1
-#include "../paper_2505_11580_b200/csrc/attn_fwd_tc.cu"
+#include "../paper_2505_11580_b200/csrc/attn_fwd_2sm.cu"
 
 #include <cstdio>
 #include <cstdlib>
@@ -43,10 +43,10 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int it = 0; it < 3; ++it) launch_attn_fwd_tc(d, a, 0);
+    for (int it = 0; it < 3; ++it) launch_attn_fwd_2sm(d, a, 0);
     cudaEventRecord(e0);
     const int reps = 10;
-    for (int it = 0; it < reps; ++it) launch_attn_fwd_tc(d, a, 0);
+    for (int it = 0; it < reps; ++it) launch_attn_fwd_2sm(d, a, 0);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0;
@@ -55,19 +55,22 @@ int main(int argc, char** argv) {
     const double flops = 2.0 * BH * L * double(L) * (424 + 420);
     printf("status %s  B=%d L=%d  %.3f ms  %.1f TFLOP/s\n", cudaGetErrorString(err), B, L, ms,
            flops / ms / 1e9);
-    std::vector<long long> t(16 * 256);
+    std::vector<long long> t(2 * 16 * 16 * 128);
     cudaMemcpyFromSymbol(t.data(), g_attn_trace, t.size() * sizeof(long long));
-    const long long t0 = t[2 * 256 + 0];
-    const char* names[9] = {"Kload", "Vload", "QKiss", "PViss", "Sfull", "PVdone", "Pfull", "SIMTend", "ofull/end"};
+    auto T = [&](int cta, int w, int ev, int j) { return t[((cta * 16 + w) * 16 + ev) * 128 + j]; };
+    const long long t0 = T(0, 1, 0, 0);
     const int nt = (L + 63) / 64;
-    printf("tile ");
-    for (int e = 0; e < 8; ++e) printf("%9s", names[e]);
-    printf("\n");
-    for (int j = 0; j < nt && j < 40; ++j) {
-        printf("%4d ", j);
-        for (int e = 0; e < 8; ++e) printf("%9lld", t[e * 256 + j] ? t[e * 256 + j] - t0 : -1);
-        printf("\n");
-    }
-    printf("o_full %lld  end %lld\n", t[8 * 256] - t0, t[8 * 256 + 1] - t0);
+    printf("MMA leader: tile sfree kfull pfull(j) pv0(j) pvend(j) | Kissue(j) Vissue(2j) Vissue(2j+1)\n");
+    for (int j = 0; j < nt && j < 64; ++j)
+        printf("  %3d %8lld %8lld %8lld %8lld %8lld | %8lld %8lld %8lld\n", j, T(0,1,7,j)-t0, T(0,1,0,j)-t0,
+               T(0,1,8,j)-t0, T(0,1,1,j)-t0, T(0,1,11,j)-t0, T(0,0,5,j)-t0, T(0,10,6,2*j)-t0, T(0,10,6,2*j+1)-t0);
+    for (int cta = 0; cta < 2; ++cta)
+        for (int w : {2, 6}) {
+            printf("softmax cta%d w%d: tile sfull sfree expd pvdone resc ppub\n", cta, w);
+            for (int j = 0; j < nt && j < 64; j += (w == 2 && cta == 0 ? 1 : 4))
+                printf("  %3d %8lld %8lld %8lld %8lld %8lld %8lld\n", j, T(cta,w,2,j)-t0, T(cta,w,12,j)-t0,
+                       T(cta,w,13,j)-t0, j ? T(cta,w,3,j)-t0 : 0, T(cta,w,14,j)-t0, T(cta,w,4,j)-t0);
+        }
+    printf("o_full %lld  end %lld\n", T(0,2,9,0)-t0, T(0,2,9,1)-t0);
     return 0;
 }
