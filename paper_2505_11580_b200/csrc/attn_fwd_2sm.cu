@@ -54,6 +54,7 @@ constexpr float kLn2 = 0.6931471805599453f;
 struct Attn2Params {
     int L, H, dqk_mma, dv_mma, n_qkb, n1, n2, nb1, nb2;
     int c, d_z, rank, n_value, seg, feat_ld;
+    int z1_tma;  // z1 staged by TMA into shared memory for the epilogue
     const float* z1;
     const float* rot;
     const float* trans;
@@ -65,7 +66,7 @@ struct Bars {
     uint64_t q_full;
     uint64_t k_full[kKStages], k_empty[kKStages];
     uint64_t v_full[kVStages], v_empty[kVStages];
-    uint64_t s_full, s_free, p_full, pv_done, o_full;
+    uint64_t s_full, s_free, p_full, pv_done, o_full, z_full;
     uint32_t tmem_slot;
 };
 
@@ -86,7 +87,7 @@ __host__ __device__ inline Layout smem_layout(int n_qkb, int nb1, int nb2) {
     return l;
 }
 __host__ __device__ constexpr int epilogue_smem(int seg) {
-    return BM * ((seg + 7) / 8 * 8 + 8) * 2 + BM * 49 * 4;
+    return (BM * ((seg + 7) / 8 * 8 + 8) * 2 + 1023) / 1024 * 1024;
 }
 
 // Optional per-event timestamps of clusters (0,0) for pipeline analysis (tools/attn_trace2.cu).
@@ -110,12 +111,14 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // Fused output epilogue (proj/src/flash_ipa.cpp:171-210), one thread per query row reading the
 // row's O accumulator straight from TMEM; the two warps of a lane quadrant split the columns:
 //   feat block = [ sum_rho z1[i,rho,:] * O_pair[rho,:] | O_scalar | R_i^T(g_p - t_i) | |.| ]
-// with g_p = agg(R_j v_p) + agg(t_j hi) + agg(t_j lo).  The z1 row chunks are fetched one chunk
-// ahead of their use (the TMEM loads are ordered asm, so the prefetch is explicit).  Rows are
-// assembled as bf16 in shared memory, then the 128 x seg block is written with coalesced
-// 16-byte stores by all 256 epilogue threads.
-__device__ __forceinline__ void load_z16(const float* zp, bool full, int rem, float* z) {
-    if (full) {
+// with g_p = agg(t_j hi) + agg(t_j lo) + agg(R_j v_p) (value point block [t hi|t lo|R v_p]).
+// z1 rows arrive by one TMA (swizzled 128-byte blocks, conflict-free 16-byte reads) issued when
+// the accumulator is final; shapes the TMA path does not cover read z1 from global instead.
+// Rows are assembled as bf16 in shared memory and written out with coalesced 16-byte stores.
+constexpr int kMaxPoints = 14;
+
+__device__ __forceinline__ void load_z16_global(const float* zp, bool vec, int rem, float* z) {
+    if (vec && rem >= 16) {
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4) {
             const float4 f = __ldg(reinterpret_cast<const float4*>(zp) + v4);
@@ -130,18 +133,32 @@ __device__ __forceinline__ void load_z16(const float* zp, bool full, int rem, fl
     }
 }
 
+// 16 consecutive floats (f % 16 == 0) of row `row` from the swizzled z1 staging block.
+__device__ __forceinline__ void load_z16_smem(const uint8_t* zs, int row, int f, float* z) {
+    const uint8_t* rb = zs + (f >> 5) * (BM * 128) + row * 128;
+    const int k0 = (f & 31) >> 2;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 v = *reinterpret_cast<const float4*>(rb + (((k0 + k) ^ (row & 7)) << 4));
+        z[4 * k] = v.x;
+        z[4 * k + 1] = v.y;
+        z[4 * k + 2] = v.z;
+        z[4 * k + 3] = v.w;
+    }
+}
+
 __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl, float inv_l,
-                                               int row, int q0, int bh, uint8_t* smem, int half) {
+                                               int row, int q0, int bh, uint8_t* smem, int half,
+                                               const uint8_t* zs, uint64_t* z_full) {
     const int seg = p.seg, sst = (seg + 7) / 8 * 8 + 8;
     __nv_bfloat16* fst = reinterpret_cast<__nv_bfloat16*>(smem);
     __nv_bfloat16* frow = fst + row * sst;
-    float* pts = reinterpret_cast<float*>(smem + BM * sst * 2) + row * 49;
     const int H = p.H, b = bh / H, h = bh % H;
     const int q = q0 + row;
     const bool ok = q < p.L;
     const int64_t grow = static_cast<int64_t>(b) * p.L + (ok ? q : 0);
     const int c = p.c, dz = p.d_z, Nv = p.n_value;
-    const int base = c + p.rank * dz, npt = 3 * Nv + 6;
+    const int base = c + p.rank * dz;
 
     // scalar aggregate -> [d_z, d_z + c): 16-column chunks split between the halves
     const int nsc = (c + 15) / 16;
@@ -154,49 +171,13 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
         for (int e = 0; e < 16; ++e)
             if (c0 + e < c) frow[dz + c0 + e] = __float2bfloat16_rn(__uint_as_float(o[e]) * inv_l);
     }
-    // pair contraction -> [0, d_z), z1 chunks prefetched one (chunk, rho) step ahead
-    const float* z1r = p.z1 + grow * (p.rank * dz);
-    const bool vec = (reinterpret_cast<uintptr_t>(z1r) & 15) == 0 && dz % 16 == 0;
-    const int npc = (dz + 15) / 16;
-    const int pc0 = half ? (npc + 1) / 2 : 0, pc1 = half ? npc : (npc + 1) / 2;
-    const int nsteps = (pc1 - pc0) * p.rank;
-    float zc[16], zn[16];
-    if (nsteps > 0) load_z16(z1r + 16 * pc0, vec, dz - 16 * pc0, zc);
-    float acc[16];
-    for (int st = 0; st < nsteps; ++st) {
-        const int ch = pc0 + st / p.rank, rho = st % p.rank;
-        const int d0 = 16 * ch;
-        if (st + 1 < nsteps) {
-            const int ch2 = pc0 + (st + 1) / p.rank, rho2 = (st + 1) % p.rank;
-            load_z16(z1r + rho2 * dz + 16 * ch2, vec, dz - 16 * ch2, zn);
-        }
-        if (rho == 0) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-        }
-        uint32_t o[16];
-        ptx::tmem_ld16(tl + c + rho * dz + d0, o);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = fmaf(zc[e], __uint_as_float(o[e]), acc[e]);
-        if (rho == p.rank - 1) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                if (d0 + e < dz) frow[d0 + e] = __float2bfloat16_rn(acc[e] * inv_l);
-        }
-#pragma unroll
-        for (int e = 0; e < 16; ++e) zc[e] = zn[e];
-    }
-    // points (half 0): point block [base, base + npt) of O_hat -> per-row scratch -> local frame
+    // points (half 0), all in registers: local = R_i^T (g - t_i)   (proj/src/geometry.cpp:70-76)
     if (half == 0) {
-        for (int c0 = 0; c0 < npt; c0 += 16) {
-            uint32_t o[16];
-            ptx::tmem_ld16(tl + base + c0, o);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                if (c0 + e < npt) pts[c0 + e] = __uint_as_float(o[e]) * inv_l;
-        }
+        uint32_t o[48];
+        ptx::tmem_ld16(tl + base, o);
+        ptx::tmem_ld16(tl + base + 16, o + 16);
+        ptx::tmem_ld16(tl + base + 32, o + 32);
+        ptx::tmem_wait_ld();
         if (ok) {
             const float* R = p.rot + grow * 9;
             const float* t = p.trans + grow * 3;
@@ -204,20 +185,52 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
 #pragma unroll
             for (int k = 0; k < 9; ++k) Rm[k] = __ldg(R + k);
 #pragma unroll
-            for (int y = 0; y < 3; ++y) tg[y] = pts[3 * Nv + y] + pts[3 * Nv + 3 + y] - __ldg(t + y);
+            for (int y = 0; y < 3; ++y)
+                tg[y] = (__uint_as_float(o[y]) + __uint_as_float(o[3 + y])) * inv_l - __ldg(t + y);
             __nv_bfloat16* fp = frow + dz + c;
-            for (int pt = 0; pt < Nv; ++pt) {
-                const float gx = pts[3 * pt] + tg[0], gy = pts[3 * pt + 1] + tg[1], gz = pts[3 * pt + 2] + tg[2];
-                // apply_inverse: R^T g   (proj/src/geometry.cpp:70-76)
-                const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
-                const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));
-                const float lz = fmaf(Rm[2], gx, fmaf(Rm[5], gy, Rm[8] * gz));
-                fp[3 * pt] = __float2bfloat16_rn(lx);
-                fp[3 * pt + 1] = __float2bfloat16_rn(ly);
-                fp[3 * pt + 2] = __float2bfloat16_rn(lz);
-                fp[3 * Nv + pt] = __float2bfloat16_rn(sqrtf(lx * lx + ly * ly + lz * lz));
+#pragma unroll
+            for (int pt = 0; pt < kMaxPoints; ++pt) {
+                if (pt < Nv) {
+                    const float gx = __uint_as_float(o[6 + 3 * pt]) * inv_l + tg[0];
+                    const float gy = __uint_as_float(o[7 + 3 * pt]) * inv_l + tg[1];
+                    const float gz = __uint_as_float(o[8 + 3 * pt]) * inv_l + tg[2];
+                    const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
+                    const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));
+                    const float lz = fmaf(Rm[2], gx, fmaf(Rm[5], gy, Rm[8] * gz));
+                    fp[3 * pt] = __float2bfloat16_rn(lx);
+                    fp[3 * pt + 1] = __float2bfloat16_rn(ly);
+                    fp[3 * pt + 2] = __float2bfloat16_rn(lz);
+                    fp[3 * Nv + pt] = __float2bfloat16_rn(sqrtf(lx * lx + ly * ly + lz * lz));
+                }
             }
         }
+    }
+    // pair contraction -> [0, d_z): 16-column chunks split between the halves
+    const float* z1r = p.z1 + grow * (p.rank * dz);
+    const bool vec = (reinterpret_cast<uintptr_t>(z1r) & 15) == 0;
+    if (zs != nullptr) ptx::mbar_wait(z_full, 0);
+    const int npc = (dz + 15) / 16;
+    for (int ch = half ? (npc + 1) / 2 : 0; ch < (half ? npc : (npc + 1) / 2); ++ch) {
+        const int d0 = 16 * ch;
+        float acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+        for (int rho = 0; rho < p.rank; ++rho) {
+            float z[16];
+            if (zs != nullptr) {
+                load_z16_smem(zs, row, rho * dz + d0, z);
+            } else {
+                load_z16_global(z1r + rho * dz + d0, vec, dz - d0, z);
+            }
+            uint32_t o[16];
+            ptx::tmem_ld16(tl + c + rho * dz + d0, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] = fmaf(z[e], __uint_as_float(o[e]), acc[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (d0 + e < dz) frow[d0 + e] = __float2bfloat16_rn(acc[e] * inv_l);
     }
     named_bar_sync(1, 256);
     const int tid = threadIdx.x - 64;  // 0..255 over warps 2..9
@@ -242,7 +255,8 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap mapQ,
                         const __grid_constant__ CUtensorMap mapK,
-                        const __grid_constant__ CUtensorMap mapV, Attn2Params p) {
+                        const __grid_constant__ CUtensorMap mapV,
+                        const __grid_constant__ CUtensorMap mapZ, Attn2Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -266,6 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(&mapQ);
         ptx::tma_prefetch(&mapK);
         ptx::tma_prefetch(&mapV);
+        if (p.z1_tma) ptx::tma_prefetch(&mapZ);
         ptx::mbar_init(&bars->q_full, 1);
         for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(&bars->k_full[s], 1);
@@ -280,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&bars->p_full, 16);
         ptx::mbar_init(&bars->pv_done, 1);
         ptx::mbar_init(&bars->o_full, 1);
+        ptx::mbar_init(&bars->z_full, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm(&bars->tmem_slot, 512);
@@ -497,7 +513,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int qi = q0 + row;
         if (half == 0 && qi < p.L)
             p.lse[static_cast<int64_t>(bh) * p.L + qi] = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
-        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half);
+        uint8_t* zs = smem + epilogue_smem(p.seg);
+        if (p.z1_tma && warp == 2 && lane == 0) {
+            // All MMAs are complete (o_full), so the Q/K/V/P regions are free for the z1 rows.
+            ptx::mbar_expect_tx(&bars->z_full, BM * p.rank * p.d_z * 4);
+            ptx::tma_load_3d(zs, &mapZ, &bars->z_full, 0, (bh / p.H) * p.L + q0, 0);
+        }
+        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full);
         if (lane == 0) FIPA_TRACE(9, 1);
     }
 
@@ -546,12 +568,20 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     const CUtensorMap mapQ = make_map_blocks_bf16(a.qhat, a.L, BH, d.dqk_pad, BM, p.n_qkb);
     const CUtensorMap mapK = make_map_blocks_bf16(a.khat, a.L, BH, d.dqk_pad, 32, p.n_qkb);
     const CUtensorMap mapV = make_map_3d_bf16(a.vhat, d.dv_pad, a.L, BH, d.dv_pad, 64, kVKeys);
+    const int rdz = d.rank * d.d_z;
+    const Layout lay0 = smem_layout(p.n_qkb, p.nb1, p.nb2);
+    p.z1_tma = (rdz % 32 == 0 && rdz / 32 <= 256 && (reinterpret_cast<uintptr_t>(a.z1) & 15) == 0 &&
+                epilogue_smem(d.seg) + BM * rdz * 4 <= lay0.xch)
+                   ? 1
+                   : 0;
+    const CUtensorMap mapZ = p.z1_tma ? make_map_blocks_f32(a.z1, static_cast<uint64_t>(a.B) * a.L, rdz, BM, rdz / 32)
+                                      : mapV;
     const Layout lay = smem_layout(p.n_qkb, p.nb1, p.nb2);
     const int smem = lay.total + 1024;
     cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int qtiles = (a.L + BM - 1) / BM;
     dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(BH));
-    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, p);
+    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, p);
 }
 
 }  // namespace fipa_b200

@@ -173,10 +173,11 @@ __device__ __forceinline__ void fused_epilogue(const AttnParams& p, uint32_t tl,
 #pragma unroll
         for (int k = 0; k < 9; ++k) Rm[k] = __ldg(R + k);
 #pragma unroll
-        for (int y = 0; y < 3; ++y) tg[y] = pts[3 * Nv + y] + pts[3 * Nv + 3 + y] - __ldg(t + y);
+        for (int y = 0; y < 3; ++y) tg[y] = pts[y] + pts[3 + y] - __ldg(t + y);
         __nv_bfloat16* fp = frow + dz + c;
         for (int pt = 0; pt < Nv; ++pt) {
-            const float gx = pts[3 * pt] + tg[0], gy = pts[3 * pt + 1] + tg[1], gz = pts[3 * pt + 2] + tg[2];
+            const float* pv = pts + 6 + 3 * pt;  // point block = [t hi | t lo | R_j v_p]
+            const float gx = pv[0] + tg[0], gy = pv[1] + tg[1], gz = pv[2] + tg[2];
             // apply_inverse: R^T g   (proj/src/geometry.cpp:70-76)
             const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
             const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));

@@ -39,7 +39,7 @@ struct LayerDims {
     int dqk_used;    // c + 3Nq + 20 + r*d_z      (lifted query/key width, see pack.cu)
     int dqk_mma;     // dqk_used rounded up to 16  (MMA K extent of Q.K^T)
     int dqk_pad;     // dqk_used rounded up to 64  (row stride of q_hat / k_hat: 128-byte blocks)
-    int dv_used;     // c + r*d_z + 3Nv + 6       (v | z2 | R v_p | t_hi | t_lo)
+    int dv_used;     // c + r*d_z + 6 + 3Nv       (v | z2 | t_hi | t_lo | R v_p)
     int dv_mma;      // dv_used rounded up to 16   (MMA N extent of P.V)
     int dv_pad;      // dv_used rounded up to 64   (row stride of v_hat)
     int dv_tc;       // value columns accumulated by the tensor cores (multiple of 16, <= 416)

@@ -22,7 +22,7 @@
 // The reference's |T_i q_p|^2 column (paired with -g/2) is constant along a query row and
 // cancels in the softmax, so it is dropped; its (ones, -g/2 |k|^2) pair becomes the folded
 // column bias cb.  Values:
-//   v_hat = [ v | z2_j flat | R_j v_p (3Nv) | t_j hi (3) | t_j lo (3) | 0 ]
+//   v_hat = [ v | z2_j flat | t_j hi (3) | t_j lo (3) | R_j v_p (3Nv) | 0 ]
 // (sum_j p_ij T_j v_p = sum_j p_ij R_j v_p + sum_j p_ij t_j, translation kept to ~2^-17).
 // For the fp32 path the same layout is written with hi = value, lo = 0.
 #include <cuda_bf16.h>
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     const int g0 = c + 3 * Nq;        // start of the 20 translation/bias columns
     const int zq = g0 + 20;           // start of the pair-factor columns
     const int qk_used = d.dqk_used;
-    const int v_pair = c + rdz, v_pts = v_pair + 3 * Nv, v_used = d.dv_used;
+    const int v_pair = c + rdz, v_used = d.dv_used;
 
     for (int h = 0; h < H; ++h) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
@@ -200,12 +200,12 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
                     x = s_proj[off_v + h * c + cc];
                 } else if (cc < v_pair) {
                     x = s_z2[cc - c];
-                } else if (cc < v_pts) {
-                    x = s_rv[h * Nv * 3 + (cc - v_pair)];
-                } else if (cc < v_pts + 3) {
-                    x = hi_part<OutT>(t[cc - v_pts]);
+                } else if (cc < v_pair + 3) {
+                    x = hi_part<OutT>(t[cc - v_pair]);
+                } else if (cc < v_pair + 6) {
+                    x = lo_part<OutT>(t[cc - v_pair - 3]);
                 } else if (cc < v_used) {
-                    x = lo_part<OutT>(t[cc - v_pts - 3]);
+                    x = s_rv[h * Nv * 3 + (cc - v_pair - 6)];
                 } else {
                     x = 0.f;
                 }

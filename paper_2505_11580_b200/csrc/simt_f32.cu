@@ -151,9 +151,10 @@ __global__ void __launch_bounds__(kWarps * 32) attn_fwd_f32_kernel(AttnF32Args a
         const float* R = a.rot + grow * 9;
         const float* t = a.trans + grow * 3;
         const float* pt = so + base;
-        const float gx = pt[3 * q2 + 0] + pt[3 * Nv + 0] + pt[3 * Nv + 3] - t[0];
-        const float gy = pt[3 * q2 + 1] + pt[3 * Nv + 1] + pt[3 * Nv + 4] - t[1];
-        const float gz = pt[3 * q2 + 2] + pt[3 * Nv + 2] + pt[3 * Nv + 5] - t[2];
+        // point block = [t hi (3) | t lo (3) | R_j v_p (3Nv)]  (pack.cu)
+        const float gx = pt[6 + 3 * q2 + 0] + pt[0] + pt[3] - t[0];
+        const float gy = pt[6 + 3 * q2 + 1] + pt[1] + pt[4] - t[1];
+        const float gz = pt[6 + 3 * q2 + 2] + pt[2] + pt[5] - t[2];
         const float lx = R[0] * gx + R[3] * gy + R[6] * gz;
         const float ly = R[1] * gx + R[4] * gy + R[7] * gz;
         const float lz = R[2] * gx + R[5] * gy + R[8] * gz;

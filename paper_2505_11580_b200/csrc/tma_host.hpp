@@ -87,4 +87,23 @@ inline CUtensorMap make_map_blocks_bf16(const void* base, uint64_t rows, uint64_
     return m;
 }
 
+// fp32 matrix [rows][ld] viewed as 128-byte (32-float) column blocks, one box = {32, box_rows,
+// nblk}: nblk consecutive SWIZZLE_128B [box_rows][128 B] blocks in shared memory.  ld % 32 == 0.
+inline CUtensorMap make_map_blocks_f32(const void* base, uint64_t rows, uint64_t ld, uint32_t box_rows,
+                                       uint32_t nblk) {
+    CUtensorMap m{};
+    cuuint64_t dims[3] = {32, rows, ld / 32};
+    cuuint64_t strides[2] = {ld * 4, 128};
+    cuuint32_t box[3] = {32, box_rows, nblk};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(f32 blocks) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 }  // namespace fipa_b200

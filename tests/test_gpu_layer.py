@@ -56,11 +56,14 @@ def test_stage_by_stage_main_shape(fipa, precision):
         d_gpu = s_gpu[:, :, valid] - s_gpu[:, :, valid][:, :, :1]
         d_ref = L2E * (elog[:, :, valid] - elog[:, :, valid][:, :, :1])
         assert rel_dev(d_ref, d_gpu) < (4e-3 if bf else 1e-6)
-        nv = ev.shape[-1] - 3
-        assert rel_dev(ev[..., :nv], vh[b, :, :, :nv]) < (8e-3 if bf else 1e-6)
-        t_sum = vh[b, :, :, nv:nv + 3] + vh[b, :, :, nv + 3:nv + 6]
-        assert rel_dev(ev[..., nv:], t_sum) < (1e-5 if bf else 1e-6)
-        assert np.all(vh[b, :, :, nv + 6:] == 0)
+        # v_hat = [v | z2 | t hi | t lo | R_j v_p | 0]   (pack.cu)
+        npair = MAIN["c"] + MAIN["rank"] * MAIN["d_z"]
+        npts = 3 * MAIN["n_value"]
+        assert rel_dev(ev[..., :npair], vh[b, :, :, :npair]) < (8e-3 if bf else 1e-6)
+        t_sum = vh[b, :, :, npair:npair + 3] + vh[b, :, :, npair + 3:npair + 6]
+        assert rel_dev(ev[..., -3:], t_sum) < (1e-5 if bf else 1e-6)
+        assert rel_dev(ev[..., npair:npair + npts], vh[b, :, :, npair + 6:npair + 6 + npts]) < (8e-3 if bf else 1e-6)
+        assert np.all(vh[b, :, :, npair + 6 + npts:] == 0)
         fin = np.isfinite(ecb)
         assert np.array_equal(fin, np.isfinite(cb[b]))
         assert rel_dev(ecb[fin], cb[b][fin]) < 1e-5
