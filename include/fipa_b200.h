@@ -45,14 +45,15 @@ extern "C" {
 #define FIPA_ERR_CUDA 4    /* CUDA runtime / launch failure, or no usable GPU         */
 #define FIPA_ERR_OTHER 9
 
-#define FIPA_PREC_BF16 0
-#define FIPA_PREC_F32 1
+#define FIPA_PREC_BF16 0 /* tcgen05 path: bf16 operands, fp32 accumulation; f64 master weights */
+#define FIPA_PREC_F32 1  /* fp32 SIMT path; master weights rounded to f32 (reference "f32")    */
+#define FIPA_PREC_F64 2  /* reference "f64" models: f64 master weights, fp32 SIMT compute     */
 
 /* Hyper-parameters (IpaConfig).  Names follow the reference: d_in = c_s, d_z = c_z,
  * c = c_hidden, n_query = qk-points, n_value = v-points, rank = z_factor_rank. */
 typedef struct fipa_config {
     uint64_t d_in, d_z, heads, c, n_query, n_value, rank;
-    int32_t precision;        /* FIPA_PREC_BF16 | FIPA_PREC_F32                       */
+    int32_t precision;        /* FIPA_PREC_BF16 | FIPA_PREC_F32 | FIPA_PREC_F64      */
     int32_t enforce_head_cap; /* reference default 1: max(qk_width, v_width) <= 256   */
 } fipa_config;
 

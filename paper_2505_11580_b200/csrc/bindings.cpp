@@ -47,7 +47,8 @@ void check(int rc) {
 
 int parse_precision(const std::string& name) {
     if (name == "bf16") return FIPA_PREC_BF16;
-    if (name == "f32" || name == "f64") return FIPA_PREC_F32;
+    if (name == "f32") return FIPA_PREC_F32;
+    if (name == "f64") return FIPA_PREC_F64;
     throw FipaValueError("unknown precision '" + name + "' (expected f32, f64 or bf16)");
 }
 

@@ -61,6 +61,9 @@ fipa_b200::Config to_cfg(const fipa_config* c) {
         cfg.precision = fipa_b200::Precision::bf16;
     } else if (c->precision == FIPA_PREC_F32) {
         cfg.precision = fipa_b200::Precision::f32;
+        cfg.weights_f32 = true;
+    } else if (c->precision == FIPA_PREC_F64) {
+        cfg.precision = fipa_b200::Precision::f32;  // no GPU f64 path: fp32 compute, f64 masters
     } else {
         throw fipa_b200::ValueError("unknown precision code " + std::to_string(c->precision));
     }
@@ -125,7 +128,7 @@ int fipa_layer_set_weights(fipa_layer* layer, const fipa_host_weights* w) {
         }
         hw.w_l = w->w_l;
         hw.w_c = w->w_c;
-        hw.stored_f32 = impl.config().precision == fipa_b200::Precision::f32;
+        hw.stored_f32 = impl.config().weights_f32;
         impl.set_weights(hw);
     });
 }

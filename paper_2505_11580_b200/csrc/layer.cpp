@@ -342,7 +342,7 @@ FlashIpaLayer::FlashIpaLayer(const Config& cfg) : cfg_(cfg) {
         device_ = 0;
         cudaGetLastError();
     }
-    w_ = fipa_b200::init_weights(cfg_, 0, cfg_.precision == Precision::f32);
+    w_ = fipa_b200::init_weights(cfg_, 0, cfg_.weights_f32);
     dirty_ = true;  // device copies are made lazily by the first forward
 }
 
@@ -367,7 +367,7 @@ void FlashIpaLayer::release_device() {
 }
 
 void FlashIpaLayer::init_weights(std::uint64_t seed) {
-    w_ = fipa_b200::init_weights(cfg_, seed, cfg_.precision == Precision::f32);
+    w_ = fipa_b200::init_weights(cfg_, seed, cfg_.weights_f32);
     dirty_ = true;
 }
 

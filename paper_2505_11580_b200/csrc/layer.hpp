@@ -41,7 +41,8 @@ enum class Precision { bf16 = 0, f32 = 1 };
 
 struct Config {
     std::size_t d_in = 32, d_z = 4, heads = 2, c = 8, n_query = 2, n_value = 2, rank = 2;
-    Precision precision = Precision::bf16;
+    Precision precision = Precision::bf16;  // compute path
+    bool weights_f32 = false;               // master weights stored at f32 (reference "f32" models)
     bool enforce_head_cap = true;
 
     std::size_t qk_width() const { return c + 5 * n_query + rank * d_z; }  // ipa.hpp:27
