@@ -424,3 +424,97 @@ def make_problem(cfg: IpaConfig, L: int, seed: int, translation_scale: float = 1
         u = rng._uniforms(L)
         mask = u >= mask_frac
     return Problem(s, z1, z2, rot, trans, mask)
+
+
+# ---------------------------------------------------------------------- backward
+def flash_ipa_backward(s, z1, z2, rot, trans, mask, cfg: IpaConfig, w, dout):
+    """Reverse-mode derivative of the layer, float64.
+
+    The reference has no backward (proj/SPEC.md:8, :80); this differentiates the quadratic
+    restatement of proj/src/ipa.cpp:244-310 (== flash_ipa_forward, proj/src/flash_ipa.cpp:141-218,
+    pinned by tests/test_oracle.py) by hand.  Rotations are treated as free 3x3 matrices, exactly
+    as the forward consumes them (geometry.cpp:63-76).  It is pinned against central finite
+    differences of the compiled reference forward (tests/test_oracle.py::test_backward_fd).
+    Returns a dict with the gradient of sum(out * dout) w.r.t. s, z1, z2, rot, trans and every
+    weight tensor (reference names).
+    """
+    L = s.shape[0]
+    H, c, Nq, Nv, r, dz = cfg.heads, cfg.c, cfg.n_query, cfg.n_value, cfg.rank, cfg.d_z
+    mask = np.ones(L, bool) if mask is None else np.asarray(mask, bool)
+    g = {n: np.zeros_like(np.asarray(w[n], np.float64)) for n in WEIGHT_NAMES}
+    g.update(s=np.zeros_like(s), z1=np.zeros_like(z1), z2=np.zeros_like(z2),
+             rot=np.zeros_like(rot), trans=np.zeros_like(trans))
+    if not mask.any():  # flash_ipa.cpp:156-159: constant zero output
+        return g
+    wl, wc = w["w_l"], w["w_c"]
+    z = np.einsum("ird,jrd->ijd", z1, z2)
+    q, k, v, qp, kp, vp = project_inputs(s, cfg, w)
+    R, t = rot[None, :, None], trans[None, :, None]
+    gq, gk, gv = apply(R, t, qp), apply(R, t, kp), apply(R, t, vp)
+    gamma = softplus(w["gamma_raw"])
+    diff = gq[:, :, None] - gk[:, None, :]  # [H, i, j, Nq, 3]
+    dist = (diff ** 2).sum((-1, -2))
+    bias = np.einsum("hd,ijd->hij", w["w_bias"], z)
+    logits = wl * (np.einsum("hic,hjc->hij", q, k) / math.sqrt(c) + bias
+                   - (0.5 * gamma * wc)[:, None, None] * dist)
+    logits = np.where(mask[None, None, :], logits, -np.inf)
+    attn = np.exp(logits - logits.max(-1, keepdims=True))
+    attn /= attn.sum(-1, keepdims=True)
+    agg_z = np.einsum("hij,ijd->hid", attn, z)
+    agg_v = np.einsum("hij,hjc->hic", attn, v)
+    agg_p = np.einsum("hij,hjpx->hipx", attn, gv)
+    y = agg_p - t
+    loc = np.einsum("iba,hipb->hipa", rot, y)
+    nrm = np.sqrt((loc ** 2).sum(-1))
+    blk = np.concatenate([agg_z, agg_v, loc.reshape(H, L, -1), nrm], -1)
+    feat = blk.transpose(1, 0, 2).reshape(L, -1)
+
+    dout_m = np.where(mask[:, None], dout, 0.0)  # flash_ipa.cpp:213-216
+    g["b_out"] = dout_m.sum(0)
+    g["w_out"] = feat.T @ dout_m
+    dblk = (dout_m @ w["w_out"].T).reshape(L, H, cfg.seg()).transpose(1, 0, 2)
+    d_aggz = dblk[..., :dz]
+    d_aggv = dblk[..., dz:dz + c]
+    d_loc = dblk[..., dz + c:dz + c + 3 * Nv].reshape(H, L, Nv, 3).copy()
+    d_nrm = dblk[..., dz + c + 3 * Nv:]
+    safe = np.where(nrm > 0, nrm, 1.0)
+    d_loc += np.where(nrm > 0, d_nrm / safe, 0.0)[..., None] * loc
+    d_aggp = np.einsum("iab,hipb->hipa", rot, d_loc)
+    g["trans"] -= d_aggp.sum((0, 2))
+    g["rot"] += np.einsum("hipb,hipa->iba", y, d_loc)
+
+    d_attn = (np.einsum("hid,ijd->hij", d_aggz, z) + np.einsum("hic,hjc->hij", d_aggv, v)
+              + np.einsum("hipx,hjpx->hij", d_aggp, gv))
+    dzz = np.einsum("hij,hid->ijd", attn, d_aggz)
+    dv = np.einsum("hij,hic->hjc", attn, d_aggv)
+    dgv = np.einsum("hij,hipx->hjpx", attn, d_aggp)
+    dlog = attn * (d_attn - (attn * d_attn).sum(-1, keepdims=True))
+
+    dq = wl / math.sqrt(c) * np.einsum("hij,hjc->hic", dlog, k)
+    dk = wl / math.sqrt(c) * np.einsum("hij,hic->hjc", dlog, q)
+    dbias = wl * dlog
+    g["w_bias"] = np.einsum("hij,ijd->hd", dbias, z)
+    dzz += np.einsum("hij,hd->ijd", dbias, w["w_bias"])
+    ddist = -0.5 * wl * wc * gamma[:, None, None] * dlog
+    dgamma = -0.5 * wl * wc * (dlog * dist).sum((1, 2))
+    g["gamma_raw"] = dgamma / (1.0 + np.exp(-np.asarray(w["gamma_raw"], np.float64)))
+    dgq = 2.0 * np.einsum("hij,hijpx->hipx", ddist, diff)
+    dgk = -2.0 * np.einsum("hij,hijpx->hjpx", ddist, diff)
+
+    g["z1"] = np.einsum("ijd,jrd->ird", dzz, z2)
+    g["z2"] = np.einsum("ijd,ird->jrd", dzz, z1)
+    dpts = []
+    for dgx, x in ((dgq, qp), (dgk, kp), (dgv, vp)):
+        g["trans"] += dgx.sum((0, 2))
+        g["rot"] += np.einsum("hipa,hipb->iab", dgx, x)
+        dpts.append(np.einsum("iab,hipa->hipb", rot, dgx))
+
+    def flat(x):  # [H, L, ...] -> [L, H*...] (inverse of _head_major)
+        return x.reshape(H, L, -1).transpose(1, 0, 2).reshape(L, -1)
+
+    for name, dx in (("w_q", dq), ("w_k", dk), ("w_v", dv), ("w_qp", dpts[0]), ("w_kp", dpts[1]),
+                     ("w_vp", dpts[2])):
+        f = flat(dx)
+        g[name] = s.T @ f
+        g["s"] += f @ w[name].T
+    return g

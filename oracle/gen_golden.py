@@ -79,7 +79,49 @@ def main():
                 wf = ref.init_weights(cf, 7)
                 rec[f"{tag}/flash_f32"] = ref.flash_forward(cf, wf, p.s, p.z1, p.z2, p.rot, p.trans, p.mask)
         np.savez_compressed(os.path.join(OUT, f"forward_{name}.npz"), **rec)
+
+    # Backward: the reference has no autodiff (proj/SPEC.md:8), so its gradient is pinned by
+    # central finite differences of the reference's own flash_ipa_forward (f64).
+    np.savez_compressed(os.path.join(OUT, "backward_fd.npz"), **backward_fd_fixture())
     print("golden fixtures written to", OUT)
+
+
+FD_SHAPE = dict(d_in=12, d_z=3, heads=2, c=4, n_query=2, n_value=3, rank=2)
+FD_EPS = 1e-6
+
+
+def backward_fd_fixture():
+    cfg = cfg_of(FD_SHAPE)
+    w = ref.init_weights(cfg, 3)
+    rng = np.random.default_rng(0)
+    w["b_out"] = rng.standard_normal(w["b_out"].shape)
+    w["gamma_raw"] = np.array([0.3, -0.7])
+    L = 7
+    p = make_problem(cfg, L, seed=11, translation_scale=2.0)
+    mask = np.ones(L, bool)
+    mask[2] = False
+    dout = rng.standard_normal((L, cfg.d_in))
+    inputs = dict(s=p.s, z1=p.z1, z2=p.z2, rot=p.rot, trans=p.trans)
+    rec = {f"in/{k}": v for k, v in inputs.items()}
+    rec["in/mask"], rec["in/dout"] = mask, dout
+    rec.update({f"w/{n}": w[n] for n in WEIGHT_NAMES})
+
+    def loss(name, x):
+        a, ww = dict(inputs), dict(w)
+        (a if name in a else ww)[name] = x
+        out = ref.flash_forward(cfg, ww, a["s"], a["z1"], a["z2"], a["rot"], a["trans"], mask)
+        return float((out * dout).sum())
+
+    for name in list(inputs) + list(WEIGHT_NAMES):
+        x = np.array(inputs[name] if name in inputs else w[name], dtype=np.float64)
+        fd = np.zeros_like(x)
+        for idx in np.ndindex(x.shape):
+            xp, xm = x.copy(), x.copy()
+            xp[idx] += FD_EPS
+            xm[idx] -= FD_EPS
+            fd[idx] = (loss(name, xp) - loss(name, xm)) / (2 * FD_EPS)
+        rec[f"grad/{name}"] = fd
+    return rec
 
 
 if __name__ == "__main__":

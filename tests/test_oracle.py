@@ -130,3 +130,34 @@ def test_live_reference_cross_check():
     a = ref.flash_forward(cfg, w, p.s, p.z1, p.z2, p.rot, p.trans, p.mask, tile_rows=7, tile_cols=5, threads=3)
     b = fo.flash_ipa_forward(p.s, p.z1, p.z2, p.rot, p.trans, p.mask, cfg, fo.init_weights(cfg, 21))
     assert fo.rel_dev(a, b) < 1e-12
+
+
+def test_backward_matches_reference_finite_differences():
+    """The float64 backward restatement (fipa_oracle.flash_ipa_backward) against central finite
+    differences of the reference's own flash_ipa_forward (fixture from oracle/gen_golden.py),
+    with a masked residue, non-unit gamma and a nonzero output bias."""
+    g = np.load(os.path.join(GOLD, "backward_fd.npz"))
+    from oracle.gen_golden import FD_SHAPE
+
+    cfg = fo.IpaConfig(**FD_SHAPE, enforce_head_cap=False)
+    w = {n: g[f"w/{n}"] for n in fo.WEIGHT_NAMES}
+    w["w_l"] = np.sqrt(1.0 / 3.0)
+    w["w_c"] = np.sqrt(2.0 / (9.0 * cfg.n_query))
+    ins = {k: g[f"in/{k}"] for k in ("s", "z1", "z2", "rot", "trans")}
+    got = fo.flash_ipa_backward(ins["s"], ins["z1"], ins["z2"], ins["rot"], ins["trans"],
+                                g["in/mask"], cfg, w, g["in/dout"])
+    for name in list(ins) + list(fo.WEIGHT_NAMES):
+        assert fo.rel_dev(g[f"grad/{name}"], got[name]) < 1e-7, name
+    # masked residue: no gradient reaches its inputs
+    m = ~g["in/mask"].astype(bool)
+    for name in ("s", "z1", "z2", "rot", "trans"):
+        assert np.abs(got[name][m]).max() < 1e-12, name
+
+
+def test_backward_all_masked_is_zero():
+    cfg = cfg_of("tiny")
+    w = fo.init_weights(cfg, 1)
+    p = fo.make_problem(cfg, 5, 3)
+    got = fo.flash_ipa_backward(p.s, p.z1, p.z2, p.rot, p.trans, np.zeros(5, bool), cfg, w,
+                                np.ones((5, cfg.d_in)))
+    assert all(np.abs(v).max() == 0 for v in got.values())
