@@ -17,6 +17,10 @@
  *   fipa_layer_forward_host (host f64)   Model.flash                python/bindings.cpp:122-135
  *   fipa_last_error + status codes       ValueError / NumericError / IoError
  *                                                                   include/fipa/error.hpp:10-28
+ *   fipa_layer_forward_train /           no reference counterpart: the reference is inference-only
+ *   fipa_layer_backward / _grad_host     (proj/SPEC.md:8); the gradient of flash_ipa_forward
+ *                                        (src/flash_ipa.cpp:141-218), checked against finite
+ *                                        differences of the reference (tests/test_oracle.py)
  *
  * Differences from the reference, all additive: a leading batch axis B (each sample is an
  * independent reference call with its own mask), caller-owned device buffers + a CUDA stream,
@@ -111,6 +115,39 @@ int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L, const doubl
  * {n_proj, dqk_pad, dv_pad, H*seg}.  Returns the number of offsets written (9). */
 int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
                                 int64_t* dims);
+
+/* ---------------------------------------------------------------------------- training
+ * Training forward: identical outputs to fipa_layer_forward, but over a workspace of
+ * fipa_layer_train_workspace_size bytes in which it keeps what fipa_layer_backward needs (the
+ * normalised attention output).  FIPA_PREC_BF16 only (tcgen05 path); lifted widths <= 448. */
+size_t fipa_layer_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L);
+int fipa_layer_forward_train(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                             const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                             float* out, void* workspace, size_t workspace_bytes, void* stream);
+/* Total number of weight scalars (w_q .. b_out in reference order). */
+uint64_t fipa_layer_num_weights(const fipa_layer* layer);
+/* Backward of the last fipa_layer_forward_train on the same workspace and inputs: gradients of
+ * sum(out * dout) (device float32, same shapes as the inputs): ds [B,L,d_in], dz1/dz2
+ * [B,L,rank,d_z], drot [B,L,3,3] and dtrans [B,L,3] (either may be NULL), dweights
+ * [fipa_layer_num_weights] = w_q|w_k|w_v|w_qp|w_kp|w_vp|w_bias|gamma_raw|w_out|b_out flattened
+ * row-major.  Masked residues receive zero gradients. */
+int fipa_layer_backward(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                        const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                        const float* dout, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                        float* dweights, void* workspace, size_t workspace_bytes, void* stream);
+/* Forward + backward over HOST float64 buffers (copies in, runs, copies out, synchronises).
+ * Any gradient output may be NULL. */
+int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L, const double* s, const double* z1,
+                         const double* z2, const double* rot, const double* trans, const uint8_t* mask,
+                         const double* dout, double* out, double* ds, double* dz1, double* dz2,
+                         double* drot, double* dtrans, double* dweights);
+/* Byte offsets of the training intermediates in a train workspace, -1 when absent:
+ *   0 o_hat (bf16 [B*H,L,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
+ *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B*H,L,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
+ *   7 dfeat (f32 [B*L,feat_ld]).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.  Returns 8. */
+int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
+                                      int64_t* dims);
+int fipa_layer_backward_launches(const fipa_layer* layer);
 
 /* Number of kernels fipa_layer_forward launches per call for this configuration. */
 int fipa_layer_forward_launches(const fipa_layer* layer);

@@ -1,0 +1,507 @@
+// FlashIPA attention backward on tcgen05 (the reference has no backward -- proj/SPEC.md:8 --
+// so this differentiates its forward, proj/src/attention_kernel.cpp:112-188, against the oracle
+// backward in oracle/fipa_oracle.py, itself pinned by finite differences of the reference).
+//
+// With S = Q_hat K_hat^T in log2 units (pack.cu), P = 2^(S - lse2) (lse saved by the forward),
+// dO_hat and D = rowsum(dO_hat * O_hat) from bwd_prep (bwd.cu):
+//   dP = dO_hat V_hat^T,  dS = P * (dP - D)            (natural-logit gradient)
+//   dV_acc = P^T dO_hat,  dK_acc = dS^T Q_hat,  dQ_acc = dS K_hat
+// The lifted head width (432 columns for the north-star shape) is the constraint that shapes the
+// design: one accumulator of 128 rows x 432 fp32 fills 432 of a CTA's 512 TMEM columns, so
+// dK and dV of the same keys cannot share an SM, and a 128 x 448 bf16 stationary tile fills half
+// of the shared memory.  Each kernel therefore runs a CLUSTER OF FOUR: two tcgen05 CTA pairs
+// (cta_group::2, M = 256 rows) over the same 256 rows of one (sample, head):
+//   "P pair"  (ranks 0,1): X = A_stat . B1_j^T into TMEM, P = 2^(X - lse2) (bf16),
+//                          optional acc += P . B2_j, and P streamed to the peer pair's shared
+//                          memory with st.async (DSMEM, completion counted on its mbarrier);
+//   "dS pair" (ranks 2,3): X = A_stat . B1_j^T -> dP, dS = P (dP - D) written over the received P
+//                          in place, acc += dS . B2_j; the MMA commit that retires dS releases
+//                          the P pair's next send (multicast tcgen05.commit).
+// KV kernel (rows = keys, tile columns = 64 queries):
+//   P pair : A_stat = K_hat, B1 = Q_hat tiles, B2 = dO_hat slices -> acc = dV_acc
+//   dS pair: A_stat = V_hat, B1 = dO_hat tiles, B2 = Q_hat slices -> acc = dK_acc
+// Q kernel (rows = queries, tile columns = 64 keys):
+//   P pair : A_stat = Q_hat, B1 = K_hat tiles (no second MMA)
+//   dS pair: A_stat = dO_hat, B1 = V_hat tiles, B2 = K_hat slices -> acc = dQ_acc
+// Per-query vectors (lse, D) are per tile column in the KV kernel and per row in the Q kernel.
+// The ring structure (whole 32-row B1 tiles, 32-row B2 slices split over the pair) is the
+// forward's (attn_fwd_2sm.cu); MMA1 writes TMEM columns [448,512), the accumulator [0,n2).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+#include "tma_host.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+constexpr int BM = 128;       // rows per CTA (256 per pair)
+constexpr int BN = 64;        // tile columns
+constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
+constexpr int kStages1 = 2;
+constexpr int kStages2 = 2;
+constexpr int kSlice = 32;
+constexpr int kSliceBox = kSlice * 128;
+constexpr uint32_t kXCol = 448;
+constexpr float kL2E = 1.4426950408889634f;
+
+struct RoleDims {
+    int k1;        // MMA1 K extent (multiple of 16)
+    int nb1;       // 64-wide blocks of the stationary tile / B1 tiles
+    int n2;        // MMA2 N extent (accumulator columns), 0 = no second MMA
+    int n2a, n2b;  // split into N <= 256 MMAs
+    int nba, nbb;  // per-CTA 64-wide TMA boxes of each half of a B2 slice
+};
+
+struct BwdParams {
+    int L;
+    RoleDims role[2];  // 0 = P pair, 1 = dS pair
+    int stat_bytes, b1_stage, b2_stage;
+    const float* lse;  // [BH, L] natural-log LSE of the forward
+    const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
+    float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
+    int acc_ld;
+};
+
+struct Bars {
+    uint64_t stat_full;
+    uint64_t b1_full[kStages1], b1_empty[kStages1];
+    uint64_t b2_full[kStages2], b2_empty[kStages2];
+    uint64_t x_full, x_free, a_full, mma2_done, acc_full, pin_full, pin_free;
+    uint32_t tmem_slot;
+};
+
+struct Layout {
+    int stat, abuf, b1, b2, bars, total;
+};
+__host__ __device__ inline Layout smem_layout(const BwdParams& p) {
+    Layout l{};
+    l.stat = 0;
+    l.abuf = p.stat_bytes;
+    l.b1 = l.abuf + BM * 128;
+    l.b2 = l.b1 + kStages1 * p.b1_stage;
+    l.bars = l.b2 + kStages2 * p.b2_stage;
+    l.total = l.bars + static_cast<int>(sizeof(Bars));
+    return l;
+}
+
+__device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// 32 consecutive per-query floats starting at q (entries >= L come back as `fill`).
+__device__ __forceinline__ void load_vec32(const float* base, int q, int L, float fill, float* out) {
+    if (q + 32 <= L && (q & 3) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(base + q) + k);
+            out[4 * k] = f.x;
+            out[4 * k + 1] = f.y;
+            out[4 * k + 2] = f.z;
+            out[4 * k + 3] = f.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) out[k] = q + k < L ? __ldg(base + q + k) : fill;
+    }
+}
+
+template <bool KV>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
+                    const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
+                    const __grid_constant__ CUtensorMap b1D, const __grid_constant__ CUtensorMap b2D,
+                    BwdParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const Layout lay = smem_layout(p);
+    uint8_t* sStat = smem + lay.stat;
+    uint8_t* sA = smem + lay.abuf;
+    uint8_t* sB1 = smem + lay.b1;
+    uint8_t* sB2 = smem + lay.b2;
+    Bars* bars = reinterpret_cast<Bars*>(smem + lay.bars);
+
+    const int warp = ptx::warp_id();
+    const int lane = ptx::lane_id();
+    const uint32_t crank = ptx::cluster_ctarank();  // 0..3
+    const int role = static_cast<int>(crank >> 1);  // 0 = P pair, 1 = dS pair
+    const uint32_t prank = crank & 1u;              // rank within the pair
+    const bool leader = prank == 0;
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (crank & 2u));
+    const RoleDims rd = p.role[role];
+    const int bh = blockIdx.y;
+    const int r0 = (blockIdx.x >> 2) * 256 + static_cast<int>(prank) * BM;  // first row of this CTA
+    const int ntiles = (p.L + BN - 1) / BN;
+    const bool has_mma2 = rd.n2 > 0;
+    const CUtensorMap* mStat = role ? &statD : &statP;
+    const CUtensorMap* mB1 = role ? &b1D : &b1P;
+    const CUtensorMap* mB2 = role ? &b2D : &b2P;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(mStat);
+        ptx::tma_prefetch(mB1);
+        if (has_mma2) ptx::tma_prefetch(mB2);
+        ptx::mbar_init(&bars->stat_full, 1);
+        for (int s = 0; s < kStages1; ++s) {
+            ptx::mbar_init(&bars->b1_full[s], 1);
+            ptx::mbar_init(&bars->b1_empty[s], 1);
+        }
+        for (int s = 0; s < kStages2; ++s) {
+            ptx::mbar_init(&bars->b2_full[s], 1);
+            ptx::mbar_init(&bars->b2_empty[s], 1);
+        }
+        ptx::mbar_init(&bars->x_full, 1);
+        ptx::mbar_init(&bars->x_free, 16);
+        ptx::mbar_init(&bars->a_full, 16);
+        ptx::mbar_init(&bars->mma2_done, 1);
+        ptx::mbar_init(&bars->acc_full, 1);
+        ptx::mbar_init(&bars->pin_full, 1);
+        ptx::mbar_init(&bars->pin_free, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm(&bars->tmem_slot, 512);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_slot, 0);
+
+    if (warp == 0) {
+        // ------------------------------------------- stationary tile + B1 tile producer
+        if (lane == 0) {
+            if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
+            ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
+            const int stage = rd.nb1 * 32 * 128;
+            for (int j = 0; j < ntiles; ++j) {
+                const int s = j % kStages1;
+                if (j >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((j / kStages1) - 1) & 1);
+                if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
+                ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
+                                     j * BN + 32 * static_cast<int>(prank), 0, bh);
+            }
+        }
+    } else if (warp == 10) {
+        // ------------------------------------------------------------ B2 slice producer
+        if (lane == 0 && has_mma2) {
+            const int halfa = rd.n2a / 2, halfb = rd.n2b / 2;
+            const int stage_bytes = (rd.nba + rd.nbb) * kSliceBox;
+            const int nslices = ntiles * (BN / kSlice);
+            for (int n = 0; n < nslices; ++n) {
+                const int s = n % kStages2;
+                if (n >= kStages2) ptx::mbar_wait(&bars->b2_empty[s], ((n / kStages2) - 1) & 1);
+                if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
+                uint8_t* dst = sB2 + s * p.b2_stage;
+                const int row = n * kSlice;
+                for (int x = 0; x < rd.nba; ++x)
+                    ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s],
+                                         halfa * static_cast<int>(prank) + 64 * x, row, bh);
+                for (int x = 0; x < rd.nbb; ++x)
+                    ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
+                                         rd.n2a + halfb * static_cast<int>(prank) + 64 * x, row, bh);
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------- MMA issue (pair leaders)
+        if (leader) {
+            const uint32_t idesc1 = ptx::idesc_bf16(256, BN, false, false);
+            const uint32_t idesc2a = ptx::idesc_bf16(256, rd.n2a > 0 ? rd.n2a : 16, false, true);
+            const uint32_t idesc2b = ptx::idesc_bf16(256, rd.n2b > 0 ? rd.n2b : 16, false, true);
+            const uint32_t stat_base = ptx::smem_u32(sStat);
+            const uint32_t a_base = ptx::smem_u32(sA);
+            const uint32_t b1_base = ptx::smem_u32(sB1);
+            const uint32_t b2_base = ptx::smem_u32(sB2);
+            const int k1_steps = rd.k1 / 16;
+            ptx::mbar_wait(&bars->stat_full, 0);
+            for (int j = 0; j <= ntiles; ++j) {
+                if (j < ntiles) {
+                    if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
+                    const int s = j % kStages1;
+                    ptx::mbar_wait(&bars->b1_full[s], (j / kStages1) & 1);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t bb = b1_base + s * p.b1_stage;
+                        for (int kk = 0; kk < k1_steps; ++kk) {
+                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
+                            const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
+                            const uint64_t db = ptx::sw128_desc(bb + blk * (32 * 128) + sub, 16, 1024);
+                            ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
+                        }
+                        ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
+                        ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                    }
+                    __syncwarp();
+                }
+                if (j > 0 && has_mma2) {
+                    const int jj = j - 1;
+                    ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
+                    for (int h2 = 0; h2 < BN / kSlice; ++h2) {
+                        const int n = jj * (BN / kSlice) + h2;
+                        const int s = n % kStages2;
+                        ptx::mbar_wait(&bars->b2_full[s], (n / kStages2) & 1);
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            for (int kk = 0; kk < kSlice / 16; ++kk) {
+                                const uint64_t da = ptx::sw128_desc(a_base + (2 * h2 + kk) * 32, 16, 1024);
+                                const uint32_t vb = b2_base + s * p.b2_stage + kk * 2048;
+                                const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
+                                ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kSliceBox, 1024), idesc2a, acc);
+                                if (rd.n2b > 0)
+                                    ptx::mma2_ss(tmem + rd.n2a, da,
+                                                 ptx::sw128_desc(vb + rd.nba * kSliceBox, kSliceBox, 1024),
+                                                 idesc2b, acc);
+                            }
+                            ptx::mma_commit_2sm(&bars->b2_empty[s], pair_mask);
+                        }
+                        __syncwarp();
+                    }
+                    if (ptx::elect_one()) {
+                        // P pair: its P buffer is free again.  dS pair: the received-P buffer
+                        // is free -> the P pair may send the next tile.
+                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done, pair_mask);
+                        else ptx::mma_commit_2sm(&bars->pin_free, 0x3);
+                        if (j == ntiles) ptx::mma_commit_2sm(&bars->acc_full, pair_mask);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------- elementwise
+        const int sw = warp - 2;
+        const int quad = warp & 3;
+        const int half = sw >> 2;
+        const int row = quad * 32 + lane;
+        const uint32_t tl = tmem + (uint32_t(quad * 32) << 16);
+        const uint32_t leader_rank = crank & 2u;
+        const uint32_t x_free_remote = ptx::mapa(&bars->x_free, leader_rank);
+        const uint32_t a_full_remote = ptx::mapa(&bars->a_full, leader_rank);
+        const int64_t vec_base = static_cast<int64_t>(bh) * p.L;
+        const int grow = r0 + row;  // global row (key in KV, query in Q)
+        // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.
+        float row_v = 0.f;
+        if (!KV && grow < p.L) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
+                                                 : __ldg(p.Dvec + vec_base + grow);
+        uint8_t* arow = sA + row * 128;
+        const uint32_t peer_rank = crank + 2u;  // P pair -> dS pair partner
+        const uint32_t peer_row = ptx::mapa(arow, role == 0 ? peer_rank : crank);
+        const uint32_t peer_bar = ptx::mapa(&bars->pin_full, role == 0 ? peer_rank : crank);
+
+        for (int j = 0; j < ntiles; ++j) {
+            const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
+            if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full, BM * 128);
+            // per-column vector (KV kernel)
+            float cv[32];
+            if (KV) {
+                if (role == 0) {
+                    load_vec32(p.lse + vec_base, c0, p.L, INFINITY, cv);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) cv[k] *= kL2E;
+                } else {
+                    load_vec32(p.Dvec + vec_base, c0, p.L, 0.f, cv);
+                }
+            }
+            ptx::mbar_wait(&bars->x_full, j & 1);
+            ptx::tc_fence_after();
+            uint32_t xr[32];
+            ptx::tmem_ld32(tl + kXCol + 32 * half, xr);
+            ptx::tmem_wait_ld();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(x_free_remote);
+
+            uint32_t pk[16];
+            if (role == 0) {
+                // P = 2^(X - lse2), zero past the sequence end (padding rows of K/Q tiles)
+#pragma unroll
+                for (int cc = 0; cc < 16; ++cc) {
+                    float pv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int k = 2 * cc + u;
+                        const float x = __uint_as_float(xr[k]);
+                        if (KV) {
+                            pv[u] = ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
+                        } else {
+                            pv[u] = c0 + k < p.L ? ptx::ex2(x - row_v) : 0.f;
+                        }
+                    }
+                    pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);
+                }
+                if (has_mma2) {
+                    if (j > 0) {
+                        ptx::mbar_wait(&bars->mma2_done, (j - 1) & 1);
+                        ptx::tc_fence_after();
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int chunk = 4 * half + k;
+                        *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
+                            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                }
+                // stream P to the dS pair once it has retired the previous tile's dS
+                if (j > 0) ptx::mbar_wait_cluster(&bars->pin_free, (j - 1) & 1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = 4 * half + k;
+                    st_async_v4(peer_row + ((chunk ^ (row & 7)) << 4),
+                                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), peer_bar);
+                }
+            } else {
+                ptx::mbar_wait_cluster(&bars->pin_full, j & 1);
+                uint4 pin[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = 4 * half + k;
+                    pin[k] = *reinterpret_cast<const uint4*>(arow + ((chunk ^ (row & 7)) << 4));
+                }
+                const uint32_t* pw = reinterpret_cast<const uint32_t*>(pin);
+#pragma unroll
+                for (int cc = 0; cc < 16; ++cc) {
+                    const float d0 = KV ? cv[2 * cc] : row_v;
+                    const float d1 = KV ? cv[2 * cc + 1] : row_v;
+                    const float s0 = bf_lo(pw[cc]) * (__uint_as_float(xr[2 * cc]) - d0);
+                    const float s1 = bf_hi(pw[cc]) * (__uint_as_float(xr[2 * cc + 1]) - d1);
+                    pk[cc] = ptx::pack_bf16x2(s0, s1);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = 4 * half + k;
+                    *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
+                        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+            }
+        }
+
+        // ------------------------------------------------------------- epilogue
+        float* out = p.acc_out[role];
+        if (has_mma2 && out != nullptr) {
+            ptx::mbar_wait(&bars->acc_full, 0);
+            ptx::tc_fence_after();
+            const int n16 = rd.n2 / 16;
+            const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
+            float* orow = out + (vec_base + (grow < p.L ? grow : 0)) * p.acc_ld;
+            for (int ch = lo; ch < hi; ++ch) {
+                uint32_t o[16];
+                ptx::tmem_ld16(tl + 16 * ch, o);
+                ptx::tmem_wait_ld();
+                if (grow < p.L) {
+                    float4* dst = reinterpret_cast<float4*>(orow + 16 * ch);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        dst[q] = make_float4(__uint_as_float(o[4 * q]), __uint_as_float(o[4 * q + 1]),
+                                             __uint_as_float(o[4 * q + 2]), __uint_as_float(o[4 * q + 3]));
+                }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) ptx::tmem_dealloc_2sm(tmem, 512);
+}
+
+RoleDims make_role(int k1, int n2) {
+    RoleDims r{};
+    r.k1 = k1;
+    r.nb1 = (k1 + 63) / 64;
+    r.n2 = n2;
+    r.n2a = std::min(n2, 256);
+    r.n2b = n2 - r.n2a;
+    r.nba = (r.n2a / 2 + 63) / 64;
+    r.nbb = (r.n2b / 2 + 63) / 64;
+    return r;
+}
+
+void finish_params(BwdParams& p) {
+    int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
+    int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
+    p.stat_bytes = nb1 * BM * 128;
+    p.b1_stage = nb1 * 32 * 128;
+    p.b2_stage = std::max(nb2, 1) * kSliceBox;
+}
+
+template <bool KV>
+void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
+            cudaStream_t stream) {
+    const Layout lay = smem_layout(p);
+    const int smem = lay.total + 1024;
+    if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
+    auto kern = attn_bwd_kernel<KV>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int clusters = (a.L + 255) / 256;
+    dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
+    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
+}
+
+}  // namespace
+
+bool attn_bwd_supported(const LayerDims& d) {
+    if (d.dqk_mma > 448 || d.dv_mma > 448 || d.dqk_pad % 64 || d.dv_pad % 64) return false;
+    BwdParams p{};
+    p.role[0] = make_role(d.dqk_mma, d.dv_mma);
+    p.role[1] = make_role(d.dv_mma, d.dqk_mma);
+    finish_params(p);
+    return smem_layout(p).total + 1024 <= 232448;
+}
+
+void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream) {
+    if (!attn_bwd_supported(d)) throw std::invalid_argument("tcgen05 attention backward: unsupported widths");
+    const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
+    const int nqk = (d.dqk_mma + 63) / 64, nv = (d.dv_mma + 63) / 64;
+    auto ld_of = [&](const void* x) { return (x == a.vhat || x == a.dohat) ? d.dv_pad : d.dqk_pad; };
+    auto stat = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), BM, nb); };
+    auto tile = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), 32, nb); };
+    auto slice = [&](const void* x) { return make_map_3d_bf16(x, ld_of(x), a.L, BH, ld_of(x), 64, kSlice); };
+    {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
+        BwdParams p{};
+        p.L = a.L;
+        p.role[0] = make_role(d.dqk_mma, d.dv_mma);
+        p.role[1] = make_role(d.dv_mma, d.dqk_mma);
+        finish_params(p);
+        p.lse = a.lse;
+        p.Dvec = a.Dvec;
+        p.acc_out[0] = a.dv_acc;
+        p.acc_out[1] = a.dk_acc;
+        p.acc_ld = a.acc_ld;
+        const CUtensorMap maps[6] = {stat(a.khat, nqk), tile(a.qhat, nqk), slice(a.dohat),
+                                     stat(a.vhat, nv),  tile(a.dohat, nv), slice(a.qhat)};
+        launch<true>(d, a, p, maps, stream);
+    }
+    {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
+        BwdParams p{};
+        p.L = a.L;
+        p.role[0] = make_role(d.dqk_mma, 0);
+        p.role[1] = make_role(d.dv_mma, d.dqk_mma);
+        finish_params(p);
+        p.lse = a.lse;
+        p.Dvec = a.Dvec;
+        p.acc_out[0] = nullptr;
+        p.acc_out[1] = a.dq_acc;
+        p.acc_ld = a.acc_ld;
+        const CUtensorMap maps[6] = {stat(a.qhat, nqk), tile(a.khat, nqk), slice(a.khat),
+                                     stat(a.dohat, nv), tile(a.vhat, nv),  slice(a.khat)};
+        launch<false>(d, a, p, maps, stream);
+    }
+}
+
+}  // namespace fipa_b200

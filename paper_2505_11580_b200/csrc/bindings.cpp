@@ -208,6 +208,99 @@ public:
     }
 
     int forward_launches() const { return fipa_layer_forward_launches(layer_); }
+    int backward_launches() const { return fipa_layer_backward_launches(layer_); }
+    size_t train_workspace_size(int64_t B, int64_t L) const { return fipa_layer_train_workspace_size(layer_, B, L); }
+    uint64_t num_weights() const { return fipa_layer_num_weights(layer_); }
+    void forward_train_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                              uintptr_t trans, uintptr_t mask, uintptr_t out, uintptr_t ws, size_t ws_bytes,
+                              uintptr_t stream) {
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_forward_train(layer_, B, L, reinterpret_cast<const float*>(s),
+                                          reinterpret_cast<const float*>(z1), reinterpret_cast<const float*>(z2),
+                                          reinterpret_cast<const float*>(rot), reinterpret_cast<const float*>(trans),
+                                          reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(out),
+                                          reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    void backward_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                         uintptr_t trans, uintptr_t mask, uintptr_t dout, uintptr_t ds, uintptr_t dz1,
+                         uintptr_t dz2, uintptr_t drot, uintptr_t dtrans, uintptr_t dweights, uintptr_t ws,
+                         size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_backward(layer_, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                     reinterpret_cast<const uint8_t*>(mask), f(dout), f(ds), f(dz1), f(dz2),
+                                     f(drot), f(dtrans), f(dweights), reinterpret_cast<void*>(ws), ws_bytes,
+                                     reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    py::tuple train_workspace_layout(int64_t B, int64_t L) const {
+        int64_t off[8], dims[3];
+        if (fipa_layer_train_workspace_layout(layer_, B, L, off, dims) != 8) throw FipaValueError("invalid batch shape");
+        return py::make_tuple(std::vector<int64_t>(off, off + 8), std::vector<int64_t>(dims, dims + 3));
+    }
+    // flash_grad(s, z1, z2, rotations, translations, dout, mask=None) -> (out, grads)
+    // Forward + backward of sum(out * dout) through the host-buffer C ABI; grads is a dict with
+    // s, z1, z2, rotations, translations and every weight tensor (reference names).
+    py::tuple flash_grad(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
+                         const DArr& translations, const DArr& dout, const py::object& mask) {
+        const bool batched = s.ndim() == 3;
+        if (s.ndim() != 2 && s.ndim() != 3)
+            throw FipaValueError("single representation must be [L, d_in] or [B, L, d_in]");
+        const int64_t B = batched ? s.shape(0) : 1;
+        const int64_t L = batched ? s.shape(1) : s.shape(0);
+        if (dout.size() != s.size()) throw FipaValueError("dout must have the output's shape");
+        if (z1.size() != B * L * int64_t(cfg_.rank * cfg_.d_z) || z2.size() != z1.size() ||
+            rotations.size() != B * L * 9 || translations.size() != B * L * 3 ||
+            s.size() != B * L * int64_t(cfg_.d_in))
+            throw FipaValueError("input shapes disagree with the configuration");
+        std::vector<uint8_t> m;
+        const uint8_t* mp = nullptr;
+        if (!mask.is_none()) {
+            py::array_t<uint8_t, py::array::c_style | py::array::forcecast> ma(mask);
+            if (ma.size() != B * L) throw FipaValueError("mask length must equal L");
+            m.assign(ma.data(), ma.data() + ma.size());
+            for (auto& v : m) v = v ? 1 : 0;
+            mp = m.data();
+        }
+        auto like = [](const DArr& a) {
+            return py::array_t<double>(std::vector<py::ssize_t>(a.shape(), a.shape() + a.ndim()));
+        };
+        py::array_t<double> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
+                            gt = like(translations);
+        const uint64_t nw = fipa_layer_num_weights(layer_);
+        std::vector<double> gw(nw);
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_grad_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                      translations.data(), mp, dout.data(), out.mutable_data(), gs.mutable_data(),
+                                      gz1.mutable_data(), gz2.mutable_data(), gr.mutable_data(), gt.mutable_data(),
+                                      gw.data());
+        }
+        check(rc);
+        py::dict g;
+        g["s"] = gs;
+        g["z1"] = gz1;
+        g["z2"] = gz2;
+        g["rotations"] = gr;
+        g["translations"] = gt;
+        const auto sh = shapes();
+        size_t o = 0;
+        for (int i = 0; i < 10; ++i) {
+            py::array_t<double> a(std::vector<py::ssize_t>(sh[i].begin(), sh[i].end()));
+            std::copy(gw.begin() + o, gw.begin() + o + a.size(), a.mutable_data());
+            o += a.size();
+            g[kNames[i]] = a;
+        }
+        return py::make_tuple(out, g);
+    }
     void set_timing(bool on) { check(fipa_layer_set_timing(layer_, on ? 1 : 0)); }
     std::vector<float> stage_times() const {
         std::vector<float> t(16);
@@ -265,6 +358,20 @@ PYBIND11_MODULE(_fipa_b200, m) {
              py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
         .def("workspace_layout", &Model::workspace_layout, py::arg("B"), py::arg("L"))
         .def("forward_launches", &Model::forward_launches)
+        .def("backward_launches", &Model::backward_launches)
+        .def("train_workspace_size", &Model::train_workspace_size, py::arg("B"), py::arg("L"))
+        .def("num_weights", &Model::num_weights)
+        .def("forward_train_device", &Model::forward_train_device, py::arg("B"), py::arg("L"), py::arg("s"),
+             py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("backward_device", &Model::backward_device, py::arg("B"), py::arg("L"), py::arg("s"),
+             py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("dout"),
+             py::arg("ds"), py::arg("dz1"), py::arg("dz2"), py::arg("drot"), py::arg("dtrans"),
+             py::arg("dweights"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("train_workspace_layout", &Model::train_workspace_layout, py::arg("B"), py::arg("L"))
+        .def("flash_grad", &Model::flash_grad, py::arg("s"), py::arg("z1"), py::arg("z2"),
+             py::arg("rotations"), py::arg("translations"), py::arg("dout"), py::arg("mask") = py::none(),
+             "Forward + backward (gradient of sum(out * dout)) on the GPU")
         .def("set_timing", &Model::set_timing, py::arg("enable"))
         .def("stage_times", &Model::stage_times)
         .def_property_readonly("precision", &Model::precision)

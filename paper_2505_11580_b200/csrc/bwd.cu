@@ -1,0 +1,381 @@
+// Memory-bound kernels of the FlashIPA backward (the reference has no backward, proj/SPEC.md:8;
+// these differentiate its forward, pinned by finite differences in tests/test_oracle.py):
+//
+//   bwd_prep   : the output epilogue (proj/src/flash_ipa.cpp:171-210, apply_inverse
+//                proj/src/geometry.cpp:70-76) run backwards.  From dfeat = dOut . w_out^T and the
+//                saved O_hat it writes dO_hat in the v_hat column layout of pack.cu
+//                ([dv | z1 (.) d(pair) | sum_p dg_p | sum_p dg_p | dg_p]), D = rowsum(dO_hat*O_hat)
+//                (bf16-rounded dO_hat, as the MMAs see it) and the epilogue's own gradients
+//                (z1 through the pair contraction, frames through R^T(g - t)).
+//   bwd_unpack : the lifts (proj/src/flash_ipa.cpp:23-126, pack.cu) run backwards.  It maps
+//                the attention accumulators dQ_acc = dS.K_hat, dK_acc = dS^T.Q_hat,
+//                dV_acc = P^T.dO_hat in the lifted layout back to natural gradients: the
+//                projection columns (reference order w_q|w_k|w_v|w_qp|w_kp|w_vp), z1, z2,
+//                rotations, translations, d(gamma w_l w_c) and d(w_l w_bias).  The column
+//                bookkeeping is the one checked on the CPU by tests/bwd_emulation.py.
+// Logits are q_hat.k_hat in log2 units, so dL/d(q_hat) = ln2 dQ_acc, dL/d(k_hat) = ln2 dK_acc;
+// q_hat carries a log2(e) factor, which cancels on the query side.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One block per residue (b, i); warp w handles heads w, w+8, ...
+__global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
+    extern __shared__ float sm[];
+    const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nv = d.n_value;
+    float* s_dz1 = sm;                 // rdz
+    float* s_red = s_dz1 + rdz;        // 12: dR (9), dt (3)
+    float* s_dopt = s_red + 12;        // 8 warps x 3*Nv
+    const int64_t row = blockIdx.x;
+    const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < rdz + 12; e += blockDim.x) sm[e] = 0.f;
+    float R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
+    const float* z1 = a.z1 + row * rdz;
+    __syncthreads();
+
+    const int vpair = c + rdz, vpts = vpair + 6;
+    float* dopt_s = s_dopt + warp * 3 * Nv;
+    float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
+    for (int h = warp; h < H; h += 8) {
+        const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
+        const __nv_bfloat16* o = a.ohat + hrow * d.dv_pad;
+        const float* df = a.dfeat + row * d.feat_ld + static_cast<int64_t>(h) * d.seg;
+        float ds[3] = {0.f, 0.f, 0.f};
+        if (lane < Nv) {
+            const int p = lane;
+            float y[3], loc[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+                y[x] = __bfloat162float(o[vpts + 3 * p + x]) + __bfloat162float(o[vpair + x]) +
+                       __bfloat162float(o[vpair + 3 + x]) - t[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) loc[x] = R[x] * y[0] + R[3 + x] * y[1] + R[6 + x] * y[2];
+            const float nrm = sqrtf(loc[0] * loc[0] + loc[1] * loc[1] + loc[2] * loc[2]);
+            const float dn = df[dz + c + 3 * Nv + p];
+            const float sc = nrm > 0.f ? dn / nrm : 0.f;
+            float dl[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) dl[x] = df[dz + c + 3 * p + x] + sc * loc[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                ds[x] = R[3 * x] * dl[0] + R[3 * x + 1] * dl[1] + R[3 * x + 2] * dl[2];
+                dopt_s[3 * p + x] = ds[x];
+                dt[x] -= ds[x];
+            }
+            // local = R^T y  =>  dR[b][a] += y_b dl_a
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                for (int aa = 0; aa < 3; ++aa) dR[3 * bb + aa] += y[bb] * dl[aa];
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x) ds[x] = warp_sum(ds[x]);
+        __syncwarp();
+        __nv_bfloat16* out = a.dohat + hrow * d.dv_pad;
+        float Dp = 0.f;
+        for (int col = lane; col < d.dv_pad; col += 32) {
+            float v;
+            if (col < c) {
+                v = df[dz + col];
+            } else if (col < vpair) {
+                const int e = col - c;
+                const float dpc = df[e % dz];
+                v = z1[e] * dpc;
+                atomicAdd(&s_dz1[e], __bfloat162float(o[col]) * dpc);
+            } else if (col < vpts) {
+                v = ds[(col - vpair) % 3];
+            } else if (col < vpts + 3 * Nv) {
+                v = dopt_s[col - vpts];
+            } else {
+                v = 0.f;
+            }
+            const __nv_bfloat16 vb = __float2bfloat16_rn(v);
+            out[col] = vb;
+            if (col < d.dv_used) Dp += __bfloat162float(vb) * __bfloat162float(o[col]);
+        }
+        Dp = warp_sum(Dp);
+        if (lane == 0) a.Dvec[hrow] = Dp;
+        __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
+    if (lane == 0) {
+        for (int k = 0; k < 9; ++k) atomicAdd(&s_red[k], dR[k]);
+        for (int k = 0; k < 3; ++k) atomicAdd(&s_red[9 + k], dt[k]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rdz; e += blockDim.x) a.dz1_epi[row * rdz + e] = s_dz1[e];
+    if (threadIdx.x < 9) a.drot_epi[row * 9 + threadIdx.x] = s_red[threadIdx.x];
+    if (threadIdx.x < 3) a.dt_epi[row * 3 + threadIdx.x] = s_red[9 + threadIdx.x];
+}
+
+constexpr int kUnpackRows = 16;
+
+// A block handles kUnpackRows consecutive residues; d(w_l w_bias) and d(g) are reduced in shared
+// memory across them and flushed with one global atomic per entry per block.
+__global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+    extern __shared__ float sm[];
+    const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
+    float* s_dwlb = sm;              // H*dz
+    float* s_dg = s_dwlb + H * dz;   // H
+    float* s_red = s_dg + H;         // 12
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) sm[e] = 0.f;
+    const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
+    const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
+    const int g0 = c + 3 * Nq, zq = g0 + 20, vpair = c + rdz;
+    const int64_t BL = static_cast<int64_t>(a.B) * a.L;
+    const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
+
+    for (int rr = 0; rr < kUnpackRows; ++rr) {
+        const int64_t row = row_begin + rr;
+        if (row >= BL) break;
+        const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
+        if (threadIdx.x < 12) s_red[threadIdx.x] = 0.f;
+        __syncthreads();
+        auto acc_row = [&](const float* base, int h) {
+            return base + ((static_cast<int64_t>(b) * H + h) * a.L + i) * a.acc_ld;
+        };
+        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+        // pair factors: z1 (query side), z2 (key + value side), d(w_l w_bias)
+        const float* z2 = a.z2 + row * rdz;
+        for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
+            const int dd = e % dz;
+            float s1 = a.dz1_epi[row * rdz + e], s2 = 0.f;
+            const float z2e = z2[e];
+            for (int h = 0; h < H; ++h) {
+                const float kq = kLn2 * acc_row(a.dk_acc, h)[zq + e];
+                s1 += acc_row(a.dq_acc, h)[zq + e];
+                s2 += a.wl_bias[h * dz + dd] * kq + acc_row(a.dv_acc, h)[c + e];
+                atomicAdd(&s_dwlb[h * dz + dd], kq * z2e);
+            }
+            a.dz1[row * rdz + e] = s1;
+            a.dz2[row * rdz + e] = s2;
+        }
+        // scalar channels
+        for (int e = threadIdx.x; e < H * c; e += blockDim.x) {
+            const int h = e / c, cc = e - h * c;
+            dp[off_q + e] = __float2bfloat16_rn(acc_row(a.dq_acc, h)[cc]);
+            dp[off_k + e] = __float2bfloat16_rn(a.k_scale * kLn2 * acc_row(a.dk_acc, h)[cc]);
+            dp[off_v + e] = __float2bfloat16_rn(acc_row(a.dv_acc, h)[cc]);
+        }
+        // geometry: warp per head, lane per point
+        float R[9], t[3];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
+        const float* pr = a.proj + row * d.n_proj;
+        float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dg = 0.f;
+        for (int h = warp; h < H; h += 8) {
+            const float* qa = acc_row(a.dq_acc, h);
+            const float* ka = acc_row(a.dk_acc, h);
+            const float* va = acc_row(a.dv_acc, h);
+            const float g = a.head_g[h];
+            const float cs = ka[g0 + 18];
+            float dW[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (ka[g0 + 9 + x] + ka[g0 + 12 + x]);
+            float dgh = 0.f;
+            if (lane < Nq) {
+                const int p = lane;
+                // query point p: A = R q_p + t,  dA = g sum_j dS_ij B_jp
+                float qp[3], dA[3], A[3];
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    qp[x] = pr[off_qp + (h * Nq + p) * 3 + x];
+                    dA[x] = qa[c + 3 * p + x] + qa[g0 + x] + qa[g0 + 3 + x];
+                }
+#pragma unroll
+                for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
+                dgh += (A[0] * dA[0] + A[1] * dA[1] + A[2] * dA[2]) / g;
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    dp[off_qp + (h * Nq + p) * 3 + x] =
+                        __float2bfloat16_rn(R[x] * dA[0] + R[3 + x] * dA[1] + R[6 + x] * dA[2]);
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
+                }
+                // key point p: B = R k_p + t
+                float kp[3], B[3], dB[3];
+#pragma unroll
+                for (int x = 0; x < 3; ++x) kp[x] = pr[off_kp + (h * Nq + p) * 3 + x];
+#pragma unroll
+                for (int x = 0; x < 3; ++x) B[x] = R[3 * x] * kp[0] + R[3 * x + 1] * kp[1] + R[3 * x + 2] * kp[2] + t[x];
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    dB[x] = g * kLn2 * ka[c + 3 * p + x] + dW[x] - g * B[x] * cs;
+                    dt[x] -= g * B[x] * cs;
+                }
+                dgh += -0.5f * (B[0] * B[0] + B[1] * B[1] + B[2] * B[2]) * cs;
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    dp[off_kp + (h * Nq + p) * 3 + x] =
+                        __float2bfloat16_rn(R[x] * dB[0] + R[3 + x] * dB[1] + R[6 + x] * dB[2]);
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
+                }
+            }
+            if (lane < Nv) {
+                const int p = lane;
+                float vp[3], dV[3];
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    vp[x] = pr[off_vp + (h * Nv + p) * 3 + x];
+                    dV[x] = va[vpair + 6 + 3 * p + x];
+                }
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    dp[off_vp + (h * Nv + p) * 3 + x] =
+                        __float2bfloat16_rn(R[x] * dV[0] + R[3 + x] * dV[1] + R[6 + x] * dV[2]);
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
+                }
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int x = 0; x < 3; ++x)
+                    dt[x] += qa[g0 + 9 + x] + qa[g0 + 15 + x]                                   // query
+                             + g * kLn2 * (ka[g0 + x] + ka[g0 + 6 + x]) + float(Nq) * dW[x]   // key
+                             + va[vpair + x];                                                  // value
+            }
+            dgh = warp_sum(dgh);
+            dg += dgh;
+            if (lane == 0) s_dg[h] += dgh;  // one warp per head: no race
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
+        if (lane == 0) {
+            for (int k = 0; k < 9; ++k) atomicAdd(&s_red[k], dR[k]);
+            for (int k = 0; k < 3; ++k) atomicAdd(&s_red[9 + k], dt[k]);
+        }
+        __syncthreads();
+        if (threadIdx.x < 9 && a.drot != nullptr)
+            a.drot[row * 9 + threadIdx.x] = s_red[threadIdx.x] + a.drot_epi[row * 9 + threadIdx.x];
+        if (threadIdx.x < 3) a.dt_c[row * 3 + threadIdx.x] = s_red[9 + threadIdx.x] + a.dt_epi[row * 3 + threadIdx.x];
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
+    for (int e = threadIdx.x; e < H; e += blockDim.x) atomicAdd(&a.dg[e], s_dg[e]);
+}
+
+__global__ void bwd_dout_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ mask,
+                                __nv_bfloat16* __restrict__ out, int ld_out, float* __restrict__ db,
+                                int64_t rows, int cols) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= cols) return;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64;
+    float s = 0.f;
+    for (int64_t r = r0; r < min(rows, r0 + 64); ++r) {
+        const bool ok = mask == nullptr || mask[r] != 0;
+        const float v = ok ? dout[r * cols + col] : 0.f;
+        out[r * ld_out + col] = __float2bfloat16_rn(v);
+        s += v;
+    }
+    atomicAdd(&db[col], s);
+}
+
+__global__ void bwd_recenter_kernel(const float* __restrict__ dtc, const uint8_t* __restrict__ mask,
+                                    float* __restrict__ dt, int L) {
+    __shared__ float red[4][32];
+    const int b = blockIdx.x;
+    const float* g = dtc + int64_t(b) * L * 3;
+    float sx = 0.f, sy = 0.f, sz = 0.f, cnt = 0.f;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        if (mask == nullptr || mask[int64_t(b) * L + i] != 0) {
+            sx += g[i * 3];
+            sy += g[i * 3 + 1];
+            sz += g[i * 3 + 2];
+            cnt += 1.f;
+        }
+    }
+    sx = warp_sum(sx);
+    sy = warp_sum(sy);
+    sz = warp_sum(sz);
+    cnt = warp_sum(cnt);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[0][w] = sx;
+        red[1][w] = sy;
+        red[2][w] = sz;
+        red[3][w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int nw = blockDim.x >> 5;
+        for (int k = 0; k < 4; ++k) {
+            float v = l < nw ? red[k][l] : 0.f;
+            v = warp_sum(v);
+            if (l == 0) red[k][0] = v;
+        }
+    }
+    __syncthreads();
+    const float n = red[3][0] > 0.f ? red[3][0] : 1.f;
+    const float mx = red[0][0] / n, my = red[1][0] / n, mz = red[2][0] / n;
+    float* o = dt + int64_t(b) * L * 3;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const bool ok = mask == nullptr || mask[int64_t(b) * L + i] != 0;
+        o[i * 3] = ok ? g[i * 3] - mx : 0.f;
+        o[i * 3 + 1] = ok ? g[i * 3 + 1] - my : 0.f;
+        o[i * 3 + 2] = ok ? g[i * 3 + 2] - mz : 0.f;
+    }
+}
+
+__global__ void scale_vec_kernel(const float* in, const float* scale, int period, float* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i] * scale[i % period];
+}
+
+}  // namespace
+
+void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream) {
+    const size_t smem = sizeof(float) * (d.rank * d.d_z + 12 + 8 * 3 * d.n_value);
+    bwd_prep_kernel<<<static_cast<unsigned>(int64_t(a.B) * a.L), 256, smem, stream>>>(d, a);
+}
+
+void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
+    const size_t smem = sizeof(float) * (d.heads * d.d_z + d.heads + 12);
+    const int64_t BL = int64_t(a.B) * a.L;
+    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a);
+}
+
+void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
+                     int64_t rows, int cols, cudaStream_t stream) {
+    dim3 grid((cols + 127) / 128, static_cast<unsigned>((rows + 63) / 64));
+    bwd_dout_kernel<<<grid, 128, 0, stream>>>(dout, mask, out, ld_out, db, rows, cols);
+}
+
+void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {
+    bwd_recenter_kernel<<<B, 256, 0, stream>>>(dt_c, mask, dt, L);
+}
+
+void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream) {
+    if (n > 0) scale_vec_kernel<<<(n + 255) / 256, 256, 0, stream>>>(in, scale, period, out, n);
+}
+
+}  // namespace fipa_b200

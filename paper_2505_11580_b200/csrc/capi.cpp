@@ -228,4 +228,65 @@ int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n) {
     return k;
 }
 
+size_t fipa_layer_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_) {
+    if (layer == nullptr || B < 1 || L_ < 1) return 0;
+    return layer->impl.train_workspace_size(B, L_);
+}
+
+int fipa_layer_forward_train(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                             const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                             float* out, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        L(layer).forward(B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
+                         static_cast<cudaStream_t>(stream), true);
+    });
+}
+
+uint64_t fipa_layer_num_weights(const fipa_layer* layer) { return layer ? layer->impl.num_weights() : 0; }
+
+int fipa_layer_backward(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                        const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                        const float* dout, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                        float* dweights, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        L(layer).backward(B, L_, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
+                          workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L_, const double* s, const double* z1,
+                         const double* z2, const double* rot, const double* trans, const uint8_t* mask,
+                         const double* dout, double* out, double* ds, double* dz1, double* dz2,
+                         double* drot, double* dtrans, double* dweights) {
+    return guarded([&] {
+        if (!s || !z1 || !z2 || !rot || !trans || !dout) throw fipa_b200::ValueError("null buffer");
+        L(layer).grad_host(B, L_, s, z1, z2, rot, trans, mask, dout, out, ds, dz1, dz2, drot, dtrans, dweights);
+    });
+}
+
+int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, int64_t* offsets,
+                                      int64_t* dims) {
+    if (layer == nullptr || offsets == nullptr || B < 1 || L_ < 1) return 0;
+    const auto w = layer->impl.carve(nullptr, B, L_, true);
+    auto off = [](const void* p) { return static_cast<int64_t>(reinterpret_cast<uintptr_t>(p)); };
+    offsets[0] = off(w.o_hat);
+    offsets[1] = off(w.do_hat);
+    offsets[2] = off(w.Dvec);
+    offsets[3] = off(w.dq_acc);
+    offsets[4] = off(w.dk_acc);
+    offsets[5] = off(w.dv_acc);
+    offsets[6] = off(w.dproj);
+    offsets[7] = off(w.dfeat);
+    if (dims != nullptr) {
+        dims[0] = fipa_b200::FlashIpaLayer::kAccLd;
+        dims[1] = layer->impl.nproj_ld();
+        dims[2] = layer->impl.dims().feat_ld;
+    }
+    return 8;
+}
+
+int fipa_layer_backward_launches(const fipa_layer* layer) {
+    return layer ? layer->impl.launches_per_backward() : 0;
+}
+
 }  // extern "C"

@@ -8,6 +8,7 @@
 // output projection (proj/src/flash_ipa.cpp:212) and the backward GEMMs.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -37,6 +38,7 @@ struct EpiParams {
     int64_t ldc;
     int M, N, K;
     bool out_bf16, accumulate;
+    int split_k;
     float alpha;
     const float* bias;
     const uint8_t* row_mask;
@@ -60,7 +62,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = ptx::lane_id();
     const int m0 = blockIdx.y * BM;
     const int n0 = blockIdx.x * BN;
-    const int nk = (p.K + BK - 1) / BK;
+    const int nk_all = (p.K + BK - 1) / BK;
+    const int kb0 = static_cast<int>((int64_t(nk_all) * blockIdx.z) / p.split_k);
+    const int nk = static_cast<int>((int64_t(nk_all) * (blockIdx.z + 1)) / p.split_k) - kb0;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&mapA);
@@ -88,15 +92,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
                 if (A_MN) {
                     for (int mb = 0; mb < BM / 64; ++mb)
-                        ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kb * BK);
+                        ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, (kb0 + kb) * BK);
                 } else {
-                    ptx::tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
+                    ptx::tma_load_2d(sa, &mapA, &full[s], (kb0 + kb) * BK, m0);
                 }
                 if (B_MN) {
                     for (int nb = 0; nb < BN / 64; ++nb)
-                        ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kb * BK);
+                        ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, (kb0 + kb) * BK);
                 } else {
-                    ptx::tma_load_2d(sb, &mapB, &full[s], kb * BK, n0);
+                    ptx::tma_load_2d(sb, &mapB, &full[s], (kb0 + kb) * BK, n0);
                 }
             }
         }
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
         const int quad = warp & 3;
         const int row = m0 + quad * 32 + lane;
-        ptx::mbar_wait(done, 0);
+        if (nk > 0) ptx::mbar_wait(done, 0);
         ptx::tc_fence_after();
         const bool row_ok = row < p.M;
         const bool zero_row = row_ok && p.row_mask != nullptr && p.row_mask[row] == 0;
@@ -137,6 +141,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col0 = n0 + c0;
             if (col0 >= p.N) continue;
             float v[32];
+            if (p.split_k > 1) {
+                if (nk <= 0) continue;
+                float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
+                if (col0 + 32 <= p.N && (p.ldc % 4) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        atomicAdd(reinterpret_cast<float4*>(out) + q,
+                                  make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
+                                              __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha));
+                } else {
+                    for (int i = 0; i < 32 && col0 + i < p.N; ++i) atomicAdd(out + i, __uint_as_float(r[i]) * p.alpha);
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 float x = __uint_as_float(r[i]) * p.alpha;
@@ -196,14 +214,14 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
                                   : make_map_2d_bf16(a.A, a.M, a.K, a.lda, 64, BM);
     const CUtensorMap mapB = B_MN ? make_map_2d_bf16(a.B, a.K, a.N, a.ldb, 64, BK)
                                   : make_map_2d_bf16(a.B, a.N, a.K, a.ldb, 64, BN);
-    EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, a.alpha, a.bias, a.row_mask};
+    EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, std::max(1, a.split_k), a.alpha, a.bias, a.row_mask};
     auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         configured = true;
     }
-    dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
+    dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, std::max(1, a.split_k));
     kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, p);
 }
 
@@ -216,6 +234,8 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
     if ((a.lda * 2) % 16 != 0 || (a.ldb * 2) % 16 != 0)
         throw std::invalid_argument("gemm: operand row strides must be multiples of 8 elements");
     if (a.accumulate && a.out_bf16) throw std::invalid_argument("gemm: accumulate needs fp32 C");
+    if (a.split_k > 1 && (a.out_bf16 || a.bias || a.row_mask))
+        throw std::invalid_argument("gemm: split-K accumulates plain fp32 C");
     const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512);
     const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);
     if (wide) {

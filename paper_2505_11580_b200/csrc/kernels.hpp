@@ -25,6 +25,7 @@ struct GemmArgs {
     bool b_mn_major = false;
     bool out_bf16 = false;
     bool accumulate = false;  // C += result (fp32 output only)
+    int split_k = 1;          // >1: K split over gridDim.z, fp32 C accumulated atomically (zero it first)
     float alpha = 1.0f;
     const float* bias = nullptr;        // [N] or null
     const uint8_t* row_mask = nullptr;  // [M] or null: rows with 0 are written as 0
@@ -79,6 +80,7 @@ struct AttnArgs {
     const float* trans;
     __nv_bfloat16* feat;   // [BL, feat]
     float* lse;            // [B*H, L] natural-log LSE of the shifted logits
+    __nv_bfloat16* o_save; // [B*H, L, dv_pad] normalised O_hat for the backward, or null
     int B, L;
 };
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
@@ -87,6 +89,73 @@ void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stre
 // CTA-pair version (tcgen05 cta_group::2, 256 query rows per pair, streamed K/V rings).
 bool attn_fwd_2sm_supported(const LayerDims& d);
 void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
+
+// ------------------------------------------------------------- backward
+struct AttnBwdArgs {
+    const __nv_bfloat16* qhat;
+    const __nv_bfloat16* khat;
+    const __nv_bfloat16* vhat;
+    const __nv_bfloat16* dohat;  // [B*H, L, dv_pad]
+    const float* lse;            // [B*H, L]
+    const float* Dvec;           // [B*H, L]
+    float* dq_acc;               // [B*H, L, acc_ld] = dS . K_hat
+    float* dk_acc;               //                  = dS^T . Q_hat
+    float* dv_acc;               //                  = P^T . dO_hat
+    int acc_ld;
+    int B, L;
+};
+bool attn_bwd_supported(const LayerDims& d);
+void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream);
+
+struct BwdPrepArgs {
+    const float* dfeat;           // [BL, feat_ld] dOut . w_out^T
+    const __nv_bfloat16* ohat;    // [B*H, L, dv_pad] saved by the forward
+    const float* z1;              // [BL, r*d_z]
+    const float* rot;             // [BL, 9]
+    const float* trans_c;         // [BL, 3] recentred
+    __nv_bfloat16* dohat;         // [B*H, L, dv_pad]
+    float* Dvec;                  // [B*H, L]
+    float* dz1_epi;               // [BL, r*d_z]
+    float* drot_epi;              // [BL, 9]
+    float* dt_epi;                // [BL, 3]
+    int B, L;
+};
+void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream);
+
+struct BwdUnpackArgs {
+    const float* dq_acc;
+    const float* dk_acc;
+    const float* dv_acc;
+    int acc_ld;
+    const float* proj;      // [BL, n_proj] forward projections (local points)
+    const float* rot;
+    const float* trans_c;
+    const float* z2;
+    const float* head_g;    // [H]
+    const float* wl_bias;   // [H, d_z]
+    float k_scale;
+    const float* dz1_epi;
+    const float* drot_epi;
+    const float* dt_epi;
+    __nv_bfloat16* dproj;   // [BL, nproj_ld]
+    int nproj_ld;
+    float* dz1;             // [BL, r*d_z]
+    float* dz2;             // [BL, r*d_z]
+    float* drot;            // [BL, 9] or null
+    float* dt_c;            // [BL, 3] gradient w.r.t. the recentred translations
+    float* dg;              // [H]     accumulated (zero first): dL/d(gamma_h w_l w_c)
+    float* dwlb;            // [H, d_z] accumulated (zero first): dL/d(w_l w_bias)
+    int B, L;
+};
+void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream);
+
+// dOut with masked rows zeroed -> bf16 [BL, ld_out]; db[d_in] += column sums (zero db first).
+void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
+                     int64_t rows, int cols, cudaStream_t stream);
+// Translation gradient through the per-sample recentring: dt = mask*(dt_c - mean_valid(dt_c)).
+void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream);
+// out[i] = in[i] * scale[i % period]
+void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream);
 
 // Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);

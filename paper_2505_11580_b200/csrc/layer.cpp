@@ -359,11 +359,11 @@ void FlashIpaLayer::release_device() {
     for (void* p : {static_cast<void*>(d_wproj_t_), static_cast<void*>(d_wout_t_),
                     static_cast<void*>(d_wproj_), static_cast<void*>(d_wout_),
                     static_cast<void*>(d_bout_), static_cast<void*>(d_head_g_),
-                    static_cast<void*>(d_wl_bias_)}) {
+                    static_cast<void*>(d_wl_bias_), static_cast<void*>(d_bwd_scale_)}) {
         if (p) cudaFree(p);
     }
     d_wproj_t_ = d_wout_t_ = nullptr;
-    d_wproj_ = d_wout_ = d_bout_ = d_head_g_ = d_wl_bias_ = nullptr;
+    d_wproj_ = d_wout_ = d_bout_ = d_head_g_ = d_wl_bias_ = d_bwd_scale_ = nullptr;
 }
 
 void FlashIpaLayer::init_weights(std::uint64_t seed) {
@@ -434,11 +434,16 @@ void FlashIpaLayer::upload_weights() {
     for (std::size_t e = 0; e < wlb.size(); ++e) wlb[e] = static_cast<float>(w_.w_l * w_.w_bias[e]);
     up(&d_head_g_, g);
     up(&d_wl_bias_, wlb);
+    std::vector<float> bs(H + 1);
+    for (std::size_t h = 0; h < H; ++h)
+        bs[h] = static_cast<float>(w_.w_l * w_.w_c / (1.0 + std::exp(-w_.gamma_raw[h])));
+    bs[H] = static_cast<float>(w_.w_l);
+    up(&d_bwd_scale_, bs);
     k_scale_ = static_cast<float>(w_.w_l / std::sqrt(static_cast<double>(cfg_.c)));
     dirty_ = false;
 }
 
-FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::int64_t L) const {
+FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::int64_t L, bool train) const {
     const LayerDims& d = dims_;
     const std::size_t BL = std::size_t(B) * L, BHL = BL * d.heads;
     const std::size_t el = cfg_.precision == Precision::bf16 ? 2 : 4;
@@ -458,12 +463,51 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     w.colbias = reinterpret_cast<float*>(take(BHL * 4));
     w.lse = reinterpret_cast<float*>(take(BHL * 4));
     w.feat = take(BL * d.feat_ld * el);
+    if (train) {
+        const std::size_t rdz = std::size_t(d.rank) * d.d_z;
+        w.o_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));
+        w.dout_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
+        w.dfeat = reinterpret_cast<float*>(take(BL * d.feat_ld * 4));
+        w.do_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));
+        w.Dvec = reinterpret_cast<float*>(take(BHL * 4));
+        w.dq_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
+        w.dk_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
+        w.dv_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
+        w.dproj = reinterpret_cast<__nv_bfloat16*>(take(BL * nproj_ld() * 2));
+        w.dz1_epi = reinterpret_cast<float*>(take(BL * rdz * 4));
+        w.drot_epi = reinterpret_cast<float*>(take(BL * 9 * 4));
+        w.dt_epi = reinterpret_cast<float*>(take(BL * 3 * 4));
+        w.dt_c = reinterpret_cast<float*>(take(BL * 3 * 4));
+        w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
+        w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
+    }
     w.bytes = off;
     return w;
 }
 
 std::size_t FlashIpaLayer::workspace_size(std::int64_t B, std::int64_t L) const {
     return carve(nullptr, B, L).bytes;
+}
+
+std::size_t FlashIpaLayer::train_workspace_size(std::int64_t B, std::int64_t L) const {
+    return carve(nullptr, B, L, true).bytes;
+}
+
+std::size_t FlashIpaLayer::num_weights() const {
+    std::size_t n = 0;
+    for (const auto& sh : weight_shapes(cfg_)) n += numel(sh);
+    return n;
+}
+
+bool FlashIpaLayer::backward_supported() const {
+    return cfg_.precision == Precision::bf16 && attn_fwd_2sm_supported(dims_) && attn_bwd_supported(dims_) &&
+           dims_.n_value <= 32 && dims_.n_query <= 32;
+}
+
+int FlashIpaLayer::launches_per_backward() const {
+    // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, attn Q, unpack, recenter, ds GEMM,
+    // dW_proj GEMM, two scale kernels (memsets and 2-D copies are not kernels of ours)
+    return 12;
 }
 
 int FlashIpaLayer::launches_per_forward() const {
@@ -491,11 +535,13 @@ std::vector<float> FlashIpaLayer::stage_times() const {
 void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
                             const float* z2, const float* rot, const float* trans,
                             const std::uint8_t* mask, float* out, void* workspace,
-                            std::size_t workspace_bytes, cudaStream_t stream) {
+                            std::size_t workspace_bytes, cudaStream_t stream, bool train) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
-    const Workspace ws = carve(workspace, B, L);
+    REQUIRE(!train || backward_supported(),
+            "training (forward_train/backward) needs precision='bf16' and lifted widths <= 448");
+    const Workspace ws = carve(workspace, B, L, train);
     REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "workspace too small: need ",
             ws.bytes, " bytes, got ", workspace_bytes);
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -560,9 +606,10 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         aa.trans = ws.trans_c;
         aa.feat = static_cast<__nv_bfloat16*>(ws.feat);
         aa.lse = ws.lse;
+        aa.o_save = train ? ws.o_hat : nullptr;
         aa.B = int(B);
         aa.L = int(L);
-        if (use_2sm_attention(d)) {
+        if (train || use_2sm_attention(d)) {
             launch_attn_fwd_2sm(d, aa, stream);
         } else {
             launch_attn_fwd_tc(d, aa, stream);
@@ -652,6 +699,259 @@ void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s
                "D2H");
     cuda_check(cudaStreamSynchronize(own_stream_), "forward");
     for (std::size_t i = 0; i < n_out; ++i) out[i] = static_cast<double>(h[n_in + i]);
+}
+
+
+void FlashIpaLayer::ensure_staging(std::size_t host_bytes, std::size_t dev_bytes) {
+    if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");
+    if (h_stage_bytes_ < host_bytes) {
+        if (h_stage_) cudaFreeHost(h_stage_);
+        h_stage_ = nullptr;
+        cuda_check(cudaMallocHost(&h_stage_, host_bytes), "cudaMallocHost");
+        h_stage_bytes_ = host_bytes;
+    }
+    if (d_stage_bytes_ < dev_bytes) {
+        if (d_stage_) cudaFree(d_stage_);
+        d_stage_ = nullptr;
+        cuda_check(cudaMalloc(&d_stage_, dev_bytes), "cudaMalloc");
+        d_stage_bytes_ = dev_bytes;
+    }
+}
+
+// Backward of the layer (no reference counterpart: proj/SPEC.md:8).  Order of work:
+//   dOut (masked rows zeroed, proj/src/flash_ipa.cpp:213-216) -> db_out, dfeat = dOut.w_out^T,
+//   dw_out = feat^T.dOut -> bwd_prep (epilogue^T) -> attention backward (attn_bwd.cu)
+//   -> bwd_unpack (lifts^T) -> ds = dproj.W^T, dW = s^T.dproj, d(w_bias), d(gamma_raw).
+void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                             const float* z2, const float* rot, const float* trans,
+                             const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
+                             float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
+                             std::size_t workspace_bytes, cudaStream_t stream) {
+    REQUIRE(B >= 1, "batch must be >= 1");
+    REQUIRE(L >= 1, "empty frame set");
+    REQUIRE(s && z1 && z2 && rot && trans && dout && ds && dz1 && dz2 && dweights,
+            "null input/output pointer");
+    REQUIRE(backward_supported(), "backward needs precision='bf16' and lifted widths <= 448");
+    const Workspace ws = carve(workspace, B, L, true);
+    REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "train workspace too small: need ",
+            ws.bytes, " bytes, got ", workspace_bytes);
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    REQUIRE(!dirty_, "backward: weights changed since the training forward");
+    const LayerDims& d = dims_;
+    const int BL = static_cast<int>(B * L);
+    const int H = d.heads;
+    // dweights regions (reference order)
+    const auto shapes = weight_shapes(cfg_);
+    std::size_t woff[11] = {0};
+    for (int i = 0; i < 10; ++i) woff[i + 1] = woff[i] + numel(shapes[i]);
+    float* dw_bias = dweights + woff[6];
+    float* dgamma = dweights + woff[7];
+    float* dw_out = dweights + woff[8];
+    float* db_out = dweights + woff[9];
+
+    cuda_check(cudaMemsetAsync(dw_out, 0, (woff[10] - woff[8]) * 4, stream), "memset");
+    cuda_check(cudaMemsetAsync(ws.red, 0, (H + std::size_t(H) * d.d_z) * 4, stream), "memset");
+    cuda_check(cudaMemsetAsync(ws.dwproj, 0, std::size_t(d.d_in) * d.n_proj * 4, stream), "memset");
+
+    launch_bwd_dout(dout, mask, ws.dout_bf16, d.din_ld, db_out, BL, d.d_in, stream);
+    {  // dfeat = dOut . w_out^T
+        GemmArgs g;
+        g.A = ws.dout_bf16;
+        g.lda = d.din_ld;
+        g.B = d_wout_t_;
+        g.ldb = d.feat_ld;
+        g.b_mn_major = true;
+        g.C = ws.dfeat;
+        g.ldc = d.feat_ld;
+        g.M = BL;
+        g.N = d.feat;
+        g.K = d.d_in;
+        launch_gemm_bf16(g, stream);
+    }
+    {  // dw_out = feat^T . dOut
+        GemmArgs g;
+        g.A = static_cast<const __nv_bfloat16*>(ws.feat);
+        g.lda = d.feat_ld;
+        g.a_mn_major = true;
+        g.B = ws.dout_bf16;
+        g.ldb = d.din_ld;
+        g.b_mn_major = true;
+        g.C = dw_out;
+        g.ldc = d.d_in;
+        g.M = d.feat;
+        g.N = d.d_in;
+        g.K = BL;
+        const int tiles = ((d.feat + 127) / 128) * ((d.d_in + 127) / 128);
+        g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
+        launch_gemm_bf16(g, stream);
+    }
+    {
+        BwdPrepArgs a{};
+        a.dfeat = ws.dfeat;
+        a.ohat = ws.o_hat;
+        a.z1 = z1;
+        a.rot = rot;
+        a.trans_c = ws.trans_c;
+        a.dohat = ws.do_hat;
+        a.Dvec = ws.Dvec;
+        a.dz1_epi = ws.dz1_epi;
+        a.drot_epi = ws.drot_epi;
+        a.dt_epi = ws.dt_epi;
+        a.B = int(B);
+        a.L = int(L);
+        launch_bwd_prep(d, a, stream);
+    }
+    {
+        AttnBwdArgs a{};
+        a.qhat = static_cast<const __nv_bfloat16*>(ws.qhat);
+        a.khat = static_cast<const __nv_bfloat16*>(ws.khat);
+        a.vhat = static_cast<const __nv_bfloat16*>(ws.vhat);
+        a.dohat = ws.do_hat;
+        a.lse = ws.lse;
+        a.Dvec = ws.Dvec;
+        a.dq_acc = ws.dq_acc;
+        a.dk_acc = ws.dk_acc;
+        a.dv_acc = ws.dv_acc;
+        a.acc_ld = kAccLd;
+        a.B = int(B);
+        a.L = int(L);
+        launch_attn_bwd(d, a, stream);
+    }
+    {
+        BwdUnpackArgs a{};
+        a.dq_acc = ws.dq_acc;
+        a.dk_acc = ws.dk_acc;
+        a.dv_acc = ws.dv_acc;
+        a.acc_ld = kAccLd;
+        a.proj = ws.proj;
+        a.rot = rot;
+        a.trans_c = ws.trans_c;
+        a.z2 = z2;
+        a.head_g = d_head_g_;
+        a.wl_bias = d_wl_bias_;
+        a.k_scale = k_scale_;
+        a.dz1_epi = ws.dz1_epi;
+        a.drot_epi = ws.drot_epi;
+        a.dt_epi = ws.dt_epi;
+        a.dproj = ws.dproj;
+        a.nproj_ld = nproj_ld();
+        a.dz1 = dz1;
+        a.dz2 = dz2;
+        a.drot = drot;
+        a.dt_c = ws.dt_c;
+        a.dg = ws.red;
+        a.dwlb = ws.red + H;
+        a.B = int(B);
+        a.L = int(L);
+        launch_bwd_unpack(d, a, stream);
+    }
+    if (dtrans != nullptr) launch_bwd_recenter(ws.dt_c, mask, dtrans, int(B), int(L), stream);
+    {  // ds = dproj . W^T
+        GemmArgs g;
+        g.A = ws.dproj;
+        g.lda = nproj_ld();
+        g.B = d_wproj_t_;
+        g.ldb = d.din_ld;
+        g.b_mn_major = true;
+        g.C = ds;
+        g.ldc = d.d_in;
+        g.M = BL;
+        g.N = d.d_in;
+        g.K = d.n_proj;
+        launch_gemm_bf16(g, stream);
+    }
+    {  // dW = s^T . dproj  [d_in, n_proj]
+        GemmArgs g;
+        g.A = ws.s_bf16;
+        g.lda = d.din_ld;
+        g.a_mn_major = true;
+        g.B = ws.dproj;
+        g.ldb = nproj_ld();
+        g.b_mn_major = true;
+        g.C = ws.dwproj;
+        g.ldc = d.n_proj;
+        g.M = d.d_in;
+        g.N = d.n_proj;
+        g.K = BL;
+        const int bn = (d.n_proj >= 2048) ? 256 : 128;
+        const int tiles = ((d.d_in + 127) / 128) * ((d.n_proj + bn - 1) / bn);
+        g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
+        launch_gemm_bf16(g, stream);
+    }
+    // scatter the fused projection gradient into w_q .. w_vp
+    std::size_t col0 = 0;
+    for (int i = 0; i < 6; ++i) {
+        const std::size_t wcols = shapes[i][1];
+        cuda_check(cudaMemcpy2DAsync(dweights + woff[i], wcols * 4, ws.dwproj + col0, std::size_t(d.n_proj) * 4,
+                                     wcols * 4, d.d_in, cudaMemcpyDeviceToDevice, stream),
+                   "cudaMemcpy2DAsync");
+        col0 += wcols;
+    }
+    launch_scale_vec(ws.red + H, d_bwd_scale_ + H, 1, dw_bias, H * d.d_z, stream);
+    launch_scale_vec(ws.red, d_bwd_scale_, H, dgamma, H, stream);
+    cuda_check(cudaGetLastError(), "backward launch");
+}
+
+void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
+                              const double* z2, const double* rot, const double* trans,
+                              const std::uint8_t* mask, const double* dout, double* out, double* ds,
+                              double* dz1, double* dz2, double* drot, double* dtrans, double* dweights) {
+    REQUIRE(B >= 1, "batch must be >= 1");
+    REQUIRE(L >= 1, "empty frame set");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const std::size_t BL = std::size_t(B) * L;
+    const std::size_t rdz = cfg_.rank * cfg_.d_z;
+    const std::size_t n_s = BL * cfg_.d_in, n_z = BL * rdz, n_r = BL * 9, n_t = BL * 3;
+    const std::size_t n_in = n_s + 2 * n_z + n_r + n_t + n_s /*dout*/;
+    const std::size_t n_grad = n_s + 2 * n_z + n_r + n_t + num_weights();
+    const std::size_t n_out = n_s + n_grad;
+    const std::size_t io_bytes = round_up((n_in + n_out) * 4 + BL, 256);
+    const std::size_t ws_bytes = train_workspace_size(B, L);
+    ensure_staging(io_bytes, io_bytes + ws_bytes);
+    float* h = static_cast<float*>(h_stage_);
+    auto cvt = [](float* dst, const double* src, std::size_t n) {
+        for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<float>(src[i]);
+    };
+    std::size_t o = 0;
+    for (auto [src, n] : {std::pair{s, n_s}, std::pair{z1, n_z}, std::pair{z2, n_z}, std::pair{rot, n_r},
+                          std::pair{trans, n_t}, std::pair{dout, n_s}}) {
+        cvt(h + o, src, n);
+        o += n;
+    }
+    std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
+    if (mask) std::memcpy(hmask, mask, BL);
+    float* dbase = static_cast<float*>(d_stage_);
+    std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
+    cuda_check(cudaMemcpyAsync(dbase, h, n_in * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
+    if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
+    void* ws = static_cast<char*>(d_stage_) + io_bytes;
+    const float* di = dbase;
+    float* dout_d = dbase + n_in;  // out, then grads
+    const float *d_s = di, *d_z1 = di + n_s, *d_z2 = d_z1 + n_z, *d_rot = d_z2 + n_z, *d_t = d_rot + n_r,
+                *d_dout = d_t + n_t;
+    float* g_s = dout_d + n_s;
+    float* g_z1 = g_s + n_s;
+    float* g_z2 = g_z1 + n_z;
+    float* g_rot = g_z2 + n_z;
+    float* g_t = g_rot + n_r;
+    float* g_w = g_t + n_t;
+    forward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, dout_d, ws, ws_bytes, own_stream_, true);
+    backward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, d_dout, g_s, g_z1, g_z2, g_rot, g_t,
+             g_w, ws, ws_bytes, own_stream_);
+    cuda_check(cudaMemcpyAsync(h + n_in, dout_d, n_out * 4, cudaMemcpyDeviceToHost, own_stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(own_stream_), "grad");
+    const float* r = h + n_in;
+    auto back = [](double* dst, const float* src, std::size_t n) {
+        if (dst)
+            for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<double>(src[i]);
+    };
+    back(out, r, n_s);
+    back(ds, r + n_s, n_s);
+    back(dz1, r + 2 * n_s, n_z);
+    back(dz2, r + 2 * n_s + n_z, n_z);
+    back(drot, r + 2 * n_s + 2 * n_z, n_r);
+    back(dtrans, r + 2 * n_s + 2 * n_z + n_r, n_t);
+    back(dweights, r + 2 * n_s + 2 * n_z + n_r + n_t, num_weights());
 }
 
 }  // namespace fipa_b200

@@ -93,7 +93,24 @@ public:
     std::size_t workspace_size(std::int64_t B, std::int64_t L) const;
     void forward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                  const float* rot, const float* trans, const std::uint8_t* mask, float* out,
-                 void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+                 void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
+                 bool train = false);
+    // Training: forward(..., train=true) over a train_workspace_size() workspace keeps what the
+    // backward needs; backward() then consumes the same workspace.  Gradients of
+    // sum(out * dout) w.r.t. the inputs (fp32, any of drot/dtrans may be null) and the weights
+    // (fp32, reference order w_q..b_out concatenated, num_weights() values).
+    std::size_t train_workspace_size(std::int64_t B, std::int64_t L) const;
+    std::size_t num_weights() const;
+    void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                  const float* rot, const float* trans, const std::uint8_t* mask, const float* dout,
+                  float* ds, float* dz1, float* dz2, float* drot, float* dtrans, float* dweights,
+                  void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+    void grad_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
+                   const double* rot, const double* trans, const std::uint8_t* mask, const double* dout,
+                   double* out, double* ds, double* dz1, double* dz2, double* drot, double* dtrans,
+                   double* dweights);
+    bool backward_supported() const;
+    int launches_per_backward() const;
     void forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
                       const double* z2, const double* rot, const double* trans,
                       const std::uint8_t* mask, double* out);
@@ -113,9 +130,27 @@ public:
         float* colbias = nullptr;
         float* lse = nullptr;
         void* feat = nullptr;
+        // training extras (carve(..., train = true))
+        __nv_bfloat16* o_hat = nullptr;    // [BH, L, dv_pad]
+        __nv_bfloat16* dout_bf16 = nullptr; // [BL, din_ld]
+        float* dfeat = nullptr;            // [BL, feat_ld]
+        __nv_bfloat16* do_hat = nullptr;   // [BH, L, dv_pad]
+        float* Dvec = nullptr;             // [BH, L]
+        float* dq_acc = nullptr;           // [BH, L, acc_ld]
+        float* dk_acc = nullptr;
+        float* dv_acc = nullptr;
+        __nv_bfloat16* dproj = nullptr;    // [BL, nproj_ld]
+        float* dz1_epi = nullptr;          // [BL, r d_z]
+        float* drot_epi = nullptr;         // [BL, 9]
+        float* dt_epi = nullptr;           // [BL, 3]
+        float* dt_c = nullptr;             // [BL, 3]
+        float* red = nullptr;              // [H + H d_z]  d(g) | d(w_l w_bias)
+        float* dwproj = nullptr;           // [d_in, n_proj]
         std::size_t bytes = 0;
     };
-    Workspace carve(void* base, std::int64_t B, std::int64_t L) const;
+    static constexpr int kAccLd = 448;
+    int nproj_ld() const { return (dims_.n_proj + 7) / 8 * 8; }
+    Workspace carve(void* base, std::int64_t B, std::int64_t L, bool train = false) const;
 
 private:
     void upload_weights();
@@ -133,6 +168,7 @@ private:
     float* d_bout_ = nullptr;             // [d_in]
     float* d_head_g_ = nullptr;           // [H]
     float* d_wl_bias_ = nullptr;          // [H, d_z]
+    float* d_bwd_scale_ = nullptr;        // [H + 1]: w_l w_c sigmoid(gamma_raw_h) | w_l
     float k_scale_ = 0.f;
     bool dirty_ = true;
     std::mutex upload_mu_;
@@ -141,6 +177,7 @@ private:
     std::size_t h_stage_bytes_ = 0;
     void* d_stage_ = nullptr;
     std::size_t d_stage_bytes_ = 0;
+    void ensure_staging(std::size_t host_bytes, std::size_t dev_bytes);
     cudaStream_t own_stream_ = nullptr;
     // timing
     bool timing_ = false;

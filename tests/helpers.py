@@ -136,3 +136,52 @@ def expected_lifted(shape, w, batch, b):
     cb = -0.5 * g * (gk ** 2).sum((-1, -2))
     cb = np.where(valid[None], cb, -np.inf)
     return logits, v_parts, cb
+
+
+def oracle_backward(shape, w, batch, dout):
+    """Per-sample oracle gradients (fipa_oracle.flash_ipa_backward), stacked on the batch axis."""
+    cfg = oracle_cfg(shape)
+    res = []
+    for b in range(batch["s"].shape[0]):
+        res.append(fo.flash_ipa_backward(batch["s"][b], batch["z1"][b], batch["z2"][b], batch["rot"][b],
+                                         batch["trans"][b], batch["mask"][b], cfg, w, dout[b]))
+    out = {k: np.stack([r[k] for r in res]) for k in ("s", "z1", "z2", "rot", "trans")}
+    for n in fo.WEIGHT_NAMES:
+        out[n] = sum(r[n] for r in res)
+    return out
+
+
+def gpu_train_device(model, batch, dout):
+    """forward_train + backward through the C ABI over torch-owned device buffers.
+    Returns (out, grads, workspace, layouts)."""
+    import torch
+
+    dev = torch.device("cuda:0")
+    B, L = batch["s"].shape[:2]
+    t = {k: torch.from_numpy(np.ascontiguousarray(batch[k], dtype=np.float32)).to(dev)
+         for k in ("s", "z1", "z2", "rot", "trans")}
+    mask = torch.from_numpy(np.ascontiguousarray(batch["mask"], dtype=np.uint8)).to(dev)
+    dt = torch.from_numpy(np.ascontiguousarray(dout, dtype=np.float32)).to(dev)
+    out = torch.empty((B, L, model.config["d_in"]), dtype=torch.float32, device=dev)
+    nbytes = model.train_workspace_size(B, L)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    g = {k: torch.full_like(v, float("nan")) for k, v in t.items()}
+    gw = torch.full((model.num_weights(),), float("nan"), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    p = {k: v.data_ptr() for k, v in t.items()}
+    model.forward_train_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], mask.data_ptr(),
+                               out.data_ptr(), ws.data_ptr(), nbytes, st)
+    model.backward_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], mask.data_ptr(),
+                          dt.data_ptr(), g["s"].data_ptr(), g["z1"].data_ptr(), g["z2"].data_ptr(),
+                          g["rot"].data_ptr(), g["trans"].data_ptr(), gw.data_ptr(), ws.data_ptr(), nbytes, st)
+    torch.cuda.synchronize()
+    grads = {k: v.cpu().numpy().astype(np.float64) for k, v in g.items()}
+    flat = gw.cpu().numpy().astype(np.float64)
+    sh = fo.weight_shapes(oracle_cfg({k: model.config[k] for k in MAIN}))
+    o = 0
+    for n in fo.WEIGHT_NAMES:
+        size = int(np.prod(sh[n]))
+        grads[n] = flat[o:o + size].reshape(sh[n])
+        o += size
+    return (out.cpu().numpy().astype(np.float64), grads, ws,
+            (model.workspace_layout(B, L), model.train_workspace_layout(B, L)))

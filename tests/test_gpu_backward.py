@@ -1,0 +1,116 @@
+"""GPU parity of the training path (forward_train + backward through the C ABI) against the
+float64 oracle backward (oracle/fipa_oracle.flash_ipa_backward, pinned by finite differences of
+the reference forward).  bf16 operands / fp32 accumulation: gate 2e-2 on max|a-b|/max|ref| per
+gradient tensor, the oracle fed the same bf16-rounded inputs and weights."""
+
+import numpy as np
+import pytest
+
+import bwd_emulation as be
+from helpers import (BF16_TOL, MAIN, TINY, gpu_forward_device, gpu_train_device, make_batch,
+                     oracle_backward, oracle_forward, oracle_weights_for, rel_dev, ws_view)
+from oracle import fipa_oracle as fo
+
+pytestmark = pytest.mark.gpu
+
+GRADS = ("s", "z1", "z2", "rot", "trans") + fo.WEIGHT_NAMES
+
+
+def _model(fipa, shape, seed=0):
+    m = fipa.Model(**shape, precision="bf16", seed=seed, enforce_head_cap=False)
+    w = m.weights()
+    # non-trivial gamma and output bias so their gradients are exercised
+    w["gamma_raw"] = np.linspace(-0.6, 0.9, shape["heads"])
+    w["b_out"] = np.random.default_rng(seed).standard_normal(shape["d_in"]) * 0.1
+    m.set_weights(w)
+    return m
+
+
+def _check(fipa, shape, B, L, seed, mask_frac=0.0, scale=1.0, tol=BF16_TOL):
+    model = _model(fipa, shape, seed)
+    w = oracle_weights_for(model, "bf16")
+    batch = make_batch(shape, B, L, seed=seed, translation_scale=scale, mask_frac=mask_frac, bf16=True)
+    dout = np.random.default_rng(seed + 1).standard_normal((B, L, shape["d_in"]))
+    out, g, _, _ = gpu_train_device(model, batch, dout)
+    ref_out = oracle_forward(shape, w, batch)
+    assert rel_dev(ref_out, out) < tol
+    ref = oracle_backward(shape, w, batch, dout)
+    errs = {n: rel_dev(ref[n], g[n]) for n in GRADS}
+    bad = {n: e for n, e in errs.items() if not (np.isfinite(e) and e < tol)}
+    assert not bad, f"gradients off: {bad} (all: {errs})"
+    return errs
+
+
+@pytest.mark.parametrize("L", [64, 200, 300])
+def test_backward_main_shape(fipa, L):
+    _check(fipa, MAIN, 2, L, seed=10 + L, mask_frac=0.1)
+
+
+def test_backward_tiny_shape(fipa):
+    _check(fipa, TINY, 3, 37, seed=3, mask_frac=0.2)
+
+
+def test_backward_protein_scale_coordinates(fipa):
+    """30 A translations: the hi/lo translation split must keep the gradients inside the gate."""
+    _check(fipa, MAIN, 1, 256, seed=4, scale=30.0)
+
+
+def test_backward_fully_masked_sample_is_zero(fipa):
+    model = _model(fipa, MAIN, 2)
+    batch = make_batch(MAIN, 2, 80, seed=2, bf16=True)
+    batch["mask"][1, :] = False
+    dout = np.random.default_rng(0).standard_normal((2, 80, MAIN["d_in"]))
+    _, g, _, _ = gpu_train_device(model, batch, dout)
+    for n in ("s", "z1", "z2", "rot", "trans"):
+        assert np.all(g[n][1] == 0.0), n
+        assert np.all(np.isfinite(g[n])), n
+
+
+def test_training_forward_matches_inference_forward(fipa):
+    model = _model(fipa, MAIN, 6)
+    batch = make_batch(MAIN, 2, 130, seed=6, mask_frac=0.1, bf16=True)
+    out_inf, _, _ = gpu_forward_device(model, batch)
+    out_tr, _, _, _ = gpu_train_device(model, batch, np.zeros((2, 130, MAIN["d_in"])))
+    assert np.array_equal(out_inf, out_tr)
+
+
+def test_attention_backward_stage_parity(fipa):
+    """dO_hat, D and the three attention accumulators against the layout emulation
+    (tests/bwd_emulation.py) fed the device's own q/k/v_hat, O_hat and lse."""
+    B, L = 1, 160
+    shape = MAIN
+    model = _model(fipa, shape, 8)
+    batch = make_batch(shape, B, L, seed=8, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(9).standard_normal((B, L, shape["d_in"]))
+    _, _, ws, ((off, dims), (toff, tdims)) = gpu_train_device(model, batch, dout)
+    n_proj, dqk_pad, dv_pad, nfeat = dims
+    acc_ld = tdims[0]
+    H = shape["heads"]
+    q = ws_view(ws, off[3], H * L * dqk_pad, "bf16").reshape(H, L, dqk_pad)
+    k = ws_view(ws, off[4], H * L * dqk_pad, "bf16").reshape(H, L, dqk_pad)
+    v = ws_view(ws, off[5], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
+    lse = ws_view(ws, off[7], H * L, "f32").reshape(H, L)
+    o = ws_view(ws, toff[0], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
+    do = ws_view(ws, toff[1], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
+    D = ws_view(ws, toff[2], H * L, "f32").reshape(H, L)
+    o_ref, lse_ref = be.attention(q, k, v, L)
+    assert rel_dev(o_ref, o) < 1e-2
+    assert rel_dev(lse_ref, lse) < 1e-3
+    assert rel_dev((do * o).sum(-1), D) < 1e-3
+    dq_r, dk_r, dv_r = be.attention_backward(q, k, v, lse, do, D)
+    for name, idx, ref in (("dq", 3, dq_r), ("dk", 4, dk_r), ("dv", 5, dv_r)):
+        got = ws_view(ws, toff[idx], H * L * acc_ld, "f32").reshape(H, L, acc_ld)
+        assert rel_dev(ref[..., :432], got[..., :432]) < 1e-2, name
+
+
+def test_flash_grad_host_api_matches_device(fipa):
+    model = _model(fipa, TINY, 12)
+    batch = make_batch(TINY, 2, 50, seed=12, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(1).standard_normal((2, 50, TINY["d_in"]))
+    out_d, g_d, _, _ = gpu_train_device(model, batch, dout)
+    out_h, g_h = model.flash_grad(batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"], dout,
+                                  mask=batch["mask"])
+    assert rel_dev(out_d, out_h) < 1e-6
+    for n, m in (("s", "s"), ("z1", "z1"), ("rot", "rotations"), ("trans", "translations"), ("w_q", "w_q"),
+                 ("gamma_raw", "gamma_raw"), ("w_out", "w_out")):
+        assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
