@@ -102,7 +102,7 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 
 // 32 consecutive per-query floats starting at q (entries >= L come back as `fill`).
 __device__ __forceinline__ void load_vec32(const float* base, int q, int L, float fill, float* out) {
-    if (q + 32 <= L && (q & 3) == 0) {
+    if (q + 32 <= L && (reinterpret_cast<uintptr_t>(base + q) & 15) == 0) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const float4 f = __ldg(reinterpret_cast<const float4*>(base + q) + k);

@@ -60,7 +60,7 @@ struct Attn2Params {
     const float* trans;
     __nv_bfloat16* feat_out;
     float* lse;
-    __nv_bfloat16* o_save;  // [BH, L, dv_pad] normalised O_hat for the backward, or null
+    float* o_save;  // [BH, L, dv_pad] normalised O_hat (fp32) for the backward, or null
     int dv_pad;
 };
 
@@ -516,28 +516,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (half == 0 && qi < p.L)
             p.lse[static_cast<int64_t>(bh) * p.L + qi] = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
         if (p.o_save != nullptr) {
-            // Training: keep the normalised O_hat row (bf16) for bwd_prep (D = rowsum(dO*O) and
-            // the pair-contraction gradient).  tcgen05.ld is warp-collective: load first, then
-            // store only rows inside the sequence.
+            // Training: keep the normalised O_hat row in fp32 for bwd_prep.  D = rowsum(dO*O) is
+            // compared against dP = dO.V_j^T of the (often near one-hot) attended keys, where
+            // dP - D is a small difference: a bf16 O would put its 2^-9 rounding straight into dS.
+            // tcgen05.ld is warp-collective: load first, store only rows inside the sequence.
             const int n16 = p.dv_mma / 16;
             const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
-            __nv_bfloat16* orow = p.o_save + (static_cast<int64_t>(bh) * p.L + (qi < p.L ? qi : 0)) * p.dv_pad;
+            float* orow = p.o_save + (static_cast<int64_t>(bh) * p.L + (qi < p.L ? qi : 0)) * p.dv_pad;
             for (int ch = lo; ch < hi; ++ch) {
                 uint32_t o[16];
                 ptx::tmem_ld16(tl + 16 * ch, o);
                 ptx::tmem_wait_ld();
                 if (qi < p.L) {
-                    uint4 w0, w1;
-                    w0.x = ptx::pack_bf16x2(__uint_as_float(o[0]) * inv_l, __uint_as_float(o[1]) * inv_l);
-                    w0.y = ptx::pack_bf16x2(__uint_as_float(o[2]) * inv_l, __uint_as_float(o[3]) * inv_l);
-                    w0.z = ptx::pack_bf16x2(__uint_as_float(o[4]) * inv_l, __uint_as_float(o[5]) * inv_l);
-                    w0.w = ptx::pack_bf16x2(__uint_as_float(o[6]) * inv_l, __uint_as_float(o[7]) * inv_l);
-                    w1.x = ptx::pack_bf16x2(__uint_as_float(o[8]) * inv_l, __uint_as_float(o[9]) * inv_l);
-                    w1.y = ptx::pack_bf16x2(__uint_as_float(o[10]) * inv_l, __uint_as_float(o[11]) * inv_l);
-                    w1.z = ptx::pack_bf16x2(__uint_as_float(o[12]) * inv_l, __uint_as_float(o[13]) * inv_l);
-                    w1.w = ptx::pack_bf16x2(__uint_as_float(o[14]) * inv_l, __uint_as_float(o[15]) * inv_l);
-                    reinterpret_cast<uint4*>(orow + 16 * ch)[0] = w0;
-                    reinterpret_cast<uint4*>(orow + 16 * ch)[1] = w1;
+                    float4* dst = reinterpret_cast<float4*>(orow + 16 * ch);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
+                                              __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
                 }
             }
         }

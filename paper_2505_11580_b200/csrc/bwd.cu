@@ -5,7 +5,7 @@
 //                proj/src/geometry.cpp:70-76) run backwards.  From dfeat = dOut . w_out^T and the
 //                saved O_hat it writes dO_hat in the v_hat column layout of pack.cu
 //                ([dv | z1 (.) d(pair) | sum_p dg_p | sum_p dg_p | dg_p]), D = rowsum(dO_hat*O_hat)
-//                (bf16-rounded dO_hat, as the MMAs see it) and the epilogue's own gradients
+//                (bf16-rounded dO_hat as the MMAs see it, fp32 O_hat) and the epilogue's own gradients
 //                (z1 through the pair contraction, frames through R^T(g - t)).
 //   bwd_unpack : the lifts (proj/src/flash_ipa.cpp:23-126, pack.cu) run backwards.  It maps
 //                the attention accumulators dQ_acc = dS.K_hat, dK_acc = dS^T.Q_hat,
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
     float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
     for (int h = warp; h < H; h += 8) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
-        const __nv_bfloat16* o = a.ohat + hrow * d.dv_pad;
+        const float* o = a.ohat + hrow * d.dv_pad;
         const float* df = a.dfeat + row * d.feat_ld + static_cast<int64_t>(h) * d.seg;
         float ds[3] = {0.f, 0.f, 0.f};
         if (lane < Nv) {
@@ -67,8 +67,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
             float y[3], loc[3];
 #pragma unroll
             for (int x = 0; x < 3; ++x)
-                y[x] = __bfloat162float(o[vpts + 3 * p + x]) + __bfloat162float(o[vpair + x]) +
-                       __bfloat162float(o[vpair + 3 + x]) - t[x];
+                y[x] = o[vpts + 3 * p + x] + o[vpair + x] + o[vpair + 3 + x] - t[x];
 #pragma unroll
             for (int x = 0; x < 3; ++x) loc[x] = R[x] * y[0] + R[3 + x] * y[1] + R[6 + x] * y[2];
             const float nrm = sqrtf(loc[0] * loc[0] + loc[1] * loc[1] + loc[2] * loc[2]);
@@ -102,7 +101,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
                 const int e = col - c;
                 const float dpc = df[e % dz];
                 v = z1[e] * dpc;
-                atomicAdd(&s_dz1[e], __bfloat162float(o[col]) * dpc);
+                atomicAdd(&s_dz1[e], o[col] * dpc);
             } else if (col < vpts) {
                 v = ds[(col - vpair) % 3];
             } else if (col < vpts + 3 * Nv) {
@@ -112,7 +111,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
             }
             const __nv_bfloat16 vb = __float2bfloat16_rn(v);
             out[col] = vb;
-            if (col < d.dv_used) Dp += __bfloat162float(vb) * __bfloat162float(o[col]);
+            if (col < d.dv_used) Dp += __bfloat162float(vb) * o[col];
         }
         Dp = warp_sum(Dp);
         if (lane == 0) a.Dvec[hrow] = Dp;
@@ -146,7 +145,7 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
     for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) sm[e] = 0.f;
     const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
-    const int g0 = c + 3 * Nq, zq = g0 + 20, vpair = c + rdz;
+    const int g0 = c + 3 * Nq, zq = g0 + 21, vpair = c + rdz;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
     const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
 
@@ -200,18 +199,30 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
 #pragma unroll
             for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (ka[g0 + 9 + x] + ka[g0 + 12 + x]);
             float dgh = 0.f;
+            const float S1 = qa[g0 + 20];  // sum_j dS_ij, as rounded for the MMAs
+            float dAsum[3] = {0.f, 0.f, 0.f};
             if (lane < Nq) {
                 const int p = lane;
-                // query point p: A = R q_p + t,  dA = g sum_j dS_ij B_jp
-                float qp[3], dA[3], A[3];
+                // query point p: A = R q_p + t,
+                //   dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS_ij B_jp] - g A S1
+                // (the exact S1 = 0 is not assumed: subtracting g A S1 with the same rounded dS
+                // cancels the translation-sized common mode of the first term).
+                float qp[3], gB[3], A[3], dA[3];
 #pragma unroll
                 for (int x = 0; x < 3; ++x) {
                     qp[x] = pr[off_qp + (h * Nq + p) * 3 + x];
-                    dA[x] = qa[c + 3 * p + x] + qa[g0 + x] + qa[g0 + 3 + x];
+                    gB[x] = qa[c + 3 * p + x] + qa[g0 + x] + qa[g0 + 3 + x];
                 }
 #pragma unroll
                 for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
-                dgh += (A[0] * dA[0] + A[1] * dA[1] + A[2] * dA[2]) / g;
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    dA[x] = gB[x] - g * A[x] * S1;
+                    dAsum[x] = dA[x];
+                }
+                // d(-g/2 |A - B|^2)/dg summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
+                dgh += (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
+                       0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
 #pragma unroll
                 for (int x = 0; x < 3; ++x) {
                     dp[off_qp + (h * Nq + p) * 3 + x] =
@@ -255,12 +266,13 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
                     for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
                 }
             }
+#pragma unroll
+            for (int x = 0; x < 3; ++x) dt[x] += dAsum[x];  // query side: sum_p dA_p
             if (lane == 0) {
 #pragma unroll
                 for (int x = 0; x < 3; ++x)
-                    dt[x] += qa[g0 + 9 + x] + qa[g0 + 15 + x]                                   // query
-                             + g * kLn2 * (ka[g0 + x] + ka[g0 + 6 + x]) + float(Nq) * dW[x]   // key
-                             + va[vpair + x];                                                  // value
+                    dt[x] += g * kLn2 * (ka[g0 + x] + ka[g0 + 6 + x]) + float(Nq) * dW[x]   // key
+                             + va[vpair + x];                                                // value
             }
             dgh = warp_sum(dgh);
             dg += dgh;

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.split_k > 1) {
                 if (nk <= 0) continue;
                 float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
-                if (col0 + 32 <= p.N && (p.ldc % 4) == 0) {
+                if (col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         atomicAdd(reinterpret_cast<float4*>(out) + q,
@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.bias != nullptr && col < p.N) x += p.bias[col];
                 v[i] = zero_row ? 0.0f : x;
             }
-            const bool full_chunk = col0 + 32 <= p.N;
+            const size_t esz = p.out_bf16 ? 2 : 4;
+            const bool full_chunk = col0 + 32 <= p.N &&
+                                    ((reinterpret_cast<uintptr_t>(p.C) + (size_t(row) * p.ldc + col0) * esz) & 15) == 0;
             if (p.out_bf16) {
                 __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + int64_t(row) * p.ldc + col0;
                 if (full_chunk) {

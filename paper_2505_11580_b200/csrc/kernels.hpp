@@ -37,7 +37,7 @@ void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 struct LayerDims {
     int d_in, d_z, heads, c, n_query, n_value, rank;
     int n_proj;      // H*(3c + 6Nq + 3Nv): fused projection width
-    int dqk_used;    // c + 3Nq + 20 + r*d_z      (lifted query/key width, see pack.cu)
+    int dqk_used;    // c + 3Nq + 21 + r*d_z      (lifted query/key width, see pack.cu)
     int dqk_mma;     // dqk_used rounded up to 16  (MMA K extent of Q.K^T)
     int dqk_pad;     // dqk_used rounded up to 64  (row stride of q_hat / k_hat: 128-byte blocks)
     int dv_used;     // c + r*d_z + 6 + 3Nv       (v | z2 | t_hi | t_lo | R v_p)
@@ -80,7 +80,7 @@ struct AttnArgs {
     const float* trans;
     __nv_bfloat16* feat;   // [BL, feat]
     float* lse;            // [B*H, L] natural-log LSE of the shifted logits
-    __nv_bfloat16* o_save; // [B*H, L, dv_pad] normalised O_hat for the backward, or null
+    float* o_save;         // [B*H, L, dv_pad] normalised O_hat (fp32) for the backward, or null
     int B, L;
 };
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
@@ -109,7 +109,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
 
 struct BwdPrepArgs {
     const float* dfeat;           // [BL, feat_ld] dOut . w_out^T
-    const __nv_bfloat16* ohat;    // [B*H, L, dv_pad] saved by the forward
+    const float* ohat;            // [B*H, L, dv_pad] fp32, saved by the forward
     const float* z1;              // [BL, r*d_z]
     const float* rot;             // [BL, 9]
     const float* trans_c;         // [BL, 3] recentred

@@ -115,7 +115,7 @@ LayerDims Config::dims() const {
     d.n_value = int(n_value);
     d.rank = int(rank);
     d.n_proj = int(heads * (3 * c + 6 * n_query + 3 * n_value));
-    d.dqk_used = int(c + 3 * n_query + 20 + rank * d_z);
+    d.dqk_used = int(c + 3 * n_query + 21 + rank * d_z);
     d.dqk_mma = int(round_up(d.dqk_used, 16));
     d.dqk_pad = int(round_up(d.dqk_used, 64));
     d.dv_used = int(c + rank * d_z + 3 * n_value + 6);
@@ -465,7 +465,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     w.feat = take(BL * d.feat_ld * el);
     if (train) {
         const std::size_t rdz = std::size_t(d.rank) * d.d_z;
-        w.o_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));
+        w.o_hat = reinterpret_cast<float*>(take(BHL * d.dv_pad * 4));
         w.dout_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
         w.dfeat = reinterpret_cast<float*>(take(BL * d.feat_ld * 4));
         w.do_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));

@@ -131,7 +131,7 @@ public:
         float* lse = nullptr;
         void* feat = nullptr;
         // training extras (carve(..., train = true))
-        __nv_bfloat16* o_hat = nullptr;    // [BH, L, dv_pad]
+        float* o_hat = nullptr;            // [BH, L, dv_pad] fp32
         __nv_bfloat16* dout_bf16 = nullptr; // [BL, din_ld]
         float* dfeat = nullptr;            // [BL, feat_ld]
         __nv_bfloat16* do_hat = nullptr;   // [BH, L, dv_pad]

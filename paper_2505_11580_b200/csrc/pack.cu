@@ -15,13 +15,15 @@
 // bf16 logits accurate for protein-scale coordinates (tens of Angstrom), where a plain bf16
 // T_i q_p column loses ~1 logit unit.  Per head (L2E = log2 e, queries pre-scaled so that
 // S = q_hat . k_hat is in log2 units):
-//   q_hat = L2E*[ q | R_i q_p | Qbar hi,hi,lo | t_i hi,lo,hi ] | 1, 1 | L2E*z1_i | 0
-//   k_hat = [ (w_l/sqrt c) k | g R_j k_p | g t_j hi,lo,hi | g W_j hi,hi,lo ] | cb hi, lo |
+//   q_hat = L2E*[ q | R_i q_p | Qbar hi,hi,lo | t_i hi,lo,hi ] | 1, 1, 0 | L2E*z1_i | 0
+//   k_hat = [ (w_l/sqrt c) k | g R_j k_p | g t_j hi,lo,hi | g W_j hi,hi,lo ] | cb hi, lo, 1 |
 //           w_l w_bias[h] (.) z2_j | 0
 //   cb_j  = L2E * (-g/2 sum_p |T_j k_p|^2)   (-1e30 for masked keys, lo = 0)
 // The reference's |T_i q_p|^2 column (paired with -g/2) is constant along a query row and
 // cancels in the softmax, so it is dropped; its (ones, -g/2 |k|^2) pair becomes the folded
-// column bias cb.  Values:
+// column bias cb.  The (0, 1) column does not change the logits; it makes the backward's
+// dQ_acc = dS.K_hat carry sum_j dS_ij (as rounded for the MMA), so the translation-sized
+// query-side terms can be formed as sum_j dS_ij (t_j - t_i) without cancellation error.  Values:
 //   v_hat = [ v | z2_j flat | t_j hi (3) | t_j lo (3) | R_j v_p (3Nv) | 0 ]
 // (sum_j p_ij T_j v_p = sum_j p_ij R_j v_p + sum_j p_ij t_j, translation kept to ~2^-17).
 // For the fp32 path the same layout is written with hi = value, lo = 0.
@@ -139,8 +141,8 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     OutT* qh = static_cast<OutT*>(a.qhat);
     OutT* kh = static_cast<OutT*>(a.khat);
     OutT* vh = static_cast<OutT*>(a.vhat);
-    const int g0 = c + 3 * Nq;        // start of the 20 translation/bias columns
-    const int zq = g0 + 20;           // start of the pair-factor columns
+    const int g0 = c + 3 * Nq;        // start of the 21 translation/bias columns
+    const int zq = g0 + 21;           // start of the pair-factor columns
     const int qk_used = d.dqk_used;
     const int v_pair = c + rdz, v_used = d.dv_used;
 
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
                     qv[u] = kL2E * s_rq[h * Nq * 3 + (cc - c)];
                     kv[u] = g * s_rk[h * Nq * 3 + (cc - c)];
                 } else if (cc < zq) {
-                    const int e = cc - g0;     // 0..19
+                    const int e = cc - g0;     // 0..20
                     const int x = e % 3;
                     if (e < 9) {               // <Qbar_i, g t_j>:  [Qh Qh Ql] . [th tl th]
                         const float qq = kL2E * hd[x], tt = g * t[x];
@@ -174,9 +176,12 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
                         const float tq = kL2E * t[x], ww = g * hd[3 + x];
                         qv[u] = (e >= 12 && e < 15) ? lo_part<OutT>(tq) : hi_part<OutT>(tq);
                         kv[u] = e < 15 ? hi_part<OutT>(ww) : lo_part<OutT>(ww);
-                    } else {                   // folded column bias: [1 1] . [cb_hi cb_lo]
+                    } else if (e < 20) {       // folded column bias: [1 1] . [cb_hi cb_lo]
                         qv[u] = 1.0f;
                         kv[u] = e == 18 ? hi_part<OutT>(cb) : (valid ? lo_part<OutT>(cb) : 0.f);
+                    } else {                   // [0] . [1]: logit-neutral; in the backward
+                        qv[u] = 0.f;           // dS.K_hat picks up sum_j dS_ij here
+                        kv[u] = 1.0f;
                     }
                 } else if (cc < qk_used) {
                     const int e = cc - zq;

@@ -52,14 +52,15 @@ def pack(cfg: fo.IpaConfig, w, s, z1, z2, rot, trans_c, mask):
     cb_lo = np.where(valid, _lo(cb), 0.0)
     Qb, T, gt, gW = L2E * qbar, L2E * t, g * t, g * W
     ones = np.ones((H, L, 1))
+    zeros = np.zeros((H, L, 1))
     z1f = np.broadcast_to(z1.reshape(1, L, rdz), (H, L, rdz))
     z2f = np.broadcast_to(z2.reshape(1, L, rdz), (H, L, rdz))
     wlb = np.repeat((w["w_l"] * w["w_bias"])[:, None, :], cfg.rank, 1).reshape(H, 1, rdz)
     q_hat = np.concatenate([L2E * q, L2E * rq.reshape(H, L, -1), _hi(Qb), _hi(Qb), _lo(Qb),
-                            _hi(T), _lo(T), _hi(T), ones, ones, L2E * z1f], -1)
+                            _hi(T), _lo(T), _hi(T), ones, ones, zeros, L2E * z1f], -1)
     k_hat = np.concatenate([w["w_l"] / math.sqrt(c) * k, g * rk.reshape(H, L, -1), _hi(gt), _lo(gt),
                             _hi(gt), _hi(gW), _hi(gW), _lo(gW), cb_hi[..., None], cb_lo[..., None],
-                            wlb * z2f], -1)
+                            ones, wlb * z2f], -1)
     v_hat = np.concatenate([v, z2f, _hi(t), _lo(t), rv.reshape(H, L, -1)], -1)
     return dict(q_hat=q_hat, k_hat=k_hat, v_hat=v_hat, proj=(q, k, v, qp, kp, vp), g=g[:, 0, 0])
 
@@ -129,14 +130,16 @@ def unpack(cfg, w, pk, rot, trans_c, z1, z2, dq_acc, dk_acc, dv_acc):
     L = rot.shape[0]
     q, k, v, qp, kp, vp = pk["proj"]
     g = pk["g"][:, None, None]
-    g0, zq = c + 3 * Nq, c + 3 * Nq + 20
-    # query side
+    g0, zq = c + 3 * Nq, c + 3 * Nq + 21
+    # query side: dA = g sum_j dS (B_j - A_i) with S1 = sum_j dS_ij from the (0, 1) column
     dq = dq_acc[..., :c]
-    dA = dq_acc[..., c:g0].reshape(H, L, Nq, 3) + (dq_acc[..., g0:g0 + 3] + dq_acc[..., g0 + 3:g0 + 6])[:, :, None]
-    dt_q = dq_acc[..., g0 + 9:g0 + 12] + dq_acc[..., g0 + 15:g0 + 18]
-    dz1 = dq_acc[..., zq:zq + rdz].sum(0).reshape(L, cfg.rank, cfg.d_z)
+    S1 = dq_acc[..., g0 + 20]
+    gB = dq_acc[..., c:g0].reshape(H, L, Nq, 3) + (dq_acc[..., g0:g0 + 3] + dq_acc[..., g0 + 3:g0 + 6])[:, :, None]
     A = np.einsum("lab,hlpb->hlpa", rot, qp) + trans_c[None, :, None]
-    dg = (A * dA).sum((-1, -2)) / g[..., 0]
+    dA = gB - g[..., None] * A * S1[..., None, None]
+    dt_q = dA.sum(2)
+    dz1 = dq_acc[..., zq:zq + rdz].sum(0).reshape(L, cfg.rank, cfg.d_z)
+    dg = (A * gB).sum((-1, -2)) / g[..., 0] - 0.5 * (A ** 2).sum((-1, -2)) * S1
     # key side
     dk = w["w_l"] / math.sqrt(c) * LN2 * dk_acc[..., :c]
     cs = dk_acc[..., g0 + 18]
