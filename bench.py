@@ -5,7 +5,8 @@ Workload (BASELINE.json configs[1] shape): the north-star FlashIPA layer
 (c_s 256, c_z 128, c_hidden 128, 8 heads, 8 qk-points, 12 v-points, z_factor_rank 2) on
 B=8 sequences of L=1024 residues, bf16 operands / fp32 accumulation, random-init weights
 (IpaWeights::init, seed 0), synthetic reference-distribution inputs.
-A step = one layer forward over the batch (see config.pass).
+A step = one layer forward + backward over the batch (cfg2, "fwd+bwd bf16"); --pass fwd times the
+forward alone.
 
 --impl ours (default): libfipa_b200.so through the C ABI; device-timed with CUDA events on the
    stream the kernels run on, L2 flushed (256 MiB write) before every timed step, max over ranks.
@@ -46,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-L", type=int, default=0, help="residues per CPU sample (default L)")
+    ap.add_argument("--pass", dest="pass_", choices=["fwd+bwd", "fwd"], default="fwd+bwd")
     return ap.parse_args()
 
 
@@ -60,6 +62,13 @@ def attn_flops(shape, B, L):
     (IpaConfig::qk_width / v_width, proj/include/fipa/ipa.hpp:27-28)."""
     qk, v = dims(shape)
     return 2.0 * B * shape["heads"] * L * L * (qk + v)
+
+
+def attn_bwd_flops(shape, B, L):
+    """Algorithmic attention-backward FLOPs: 2*B*H*L^2*(3*D_qk + 2*D_v)
+    (S recompute, dP, dV, dQ, dK); the dQ kernel's second S/dP recompute is not counted."""
+    qk, v = dims(shape)
+    return 2.0 * B * shape["heads"] * L * L * (3 * qk + 2 * v)
 
 
 def load_peaks():
@@ -211,15 +220,29 @@ def run_ours(args, shape):
     host = synth_inputs(B, L, shape, seed=1234 + rank)
     t = {k: torch.from_numpy(v).to(dev) for k, v in host.items()}
     out = torch.empty((B, L, shape["d_in"]), dtype=torch.float32, device=dev)
-    ws_bytes = model.workspace_size(B, L)
+    train = args.pass_ == "fwd+bwd"
+    ws_bytes = model.train_workspace_size(B, L) if train else model.workspace_size(B, L)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    if train:
+        dout = torch.randn((B, L, shape["d_in"]), dtype=torch.float32, device=dev,
+                           generator=torch.Generator(device=dev).manual_seed(99 + rank))
+        grads = {k: torch.empty_like(t[k]) for k in ("s", "z1", "z2", "rot", "trans")}
+        gw = torch.empty(model.num_weights(), dtype=torch.float32, device=dev)
+    p = {k: v.data_ptr() for k, v in t.items()}
 
     def step():
-        model.forward_device(B, L, t["s"].data_ptr(), t["z1"].data_ptr(), t["z2"].data_ptr(),
-                             t["rot"].data_ptr(), t["trans"].data_ptr(), t["mask"].data_ptr(),
-                             out.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+        if not train:
+            model.forward_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], p["mask"],
+                                 out.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+            return
+        model.forward_train_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], p["mask"],
+                                   out.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+        model.backward_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], p["mask"],
+                              dout.data_ptr(), grads["s"].data_ptr(), grads["z1"].data_ptr(),
+                              grads["z2"].data_ptr(), grads["rot"].data_ptr(), grads["trans"].data_ptr(),
+                              gw.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
 
     for _ in range(args.warmup):
         step()
@@ -240,7 +263,7 @@ def run_ours(args, shape):
             b.record(stream)
             if stage_timing:
                 b.synchronize()
-                stages.append(model.stage_times())
+                stages.append(model.stage_times() + (model.bwd_stage_times() if train else []))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -261,11 +284,19 @@ def run_ours(args, shape):
     residues = B * L * world * args.steps
     value = residues / (ms_total / 1e3)
 
-    st = np.array(stages, dtype=np.float64)  # recenter, cast, proj, pack, attn, out
-    st_mean = st.mean(0) if len(st) else np.zeros(6)
-    attn_ms = float(st_mean[4])
+    st = np.array(stages, dtype=np.float64)  # fwd: recenter, cast, proj, pack, attn, out (+ bwd)
+    st_mean = st.mean(0) if len(st) else np.zeros(17 if train else 6)
+    fwd_names = ["recenter", "cast", "proj_gemm", "pack", "attn_fwd+epilogue", "out_gemm"]
+    bwd_names = ["bwd_dout", "bwd_dfeat_gemm", "bwd_dw_out_gemm", "bwd_prep", "attn_bwd_dkdv", "attn_bwd_dq",
+                 "bwd_unpack", "bwd_recenter", "bwd_ds_gemm", "bwd_dw_gemm", "bwd_scatter"]
+    names = fwd_names + (bwd_names if train else [])
+    stage_ms = {k: float(v) for k, v in zip(names, st_mean)}
+    attn_ms = stage_ms["attn_fwd+epilogue"]
     flops = attn_flops(shape, B, L)
     achieved = flops / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
+    bwd_attn_ms = (stage_ms["attn_bwd_dkdv"] + stage_ms["attn_bwd_dq"]) if train else 0.0
+    bflops = attn_bwd_flops(shape, B, L)
+    achieved_bwd = bflops / (bwd_attn_ms / 1e3) / 1e12 if bwd_attn_ms > 0 else None
     peak, peak_sus, peak_kind = load_peaks()
 
     traffic = None
@@ -282,21 +313,32 @@ def run_ours(args, shape):
     e2e = None
     if not args.no_e2e:
         hin = {k: host[k].astype(np.float64) for k in ("s", "z1", "z2", "rot", "trans")}
-        model.flash(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], mask=host["mask"])
+        hdout = np.random.default_rng(99).standard_normal((B, L, shape["d_in"]))
+
+        def e2e_step():
+            if train:
+                model.flash_grad(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], hdout,
+                                 mask=host["mask"])
+            else:
+                model.flash(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], mask=host["mask"])
+
+        e2e_step()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         n_e2e = max(3, min(args.steps, 10))
         for _ in range(n_e2e):
-            model.flash(hin["s"], hin["z1"], hin["z2"], hin["rot"], hin["trans"], mask=host["mask"])
+            e2e_step()
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        h2d = 4 * B * L * (shape["d_in"] + 2 * shape["rank"] * shape["d_z"] + 12) + B * L
-        d2h = 4 * B * L * shape["d_in"]
+        n_in = B * L * (shape["d_in"] + 2 * shape["rank"] * shape["d_z"] + 12)
+        h2d = 4 * (n_in + (B * L * shape["d_in"] if train else 0)) + B * L
+        d2h = 4 * B * L * shape["d_in"] + (4 * (n_in + model.num_weights()) if train else 0)
         e2e = {"value": B * L * world * n_e2e / float(el.item()), "unit": "residues/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "Model.flash (float64 numpy in/out, fipa_layer_forward_host)"}
+               "api": ("Model.flash_grad (float64 numpy in/out, fipa_layer_grad_host: forward_train + backward)"
+                       if train else "Model.flash (float64 numpy in/out, fipa_layer_forward_host)")}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -317,28 +359,42 @@ def run_ours(args, shape):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic (reference input distribution), random-init weights",
-            "config": {"workload": f"FlashIPA layer forward, B={B} L={L} per GPU (cfg2 shape; backward pending)",
-                       "pass": "fwd", "model": "FlashIPA layer", "global_batch": B * world, "seq_len": L,
+            "config": {"workload": f"FlashIPA layer {args.pass_}, B={B} L={L} per GPU (BASELINE cfg2)",
+                       "pass": args.pass_, "model": "FlashIPA layer", "global_batch": B * world, "seq_len": L,
                        "shape": shape, "parallelism": f"dp{world} (independent samples)",
                        "l2": "flushed (256 MiB write) before every timed step"},
             "attn_tflops": achieved,
-            "stage_ms": {k: float(v) for k, v in zip(
-                ["recenter", "cast", "proj_gemm", "pack", "attn_fwd+epilogue", "out_gemm"], st_mean)},
-            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel", "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
-                         "traffic": traffic,
-                         "algorithmic": f"2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per launch"},
+            "attn_bwd_tflops": achieved_bwd,
+            "stage_ms": stage_ms,
+            "roofline": roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus,
+                                       peak_kind, traffic),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": model.forward_launches() * args.steps,
+            "gpu_launches": (model.forward_launches() + (model.backward_launches() if train else 0)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus, peak_kind, traffic):
+    """Roofline of the dominant attention kernel(s) of the step (tensor-bound)."""
+    fwd = {"bound": "tensor", "kernel": "attn_fwd_2sm_kernel", "achieved": achieved, "peak": peak,
+           "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+           "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})", "traffic": traffic,
+           "algorithmic": f"2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per launch"}
+    if not train or not achieved_bwd:
+        return fwd
+    bwd_ms = stage_ms["attn_bwd_dkdv"] + stage_ms["attn_bwd_dq"]
+    if bwd_ms < stage_ms["attn_fwd+epilogue"]:
+        return fwd
+    return {"bound": "tensor", "kernel": "attn_bwd_kernel<true> + attn_bwd_kernel<false> (dK/dV + dQ)",
+            "achieved": achieved_bwd, "peak": peak, "unit": "TFLOP/s", "frac": achieved_bwd / peak,
+            "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})", "traffic": None,
+            "algorithmic": f"2*B*H*L^2*(3*D_qk+2*D_v) = {bflops:.4g} FLOP per backward",
+            "forward_kernel": fwd}
 
 
 def main():

@@ -157,6 +157,9 @@ int fipa_layer_forward_launches(const fipa_layer* layer);
  * order recenter, cast, projection, pack, attention, output and returns the count. */
 int fipa_layer_set_timing(fipa_layer* layer, int enable);
 int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n);
+/* Backward stage times (ms) in the order dout, dfeat, dw_out, prep, attn_kv, attn_q, unpack,
+ * recenter, ds, dW, scatter; same enable switch. */
+int fipa_layer_bwd_stage_times(const fipa_layer* layer, float* ms, int n);
 
 #ifdef __cplusplus
 }

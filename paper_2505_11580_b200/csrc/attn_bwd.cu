@@ -464,7 +464,7 @@ bool attn_bwd_supported(const LayerDims& d) {
     return smem_layout(p).total + 1024 <= 232448;
 }
 
-void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream) {
+void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream, int which) {
     if (!attn_bwd_supported(d)) throw std::invalid_argument("tcgen05 attention backward: unsupported widths");
     const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
     const int nqk = (d.dqk_mma + 63) / 64, nv = (d.dv_mma + 63) / 64;
@@ -472,7 +472,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     auto stat = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), BM, nb); };
     auto tile = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), 32, nb); };
     auto slice = [&](const void* x) { return make_map_3d_bf16(x, ld_of(x), a.L, BH, ld_of(x), 64, kSlice); };
-    {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
+    if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
         p.L = a.L;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
@@ -487,7 +487,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
                                      stat(a.vhat, nv),  tile(a.dohat, nv), slice(a.qhat)};
         launch<true>(d, a, p, maps, stream);
     }
-    {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
+    if (which & 2) {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
         BwdParams p{};
         p.L = a.L;
         p.role[0] = make_role(d.dqk_mma, 0);

@@ -307,6 +307,11 @@ public:
         t.resize(fipa_layer_stage_times(layer_, t.data(), 16));
         return t;
     }
+    std::vector<float> bwd_stage_times() const {
+        std::vector<float> t(16);
+        t.resize(fipa_layer_bwd_stage_times(layer_, t.data(), 16));
+        return t;
+    }
     std::string precision() const { return precision_name_; }
     py::dict config() const {
         py::dict d;
@@ -374,6 +379,7 @@ PYBIND11_MODULE(_fipa_b200, m) {
              "Forward + backward (gradient of sum(out * dout)) on the GPU")
         .def("set_timing", &Model::set_timing, py::arg("enable"))
         .def("stage_times", &Model::stage_times)
+        .def("bwd_stage_times", &Model::bwd_stage_times)
         .def_property_readonly("precision", &Model::precision)
         .def_property_readonly("config", &Model::config);
 }

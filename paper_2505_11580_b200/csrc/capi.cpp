@@ -285,6 +285,14 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
     return 8;
 }
 
+int fipa_layer_bwd_stage_times(const fipa_layer* layer, float* ms, int n) {
+    if (layer == nullptr || ms == nullptr) return 0;
+    const auto t = layer->impl.bwd_stage_times();
+    int k = 0;
+    for (; k < n && k < int(t.size()); ++k) ms[k] = t[k];
+    return k;
+}
+
 int fipa_layer_backward_launches(const fipa_layer* layer) {
     return layer ? layer->impl.launches_per_backward() : 0;
 }

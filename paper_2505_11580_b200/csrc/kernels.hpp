@@ -105,7 +105,8 @@ struct AttnBwdArgs {
     int B, L;
 };
 bool attn_bwd_supported(const LayerDims& d);
-void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream);
+// which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both
+void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream, int which = 3);
 
 struct BwdPrepArgs {
     const float* dfeat;           // [BL, feat_ld] dOut . w_out^T

@@ -353,6 +353,8 @@ FlashIpaLayer::~FlashIpaLayer() {
     if (own_stream_) cudaStreamDestroy(own_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
+    for (auto& e : evb_)
+        if (e) cudaEventDestroy(e);
 }
 
 void FlashIpaLayer::release_device() {
@@ -518,7 +520,19 @@ void FlashIpaLayer::set_timing(bool on) {
     timing_ = on;
     if (on && !ev_[0]) {
         for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        for (auto& e : evb_) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     }
+}
+
+std::vector<float> FlashIpaLayer::bwd_stage_times() const {
+    std::vector<float> out;
+    if (!bwd_timed_once_) return out;
+    for (int i = 0; i < kBwdStages; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, evb_[i], evb_[i + 1]) != cudaSuccess) ms = -1.f;
+        out.push_back(ms);
+    }
+    return out;
 }
 
 std::vector<float> FlashIpaLayer::stage_times() const {
@@ -749,11 +763,16 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
     float* dw_out = dweights + woff[8];
     float* db_out = dweights + woff[9];
 
+    auto mark = [&](int i) {
+        if (timing_) cuda_check(cudaEventRecord(evb_[i], stream), "cudaEventRecord");
+    };
+    mark(0);
     cuda_check(cudaMemsetAsync(dw_out, 0, (woff[10] - woff[8]) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.red, 0, (H + std::size_t(H) * d.d_z) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.dwproj, 0, std::size_t(d.d_in) * d.n_proj * 4, stream), "memset");
 
     launch_bwd_dout(dout, mask, ws.dout_bf16, d.din_ld, db_out, BL, d.d_in, stream);
+    mark(1);
     {  // dfeat = dOut . w_out^T
         GemmArgs g;
         g.A = ws.dout_bf16;
@@ -768,6 +787,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         g.K = d.d_in;
         launch_gemm_bf16(g, stream);
     }
+    mark(2);
     {  // dw_out = feat^T . dOut
         GemmArgs g;
         g.A = static_cast<const __nv_bfloat16*>(ws.feat);
@@ -785,6 +805,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
         launch_gemm_bf16(g, stream);
     }
+    mark(3);
     {
         BwdPrepArgs a{};
         a.dfeat = ws.dfeat;
@@ -801,6 +822,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.L = int(L);
         launch_bwd_prep(d, a, stream);
     }
+    mark(4);
     {
         AttnBwdArgs a{};
         a.qhat = static_cast<const __nv_bfloat16*>(ws.qhat);
@@ -815,8 +837,11 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.acc_ld = kAccLd;
         a.B = int(B);
         a.L = int(L);
-        launch_attn_bwd(d, a, stream);
+        launch_attn_bwd(d, a, stream, 1);
+        mark(5);
+        launch_attn_bwd(d, a, stream, 2);
     }
+    mark(6);
     {
         BwdUnpackArgs a{};
         a.dq_acc = ws.dq_acc;
@@ -845,7 +870,9 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.L = int(L);
         launch_bwd_unpack(d, a, stream);
     }
+    mark(7);
     if (dtrans != nullptr) launch_bwd_recenter(ws.dt_c, mask, dtrans, int(B), int(L), stream);
+    mark(8);
     {  // ds = dproj . W^T
         GemmArgs g;
         g.A = ws.dproj;
@@ -860,6 +887,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         g.K = d.n_proj;
         launch_gemm_bf16(g, stream);
     }
+    mark(9);
     {  // dW = s^T . dproj  [d_in, n_proj]
         GemmArgs g;
         g.A = ws.s_bf16;
@@ -878,6 +906,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
         launch_gemm_bf16(g, stream);
     }
+    mark(10);
     // scatter the fused projection gradient into w_q .. w_vp
     std::size_t col0 = 0;
     for (int i = 0; i < 6; ++i) {
@@ -889,6 +918,8 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
     }
     launch_scale_vec(ws.red + H, d_bwd_scale_ + H, 1, dw_bias, H * d.d_z, stream);
     launch_scale_vec(ws.red, d_bwd_scale_, H, dgamma, H, stream);
+    mark(11);
+    if (timing_) bwd_timed_once_ = true;
     cuda_check(cudaGetLastError(), "backward launch");
 }
 

@@ -183,6 +183,13 @@ private:
     bool timing_ = false;
     static constexpr int kStages = 6;
     cudaEvent_t ev_[kStages + 1] = {};
+public:
+    // backward stages: dout, dfeat, dw_out, prep, attn_kv, attn_q, unpack, recenter, ds, dW, scatter
+    static constexpr int kBwdStages = 11;
+    std::vector<float> bwd_stage_times() const;
+private:
+    cudaEvent_t evb_[kBwdStages + 1] = {};
+    bool bwd_timed_once_ = false;
     bool timed_once_ = false;
 };
 
