@@ -11,12 +11,16 @@
 // dK and dV of the same keys cannot share an SM, and a 128 x 448 bf16 stationary tile fills half
 // of the shared memory.  Each kernel therefore runs a CLUSTER OF FOUR: two tcgen05 CTA pairs
 // (cta_group::2, M = 256 rows) over the same 256 rows of one (sample, head):
-//   "P pair"  (ranks 0,1): X = A_stat . B1_j^T into TMEM, P = 2^(X - lse2) (bf16),
-//                          optional acc += P . B2_j, and P streamed to the peer pair's shared
-//                          memory with st.async (DSMEM, completion counted on its mbarrier);
+//   "P pair"  (ranks 0,1): X = A_stat . B1_j^T into TMEM, P = 2^(X - lse2) (bf16) into one of
+//                          two shared-memory buffers, optional acc += P . B2_j, and the 16 KB P
+//                          tile pushed to the peer pair with ONE cp.async.bulk smem->DSMEM copy
+//                          (completion counted on the peer's mbarrier);
 //   "dS pair" (ranks 2,3): X = A_stat . B1_j^T -> dP, dS = P (dP - D) written over the received P
-//                          in place, acc += dS . B2_j; the MMA commit that retires dS releases
-//                          the P pair's next send (multicast tcgen05.commit).
+//                          in place (double-buffered), acc += dS . B2_j; the MMA commit that
+//                          retires dS releases that buffer to the P pair (multicast commit).
+// Measured (tools/attn_bwd_trace.cu): per-thread st.async stores moved the tile at ~9 B/clk and
+// serialised the pairs; the bulk copy runs at ~16 B/clk.  The remaining limiter is the B2 ring
+// (3 x 8 KB next to the 112 KB stationary tile): TMA latency exceeds its lead time.
 // KV kernel (rows = keys, tile columns = 64 queries):
 //   P pair : A_stat = K_hat, B1 = Q_hat tiles, B2 = dO_hat slices -> acc = dV_acc
 //   dS pair: A_stat = V_hat, B1 = dO_hat tiles, B2 = Q_hat slices -> acc = dK_acc
@@ -45,8 +49,8 @@ constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
 constexpr int kStages1 = 2;
-constexpr int kStages2 = 2;
-constexpr int kSlice = 32;
+constexpr int kStages2 = 3;  // 16-row B2 slices (3 x 8 KB: what is left next to two 16 KB P/dS buffers)
+constexpr int kSlice = 16;
 constexpr int kSliceBox = kSlice * 128;
 constexpr uint32_t kXCol = 448;
 constexpr float kL2E = 1.4426950408889634f;
@@ -73,7 +77,8 @@ struct Bars {
     uint64_t stat_full;
     uint64_t b1_full[kStages1], b1_empty[kStages1];
     uint64_t b2_full[kStages2], b2_empty[kStages2];
-    uint64_t x_full, x_free, a_full, mma2_done, acc_full, pin_full, pin_free;
+    uint64_t x_full, x_free, a_full, acc_full;
+    uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
     uint32_t tmem_slot;
 };
 
@@ -84,17 +89,40 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     Layout l{};
     l.stat = 0;
     l.abuf = p.stat_bytes;
-    l.b1 = l.abuf + BM * 128;
+    l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
     l.b2 = l.b1 + kStages1 * p.b1_stage;
     l.bars = l.b2 + kStages2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
 }
 
-__device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
-                 ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
+// Optional per-event timestamps of cluster (0, bh 0) for pipeline analysis (tools/attn_bwd_trace.cu).
+#ifdef FIPA_ATTN_BWD_TRACE
+__device__ long long g_bwd_trace[4 * 12 * 16 * 64];  // [cta][warp][event][tile]
+#define BTRACE(ev, j)                                                                                    \
+    do {                                                                                                 \
+        if (blockIdx.x < 4 && blockIdx.y == 0 && (j) < 64)                                               \
+            g_bwd_trace[((blockIdx.x * 12 + ptx::warp_id()) * 16 + (ev)) * 64 + (j)] = clock64();        \
+    } while (0)
+#else
+#define BTRACE(ev, j) \
+    do {              \
+    } while (0)
+#endif
+
+// Bulk copy (async proxy) of `bytes` from this CTA's shared memory into a peer CTA's shared
+// memory; completion is counted on the peer's mbarrier.  One 16 KB copy per tile sustains far more
+// than per-thread st.async stores, which each carry their own mbarrier transaction (measured
+// ~9 B/clk, tools/attn_bwd_trace.cu).
+__device__ __forceinline__ void bulk_copy_s2cluster(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                                    uint32_t bar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst_cluster), "r"(ptx::smem_u32(src)), "r"(bytes), "r"(bar_cluster)
                  : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -165,10 +193,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&bars->x_full, 1);
         ptx::mbar_init(&bars->x_free, 16);
         ptx::mbar_init(&bars->a_full, 16);
-        ptx::mbar_init(&bars->mma2_done, 1);
         ptx::mbar_init(&bars->acc_full, 1);
-        ptx::mbar_init(&bars->pin_full, 1);
-        ptx::mbar_init(&bars->pin_free, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->mma2_done[b], 1);
+            ptx::mbar_init(&bars->pin_full[b], 1);
+            ptx::mbar_init(&bars->pin_free[b], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm(&bars->tmem_slot, 512);
@@ -186,6 +216,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             for (int j = 0; j < ntiles; ++j) {
                 const int s = j % kStages1;
                 if (j >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((j / kStages1) - 1) & 1);
+                BTRACE(11, j);
                 if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
                 ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
                                      j * BN + 32 * static_cast<int>(prank), 0, bh);
@@ -200,6 +231,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             for (int n = 0; n < nslices; ++n) {
                 const int s = n % kStages2;
                 if (n >= kStages2) ptx::mbar_wait(&bars->b2_empty[s], ((n / kStages2) - 1) & 1);
+                BTRACE(12, n);
                 if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
                 uint8_t* dst = sB2 + s * p.b2_stage;
                 const int row = n * kSlice;
@@ -226,8 +258,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
                     if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
+                    if (lane == 0) BTRACE(2, j);
                     const int s = j % kStages1;
                     ptx::mbar_wait(&bars->b1_full[s], (j / kStages1) & 1);
+                    if (lane == 0) BTRACE(0, j);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint32_t bb = b1_base + s * p.b1_stage;
@@ -245,14 +279,17 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
                     ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
+                    if (lane == 0) BTRACE(1, jj);
                     for (int h2 = 0; h2 < BN / kSlice; ++h2) {
                         const int n = jj * (BN / kSlice) + h2;
                         const int s = n % kStages2;
                         ptx::mbar_wait(&bars->b2_full[s], (n / kStages2) & 1);
+                        if (lane == 0 && h2 == BN / kSlice - 1) BTRACE(13, jj);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
                             for (int kk = 0; kk < kSlice / 16; ++kk) {
-                                const uint64_t da = ptx::sw128_desc(a_base + (2 * h2 + kk) * 32, 16, 1024);
+                                const uint64_t da = ptx::sw128_desc(
+                                    a_base + (jj & 1) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32, 16, 1024);
                                 const uint32_t vb = b2_base + s * p.b2_stage + kk * 2048;
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
                                 ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kSliceBox, 1024), idesc2a, acc);
@@ -268,8 +305,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     if (ptx::elect_one()) {
                         // P pair: its P buffer is free again.  dS pair: the received-P buffer
                         // is free -> the P pair may send the next tile.
-                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done, pair_mask);
-                        else ptx::mma_commit_2sm(&bars->pin_free, 0x3);
+                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done[jj & 1], pair_mask);
+                        else ptx::mma_commit_2sm(&bars->pin_free[jj & 1], 0x3);
                         if (j == ntiles) ptx::mma_commit_2sm(&bars->acc_full, pair_mask);
                     }
                     __syncwarp();
@@ -292,14 +329,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         float row_v = 0.f;
         if (!KV && grow < p.L) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
                                                  : __ldg(p.Dvec + vec_base + grow);
-        uint8_t* arow = sA + row * 128;
         const uint32_t peer_rank = crank + 2u;  // P pair -> dS pair partner
-        const uint32_t peer_row = ptx::mapa(arow, role == 0 ? peer_rank : crank);
-        const uint32_t peer_bar = ptx::mapa(&bars->pin_full, role == 0 ? peer_rank : crank);
 
         for (int j = 0; j < ntiles; ++j) {
             const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
-            if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full, BM * 128);
+            const int buf = j & 1;
+            uint8_t* abuf = sA + buf * (BM * 128);
+            uint8_t* arow = abuf + row * 128;
+            if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full[buf], BM * 128);
             // per-column vector (KV kernel)
             float cv[32];
             if (KV) {
@@ -312,6 +349,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::mbar_wait(&bars->x_full, j & 1);
+            if (lane == 0) BTRACE(3, j);
             ptx::tc_fence_after();
             uint32_t xr[32];
             ptx::tmem_ld32(tl + kXCol + 32 * half, xr);
@@ -338,32 +376,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);
                 }
-                if (has_mma2) {
-                    if (j > 0) {
-                        ptx::mbar_wait(&bars->mma2_done, (j - 1) & 1);
-                        ptx::tc_fence_after();
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int chunk = 4 * half + k;
-                        *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
-                            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                    }
-                    ptx::fence_proxy_async_smem();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                if (lane == 0) BTRACE(4, j);
+                // Buffer `buf` held P_{j-2}: free once the local dV MMA of tile j-2 (KV) and the dS
+                // pair's MMA of tile j-2 (which implies the copy of P_{j-2} landed) are done; the
+                // latter also frees the dS pair's buffer `buf` for the copy of P_j.
+                if (j >= 2) {
+                    if (has_mma2) ptx::mbar_wait(&bars->mma2_done[buf], ((j >> 1) - 1) & 1);
+                    ptx::mbar_wait_cluster(&bars->pin_free[buf], ((j >> 1) - 1) & 1);
+                    ptx::tc_fence_after();
                 }
-                // stream P to the dS pair once it has retired the previous tile's dS
-                if (j > 0) ptx::mbar_wait_cluster(&bars->pin_free, (j - 1) & 1);
+                if (lane == 0) BTRACE(5, j);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int chunk = 4 * half + k;
-                    st_async_v4(peer_row + ((chunk ^ (row & 7)) << 4),
-                                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), peer_bar);
+                    *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
+                        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (has_mma2 && lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                // all 128 rows written -> one bulk copy of the 16 KB tile into the dS pair
+                named_bar_sync(1, 256);
+                if (warp == 2 && lane == 0) {
+                    bulk_copy_s2cluster(ptx::mapa(abuf, peer_rank), abuf, BM * 128, ptx::mapa(&bars->pin_full[buf], peer_rank));
+                    BTRACE(7, j);
                 }
             } else {
-                ptx::mbar_wait_cluster(&bars->pin_full, j & 1);
+                ptx::mbar_wait_cluster(&bars->pin_full[buf], (j >> 1) & 1);
+                if (lane == 0) BTRACE(9, j);
                 uint4 pin[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -389,6 +430,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                if (lane == 0) BTRACE(10, j);
             }
         }
 

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
 
 #include "kernels.hpp"
 
@@ -29,35 +30,45 @@ namespace {
 
 constexpr float kLn2 = 0.6931471805599453f;
 
+__device__ __forceinline__ uint32_t ptx_pack(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-// One block per residue (b, i); warp w handles heads w, w+8, ...
+// One block per residue (b, i), warp w handles heads w, w+8, ...; rows are read with 16-byte
+// vector loads and dO_hat written 4 columns (8 bytes) per lane.  Cross-head sums (dz1, frames)
+// go through per-warp shared-memory slices, no atomics.
 __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
     extern __shared__ float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nv = d.n_value;
-    float* s_dz1 = sm;                 // rdz
-    float* s_red = s_dz1 + rdz;        // 12: dR (9), dt (3)
-    float* s_dopt = s_red + 12;        // 8 warps x 3*Nv
+    const int nw = blockDim.x >> 5;
+    float* s_z1 = sm;                        // rdz
+    float* s_pair = s_z1 + rdz;              // nw x rdz   per-warp dz1 partials
+    float* s_geo = s_pair + nw * rdz;        // nw x 12    per-warp dR (9) | dt (3)
+    float* s_dopt = s_geo + nw * 12;         // nw x 3*Nv
     const int64_t row = blockIdx.x;
     const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < rdz + 12; e += blockDim.x) sm[e] = 0.f;
+    for (int e = threadIdx.x; e < rdz; e += blockDim.x) s_z1[e] = a.z1[row * rdz + e];
+    for (int e = threadIdx.x; e < nw * (rdz + 12); e += blockDim.x) s_pair[e] = 0.f;  // s_pair + s_geo
     float R[9], t[3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
 #pragma unroll
     for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
-    const float* z1 = a.z1 + row * rdz;
     __syncthreads();
 
-    const int vpair = c + rdz, vpts = vpair + 6;
+    const int vpair = c + rdz, vpts = vpair + 6, vend = vpts + 3 * Nv;
     float* dopt_s = s_dopt + warp * 3 * Nv;
+    float* pair_s = s_pair + warp * rdz;
     float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
-    for (int h = warp; h < H; h += 8) {
+    for (int h = warp; h < H; h += nw) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
         const float* o = a.ohat + hrow * d.dv_pad;
         const float* df = a.dfeat + row * d.feat_ld + static_cast<int64_t>(h) * d.seg;
@@ -66,13 +77,11 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
             const int p = lane;
             float y[3], loc[3];
 #pragma unroll
-            for (int x = 0; x < 3; ++x)
-                y[x] = o[vpts + 3 * p + x] + o[vpair + x] + o[vpair + 3 + x] - t[x];
+            for (int x = 0; x < 3; ++x) y[x] = o[vpts + 3 * p + x] + o[vpair + x] + o[vpair + 3 + x] - t[x];
 #pragma unroll
             for (int x = 0; x < 3; ++x) loc[x] = R[x] * y[0] + R[3 + x] * y[1] + R[6 + x] * y[2];
             const float nrm = sqrtf(loc[0] * loc[0] + loc[1] * loc[1] + loc[2] * loc[2]);
-            const float dn = df[dz + c + 3 * Nv + p];
-            const float sc = nrm > 0.f ? dn / nrm : 0.f;
+            const float sc = nrm > 0.f ? df[dz + c + 3 * Nv + p] / nrm : 0.f;
             float dl[3];
 #pragma unroll
             for (int x = 0; x < 3; ++x) dl[x] = df[dz + c + 3 * p + x] + sc * loc[x];
@@ -93,25 +102,34 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
         __syncwarp();
         __nv_bfloat16* out = a.dohat + hrow * d.dv_pad;
         float Dp = 0.f;
-        for (int col = lane; col < d.dv_pad; col += 32) {
-            float v;
-            if (col < c) {
-                v = df[dz + col];
-            } else if (col < vpair) {
-                const int e = col - c;
-                const float dpc = df[e % dz];
-                v = z1[e] * dpc;
-                atomicAdd(&s_dz1[e], o[col] * dpc);
-            } else if (col < vpts) {
-                v = ds[(col - vpair) % 3];
-            } else if (col < vpts + 3 * Nv) {
-                v = dopt_s[col - vpts];
-            } else {
-                v = 0.f;
+        for (int c4 = lane; 4 * c4 < d.dv_pad; c4 += 32) {
+            const float4 ov = *reinterpret_cast<const float4*>(o + 4 * c4);
+            const float oo[4] = {ov.x, ov.y, ov.z, ov.w};
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int col = 4 * c4 + u;
+                if (col < c) {
+                    v[u] = df[dz + col];
+                } else if (col < vpair) {
+                    const int e = col - c;
+                    const float dpc = df[e % dz];
+                    v[u] = s_z1[e] * dpc;
+                    pair_s[e] += oo[u] * dpc;  // warp-private slice, one lane per e
+                } else if (col < vpts) {
+                    v[u] = ds[(col - vpair) % 3];
+                } else if (col < vend) {
+                    v[u] = dopt_s[col - vpts];
+                } else {
+                    v[u] = 0.f;
+                }
+                v[u] = __bfloat162float(__float2bfloat16_rn(v[u]));
+                if (col < d.dv_used) Dp += v[u] * oo[u];
             }
-            const __nv_bfloat16 vb = __float2bfloat16_rn(v);
-            out[col] = vb;
-            if (col < d.dv_used) Dp += __bfloat162float(vb) * o[col];
+            uint2 w;
+            w.x = ptx_pack(v[0], v[1]);
+            w.y = ptx_pack(v[2], v[3]);
+            *reinterpret_cast<uint2*>(out + 4 * c4) = w;
         }
         Dp = warp_sum(Dp);
         if (lane == 0) a.Dvec[hrow] = Dp;
@@ -121,92 +139,107 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
     for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
-    if (lane == 0) {
-        for (int k = 0; k < 9; ++k) atomicAdd(&s_red[k], dR[k]);
-        for (int k = 0; k < 3; ++k) atomicAdd(&s_red[9 + k], dt[k]);
-    }
+    if (lane < 12) s_geo[warp * 12 + lane] = lane < 9 ? dR[lane] : dt[lane - 9];
     __syncthreads();
-    for (int e = threadIdx.x; e < rdz; e += blockDim.x) a.dz1_epi[row * rdz + e] = s_dz1[e];
-    if (threadIdx.x < 9) a.drot_epi[row * 9 + threadIdx.x] = s_red[threadIdx.x];
-    if (threadIdx.x < 3) a.dt_epi[row * 3 + threadIdx.x] = s_red[9 + threadIdx.x];
+    for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
+        float acc = 0.f;
+        for (int w = 0; w < nw; ++w) acc += s_pair[w * rdz + e];
+        a.dz1_epi[row * rdz + e] = acc;
+    }
+    if (threadIdx.x < 12) {
+        float acc = 0.f;
+        for (int w = 0; w < nw; ++w) acc += s_geo[w * 12 + threadIdx.x];
+        if (threadIdx.x < 9) a.drot_epi[row * 9 + threadIdx.x] = acc;
+        else a.dt_epi[row * 3 + threadIdx.x - 9] = acc;
+    }
 }
 
-constexpr int kUnpackRows = 16;
+constexpr int kUnpackRows = 8;
 
-// A block handles kUnpackRows consecutive residues; d(w_l w_bias) and d(g) are reduced in shared
-// memory across them and flushed with one global atomic per entry per block.
-__global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+// Block = 8 warps, warp w handles heads w, w+8, ... of kUnpackRows consecutive residues.  Per
+// (residue, head) the warp stages the three accumulator rows in its shared-memory slice with
+// 16-byte loads, then derives the natural gradients; cross-head sums go through shared memory,
+// d(w_l w_bias) and d(g) are flushed with one global atomic per entry per block.
+__global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a, int stage_w) {
     extern __shared__ float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
-    float* s_dwlb = sm;              // H*dz
-    float* s_dg = s_dwlb + H * dz;   // H
-    float* s_red = s_dg + H;         // 12
+    const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) sm[e] = 0.f;
+    float* s_acc = sm;                                  // nw x 3 x stage_w
+    float* s_pq = s_acc + nw * 3 * stage_w;             // H x rdz  query-side pair grads
+    float* s_pk = s_pq + H * rdz;                       // H x rdz  key+value-side pair grads
+    float* s_geo = s_pk + H * rdz;                      // H x 12
+    float* s_dwlb = s_geo + H * 12;                     // H x dz
+    float* s_dg = s_dwlb + H * dz;                      // H
+    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) s_dwlb[e] = 0.f;
     const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
     const int g0 = c + 3 * Nq, zq = g0 + 21, vpair = c + rdz;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
     const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
+    float* qa = s_acc + warp * 3 * stage_w;
+    float* ka = qa + stage_w;
+    float* va = ka + stage_w;
+    __syncthreads();
 
     for (int rr = 0; rr < kUnpackRows; ++rr) {
         const int64_t row = row_begin + rr;
         if (row >= BL) break;
         const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
-        if (threadIdx.x < 12) s_red[threadIdx.x] = 0.f;
-        __syncthreads();
-        auto acc_row = [&](const float* base, int h) {
-            return base + ((static_cast<int64_t>(b) * H + h) * a.L + i) * a.acc_ld;
-        };
-        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
-        // pair factors: z1 (query side), z2 (key + value side), d(w_l w_bias)
-        const float* z2 = a.z2 + row * rdz;
-        for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
-            const int dd = e % dz;
-            float s1 = a.dz1_epi[row * rdz + e], s2 = 0.f;
-            const float z2e = z2[e];
-            for (int h = 0; h < H; ++h) {
-                const float kq = kLn2 * acc_row(a.dk_acc, h)[zq + e];
-                s1 += acc_row(a.dq_acc, h)[zq + e];
-                s2 += a.wl_bias[h * dz + dd] * kq + acc_row(a.dv_acc, h)[c + e];
-                atomicAdd(&s_dwlb[h * dz + dd], kq * z2e);
-            }
-            a.dz1[row * rdz + e] = s1;
-            a.dz2[row * rdz + e] = s2;
-        }
-        // scalar channels
-        for (int e = threadIdx.x; e < H * c; e += blockDim.x) {
-            const int h = e / c, cc = e - h * c;
-            dp[off_q + e] = __float2bfloat16_rn(acc_row(a.dq_acc, h)[cc]);
-            dp[off_k + e] = __float2bfloat16_rn(a.k_scale * kLn2 * acc_row(a.dk_acc, h)[cc]);
-            dp[off_v + e] = __float2bfloat16_rn(acc_row(a.dv_acc, h)[cc]);
-        }
-        // geometry: warp per head, lane per point
         float R[9], t[3];
 #pragma unroll
         for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
 #pragma unroll
         for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
         const float* pr = a.proj + row * d.n_proj;
-        float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dg = 0.f;
-        for (int h = warp; h < H; h += 8) {
-            const float* qa = acc_row(a.dq_acc, h);
-            const float* ka = acc_row(a.dk_acc, h);
-            const float* va = acc_row(a.dv_acc, h);
+        const float* z2 = a.z2 + row * rdz;
+        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+        for (int h = warp; h < H; h += nw) {
+            const int64_t arow = ((static_cast<int64_t>(b) * H + h) * a.L + i) * a.acc_ld;
+            for (int e4 = lane; 4 * e4 < stage_w; e4 += 32) {
+                reinterpret_cast<float4*>(qa)[e4] = __ldg(reinterpret_cast<const float4*>(a.dq_acc + arow) + e4);
+                reinterpret_cast<float4*>(ka)[e4] = __ldg(reinterpret_cast<const float4*>(a.dk_acc + arow) + e4);
+                reinterpret_cast<float4*>(va)[e4] = __ldg(reinterpret_cast<const float4*>(a.dv_acc + arow) + e4);
+            }
+            __syncwarp();
+            // scalar channels (bf16 pairs)
+            for (int c2 = lane; 2 * c2 < c; c2 += 32) {
+                const int cc = 2 * c2;
+                const int o = h * c + cc;
+                const bool two = cc + 1 < c;
+                auto st2 = [&](int base, float x0, float x1) {
+                    if (two && ((base + o) & 1) == 0) {
+                        *reinterpret_cast<uint32_t*>(dp + base + o) = ptx_pack(x0, x1);
+                    } else {
+                        dp[base + o] = __float2bfloat16_rn(x0);
+                        if (two) dp[base + o + 1] = __float2bfloat16_rn(x1);
+                    }
+                };
+                st2(off_q, qa[cc], two ? qa[cc + 1] : 0.f);
+                st2(off_k, a.k_scale * kLn2 * ka[cc], two ? a.k_scale * kLn2 * ka[cc + 1] : 0.f);
+                st2(off_v, va[cc], two ? va[cc + 1] : 0.f);
+            }
+            // pair factors
+            for (int e = lane; e < rdz; e += 32) {
+                const int dd = e % dz;
+                const float kq = kLn2 * ka[zq + e];
+                s_pq[h * rdz + e] = qa[zq + e];
+                s_pk[h * rdz + e] = a.wl_bias[h * dz + dd] * kq + va[c + e];
+                atomicAdd(&s_dwlb[h * dz + dd], kq * z2[e]);
+            }
+            // geometry: lane per point
             const float g = a.head_g[h];
             const float cs = ka[g0 + 18];
+            const float S1 = qa[g0 + 20];  // sum_j dS_ij, as rounded for the MMAs
             float dW[3];
 #pragma unroll
             for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (ka[g0 + 9 + x] + ka[g0 + 12 + x]);
-            float dgh = 0.f;
-            const float S1 = qa[g0 + 20];  // sum_j dS_ij, as rounded for the MMAs
-            float dAsum[3] = {0.f, 0.f, 0.f};
+            float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dgh = 0.f;
             if (lane < Nq) {
                 const int p = lane;
-                // query point p: A = R q_p + t,
-                //   dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS_ij B_jp] - g A S1
-                // (the exact S1 = 0 is not assumed: subtracting g A S1 with the same rounded dS
-                // cancels the translation-sized common mode of the first term).
+                // query point: A = R q_p + t,  dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS B] - g A S1
+                // (S1 = 0 is not assumed: subtracting g A S1 with the same rounded dS cancels the
+                // translation-sized common mode of the first term)
                 float qp[3], gB[3], A[3], dA[3];
 #pragma unroll
                 for (int x = 0; x < 3; ++x) {
@@ -218,9 +251,9 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
 #pragma unroll
                 for (int x = 0; x < 3; ++x) {
                     dA[x] = gB[x] - g * A[x] * S1;
-                    dAsum[x] = dA[x];
+                    dt[x] += dA[x];
                 }
-                // d(-g/2 |A - B|^2)/dg summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
+                // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
                 dgh += (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
                        0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
 #pragma unroll
@@ -230,7 +263,7 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
 #pragma unroll
                     for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
                 }
-                // key point p: B = R k_p + t
+                // key point: B = R k_p + t
                 float kp[3], B[3], dB[3];
 #pragma unroll
                 for (int x = 0; x < 3; ++x) kp[x] = pr[off_kp + (h * Nq + p) * 3 + x];
@@ -266,30 +299,40 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
                     for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
                 }
             }
-#pragma unroll
-            for (int x = 0; x < 3; ++x) dt[x] += dAsum[x];  // query side: sum_p dA_p
             if (lane == 0) {
 #pragma unroll
                 for (int x = 0; x < 3; ++x)
                     dt[x] += g * kLn2 * (ka[g0 + x] + ka[g0 + 6 + x]) + float(Nq) * dW[x]   // key
                              + va[vpair + x];                                                // value
             }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
             dgh = warp_sum(dgh);
-            dg += dgh;
-            if (lane == 0) s_dg[h] += dgh;  // one warp per head: no race
-        }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
-        if (lane == 0) {
-            for (int k = 0; k < 9; ++k) atomicAdd(&s_red[k], dR[k]);
-            for (int k = 0; k < 3; ++k) atomicAdd(&s_red[9 + k], dt[k]);
+            if (lane < 12) s_geo[h * 12 + lane] = lane < 9 ? dR[lane] : dt[lane - 9];
+            if (lane == 0) s_dg[h] += dgh;  // one warp per head
+            __syncwarp();
         }
         __syncthreads();
-        if (threadIdx.x < 9 && a.drot != nullptr)
-            a.drot[row * 9 + threadIdx.x] = s_red[threadIdx.x] + a.drot_epi[row * 9 + threadIdx.x];
-        if (threadIdx.x < 3) a.dt_c[row * 3 + threadIdx.x] = s_red[9 + threadIdx.x] + a.dt_epi[row * 3 + threadIdx.x];
+        for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
+            float s1 = a.dz1_epi[row * rdz + e], s2 = 0.f;
+            for (int h = 0; h < H; ++h) {
+                s1 += s_pq[h * rdz + e];
+                s2 += s_pk[h * rdz + e];
+            }
+            a.dz1[row * rdz + e] = s1;
+            a.dz2[row * rdz + e] = s2;
+        }
+        if (threadIdx.x < 12) {
+            float acc = 0.f;
+            for (int h = 0; h < H; ++h) acc += s_geo[h * 12 + threadIdx.x];
+            if (threadIdx.x < 9) {
+                if (a.drot != nullptr) a.drot[row * 9 + threadIdx.x] = acc + a.drot_epi[row * 9 + threadIdx.x];
+            } else {
+                a.dt_c[row * 3 + threadIdx.x - 9] = acc + a.dt_epi[row * 3 + threadIdx.x - 9];
+            }
+        }
         __syncthreads();
     }
     for (int e = threadIdx.x; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
@@ -366,14 +409,22 @@ __global__ void scale_vec_kernel(const float* in, const float* scale, int period
 }  // namespace
 
 void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream) {
-    const size_t smem = sizeof(float) * (d.rank * d.d_z + 12 + 8 * 3 * d.n_value);
+    const int rdz = d.rank * d.d_z;
+    const size_t smem = sizeof(float) * (rdz + 8 * (rdz + 12 + 3 * d.n_value));
+    if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     bwd_prep_kernel<<<static_cast<unsigned>(int64_t(a.B) * a.L), 256, smem, stream>>>(d, a);
 }
 
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
-    const size_t smem = sizeof(float) * (d.heads * d.d_z + d.heads + 12);
+    const int rdz = d.rank * d.d_z;
+    // staged accumulator width: every column the unpack reads, rounded to 16-byte vectors
+    const int need = std::max(d.dqk_used, d.dv_used);
+    const int stage_w = (need + 3) / 4 * 4;
+    if (stage_w > a.acc_ld) throw std::invalid_argument("bwd_unpack: accumulator stride too small");
+    const size_t smem = sizeof(float) * (8 * 3 * stage_w + 2 * d.heads * rdz + d.heads * 12 + d.heads * d.d_z + d.heads);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int64_t BL = int64_t(a.B) * a.L;
-    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a);
+    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a, stage_w);
 }
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
