@@ -149,6 +149,39 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
                                       int64_t* dims);
 int fipa_layer_backward_launches(const fipa_layer* layer);
 
+/* ------------------------------------------------------------ multi-GPU (query-row sharding)
+ * One process per GPU.  A sequence of G*L residues is split into G contiguous blocks of L rows
+ * (rank r owns rows [r*L, (r+1)*L)); the packed key/value rows are all-gathered over NCCL and each
+ * rank returns the output rows of its block.  NCCL is loaded at run time (libnccl.so.2).
+ * Reference counterpart: none -- the reference is single-process. */
+typedef struct fipa_comm fipa_comm;
+#define FIPA_ERR_COMM 5 /* NCCL failure / NCCL unavailable */
+int fipa_comm_unique_id(uint8_t out[128]);
+int fipa_comm_create(int world, int rank, const uint8_t id[128], int device, fipa_comm** out);
+void fipa_comm_destroy(fipa_comm* comm);
+size_t fipa_layer_sharded_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_local, int world);
+int fipa_layer_forward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_local, const float* s,
+                               const float* z1, const float* z2, const float* rot, const float* trans,
+                               const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                               void* stream);
+/* Collective-agnostic building blocks of the same path (any all-reduce / all-gather may join them):
+ *   1. fipa_layer_shard_centroid_sums: device float sums[B*4] = per-sample {sum t, count} of the
+ *      local valid rows; the caller all-reduces (sums) them across ranks.
+ *   2. fipa_layer_shard_pack: recentre with the global sums, project and pack the local rows into
+ *      the workspace (a fipa_layer_workspace_size(B, L_local) buffer); *khat / *vhat point at the
+ *      local packed rows (k_bytes / v_bytes each); the caller all-gathers them rank-major.
+ *   3. fipa_layer_shard_attend: local queries against the gathered keys -> out [B, L_local, d_in]. */
+int fipa_layer_shard_centroid_sums(fipa_layer* layer, int64_t B, int64_t L_local, const float* trans,
+                                   const uint8_t* mask, float* sums, void* stream);
+int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_local, const float* s, const float* z1,
+                          const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                          const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                          void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes);
+int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_local, int world, const float* s,
+                            const float* z1, const float* z2, const float* rot, const float* trans,
+                            const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of kernels fipa_layer_forward launches per call for this configuration. */
 int fipa_layer_forward_launches(const fipa_layer* layer);
 

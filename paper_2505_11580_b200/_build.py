@@ -29,7 +29,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_tc.cu", "pack.cu", "attn_fwd_tc.cu", "attn_fwd_2sm.cu", "simt_f32.cu", "attn_bwd.cu",
               "bwd.cu"]
-CXX_SOURCES = ["layer.cpp", "capi.cpp"]
+CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp"]
 HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp"]
 
 LIB_NAME = "libfipa_b200.so"
@@ -81,7 +81,7 @@ def build_native(verbose=False):
         objs = list(ex.map(_compile, CU_SOURCES + CXX_SOURCES))
     if _stale(LIB_PATH, objs):
         tmp = LIB_PATH + ".tmp"
-        _run([NVCC, *GENCODE, "-shared", "-o", tmp, *objs, "-Xlinker", "-soname=" + LIB_NAME])
+        _run([NVCC, *GENCODE, "-shared", "-o", tmp, *objs, "-Xlinker", "-soname=" + LIB_NAME, "-ldl"])
         os.replace(tmp, LIB_PATH)
     import pybind11
 

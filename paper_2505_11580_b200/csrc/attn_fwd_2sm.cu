@@ -53,6 +53,7 @@ constexpr float kLn2 = 0.6931471805599453f;
 
 struct Attn2Params {
     int L, H, dqk_mma, dv_mma, n_qkb, n1, n2, nb1, nb2;
+    int Lk, kchunk;  // keys: Lk total, stored as shards of kchunk rows (kchunk % 64 == 0 or == Lk)
     int c, d_z, rank, n_value, seg, feat_ld;
     int z1_tma;  // z1 staged by TMA into shared memory for the epilogue
     const float* z1;
@@ -275,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool leader = rank == 0;
     const int bh = blockIdx.y;
     const int q0 = blockIdx.x * BM;
-    const int ntiles = (p.L + BN - 1) / BN;
+    const int ntiles = (p.Lk + BN - 1) / BN;
     const int qk_steps = p.dqk_mma / 16;
 
     if (warp == 0 && lane == 0) {
@@ -316,8 +317,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (j >= kKStages) ptx::mbar_wait(&bars->k_empty[s], ((j / kKStages) - 1) & 1);
                 FIPA_TRACE(5, j);
                 if (leader) ptx::mbar_expect_tx(&bars->k_full[s], 2 * lay.kstage);
-                ptx::tma_load_4d_2sm(sK + s * lay.kstage, &mapK, &bars->k_full[s], 0,
-                                     j * BN + 32 * static_cast<int>(rank), 0, bh);
+                const int key = j * BN + 32 * static_cast<int>(rank);
+                const int g = key / p.kchunk;  // keys past Lk land in shard G: TMA zero fill
+                ptx::tma_load_5d_2sm(sK + s * lay.kstage, &mapK, &bars->k_full[s], 0, key - g * p.kchunk, 0, bh, g);
             }
         }
     } else if (warp == 10) {
@@ -332,12 +334,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (leader) ptx::mbar_expect_tx(&bars->v_full[s], 2 * lay.vstage);
                 uint8_t* dst = sV + s * lay.vstage;
                 const int key = n * kVKeys;
+                const int g = key / p.kchunk, kk = key - g * p.kchunk;
                 for (int x = 0; x < p.nb1; ++x)
-                    ptx::tma_load_3d_2sm(dst + x * kVBoxBytes, &mapV, &bars->v_full[s],
-                                         half1 * static_cast<int>(rank) + 64 * x, key, bh);
+                    ptx::tma_load_4d_2sm(dst + x * kVBoxBytes, &mapV, &bars->v_full[s],
+                                         half1 * static_cast<int>(rank) + 64 * x, kk, bh, g);
                 for (int x = 0; x < p.nb2; ++x)
-                    ptx::tma_load_3d_2sm(dst + (p.nb1 + x) * kVBoxBytes, &mapV, &bars->v_full[s],
-                                         p.n1 + half2 * static_cast<int>(rank) + 64 * x, key, bh);
+                    ptx::tma_load_4d_2sm(dst + (p.nb1 + x) * kVBoxBytes, &mapV, &bars->v_full[s],
+                                         p.n1 + half2 * static_cast<int>(rank) + 64 * x, kk, bh, g);
             }
         }
     } else if (warp == 1) {
@@ -437,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (lane == 0) FIPA_TRACE(12, j);
 
             float x[32];
-            const int kvalid = p.L - j * BN - 32 * half;  // keys >= L are not real
+            const int kvalid = p.Lk - j * BN - 32 * half;  // keys >= Lk are not real
 #pragma unroll
             for (int cc = 0; cc < 32; ++cc) x[cc] = cc < kvalid ? __uint_as_float(sr[cc]) : -INFINITY;
             float mx[8];
@@ -591,8 +594,13 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     p.dv_pad = d.dv_pad;
     const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
     const CUtensorMap mapQ = make_map_blocks_bf16(a.qhat, a.L, BH, d.dqk_pad, BM, p.n_qkb);
-    const CUtensorMap mapK = make_map_blocks_bf16(a.khat, a.L, BH, d.dqk_pad, 32, p.n_qkb);
-    const CUtensorMap mapV = make_map_3d_bf16(a.vhat, d.dv_pad, a.L, BH, d.dv_pad, 64, kVKeys);
+    p.Lk = a.Lk > 0 ? a.Lk : a.L;
+    p.kchunk = a.kchunk > 0 ? a.kchunk : p.Lk;
+    const int G = (p.Lk + p.kchunk - 1) / p.kchunk;
+    if (G * p.kchunk != p.Lk || (G > 1 && p.kchunk % BN != 0))
+        throw std::invalid_argument("attention: key shards must be equal and a multiple of 64 rows");
+    const CUtensorMap mapK = make_map_blocks_bf16_sharded(a.khat, p.kchunk, BH, G, d.dqk_pad, 32, p.n_qkb);
+    const CUtensorMap mapV = make_map_4d_bf16_sharded(a.vhat, d.dv_pad, p.kchunk, BH, G, 64, kVKeys);
     const int rdz = d.rank * d.d_z;
     const Layout lay0 = smem_layout(p.n_qkb, p.nb1, p.nb2);
     p.z1_tma = (rdz % 32 == 0 && rdz / 32 <= 256 && (reinterpret_cast<uintptr_t>(a.z1) & 15) == 0 &&

@@ -32,6 +32,9 @@ struct FipaIoError : std::runtime_error {
 struct FipaCudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct FipaCommError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 void check(int rc) {
     if (rc == FIPA_OK) return;
@@ -41,6 +44,7 @@ void check(int rc) {
         case FIPA_ERR_NUMERIC: throw FipaNumericError(msg);
         case FIPA_ERR_IO: throw FipaIoError(msg);
         case FIPA_ERR_CUDA: throw FipaCudaError(msg);
+        case FIPA_ERR_COMM: throw FipaCommError(msg);
         default: throw std::runtime_error(msg);
     }
 }
@@ -53,6 +57,39 @@ int parse_precision(const std::string& name) {
 }
 
 const char* kNames[10] = {"w_q", "w_k", "w_v", "w_qp", "w_kp", "w_vp", "w_bias", "gamma_raw", "w_out", "b_out"};
+
+// NCCL communicator for query-row sharding (one per process / GPU).
+class Comm {
+public:
+    Comm(int world, int rank, const py::bytes& uid, int device) {
+        const std::string id = uid;
+        if (id.size() != 128) throw FipaValueError("NCCL unique id must be 128 bytes");
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_comm_create(world, rank, reinterpret_cast<const uint8_t*>(id.data()), device, &comm_);
+        }
+        check(rc);
+        world_ = world;
+        rank_ = rank;
+    }
+    ~Comm() { fipa_comm_destroy(comm_); }
+    Comm(const Comm&) = delete;
+    Comm& operator=(const Comm&) = delete;
+    fipa_comm* get() const { return comm_; }
+    int world() const { return world_; }
+    int rank() const { return rank_; }
+
+private:
+    fipa_comm* comm_ = nullptr;
+    int world_ = 1, rank_ = 0;
+};
+
+py::bytes comm_unique_id() {
+    uint8_t id[128];
+    check(fipa_comm_unique_id(id));
+    return py::bytes(reinterpret_cast<const char*>(id), 128);
+}
 
 class Model {
 public:
@@ -209,6 +246,47 @@ public:
 
     int forward_launches() const { return fipa_layer_forward_launches(layer_); }
     int backward_launches() const { return fipa_layer_backward_launches(layer_); }
+    size_t sharded_workspace_size(int64_t B, int64_t L, int world) const {
+        return fipa_layer_sharded_workspace_size(layer_, B, L, world);
+    }
+    void forward_sharded_device(Comm& comm, int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2,
+                                uintptr_t rot, uintptr_t trans, uintptr_t mask, uintptr_t out, uintptr_t ws,
+                                size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_forward_sharded(layer_, comm.get(), B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                            reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(out),
+                                            reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    void shard_centroid_sums(int64_t B, int64_t L, uintptr_t trans, uintptr_t mask, uintptr_t sums, uintptr_t stream) {
+        check(fipa_layer_shard_centroid_sums(layer_, B, L, reinterpret_cast<const float*>(trans),
+                                             reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(sums),
+                                             reinterpret_cast<void*>(stream)));
+    }
+    py::tuple shard_pack(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                         uintptr_t trans, uintptr_t mask, uintptr_t sums, uintptr_t ws, size_t ws_bytes,
+                         uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
+        void *k = nullptr, *v = nullptr;
+        size_t kb = 0, vb = 0;
+        check(fipa_layer_shard_pack(layer_, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                    reinterpret_cast<const uint8_t*>(mask), f(sums), reinterpret_cast<void*>(ws),
+                                    ws_bytes, reinterpret_cast<void*>(stream), &k, &kb, &v, &vb));
+        return py::make_tuple(reinterpret_cast<uintptr_t>(k), kb, reinterpret_cast<uintptr_t>(v), vb);
+    }
+    void shard_attend(int64_t B, int64_t L, int world, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                      uintptr_t trans, uintptr_t mask, uintptr_t k_all, uintptr_t v_all, uintptr_t out, uintptr_t ws,
+                      size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
+        check(fipa_layer_shard_attend(layer_, B, L, world, f(s), f(z1), f(z2), f(rot), f(trans),
+                                      reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<const void*>(k_all),
+                                      reinterpret_cast<const void*>(v_all), reinterpret_cast<float*>(out),
+                                      reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream)));
+    }
     size_t train_workspace_size(int64_t B, int64_t L) const { return fipa_layer_train_workspace_size(layer_, B, L); }
     uint64_t num_weights() const { return fipa_layer_num_weights(layer_); }
     void forward_train_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
@@ -342,6 +420,13 @@ PYBIND11_MODULE(_fipa_b200, m) {
     py::register_exception<FipaNumericError>(m, "FipaNumericError", PyExc_ArithmeticError);
     py::register_exception<FipaIoError>(m, "FipaIoError", PyExc_IOError);
     py::register_exception<FipaCudaError>(m, "FipaCudaError", PyExc_RuntimeError);
+    py::register_exception<FipaCommError>(m, "FipaCommError", PyExc_RuntimeError);
+    m.def("comm_unique_id", &comm_unique_id, "128-byte NCCL unique id (rank 0 creates, all ranks share)");
+    py::class_<Comm>(m, "Comm", "NCCL communicator for query-row sharding (one process per GPU)")
+        .def(py::init<int, int, const py::bytes&, int>(), py::arg("world"), py::arg("rank"), py::arg("unique_id"),
+             py::arg("device"))
+        .def_property_readonly("world", &Comm::world)
+        .def_property_readonly("rank", &Comm::rank);
 
     py::class_<Model>(m, "Model", "One FlashIPA layer: hyper-parameters plus deterministic weights")
         .def(py::init<uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t,
@@ -364,6 +449,18 @@ PYBIND11_MODULE(_fipa_b200, m) {
         .def("workspace_layout", &Model::workspace_layout, py::arg("B"), py::arg("L"))
         .def("forward_launches", &Model::forward_launches)
         .def("backward_launches", &Model::backward_launches)
+        .def("sharded_workspace_size", &Model::sharded_workspace_size, py::arg("B"), py::arg("L"), py::arg("world"))
+        .def("forward_sharded_device", &Model::forward_sharded_device, py::arg("comm"), py::arg("B"), py::arg("L"),
+             py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("shard_centroid_sums", &Model::shard_centroid_sums, py::arg("B"), py::arg("L"), py::arg("trans"),
+             py::arg("mask"), py::arg("sums"), py::arg("stream"))
+        .def("shard_pack", &Model::shard_pack, py::arg("B"), py::arg("L"), py::arg("s"), py::arg("z1"),
+             py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("sums"), py::arg("workspace"),
+             py::arg("workspace_bytes"), py::arg("stream"))
+        .def("shard_attend", &Model::shard_attend, py::arg("B"), py::arg("L"), py::arg("world"), py::arg("s"),
+             py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("k_all"),
+             py::arg("v_all"), py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
         .def("train_workspace_size", &Model::train_workspace_size, py::arg("B"), py::arg("L"))
         .def("num_weights", &Model::num_weights)
         .def("forward_train_device", &Model::forward_train_device, py::arg("B"), py::arg("L"), py::arg("s"),

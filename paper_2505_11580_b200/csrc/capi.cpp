@@ -14,6 +14,11 @@ struct fipa_layer {
     explicit fipa_layer(const fipa_b200::Config& c) : impl(c) {}
 };
 
+struct fipa_comm {
+    fipa_b200::Comm impl;
+    fipa_comm(int world, int rank, const uint8_t* id, int device) : impl(world, rank, id, device) {}
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -35,6 +40,9 @@ int guarded(F&& f) {
     } catch (const fipa_b200::CudaError& e) {
         g_err = e.what();
         return FIPA_ERR_CUDA;
+    } catch (const fipa_b200::CommError& e) {
+        g_err = e.what();
+        return FIPA_ERR_COMM;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return FIPA_ERR_VALUE;
@@ -295,6 +303,89 @@ int fipa_layer_bwd_stage_times(const fipa_layer* layer, float* ms, int n) {
 
 int fipa_layer_backward_launches(const fipa_layer* layer) {
     return layer ? layer->impl.launches_per_backward() : 0;
+}
+
+int fipa_comm_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        if (out == nullptr) throw fipa_b200::ValueError("null output");
+        const auto id = fipa_b200::Comm::unique_id();
+        std::copy(id.begin(), id.end(), out);
+    });
+}
+
+int fipa_comm_create(int world, int rank, const uint8_t id[128], int device, fipa_comm** out) {
+    return guarded([&] {
+        if (out == nullptr) throw fipa_b200::ValueError("null output handle");
+        *out = nullptr;
+        *out = new fipa_comm(world, rank, id, device);
+    });
+}
+
+void fipa_comm_destroy(fipa_comm* comm) { delete comm; }
+
+size_t fipa_layer_sharded_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_, int world) {
+    if (layer == nullptr || B < 1 || L_ < 1 || world < 1) return 0;
+    return layer->impl.sharded_workspace_size(B, L_, world);
+}
+
+int fipa_layer_forward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_, const float* s,
+                               const float* z1, const float* z2, const float* rot, const float* trans,
+                               const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+    return guarded([&] {
+        if (comm == nullptr) throw fipa_b200::ValueError("null fipa_comm");
+        L(layer).forward_sharded(comm->impl, B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_layer_shard_centroid_sums(fipa_layer* layer, int64_t B, int64_t L_, const float* trans,
+                                   const uint8_t* mask, float* sums, void* stream) {
+    return guarded([&] {
+        L(layer);
+        if (trans == nullptr || sums == nullptr || B < 1 || L_ < 1) throw fipa_b200::ValueError("bad arguments");
+        fipa_b200::launch_centroid_sums(trans, mask, sums, int(B), int(L_), static_cast<cudaStream_t>(stream));
+        fipa_b200::cuda_check(cudaGetLastError(), "centroid sums");
+    });
+}
+
+int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                          const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                          const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                          void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes) {
+    return guarded([&] {
+        auto& impl = L(layer);
+        if (sums == nullptr) throw fipa_b200::ValueError("null centroid sums");
+        fipa_b200::ShardStage st;
+        st.stage = 1;
+        st.sums = sums;
+        // out is not written in stage 1; any non-null pointer satisfies the argument check
+        impl.forward(B, L_, s, z1, z2, rot, trans, mask, reinterpret_cast<float*>(workspace), workspace,
+                     workspace_bytes, static_cast<cudaStream_t>(stream), false, &st);
+        const auto w = impl.carve(workspace, B, L_);
+        const std::size_t BHL = std::size_t(B) * L_ * impl.dims().heads;
+        if (khat) *khat = w.khat;
+        if (vhat) *vhat = w.vhat;
+        if (k_bytes) *k_bytes = BHL * impl.dims().dqk_pad * 2;
+        if (v_bytes) *v_bytes = BHL * impl.dims().dv_pad * 2;
+    });
+}
+
+int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_, int world, const float* s, const float* z1,
+                            const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                            const void* khat_all, const void* vhat_all, float* out, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        if (khat_all == nullptr || vhat_all == nullptr || world < 1) throw fipa_b200::ValueError("bad key shards");
+        if (world > 1 && L_ % 64 != 0) throw fipa_b200::ValueError("query-row sharding needs L_local % 64 == 0");
+        fipa_b200::ShardStage st;
+        st.stage = 2;
+        st.k_all = khat_all;
+        st.v_all = vhat_all;
+        st.groups = world;
+        L(layer).forward(B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
+                         static_cast<cudaStream_t>(stream), false, &st);
+    });
 }
 
 }  // extern "C"

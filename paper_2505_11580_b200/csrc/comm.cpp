@@ -1,0 +1,156 @@
+// Multi-GPU query-row sharding over NCCL (one process per GPU).  SURVEY.md §8(e): a long single
+// structure is split into G contiguous residue blocks; every rank projects and packs its own
+// rows, the packed key/value rows (k_hat, v_hat: bf16 [B*H][L_local][pad]) are all-gathered over
+// NVLink into [G][B*H][L_local][pad] -- exactly the sharded layout the attention kernel's 5-D
+// TMA maps read (attn_fwd_2sm.cu) -- and every rank attends its local queries to all keys.  The
+// translation centroid used for recentring is all-reduced first (4 floats per sample).
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2: the copy torch already loaded, or the
+// system one), so the library itself has no link-time NCCL dependency and still loads on hosts
+// without it; nccl.h supplies only the types.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "layer.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+struct NcclApi {
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (api.handle) break;
+        }
+        if (!api.handle) {
+            err = "NCCL not found (dlopen libnccl.so.2 failed)";
+            return;
+        }
+        auto sym = [](const char* n) { return dlsym(api.handle, n); };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.AllReduce) {
+            err = "NCCL library lacks required symbols";
+            api.handle = nullptr;
+        }
+    });
+    if (!api.handle) throw CommError(err);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const auto& api = nccl();
+        throw CommError(std::string(what) + ": " + (api.GetErrorString ? api.GetErrorString(r) : "NCCL error"));
+    }
+}
+
+}  // namespace
+
+std::array<std::uint8_t, 128> Comm::unique_id() {
+    static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::array<std::uint8_t, 128> out{};
+    std::memcpy(out.data(), &id, 128);
+    return out;
+}
+
+Comm::Comm(int world, int rank, const std::uint8_t* id, int device) : world_(world), rank_(rank), device_(device) {
+    if (world < 1 || rank < 0 || rank >= world) throw ValueError("invalid world/rank");
+    if (id == nullptr) throw ValueError("null NCCL unique id");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().CommInitRank(&c, world, uid, rank), "ncclCommInitRank");
+    comm_ = c;
+}
+
+Comm::~Comm() {
+    if (comm_) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
+}
+
+void Comm::all_reduce_sum_f32(float* buf, std::size_t n, cudaStream_t stream) {
+    nccl_check(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), stream),
+               "ncclAllReduce");
+}
+
+void Comm::all_gather_bytes(const void* send, void* recv, std::size_t bytes, cudaStream_t stream) {
+    nccl_check(nccl().AllGather(send, recv, bytes, ncclUint8, static_cast<ncclComm_t>(comm_), stream),
+               "ncclAllGather");
+}
+
+// ---------------------------------------------------------------- sharded forward
+FlashIpaLayer::ShardedWorkspace FlashIpaLayer::carve_sharded(void* base, std::int64_t B, std::int64_t L,
+                                                            int groups) const {
+    ShardedWorkspace w;
+    w.local = carve(base, B, L);
+    std::size_t off = (w.local.bytes + 255) / 256 * 256;
+    auto take = [&](std::size_t bytes) {
+        char* p = reinterpret_cast<char*>(reinterpret_cast<std::uintptr_t>(base) + off);
+        off += (bytes + 255) / 256 * 256;
+        return p;
+    };
+    const std::size_t BHL = std::size_t(B) * L * dims_.heads;
+    w.kv_bytes = BHL * dims_.dqk_pad * 2;
+    w.v_bytes = BHL * dims_.dv_pad * 2;
+    w.k_all = take(w.kv_bytes * groups);
+    w.v_all = take(w.v_bytes * groups);
+    w.sums = reinterpret_cast<float*>(take(std::size_t(B) * 4 * 4));
+    w.bytes = off;
+    return w;
+}
+
+std::size_t FlashIpaLayer::sharded_workspace_size(std::int64_t B, std::int64_t L, int groups) const {
+    return carve_sharded(nullptr, B, L, groups).bytes;
+}
+
+void FlashIpaLayer::forward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                    const float* z2, const float* rot, const float* trans,
+                                    const std::uint8_t* mask, float* out, void* workspace,
+                                    std::size_t workspace_bytes, cudaStream_t stream) {
+    const int G = comm.world();
+    if (G > 1 && L % 64 != 0) throw ValueError("query-row sharding needs L_local % 64 == 0");
+    const ShardedWorkspace ws = carve_sharded(workspace, B, L, G);
+    if (workspace == nullptr || workspace_bytes < ws.bytes)
+        throw ValueError("sharded workspace too small: need " + std::to_string(ws.bytes) + " bytes");
+    launch_centroid_sums(trans, mask, ws.sums, int(B), int(L), stream);
+    comm.all_reduce_sum_f32(ws.sums, std::size_t(B) * 4, stream);
+    ShardStage st;
+    st.stage = 1;
+    st.sums = ws.sums;
+    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, false, &st);
+    comm.all_gather_bytes(ws.local.khat, ws.k_all, ws.kv_bytes, stream);
+    comm.all_gather_bytes(ws.local.vhat, ws.v_all, ws.v_bytes, stream);
+    st.stage = 2;
+    st.k_all = ws.k_all;
+    st.v_all = ws.v_all;
+    st.groups = G;
+    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, false, &st);
+}
+
+}  // namespace fipa_b200

@@ -81,7 +81,10 @@ struct AttnArgs {
     __nv_bfloat16* feat;   // [BL, feat]
     float* lse;            // [B*H, L] natural-log LSE of the shifted logits
     float* o_save;         // [B*H, L, dv_pad] normalised O_hat (fp32) for the backward, or null
-    int B, L;
+    int B, L;              // L = query rows (local rows when sharded)
+    // Keys (query-row sharding): khat/vhat hold Lk keys as kgroups shards of kchunk rows,
+    // [kgroups][B*H][kchunk][pad] (shard g = keys g*kchunk ..).  0 = unsharded (Lk = L).
+    int Lk = 0, kchunk = 0;
 };
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
 // inverse frame / norms) writing bf16 features.
@@ -163,6 +166,10 @@ void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStre
 // Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
 void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
                            cudaStream_t stream);
+// Query-row sharding: per-sample {sum x, sum y, sum z, count} of valid local translations, and
+// recentring with (all-reduced) global sums.
+void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, int B, int L, cudaStream_t stream);
+void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream);
 // Subtract each sample's translation centroid (exact: the layer is invariant to it).
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream);

@@ -549,12 +549,17 @@ std::vector<float> FlashIpaLayer::stage_times() const {
 void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
                             const float* z2, const float* rot, const float* trans,
                             const std::uint8_t* mask, float* out, void* workspace,
-                            std::size_t workspace_bytes, cudaStream_t stream, bool train) {
+                            std::size_t workspace_bytes, cudaStream_t stream, bool train,
+                            const ShardStage* shard) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
     REQUIRE(!train || backward_supported(),
             "training (forward_train/backward) needs precision='bf16' and lifted widths <= 448");
+    REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && attn_fwd_2sm_supported(dims_) && !train),
+            "query-row sharding needs precision='bf16' (inference forward)");
+    const bool do_pack = shard == nullptr || shard->stage == 1;
+    const bool do_attend = shard == nullptr || shard->stage == 2;
     const Workspace ws = carve(workspace, B, L, train);
     REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "workspace too small: need ",
             ws.bytes, " bytes, got ", workspace_bytes);
@@ -569,8 +574,13 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         if (timing_) cuda_check(cudaEventRecord(ev_[i], stream), "cudaEventRecord");
     };
     mark(0);
-    launch_recenter(trans, mask, ws.trans_c, int(B), int(L), stream);
+    if (shard == nullptr) {
+        launch_recenter(trans, mask, ws.trans_c, int(B), int(L), stream);
+    } else if (do_pack) {
+        launch_recenter_with_sums(trans, shard->sums, ws.trans_c, int(B), int(L), stream);
+    }
     mark(1);
+    if (do_pack) {
     if (cfg_.precision == Precision::bf16) {
         launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
         mark(2);
@@ -608,7 +618,12 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
     pa.L = int(L);
     pa.out_f32 = cfg_.precision == Precision::f32;
     launch_pack(d, pa, stream);
+    }
     mark(4);
+    if (!do_attend) {
+        cuda_check(cudaGetLastError(), "kernel launch");
+        return;
+    }
     if (cfg_.precision == Precision::bf16) {
         AttnArgs aa{};
         aa.qhat = static_cast<const __nv_bfloat16*>(ws.qhat);
@@ -623,6 +638,12 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         aa.o_save = train ? ws.o_hat : nullptr;
         aa.B = int(B);
         aa.L = int(L);
+        if (shard != nullptr) {  // keys = all shards' rows, gathered [G][B*H][L][pad]
+            aa.khat = static_cast<const __nv_bfloat16*>(shard->k_all);
+            aa.vhat = static_cast<const __nv_bfloat16*>(shard->v_all);
+            aa.Lk = int(L) * shard->groups;
+            aa.kchunk = int(L);
+        }
         if (train || use_2sm_attention(d)) {
             launch_attn_fwd_2sm(d, aa, stream);
         } else {

@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <mutex>
 #include <stdexcept>
@@ -32,6 +33,9 @@ struct IoError : Error {
     using Error::Error;
 };
 struct CudaError : Error {
+    using Error::Error;
+};
+struct CommError : Error {  // NCCL failure or NCCL unavailable
     using Error::Error;
 };
 
@@ -74,6 +78,36 @@ void save_weights_file(const HostWeights& w, const std::vector<std::vector<std::
 HostWeights load_weights_file(const std::string& path,
                               const std::vector<std::vector<std::size_t>>& shapes);
 
+// One NCCL communicator (one process per GPU), resolved from libnccl at run time (comm.cpp).
+class Comm {
+public:
+    static std::array<std::uint8_t, 128> unique_id();
+    Comm(int world, int rank, const std::uint8_t* id, int device);
+    ~Comm();
+    Comm(const Comm&) = delete;
+    Comm& operator=(const Comm&) = delete;
+    int world() const { return world_; }
+    int rank() const { return rank_; }
+    void all_reduce_sum_f32(float* buf, std::size_t n, cudaStream_t stream);
+    void all_gather_bytes(const void* send, void* recv, std::size_t bytes, cudaStream_t stream);
+
+private:
+    int world_, rank_, device_;
+    void* comm_ = nullptr;
+};
+
+// Query-row sharding stage (forward over the local rows of a sequence split across G ranks):
+//   stage 1: recentre with the all-reduced centroid sums, project, pack local q/k/v_hat rows;
+//   stage 2: attention of the local queries against all G shards' keys, gathered as
+//            [G][B*H][L_local][pad], then the output projection of the local rows.
+struct ShardStage {
+    int stage = 1;
+    const float* sums = nullptr;   // [B,4] global {sum t, count} (stage 1)
+    const void* k_all = nullptr;   // stage 2
+    const void* v_all = nullptr;
+    int groups = 1;
+};
+
 class FlashIpaLayer {
 public:
     explicit FlashIpaLayer(const Config& cfg);
@@ -94,7 +128,7 @@ public:
     void forward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                  const float* rot, const float* trans, const std::uint8_t* mask, float* out,
                  void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
-                 bool train = false);
+                 bool train = false, const ShardStage* shard = nullptr);
     // Training: forward(..., train=true) over a train_workspace_size() workspace keeps what the
     // backward needs; backward() then consumes the same workspace.  Gradients of
     // sum(out * dout) w.r.t. the inputs (fp32, any of drot/dtrans may be null) and the weights
@@ -111,6 +145,8 @@ public:
                    double* dweights);
     bool backward_supported() const;
     int launches_per_backward() const;
+
+
     void forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
                       const double* z2, const double* rot, const double* trans,
                       const std::uint8_t* mask, double* out);
@@ -151,6 +187,21 @@ public:
     static constexpr int kAccLd = 448;
     int nproj_ld() const { return (dims_.n_proj + 7) / 8 * 8; }
     Workspace carve(void* base, std::int64_t B, std::int64_t L, bool train = false) const;
+
+    // Query-row sharded forward (comm.cpp): this rank holds residues [rank*L, (rank+1)*L) of B
+    // sequences of comm.world()*L residues; out receives its rows.  L % 64 == 0 when world > 1.
+    struct ShardedWorkspace {
+        Workspace local;
+        void* k_all = nullptr;
+        void* v_all = nullptr;
+        float* sums = nullptr;
+        std::size_t kv_bytes = 0, v_bytes = 0, bytes = 0;
+    };
+    ShardedWorkspace carve_sharded(void* base, std::int64_t B, std::int64_t L, int groups) const;
+    std::size_t sharded_workspace_size(std::int64_t B, std::int64_t L, int groups) const;
+    void forward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                         const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                         float* out, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
 
 private:
     void upload_weights();

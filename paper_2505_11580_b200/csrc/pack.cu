@@ -304,7 +304,55 @@ __global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* 
     }
 }
 
+// Query-row sharding: per-sample partial sums {sum x, sum y, sum z, count} of the valid local
+// translations (all-reduced across shards by the caller), then recentring with the global sums.
+__global__ void centroid_sums_kernel(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
+                                     float* __restrict__ sums, int L) {
+    __shared__ float red[4][32];
+    const int b = blockIdx.x;
+    const float* t = trans + int64_t(b) * L * 3;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        if (mask == nullptr || mask[int64_t(b) * L + i] != 0) {
+            v[0] += t[i * 3];
+            v[1] += t[i * 3 + 1];
+            v[2] += t[i * 3 + 2];
+            v[3] += 1.f;
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int k = 0; k < 4; ++k) {
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (l == 0) red[k][w] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        float acc = 0.f;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) acc += red[threadIdx.x][k];
+        sums[b * 4 + threadIdx.x] = acc;
+    }
+}
+
+__global__ void recenter_with_sums_kernel(const float* __restrict__ trans, const float* __restrict__ sums,
+                                          float* __restrict__ out, int L) {
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    const float n = sums[b * 4 + 3] > 0.f ? sums[b * 4 + 3] : 1.f;
+    const int64_t r = (int64_t(b) * L + i) * 3;
+    for (int x = 0; x < 3; ++x) out[r + x] = trans[r + x] - sums[b * 4 + x] / n;
+}
+
 }  // namespace
+
+void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, int B, int L, cudaStream_t stream) {
+    centroid_sums_kernel<<<B, 256, 0, stream>>>(trans, mask, sums, L);
+}
+
+void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream) {
+    dim3 grid((L + 255) / 256, B);
+    recenter_with_sums_kernel<<<grid, 256, 0, stream>>>(trans, sums, out, L);
+}
 
 void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;

@@ -106,4 +106,40 @@ inline CUtensorMap make_map_blocks_f32(const void* base, uint64_t rows, uint64_t
     return m;
 }
 
+// Key/value rows gathered from G shards: bf16 [G][d2][rows][ld] (row i of shard g is global key
+// g*rows + i).  5-D block map {64, rows, ld/64, d2, G}: one box {64, box_rows, nblk, 1, 1} is the
+// same 128-byte-block operand tile as make_map_blocks_bf16.  G = 1 is the unsharded layout.
+inline CUtensorMap make_map_blocks_bf16_sharded(const void* base, uint64_t rows, uint64_t d2, uint64_t G,
+                                                uint64_t ld, uint32_t box_rows, uint32_t nblk) {
+    CUtensorMap m{};
+    cuuint64_t dims[5] = {64, rows, ld / 64, d2, G};
+    cuuint64_t strides[4] = {ld * 2, 128, rows * ld * 2, d2 * rows * ld * 2};
+    cuuint32_t box[5] = {64, box_rows, nblk, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(5d sharded blocks) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
+// bf16 [G][d2][rows][ld] as a 4-D map {ld, rows, d2, G} with box {box0, box1, 1, 1}.
+inline CUtensorMap make_map_4d_bf16_sharded(const void* base, uint64_t ld, uint64_t rows, uint64_t d2, uint64_t G,
+                                            uint32_t box0, uint32_t box1) {
+    CUtensorMap m{};
+    cuuint64_t dims[4] = {ld, rows, d2, G};
+    cuuint64_t strides[3] = {ld * 2, rows * ld * 2, d2 * rows * ld * 2};
+    cuuint32_t box[4] = {box0, box1, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(4d sharded) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 }  // namespace fipa_b200
