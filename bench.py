@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-L", type=int, default=0, help="residues per CPU sample (default L)")
     ap.add_argument("--pass", dest="pass_", choices=["fwd+bwd", "fwd"], default="fwd+bwd")
+    ap.add_argument("--shard", choices=["batch", "rows"], default="batch",
+                    help="batch: independent samples per GPU (weak scaling); rows: one long sequence "
+                         "query-row sharded over the GPUs with an NCCL all-gather of packed K/V (cfg4)")
     return ap.parse_args()
 
 
@@ -397,11 +400,107 @@ def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak,
             "forward_kernel": fwd}
 
 
+def run_sharded(args, shape):
+    """BASELINE cfg4: B sequences of L residues, query rows sharded over the ranks (strong scaling).
+    Forward through fipa_layer_forward_sharded (NCCL all-reduce of the centroid + all-gather of the
+    packed K/V rows inside the timed step)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl" if world > 1 else "gloo", device_id=dev if world > 1 else None,
+                            **({} if world > 1 else dict(rank=0, world_size=1,
+                                                        init_method="tcp://127.0.0.1:%d" % _free_port())))
+    import paper_2505_11580_b200 as fipa
+    from paper_2505_11580_b200 import sharding
+
+    B, L = args.B, args.L
+    lo, hi = sharding.row_block(L, world, rank)
+    n = hi - lo
+    model = fipa.Model(**shape, precision="bf16", seed=0, enforce_head_cap=False)
+    comm = sharding.make_comm(fipa, local)
+    host = synth_inputs(B, L, shape, seed=1234)
+    t = {k: torch.from_numpy(np.ascontiguousarray(v[:, lo:hi])).to(dev) for k, v in host.items()}
+    out = torch.empty((B, n, shape["d_in"]), dtype=torch.float32, device=dev)
+    ws_bytes = model.sharded_workspace_size(B, n, world)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    p = {k: v.data_ptr() for k, v in t.items()}
+
+    def step():
+        model.forward_sharded_device(comm, B, n, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], p["mask"],
+                                     out.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    value = B * L * args.steps / (ms_total / 1e3)
+    flops = attn_flops(shape, B, L)
+    layer_tflops = flops * args.steps / (ms_total / 1e3) / 1e12
+    peak, peak_sus, peak_kind = load_peaks()
+    if rank == 0:
+        kv_bytes = B * shape["heads"] * n * (448 + 448) * 2
+        line = {
+            "metric": METRIC, "value": value, "unit": "residues/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference input distribution), random-init weights",
+            "config": {"workload": f"FlashIPA layer forward, B={B} sequence(s) of L={L}, query rows sharded over "
+                                   f"{world} GPU(s) (BASELINE cfg4)", "pass": "fwd", "model": "FlashIPA layer",
+                       "global_batch": B, "seq_len": L, "shape": shape, "parallelism": f"query-rows x{world}",
+                       "collectives": "NCCL all-reduce (centroid) + all-gather of packed K/V rows "
+                                      f"({kv_bytes * world / 1e6:.1f} MB gathered per rank per step)",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "attn_tflops_whole_layer": layer_tflops,
+            "roofline": {"bound": "tensor", "kernel": "whole sharded layer step (attention-dominated)",
+                         "achieved": layer_tflops / world, "peak": peak, "unit": "TFLOP/s per GPU",
+                         "frac": layer_tflops / world / peak, "traffic": None,
+                         "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
+                         "algorithmic": f"2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per step (all ranks)"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": 6 * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
 def main():
     args = parse()
     shape = dict(SHAPE, rank=args.zrank)
     if args.impl == "reference":
         return run_reference(args, shape)
+    if args.shard == "rows":
+        return run_sharded(args, shape)
     return run_ours(args, shape)
 
 
