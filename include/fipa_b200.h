@@ -142,8 +142,8 @@ int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L, const double* 
                          const double* dout, double* out, double* ds, double* dz1, double* dz2,
                          double* drot, double* dtrans, double* dweights);
 /* Byte offsets of the training intermediates in a train workspace, -1 when absent:
- *   0 o_hat (f32 [B*H,L,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
- *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B*H,L,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
+ *   0 o_hat (f32 [B,L,H,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
+ *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B,L,H,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
  *   7 dfeat (f32 [B*L,feat_ld]).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.  Returns 8. */
 int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
                                       int64_t* dims);

@@ -64,7 +64,7 @@ struct RoleDims {
 };
 
 struct BwdParams {
-    int L;
+    int L, H;
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
     int stat_bytes, b1_stage, b2_stage;
     const float* lse;  // [BH, L] natural-log LSE of the forward
@@ -441,7 +441,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const int n16 = rd.n2 / 16;
             const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
-            float* orow = out + (vec_base + (grow < p.L ? grow : 0)) * p.acc_ld;
+            // residue-major [B, L, H, acc_ld]: the H rows of a residue are contiguous for bwd_unpack
+            const int bb = bh / p.H, hh = bh - bb * p.H;
+            float* orow = out + ((static_cast<int64_t>(bb) * p.L + (grow < p.L ? grow : 0)) * p.H + hh) * p.acc_ld;
             for (int ch = lo; ch < hi; ++ch) {
                 uint32_t o[16];
                 ptx::tmem_ld16(tl + 16 * ch, o);
@@ -517,6 +519,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
         p.L = a.L;
+        p.H = d.heads;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
         finish_params(p);
@@ -532,6 +535,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     if (which & 2) {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
         BwdParams p{};
         p.L = a.L;
+        p.H = d.heads;
         p.role[0] = make_role(d.dqk_mma, 0);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
         finish_params(p);

@@ -525,7 +525,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // tcgen05.ld is warp-collective: load first, store only rows inside the sequence.
             const int n16 = p.dv_mma / 16;
             const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
-            float* orow = p.o_save + (static_cast<int64_t>(bh) * p.L + (qi < p.L ? qi : 0)) * p.dv_pad;
+            // residue-major [B, L, H, dv_pad]: bwd_prep stages a residue's H rows with one copy
+            const int ob = bh / p.H, oh = bh - ob * p.H;
+            float* orow = p.o_save + ((static_cast<int64_t>(ob) * p.L + (qi < p.L ? qi : 0)) * p.H + oh) * p.dv_pad;
             for (int ch = lo; ch < hi; ++ch) {
                 uint32_t o[16];
                 ptx::tmem_ld16(tl + 16 * ch, o);

@@ -23,6 +23,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "ptx.cuh"
 
 namespace fipa_b200 {
 
@@ -41,20 +42,43 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// One block per residue (b, i), warp w handles heads w, w+8, ...; rows are read with 16-byte
-// vector loads and dO_hat written 4 columns (8 bytes) per lane.  Cross-head sums (dz1, frames)
-// go through per-warp shared-memory slices, no atomics.
-__global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
-    extern __shared__ float sm[];
+// Bulk (TMA-engine) copy of `bytes` contiguous global bytes into shared memory, completion
+// counted on a local mbarrier.  The memory-bound backward kernels stage whole rows this way: one
+// instruction moves a 1.7-10 KB row, so the LSU queues (the "lg_throttle" stall that dominated
+// the per-lane version, profiles/r1_bwd_ncu_summary.json) stay empty and many KB stay in flight.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(ptx::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
+                 : "memory");
+}
+
+// One block per residue (b, i), warp w handles heads w, w+8, ...  The residue's dfeat row and the
+// H saved O_hat rows arrive by bulk copies; dO_hat rows are assembled in shared memory and
+// written with 16-byte stores; cross-head sums (dz1, frames) go through per-warp slices.
+__global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
+    extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nv = d.n_value;
     const int nw = blockDim.x >> 5;
-    float* s_z1 = sm;                        // rdz
-    float* s_pair = s_z1 + rdz;              // nw x rdz   per-warp dz1 partials
-    float* s_geo = s_pair + nw * rdz;        // nw x 12    per-warp dR (9) | dt (3)
-    float* s_dopt = s_geo + nw * 12;         // nw x 3*Nv
+    float* s_df = sm;                               // feat_ld   dfeat row
+    float* s_o = s_df + d.feat_ld;                  // H x dv_pad  O_hat rows
+    float* s_z1 = s_o + H * d.dv_pad;               // rdz
+    float* s_pair = s_z1 + ((rdz + 3) & ~3);        // nw x rdz   per-warp dz1 partials
+    float* s_geo = s_pair + nw * rdz;               // nw x 12    per-warp dR (9) | dt (3)
+    float* s_dopt = s_geo + nw * 12;                // nw x 3*Nv
+    __nv_bfloat16* s_out = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(s_dopt + nw * 3 * Nv) + 15) & ~uintptr_t(15));  // H x dv_pad
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_out + H * d.dv_pad);
     const int64_t row = blockIdx.x;
     const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::fence_mbar_init();
+        const uint32_t df_bytes = d.feat_ld * 4, o_bytes = d.dv_pad * 4;
+        ptx::mbar_expect_tx(bar, df_bytes + H * o_bytes);
+        bulk_g2s(s_df, a.dfeat + row * d.feat_ld, df_bytes, bar);
+        bulk_g2s(s_o, a.ohat + row * H * d.dv_pad, H * o_bytes, bar);  // residue-major O_hat rows
+    }
     for (int e = threadIdx.x; e < rdz; e += blockDim.x) s_z1[e] = a.z1[row * rdz + e];
     for (int e = threadIdx.x; e < nw * (rdz + 12); e += blockDim.x) s_pair[e] = 0.f;  // s_pair + s_geo
     float R[9], t[3];
@@ -63,6 +87,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
 #pragma unroll
     for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
     __syncthreads();
+    ptx::mbar_wait(bar, 0);
 
     const int vpair = c + rdz, vpts = vpair + 6, vend = vpts + 3 * Nv;
     float* dopt_s = s_dopt + warp * 3 * Nv;
@@ -70,8 +95,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
     float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
     for (int h = warp; h < H; h += nw) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
-        const float* o = a.ohat + hrow * d.dv_pad;
-        const float* df = a.dfeat + row * d.feat_ld + static_cast<int64_t>(h) * d.seg;
+        const float* o = s_o + h * d.dv_pad;
+        const float* df = s_df + h * d.seg;
         float ds[3] = {0.f, 0.f, 0.f};
         if (lane < Nv) {
             const int p = lane;
@@ -100,7 +125,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
 #pragma unroll
         for (int x = 0; x < 3; ++x) ds[x] = warp_sum(ds[x]);
         __syncwarp();
-        __nv_bfloat16* out = a.dohat + hrow * d.dv_pad;
+        __nv_bfloat16* out = s_out + h * d.dv_pad;
         float Dp = 0.f;
         for (int c4 = lane; 4 * c4 < d.dv_pad; c4 += 32) {
             const float4 ov = *reinterpret_cast<const float4*>(o + 4 * c4);
@@ -141,6 +166,12 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
     for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
     if (lane < 12) s_geo[warp * 12 + lane] = lane < 9 ? dR[lane] : dt[lane - 9];
     __syncthreads();
+    const int per_row = d.dv_pad / 8;  // 16-byte chunks per dO_hat row
+    for (int e = threadIdx.x; e < H * per_row; e += blockDim.x) {
+        const int h = e / per_row, k = e - h * per_row;
+        reinterpret_cast<uint4*>(a.dohat + ((static_cast<int64_t>(b) * H + h) * a.L + i) * d.dv_pad)[k] =
+            reinterpret_cast<const uint4*>(s_out + h * d.dv_pad)[k];
+    }
     for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
         float acc = 0.f;
         for (int w = 0; w < nw; ++w) acc += s_pair[w * rdz + e];
@@ -156,53 +187,96 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(LayerDims d, BwdPrepArgs 
 
 constexpr int kUnpackRows = 8;
 
-// Block = 8 warps, warp w handles heads w, w+8, ... of kUnpackRows consecutive residues.  Per
-// (residue, head) the warp stages the three accumulator rows in its shared-memory slice with
-// 16-byte loads, then derives the natural gradients; cross-head sums go through shared memory,
-// d(w_l w_bias) and d(g) are flushed with one global atomic per entry per block.
-__global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a, int stage_w) {
-    extern __shared__ float sm[];
+// Block = 8 warps, warp w handles heads w, w+8, ... of kUnpackRows consecutive residues.  The
+// residue's 3*H accumulator rows (and the point columns of its projection row) arrive by bulk
+// copies into one of two shared-memory stages while the previous residue is being processed;
+// the dproj row is assembled in shared memory and written with 16-byte stores.  Cross-head sums
+// go through shared memory; d(w_l w_bias) and d(g) are flushed with one global atomic per entry
+// per block.
+__global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a, int stage_w) {
+    extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_acc = sm;                                  // nw x 3 x stage_w
-    float* s_pq = s_acc + nw * 3 * stage_w;             // H x rdz  query-side pair grads
-    float* s_pk = s_pq + H * rdz;                       // H x rdz  key+value-side pair grads
-    float* s_geo = s_pk + H * rdz;                      // H x 12
-    float* s_dwlb = s_geo + H * 12;                     // H x dz
-    float* s_dg = s_dwlb + H * dz;                      // H
-    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) s_dwlb[e] = 0.f;
     const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
+    const int npts = d.n_proj - off_qp;                       // point columns of a projection row
+    const int npts_pad = (npts + 3) & ~3;
+    const int rdz_pad = (rdz + 3) & ~3;
+    const int stage_floats = 3 * H * stage_w + npts_pad + rdz_pad;  // one residue: dq|dk|dv rows, points, z2
+    float* s_stage = sm;                                      // 2 x stage_floats
+    float* s_pq = s_stage + 2 * stage_floats;                 // H x rdz  query-side pair grads
+    float* s_pk = s_pq + H * rdz;                             // H x rdz  key+value-side pair grads
+    float* s_geo = s_pk + H * rdz;                            // H x 12
+    float* s_dwlb = s_geo + H * 12;                           // H x dz
+    float* s_dg = s_dwlb + H * dz;                            // H
+    float* s_wlb = s_dg + H;                                  // H x dz  w_l w_bias
+    __nv_bfloat16* s_dp = reinterpret_cast<__nv_bfloat16*>((reinterpret_cast<uintptr_t>(s_wlb + H * dz) + 15) & ~uintptr_t(15));
+    uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_dp + a.nproj_ld) + 7) & ~uintptr_t(7));
     const int g0 = c + 3 * Nq, zq = g0 + 21, vpair = c + rdz;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
     const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
-    float* qa = s_acc + warp * 3 * stage_w;
-    float* ka = qa + stage_w;
-    float* va = ka + stage_w;
+    const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
+    const bool pts_bulk = ((off_qp * 4) & 15) == 0 && ((d.n_proj * 4) & 15) == 0 && ((npts * 4) & 15) == 0 &&
+                          ((rdz * 4) & 15) == 0;
+    // d(w_l w_bias) partials live in the head's warp-private slice; lanes of one step never share
+    // a d_z index when d_z >= 32, so plain adds suffice there
+    const bool dwlb_plain = dz >= 32;
+
+    auto issue = [&](int rr) {  // thread 0: stage residue row_begin + rr into buffer rr & 1
+        const int64_t row = row_begin + rr;
+        const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
+        float* st = s_stage + (rr & 1) * stage_floats;
+        uint64_t* bar = bars + (rr & 1);
+        (void)b;
+        (void)i;
+        // accumulators are residue-major [B, L, H, acc_ld]: one copy per tensor moves all heads
+        const uint32_t rbytes = H * stage_w * 4;
+        ptx::mbar_expect_tx(bar, 3 * rbytes + (pts_bulk ? (npts + rdz) * 4 : 0));
+        const int64_t arow = row * H * a.acc_ld;
+        bulk_g2s(st, a.dq_acc + arow, rbytes, bar);
+        bulk_g2s(st + H * stage_w, a.dk_acc + arow, rbytes, bar);
+        bulk_g2s(st + 2 * H * stage_w, a.dv_acc + arow, rbytes, bar);
+        if (pts_bulk) {
+            bulk_g2s(st + 3 * H * stage_w, a.proj + row * d.n_proj + off_qp, npts * 4, bar);
+            bulk_g2s(st + 3 * H * stage_w + npts_pad, a.z2 + row * rdz, rdz * 4, bar);
+        }
+    };
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bars[0], 1);
+        ptx::mbar_init(&bars[1], 1);
+        ptx::fence_mbar_init();
+        if (nrows > 0) issue(0);
+    }
+    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) s_dwlb[e] = 0.f;
+    for (int e = threadIdx.x; e < H * dz; e += blockDim.x) s_wlb[e] = a.wl_bias[e];
     __syncthreads();
 
-    for (int rr = 0; rr < kUnpackRows; ++rr) {
+    for (int rr = 0; rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
-        if (row >= BL) break;
-        const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
+        // prefetch the next residue into the other stage (freed by the previous iteration's sync)
+        if (threadIdx.x == 0 && rr + 1 < nrows) issue(rr + 1);
+        float* st = s_stage + (rr & 1) * stage_floats;
+        if (!pts_bulk) {
+            for (int e = threadIdx.x; e < npts; e += blockDim.x) st[3 * H * stage_w + e] = a.proj[row * d.n_proj + off_qp + e];
+            for (int e = threadIdx.x; e < rdz; e += blockDim.x) st[3 * H * stage_w + npts_pad + e] = a.z2[row * rdz + e];
+        }
         float R[9], t[3];
 #pragma unroll
         for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
 #pragma unroll
         for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
-        const float* pr = a.proj + row * d.n_proj;
-        const float* z2 = a.z2 + row * rdz;
-        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+        const float* z2 = st + 3 * H * stage_w + npts_pad;
+        const float* pr = st + 3 * H * stage_w - off_qp;  // pr[off_qp + ...] = point columns
+        if (!pts_bulk) __syncthreads();
+        ptx::mbar_wait(&bars[rr & 1], (rr >> 1) & 1);
+        __nv_bfloat16* dp = s_dp;
         for (int h = warp; h < H; h += nw) {
-            const int64_t arow = ((static_cast<int64_t>(b) * H + h) * a.L + i) * a.acc_ld;
-            for (int e4 = lane; 4 * e4 < stage_w; e4 += 32) {
-                reinterpret_cast<float4*>(qa)[e4] = __ldg(reinterpret_cast<const float4*>(a.dq_acc + arow) + e4);
-                reinterpret_cast<float4*>(ka)[e4] = __ldg(reinterpret_cast<const float4*>(a.dk_acc + arow) + e4);
-                reinterpret_cast<float4*>(va)[e4] = __ldg(reinterpret_cast<const float4*>(a.dv_acc + arow) + e4);
-            }
-            __syncwarp();
-            // scalar channels (bf16 pairs)
+            const float* qa = st + (0 * H + h) * stage_w;
+            const float* ka = st + (1 * H + h) * stage_w;
+            const float* va = st + (2 * H + h) * stage_w;
+            // scalar channels (bf16 pairs into the staged dproj row)
             for (int c2 = lane; 2 * c2 < c; c2 += 32) {
                 const int cc = 2 * c2;
                 const int o = h * c + cc;
@@ -224,8 +298,9 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
                 const int dd = e % dz;
                 const float kq = kLn2 * ka[zq + e];
                 s_pq[h * rdz + e] = qa[zq + e];
-                s_pk[h * rdz + e] = a.wl_bias[h * dz + dd] * kq + va[c + e];
-                atomicAdd(&s_dwlb[h * dz + dd], kq * z2[e]);
+                s_pk[h * rdz + e] = s_wlb[h * dz + dd] * kq + va[c + e];
+                if (dwlb_plain) s_dwlb[h * dz + dd] += kq * z2[e];
+                else atomicAdd(&s_dwlb[h * dz + dd], kq * z2[e]);
             }
             // geometry: lane per point
             const float g = a.head_g[h];
@@ -315,6 +390,11 @@ __global__ void __launch_bounds__(256) bwd_unpack_kernel(LayerDims d, BwdUnpackA
             __syncwarp();
         }
         __syncthreads();
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(s_dp);
+            uint4* dst = reinterpret_cast<uint4*>(a.dproj + row * a.nproj_ld);
+            for (int e = threadIdx.x; e < a.nproj_ld / 8; e += blockDim.x) dst[e] = src[e];
+        }
         for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
             float s1 = a.dz1_epi[row * rdz + e], s2 = 0.f;
             for (int h = 0; h < H; ++h) {
@@ -410,18 +490,26 @@ __global__ void scale_vec_kernel(const float* in, const float* scale, int period
 
 void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
-    const size_t smem = sizeof(float) * (rdz + 8 * (rdz + 12 + 3 * d.n_value));
+    if ((d.feat_ld * 4) % 16 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
+        throw std::invalid_argument("bwd_prep: row strides must be multiples of 16 bytes");
+    const size_t smem = sizeof(float) * (d.feat_ld + d.heads * d.dv_pad + ((rdz + 3) & ~3) +
+                                         8 * (rdz + 12 + 3 * d.n_value)) +
+                        16 + 2 * size_t(d.heads) * d.dv_pad + 16;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     bwd_prep_kernel<<<static_cast<unsigned>(int64_t(a.B) * a.L), 256, smem, stream>>>(d, a);
 }
 
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
-    // staged accumulator width: every column the unpack reads, rounded to 16-byte vectors
-    const int need = std::max(d.dqk_used, d.dv_used);
-    const int stage_w = (need + 3) / 4 * 4;
-    if (stage_w > a.acc_ld) throw std::invalid_argument("bwd_unpack: accumulator stride too small");
-    const size_t smem = sizeof(float) * (8 * 3 * stage_w + 2 * d.heads * rdz + d.heads * 12 + d.heads * d.d_z + d.heads);
+    // a residue's H accumulator rows are staged whole (row stride acc_ld)
+    const int stage_w = a.acc_ld;
+    if (std::max(d.dqk_used, d.dv_used) > a.acc_ld || (a.acc_ld * 4) % 16)
+        throw std::invalid_argument("bwd_unpack: accumulator stride");
+    if (a.nproj_ld % 8 != 0) throw std::invalid_argument("bwd_unpack: dproj stride must be a multiple of 8");
+    const int npts = d.n_proj - 3 * d.heads * d.c;
+    const int stage_floats = 3 * d.heads * stage_w + ((npts + 3) & ~3) + ((rdz + 3) & ~3);
+    const size_t smem = sizeof(float) * (2 * stage_floats + 2 * d.heads * rdz + d.heads * 12 + 2 * d.heads * d.d_z +
+                                         d.heads) + 16 + 2 * size_t(a.nproj_ld) + 8 + 16;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int64_t BL = int64_t(a.B) * a.L;
     bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a, stage_w);

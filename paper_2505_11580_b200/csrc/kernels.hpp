@@ -80,7 +80,7 @@ struct AttnArgs {
     const float* trans;
     __nv_bfloat16* feat;   // [BL, feat]
     float* lse;            // [B*H, L] natural-log LSE of the shifted logits
-    float* o_save;         // [B*H, L, dv_pad] normalised O_hat (fp32) for the backward, or null
+    float* o_save;         // [B, L, H, dv_pad] normalised O_hat (fp32, residue-major) for the backward, or null
     int B, L;              // L = query rows (local rows when sharded)
     // Keys (query-row sharding): khat/vhat hold Lk keys as kgroups shards of kchunk rows,
     // [kgroups][B*H][kchunk][pad] (shard g = keys g*kchunk ..).  0 = unsharded (Lk = L).
@@ -101,7 +101,7 @@ struct AttnBwdArgs {
     const __nv_bfloat16* dohat;  // [B*H, L, dv_pad]
     const float* lse;            // [B*H, L]
     const float* Dvec;           // [B*H, L]
-    float* dq_acc;               // [B*H, L, acc_ld] = dS . K_hat
+    float* dq_acc;               // [B, L, H, acc_ld] (residue-major) = dS . K_hat
     float* dk_acc;               //                  = dS^T . Q_hat
     float* dv_acc;               //                  = P^T . dO_hat
     int acc_ld;
@@ -113,7 +113,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
 
 struct BwdPrepArgs {
     const float* dfeat;           // [BL, feat_ld] dOut . w_out^T
-    const float* ohat;            // [B*H, L, dv_pad] fp32, saved by the forward
+    const float* ohat;            // [B, L, H, dv_pad] fp32 (residue-major), saved by the forward
     const float* z1;              // [BL, r*d_z]
     const float* rot;             // [BL, 9]
     const float* trans_c;         // [BL, 3] recentred

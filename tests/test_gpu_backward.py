@@ -102,7 +102,7 @@ def test_attention_backward_stage_parity(fipa):
     k = ws_view(ws, off[4], H * L * dqk_pad, "bf16").reshape(H, L, dqk_pad)
     v = ws_view(ws, off[5], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
     lse = ws_view(ws, off[7], H * L, "f32").reshape(H, L)
-    o = ws_view(ws, toff[0], H * L * dv_pad, "f32").reshape(H, L, dv_pad)
+    o = ws_view(ws, toff[0], H * L * dv_pad, "f32").reshape(L, H, dv_pad).transpose(1, 0, 2)
     do = ws_view(ws, toff[1], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
     D = ws_view(ws, toff[2], H * L, "f32").reshape(H, L)
     o_ref, lse_ref = be.attention(q, k, v, L)
@@ -111,7 +111,7 @@ def test_attention_backward_stage_parity(fipa):
     assert rel_dev((do * o).sum(-1), D) < 1e-3
     dq_r, dk_r, dv_r = be.attention_backward(q, k, v, lse, do, D)
     for name, idx, ref in (("dq", 3, dq_r), ("dk", 4, dk_r), ("dv", 5, dv_r)):
-        got = ws_view(ws, toff[idx], H * L * acc_ld, "f32").reshape(H, L, acc_ld)
+        got = ws_view(ws, toff[idx], H * L * acc_ld, "f32").reshape(L, H, acc_ld).transpose(1, 0, 2)
         assert rel_dev(ref[..., :432], got[..., :432]) < 1e-2, name
 
 

@@ -28,10 +28,10 @@ q = ws_view(ws, off[3], H * L * dqk_pad, "bf16").reshape(H, L, dqk_pad)
 k = ws_view(ws, off[4], H * L * dqk_pad, "bf16").reshape(H, L, dqk_pad)
 v = ws_view(ws, off[5], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
 lse = ws_view(ws, off[7], H * L, "f32").reshape(H, L)
-o = ws_view(ws, toff[0], H * L * dv_pad, "f32").reshape(H, L, dv_pad)
+o = ws_view(ws, toff[0], H * L * dv_pad, "f32").reshape(L, H, dv_pad).transpose(1, 0, 2)
 do = ws_view(ws, toff[1], H * L * dv_pad, "bf16").reshape(H, L, dv_pad)
 D = ws_view(ws, toff[2], H * L, "f32").reshape(H, L)
-accs = [ws_view(ws, toff[i], H * L * acc_ld, "f32").reshape(H, L, acc_ld) for i in (3, 4, 5)]
+accs = [ws_view(ws, toff[i], H * L * acc_ld, "f32").reshape(L, H, acc_ld).transpose(1, 0, 2) for i in (3, 4, 5)]
 dproj = ws_view(ws, toff[6], L * nproj_ld, "bf16").reshape(L, nproj_ld)[:, :n_proj]
 o_ref, lse_ref = be.attention(q, k, v, L)
 print("O vs emu(device qkv):", rel_dev(o_ref, o), "lse:", rel_dev(lse_ref, lse))
