@@ -182,6 +182,28 @@ int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_local, int w
                             const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* -------------------------------------------------------------------------- trunk
+ * BASELINE cfg3: n_layers FlashIPA layers with residual and per-layer backbone frame update
+ * (FrameFlow-style; the reference has no trunk -- the definition is oracle/fipa_oracle.py
+ * trunk_forward):  s <- s + layer_l(s, z, T);  u = s.W_bb,l + b_bb,l;
+ * T <- compose(T, (R(normalised (1, u0, u1, u2)), u[3:6])) (proj/src/geometry.cpp:78-90, 107-132).
+ * Layer l has IpaWeights::init(cfg, Rng(seed + l)); fipa_trunk_layer returns a borrowed layer
+ * handle (get/set/save/load weights through the layer API; fipa_layer_destroy on it is a no-op). */
+typedef struct fipa_trunk fipa_trunk;
+int fipa_trunk_create(const fipa_config* cfg, int n_layers, uint64_t seed, fipa_trunk** out);
+void fipa_trunk_destroy(fipa_trunk* trunk);
+int fipa_trunk_num_layers(const fipa_trunk* trunk);
+fipa_layer* fipa_trunk_layer(fipa_trunk* trunk, int layer);
+int fipa_trunk_get_backbone(const fipa_trunk* trunk, int layer, double* w /* [d_in*6] */, double* b /* [6] */);
+int fipa_trunk_set_backbone(fipa_trunk* trunk, int layer, const double* w, const double* b);
+size_t fipa_trunk_workspace_size(const fipa_trunk* trunk, int64_t B, int64_t L);
+/* Device buffers as in fipa_layer_forward; outputs s_out [B,L,d_in], rot_out [B,L,3,3],
+ * trans_out [B,L,3] (may alias the inputs). */
+int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L, const float* s, const float* z1, const float* z2,
+                       const float* rot, const float* trans, const uint8_t* mask, float* s_out, float* rot_out,
+                       float* trans_out, void* workspace, size_t workspace_bytes, void* stream);
+int fipa_trunk_forward_launches(const fipa_trunk* trunk);
+
 /* Number of kernels fipa_layer_forward launches per call for this configuration. */
 int fipa_layer_forward_launches(const fipa_layer* layer);
 

@@ -518,3 +518,51 @@ def flash_ipa_backward(s, z1, z2, rot, trans, mask, cfg: IpaConfig, w, dout):
         g[name] = s.T @ f
         g["s"] += f @ w[name].T
     return g
+
+
+# ------------------------------------------------------------------------- trunk
+# BASELINE cfg3 ("6-layer FrameFlow-style IPA trunk with per-layer backbone frame update").  The
+# reference has no trunk, residual or backbone update (proj/SPEC.md:307), so the
+# build defines one, FrameFlow-style, from reference pieces: per layer
+#   s <- s + flash_ipa_forward(s, z, T)                       (proj/src/flash_ipa.cpp:141-218)
+#   u = s . W_bb + b_bb  (Linear(c_s, 6)),  q = (1, u0, u1, u2)/|.|,  dT = (R(q), u[3:6])
+#   T <- compose(T, dT) = (R dR, R du + t)                    (proj/src/geometry.cpp:78-90)
+# with R(q) the reference's quaternion->matrix map (geometry.cpp:107-132); masked residues keep
+# their frames.  Layer l's IPA weights are IpaWeights::init(cfg, Rng(seed + l)); its backbone
+# weights are N(0, (0.1/sqrt(d_in))^2) draws from Rng(seed + 1000 + l), bias zero.
+def quat_to_rot(qw, qx, qy, qz):
+    """Normalised quaternion -> rotation (the matrix of proj/src/geometry.cpp:107-132)."""
+    n = np.sqrt(qw * qw + qx * qx + qy * qy + qz * qz)
+    qw, qx, qy, qz = qw / n, qx / n, qy / n, qz / n
+    r = np.stack([
+        1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+        2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+        2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)], -1)
+    return r.reshape(np.shape(qw) + (3, 3))
+
+
+def init_backbone(cfg: IpaConfig, seed: int, layer: int):
+    w = gaussian_tensor(Rng(seed + 1000 + layer), (cfg.d_in, 6), 0.1 / math.sqrt(cfg.d_in))
+    return {"w": w, "b": np.zeros(6)}
+
+
+def init_trunk(cfg: IpaConfig, n_layers: int, seed: int):
+    return ([init_weights(cfg, seed + l) for l in range(n_layers)],
+            [init_backbone(cfg, seed, l) for l in range(n_layers)])
+
+
+def backbone_update(s, rot, trans, mask, bb):
+    u = s @ bb["w"] + bb["b"]
+    dR = quat_to_rot(np.ones(len(s)), u[:, 0], u[:, 1], u[:, 2])
+    new_rot = np.einsum("lab,lbc->lac", rot, dR)
+    new_t = np.einsum("lab,lb->la", rot, u[:, 3:6]) + trans
+    m = np.asarray(mask, bool)[:, None]
+    return np.where(m[..., None], new_rot, rot), np.where(m, new_t, trans)
+
+
+def trunk_forward(s, z1, z2, rot, trans, mask, cfg: IpaConfig, layers, backbones):
+    mask = np.ones(s.shape[0], bool) if mask is None else np.asarray(mask, bool)
+    for w, bb in zip(layers, backbones):
+        s = s + flash_ipa_forward(s, z1, z2, rot, trans, mask, cfg, w)
+        rot, trans = backbone_update(s, rot, trans, mask, bb)
+    return s, rot, trans

@@ -29,8 +29,8 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_tc.cu", "pack.cu", "attn_fwd_tc.cu", "attn_fwd_2sm.cu", "simt_f32.cu", "attn_bwd.cu",
               "bwd.cu"]
-CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp"]
-HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp"]
+CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp", "trunk.cpp"]
+HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp", "trunk.hpp"]
 
 LIB_NAME = "libfipa_b200.so"
 EXT_NAME = "_fipa_b200" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so")

@@ -110,6 +110,9 @@ public:
         check(fipa_layer_create(&cfg_, &layer_));
         check(fipa_layer_init_weights(layer_, seed));
     }
+    // Borrowed view of a trunk layer (fipa_trunk_layer); destroying it is a no-op in the C ABI.
+    Model(fipa_layer* borrowed, const fipa_config& cfg, const std::string& precision)
+        : cfg_(cfg), layer_(borrowed), precision_name_(precision) {}
     ~Model() { fipa_layer_destroy(layer_); }
     Model(const Model&) = delete;
     Model& operator=(const Model&) = delete;
@@ -413,6 +416,64 @@ private:
 
 }  // namespace
 
+// BASELINE cfg3 trunk: n_layers layers + residual + backbone frame update (fipa_trunk_* C ABI).
+class Trunk {
+public:
+    Trunk(uint64_t d_in, uint64_t d_z, uint64_t heads, uint64_t c, uint64_t n_query, uint64_t n_value, uint64_t rank,
+          const std::string& precision, uint64_t seed, bool enforce_head_cap, int n_layers)
+        : precision_name_(precision) {
+        cfg_.d_in = d_in;
+        cfg_.d_z = d_z;
+        cfg_.heads = heads;
+        cfg_.c = c;
+        cfg_.n_query = n_query;
+        cfg_.n_value = n_value;
+        cfg_.rank = rank;
+        cfg_.precision = parse_precision(precision);
+        cfg_.enforce_head_cap = enforce_head_cap ? 1 : 0;
+        check(fipa_config_validate(&cfg_));
+        check(fipa_trunk_create(&cfg_, n_layers, seed, &trunk_));
+    }
+    ~Trunk() { fipa_trunk_destroy(trunk_); }
+    Trunk(const Trunk&) = delete;
+    Trunk& operator=(const Trunk&) = delete;
+    int n_layers() const { return fipa_trunk_num_layers(trunk_); }
+    Model* layer(int l) {
+        fipa_layer* v = fipa_trunk_layer(trunk_, l);
+        if (v == nullptr) throw FipaValueError("layer index out of range");
+        return new Model(v, cfg_, precision_name_);
+    }
+    py::tuple backbone(int l) const {
+        py::array_t<double> w(std::vector<py::ssize_t>{(py::ssize_t)cfg_.d_in, 6}), b(6);
+        check(fipa_trunk_get_backbone(trunk_, l, w.mutable_data(), b.mutable_data()));
+        return py::make_tuple(w, b);
+    }
+    void set_backbone(int l, const DArr& w, const DArr& b) {
+        if (w.size() != int64_t(cfg_.d_in * 6) || b.size() != 6) throw FipaValueError("backbone must be [d_in, 6] and [6]");
+        check(fipa_trunk_set_backbone(trunk_, l, w.data(), b.data()));
+    }
+    size_t workspace_size(int64_t B, int64_t L) const { return fipa_trunk_workspace_size(trunk_, B, L); }
+    void forward_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot, uintptr_t trans,
+                        uintptr_t mask, uintptr_t s_out, uintptr_t rot_out, uintptr_t trans_out, uintptr_t ws,
+                        size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_trunk_forward(trunk_, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                    reinterpret_cast<const uint8_t*>(mask), f(s_out), f(rot_out), f(trans_out),
+                                    reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    int forward_launches() const { return fipa_trunk_forward_launches(trunk_); }
+
+private:
+    fipa_config cfg_{};
+    fipa_trunk* trunk_ = nullptr;
+    std::string precision_name_;
+};
+
 PYBIND11_MODULE(_fipa_b200, m) {
     m.doc() = "B200-native FlashIPA layer (tcgen05 sm_100a kernels behind the reference fipa.Model API)";
 
@@ -479,4 +540,19 @@ PYBIND11_MODULE(_fipa_b200, m) {
         .def("bwd_stage_times", &Model::bwd_stage_times)
         .def_property_readonly("precision", &Model::precision)
         .def_property_readonly("config", &Model::config);
+    py::class_<Trunk>(m, "Trunk", "FlashIPA trunk: layers + residual + per-layer backbone frame update (cfg3)")
+        .def(py::init<uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, const std::string&, uint64_t,
+                      bool, int>(),
+             py::arg("d_in") = 32, py::arg("d_z") = 4, py::arg("heads") = 2, py::arg("c") = 8, py::arg("n_query") = 2,
+             py::arg("n_value") = 2, py::arg("rank") = 2, py::arg("precision") = "bf16", py::arg("seed") = 0,
+             py::arg("enforce_head_cap") = true, py::arg("n_layers") = 6)
+        .def_property_readonly("n_layers", &Trunk::n_layers)
+        .def("layer", &Trunk::layer, py::arg("index"), py::keep_alive<0, 1>(), py::return_value_policy::take_ownership)
+        .def("backbone", &Trunk::backbone, py::arg("index"))
+        .def("set_backbone", &Trunk::set_backbone, py::arg("index"), py::arg("w"), py::arg("b"))
+        .def("workspace_size", &Trunk::workspace_size, py::arg("B"), py::arg("L"))
+        .def("forward_device", &Trunk::forward_device, py::arg("B"), py::arg("L"), py::arg("s"), py::arg("z1"),
+             py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("s_out"), py::arg("rot_out"),
+             py::arg("trans_out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("forward_launches", &Trunk::forward_launches);
 }

@@ -4,14 +4,28 @@
 #include "../../include/fipa_b200.h"
 
 #include <exception>
+#include <memory>
+#include <vector>
 #include <new>
 #include <string>
 
 #include "layer.hpp"
+#include "trunk.hpp"
 
 struct fipa_layer {
-    fipa_b200::FlashIpaLayer impl;
-    explicit fipa_layer(const fipa_b200::Config& c) : impl(c) {}
+    std::unique_ptr<fipa_b200::FlashIpaLayer> owned;  // null for a trunk's borrowed layer view
+    fipa_b200::FlashIpaLayer* impl;
+    explicit fipa_layer(const fipa_b200::Config& c)
+        : owned(std::make_unique<fipa_b200::FlashIpaLayer>(c)), impl(owned.get()) {}
+    explicit fipa_layer(fipa_b200::FlashIpaLayer* borrowed) : impl(borrowed) {}
+};
+
+struct fipa_trunk {
+    fipa_b200::Trunk impl;
+    std::vector<std::unique_ptr<fipa_layer>> views;
+    fipa_trunk(const fipa_b200::Config& c, int n, uint64_t seed) : impl(c, n, seed) {
+        for (int l = 0; l < n; ++l) views.push_back(std::make_unique<fipa_layer>(&impl.layer(l)));
+    }
 };
 
 struct fipa_comm {
@@ -81,11 +95,11 @@ fipa_b200::Config to_cfg(const fipa_config* c) {
 
 fipa_b200::FlashIpaLayer& L(fipa_layer* l) {
     if (l == nullptr) throw fipa_b200::ValueError("null fipa_layer");
-    return l->impl;
+    return *l->impl;
 }
 const fipa_b200::FlashIpaLayer& L(const fipa_layer* l) {
     if (l == nullptr) throw fipa_b200::ValueError("null fipa_layer");
-    return l->impl;
+    return *l->impl;
 }
 
 }  // namespace
@@ -114,7 +128,9 @@ int fipa_layer_create(const fipa_config* cfg, fipa_layer** out) {
     });
 }
 
-void fipa_layer_destroy(fipa_layer* layer) { delete layer; }
+void fipa_layer_destroy(fipa_layer* layer) {
+    if (layer != nullptr && layer->owned) delete layer;  // trunk layer views are owned by the trunk
+}
 
 int fipa_layer_init_weights(fipa_layer* layer, uint64_t seed) {
     return guarded([&] { L(layer).init_weights(seed); });
@@ -171,7 +187,7 @@ int fipa_layer_load_weights(fipa_layer* layer, const char* path) {
 
 size_t fipa_layer_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_) {
     if (layer == nullptr || B < 1 || L_ < 1) return 0;
-    return layer->impl.workspace_size(B, L_);
+    return layer->impl->workspace_size(B, L_);
 }
 
 int fipa_layer_forward(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
@@ -195,12 +211,12 @@ int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L_, const doub
 int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, int64_t* offsets,
                                 int64_t* dims) {
     if (layer == nullptr || offsets == nullptr || B < 1 || L_ < 1) return 0;
-    const auto w = layer->impl.carve(nullptr, B, L_);
+    const auto w = layer->impl->carve(nullptr, B, L_);
     // carve(nullptr) yields null-based pointers: offsets are the pointer values themselves.
     auto off = [](const void* p, bool present) -> int64_t {
         return present ? static_cast<int64_t>(reinterpret_cast<uintptr_t>(p)) : -1;
     };
-    const bool bf16 = layer->impl.config().precision == fipa_b200::Precision::bf16;
+    const bool bf16 = layer->impl->config().precision == fipa_b200::Precision::bf16;
     offsets[0] = off(w.trans_c, true);
     offsets[1] = off(w.s_bf16, bf16);
     offsets[2] = off(w.proj, true);
@@ -211,7 +227,7 @@ int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, 
     offsets[7] = off(w.lse, true);
     offsets[8] = off(w.feat, true);
     if (dims != nullptr) {
-        const auto& d = layer->impl.dims();
+        const auto& d = layer->impl->dims();
         dims[0] = d.n_proj;
         dims[1] = d.dqk_pad;
         dims[2] = d.dv_pad;
@@ -221,7 +237,7 @@ int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, 
 }
 
 int fipa_layer_forward_launches(const fipa_layer* layer) {
-    return layer ? layer->impl.launches_per_forward() : 0;
+    return layer ? layer->impl->launches_per_forward() : 0;
 }
 
 int fipa_layer_set_timing(fipa_layer* layer, int enable) {
@@ -230,7 +246,7 @@ int fipa_layer_set_timing(fipa_layer* layer, int enable) {
 
 int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n) {
     if (layer == nullptr || ms == nullptr) return 0;
-    const auto t = layer->impl.stage_times();
+    const auto t = layer->impl->stage_times();
     int k = 0;
     for (; k < n && k < int(t.size()); ++k) ms[k] = t[k];
     return k;
@@ -238,7 +254,7 @@ int fipa_layer_stage_times(const fipa_layer* layer, float* ms, int n) {
 
 size_t fipa_layer_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_) {
     if (layer == nullptr || B < 1 || L_ < 1) return 0;
-    return layer->impl.train_workspace_size(B, L_);
+    return layer->impl->train_workspace_size(B, L_);
 }
 
 int fipa_layer_forward_train(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
@@ -250,7 +266,7 @@ int fipa_layer_forward_train(fipa_layer* layer, int64_t B, int64_t L_, const flo
     });
 }
 
-uint64_t fipa_layer_num_weights(const fipa_layer* layer) { return layer ? layer->impl.num_weights() : 0; }
+uint64_t fipa_layer_num_weights(const fipa_layer* layer) { return layer ? layer->impl->num_weights() : 0; }
 
 int fipa_layer_backward(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
                         const float* z2, const float* rot, const float* trans, const uint8_t* mask,
@@ -275,7 +291,7 @@ int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L_, const double*
 int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, int64_t* offsets,
                                       int64_t* dims) {
     if (layer == nullptr || offsets == nullptr || B < 1 || L_ < 1) return 0;
-    const auto w = layer->impl.carve(nullptr, B, L_, true);
+    const auto w = layer->impl->carve(nullptr, B, L_, true);
     auto off = [](const void* p) { return static_cast<int64_t>(reinterpret_cast<uintptr_t>(p)); };
     offsets[0] = off(w.o_hat);
     offsets[1] = off(w.do_hat);
@@ -287,22 +303,22 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
     offsets[7] = off(w.dfeat);
     if (dims != nullptr) {
         dims[0] = fipa_b200::FlashIpaLayer::kAccLd;
-        dims[1] = layer->impl.nproj_ld();
-        dims[2] = layer->impl.dims().feat_ld;
+        dims[1] = layer->impl->nproj_ld();
+        dims[2] = layer->impl->dims().feat_ld;
     }
     return 8;
 }
 
 int fipa_layer_bwd_stage_times(const fipa_layer* layer, float* ms, int n) {
     if (layer == nullptr || ms == nullptr) return 0;
-    const auto t = layer->impl.bwd_stage_times();
+    const auto t = layer->impl->bwd_stage_times();
     int k = 0;
     for (; k < n && k < int(t.size()); ++k) ms[k] = t[k];
     return k;
 }
 
 int fipa_layer_backward_launches(const fipa_layer* layer) {
-    return layer ? layer->impl.launches_per_backward() : 0;
+    return layer ? layer->impl->launches_per_backward() : 0;
 }
 
 int fipa_comm_unique_id(uint8_t out[128]) {
@@ -325,7 +341,7 @@ void fipa_comm_destroy(fipa_comm* comm) { delete comm; }
 
 size_t fipa_layer_sharded_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_, int world) {
     if (layer == nullptr || B < 1 || L_ < 1 || world < 1) return 0;
-    return layer->impl.sharded_workspace_size(B, L_, world);
+    return layer->impl->sharded_workspace_size(B, L_, world);
 }
 
 int fipa_layer_forward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_, const float* s,
@@ -387,5 +403,56 @@ int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_, int world,
                          static_cast<cudaStream_t>(stream), false, &st);
     });
 }
+
+int fipa_trunk_create(const fipa_config* cfg, int n_layers, uint64_t seed, fipa_trunk** out) {
+    return guarded([&] {
+        if (out == nullptr) throw fipa_b200::ValueError("null output handle");
+        *out = nullptr;
+        *out = new fipa_trunk(to_cfg(cfg), n_layers, seed);
+    });
+}
+
+void fipa_trunk_destroy(fipa_trunk* trunk) { delete trunk; }
+
+int fipa_trunk_num_layers(const fipa_trunk* trunk) { return trunk ? trunk->impl.n_layers() : 0; }
+
+fipa_layer* fipa_trunk_layer(fipa_trunk* trunk, int l) {
+    if (trunk == nullptr || l < 0 || l >= trunk->impl.n_layers()) return nullptr;
+    return trunk->views[l].get();
+}
+
+int fipa_trunk_get_backbone(const fipa_trunk* trunk, int l, double* w, double* b) {
+    return guarded([&] {
+        if (trunk == nullptr || w == nullptr || b == nullptr) throw fipa_b200::ValueError("null argument");
+        if (l < 0 || l >= trunk->impl.n_layers()) throw fipa_b200::ValueError("layer index out of range");
+        const auto& bb = trunk->impl.backbone(l);
+        std::copy(bb.w.begin(), bb.w.end(), w);
+        std::copy(bb.b.begin(), bb.b.end(), b);
+    });
+}
+
+int fipa_trunk_set_backbone(fipa_trunk* trunk, int l, const double* w, const double* b) {
+    return guarded([&] {
+        if (trunk == nullptr || w == nullptr || b == nullptr) throw fipa_b200::ValueError("null argument");
+        trunk->impl.set_backbone(l, w, b);
+    });
+}
+
+size_t fipa_trunk_workspace_size(const fipa_trunk* trunk, int64_t B, int64_t L_) {
+    if (trunk == nullptr || B < 1 || L_ < 1) return 0;
+    return trunk->impl.workspace_size(B, L_);
+}
+
+int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L_, const float* s, const float* z1, const float* z2,
+                       const float* rot, const float* trans, const uint8_t* mask, float* s_out, float* rot_out,
+                       float* trans_out, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        if (trunk == nullptr) throw fipa_b200::ValueError("null fipa_trunk");
+        trunk->impl.forward(B, L_, s, z1, z2, rot, trans, mask, s_out, rot_out, trans_out, workspace,
+                            workspace_bytes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_trunk_forward_launches(const fipa_trunk* trunk) { return trunk ? trunk->impl.launches_per_forward() : 0; }
 
 }  // extern "C"

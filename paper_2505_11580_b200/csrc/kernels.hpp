@@ -166,6 +166,9 @@ void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStre
 // Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
 void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
                            cudaStream_t stream);
+// Trunk step: s += ipa_out; backbone update of the frames (rot [rows,9], trans [rows,3]) in place.
+void launch_trunk_update(float* s, const float* ipa_out, const float* w_bb, const float* b_bb, float* rot,
+                         float* trans, const uint8_t* mask, int64_t rows, int d_in, cudaStream_t stream);
 // Query-row sharding: per-sample {sum x, sum y, sum z, count} of valid local translations, and
 // recentring with (all-reduced) global sums.
 void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, int B, int L, cudaStream_t stream);

@@ -343,7 +343,57 @@ __global__ void recenter_with_sums_kernel(const float* __restrict__ trans, const
     for (int x = 0; x < 3; ++x) out[r + x] = trans[r + x] - sums[b * 4 + x] / n;
 }
 
+// Trunk step (BASELINE cfg3, oracle/fipa_oracle.py trunk_forward): s <- s + ipa_out, then the
+// backbone update u = s.W_bb + b_bb, dR = R(normalised (1, u0, u1, u2)) (proj/src/geometry.cpp:
+// 107-132 matrix), T <- compose(T, (dR, u[3:6])) = (R dR, R u[3:6] + t) (geometry.cpp:78-90).
+// One warp per residue; masked residues keep their frames (their IPA output is already zero).
+__global__ void trunk_update_kernel(float* __restrict__ s, const float* __restrict__ ipa_out,
+                                    const float* __restrict__ w_bb, const float* __restrict__ b_bb,
+                                    float* __restrict__ rot, float* __restrict__ trans,
+                                    const uint8_t* __restrict__ mask, int64_t rows, int d_in) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int k = lane; k < d_in; k += 32) {
+        const float v = s[row * d_in + k] + ipa_out[row * d_in + k];
+        s[row * d_in + k] = v;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) u[j] = fmaf(v, w_bb[k * 6 + j], u[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        for (int o = 16; o > 0; o >>= 1) u[j] += __shfl_xor_sync(0xffffffffu, u[j], o);
+        u[j] += b_bb[j];
+    }
+    if (lane != 0 || (mask != nullptr && mask[row] == 0)) return;
+    const float n = sqrtf(1.f + u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    const float qw = 1.f / n, qx = u[0] / n, qy = u[1] / n, qz = u[2] / n;
+    const float d[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                        2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                        2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+    float R[9], nr[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = rot[row * 9 + k];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) nr[3 * a + c] = R[3 * a] * d[c] + R[3 * a + 1] * d[3 + c] + R[3 * a + 2] * d[6 + c];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        trans[row * 3 + a] += R[3 * a] * u[3] + R[3 * a + 1] * u[4] + R[3 * a + 2] * u[5];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) rot[row * 9 + k] = nr[k];
+}
+
 }  // namespace
+
+void launch_trunk_update(float* s, const float* ipa_out, const float* w_bb, const float* b_bb, float* rot,
+                         float* trans, const uint8_t* mask, int64_t rows, int d_in, cudaStream_t stream) {
+    const int64_t threads = rows * 32;
+    trunk_update_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(s, ipa_out, w_bb, b_bb, rot,
+                                                                                          trans, mask, rows, d_in);
+}
 
 void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, int B, int L, cudaStream_t stream) {
     centroid_sums_kernel<<<B, 256, 0, stream>>>(trans, mask, sums, L);
