@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-L", type=int, default=0, help="residues per CPU sample (default L)")
     ap.add_argument("--pass", dest="pass_", choices=["fwd+bwd", "fwd"], default="fwd+bwd")
+    ap.add_argument("--trunk", type=int, default=0,
+                    help="BASELINE cfg3: time an N-layer trunk (residual + backbone update) forward; "
+                         "use with --B 4 --L 2048 --trunk 6")
     ap.add_argument("--shard", choices=["batch", "rows"], default="batch",
                     help="batch: independent samples per GPU (weak scaling); rows: one long sequence "
                          "query-row sharded over the GPUs with an NCCL all-gather of packed K/V (cfg4)")
@@ -486,6 +489,87 @@ def run_sharded(args, shape):
     return 0
 
 
+def run_trunk(args, shape):
+    """BASELINE cfg3: fipa.Trunk forward (n layers, each the 6-kernel layer + residual/backbone
+    update), B sequences of L residues, one GPU (or one independent replica per GPU)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2505_11580_b200 as fipa
+
+    B, L = args.B, args.L
+    trunk = fipa.Trunk(**shape, precision="bf16", seed=0, enforce_head_cap=False, n_layers=args.trunk)
+    host = synth_inputs(B, L, shape, seed=1234 + rank)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in host.items()}
+    out = {k: torch.empty_like(t[k]) for k in ("s", "rot", "trans")}
+    ws_bytes = trunk.workspace_size(B, L)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    p = {k: v.data_ptr() for k, v in t.items()}
+
+    def step():
+        trunk.forward_device(B, L, p["s"], p["z1"], p["z2"], p["rot"], p["trans"], p["mask"], out["s"].data_ptr(),
+                             out["rot"].data_ptr(), out["trans"].data_ptr(), ws.data_ptr(), ws_bytes,
+                             stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    value = B * L * world * args.steps / (ms_total / 1e3)
+    flops = attn_flops(shape, B, L) * args.trunk
+    tflops = flops * args.steps / (ms_total / 1e3) / 1e12
+    peak, peak_sus, peak_kind = load_peaks()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "residues/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference input distribution), random-init weights",
+            "config": {"workload": f"{args.trunk}-layer FlashIPA trunk forward with per-layer backbone frame update, "
+                                   f"B={B} L={L} per GPU (BASELINE cfg3)", "pass": "fwd", "model": "FlashIPA trunk",
+                       "global_batch": B * world, "seq_len": L, "layers": args.trunk, "shape": shape,
+                       "parallelism": f"dp{world} (independent samples)",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "attn_tflops_whole_trunk": tflops,
+            "roofline": {"bound": "tensor", "kernel": "whole trunk step (attention-dominated)", "achieved": tflops,
+                         "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak, "traffic": None,
+                         "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
+                         "algorithmic": f"layers*2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per step"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": trunk.forward_launches() * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def _free_port():
     import socket
 
@@ -501,6 +585,8 @@ def main():
         return run_reference(args, shape)
     if args.shard == "rows":
         return run_sharded(args, shape)
+    if args.trunk > 0:
+        return run_trunk(args, shape)
     return run_ours(args, shape)
 
 
