@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
 
 #include "kernels.hpp"
 
@@ -60,6 +61,33 @@ __device__ __forceinline__ float hi_part(float x) {
 template <typename T>
 __device__ __forceinline__ float lo_part(float x) {
     return sizeof(T) == 4 ? 0.f : x - __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ void ptx_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void ptx_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void ptx_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void ptx_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(parity)
+            : "memory");
+    }
 }
 
 template <typename OutT>
@@ -219,6 +247,198 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
             store_pair<OutT>(v + col, vv[0], vv[1]);
         }
         if (tid == 0) a.colbias[hrow] = valid ? -0.5f * g * hd[6] : -INFINITY;
+    }
+}
+
+// bf16 path of K2, restructured for HBM: one block per residue; the projection row and the two
+// pair-factor rows arrive by bulk copies (TMA engine, one instruction each), warp w assembles the
+// lifted rows of heads w, w+8, .. in shared memory (same column recipe as pack_kernel above), and
+// the block writes the 3*H rows with coalesced 16-byte stores.
+__device__ __forceinline__ void bulk_g2s_pack(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(src)),
+                 "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256, 4) pack_bf16_kernel(LayerDims d, PackArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const int H = d.heads, c = d.c, Nq = d.n_query, Nv = d.n_value, rdz = d.rank * d.d_z;
+    const int nw = blockDim.x >> 5;
+    float* s_proj = sm;                                  // n_proj (bulk)
+    float* s_z1 = s_proj + ((d.n_proj + 3) & ~3);        // rdz (bulk)
+    float* s_z2 = s_z1 + ((rdz + 3) & ~3);               // rdz (bulk)
+    float* s_rq = s_z2 + ((rdz + 3) & ~3);               // H*Nq*3
+    float* s_rk = s_rq + H * Nq * 3;                     // H*Nq*3
+    float* s_rv = s_rk + H * Nq * 3;                     // H*Nv*3
+    float* s_hd = s_rv + H * Nv * 3;                     // H*8: Qbar(3), W(3), |Tk|^2
+    __nv_bfloat16* s_out = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(s_hd + H * 8) + 15) & ~uintptr_t(15));  // H x (q | k | v) rows
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_out + H * (2 * d.dqk_pad + d.dv_pad));
+    const int64_t row = blockIdx.x;
+    const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool bulk = ((d.n_proj * 4) & 15) == 0 && ((rdz * 4) & 15) == 0;
+    if (threadIdx.x == 0) {
+        ptx_mbar_init(bar, 1);
+        if (bulk) {
+            ptx_expect_tx(bar, (d.n_proj + 2 * rdz) * 4);
+            bulk_g2s_pack(s_proj, a.proj + row * d.n_proj, d.n_proj * 4, bar);
+            bulk_g2s_pack(s_z1, a.z1 + row * rdz, rdz * 4, bar);
+            bulk_g2s_pack(s_z2, a.z2 + row * rdz, rdz * 4, bar);
+        } else {
+            ptx_arrive(bar);
+        }
+    }
+    if (!bulk) {
+        for (int e = threadIdx.x; e < d.n_proj; e += blockDim.x) s_proj[e] = a.proj[row * d.n_proj + e];
+        for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
+            s_z1[e] = a.z1[row * rdz + e];
+            s_z2[e] = a.z2[row * rdz + e];
+        }
+    }
+    float R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans + row * 3 + k);
+    const bool valid = a.mask == nullptr || a.mask[row] != 0;
+    __syncthreads();
+    ptx_wait(bar, 0);
+
+    const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
+    const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
+    for (int e = threadIdx.x; e < H * Nq * 2 + H * Nv; e += blockDim.x) {
+        const float* src;
+        float* dst;
+        if (e < H * Nq) {
+            src = s_proj + off_qp + e * 3;
+            dst = s_rq + e * 3;
+        } else if (e < 2 * H * Nq) {
+            src = s_proj + off_kp + (e - H * Nq) * 3;
+            dst = s_rk + (e - H * Nq) * 3;
+        } else {
+            src = s_proj + off_vp + (e - 2 * H * Nq) * 3;
+            dst = s_rv + (e - 2 * H * Nq) * 3;
+        }
+        const float x = src[0], y = src[1], z = src[2];
+        dst[0] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z));
+        dst[1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z));
+        dst[2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z));
+    }
+    __syncthreads();
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        float qb[3] = {0.f, 0.f, 0.f}, w[3] = {0.f, 0.f, 0.f}, kn = 0.f;
+        for (int p = 0; p < Nq; ++p) {
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                qb[x] += s_rq[(h * Nq + p) * 3 + x];
+                const float tk = s_rk[(h * Nq + p) * 3 + x] + t[x];
+                w[x] += tk;
+                kn = fmaf(tk, tk, kn);
+            }
+        }
+        float* hd = s_hd + h * 8;
+        hd[0] = qb[0];
+        hd[1] = qb[1];
+        hd[2] = qb[2];
+        hd[3] = w[0];
+        hd[4] = w[1];
+        hd[5] = w[2];
+        hd[6] = kn;
+    }
+    __syncthreads();
+
+    const int g0 = c + 3 * Nq, zq = g0 + 21, qk_used = d.dqk_used;
+    const int v_pair = c + rdz, v_used = d.dv_used;
+    const int rowlen = 2 * d.dqk_pad + d.dv_pad;
+    for (int h = warp; h < H; h += nw) {
+        const float g = a.head_g[h];
+        const float* hd = s_hd + h * 8;
+        const float cb = valid ? kL2E * (-0.5f * g * hd[6]) : kMaskedBias;
+        __nv_bfloat16* q = s_out + h * rowlen;
+        __nv_bfloat16* k = q + d.dqk_pad;
+        __nv_bfloat16* v = k + d.dqk_pad;
+        for (int col = 2 * lane; col < d.dqk_pad; col += 64) {
+            float qv[2], kv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int cc = col + u;
+                if (cc < c) {
+                    qv[u] = kL2E * s_proj[off_q + h * c + cc];
+                    kv[u] = a.k_scale * s_proj[off_k + h * c + cc];
+                } else if (cc < g0) {
+                    qv[u] = kL2E * s_rq[h * Nq * 3 + (cc - c)];
+                    kv[u] = g * s_rk[h * Nq * 3 + (cc - c)];
+                } else if (cc < zq) {
+                    const int e = cc - g0;
+                    const int x = e % 3;
+                    if (e < 9) {
+                        const float qq = kL2E * hd[x], tt = g * t[x];
+                        qv[u] = e < 6 ? hi_part<__nv_bfloat16>(qq) : lo_part<__nv_bfloat16>(qq);
+                        kv[u] = (e >= 3 && e < 6) ? lo_part<__nv_bfloat16>(tt) : hi_part<__nv_bfloat16>(tt);
+                    } else if (e < 18) {
+                        const float tq = kL2E * t[x], ww = g * hd[3 + x];
+                        qv[u] = (e >= 12 && e < 15) ? lo_part<__nv_bfloat16>(tq) : hi_part<__nv_bfloat16>(tq);
+                        kv[u] = e < 15 ? hi_part<__nv_bfloat16>(ww) : lo_part<__nv_bfloat16>(ww);
+                    } else if (e < 20) {
+                        qv[u] = 1.0f;
+                        kv[u] = e == 18 ? hi_part<__nv_bfloat16>(cb) : (valid ? lo_part<__nv_bfloat16>(cb) : 0.f);
+                    } else {
+                        qv[u] = 0.f;
+                        kv[u] = 1.0f;
+                    }
+                } else if (cc < qk_used) {
+                    const int e = cc - zq;
+                    qv[u] = kL2E * s_z1[e];
+                    kv[u] = a.wl_bias[h * d.d_z + (e % d.d_z)] * s_z2[e];
+                } else {
+                    qv[u] = 0.f;
+                    kv[u] = 0.f;
+                }
+            }
+            store_pair<__nv_bfloat16>(q + col, qv[0], qv[1]);
+            store_pair<__nv_bfloat16>(k + col, kv[0], kv[1]);
+        }
+        for (int col = 2 * lane; col < d.dv_pad; col += 64) {
+            float vv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int cc = col + u;
+                float x;
+                if (cc < c) {
+                    x = s_proj[off_v + h * c + cc];
+                } else if (cc < v_pair) {
+                    x = s_z2[cc - c];
+                } else if (cc < v_pair + 3) {
+                    x = hi_part<__nv_bfloat16>(t[cc - v_pair]);
+                } else if (cc < v_pair + 6) {
+                    x = lo_part<__nv_bfloat16>(t[cc - v_pair - 3]);
+                } else if (cc < v_used) {
+                    x = s_rv[h * Nv * 3 + (cc - v_pair - 6)];
+                } else {
+                    x = 0.f;
+                }
+                vv[u] = x;
+            }
+            store_pair<__nv_bfloat16>(v + col, vv[0], vv[1]);
+        }
+        if (lane == 0) a.colbias[(static_cast<int64_t>(b) * H + h) * a.L + i] = valid ? -0.5f * g * hd[6] : -INFINITY;
+    }
+    __syncthreads();
+    // 16-byte coalesced copy-out: per head q_hat, k_hat (dqk_pad) and v_hat (dv_pad) rows
+    const int nq16 = d.dqk_pad / 8, nv16 = d.dv_pad / 8, per_head = 2 * nq16 + nv16;
+    for (int e = threadIdx.x; e < H * per_head; e += blockDim.x) {
+        const int h = e / per_head, r = e - h * per_head;
+        const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
+        const uint4 val = reinterpret_cast<const uint4*>(s_out + h * rowlen)[r];
+        if (r < nq16) {
+            reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.qhat) + hrow * d.dqk_pad)[r] = val;
+        } else if (r < 2 * nq16) {
+            reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.khat) + hrow * d.dqk_pad)[r - nq16] = val;
+        } else {
+            reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.vhat) + hrow * d.dv_pad)[r - 2 * nq16] = val;
+        }
     }
 }
 
@@ -406,20 +626,22 @@ void launch_recenter_with_sums(const float* trans, const float* sums, float* out
 
 void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
-    const size_t smem =
-        sizeof(float) * (d.n_proj + 2 * rdz + d.heads * (d.n_query * 6 + d.n_value * 3) + 8 * d.heads);
     const dim3 grid(static_cast<unsigned>(int64_t(a.B) * a.L));
     if (a.out_f32) {
+        const size_t smem =
+            sizeof(float) * (d.n_proj + 2 * rdz + d.heads * (d.n_query * 6 + d.n_value * 3) + 8 * d.heads);
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(pack_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem));
+            cudaFuncSetAttribute(pack_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         pack_kernel<float><<<grid, 256, smem, stream>>>(d, a);
-    } else {
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(pack_kernel<__nv_bfloat16>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        pack_kernel<__nv_bfloat16><<<grid, 256, smem, stream>>>(d, a);
+        return;
     }
+    if (d.dqk_pad % 8 || d.dv_pad % 8) throw std::invalid_argument("pack: padded widths must be multiples of 8");
+    const size_t smem = sizeof(float) * (((d.n_proj + 3) & ~3) + 2 * ((rdz + 3) & ~3) +
+                                         d.heads * (d.n_query * 6 + d.n_value * 3) + 8 * d.heads) +
+                        16 + 2 * size_t(d.heads) * (2 * d.dqk_pad + d.dv_pad) + 16;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(pack_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    pack_bf16_kernel<<<grid, 256, smem, stream>>>(d, a);
 }
 
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream) {
