@@ -36,6 +36,8 @@ __device__ __forceinline__ uint32_t ptx_pack(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ float bfr(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     const int vpair = c + rdz, vpts = vpair + 6, vend = vpts + 3 * Nv;
     float* dopt_s = s_dopt + warp * 3 * Nv;
     float* pair_s = s_pair + warp * rdz;
+    const bool vec = (c % 4) == 0 && (rdz % 4) == 0 && (dz % 4) == 0 && (d.seg % 4) == 0;
     float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
     for (int h = warp; h < H; h += nw) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
@@ -127,7 +130,40 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
         __syncwarp();
         __nv_bfloat16* out = s_out + h * d.dv_pad;
         float Dp = 0.f;
-        for (int c4 = lane; 4 * c4 < d.dv_pad; c4 += 32) {
+        if (vec) {
+            // segment-wise, 4 columns per lane step: [dv | z1 (.) d(pair) | sum dg x2 | dg_p | 0]
+            for (int j = lane; 4 * j < c; j += 32) {
+                const float4 dv = *reinterpret_cast<const float4*>(df + dz + 4 * j);
+                const float4 ov = *reinterpret_cast<const float4*>(o + 4 * j);
+                const float v0 = bfr(dv.x), v1 = bfr(dv.y), v2 = bfr(dv.z), v3 = bfr(dv.w);
+                Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
+                *reinterpret_cast<uint2*>(out + 4 * j) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+            }
+            for (int j = lane; 4 * j < rdz; j += 32) {
+                const int e = 4 * j;
+                const float4 zz = *reinterpret_cast<const float4*>(s_z1 + e);
+                const float4 dpc = *reinterpret_cast<const float4*>(df + e % dz);
+                const float4 ov = *reinterpret_cast<const float4*>(o + c + e);
+                const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
+                Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
+                float4 ps = *reinterpret_cast<float4*>(pair_s + e);  // warp-private slice
+                ps.x += ov.x * dpc.x;
+                ps.y += ov.y * dpc.y;
+                ps.z += ov.z * dpc.z;
+                ps.w += ov.w * dpc.w;
+                *reinterpret_cast<float4*>(pair_s + e) = ps;
+                *reinterpret_cast<uint2*>(out + c + 4 * j) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+            }
+            for (int col = vpair + lane; col < d.dv_pad; col += 32) {
+                float v = 0.f;
+                if (col < vpts) v = ds[(col - vpair) % 3];
+                else if (col < vend) v = dopt_s[col - vpts];
+                v = bfr(v);
+                out[col] = __float2bfloat16_rn(v);
+                if (col < d.dv_used) Dp += v * o[col];
+            }
+        } else {
+            for (int c4 = lane; 4 * c4 < d.dv_pad; c4 += 32) {
             const float4 ov = *reinterpret_cast<const float4*>(o + 4 * c4);
             const float oo[4] = {ov.x, ov.y, ov.z, ov.w};
             float v[4];
@@ -155,6 +191,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
             w.x = ptx_pack(v[0], v[1]);
             w.y = ptx_pack(v[2], v[3]);
             *reinterpret_cast<uint2*>(out + 4 * c4) = w;
+        }
         }
         Dp = warp_sum(Dp);
         if (lane == 0) a.Dvec[hrow] = Dp;
@@ -213,7 +250,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     float* s_wlb = s_dg + H;                                  // H x dz  w_l w_bias
     __nv_bfloat16* s_dp = reinterpret_cast<__nv_bfloat16*>((reinterpret_cast<uintptr_t>(s_wlb + H * dz) + 15) & ~uintptr_t(15));
     uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_dp + a.nproj_ld) + 7) & ~uintptr_t(7));
-    const int g0 = c + 3 * Nq, zq = g0 + 21, vpair = c + rdz;
+    const int g0 = c + 3 * Nq, zq = d.zq, vpair = c + rdz;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
     const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
     const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);

@@ -37,7 +37,8 @@ void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 struct LayerDims {
     int d_in, d_z, heads, c, n_query, n_value, rank;
     int n_proj;      // H*(3c + 6Nq + 3Nv): fused projection width
-    int dqk_used;    // c + 3Nq + 21 + r*d_z      (lifted query/key width, see pack.cu)
+    int zq;          // start of the pair-factor columns: round_up(c + 3Nq + 21, 8)
+    int dqk_used;    // zq + r*d_z                (lifted query/key width, see pack.cu)
     int dqk_mma;     // dqk_used rounded up to 16  (MMA K extent of Q.K^T)
     int dqk_pad;     // dqk_used rounded up to 64  (row stride of q_hat / k_hat: 128-byte blocks)
     int dv_used;     // c + r*d_z + 6 + 3Nv       (v | z2 | t_hi | t_lo | R v_p)

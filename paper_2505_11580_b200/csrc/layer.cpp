@@ -115,7 +115,9 @@ LayerDims Config::dims() const {
     d.n_value = int(n_value);
     d.rank = int(rank);
     d.n_proj = int(heads * (3 * c + 6 * n_query + 3 * n_value));
-    d.dqk_used = int(c + 3 * n_query + 21 + rank * d_z);
+    // 21 translation/bias columns, padded so the pair-factor block starts 16-byte aligned
+    d.zq = int(round_up(c + 3 * n_query + 21, 8));
+    d.dqk_used = d.zq + int(rank * d_z);
     d.dqk_mma = int(round_up(d.dqk_used, 16));
     d.dqk_pad = int(round_up(d.dqk_used, 64));
     d.dv_used = int(c + rank * d_z + 3 * n_value + 6);

@@ -15,9 +15,9 @@
 // bf16 logits accurate for protein-scale coordinates (tens of Angstrom), where a plain bf16
 // T_i q_p column loses ~1 logit unit.  Per head (L2E = log2 e, queries pre-scaled so that
 // S = q_hat . k_hat is in log2 units):
-//   q_hat = L2E*[ q | R_i q_p | Qbar hi,hi,lo | t_i hi,lo,hi ] | 1, 1, 0 | L2E*z1_i | 0
-//   k_hat = [ (w_l/sqrt c) k | g R_j k_p | g t_j hi,lo,hi | g W_j hi,hi,lo ] | cb hi, lo, 1 |
-//           w_l w_bias[h] (.) z2_j | 0
+//   q_hat = L2E*[ q | R_i q_p | Qbar hi,hi,lo | t_i hi,lo,hi ] | 1, 1, 0 | 0.. | L2E*z1_i | 0
+//   k_hat = [ (w_l/sqrt c) k | g R_j k_p | g t_j hi,lo,hi | g W_j hi,hi,lo ] | cb hi, lo, 1 | 0.. |
+//           w_l w_bias[h] (.) z2_j | 0          (the pair block starts at zq = round_up(g0 + 21, 8))
 //   cb_j  = L2E * (-g/2 sum_p |T_j k_p|^2)   (-1e30 for masked keys, lo = 0)
 // The reference's |T_i q_p|^2 column (paired with -g/2) is constant along a query row and
 // cancels in the softmax, so it is dropped; its (ones, -g/2 |k|^2) pair becomes the folded
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
     OutT* kh = static_cast<OutT*>(a.khat);
     OutT* vh = static_cast<OutT*>(a.vhat);
     const int g0 = c + 3 * Nq;        // start of the 21 translation/bias columns
-    const int zq = g0 + 21;           // start of the pair-factor columns
+    const int zq = d.zq;              // start of the pair-factor columns (8-aligned)
     const int qk_used = d.dqk_used;
     const int v_pair = c + rdz, v_used = d.dv_used;
 
@@ -207,9 +207,12 @@ __global__ void __launch_bounds__(256) pack_kernel(LayerDims d, PackArgs a) {
                     } else if (e < 20) {       // folded column bias: [1 1] . [cb_hi cb_lo]
                         qv[u] = 1.0f;
                         kv[u] = e == 18 ? hi_part<OutT>(cb) : (valid ? lo_part<OutT>(cb) : 0.f);
-                    } else {                   // [0] . [1]: logit-neutral; in the backward
+                    } else if (e == 20) {      // [0] . [1]: logit-neutral; in the backward
                         qv[u] = 0.f;           // dS.K_hat picks up sum_j dS_ij here
                         kv[u] = 1.0f;
+                    } else {                   // alignment padding up to zq
+                        qv[u] = 0.f;
+                        kv[u] = 0.f;
                     }
                 } else if (cc < qk_used) {
                     const int e = cc - zq;
@@ -259,6 +262,11 @@ __device__ __forceinline__ void bulk_g2s_pack(void* dst, const void* src, uint32
                  ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(reinterpret_cast<uint64_t>(src)),
                  "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
                  : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
 }
 
 __global__ void __launch_bounds__(256, 4) pack_bf16_kernel(LayerDims d, PackArgs a) {
@@ -349,9 +357,10 @@ __global__ void __launch_bounds__(256, 4) pack_bf16_kernel(LayerDims d, PackArgs
     }
     __syncthreads();
 
-    const int g0 = c + 3 * Nq, zq = g0 + 21, qk_used = d.dqk_used;
+    const int g0 = c + 3 * Nq, zq = d.zq, qk_used = d.dqk_used;
     const int v_pair = c + rdz, v_used = d.dv_used;
     const int rowlen = 2 * d.dqk_pad + d.dv_pad;
+    const bool vec = (c % 4) == 0 && (rdz % 4) == 0 && (d.d_z % 4) == 0;
     for (int h = warp; h < H; h += nw) {
         const float g = a.head_g[h];
         const float* hd = s_hd + h * 8;
@@ -359,69 +368,96 @@ __global__ void __launch_bounds__(256, 4) pack_bf16_kernel(LayerDims d, PackArgs
         __nv_bfloat16* q = s_out + h * rowlen;
         __nv_bfloat16* k = q + d.dqk_pad;
         __nv_bfloat16* v = k + d.dqk_pad;
-        for (int col = 2 * lane; col < d.dqk_pad; col += 64) {
-            float qv[2], kv[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int cc = col + u;
-                if (cc < c) {
-                    qv[u] = kL2E * s_proj[off_q + h * c + cc];
-                    kv[u] = a.k_scale * s_proj[off_k + h * c + cc];
-                } else if (cc < g0) {
-                    qv[u] = kL2E * s_rq[h * Nq * 3 + (cc - c)];
-                    kv[u] = g * s_rk[h * Nq * 3 + (cc - c)];
-                } else if (cc < zq) {
-                    const int e = cc - g0;
-                    const int x = e % 3;
-                    if (e < 9) {
-                        const float qq = kL2E * hd[x], tt = g * t[x];
-                        qv[u] = e < 6 ? hi_part<__nv_bfloat16>(qq) : lo_part<__nv_bfloat16>(qq);
-                        kv[u] = (e >= 3 && e < 6) ? lo_part<__nv_bfloat16>(tt) : hi_part<__nv_bfloat16>(tt);
-                    } else if (e < 18) {
-                        const float tq = kL2E * t[x], ww = g * hd[3 + x];
-                        qv[u] = (e >= 12 && e < 15) ? lo_part<__nv_bfloat16>(tq) : hi_part<__nv_bfloat16>(tq);
-                        kv[u] = e < 15 ? hi_part<__nv_bfloat16>(ww) : lo_part<__nv_bfloat16>(ww);
-                    } else if (e < 20) {
-                        qv[u] = 1.0f;
-                        kv[u] = e == 18 ? hi_part<__nv_bfloat16>(cb) : (valid ? lo_part<__nv_bfloat16>(cb) : 0.f);
-                    } else {
-                        qv[u] = 0.f;
-                        kv[u] = 1.0f;
-                    }
-                } else if (cc < qk_used) {
-                    const int e = cc - zq;
-                    qv[u] = kL2E * s_z1[e];
-                    kv[u] = a.wl_bias[h * d.d_z + (e % d.d_z)] * s_z2[e];
+        // column recipe of one q_hat / k_hat element (pack.cu header); used for the 21 geometric
+        // columns and, for shapes without 4-aligned blocks, for every column
+        auto qk_col = [&](int cc, float& qv, float& kv) {
+            if (cc < c) {
+                qv = kL2E * s_proj[off_q + h * c + cc];
+                kv = a.k_scale * s_proj[off_k + h * c + cc];
+            } else if (cc < g0) {
+                qv = kL2E * s_rq[h * Nq * 3 + (cc - c)];
+                kv = g * s_rk[h * Nq * 3 + (cc - c)];
+            } else if (cc < zq) {
+                const int e = cc - g0;
+                const int x = e % 3;
+                if (e < 9) {
+                    const float qq = kL2E * hd[x], tt = g * t[x];
+                    qv = e < 6 ? hi_part<__nv_bfloat16>(qq) : lo_part<__nv_bfloat16>(qq);
+                    kv = (e >= 3 && e < 6) ? lo_part<__nv_bfloat16>(tt) : hi_part<__nv_bfloat16>(tt);
+                } else if (e < 18) {
+                    const float tq = kL2E * t[x], ww = g * hd[3 + x];
+                    qv = (e >= 12 && e < 15) ? lo_part<__nv_bfloat16>(tq) : hi_part<__nv_bfloat16>(tq);
+                    kv = e < 15 ? hi_part<__nv_bfloat16>(ww) : lo_part<__nv_bfloat16>(ww);
+                } else if (e < 20) {
+                    qv = 1.0f;
+                    kv = e == 18 ? hi_part<__nv_bfloat16>(cb) : (valid ? lo_part<__nv_bfloat16>(cb) : 0.f);
                 } else {
-                    qv[u] = 0.f;
-                    kv[u] = 0.f;
+                    qv = 0.f;
+                    kv = e == 20 ? 1.0f : 0.f;
                 }
+            } else if (cc < qk_used) {
+                const int e = cc - zq;
+                qv = kL2E * s_z1[e];
+                kv = a.wl_bias[h * d.d_z + (e % d.d_z)] * s_z2[e];
+            } else {
+                qv = 0.f;
+                kv = 0.f;
             }
-            store_pair<__nv_bfloat16>(q + col, qv[0], qv[1]);
-            store_pair<__nv_bfloat16>(k + col, kv[0], kv[1]);
-        }
-        for (int col = 2 * lane; col < d.dv_pad; col += 64) {
-            float vv[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int cc = col + u;
-                float x;
-                if (cc < c) {
-                    x = s_proj[off_v + h * c + cc];
-                } else if (cc < v_pair) {
-                    x = s_z2[cc - c];
-                } else if (cc < v_pair + 3) {
-                    x = hi_part<__nv_bfloat16>(t[cc - v_pair]);
-                } else if (cc < v_pair + 6) {
-                    x = lo_part<__nv_bfloat16>(t[cc - v_pair - 3]);
-                } else if (cc < v_used) {
-                    x = s_rv[h * Nv * 3 + (cc - v_pair - 6)];
-                } else {
-                    x = 0.f;
-                }
-                vv[u] = x;
+        };
+        auto v_col = [&](int cc) {
+            if (cc < c) return s_proj[off_v + h * c + cc];
+            if (cc < v_pair) return s_z2[cc - c];
+            if (cc < v_pair + 3) return hi_part<__nv_bfloat16>(t[cc - v_pair]);
+            if (cc < v_pair + 6) return lo_part<__nv_bfloat16>(t[cc - v_pair - 3]);
+            if (cc < v_used) return s_rv[h * Nv * 3 + (cc - v_pair - 6)];
+            return 0.f;
+        };
+        if (vec) {
+            // segment-wise: 4 columns per lane step with 8-byte shared stores, no per-element branching
+            const float* pq = s_proj + off_q + h * c;
+            const float* pk = s_proj + off_k + h * c;
+            const float* pv = s_proj + off_v + h * c;
+            for (int j = lane; 4 * j < c; j += 32) {
+                const float4 x = *reinterpret_cast<const float4*>(pq + 4 * j);
+                const float4 y = *reinterpret_cast<const float4*>(pk + 4 * j);
+                const float4 z = *reinterpret_cast<const float4*>(pv + 4 * j);
+                const float ks = a.k_scale;
+                *reinterpret_cast<uint2*>(q + 4 * j) = make_uint2(pack2(kL2E * x.x, kL2E * x.y), pack2(kL2E * x.z, kL2E * x.w));
+                *reinterpret_cast<uint2*>(k + 4 * j) = make_uint2(pack2(ks * y.x, ks * y.y), pack2(ks * y.z, ks * y.w));
+                *reinterpret_cast<uint2*>(v + 4 * j) = make_uint2(pack2(z.x, z.y), pack2(z.z, z.w));
             }
-            store_pair<__nv_bfloat16>(v + col, vv[0], vv[1]);
+            for (int cc = c + lane; cc < zq; cc += 32) {  // rotated points + geometric columns
+                float qv, kv;
+                qk_col(cc, qv, kv);
+                q[cc] = __float2bfloat16_rn(qv);
+                k[cc] = __float2bfloat16_rn(kv);
+            }
+            const float* wb = a.wl_bias + h * d.d_z;
+            for (int j = lane; 4 * j < rdz; j += 32) {  // pair factors (zq % 8 == 0, c % 4 == 0)
+                const float4 z1v = *reinterpret_cast<const float4*>(s_z1 + 4 * j);
+                const float4 z2v = *reinterpret_cast<const float4*>(s_z2 + 4 * j);
+                const float4 w4 = __ldg(reinterpret_cast<const float4*>(wb + (4 * j) % d.d_z));
+                *reinterpret_cast<uint2*>(q + zq + 4 * j) =
+                    make_uint2(pack2(kL2E * z1v.x, kL2E * z1v.y), pack2(kL2E * z1v.z, kL2E * z1v.w));
+                *reinterpret_cast<uint2*>(k + zq + 4 * j) =
+                    make_uint2(pack2(w4.x * z2v.x, w4.y * z2v.y), pack2(w4.z * z2v.z, w4.w * z2v.w));
+                *reinterpret_cast<uint2*>(v + c + 4 * j) = make_uint2(pack2(z2v.x, z2v.y), pack2(z2v.z, z2v.w));
+            }
+            for (int cc = qk_used + lane; cc < d.dqk_pad; cc += 32) {
+                q[cc] = __float2bfloat16_rn(0.f);
+                k[cc] = __float2bfloat16_rn(0.f);
+            }
+            for (int cc = v_pair + lane; cc < d.dv_pad; cc += 32) v[cc] = __float2bfloat16_rn(v_col(cc));
+        } else {
+            for (int col = 2 * lane; col < d.dqk_pad; col += 64) {
+                float q0, k0, q1, k1;
+                qk_col(col, q0, k0);
+                qk_col(col + 1, q1, k1);
+                store_pair<__nv_bfloat16>(q + col, q0, q1);
+                store_pair<__nv_bfloat16>(k + col, k0, k1);
+            }
+            for (int col = 2 * lane; col < d.dv_pad; col += 64)
+                store_pair<__nv_bfloat16>(v + col, v_col(col), v_col(col + 1));
         }
         if (lane == 0) a.colbias[(static_cast<int64_t>(b) * H + h) * a.L + i] = valid ? -0.5f * g * hd[6] : -INFINITY;
     }

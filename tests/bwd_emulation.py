@@ -53,14 +53,16 @@ def pack(cfg: fo.IpaConfig, w, s, z1, z2, rot, trans_c, mask):
     Qb, T, gt, gW = L2E * qbar, L2E * t, g * t, g * W
     ones = np.ones((H, L, 1))
     zeros = np.zeros((H, L, 1))
+    g0 = c + 3 * Nq
+    pad = np.zeros((H, L, (g0 + 21 + 7) // 8 * 8 - (g0 + 21)))  # zq alignment padding
     z1f = np.broadcast_to(z1.reshape(1, L, rdz), (H, L, rdz))
     z2f = np.broadcast_to(z2.reshape(1, L, rdz), (H, L, rdz))
     wlb = np.repeat((w["w_l"] * w["w_bias"])[:, None, :], cfg.rank, 1).reshape(H, 1, rdz)
     q_hat = np.concatenate([L2E * q, L2E * rq.reshape(H, L, -1), _hi(Qb), _hi(Qb), _lo(Qb),
-                            _hi(T), _lo(T), _hi(T), ones, ones, zeros, L2E * z1f], -1)
+                            _hi(T), _lo(T), _hi(T), ones, ones, zeros, pad, L2E * z1f], -1)
     k_hat = np.concatenate([w["w_l"] / math.sqrt(c) * k, g * rk.reshape(H, L, -1), _hi(gt), _lo(gt),
                             _hi(gt), _hi(gW), _hi(gW), _lo(gW), cb_hi[..., None], cb_lo[..., None],
-                            ones, wlb * z2f], -1)
+                            ones, pad, wlb * z2f], -1)
     v_hat = np.concatenate([v, z2f, _hi(t), _lo(t), rv.reshape(H, L, -1)], -1)
     return dict(q_hat=q_hat, k_hat=k_hat, v_hat=v_hat, proj=(q, k, v, qp, kp, vp), g=g[:, 0, 0])
 
@@ -130,7 +132,8 @@ def unpack(cfg, w, pk, rot, trans_c, z1, z2, dq_acc, dk_acc, dv_acc):
     L = rot.shape[0]
     q, k, v, qp, kp, vp = pk["proj"]
     g = pk["g"][:, None, None]
-    g0, zq = c + 3 * Nq, c + 3 * Nq + 21
+    g0 = c + 3 * Nq
+    zq = (g0 + 21 + 7) // 8 * 8
     # query side: dA = g sum_j dS (B_j - A_i) with S1 = sum_j dS_ij from the (0, 1) column
     dq = dq_acc[..., :c]
     S1 = dq_acc[..., g0 + 20]

@@ -16,7 +16,7 @@ int main(int argc, char** argv) {
     const int which = argc > 3 ? atoi(argv[3]) : 1;
     LayerDims d{};
     d.d_in = 256; d.d_z = 128; d.heads = 8; d.c = 128; d.n_query = 8; d.n_value = 12; d.rank = 2;
-    d.dqk_used = 128 + 24 + 21 + 256; d.dqk_mma = 432; d.dqk_pad = 448;
+    d.zq = 176; d.dqk_used = 176 + 256; d.dqk_mma = 432; d.dqk_pad = 448;
     d.dv_used = 128 + 256 + 36 + 6; d.dv_mma = 432; d.dv_pad = 448;
     const size_t BH = size_t(B) * d.heads;
     std::vector<__nv_bfloat16> hq(BH * L * 448);

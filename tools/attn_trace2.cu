@@ -15,7 +15,7 @@ int main(int argc, char** argv) {
     const int L = argc > 2 ? atoi(argv[2]) : 1024;
     LayerDims d{};
     d.d_in = 256; d.d_z = 128; d.heads = 8; d.c = 128; d.n_query = 8; d.n_value = 12; d.rank = 2;
-    d.dqk_used = 128 + 24 + 20 + 256; d.dqk_mma = 432; d.dqk_pad = 448;
+    d.zq = 176; d.dqk_used = 176 + 256; d.dqk_mma = 432; d.dqk_pad = 448;
     d.dv_used = 128 + 256 + 36 + 6; d.dv_mma = 432; d.dv_pad = 448; d.dv_tc = 416; d.dv_simt = 10;
     d.seg = 304; d.feat = 8 * 304; d.feat_ld = d.feat; d.din_ld = 256;
     const size_t BH = size_t(B) * d.heads, BL = size_t(B) * L;

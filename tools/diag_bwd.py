@@ -62,7 +62,7 @@ dq_round = np.einsum("hij,hjd->hid", dS_round, k)
 c, Nq = 128, 8
 g0 = c + 3 * Nq
 groups = {"scalar": slice(0, c), "Rk": slice(c, g0), "t hi/lo/hi": slice(g0, g0 + 9), "W": slice(g0 + 9, g0 + 18),
-          "cb": slice(g0 + 18, g0 + 20), "S1": slice(g0 + 20, g0 + 21), "pair": slice(g0 + 21, g0 + 21 + 256)}
+          "cb": slice(g0 + 18, g0 + 20), "S1": slice(g0 + 20, g0 + 21), "pair": slice(176, 176 + 256)}
 for nm, sl in groups.items():
     e_exact = np.abs(dq_r[..., sl] - accs[0][..., sl]).max()
     e_round = np.abs(dq_round[..., sl] - accs[0][..., sl]).max()
