@@ -217,8 +217,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     if (threadIdx.x < 12) {
         float acc = 0.f;
         for (int w = 0; w < nw; ++w) acc += s_geo[w * 12 + threadIdx.x];
-        if (threadIdx.x < 9) a.drot_epi[row * 9 + threadIdx.x] = acc;
-        else a.dt_epi[row * 3 + threadIdx.x - 9] = acc;
+        a.geo_epi[row * 12 + threadIdx.x] = acc;
     }
 }
 
@@ -240,7 +239,8 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     const int npts = d.n_proj - off_qp;                       // point columns of a projection row
     const int npts_pad = (npts + 3) & ~3;
     const int rdz_pad = (rdz + 3) & ~3;
-    const int stage_floats = 3 * H * stage_w + npts_pad + rdz_pad;  // one residue: dq|dk|dv rows, points, z2
+    // one residue: dq|dk|dv rows, points, z2, dz1_epi, geo_epi (12)
+    const int stage_floats = 3 * H * stage_w + npts_pad + 2 * rdz_pad + 12;
     float* s_stage = sm;                                      // 2 x stage_floats
     float* s_pq = s_stage + 2 * stage_floats;                 // H x rdz  query-side pair grads
     float* s_pk = s_pq + H * rdz;                             // H x rdz  key+value-side pair grads
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         (void)i;
         // accumulators are residue-major [B, L, H, acc_ld]: one copy per tensor moves all heads
         const uint32_t rbytes = H * stage_w * 4;
-        ptx::mbar_expect_tx(bar, 3 * rbytes + (pts_bulk ? (npts + rdz) * 4 : 0));
+        ptx::mbar_expect_tx(bar, 3 * rbytes + (pts_bulk ? (npts + 2 * rdz + 12) * 4 : 0));
         const int64_t arow = row * H * a.acc_ld;
         bulk_g2s(st, a.dq_acc + arow, rbytes, bar);
         bulk_g2s(st + H * stage_w, a.dk_acc + arow, rbytes, bar);
@@ -277,6 +277,8 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         if (pts_bulk) {
             bulk_g2s(st + 3 * H * stage_w, a.proj + row * d.n_proj + off_qp, npts * 4, bar);
             bulk_g2s(st + 3 * H * stage_w + npts_pad, a.z2 + row * rdz, rdz * 4, bar);
+            bulk_g2s(st + 3 * H * stage_w + npts_pad + rdz_pad, a.dz1_epi + row * rdz, rdz * 4, bar);
+            bulk_g2s(st + 3 * H * stage_w + npts_pad + 2 * rdz_pad, a.geo_epi + row * 12, 48, bar);
         }
     };
 
@@ -297,7 +299,11 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         float* st = s_stage + (rr & 1) * stage_floats;
         if (!pts_bulk) {
             for (int e = threadIdx.x; e < npts; e += blockDim.x) st[3 * H * stage_w + e] = a.proj[row * d.n_proj + off_qp + e];
-            for (int e = threadIdx.x; e < rdz; e += blockDim.x) st[3 * H * stage_w + npts_pad + e] = a.z2[row * rdz + e];
+            for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
+                st[3 * H * stage_w + npts_pad + e] = a.z2[row * rdz + e];
+                st[3 * H * stage_w + npts_pad + rdz_pad + e] = a.dz1_epi[row * rdz + e];
+            }
+            if (threadIdx.x < 12) st[3 * H * stage_w + npts_pad + 2 * rdz_pad + threadIdx.x] = a.geo_epi[row * 12 + threadIdx.x];
         }
         float R[9], t[3];
 #pragma unroll
@@ -305,6 +311,8 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
 #pragma unroll
         for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
         const float* z2 = st + 3 * H * stage_w + npts_pad;
+        const float* z1e = z2 + rdz_pad;           // dz1 of the output epilogue
+        const float* epi = z1e + rdz_pad;          // dR (9) | dt (3) of the output epilogue
         const float* pr = st + 3 * H * stage_w - off_qp;  // pr[off_qp + ...] = point columns
         if (!pts_bulk) __syncthreads();
         ptx::mbar_wait(&bars[rr & 1], (rr >> 1) & 1);
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
             for (int e = threadIdx.x; e < a.nproj_ld / 8; e += blockDim.x) dst[e] = src[e];
         }
         for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
-            float s1 = a.dz1_epi[row * rdz + e], s2 = 0.f;
+            float s1 = z1e[e], s2 = 0.f;
             for (int h = 0; h < H; ++h) {
                 s1 += s_pq[h * rdz + e];
                 s2 += s_pk[h * rdz + e];
@@ -445,9 +453,9 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
             float acc = 0.f;
             for (int h = 0; h < H; ++h) acc += s_geo[h * 12 + threadIdx.x];
             if (threadIdx.x < 9) {
-                if (a.drot != nullptr) a.drot[row * 9 + threadIdx.x] = acc + a.drot_epi[row * 9 + threadIdx.x];
+                if (a.drot != nullptr) a.drot[row * 9 + threadIdx.x] = acc + epi[threadIdx.x];
             } else {
-                a.dt_c[row * 3 + threadIdx.x - 9] = acc + a.dt_epi[row * 3 + threadIdx.x - 9];
+                a.dt_c[row * 3 + threadIdx.x - 9] = acc + epi[threadIdx.x];
             }
         }
         __syncthreads();
@@ -544,7 +552,7 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
         throw std::invalid_argument("bwd_unpack: accumulator stride");
     if (a.nproj_ld % 8 != 0) throw std::invalid_argument("bwd_unpack: dproj stride must be a multiple of 8");
     const int npts = d.n_proj - 3 * d.heads * d.c;
-    const int stage_floats = 3 * d.heads * stage_w + ((npts + 3) & ~3) + ((rdz + 3) & ~3);
+    const int stage_floats = 3 * d.heads * stage_w + ((npts + 3) & ~3) + 2 * ((rdz + 3) & ~3) + 12;
     const size_t smem = sizeof(float) * (2 * stage_floats + 2 * d.heads * rdz + d.heads * 12 + 2 * d.heads * d.d_z +
                                          d.heads) + 16 + 2 * size_t(a.nproj_ld) + 8 + 16;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -121,8 +121,7 @@ struct BwdPrepArgs {
     __nv_bfloat16* dohat;         // [B*H, L, dv_pad]
     float* Dvec;                  // [B*H, L]
     float* dz1_epi;               // [BL, r*d_z]
-    float* drot_epi;              // [BL, 9]
-    float* dt_epi;                // [BL, 3]
+    float* geo_epi;               // [BL, 12]: dR (9) | dt (3) of the epilogue
     int B, L;
 };
 void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream);
@@ -140,8 +139,7 @@ struct BwdUnpackArgs {
     const float* wl_bias;   // [H, d_z]
     float k_scale;
     const float* dz1_epi;
-    const float* drot_epi;
-    const float* dt_epi;
+    const float* geo_epi;   // [BL, 12]
     __nv_bfloat16* dproj;   // [BL, nproj_ld]
     int nproj_ld;
     float* dz1;             // [BL, r*d_z]

@@ -479,8 +479,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dv_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
         w.dproj = reinterpret_cast<__nv_bfloat16*>(take(BL * nproj_ld() * 2));
         w.dz1_epi = reinterpret_cast<float*>(take(BL * rdz * 4));
-        w.drot_epi = reinterpret_cast<float*>(take(BL * 9 * 4));
-        w.dt_epi = reinterpret_cast<float*>(take(BL * 3 * 4));
+        w.geo_epi = reinterpret_cast<float*>(take(BL * 12 * 4));
         w.dt_c = reinterpret_cast<float*>(take(BL * 3 * 4));
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
@@ -839,8 +838,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.dohat = ws.do_hat;
         a.Dvec = ws.Dvec;
         a.dz1_epi = ws.dz1_epi;
-        a.drot_epi = ws.drot_epi;
-        a.dt_epi = ws.dt_epi;
+        a.geo_epi = ws.geo_epi;
         a.B = int(B);
         a.L = int(L);
         launch_bwd_prep(d, a, stream);
@@ -879,8 +877,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.wl_bias = d_wl_bias_;
         a.k_scale = k_scale_;
         a.dz1_epi = ws.dz1_epi;
-        a.drot_epi = ws.drot_epi;
-        a.dt_epi = ws.dt_epi;
+        a.geo_epi = ws.geo_epi;
         a.dproj = ws.dproj;
         a.nproj_ld = nproj_ld();
         a.dz1 = dz1;

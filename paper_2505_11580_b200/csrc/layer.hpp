@@ -177,8 +177,7 @@ public:
         float* dv_acc = nullptr;
         __nv_bfloat16* dproj = nullptr;    // [BL, nproj_ld]
         float* dz1_epi = nullptr;          // [BL, r d_z]
-        float* drot_epi = nullptr;         // [BL, 9]
-        float* dt_epi = nullptr;           // [BL, 3]
+        float* geo_epi = nullptr;          // [BL, 12] dR | dt of the output epilogue
         float* dt_c = nullptr;             // [BL, 3]
         float* red = nullptr;              // [H + H d_z]  d(g) | d(w_l w_bias)
         float* dwproj = nullptr;           // [d_in, n_proj]
