@@ -31,6 +31,7 @@ struct GemmCfg {
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static_assert(2 * BN <= 512, "double-buffered accumulator must fit TMEM");
 };
 
 struct EpiParams {
@@ -44,6 +45,9 @@ struct EpiParams {
     const uint8_t* row_mask;
 };
 
+// Persistent: each CTA walks work units u = blockIdx.x, += gridDim.x over (split, m-tile, n-tile).
+// The smem ring runs continuously across units; the accumulator is double-buffered in TMEM
+// (2 x BN columns) so the epilogue warps drain unit u while the tensor pipe computes unit u+1.
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -55,16 +59,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* tiles = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
     uint64_t* empty = full + Cfg::kStages;
-    uint64_t* done = empty + Cfg::kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* acc_full = empty + Cfg::kStages;   // [2]
+    uint64_t* acc_empty = acc_full + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = ptx::warp_id();
     const int lane = ptx::lane_id();
-    const int m0 = blockIdx.y * BM;
-    const int n0 = blockIdx.x * BN;
+    const int n_tiles_n = (p.N + BN - 1) / BN;
+    const int n_tiles_m = (p.M + BM - 1) / BM;
+    const int units = n_tiles_n * n_tiles_m * p.split_k;
     const int nk_all = (p.K + BK - 1) / BK;
-    const int kb0 = static_cast<int>((int64_t(nk_all) * blockIdx.z) / p.split_k);
-    const int nk = static_cast<int>((int64_t(nk_all) * (blockIdx.z + 1)) / p.split_k) - kb0;
+    auto unit_coords = [&](int u, int& m0, int& n0, int& kb0, int& nk) {
+        const int z = u / (n_tiles_n * n_tiles_m);
+        const int r = u - z * (n_tiles_n * n_tiles_m);
+        m0 = (r / n_tiles_n) * BM;
+        n0 = (r % n_tiles_n) * BN;
+        kb0 = static_cast<int>((int64_t(nk_all) * z) / p.split_k);
+        nk = static_cast<int>((int64_t(nk_all) * (z + 1)) / p.split_k) - kb0;
+    };
+    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&mapA);
@@ -73,10 +86,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(done, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&acc_full[b], 1);
+            ptx::mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+        }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, kTmemCols);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -84,127 +100,150 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % Cfg::kStages;
-                if (kb >= Cfg::kStages) ptx::mbar_wait(&empty[s], ((kb / Cfg::kStages) - 1) & 1);
-                uint8_t* sa = tiles + s * Cfg::kStageBytes;
-                uint8_t* sb = sa + Cfg::kABytes;
-                ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
-                if (A_MN) {
-                    for (int mb = 0; mb < BM / 64; ++mb)
-                        ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, (kb0 + kb) * BK);
-                } else {
-                    ptx::tma_load_2d(sa, &mapA, &full[s], (kb0 + kb) * BK, m0);
-                }
-                if (B_MN) {
-                    for (int nb = 0; nb < BN / 64; ++nb)
-                        ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, (kb0 + kb) * BK);
-                } else {
-                    ptx::tma_load_2d(sb, &mapB, &full[s], (kb0 + kb) * BK, n0);
+            int it = 0;  // global k-block counter (ring position)
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int m0, n0, kb0, nk;
+                unit_coords(u, m0, n0, kb0, nk);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % Cfg::kStages;
+                    if (it >= Cfg::kStages) ptx::mbar_wait(&empty[s], ((it / Cfg::kStages) - 1) & 1);
+                    uint8_t* sa = tiles + s * Cfg::kStageBytes;
+                    uint8_t* sb = sa + Cfg::kABytes;
+                    ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
+                    const int kc = (kb0 + kb) * BK;
+                    if (A_MN) {
+                        for (int mb = 0; mb < BM / 64; ++mb)
+                            ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kc);
+                    } else {
+                        ptx::tma_load_2d(sa, &mapA, &full[s], kc, m0);
+                    }
+                    if (B_MN) {
+                        for (int nb = 0; nb < BN / 64; ++nb)
+                            ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kc);
+                    } else {
+                        ptx::tma_load_2d(sb, &mapB, &full[s], kc, n0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % Cfg::kStages;
-                ptx::mbar_wait(&full[s], (kb / Cfg::kStages) & 1);
+            int it = 0, lu = 0;  // k-block counter, local unit counter
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
+                int m0, n0, kb0, nk;
+                unit_coords(u, m0, n0, kb0, nk);
+                const int buf = lu & 1;
+                if (lu >= 2) ptx::mbar_wait(&acc_empty[buf], ((lu >> 1) - 1) & 1);
                 ptx::tc_fence_after();
-                const uint32_t sa = ptx::smem_u32(tiles + s * Cfg::kStageBytes);
-                const uint32_t sb = sa + Cfg::kABytes;
+                const uint32_t acc = tmem + buf * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % Cfg::kStages;
+                    ptx::mbar_wait(&full[s], (it / Cfg::kStages) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(tiles + s * Cfg::kStageBytes);
+                    const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk) {
-                    const uint64_t da = A_MN ? ptx::sw128_desc(sa + kk * 2048, 64 * 128, 1024)
-                                             : ptx::sw128_desc(sa + kk * 32, 16, 1024);
-                    const uint64_t db = B_MN ? ptx::sw128_desc(sb + kk * 2048, 64 * 128, 1024)
-                                             : ptx::sw128_desc(sb + kk * 32, 16, 1024);
-                    ptx::mma_ss(tmem, da, db, idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t da = A_MN ? ptx::sw128_desc(sa + kk * 2048, 64 * 128, 1024)
+                                                 : ptx::sw128_desc(sa + kk * 32, 16, 1024);
+                        const uint64_t db = B_MN ? ptx::sw128_desc(sb + kk * 2048, 64 * 128, 1024)
+                                                 : ptx::sw128_desc(sb + kk * 32, 16, 1024);
+                        ptx::mma_ss(acc, da, db, idesc, (kb | kk) != 0);
+                    }
+                    ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&empty[s]);
+                ptx::mma_commit(&acc_full[buf]);
             }
-            ptx::mma_commit(done);
         }
     } else {
         // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
         const int quad = warp & 3;
-        const int row = m0 + quad * 32 + lane;
-        if (nk > 0) ptx::mbar_wait(done, 0);
-        ptx::tc_fence_after();
-        const bool row_ok = row < p.M;
-        const bool zero_row = row_ok && p.row_mask != nullptr && p.row_mask[row] == 0;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t r[32];
-            ptx::tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c0, r);
-            ptx::tmem_wait_ld();
-            if (!row_ok) continue;
-            const int col0 = n0 + c0;
-            if (col0 >= p.N) continue;
-            float v[32];
-            if (p.split_k > 1) {
-                if (nk <= 0) continue;
-                float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
-                if (col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        int lu = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
+            int m0, n0, kb0, nk;
+            unit_coords(u, m0, n0, kb0, nk);
+            const int buf = lu & 1;
+            ptx::mbar_wait(&acc_full[buf], (lu >> 1) & 1);
+            ptx::tc_fence_after();
+            const int row = m0 + quad * 32 + lane;
+            const bool row_ok = row < p.M;
+            const bool zero_row = row_ok && p.row_mask != nullptr && p.row_mask[row] == 0;
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld32(tmem + buf * BN + (uint32_t(quad * 32) << 16) + c0, r);
+                ptx::tmem_wait_ld();
+                if (!row_ok || nk <= 0) continue;
+                const int col0 = n0 + c0;
+                if (col0 >= p.N) continue;
+                if (p.split_k > 1) {
+                    float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
+                    if (col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        atomicAdd(reinterpret_cast<float4*>(out) + q,
-                                  make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
-                                              __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha));
-                } else {
-                    for (int i = 0; i < 32 && col0 + i < p.N; ++i) atomicAdd(out + i, __uint_as_float(r[i]) * p.alpha);
-                }
-                continue;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                float x = __uint_as_float(r[i]) * p.alpha;
-                const int col = col0 + i;
-                if (p.bias != nullptr && col < p.N) x += p.bias[col];
-                v[i] = zero_row ? 0.0f : x;
-            }
-            const size_t esz = p.out_bf16 ? 2 : 4;
-            const bool full_chunk = col0 + 32 <= p.N &&
-                                    ((reinterpret_cast<uintptr_t>(p.C) + (size_t(row) * p.ldc + col0) * esz) & 15) == 0;
-            if (p.out_bf16) {
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + int64_t(row) * p.ldc + col0;
-                if (full_chunk) {
-                    uint4* o4 = reinterpret_cast<uint4*>(out);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 w;
-                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-                        o4[q] = w;
+                        for (int q = 0; q < 8; ++q)
+                            atomicAdd(reinterpret_cast<float4*>(out) + q,
+                                      make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
+                                                  __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha));
+                    } else {
+                        for (int i = 0; i < 32 && col0 + i < p.N; ++i) atomicAdd(out + i, __uint_as_float(r[i]) * p.alpha);
                     }
-                } else {
-                    for (int i = 0; i < 32 && col0 + i < p.N; ++i) out[i] = __float2bfloat16_rn(v[i]);
+                    continue;
                 }
-            } else {
-                float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
-                if (full_chunk) {
-                    float4* o4 = reinterpret_cast<float4*>(out);
+                float v[32];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                        if (p.accumulate) {
-                            const float4 o = o4[q];
-                            w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+                for (int i = 0; i < 32; ++i) {
+                    float x = __uint_as_float(r[i]) * p.alpha;
+                    const int col = col0 + i;
+                    if (p.bias != nullptr && col < p.N) x += p.bias[col];
+                    v[i] = zero_row ? 0.0f : x;
+                }
+                const size_t esz = p.out_bf16 ? 2 : 4;
+                const bool full_chunk = col0 + 32 <= p.N &&
+                                        ((reinterpret_cast<uintptr_t>(p.C) + (size_t(row) * p.ldc + col0) * esz) & 15) == 0;
+                if (p.out_bf16) {
+                    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + int64_t(row) * p.ldc + col0;
+                    if (full_chunk) {
+                        uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint4 w;
+                            w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                            w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                            w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                            w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                            o4[q] = w;
                         }
-                        o4[q] = w;
+                    } else {
+                        for (int i = 0; i < 32 && col0 + i < p.N; ++i) out[i] = __float2bfloat16_rn(v[i]);
                     }
                 } else {
-                    for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-                        out[i] = p.accumulate ? out[i] + v[i] : v[i];
+                    float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
+                    if (full_chunk) {
+                        float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                            if (p.accumulate) {
+                                const float4 o = o4[q];
+                                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+                            }
+                            o4[q] = w;
+                        }
+                    } else {
+                        for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+                            out[i] = p.accumulate ? out[i] + v[i] : v[i];
+                    }
                 }
             }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&acc_empty[buf]);
         }
     }
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+    if (warp == 1) ptx::tmem_dealloc(tmem, kTmemCols);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -223,7 +262,15 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         configured = true;
     }
-    dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, std::max(1, a.split_k));
+    const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    dim3 grid(static_cast<unsigned>(std::min(units, sms)));
     kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, p);
 }
 
