@@ -356,14 +356,15 @@ public:
         py::array_t<double> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
                             gt = like(translations);
         const uint64_t nw = fipa_layer_num_weights(layer_);
-        std::vector<double> gw(nw);
+        py::array_t<double> gw(static_cast<py::ssize_t>(nw));  // weight grads land here directly
+        double* gwp = gw.mutable_data();
         int rc;
         {
             py::gil_scoped_release nogil;
             rc = fipa_layer_grad_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
                                       translations.data(), mp, dout.data(), out.mutable_data(), gs.mutable_data(),
                                       gz1.mutable_data(), gz2.mutable_data(), gr.mutable_data(), gt.mutable_data(),
-                                      gw.data());
+                                      gwp);
         }
         check(rc);
         py::dict g;
@@ -373,12 +374,13 @@ public:
         g["rotations"] = gr;
         g["translations"] = gt;
         const auto sh = shapes();
-        size_t o = 0;
+        py::ssize_t o = 0;
         for (int i = 0; i < 10; ++i) {
-            py::array_t<double> a(std::vector<py::ssize_t>(sh[i].begin(), sh[i].end()));
-            std::copy(gw.begin() + o, gw.begin() + o + a.size(), a.mutable_data());
-            o += a.size();
-            g[kNames[i]] = a;
+            py::ssize_t n = 1;
+            for (auto v : sh[i]) n *= static_cast<py::ssize_t>(v);
+            py::object view = gw[py::slice(o, o + n, 1)];
+            g[kNames[i]] = view.attr("reshape")(py::cast(std::vector<py::ssize_t>(sh[i].begin(), sh[i].end())));
+            o += n;
         }
         return py::make_tuple(out, g);
     }

@@ -13,6 +13,7 @@
 #include <mutex>
 #include <numbers>
 #include <sstream>
+#include <thread>
 
 namespace fipa_b200 {
 
@@ -37,6 +38,32 @@ std::string cat(P&&... parts) {
     } while (0)
 
 std::size_t round_up(std::size_t x, std::size_t m) { return (x + m - 1) / m * m; }
+
+// Host-side float64 <-> float32 conversion of the host-buffer entry points, split over the host
+// cores (the reference API is float64; the conversion is the dominant cost of the host path).
+template <class F>
+void parallel_chunks(std::size_t n, F&& f) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned T = std::min<unsigned>(16, hw);
+    if (n < (std::size_t(1) << 16) || T == 1) {
+        f(std::size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const std::size_t per = (n + T - 1) / T;
+    for (unsigned t = 0; t < T; ++t) {
+        const std::size_t a = t * per, b = std::min(n, a + per);
+        if (a < b) th.emplace_back([&f, a, b] { f(a, b); });
+    }
+    for (auto& x : th) x.join();
+}
+
+template <class D, class S>
+void convert(D* dst, const S* src, std::size_t n) {
+    parallel_chunks(n, [dst, src](std::size_t a, std::size_t b) {
+        for (std::size_t i = a; i < b; ++i) dst[i] = static_cast<D>(src[i]);
+    });
+}
 
 // CTA-pair attention unless FIPA_ATTN_IMPL=1sm forces the single-CTA kernel.
 bool use_2sm_attention(const LayerDims& d) {
@@ -356,6 +383,8 @@ FlashIpaLayer::~FlashIpaLayer() {
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : evb_)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : d2h_ev_)
         if (e) cudaEventDestroy(e);
 }
 
@@ -713,19 +742,17 @@ void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s
         d_stage_bytes_ = io_bytes + ws_bytes;
     }
     float* h = static_cast<float*>(h_stage_);
-    auto cvt = [](float* dst, const double* src, std::size_t n) {
-        for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<float>(src[i]);
-    };
-    cvt(h, s, n_s);
-    cvt(h + n_s, z1, n_z);
-    cvt(h + n_s + n_z, z2, n_z);
-    cvt(h + n_s + 2 * n_z, rot, n_r);
-    cvt(h + n_s + 2 * n_z + n_r, trans, n_t);
+    float* dbase = static_cast<float*>(d_stage_);
+    std::size_t o = 0;
+    for (auto [src, n] : {std::pair{s, n_s}, std::pair{z1, n_z}, std::pair{z2, n_z}, std::pair{rot, n_r},
+                          std::pair{trans, n_t}}) {
+        convert(h + o, src, n);  // the copy of this tensor overlaps the conversion of the next
+        cuda_check(cudaMemcpyAsync(dbase + o, h + o, n * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
+        o += n;
+    }
     std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
     if (mask) std::memcpy(hmask, mask, BL);
-    float* dbase = static_cast<float*>(d_stage_);
     std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
-    cuda_check(cudaMemcpyAsync(dbase, h, n_in * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
     if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
     void* ws = static_cast<char*>(d_stage_) + io_bytes;
     forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
@@ -734,7 +761,7 @@ void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s
     cuda_check(cudaMemcpyAsync(h + n_in, dbase + n_in, n_out * 4, cudaMemcpyDeviceToHost, own_stream_),
                "D2H");
     cuda_check(cudaStreamSynchronize(own_stream_), "forward");
-    for (std::size_t i = 0; i < n_out; ++i) out[i] = static_cast<double>(h[n_in + i]);
+    convert(out, h + n_in, n_out);
 }
 
 
@@ -960,20 +987,17 @@ void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, c
     const std::size_t ws_bytes = train_workspace_size(B, L);
     ensure_staging(io_bytes, io_bytes + ws_bytes);
     float* h = static_cast<float*>(h_stage_);
-    auto cvt = [](float* dst, const double* src, std::size_t n) {
-        for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<float>(src[i]);
-    };
+    float* dbase = static_cast<float*>(d_stage_);
     std::size_t o = 0;
     for (auto [src, n] : {std::pair{s, n_s}, std::pair{z1, n_z}, std::pair{z2, n_z}, std::pair{rot, n_r},
                           std::pair{trans, n_t}, std::pair{dout, n_s}}) {
-        cvt(h + o, src, n);
+        convert(h + o, src, n);  // the copy of this tensor overlaps the conversion of the next
+        cuda_check(cudaMemcpyAsync(dbase + o, h + o, n * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
         o += n;
     }
     std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
     if (mask) std::memcpy(hmask, mask, BL);
-    float* dbase = static_cast<float*>(d_stage_);
     std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
-    cuda_check(cudaMemcpyAsync(dbase, h, n_in * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
     if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
     void* ws = static_cast<char*>(d_stage_) + io_bytes;
     const float* di = dbase;
@@ -989,20 +1013,26 @@ void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, c
     forward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, dout_d, ws, ws_bytes, own_stream_, true);
     backward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, d_dout, g_s, g_z1, g_z2, g_rot, g_t,
              g_w, ws, ws_bytes, own_stream_);
-    cuda_check(cudaMemcpyAsync(h + n_in, dout_d, n_out * 4, cudaMemcpyDeviceToHost, own_stream_), "D2H");
-    cuda_check(cudaStreamSynchronize(own_stream_), "grad");
+    // Per-tensor device->host copies, each followed by an event, so the float64 conversion of one
+    // output overlaps the transfer of the next.
     const float* r = h + n_in;
-    auto back = [](double* dst, const float* src, std::size_t n) {
-        if (dst)
-            for (std::size_t i = 0; i < n; ++i) dst[i] = static_cast<double>(src[i]);
-    };
-    back(out, r, n_s);
-    back(ds, r + n_s, n_s);
-    back(dz1, r + 2 * n_s, n_z);
-    back(dz2, r + 2 * n_s + n_z, n_z);
-    back(drot, r + 2 * n_s + 2 * n_z, n_r);
-    back(dtrans, r + 2 * n_s + 2 * n_z + n_r, n_t);
-    back(dweights, r + 2 * n_s + 2 * n_z + n_r + n_t, num_weights());
+    const std::size_t offs[8] = {0, n_s, 2 * n_s, 2 * n_s + n_z, 2 * n_s + 2 * n_z, 2 * n_s + 2 * n_z + n_r,
+                                 2 * n_s + 2 * n_z + n_r + n_t, n_out};
+    double* dsts[7] = {out, ds, dz1, dz2, drot, dtrans, dweights};
+    if (!d2h_ev_[0])
+        for (auto& e : d2h_ev_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (int k = 0; k < 7; ++k) {
+        const std::size_t n = offs[k + 1] - offs[k];
+        if (dsts[k] != nullptr && n > 0)
+            cuda_check(cudaMemcpyAsync(h + n_in + offs[k], dout_d + offs[k], n * 4, cudaMemcpyDeviceToHost, own_stream_),
+                       "D2H");
+        cuda_check(cudaEventRecord(d2h_ev_[k], own_stream_), "event");
+    }
+    for (int k = 0; k < 7; ++k) {
+        cuda_check(cudaEventSynchronize(d2h_ev_[k]), "grad");
+        if (dsts[k] != nullptr) convert(dsts[k], r + offs[k], offs[k + 1] - offs[k]);
+    }
+}
 }
 
 }  // namespace fipa_b200

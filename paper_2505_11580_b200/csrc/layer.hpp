@@ -239,6 +239,7 @@ public:
     std::vector<float> bwd_stage_times() const;
 private:
     cudaEvent_t evb_[kBwdStages + 1] = {};
+    cudaEvent_t d2h_ev_[7] = {};
     bool bwd_timed_once_ = false;
     bool timed_once_ = false;
 };
