@@ -1033,6 +1033,5 @@ void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, c
         if (dsts[k] != nullptr) convert(dsts[k], r + offs[k], offs[k + 1] - offs[k]);
     }
 }
-}
 
 }  // namespace fipa_b200
