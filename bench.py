@@ -396,9 +396,17 @@ def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak,
     bwd_ms = stage_ms["attn_bwd_dkdv"] + stage_ms["attn_bwd_dq"]
     if bwd_ms < stage_ms["attn_fwd+epilogue"]:
         return fwd
+    bwd_traffic = None
+    prof = os.path.join(ROOT, "profiles", "attn_bwd_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                bwd_traffic = json.load(f).get("dram_bytes_per_backward")
+        except Exception:
+            bwd_traffic = None
     return {"bound": "tensor", "kernel": "attn_bwd_kernel<true> + attn_bwd_kernel<false> (dK/dV + dQ)",
             "achieved": achieved_bwd, "peak": peak, "unit": "TFLOP/s", "frac": achieved_bwd / peak,
-            "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})", "traffic": None,
+            "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})", "traffic": bwd_traffic,
             "algorithmic": f"2*B*H*L^2*(3*D_qk+2*D_v) = {bflops:.4g} FLOP per backward",
             "forward_kernel": fwd}
 
