@@ -204,6 +204,25 @@ int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L, const float* s, 
                        float* trans_out, void* workspace, size_t workspace_bytes, void* stream);
 int fipa_trunk_forward_launches(const fipa_trunk* trunk);
 
+/* ----------------------------------------------------------- pair-factor producer (§8 f2)
+ * knn_distogram (proj/src/pair_features.cpp:10-64): translations [B,L,3] -> features
+ * [B,L,k,n_bins+pe_dim]: the k nearest other residues (float64 distances, ties to the lower
+ * index), one-hot distance bins clipped into the end bins, and the sinusoidal encoding of the
+ * offset j-i (positional_encoding, pair_features.cpp:66-81).  Reference defaults: k 20, n_bins 22,
+ * d_min 2, d_max 22, pe_dim 16.  Errors as the reference (ValueError on invalid specs).
+ * build_factors (pair_features.cpp:83-97): z1 = features.w1, z2 = features.w2 ([rows,f] x [f,r*d_z]);
+ * precision FIPA_PREC_BF16 uses the tcgen05 GEMM, otherwise fp32. */
+int fipa_knn_distogram(int64_t B, int64_t L, const float* trans, uint64_t k, uint64_t n_bins, double d_min,
+                       double d_max, uint64_t pe_dim, float* out, void* stream);
+int fipa_knn_distogram_host(int64_t B, int64_t L, const double* trans, uint64_t k, uint64_t n_bins, double d_min,
+                            double d_max, uint64_t pe_dim, double* out);
+size_t fipa_build_factors_workspace_size(int64_t rows, uint64_t f, uint64_t n);
+int fipa_build_factors(int64_t rows, uint64_t f, const float* features, uint64_t r, uint64_t d_z, const float* w1,
+                       const float* w2, float* z1, float* z2, int precision, void* workspace, size_t workspace_bytes,
+                       void* stream);
+int fipa_build_factors_host(int64_t rows, uint64_t f, const double* features, uint64_t r, uint64_t d_z,
+                            const double* w1, const double* w2, double* z1, double* z2, int precision);
+
 /* Number of kernels fipa_layer_forward launches per call for this configuration. */
 int fipa_layer_forward_launches(const fipa_layer* layer);
 

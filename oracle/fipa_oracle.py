@@ -566,3 +566,45 @@ def trunk_forward(s, z1, z2, rot, trans, mask, cfg: IpaConfig, layers, backbones
         s = s + flash_ipa_forward(s, z1, z2, rot, trans, mask, cfg, w)
         rot, trans = backbone_update(s, rot, trans, mask, bb)
     return s, rot, trans
+
+
+
+# --------------------------------------------------------------- pair-factor producer
+def positional_encoding(offsets, dim):
+    """proj/src/pair_features.cpp:66-81: [sin(x f_p), cos(x f_p)] with f_p = 10000^(-2p/dim)."""
+    if dim < 2 or dim % 2:
+        raise ValueError("positional encoding width must be even")
+    x = np.asarray(offsets, np.float64)[:, None]
+    p = np.arange(dim // 2)
+    freq = np.array([math.pow(10000.0, -(2.0 * q) / dim) for q in p])
+    out = np.empty((len(offsets), dim))
+    out[:, 0::2] = np.sin(x * freq)
+    out[:, 1::2] = np.cos(x * freq)
+    return out
+
+
+def knn_distogram(trans, k=20, n_bins=22, d_min=2.0, d_max=22.0, pe_dim=16):
+    """proj/src/pair_features.cpp:10-64: k nearest other residues (Euclidean, ties to the lower
+    index), one-hot distance bins (clipped into the end bins) + encoding of the offset j - i."""
+    trans = np.asarray(trans, np.float64)
+    L = trans.shape[0]
+    if L < 2 or not 1 <= k <= L - 1 or n_bins < 2 or not d_min < d_max or pe_dim % 2:
+        raise ValueError("invalid distogram spec")
+    width = (d_max - d_min) / n_bins
+    out = np.zeros((L, k, n_bins + pe_dim))
+    for i in range(L):
+        d = trans - trans[i]
+        dist = np.sqrt(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] + d[:, 2] * d[:, 2])
+        idx = np.array([j for j in range(L) if j != i])
+        order = idx[np.lexsort((idx, dist[idx]))][:k]  # distance, then lower index
+        rel = np.maximum((dist[order] - d_min) / width, 0.0)
+        bins = np.minimum(rel.astype(np.int64), n_bins - 1)
+        out[i, np.arange(k), bins] = 1.0
+        out[i, :, n_bins:] = positional_encoding(order - i, pe_dim)
+    return out
+
+
+def build_factors(features, r, d_z, w1, w2):
+    """proj/src/pair_features.cpp:83-97."""
+    L = features.shape[0]
+    return (features @ w1).reshape(L, r, d_z), (features @ w2).reshape(L, r, d_z)

@@ -154,3 +154,22 @@ def gaussian(seed, n, stddev=1.0):
     out = np.zeros(n)
     _check(lib().ref_gaussian(ctypes.c_uint64(seed), ctypes.c_uint64(n), ctypes.c_double(stddev), _dp(out)))
     return out
+
+
+def knn_distogram(trans, k=20, n_bins=22, d_min=2.0, d_max=22.0, pe_dim=16):
+    trans = _c(trans)
+    L = trans.shape[0]
+    out = np.zeros((L, k, n_bins + pe_dim))
+    _check(lib().ref_knn_distogram(ctypes.c_uint64(L), _dp(trans), ctypes.c_uint64(k), ctypes.c_uint64(n_bins),
+                                   ctypes.c_double(d_min), ctypes.c_double(d_max), ctypes.c_uint64(pe_dim), _dp(out)))
+    return out
+
+
+def build_factors(features, r, d_z, w1, w2):
+    features, w1, w2 = map(_c, (features, w1, w2))
+    L, f = features.shape
+    z1 = np.zeros((L, r, d_z))
+    z2 = np.zeros((L, r, d_z))
+    _check(lib().ref_build_factors(ctypes.c_uint64(L), ctypes.c_uint64(f), _dp(features), ctypes.c_uint64(r),
+                                   ctypes.c_uint64(d_z), _dp(w1), _dp(w2), _dp(z1), _dp(z2)))
+    return z1, z2

@@ -14,6 +14,8 @@
 //   save_weights / load_weights proj/src/model_io.cpp:121-196
 //   random_rototranslation      proj/src/geometry.cpp:107-132
 //   gaussian / Rng              proj/src/tensor.cpp:286-290, proj/src/rng.cpp:11-41
+//   knn_distogram / positional_encoding / build_factors
+//                               proj/src/pair_features.cpp:10-97
 //
 // Status codes mirror the product C-ABI: 0 ok, 1 ValueError, 2 NumericError,
 // 3 IoError, 9 other.
@@ -275,6 +277,32 @@ int ref_gaussian(std::uint64_t seed, std::uint64_t n, double stddev, double* out
     return guarded([&] {
         Rng rng(seed);
         to_ptr(gaussian(rng, {n}, stddev), out);
+    });
+}
+
+// translations [L,3] f64 -> features [L, k, n_bins + pe_dim]
+int ref_knn_distogram(std::uint64_t L, const double* trans, std::uint64_t k, std::uint64_t n_bins, double d_min,
+                      double d_max, std::uint64_t pe_dim, double* out) {
+    return guarded([&] {
+        DistogramSpec spec;
+        spec.k = k;
+        spec.n_bins = n_bins;
+        spec.d_min = d_min;
+        spec.d_max = d_max;
+        spec.pe_dim = pe_dim;
+        to_ptr(knn_distogram(from_ptr(trans, {L, 3}, Precision::f64), spec), out);
+    });
+}
+
+// features [L, f] x w1, w2 [f, r*d_z] -> z1, z2 [L, r, d_z]
+int ref_build_factors(std::uint64_t L, std::uint64_t f, const double* feat, std::uint64_t r, std::uint64_t d_z,
+                      const double* w1, const double* w2, double* z1, double* z2) {
+    return guarded([&] {
+        const FactorizedPair fp = build_factors(from_ptr(feat, {L, f}, Precision::f64), r, d_z,
+                                                from_ptr(w1, {f, r * d_z}, Precision::f64),
+                                                from_ptr(w2, {f, r * d_z}, Precision::f64));
+        to_ptr(fp.z1, z1);
+        to_ptr(fp.z2, z2);
     });
 }
 

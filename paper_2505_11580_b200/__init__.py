@@ -20,7 +20,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 try:
-    from ._fipa_b200 import Comm, Model, Trunk, comm_unique_id  # noqa: F401  (native extension, in-tree build)
+    from ._fipa_b200 import (Comm, Model, Trunk, build_factors, comm_unique_id,  # noqa: F401  (native, in-tree)
+                             knn_distogram)
 except ImportError as exc:  # fail loudly: the product has no Python fallback
     raise ImportError(
         "paper_2505_11580_b200 native extension is not built; run "
@@ -29,4 +30,4 @@ except ImportError as exc:  # fail loudly: the product has no Python fallback
 
 LIB_PATH = os.path.join(_HERE, "libfipa_b200.so")
 
-__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "LIB_PATH"]
+__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "knn_distogram", "build_factors", "LIB_PATH"]

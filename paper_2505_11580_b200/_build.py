@@ -28,9 +28,9 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_tc.cu", "pack.cu", "attn_fwd_tc.cu", "attn_fwd_2sm.cu", "simt_f32.cu", "attn_bwd.cu",
-              "bwd.cu"]
-CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp", "trunk.cpp"]
-HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp", "trunk.hpp"]
+              "bwd.cu", "pair_features.cu"]
+CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp", "trunk.cpp", "producer.cpp"]
+HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp", "trunk.hpp", "producer.hpp"]
 
 LIB_NAME = "libfipa_b200.so"
 EXT_NAME = "_fipa_b200" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so")

@@ -476,6 +476,46 @@ private:
     std::string precision_name_;
 };
 
+// knn_distogram(translations, k=20, n_bins=22, d_min=2.0, d_max=22.0, pe_dim=16) -> [.., L, k, n_bins+pe_dim]
+py::array_t<double> knn_distogram(const DArr& trans, uint64_t k, uint64_t n_bins, double d_min, double d_max,
+                                  uint64_t pe_dim) {
+    if ((trans.ndim() != 2 && trans.ndim() != 3) || trans.shape(trans.ndim() - 1) != 3)
+        throw FipaValueError("knn_distogram expects [L, 3] translations");
+    const bool batched = trans.ndim() == 3;
+    const int64_t B = batched ? trans.shape(0) : 1, L = trans.shape(batched ? 1 : 0);
+    std::vector<py::ssize_t> shape = {(py::ssize_t)L, (py::ssize_t)k, (py::ssize_t)(n_bins + pe_dim)};
+    if (batched) shape.insert(shape.begin(), (py::ssize_t)B);
+    py::array_t<double> out(shape);
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = fipa_knn_distogram_host(B, L, trans.data(), k, n_bins, d_min, d_max, pe_dim, out.mutable_data());
+    }
+    check(rc);
+    return out;
+}
+
+// build_factors(features [rows, f], r, d_z, w1 [f, r*d_z], w2, precision="bf16") -> (z1, z2) [rows, r, d_z]
+py::tuple build_factors(const DArr& features, uint64_t r, uint64_t d_z, const DArr& w1, const DArr& w2,
+                        const std::string& precision) {
+    if (features.ndim() != 2) throw FipaValueError("build_factors expects [L, f] features");
+    const int64_t rows = features.shape(0);
+    const uint64_t f = features.shape(1);
+    for (const DArr* w : {&w1, &w2})
+        if (w->ndim() != 2 || uint64_t(w->shape(0)) != f || uint64_t(w->shape(1)) != r * d_z)
+            throw FipaValueError("factor projection weights must be [f, r*d_z]");
+    const int prec = parse_precision(precision);
+    py::array_t<double> z1({(py::ssize_t)rows, (py::ssize_t)r, (py::ssize_t)d_z}), z2({(py::ssize_t)rows, (py::ssize_t)r, (py::ssize_t)d_z});
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = fipa_build_factors_host(rows, f, features.data(), r, d_z, w1.data(), w2.data(), z1.mutable_data(),
+                                     z2.mutable_data(), prec);
+    }
+    check(rc);
+    return py::make_tuple(z1, z2);
+}
+
 PYBIND11_MODULE(_fipa_b200, m) {
     m.doc() = "B200-native FlashIPA layer (tcgen05 sm_100a kernels behind the reference fipa.Model API)";
 
@@ -484,6 +524,11 @@ PYBIND11_MODULE(_fipa_b200, m) {
     py::register_exception<FipaIoError>(m, "FipaIoError", PyExc_IOError);
     py::register_exception<FipaCudaError>(m, "FipaCudaError", PyExc_RuntimeError);
     py::register_exception<FipaCommError>(m, "FipaCommError", PyExc_RuntimeError);
+    m.def("knn_distogram", &knn_distogram, py::arg("translations"), py::arg("k") = 20, py::arg("n_bins") = 22,
+          py::arg("d_min") = 2.0, py::arg("d_max") = 22.0, py::arg("pe_dim") = 16,
+          "k-NN distogram + offset encoding of each residue (reference knn_distogram), on the GPU");
+    m.def("build_factors", &build_factors, py::arg("features"), py::arg("r"), py::arg("d_z"), py::arg("w1"),
+          py::arg("w2"), py::arg("precision") = "bf16", "z1, z2 = features.w1, features.w2 on the GPU");
     m.def("comm_unique_id", &comm_unique_id, "128-byte NCCL unique id (rank 0 creates, all ranks share)");
     py::class_<Comm>(m, "Comm", "NCCL communicator for query-row sharding (one process per GPU)")
         .def(py::init<int, int, const py::bytes&, int>(), py::arg("world"), py::arg("rank"), py::arg("unique_id"),

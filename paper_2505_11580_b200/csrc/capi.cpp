@@ -10,6 +10,7 @@
 #include <string>
 
 #include "layer.hpp"
+#include "producer.hpp"
 #include "trunk.hpp"
 
 struct fipa_layer {
@@ -454,5 +455,57 @@ int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L_, const float* s,
 }
 
 int fipa_trunk_forward_launches(const fipa_trunk* trunk) { return trunk ? trunk->impl.launches_per_forward() : 0; }
+
+}  // extern "C"
+
+namespace {
+fipa_b200::KnnSpec knn_spec(uint64_t k, uint64_t n_bins, double d_min, double d_max, uint64_t pe_dim) {
+    if (k > (1u << 20) || n_bins > (1u << 20) || pe_dim > (1u << 20)) throw fipa_b200::ValueError("invalid distogram spec");
+    fipa_b200::KnnSpec s{};
+    s.k = int(k);
+    s.n_bins = int(n_bins);
+    s.pe_dim = int(pe_dim);
+    s.d_min = d_min;
+    s.d_max = d_max;
+    return s;
+}
+}  // namespace
+
+extern "C" {
+
+int fipa_knn_distogram(int64_t B, int64_t L_, const float* trans, uint64_t k, uint64_t n_bins, double d_min,
+                       double d_max, uint64_t pe_dim, float* out, void* stream) {
+    return guarded([&] {
+        fipa_b200::knn_distogram(B, L_, trans, knn_spec(k, n_bins, d_min, d_max, pe_dim), out,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_knn_distogram_host(int64_t B, int64_t L_, const double* trans, uint64_t k, uint64_t n_bins, double d_min,
+                            double d_max, uint64_t pe_dim, double* out) {
+    return guarded([&] {
+        fipa_b200::knn_distogram_host(B, L_, trans, knn_spec(k, n_bins, d_min, d_max, pe_dim), out);
+    });
+}
+
+size_t fipa_build_factors_workspace_size(int64_t rows, uint64_t f, uint64_t n) {
+    return rows < 1 ? 0 : fipa_b200::build_factors_workspace(rows, f, n);
+}
+
+int fipa_build_factors(int64_t rows, uint64_t f, const float* features, uint64_t r, uint64_t d_z, const float* w1,
+                       const float* w2, float* z1, float* z2, int precision, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    return guarded([&] {
+        fipa_b200::build_factors(rows, f, features, r, d_z, w1, w2, z1, z2, precision == FIPA_PREC_BF16, workspace,
+                                 workspace_bytes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_build_factors_host(int64_t rows, uint64_t f, const double* features, uint64_t r, uint64_t d_z,
+                            const double* w1, const double* w2, double* z1, double* z2, int precision) {
+    return guarded([&] {
+        fipa_b200::build_factors_host(rows, f, features, r, d_z, w1, w2, z1, z2, precision == FIPA_PREC_BF16);
+    });
+}
 
 }  // extern "C"

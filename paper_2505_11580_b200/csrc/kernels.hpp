@@ -160,6 +160,18 @@ void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int 
 // out[i] = in[i] * scale[i % period]
 void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream);
 
+// ------------------------------------------------- pair-factor producer (pair_features.cu)
+struct KnnSpec {
+    int k, n_bins, pe_dim;
+    double d_min, d_max;
+};
+size_t knn_smem_bytes(const KnnSpec& spec);
+// trans [B, L, 3] -> out [B, L, k, n_bins + pe_dim]; d_freq [pe_dim/2] = 10000^(-2p/pe_dim)
+void launch_knn_distogram(const float* trans, int B, int L, const KnnSpec& spec, const double* d_freq, float* out,
+                          cudaStream_t stream);
+// w [K, N] fp32 row-major -> wt [N, ld] bf16 (K-major B operand), pad columns zeroed
+void launch_transpose_to_bf16(const float* w, int K, int N, __nv_bfloat16* wt, int ld, cudaStream_t stream);
+
 // Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);
 // Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
