@@ -464,20 +464,45 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     for (int e = threadIdx.x; e < H; e += blockDim.x) atomicAdd(&a.dg[e], s_dg[e]);
 }
 
-__global__ void bwd_dout_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ mask,
-                                __nv_bfloat16* __restrict__ out, int ld_out, float* __restrict__ db,
-                                int64_t rows, int cols) {
-    const int col = blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= cols) return;
-    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64;
-    float s = 0.f;
-    for (int64_t r = r0; r < min(rows, r0 + 64); ++r) {
-        const bool ok = mask == nullptr || mask[r] != 0;
-        const float v = ok ? dout[r * cols + col] : 0.f;
-        out[r * ld_out + col] = __float2bfloat16_rn(v);
-        s += v;
+// dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 32 columns x 8 row
+// groups; each thread strides rows, partial sums reduced in shared memory, one atomic per column.
+__global__ void __launch_bounds__(256) bwd_dout_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ mask,
+                                                       __nv_bfloat16* __restrict__ out, int ld_out, float* __restrict__ db,
+                                                       int64_t rows, int cols, int rows_per_block) {
+    __shared__ float red[8][33];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int col = blockIdx.x * 32 + cx;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
+    const int64_t r1 = min(rows, r0 + rows_per_block);
+    float acc = 0.f;
+    if (col < cols) {
+        for (int64_t r = r0 + ry; r < r1; r += 8) {
+            const bool ok = mask == nullptr || mask[r] != 0;
+            const float v = ok ? dout[r * cols + col] : 0.f;
+            out[r * ld_out + col] = __float2bfloat16_rn(v);
+            acc += v;
+        }
     }
-    atomicAdd(&db[col], s);
+    red[ry][cx] = acc;
+    __syncthreads();
+    if (ry == 0 && col < cols) {
+        float sum = 0.f;
+        for (int k = 0; k < 8; ++k) sum += red[k][cx];
+        atomicAdd(&db[col], sum);
+    }
+}
+
+// Scatter the fused projection-weight gradient [d_in, n_proj] into the reference tensors
+// w_q | w_k | w_v | w_qp | w_kp | w_vp (each [d_in, width], concatenated in `dst`).
+__global__ void scatter_proj_grad_kernel(const float* __restrict__ src, int d_in, int n_proj, ScatterCols seg,
+                                         float* __restrict__ dst) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<int64_t>(d_in) * n_proj) return;
+    int i = 0;
+    while (i < 5 && e >= seg.dst_off[i + 1]) ++i;
+    const int64_t local = e - seg.dst_off[i];
+    const int r = static_cast<int>(local / seg.width[i]), c = static_cast<int>(local % seg.width[i]);
+    dst[e] = src[static_cast<int64_t>(r) * n_proj + seg.col0[i] + c];
 }
 
 __global__ void bwd_recenter_kernel(const float* __restrict__ dtc, const uint8_t* __restrict__ mask,
@@ -562,8 +587,15 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
                      int64_t rows, int cols, cudaStream_t stream) {
-    dim3 grid((cols + 127) / 128, static_cast<unsigned>((rows + 63) / 64));
-    bwd_dout_kernel<<<grid, 128, 0, stream>>>(dout, mask, out, ld_out, db, rows, cols);
+    const int rpb = 128;
+    dim3 grid((cols + 31) / 32, static_cast<unsigned>((rows + rpb - 1) / rpb));
+    bwd_dout_kernel<<<grid, 256, 0, stream>>>(dout, mask, out, ld_out, db, rows, cols, rpb);
+}
+
+void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
+                              cudaStream_t stream) {
+    const int64_t n = int64_t(d_in) * n_proj;
+    scatter_proj_grad_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(src, d_in, n_proj, seg, dst);
 }
 
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {

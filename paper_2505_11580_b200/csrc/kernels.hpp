@@ -155,6 +155,14 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
 // dOut with masked rows zeroed -> bf16 [BL, ld_out]; db[d_in] += column sums (zero db first).
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
                      int64_t rows, int cols, cudaStream_t stream);
+// Column blocks of the fused projection: block i = columns [col0[i], col0[i] + width[i]) of the
+// [d_in, n_proj] gradient, written row-major at dst_off[i] (dst_off[6] = d_in * n_proj).
+struct ScatterCols {
+    int col0[6], width[6];
+    int64_t dst_off[7];
+};
+void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
+                              cudaStream_t stream);
 // Translation gradient through the per-sample recentring: dt = mask*(dt_c - mean_valid(dt_c)).
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream);
 // out[i] = in[i] * scale[i % period]

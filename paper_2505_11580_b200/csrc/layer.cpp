@@ -538,8 +538,8 @@ bool FlashIpaLayer::backward_supported() const {
 
 int FlashIpaLayer::launches_per_backward() const {
     // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, attn Q, unpack, recenter, ds GEMM,
-    // dW_proj GEMM, two scale kernels (memsets and 2-D copies are not kernels of ours)
-    return 12;
+    // dW_proj GEMM, scatter, two scale kernels (memsets are not kernels of ours)
+    return 13;
 }
 
 int FlashIpaLayer::launches_per_forward() const {
@@ -954,14 +954,17 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         launch_gemm_bf16(g, stream);
     }
     mark(10);
-    // scatter the fused projection gradient into w_q .. w_vp
-    std::size_t col0 = 0;
-    for (int i = 0; i < 6; ++i) {
-        const std::size_t wcols = shapes[i][1];
-        cuda_check(cudaMemcpy2DAsync(dweights + woff[i], wcols * 4, ws.dwproj + col0, std::size_t(d.n_proj) * 4,
-                                     wcols * 4, d.d_in, cudaMemcpyDeviceToDevice, stream),
-                   "cudaMemcpy2DAsync");
-        col0 += wcols;
+    {  // scatter the fused projection gradient into w_q .. w_vp (one kernel)
+        ScatterCols seg{};
+        int col0 = 0;
+        for (int i = 0; i < 6; ++i) {
+            seg.col0[i] = col0;
+            seg.width[i] = int(shapes[i][1]);
+            seg.dst_off[i] = std::int64_t(woff[i]);
+            col0 += seg.width[i];
+        }
+        seg.dst_off[6] = std::int64_t(woff[6]);
+        launch_scatter_proj_grad(ws.dwproj, d.d_in, d.n_proj, seg, dweights, stream);
     }
     launch_scale_vec(ws.red + H, d_bwd_scale_ + H, 1, dw_bias, H * d.d_z, stream);
     launch_scale_vec(ws.red, d_bwd_scale_, H, dgamma, H, stream);
