@@ -71,6 +71,30 @@ struct PackArgs {
 };
 void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream);
 
+// Fused projection + pack (proj_pack.cu), bf16 path.  w_heads: head-major bf16 weight copy
+// [H * NH, din_ld] (per head: q | k | v | q_p | k_p | v_p columns, padded to NH rows).
+struct ProjPackArgs {
+    const __nv_bfloat16* s_bf16;   // [BL, din_ld]
+    const __nv_bfloat16* w_heads;  // [H * NH, din_ld]
+    const float* z1;
+    const float* z2;
+    const float* rot;
+    const float* trans;            // recentred
+    const uint8_t* mask;
+    const float* head_g;
+    const float* wl_bias;
+    float k_scale;
+    float* proj;                   // [BL, n_proj]: only the point columns are written
+    float* colbias;
+    __nv_bfloat16* qhat;
+    __nv_bfloat16* khat;
+    __nv_bfloat16* vhat;
+    int B, L;
+};
+bool proj_pack_supported(const LayerDims& d);
+int proj_pack_head_width(const LayerDims& d);
+void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t stream);
+
 struct AttnArgs {
     const __nv_bfloat16* qhat;
     const __nv_bfloat16* khat;

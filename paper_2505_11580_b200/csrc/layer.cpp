@@ -66,6 +66,13 @@ void convert(D* dst, const S* src, std::size_t n) {
 }
 
 // CTA-pair attention unless FIPA_ATTN_IMPL=1sm forces the single-CTA kernel.
+// Fused projection+pack unless FIPA_FUSED_PACK=0 (the unfused GEMM + pack path stays for the
+// fp32 path, unsupported shapes and A/B checks).
+bool fused_pack_enabled() {
+    const char* e = std::getenv("FIPA_FUSED_PACK");
+    return e == nullptr || std::string(e) != "0";
+}
+
 bool use_2sm_attention(const LayerDims& d) {
     const char* e = std::getenv("FIPA_ATTN_IMPL");
     const bool force_1sm = e != nullptr && std::string(e) == "1sm";
@@ -389,13 +396,13 @@ FlashIpaLayer::~FlashIpaLayer() {
 }
 
 void FlashIpaLayer::release_device() {
-    for (void* p : {static_cast<void*>(d_wproj_t_), static_cast<void*>(d_wout_t_),
+    for (void* p : {static_cast<void*>(d_wproj_t_), static_cast<void*>(d_wout_t_), static_cast<void*>(d_wheads_),
                     static_cast<void*>(d_wproj_), static_cast<void*>(d_wout_),
                     static_cast<void*>(d_bout_), static_cast<void*>(d_head_g_),
                     static_cast<void*>(d_wl_bias_), static_cast<void*>(d_bwd_scale_)}) {
         if (p) cudaFree(p);
     }
-    d_wproj_t_ = d_wout_t_ = nullptr;
+    d_wproj_t_ = d_wout_t_ = d_wheads_ = nullptr;
     d_wproj_ = d_wout_ = d_bout_ = d_head_g_ = d_wl_bias_ = d_bwd_scale_ = nullptr;
 }
 
@@ -449,6 +456,28 @@ void FlashIpaLayer::upload_weights() {
             for (std::size_t c = 0; c < np; ++c)
                 t[c * dld + r] = __float2bfloat16_rn(static_cast<float>(wproj[r * np + c]));
         up(&d_wproj_t_, t);
+        if (proj_pack_supported(d)) {
+            // head-major copy for the fused projection+pack kernel: per head the rows
+            // q (c) | k (c) | v (c) | q_p (3Nq) | k_p (3Nq) | v_p (3Nv), zero-padded to NH rows
+            const std::size_t NH = std::size_t(proj_pack_head_width(d)), c = cfg_.c, Nq = cfg_.n_query,
+                              Nv = cfg_.n_value;
+            std::vector<__nv_bfloat16> wh(H * NH * dld, __float2bfloat16_rn(0.f));
+            for (std::size_t h = 0; h < H; ++h) {
+                std::size_t n = 0;
+                auto put = [&](std::size_t col0, std::size_t width) {  // fused column block -> head rows
+                    for (std::size_t e = 0; e < width; ++e, ++n)
+                        for (std::size_t r = 0; r < din; ++r)
+                            wh[(h * NH + n) * dld + r] = __float2bfloat16_rn(static_cast<float>(wproj[r * np + col0 + e]));
+                };
+                put(0 * H * c + h * c, c);
+                put(1 * H * c + h * c, c);
+                put(2 * H * c + h * c, c);
+                put(3 * H * c + h * 3 * Nq, 3 * Nq);
+                put(3 * H * c + 3 * H * Nq + h * 3 * Nq, 3 * Nq);
+                put(3 * H * c + 6 * H * Nq + h * 3 * Nv, 3 * Nv);
+            }
+            up(&d_wheads_, wh);
+        }
         std::vector<__nv_bfloat16> o(din * fld, __float2bfloat16_rn(0.f));
         for (std::size_t r = 0; r < feat; ++r)
             for (std::size_t c = 0; c < din; ++c)
@@ -543,7 +572,9 @@ int FlashIpaLayer::launches_per_backward() const {
 }
 
 int FlashIpaLayer::launches_per_forward() const {
-    return cfg_.precision == Precision::bf16 ? 6 : 5;
+    if (cfg_.precision != Precision::bf16) return 5;
+    // recenter, cast, [fused projection+pack | projection GEMM, pack], attention, output GEMM
+    return (proj_pack_supported(dims_) && fused_pack_enabled()) ? 5 : 6;
 }
 
 void FlashIpaLayer::set_timing(bool on) {
@@ -610,7 +641,31 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         launch_recenter_with_sums(trans, shard->sums, ws.trans_c, int(B), int(L), stream);
     }
     mark(1);
-    if (do_pack) {
+    if (do_pack && d_wheads_ != nullptr && fused_pack_enabled()) {
+        // fused projection GEMM + frame application + packing (proj_pack.cu)
+        launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
+        mark(2);
+        ProjPackArgs pp{};
+        pp.s_bf16 = ws.s_bf16;
+        pp.w_heads = d_wheads_;
+        pp.z1 = z1;
+        pp.z2 = z2;
+        pp.rot = rot;
+        pp.trans = ws.trans_c;
+        pp.mask = mask;
+        pp.head_g = d_head_g_;
+        pp.wl_bias = d_wl_bias_;
+        pp.k_scale = k_scale_;
+        pp.proj = ws.proj;
+        pp.colbias = ws.colbias;
+        pp.qhat = static_cast<__nv_bfloat16*>(ws.qhat);
+        pp.khat = static_cast<__nv_bfloat16*>(ws.khat);
+        pp.vhat = static_cast<__nv_bfloat16*>(ws.vhat);
+        pp.B = int(B);
+        pp.L = int(L);
+        launch_proj_pack(d, pp, stream);
+        mark(3);
+    } else if (do_pack) {
     if (cfg_.precision == Precision::bf16) {
         launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
         mark(2);

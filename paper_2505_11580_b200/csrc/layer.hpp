@@ -213,6 +213,7 @@ private:
     // device weights
     __nv_bfloat16* d_wproj_t_ = nullptr;  // bf16 [n_proj, d_in]  (K-major B operand)
     __nv_bfloat16* d_wout_t_ = nullptr;   // bf16 [d_in, feat]
+    __nv_bfloat16* d_wheads_ = nullptr;   // bf16 [H * NH, d_in] head-major projection (fused path)
     float* d_wproj_ = nullptr;            // f32  [d_in, n_proj]
     float* d_wout_ = nullptr;             // f32  [feat, d_in]
     float* d_bout_ = nullptr;             // [d_in]

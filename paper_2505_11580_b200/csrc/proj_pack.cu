@@ -1,0 +1,420 @@
+// Fused projection + frame application + lifted-row packing (K1 + K2, bf16 path).
+//
+// Replaces   project_inputs  proj/src/ipa.cpp:201-217 (six bias-free linears)
+//            lift_qkv        proj/src/flash_ipa.cpp:23-139 (+ bias_factors, pair_features.cpp:141-163)
+// One CTA = 128 residues x one head.  The head's 468 projection columns
+// (q | k | v | q_p | k_p | v_p, head-major weight copy padded to NH = 480) are one tcgen05 GEMM
+// (M=128, N=256+224, K=d_in) into TMEM, fed by a 2-stage TMA ring.  The epilogue warps (thread =
+// residue) apply the residue's frame and build the q_hat / k_hat / v_hat rows of pack.cu's layout
+// directly from TMEM, one tensor at a time, into a 128-byte-swizzled shared-memory tile that
+// leaves by TMA tensor stores.  The fp32 [B*L, 3744] projection round trip of the unfused path
+// (write + read ~250 MB at B=8, L=1024) disappears; only the point columns (needed by the
+// backward) are written to the projection buffer.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+#include "tma_host.hpp"
+
+namespace fipa_b200 {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;  // w0 TMA, w1 TMEM + MMA, w2..w5 epilogue
+constexpr int kStages = 2;
+constexpr int kMaxQ = 8;       // points held in registers by the epilogue
+constexpr int kMaxV = 12;
+constexpr float kL2E = 1.4426950408889634f;
+constexpr float kMaskedBias = -1.0e30f;
+
+struct PPParams {
+    int M, L, H, c, Nq, Nv, dz, rdz, NH, N1, N2, nk;
+    int dqk_used, dqk_pad, dv_used, dv_pad, zq, n_proj, chunk_ok;
+    const float* z1;
+    const float* z2;
+    const float* rot;
+    const float* trans;  // recentred
+    const uint8_t* mask;
+    const float* head_g;
+    const float* wl_bias;
+    float k_scale;
+    float* proj;     // [M, n_proj]: point columns written (backward)
+    float* colbias;  // [B*H, L]
+    __nv_bfloat16* qhat;
+    __nv_bfloat16* khat;
+    __nv_bfloat16* vhat;
+};
+
+__device__ __forceinline__ float bf_hi(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float bf_lo(float x) { return x - __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// One element of the 128 x W bf16 staging tile: [W/64 blocks][128 rows][128 B], 16-byte chunk
+// index XOR (row % 8) -- the TMA SWIZZLE_128B layout.
+__device__ __forceinline__ void stage_put(uint8_t* tile, int row, int col, float v) {
+    uint8_t* p = tile + (col >> 6) * (BM * 128) + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) + ((col & 7) << 1);
+    *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+}
+// 8 consecutive columns (col % 8 == 0) as one 16-byte store
+__device__ __forceinline__ void stage_put8(uint8_t* tile, int row, int col, const float* v) {
+    uint8_t* p = tile + (col >> 6) * (BM * 128) + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
+    uint4 w;
+    w.x = ptx::pack_bf16x2(v[0], v[1]);
+    w.y = ptx::pack_bf16x2(v[2], v[3]);
+    w.z = ptx::pack_bf16x2(v[4], v[5]);
+    w.w = ptx::pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(p) = w;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    proj_pack_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                     const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                     const __grid_constant__ CUtensorMap mapV, PPParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int a_bytes = BM * BK * 2, b_bytes = p.NH * BK * 2, stage_bytes = a_bytes + b_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kStages;
+    uint64_t* done = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint8_t* ring = smem + 1024;
+    // two output staging tiles (alternating tensors) reuse the ring once the MMAs are done
+    uint8_t* tiles = ring;
+    const int tile_bytes = BM * (p.dqk_pad > p.dv_pad ? p.dqk_pad : p.dv_pad) * 2;
+
+    const int warp = ptx::warp_id(), lane = ptx::lane_id();
+    const int m0 = blockIdx.x * BM, h = blockIdx.y;
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&mapA);
+        ptx::tma_prefetch(&mapB);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < p.nk; ++kb) {
+                const int s = kb % kStages;
+                if (kb >= kStages) ptx::mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+                uint8_t* sa = ring + s * stage_bytes;
+                ptx::mbar_expect_tx(&full[s], stage_bytes);
+                ptx::tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
+                ptx::tma_load_2d(sa + a_bytes, &mapB, &full[s], kb * BK, h * p.NH);
+                ptx::tma_load_2d(sa + a_bytes + (p.NH / 2) * 128, &mapB, &full[s], kb * BK, h * p.NH + p.NH / 2);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id1 = ptx::idesc_bf16(BM, p.N1, false, false);
+            const uint32_t id2 = ptx::idesc_bf16(BM, p.N2 > 0 ? p.N2 : 16, false, false);
+            for (int kb = 0; kb < p.nk; ++kb) {
+                const int s = kb % kStages;
+                ptx::mbar_wait(&full[s], (kb / kStages) & 1);
+                ptx::tc_fence_after();
+                const uint32_t sa = ptx::smem_u32(ring + s * stage_bytes);
+                const uint32_t sb = sa + a_bytes;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk) {
+                    const uint64_t da = ptx::sw128_desc(sa + kk * 32, 16, 1024);
+                    ptx::mma_ss(tmem, da, ptx::sw128_desc(sb + kk * 32, 16, 1024), id1, (kb | kk) != 0);
+                    if (p.N2 > 0)
+                        ptx::mma_ss(tmem + p.N1, da, ptx::sw128_desc(sb + p.N1 * 128 + kk * 32, 16, 1024), id2,
+                                    (kb | kk) != 0);
+                }
+                ptx::mma_commit(&empty[s]);
+            }
+            ptx::mma_commit(done);
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;  // row of the tile = TMEM lane
+        const uint32_t tl = tmem + (uint32_t(quad * 32) << 16);
+        const int row = m0 + r;
+        const bool ok = row < p.M;
+        const int rowc = ok ? row : p.M - 1;
+        const int b = rowc / p.L, i = rowc - b * p.L;
+        const int c = p.c, Nq = p.Nq, Nv = p.Nv, rdz = p.rdz;
+        const int cq = 0, ck = c, cv = 2 * c, cqp = 3 * c, ckp = cqp + 3 * Nq, cvp = ckp + 3 * Nq;  // TMEM columns
+        float R[9], t[3];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = __ldg(p.rot + int64_t(rowc) * 9 + k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] = __ldg(p.trans + int64_t(rowc) * 3 + k);
+        const bool valid = p.mask == nullptr || p.mask[rowc] != 0;
+        const float g = p.head_g[h];
+        ptx::mbar_wait(done, 0);
+        ptx::tc_fence_after();
+
+        // points: raw (written back for the backward) and frame-rotated
+        float rq[3 * kMaxQ], rk[3 * kMaxQ], rv[3 * kMaxV];
+        {
+            float* prow = p.proj + int64_t(rowc) * p.n_proj;
+            const int oq = 3 * p.H * c + h * 3 * Nq, okp = oq + 3 * p.H * Nq, ov = 3 * p.H * c + 6 * p.H * Nq + h * 3 * Nv;
+#pragma unroll
+            for (int part = 0; part < 3; ++part) {
+                const int col = part == 0 ? cqp : part == 1 ? ckp : cvp;
+                const int n = part == 2 ? 3 * Nv : 3 * Nq;  // <= 36
+                uint32_t u[32], w[16];
+                ptx::tmem_ld32(tl + col, u);
+                ptx::tmem_ld16(tl + col + 32, w);
+                ptx::tmem_wait_ld();
+                if (ok) {
+                    float* dst = prow + (part == 0 ? oq : part == 1 ? okp : ov);
+                    for (int e = 0; e < n; ++e) dst[e] = __uint_as_float(e < 32 ? u[e] : w[e - 32]);
+                }
+                float* outp = part == 0 ? rq : part == 1 ? rk : rv;
+                const int cap = part == 2 ? kMaxV : kMaxQ;
+#pragma unroll
+                for (int q = 0; q < kMaxV; ++q) {
+                    if (q < cap && 3 * q < n) {
+                        const float x = __uint_as_float(3 * q < 32 ? u[3 * q] : w[3 * q - 32]);
+                        const float y = __uint_as_float(3 * q + 1 < 32 ? u[3 * q + 1] : w[3 * q + 1 - 32]);
+                        const float z = __uint_as_float(3 * q + 2 < 32 ? u[3 * q + 2] : w[3 * q + 2 - 32]);
+                        outp[3 * q] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z));
+                        outp[3 * q + 1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z));
+                        outp[3 * q + 2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z));
+                    }
+                }
+            }
+        }
+        float qb[3] = {0.f, 0.f, 0.f}, W[3] = {0.f, 0.f, 0.f}, kn = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxQ; ++q) {
+            if (q < Nq) {
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    qb[x] += rq[3 * q + x];
+                    const float tk = rk[3 * q + x] + t[x];
+                    W[x] += tk;
+                    kn = fmaf(tk, tk, kn);
+                }
+            }
+        }
+        const float cb = valid ? kL2E * (-0.5f * g * kn) : kMaskedBias;
+        if (ok) p.colbias[(int64_t(b) * p.H + h) * p.L + i] = valid ? -0.5f * g * kn : -INFINITY;
+        const int g0 = c + 3 * Nq, zq = p.zq;
+        const int64_t hrow = (int64_t(b) * p.H + h) * p.L + i;
+
+        // Three tensors through two alternating staging tiles.  Phase A (thread = row): columns
+        // derived from TMEM and the frame.  Phase B (warp-cooperative, lanes across columns): the
+        // pair-factor columns, straight from coalesced z1 / z2 row loads.
+        const float* wbh = p.wl_bias + h * p.dz;
+        for (int tsel = 0; tsel < 3; ++tsel) {
+            uint8_t* tile = tiles + (tsel & 1) * tile_bytes;
+            if (tsel == 2) {
+                // tile 0 is reused: tensor 0's TMA stores must have read it (tensor 1's may fly)
+                if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                named_sync(1, 128);
+            }
+            const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
+            float v8[8];
+            // ---- phase A: [0, c) scalar channels from TMEM, 16 per load
+            const float sc = tsel == 0 ? kL2E : tsel == 1 ? p.k_scale : 1.f;
+            const int tcol = tsel == 0 ? cq : tsel == 1 ? ck : cv;
+            for (int c0 = 0; c0 < c; c0 += 16) {
+                uint32_t u[16];
+                ptx::tmem_ld16(tl + tcol + c0, u);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[e]);
+                stage_put8(tile, r, c0, v8);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[8 + e]);
+                stage_put8(tile, r, c0 + 8, v8);
+            }
+            if (tsel < 2) {
+                // rotated points, the 21 translation / bias columns and the zq padding
+                const float gs = tsel == 0 ? kL2E : g;
+                const float* pts = tsel == 0 ? rq : rk;
+#pragma unroll
+                for (int e = 0; e < 3 * kMaxQ; ++e)
+                    if (e < 3 * Nq) stage_put(tile, r, c + e, gs * pts[e]);
+                for (int e = 0; e < zq - g0; ++e) {
+                    const int x = e % 3;
+                    float qv, kv;
+                    if (e < 9) {
+                        const float qq = kL2E * qb[x], tt = g * t[x];
+                        qv = e < 6 ? bf_hi(qq) : bf_lo(qq);
+                        kv = (e >= 3 && e < 6) ? bf_lo(tt) : bf_hi(tt);
+                    } else if (e < 18) {
+                        const float tq = kL2E * t[x], ww = g * W[x];
+                        qv = (e >= 12 && e < 15) ? bf_lo(tq) : bf_hi(tq);
+                        kv = e < 15 ? bf_hi(ww) : bf_lo(ww);
+                    } else if (e < 20) {
+                        qv = 1.0f;
+                        kv = e == 18 ? bf_hi(cb) : (valid ? bf_lo(cb) : 0.f);
+                    } else {
+                        qv = 0.f;
+                        kv = e == 20 ? 1.0f : 0.f;
+                    }
+                    stage_put(tile, r, g0 + e, tsel == 0 ? qv : kv);
+                }
+                for (int e = p.dqk_used; e < width; ++e) stage_put(tile, r, e, 0.f);
+            } else {
+                const int vp = c + rdz;
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    stage_put(tile, r, vp + x, bf_hi(t[x]));
+                    stage_put(tile, r, vp + 3 + x, bf_lo(t[x]));
+                }
+#pragma unroll
+                for (int e = 0; e < 3 * kMaxV; ++e)
+                    if (e < 3 * Nv) stage_put(tile, r, vp + 6 + e, rv[e]);
+                for (int e = p.dv_used; e < width; ++e) stage_put(tile, r, e, 0.f);
+            }
+            // ---- phase B: pair factors, warp w covers rows quad*32 .. +32, lane = 8-column chunk
+            {
+                const float* zsrc = tsel == 0 ? p.z1 : p.z2;
+                const int zcol = tsel == 2 ? c : zq;
+                const int nchunk = rdz / 8;
+                for (int j = lane; j < nchunk; j += 32) {
+                    float wm[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        wm[e] = tsel == 0 ? kL2E : tsel == 1 ? __ldg(wbh + (8 * j + e) % p.dz) : 1.f;
+                    // 8 rows of loads in flight per lane before any use
+                    for (int rb = 0; rb < 32; rb += 8) {
+                        float4 za[8][2];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            int grow = m0 + quad * 32 + rb + u;
+                            grow = grow < p.M ? grow : p.M - 1;
+                            const float* zr = zsrc + int64_t(grow) * rdz + 8 * j;
+                            za[u][0] = __ldg(reinterpret_cast<const float4*>(zr));
+                            za[u][1] = __ldg(reinterpret_cast<const float4*>(zr + 4));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            v8[0] = wm[0] * za[u][0].x;
+                            v8[1] = wm[1] * za[u][0].y;
+                            v8[2] = wm[2] * za[u][0].z;
+                            v8[3] = wm[3] * za[u][0].w;
+                            v8[4] = wm[4] * za[u][1].x;
+                            v8[5] = wm[5] * za[u][1].y;
+                            v8[6] = wm[6] * za[u][1].z;
+                            v8[7] = wm[7] * za[u][1].w;
+                            stage_put8(tile, quad * 32 + rb + u, zcol + 8 * j, v8);
+                        }
+                    }
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            named_sync(1, 128);
+            const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
+            if (p.chunk_ok) {
+                // 32-row chunks never straddle two samples (L % 32 == 0): TMA stores, one thread
+                if (warp == 2 && lane == 0) {
+                    for (int ch = 0; ch < BM / 32; ++ch) {
+                        const int rr = m0 + ch * 32;
+                        if (rr >= p.M) break;
+                        const int cb_ = rr / p.L, ci = rr - cb_ * p.L;
+                        for (int blk = 0; blk < width / 64; ++blk)
+                            tma_store_3d(map, tile + blk * (BM * 128) + ch * 32 * 128, blk * 64, ci, cb_ * p.H + h);
+                    }
+                    bulk_commit();
+                }
+            } else if (ok) {
+                // generic shapes: each thread copies its own row (16-byte chunks, un-swizzled)
+                __nv_bfloat16* dst = (tsel == 0 ? p.qhat : tsel == 1 ? p.khat : p.vhat) + hrow * width;
+                for (int ch8 = 0; ch8 < width / 8; ++ch8) {
+                    const uint8_t* src = tile + (ch8 >> 3) * (BM * 128) + r * 128 + (((ch8 & 7) ^ (r & 7)) << 4);
+                    reinterpret_cast<uint4*>(dst)[ch8] = *reinterpret_cast<const uint4*>(src);
+                }
+            }
+        }
+        if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+bool proj_pack_supported(const LayerDims& d) {
+    const int NH = (3 * d.c + 6 * d.n_query + 3 * d.n_value + 15) / 16 * 16;
+    const size_t ring = size_t(kStages) * (BM * BK * 2 + NH * BK * 2);
+    const size_t tile = size_t(BM) * std::max(d.dqk_pad, d.dv_pad) * 2;
+    return d.n_query <= kMaxQ && d.n_value <= kMaxV && d.c % 16 == 0 && (d.rank * d.d_z) % 8 == 0 &&
+           d.d_z % 8 == 0 && d.zq % 8 == 0 && NH <= 512 && (NH / 2) % 8 == 0 && NH / 2 <= 256 &&
+           d.dqk_pad % 64 == 0 && d.dv_pad % 64 == 0 && d.din_ld % 8 == 0 &&
+           std::max(ring, 2 * tile) + 2048 <= 232448;
+}
+
+int proj_pack_head_width(const LayerDims& d) { return (3 * d.c + 6 * d.n_query + 3 * d.n_value + 15) / 16 * 16; }
+
+void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t stream) {
+    if (!proj_pack_supported(d)) throw std::invalid_argument("fused projection+pack: unsupported shape");
+    PPParams p{};
+    p.M = a.B * a.L;
+    p.L = a.L;
+    p.H = d.heads;
+    p.c = d.c;
+    p.Nq = d.n_query;
+    p.Nv = d.n_value;
+    p.dz = d.d_z;
+    p.rdz = d.rank * d.d_z;
+    p.NH = proj_pack_head_width(d);
+    p.N1 = std::min(p.NH, 256);
+    p.N2 = p.NH - p.N1;
+    p.nk = (d.d_in + BK - 1) / BK;
+    p.dqk_used = d.dqk_used;
+    p.dqk_pad = d.dqk_pad;
+    p.dv_used = d.dv_used;
+    p.dv_pad = d.dv_pad;
+    p.zq = d.zq;
+    p.n_proj = d.n_proj;
+    p.chunk_ok = (a.L % 32) == 0 ? 1 : 0;
+    p.z1 = a.z1;
+    p.z2 = a.z2;
+    p.rot = a.rot;
+    p.trans = a.trans;
+    p.mask = a.mask;
+    p.head_g = a.head_g;
+    p.wl_bias = a.wl_bias;
+    p.k_scale = a.k_scale;
+    p.proj = a.proj;
+    p.colbias = a.colbias;
+    p.qhat = a.qhat;
+    p.khat = a.khat;
+    p.vhat = a.vhat;
+    const uint64_t BH = uint64_t(a.B) * d.heads;
+    const CUtensorMap mapA = make_map_2d_bf16(a.s_bf16, uint64_t(p.M), d.d_in, d.din_ld, 64, BM);
+    const CUtensorMap mapB = make_map_2d_bf16(a.w_heads, uint64_t(d.heads) * p.NH, d.d_in, d.din_ld, 64, p.NH / 2);
+    const CUtensorMap mapQ = make_map_3d_bf16(a.qhat, d.dqk_pad, a.L, BH, d.dqk_pad, 64, 32);
+    const CUtensorMap mapK = make_map_3d_bf16(a.khat, d.dqk_pad, a.L, BH, d.dqk_pad, 64, 32);
+    const CUtensorMap mapV = make_map_3d_bf16(a.vhat, d.dv_pad, a.L, BH, d.dv_pad, 64, 32);
+    const size_t ring = size_t(kStages) * (BM * BK * 2 + p.NH * BK * 2);
+    const size_t tile = size_t(BM) * std::max(d.dqk_pad, d.dv_pad) * 2;
+    const int smem = int(std::max(ring, 2 * tile)) + 1024 + 1024;
+    cudaFuncSetAttribute(proj_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    dim3 grid(static_cast<unsigned>((p.M + BM - 1) / BM), static_cast<unsigned>(d.heads));
+    proj_pack_kernel<<<grid, kThreads, smem, stream>>>(mapA, mapB, mapQ, mapK, mapV, p);
+}
+
+}  // namespace fipa_b200

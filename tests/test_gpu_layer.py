@@ -39,7 +39,9 @@ def test_stage_by_stage_main_shape(fipa, precision):
     # projection GEMM: s . W_fused (fp32 accumulation)
     proj = ws_view(ws, off[2], B * L * n_proj, "f32").reshape(B, L, n_proj)
     wf = np.concatenate([w[n] for n in ("w_q", "w_k", "w_v", "w_qp", "w_kp", "w_vp")], axis=1)
-    assert rel_dev(batch["s"] @ wf, proj) < (1e-5 if bf else 1e-5)
+    # the fused bf16 projection+pack kernel keeps only the point columns (what the backward reads)
+    pts0 = 3 * MAIN["heads"] * MAIN["c"] if bf else 0
+    assert rel_dev((batch["s"] @ wf)[..., pts0:], proj[..., pts0:]) < 1e-5
 
     qh = ws_view(ws, off[3], B * H * L * dqk_pad, el).reshape(B, H, L, dqk_pad)
     kh = ws_view(ws, off[4], B * H * L * dqk_pad, el).reshape(B, H, L, dqk_pad)
