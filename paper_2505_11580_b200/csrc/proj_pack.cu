@@ -26,7 +26,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;  // w0 TMA, w1 TMEM + MMA, w2..w5 epilogue
+constexpr int kThreads = 320;  // w0 TMA, w1 TMEM + MMA, w2..w9 epilogue (two warps per TMEM quadrant)
 constexpr int kStages = 2;
 constexpr int kMaxQ = 8;       // points held in registers by the epilogue
 constexpr int kMaxV = 12;
@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ---------------------------------------------------------------- epilogue
         const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;  // 0: scalar channels, 1: geometry columns (phase A)
         const int r = quad * 32 + lane;  // row of the tile = TMEM lane
         const uint32_t tl = tmem + (uint32_t(quad * 32) << 16);
         const int row = m0 + r;
@@ -170,9 +171,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(done, 0);
         ptx::tc_fence_after();
 
-        // points: raw (written back for the backward) and frame-rotated
+        // points: raw (written back for the backward) and frame-rotated (geometry half only)
         float rq[3 * kMaxQ], rk[3 * kMaxQ], rv[3 * kMaxV];
-        {
+        if (half == 1) {
             float* prow = p.proj + int64_t(rowc) * p.n_proj;
             const int oq = 3 * p.H * c + h * 3 * Nq, okp = oq + 3 * p.H * Nq, ov = 3 * p.H * c + 6 * p.H * Nq + h * 3 * Nv;
 #pragma unroll
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float qb[3] = {0.f, 0.f, 0.f}, W[3] = {0.f, 0.f, 0.f}, kn = 0.f;
 #pragma unroll
         for (int q = 0; q < kMaxQ; ++q) {
-            if (q < Nq) {
+            if (half == 1 && q < Nq) {
 #pragma unroll
                 for (int x = 0; x < 3; ++x) {
                     qb[x] += rq[3 * q + x];
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         const float cb = valid ? kL2E * (-0.5f * g * kn) : kMaskedBias;
-        if (ok) p.colbias[(int64_t(b) * p.H + h) * p.L + i] = valid ? -0.5f * g * kn : -INFINITY;
+        if (ok && half == 1) p.colbias[(int64_t(b) * p.H + h) * p.L + i] = valid ? -0.5f * g * kn : -INFINITY;
         const int g0 = c + 3 * Nq, zq = p.zq;
         const int64_t hrow = (int64_t(b) * p.H + h) * p.L + i;
 
@@ -229,14 +230,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tsel == 2) {
                 // tile 0 is reused: tensor 0's TMA stores must have read it (tensor 1's may fly)
                 if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                named_sync(1, 128);
+                named_sync(1, 256);
             }
             const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
             float v8[8];
-            // ---- phase A: [0, c) scalar channels from TMEM, 16 per load
+            // ---- phase A, half 0: [0, c) scalar channels from TMEM, 16 per load
             const float sc = tsel == 0 ? kL2E : tsel == 1 ? p.k_scale : 1.f;
             const int tcol = tsel == 0 ? cq : tsel == 1 ? ck : cv;
-            for (int c0 = 0; c0 < c; c0 += 16) {
+            for (int c0 = 0; c0 < (half == 0 ? c : 0); c0 += 16) {
                 uint32_t u[16];
                 ptx::tmem_ld16(tl + tcol + c0, u);
                 ptx::tmem_wait_ld();
@@ -247,7 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[8 + e]);
                 stage_put8(tile, r, c0 + 8, v8);
             }
-            if (tsel < 2) {
+            if (half == 0) {
+            } else if (tsel < 2) {
                 // rotated points, the 21 translation / bias columns and the zq padding
                 const float gs = tsel == 0 ? kL2E : g;
                 const float* pts = tsel == 0 ? rq : rk;
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (e < 3 * Nv) stage_put(tile, r, vp + 6 + e, rv[e]);
                 for (int e = p.dv_used; e < width; ++e) stage_put(tile, r, e, 0.f);
             }
-            // ---- phase B: pair factors, warp w covers rows quad*32 .. +32, lane = 8-column chunk
+            // ---- phase B: pair factors, warp covers rows quad*32 + half*16 .. +16, lane = 8-column chunk
             {
                 const float* zsrc = tsel == 0 ? p.z1 : p.z2;
                 const int zcol = tsel == 2 ? c : zq;
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < 8; ++e)
                         wm[e] = tsel == 0 ? kL2E : tsel == 1 ? __ldg(wbh + (8 * j + e) % p.dz) : 1.f;
                     // 8 rows of loads in flight per lane before any use
-                    for (int rb = 0; rb < 32; rb += 8) {
+                    for (int rb = 16 * half; rb < 16 * half + 16; rb += 8) {
                         float4 za[8][2];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::fence_proxy_async_smem();
-            named_sync(1, 128);
+            named_sync(1, 256);
             const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
             if (p.chunk_ok) {
                 // 32-row chunks never straddle two samples (L % 32 == 0): TMA stores, one thread
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     bulk_commit();
                 }
-            } else if (ok) {
+            } else if (ok && half == 0) {
                 // generic shapes: each thread copies its own row (16-byte chunks, un-swizzled)
                 __nv_bfloat16* dst = (tsel == 0 ? p.qhat : tsel == 1 ? p.khat : p.vhat) + hrow * width;
                 for (int ch8 = 0; ch8 < width / 8; ++ch8) {
