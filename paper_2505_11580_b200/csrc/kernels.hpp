@@ -117,6 +117,10 @@ void launch_attn_fwd_tc(const LayerDims& d, const AttnArgs& a, cudaStream_t stre
 // CTA-pair version (tcgen05 cta_group::2, 256 query rows per pair, streamed K/V rings).
 bool attn_fwd_2sm_supported(const LayerDims& d);
 void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
+// Two-pass CTA-pair version for lifted rows wider than the 2-SM kernel's TMEM/smem budget
+// (z_factor_rank 3-4): value columns split over two passes, K streamed in column-block groups.
+bool attn_fwd_pass_supported(const LayerDims& d);
+void launch_attn_fwd_pass(const LayerDims& d, const AttnArgs& a, cudaStream_t stream);
 
 // ------------------------------------------------------------- backward
 struct AttnBwdArgs {

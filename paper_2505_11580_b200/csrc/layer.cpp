@@ -73,10 +73,21 @@ bool fused_pack_enabled() {
     return e == nullptr || std::string(e) != "0";
 }
 
-bool use_2sm_attention(const LayerDims& d) {
+// Inference attention kernel: the CTA-pair kernel where its budget allows, the two-pass pair
+// kernel for wider lifted rows (rank 3-4), else the single-CTA kernel.  FIPA_ATTN_IMPL=1sm /
+// =pass force the alternatives (A/B checks).
+enum class AttnImpl { pair, pass, one_sm };
+AttnImpl attention_impl(const LayerDims& d) {
     const char* e = std::getenv("FIPA_ATTN_IMPL");
-    const bool force_1sm = e != nullptr && std::string(e) == "1sm";
-    return !force_1sm && attn_fwd_2sm_supported(d);
+    const std::string v = e ? std::string(e) : std::string();
+    if (v == "1sm") return AttnImpl::one_sm;
+    if (v == "pass" && attn_fwd_pass_supported(d)) return AttnImpl::pass;
+    if (attn_fwd_2sm_supported(d)) return AttnImpl::pair;
+    if (attn_fwd_pass_supported(d)) return AttnImpl::pass;
+    return AttnImpl::one_sm;
+}
+bool bf16_attention_supported(const LayerDims& d) {
+    return attn_fwd_2sm_supported(d) || attn_fwd_pass_supported(d);
 }
 
 // ------------------------------------------------------------------ Rng
@@ -617,7 +628,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
     REQUIRE(!train || backward_supported(),
             "training (forward_train/backward) needs precision='bf16' and lifted widths <= 448");
-    REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && attn_fwd_2sm_supported(dims_) && !train),
+    REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && bf16_attention_supported(dims_) && !train),
             "query-row sharding needs precision='bf16' (inference forward)");
     const bool do_pack = shard == nullptr || shard->stage == 1;
     const bool do_attend = shard == nullptr || shard->stage == 2;
@@ -729,8 +740,11 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
             aa.Lk = int(L) * shard->groups;
             aa.kchunk = int(L);
         }
-        if (train || use_2sm_attention(d)) {
+        const AttnImpl impl = train ? AttnImpl::pair : attention_impl(d);
+        if (impl == AttnImpl::pair) {
             launch_attn_fwd_2sm(d, aa, stream);
+        } else if (impl == AttnImpl::pass) {
+            launch_attn_fwd_pass(d, aa, stream);
         } else {
             launch_attn_fwd_tc(d, aa, stream);
         }

@@ -169,9 +169,9 @@ def test_reference_model_defaults_roundtrip(fipa, tmp_path):
     assert np.array_equal(other.flash(*args), got)
 
 
-@pytest.mark.parametrize("impl", ["1sm", "2sm"])
+@pytest.mark.parametrize("impl", ["1sm", "2sm", "pass"])
 def test_attention_kernels_agree(fipa, impl, monkeypatch):
-    """Both tcgen05 attention kernels (single CTA, CTA pair) against the oracle at the
+    """The tcgen05 attention kernels (single CTA, CTA pair, two-pass CTA pair) against the oracle at the
     north-star shape, ragged L with masked keys (FIPA_ATTN_IMPL selects the kernel)."""
     monkeypatch.setenv("FIPA_ATTN_IMPL", impl)
     model = _model(fipa, MAIN, "bf16", seed=21)
@@ -206,3 +206,32 @@ def test_long_sequence_properties(fipa, L):
     ref = feat @ w["w_out"] + w["b_out"]
     assert rel_dev(ref, out[0][rows]) < BF16_TOL
     del torch
+
+
+@pytest.mark.parametrize("rank", [3, 4])
+@pytest.mark.parametrize("B,L,mask_frac", [(2, 200, 0.15), (1, 513, 0.0)])
+def test_wide_rank_bf16(fipa, rank, B, L, mask_frac):
+    """z_factor_rank 3-4 (lifted widths 560-704) on the tensor cores: the two-pass CTA-pair
+    kernel (attn_fwd_pass.cu) against the oracle, ragged lengths and masked keys (BASELINE cfg5)."""
+    shape = dict(MAIN, rank=rank)
+    model = _model(fipa, shape, "bf16", seed=31 + rank)
+    w = oracle_weights_for(model, "bf16")
+    batch = make_batch(shape, B, L, seed=900 + rank * 10 + B, mask_frac=mask_frac, bf16=True)
+    got = model.flash(batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"], mask=batch["mask"])
+    ref = oracle_forward(shape, w, batch)
+    assert rel_dev(ref, got) < BF16_TOL
+    if mask_frac > 0:
+        assert np.all(got[~batch["mask"].astype(bool)] == 0.0)
+
+
+@pytest.mark.parametrize("rank", [3, 4])
+def test_wide_rank_se3_invariance(fipa, rank):
+    shape = dict(MAIN, rank=rank)
+    model = _model(fipa, shape, "bf16", seed=5)
+    batch = make_batch(shape, 1, 300, seed=61, bf16=True)
+    args = (batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"])
+    got = model.flash(*args)
+    g_rot, g_t = random_rigid(9, scale=10.0)
+    moved = move_frames(batch, g_rot, g_t)
+    got2 = model.flash(moved["s"], moved["z1"], moved["z2"], moved["rot"], moved["trans"])
+    assert rel_dev(got, got2) < BF16_TOL

@@ -3,8 +3,8 @@
 For each (rank, L): device time of one layer forward (CUDA events, median of 5 after 2 warm-ups,
 L2 flushed before each), residues/s, attention-equivalent TFLOP/s (2*B*H*L^2*(D_qk+D_v) over the
 whole layer time), and the device memory the call needs (workspace bytes + inputs/outputs) to
-show memory linear in L.  rank 1-2 run the tcgen05 path (bf16); rank 3-4 exceed the tcgen05
-kernels' 448-column head limit and run the fp32 SIMT path (precision="f32") at smaller L.
+show memory linear in L.  Every rank runs the bf16 tcgen05 path: rank 1-2 the CTA-pair kernel,
+rank 3-4 (lifted widths 560-704) the two-pass CTA-pair kernel (attn_fwd_pass.cu).
 
     python tools/sweep.py --out profiles/r1_sweep.json
 """
@@ -65,20 +65,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_sweep.json"))
     ap.add_argument("--maxL", type=int, default=65536)
+    ap.add_argument("--minL", type=int, default=256)
+    ap.add_argument("--ranks", default="1,2,3,4")
     args = ap.parse_args()
     rows = []
-    for r in (1, 2):
+    for r in [int(x) for x in args.ranks.split(",")]:
         shape = dict(bench.SHAPE, rank=r)
-        L = 256
+        L = args.minL
         while L <= args.maxL:
             rows.append(run(shape, "bf16", 1, L))
             print(json.dumps(rows[-1]), flush=True)
             L *= 2
-    for r in (3, 4):  # fp32 SIMT path (head widths > 448)
-        shape = dict(bench.SHAPE, rank=r)
-        for L in (256, 1024, 4096):
-            rows.append(run(shape, "f32", 1, L, reps=3))
-            print(json.dumps(rows[-1]), flush=True)
     with open(args.out, "w") as f:
         json.dump({"device": torch.cuda.get_device_name(0), "rows": rows}, f, indent=1)
 
