@@ -25,6 +25,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -205,54 +207,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t k_base = ptx::smem_u32(sK);
             const uint32_t v_base = ptx::smem_u32(sV);
             ptx::mbar_wait(&bars->q_full, 0);
-            int kn = 0, vn = 0;
-            for (int t = 0; t <= T; ++t) {
+            // ring slots / phases and the (pass, tile) position advance by counters: no integer
+            // division on the issue path
+            int ks = 0, kph = 0, vs = 0, vph = 0;
+            const uint64_t dq0 = ptx::sw128_desc(q_base, 16, 1024);
+            const uint64_t dk0 = ptx::sw128_desc(k_base, 16, 1024);
+            for (int t = 0, ps_prev = 0, jj = -1; t <= T; ++t) {
                 if (t < T) {
                     if (t > 0) ptx::mbar_wait_cluster(&bars->s_free, (t - 1) & 1);
-                    for (int u = 0; u < p.nkst; ++u, ++kn) {
-                        const int ks = kn % p.kst;
-                        ptx::mbar_wait(&bars->k_full[ks], (kn / p.kst) & 1);
+                    for (int u = 0; u < p.nkst; ++u) {
+                        ptx::mbar_wait(&bars->k_full[ks], kph);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
-                            const uint32_t kbase = k_base + ks * lay.kstage;
-                            const int k_lo = u * p.kb * 4, k_hi = min(p.qk_steps, (u + 1) * p.kb * 4);
-                            for (int kk = k_lo; kk < k_hi; ++kk) {
-                                const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
-                                const uint64_t da = ptx::sw128_desc(q_base + blk * (BM * 128) + sub, 16, 1024);
-                                const uint64_t db =
-                                    ptx::sw128_desc(kbase + (blk - u * p.kb) * (32 * 128) + sub, 16, 1024);
+                            const uint64_t dks = dk0 + static_cast<uint64_t>((ks * lay.kstage) >> 4);
+                            const int k_lo = u * p.kb * 4;
+                            const int k_n = min(p.qk_steps - k_lo, p.kb * 4);
+#pragma unroll 8
+                            for (int e = 0; e < k_n; ++e) {
+                                const int kk = k_lo + e;
+                                const uint64_t da = dq0 + static_cast<uint64_t>(((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4);
+                                const uint64_t db = dks + static_cast<uint64_t>(((e >> 2) * (32 * 128) + (e & 3) * 32) >> 4);
                                 ptx::mma2_ss(tmem, da, db, idesc_qk, kk != 0);
                             }
                             ptx::mma_commit_2sm(&bars->k_empty[ks], 0x3);
                             if (u == p.nkst - 1) ptx::mma_commit_2sm(&bars->s_full, 0x3);
                         }
                         __syncwarp();
+                        if (++ks == p.kst) {
+                            ks = 0;
+                            kph ^= 1;
+                        }
                     }
                 }
                 if (t > 0) {
-                    const int tt = t - 1, ps = tt / ntiles, jj = tt % ntiles;
+                    const int tt = t - 1;
+                    if (++jj == ntiles) {
+                        jj = 0;
+                        ps_prev = 1;
+                    }
+                    const int ps = ps_prev;
                     const uint32_t idesc_a = ptx::idesc_bf16(256, p.na[ps], false, true);
                     const uint32_t idesc_b = ptx::idesc_bf16(256, p.nb[ps] > 0 ? p.nb[ps] : 16, false, true);
                     const uint32_t boxb = p.vkeys * 128;
+                    const uint32_t oa = tmem + p.ob[ps], obb = oa + p.na[ps];
+                    const bool two = p.nb[ps] > 0;
                     ptx::mbar_wait_cluster(&bars->p_full, tt & 1);
-                    for (int h2 = 0; h2 < slices; ++h2, ++vn) {
-                        const int vs = vn % p.vst;
-                        ptx::mbar_wait(&bars->v_full[vs], (vn / p.vst) & 1);
+                    for (int h2 = 0; h2 < slices; ++h2) {
+                        ptx::mbar_wait(&bars->v_full[vs], vph);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
+                            const uint32_t vb0 = v_base + vs * lay.vstage;
                             for (int kk = 0; kk < p.vkeys / 16; ++kk) {
                                 const uint64_t da =
                                     ptx::sw128_desc(p_base + (h2 * (p.vkeys / 16) + kk) * 32, 16, 1024);
-                                const uint32_t vb = v_base + vs * lay.vstage + kk * 2048;
+                                const uint32_t vb = vb0 + kk * 2048;
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
-                                ptx::mma2_ss(tmem + p.ob[ps], da, ptx::sw128_desc(vb, boxb, 1024), idesc_a, acc);
-                                if (p.nb[ps] > 0)
-                                    ptx::mma2_ss(tmem + p.ob[ps] + p.na[ps], da,
-                                                 ptx::sw128_desc(vb + p.boxa[ps] * boxb, boxb, 1024), idesc_b, acc);
+                                ptx::mma2_ss(oa, da, ptx::sw128_desc(vb, boxb, 1024), idesc_a, acc);
+                                if (two)
+                                    ptx::mma2_ss(obb, da, ptx::sw128_desc(vb + p.boxa[ps] * boxb, boxb, 1024),
+                                                 idesc_b, acc);
                             }
                             ptx::mma_commit_2sm(&bars->v_empty[vs], 0x3);
                         }
                         __syncwarp();
+                        if (++vs == p.vst) {
+                            vs = 0;
+                            vph ^= 1;
+                        }
                     }
                     if (ptx::elect_one()) {
                         ptx::mma_commit_2sm(&bars->pv_done, 0x3);
@@ -556,10 +577,16 @@ bool make_plan(const LayerDims& d, PassParams& p, Layout& lay) {
     p.n_qkb = (d.dqk_mma + 63) / 64;
     p.qk_steps = d.dqk_mma / 16;
     const int vboxes = std::max(p.boxa[0] + p.boxb[0], p.boxa[1] + p.boxb[1]);
-    // ring depths, preferred first
-    const int cand[][4] = {{2, 3, 32, 2}, {2, 2, 32, 2}, {2, 2, 16, 3}, {2, 2, 16, 2}, {1, 4, 16, 2},
-                           {1, 3, 16, 2}, {1, 2, 16, 2}};
-    for (const auto& cd : cand) {
+    // ring depths, preferred first: bytes in flight and few, large K stages (each stage costs a
+    // barrier round trip; 4 KB stages measured 1.3x slower than 12 KB ones at rank 3)
+    const int cand[][4] = {{3, 3, 32, 2}, {4, 2, 32, 2}, {3, 2, 32, 2}, {2, 3, 32, 2}, {2, 2, 32, 2},
+                           {2, 2, 16, 3}, {2, 2, 16, 2}, {1, 4, 16, 2}, {1, 3, 16, 2}, {1, 2, 16, 2}};
+    int forced[4] = {0, 0, 0, 0};
+    if (const char* e = std::getenv("FIPA_PASS_RING"))  // "kb,kst,vkeys,vst" (tuning experiments)
+        std::sscanf(e, "%d,%d,%d,%d", &forced[0], &forced[1], &forced[2], &forced[3]);
+    for (const auto& cd0 : cand) {
+        const int* cd = forced[0] > 0 ? forced : cd0;
+        if (cd[1] > 4 || cd[3] > 4) return false;
         const Layout l = smem_layout(p.n_qkb, cd[0], cd[1], cd[2], cd[3], vboxes);
         if (l.total + 1024 <= kSmemLimit && BM * stage_stride(d.seg) * 2 <= l.xch) {
             p.kb = cd[0];
