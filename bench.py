@@ -236,6 +236,12 @@ def run_ours(args, shape):
                            generator=torch.Generator(device=dev).manual_seed(99 + rank))
         grads = {k: torch.empty_like(t[k]) for k in ("s", "z1", "z2", "rot", "trans")}
         gw = torch.empty(model.num_weights(), dtype=torch.float32, device=dev)
+    # data parallel over samples: the training step ends with the weight-gradient all-reduce
+    # (SURVEY.md §8(e)(1)), issued by the library's own NCCL communicator on the step's stream
+    comm = None
+    if train and world > 1:
+        from paper_2505_11580_b200 import sharding
+        comm = sharding.make_comm(fipa, local)
     p = {k: v.data_ptr() for k, v in t.items()}
 
     def step():
@@ -249,6 +255,8 @@ def run_ours(args, shape):
                               dout.data_ptr(), grads["s"].data_ptr(), grads["z1"].data_ptr(),
                               grads["z2"].data_ptr(), grads["rot"].data_ptr(), grads["trans"].data_ptr(),
                               gw.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream)
+        if comm is not None:
+            comm.all_reduce_sum_f32(gw.data_ptr(), gw.numel(), stream.cuda_stream)
 
     for _ in range(args.warmup):
         step()
@@ -367,7 +375,8 @@ def run_ours(args, shape):
             "dtype": args.precision, "data": "synthetic (reference input distribution), random-init weights",
             "config": {"workload": f"FlashIPA layer {args.pass_}, B={B} L={L} per GPU (BASELINE cfg2)",
                        "pass": args.pass_, "model": "FlashIPA layer", "global_batch": B * world, "seq_len": L,
-                       "shape": shape, "parallelism": f"dp{world} (independent samples)",
+                       "shape": shape, "parallelism": (f"dp{world} (samples sharded, weight-gradient all-reduce)" if train and world > 1
+                                       else f"dp{world} (independent samples)"),
                        "l2": "flushed (256 MiB write) before every timed step"},
             "attn_tflops": achieved,
             "attn_bwd_tflops": achieved_bwd,
@@ -562,7 +571,8 @@ def run_trunk(args, shape):
             "config": {"workload": f"{args.trunk}-layer FlashIPA trunk forward with per-layer backbone frame update, "
                                    f"B={B} L={L} per GPU (BASELINE cfg3)", "pass": "fwd", "model": "FlashIPA trunk",
                        "global_batch": B * world, "seq_len": L, "layers": args.trunk, "shape": shape,
-                       "parallelism": f"dp{world} (independent samples)",
+                       "parallelism": (f"dp{world} (samples sharded, weight-gradient all-reduce)" if train and world > 1
+                                       else f"dp{world} (independent samples)"),
                        "l2": "flushed (256 MiB write) before every timed step"},
             "attn_tflops_whole_trunk": tflops,
             "roofline": {"bound": "tensor", "kernel": "whole trunk step (attention-dominated)", "achieved": tflops,

@@ -106,6 +106,37 @@ int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L, const doubl
                             const double* z1, const double* z2, const double* rot,
                             const double* trans, const uint8_t* mask, double* out);
 
+/* ------------------------------------------------------------ quadratic-memory arm (f3)
+ * The reference's dense forward (reference_forward, src/ipa.cpp:244-310; Python Model.reference,
+ * python/bindings.cpp:187-189): materialises the pair tensor z [B,L,L,d_z] and the logits /
+ * attention [B,H,L,L] on the GPU in fp32 -- the O(L^2) baseline the linear-memory path replaces
+ * (paper Fig. 2).  Same buffers and conventions as fipa_layer_forward; any precision. */
+size_t fipa_layer_reference_workspace_size(const fipa_layer* layer, int64_t B, int64_t L);
+int fipa_layer_reference_forward(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                                 const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                                 float* out, void* workspace, size_t workspace_bytes, void* stream);
+int fipa_layer_reference_host(fipa_layer* layer, int64_t B, int64_t L, const double* s, const double* z1,
+                              const double* z2, const double* rot, const double* trans, const uint8_t* mask,
+                              double* out);
+
+/* ------------------------------------------------------------ generic attention
+ * include/fipa/attention_kernel.hpp:17-41: softmax(q k^T) v, no internal scaling (callers fold
+ * it into q or k), key mask [L] (1 = valid) or NULL, rows without a valid key are zeros.
+ * q, k [H, L, d_qk]; v, out [H, L, d_v]; fp32 device buffers.
+ *   fipa_naive_attention   naive_attention   src/attention_kernel.cpp:192-211 (logits [H,L,L]
+ *                          in the workspace: fipa_naive_attention_workspace_size bytes)
+ *   fipa_flash_attention   flash_attention   src/attention_kernel.cpp:213-243 (O(L) memory)
+ *   fipa_attention_host    python/bindings.cpp:153-165 (host float64 in/out, naive != 0 selects
+ *                          the dense path; runs synchronously on `device`) */
+size_t fipa_naive_attention_workspace_size(int64_t H, int64_t L);
+int fipa_naive_attention(int64_t H, int64_t L, int64_t dqk, int64_t dv, const float* q, const float* k,
+                         const float* v, const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                         void* stream);
+int fipa_flash_attention(int64_t H, int64_t L, int64_t dqk, int64_t dv, const float* q, const float* k,
+                         const float* v, const uint8_t* mask, float* out, void* stream);
+int fipa_attention_host(int64_t H, int64_t L, int64_t dqk, int64_t dv, const double* q, const double* k,
+                        const double* v, const uint8_t* mask, double* out, int naive, int device);
+
 /* Byte offsets of the forward's intermediates inside the workspace (for parity tests and
  * for a caller-driven backward), -1 when absent for this precision, in the order:
  *   0 trans_c (recentred translations, f32 [B,L,3])   1 s_bf16 (bf16 [B,L,d_in])
@@ -159,6 +190,9 @@ typedef struct fipa_comm fipa_comm;
 int fipa_comm_unique_id(uint8_t out[128]);
 int fipa_comm_create(int world, int rank, const uint8_t id[128], int device, fipa_comm** out);
 void fipa_comm_destroy(fipa_comm* comm);
+/* In-place sum of a device float buffer over the communicator's ranks, on `stream`: the
+ * data-parallel (batch-sharded) training step's weight-gradient all-reduce. */
+int fipa_comm_all_reduce_f32(fipa_comm* comm, float* buf, size_t n, void* stream);
 size_t fipa_layer_sharded_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_local, int world);
 int fipa_layer_forward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_local, const float* s,
                                const float* z1, const float* z2, const float* rot, const float* trans,

@@ -6,7 +6,9 @@
     out = model.flash(s, z1, z2, rotations, translations, mask=None)
 
 `Model` mirrors the reference binding (proj/python/bindings.cpp:180-195): same constructor
-arguments and defaults, `.flash`, `.save`, `.load`, same exception types.  Additive: a leading
+arguments and defaults, `.flash`, `.reference` (the quadratic-memory arm), `.save`, `.load`,
+same exception types; module functions `flash_attention`, `naive_attention`, `knn_distogram`,
+`build_factors` as in the reference module.  Additive: a leading
 batch axis, `enforce_head_cap` and `precision="bf16"` (tcgen05 tensor-core path; "f32"/"f64"
 select the fp32 path).  All compute runs in the sm_100a kernels of libfipa_b200.so through the
 C ABI (include/fipa_b200.h); there is no CPU fallback -- importing without the built extension
@@ -21,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 try:
     from ._fipa_b200 import (Comm, Model, Trunk, build_factors, comm_unique_id,  # noqa: F401  (native, in-tree)
-                             knn_distogram)
+                             flash_attention, knn_distogram, naive_attention)
 except ImportError as exc:  # fail loudly: the product has no Python fallback
     raise ImportError(
         "paper_2505_11580_b200 native extension is not built; run "
@@ -30,4 +32,5 @@ except ImportError as exc:  # fail loudly: the product has no Python fallback
 
 LIB_PATH = os.path.join(_HERE, "libfipa_b200.so")
 
-__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "knn_distogram", "build_factors", "LIB_PATH"]
+__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "knn_distogram", "build_factors", "flash_attention",
+           "naive_attention", "LIB_PATH"]

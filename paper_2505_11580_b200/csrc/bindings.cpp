@@ -58,6 +58,39 @@ int parse_precision(const std::string& name) {
 
 const char* kNames[10] = {"w_q", "w_k", "w_v", "w_qp", "w_kp", "w_vp", "w_bias", "gamma_raw", "w_out", "b_out"};
 
+
+// flash_attention / naive_attention (python/bindings.cpp:153-165, 202-220): q, k [L, d] or
+// [H, L, d], v [L, d_v] or [H, L, d_v]; the output matches v's leading shape.
+py::array_t<double> py_attention(const DArr& q, const DArr& k, const DArr& v, const py::object& mask, bool naive) {
+    if (q.ndim() != k.ndim() || q.ndim() != v.ndim()) throw FipaValueError("attention operands must share rank");
+    if (q.ndim() != 2 && q.ndim() != 3) throw FipaValueError("attention operands are [L, d] or [H, L, d]");
+    const bool heads = q.ndim() == 3;
+    const int a0 = heads ? 1 : 0;
+    const int64_t H = heads ? q.shape(0) : 1, L = q.shape(a0), dqk = q.shape(a0 + 1), dv = v.shape(a0 + 1);
+    if (heads && (k.shape(0) != H || v.shape(0) != H)) throw FipaValueError("attention operands must share the head count");
+    if (k.shape(a0) != L || v.shape(a0) != L) throw FipaValueError("attention operands must share the sequence length");
+    if (k.shape(a0 + 1) != dqk) throw FipaValueError("Q and K widths differ");
+    std::vector<uint8_t> m;
+    if (!mask.is_none()) {
+        py::array_t<uint8_t, py::array::c_style | py::array::forcecast> ma(mask);
+        if (ma.size() != L) throw FipaValueError("mask length must equal the sequence length");
+        m.assign(ma.data(), ma.data() + ma.size());
+        for (auto& x : m) x = x ? 1 : 0;
+    }
+    std::vector<py::ssize_t> shape = heads ? std::vector<py::ssize_t>{H, L, dv} : std::vector<py::ssize_t>{L, dv};
+    py::array_t<double> out(shape);
+    if (L == 0 || dv == 0) return out;
+    double* op = out.mutable_data();
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = fipa_attention_host(H, L, dqk, dv, q.data(), k.data(), v.data(), m.empty() ? nullptr : m.data(), op,
+                                 naive ? 1 : 0, 0);
+    }
+    check(rc);
+    return out;
+}
+
 // NCCL communicator for query-row sharding (one per process / GPU).
 class Comm {
 public:
@@ -77,6 +110,14 @@ public:
     Comm(const Comm&) = delete;
     Comm& operator=(const Comm&) = delete;
     fipa_comm* get() const { return comm_; }
+    void all_reduce_sum_f32(uintptr_t buf, size_t n, uintptr_t stream) {
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_comm_all_reduce_f32(comm_, reinterpret_cast<float*>(buf), n, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
     int world() const { return world_; }
     int rank() const { return rank_; }
 
@@ -135,6 +176,34 @@ public:
                               size_t tile_cols, int threads) {
         if (tile_rows == 0 || tile_cols == 0) throw FipaValueError("tile sizes must be positive");
         (void)threads;
+        return run_host(s, z1, z2, rotations, translations, mask, false);
+    }
+
+    // Quadratic-memory forward (python/bindings.cpp:187-189 `reference`), on the GPU in fp32.
+    py::array_t<double> reference(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
+                                  const DArr& translations, const py::object& mask) {
+        return run_host(s, z1, z2, rotations, translations, mask, true);
+    }
+    size_t reference_workspace_size(int64_t B, int64_t L) const {
+        return fipa_layer_reference_workspace_size(layer_, B, L);
+    }
+    void reference_device(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
+                          uintptr_t trans, uintptr_t mask, uintptr_t out, uintptr_t ws, size_t ws_bytes,
+                          uintptr_t stream) {
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_reference_forward(layer_, B, L, reinterpret_cast<const float*>(s),
+                                              reinterpret_cast<const float*>(z1), reinterpret_cast<const float*>(z2),
+                                              reinterpret_cast<const float*>(rot), reinterpret_cast<const float*>(trans),
+                                              reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(out),
+                                              reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+
+    py::array_t<double> run_host(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
+                                 const DArr& translations, const py::object& mask, bool dense) {
         const bool batched = s.ndim() == 3;
         if (s.ndim() != 2 && s.ndim() != 3)
             throw FipaValueError("single representation must be [L, d_in] or [B, L, d_in]");
@@ -175,8 +244,10 @@ public:
         int rc;
         {
             py::gil_scoped_release nogil;
-            rc = fipa_layer_forward_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
-                                         translations.data(), mp, op);
+            rc = dense ? fipa_layer_reference_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                                   translations.data(), mp, op)
+                       : fipa_layer_forward_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                                 translations.data(), mp, op);
         }
         check(rc);
         return out;
@@ -529,10 +600,30 @@ PYBIND11_MODULE(_fipa_b200, m) {
           "k-NN distogram + offset encoding of each residue (reference knn_distogram), on the GPU");
     m.def("build_factors", &build_factors, py::arg("features"), py::arg("r"), py::arg("d_z"), py::arg("w1"),
           py::arg("w2"), py::arg("precision") = "bf16", "z1, z2 = features.w1, features.w2 on the GPU");
+    m.def(
+        "flash_attention",
+        [](const DArr& q, const DArr& k, const DArr& v, const py::object& mask, size_t tile_rows, size_t tile_cols,
+           int threads) {
+            if (tile_rows == 0 || tile_cols == 0) throw FipaValueError("tile sizes must be positive");
+            (void)threads;
+            return py_attention(q, k, v, mask, false);
+        },
+        py::arg("q"), py::arg("k"), py::arg("v"), py::arg("mask") = py::none(), py::arg("tile_rows") = 64,
+        py::arg("tile_cols") = 64, py::arg("threads") = 1,
+        "Online-softmax attention on the GPU, O(L) memory (callers pre-scale their logits)");
+    m.def(
+        "naive_attention",
+        [](const DArr& q, const DArr& k, const DArr& v, const py::object& mask) {
+            return py_attention(q, k, v, mask, true);
+        },
+        py::arg("q"), py::arg("k"), py::arg("v"), py::arg("mask") = py::none(),
+        "Dense softmax attention on the GPU (materialises the [H, L, L] logits)");
     m.def("comm_unique_id", &comm_unique_id, "128-byte NCCL unique id (rank 0 creates, all ranks share)");
     py::class_<Comm>(m, "Comm", "NCCL communicator for query-row sharding (one process per GPU)")
         .def(py::init<int, int, const py::bytes&, int>(), py::arg("world"), py::arg("rank"), py::arg("unique_id"),
              py::arg("device"))
+        .def("all_reduce_sum_f32", &Comm::all_reduce_sum_f32, py::arg("buf"), py::arg("n"), py::arg("stream") = 0,
+             "In-place sum of a device float buffer (pointer) over the ranks, on `stream`")
         .def_property_readonly("world", &Comm::world)
         .def_property_readonly("rank", &Comm::rank);
 
@@ -546,6 +637,13 @@ PYBIND11_MODULE(_fipa_b200, m) {
              py::arg("translations"), py::arg("mask") = py::none(), py::arg("tile_rows") = 64,
              py::arg("tile_cols") = 64, py::arg("threads") = 1,
              "Linear-memory FlashIPA forward on the GPU")
+        .def("reference", &Model::reference, py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rotations"),
+             py::arg("translations"), py::arg("mask") = py::none(),
+             "Quadratic-memory forward pass (dense pair tensor, fp32 on the GPU)")
+        .def("reference_workspace_size", &Model::reference_workspace_size, py::arg("B"), py::arg("L"))
+        .def("reference_device", &Model::reference_device, py::arg("B"), py::arg("L"), py::arg("s"), py::arg("z1"),
+             py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("out"), py::arg("workspace"),
+             py::arg("workspace_bytes"), py::arg("stream") = 0)
         .def("save", &Model::save, py::arg("path"), "Write weights to a binary file")
         .def("load", &Model::load, py::arg("path"), "Replace weights from a binary file")
         .def("weights", &Model::weights, "Master weights as a dict of float64 arrays")

@@ -209,6 +209,106 @@ int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L_, const doub
     });
 }
 
+size_t fipa_layer_reference_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_) {
+    if (layer == nullptr || B < 1 || L_ < 1) return 0;
+    return layer->impl->reference_workspace_size(B, L_);
+}
+
+int fipa_layer_reference_forward(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                                 const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                                 float* out, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        L(layer).reference_forward(B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
+                                   static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_layer_reference_host(fipa_layer* layer, int64_t B, int64_t L_, const double* s, const double* z1,
+                              const double* z2, const double* rot, const double* trans, const uint8_t* mask,
+                              double* out) {
+    return guarded([&] {
+        if (!s || !z1 || !z2 || !rot || !trans || !out) throw fipa_b200::ValueError("null buffer");
+        L(layer).reference_host(B, L_, s, z1, z2, rot, trans, mask, out);
+    });
+}
+
+size_t fipa_naive_attention_workspace_size(int64_t H, int64_t L_) {
+    if (H < 1 || L_ < 1) return 0;
+    return size_t(H) * size_t(L_) * size_t(L_) * sizeof(float);
+}
+
+namespace {
+void check_attention_dims(int64_t H, int64_t L_, int64_t dqk, int64_t dv) {
+    if (H < 1 || dqk < 1 || dv < 1) throw fipa_b200::ValueError("attention operands need positive sizes");
+    if (L_ < 1) throw fipa_b200::ValueError("attention operands need L >= 1");
+    if (H > 65535 || L_ > (int64_t(1) << 31) / 64 || dqk > (1 << 20) || dv > (1 << 20))
+        throw fipa_b200::ValueError("attention operands too large");
+}
+}  // namespace
+
+int fipa_naive_attention(int64_t H, int64_t L_, int64_t dqk, int64_t dv, const float* q, const float* k,
+                         const float* v, const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+    return guarded([&] {
+        check_attention_dims(H, L_, dqk, dv);
+        if (!q || !k || !v || !out) throw fipa_b200::ValueError("null buffer");
+        if (!workspace || workspace_bytes < fipa_naive_attention_workspace_size(H, L_))
+            throw fipa_b200::ValueError("naive attention workspace too small");
+        fipa_b200::launch_naive_attention_f32(int(H), int(L_), int(dqk), int(dv), q, k, v, mask,
+                                              static_cast<float*>(workspace), out, static_cast<cudaStream_t>(stream));
+        fipa_b200::cuda_check(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int fipa_flash_attention(int64_t H, int64_t L_, int64_t dqk, int64_t dv, const float* q, const float* k,
+                         const float* v, const uint8_t* mask, float* out, void* stream) {
+    return guarded([&] {
+        check_attention_dims(H, L_, dqk, dv);
+        if (!q || !k || !v || !out) throw fipa_b200::ValueError("null buffer");
+        fipa_b200::launch_flash_attention_f32(int(H), int(L_), int(dqk), int(dv), q, k, v, mask, out,
+                                              static_cast<cudaStream_t>(stream));
+        fipa_b200::cuda_check(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int fipa_attention_host(int64_t H, int64_t L_, int64_t dqk, int64_t dv, const double* q, const double* k,
+                        const double* v, const uint8_t* mask, double* out, int naive, int device) {
+    return guarded([&] {
+        check_attention_dims(H, L_, dqk, dv);
+        if (!q || !k || !v || !out) throw fipa_b200::ValueError("null buffer");
+        using fipa_b200::cuda_check;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        const size_t nq = size_t(H) * L_ * dqk, nv = size_t(H) * L_ * dv;
+        const size_t ws = naive ? fipa_naive_attention_workspace_size(H, L_) : 0;
+        std::vector<float> h(2 * nq + 2 * nv);
+        for (size_t i = 0; i < nq; ++i) h[i] = float(q[i]);
+        for (size_t i = 0; i < nq; ++i) h[nq + i] = float(k[i]);
+        for (size_t i = 0; i < nv; ++i) h[2 * nq + i] = float(v[i]);
+        char* d = nullptr;
+        const size_t bytes = h.size() * 4 + size_t(L_) + ws + 256;
+        cuda_check(cudaMalloc(&d, bytes), "cudaMalloc");
+        std::unique_ptr<char, void (*)(char*)> guard(d, [](char* p) { cudaFree(p); });
+        float* dq = reinterpret_cast<float*>(d);
+        float* dk = dq + nq;
+        float* dvv = dk + nq;
+        float* dout = dvv + nv;
+        uint8_t* dm = reinterpret_cast<uint8_t*>(dout + nv);
+        void* dws = d + ((h.size() * 4 + size_t(L_) + 255) / 256 * 256);
+        cuda_check(cudaMemcpy(d, h.data(), (2 * nq + nv) * 4, cudaMemcpyHostToDevice), "H2D");
+        if (mask) cuda_check(cudaMemcpy(dm, mask, size_t(L_), cudaMemcpyHostToDevice), "H2D");
+        if (naive) {
+            fipa_b200::launch_naive_attention_f32(int(H), int(L_), int(dqk), int(dv), dq, dk, dvv, mask ? dm : nullptr,
+                                                  static_cast<float*>(dws), dout, nullptr);
+        } else {
+            fipa_b200::launch_flash_attention_f32(int(H), int(L_), int(dqk), int(dv), dq, dk, dvv, mask ? dm : nullptr,
+                                                  dout, nullptr);
+        }
+        cuda_check(cudaGetLastError(), "kernel launch");
+        cuda_check(cudaMemcpy(h.data(), dout, nv * 4, cudaMemcpyDeviceToHost), "D2H");
+        for (size_t i = 0; i < nv; ++i) out[i] = double(h[i]);
+    });
+}
+
 int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L_, int64_t* offsets,
                                 int64_t* dims) {
     if (layer == nullptr || offsets == nullptr || B < 1 || L_ < 1) return 0;
@@ -339,6 +439,14 @@ int fipa_comm_create(int world, int rank, const uint8_t id[128], int device, fip
 }
 
 void fipa_comm_destroy(fipa_comm* comm) { delete comm; }
+
+int fipa_comm_all_reduce_f32(fipa_comm* comm, float* buf, size_t n, void* stream) {
+    return guarded([&] {
+        if (comm == nullptr) throw fipa_b200::ValueError("null fipa_comm");
+        if (buf == nullptr && n > 0) throw fipa_b200::ValueError("null buffer");
+        if (n > 0) comm->impl.all_reduce_sum_f32(buf, n, static_cast<cudaStream_t>(stream));
+    });
+}
 
 size_t fipa_layer_sharded_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_, int world) {
     if (layer == nullptr || B < 1 || L_ < 1 || world < 1) return 0;

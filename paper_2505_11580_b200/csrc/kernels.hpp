@@ -241,4 +241,40 @@ struct AttnF32Args {
 };
 void launch_attn_fwd_f32(const LayerDims& d, const AttnF32Args& a, cudaStream_t stream);
 
+// ------------------------------------------------ quadratic-memory arms (dense.cu)
+// Dense IPA forward (reference_forward, proj/src/ipa.cpp:244-310), fp32: materialises the pair
+// tensor z [B, L, L, d_z] and the logits / attention [B, H, L, L].
+struct DenseArgs {
+    int B, L;
+    const float* s;
+    const float* z1;
+    const float* z2;
+    const float* rot;
+    const float* trans;     // not recentred: differences are formed directly
+    const uint8_t* mask;    // [BL] or null
+    const float* wproj;     // f32 [d_in, n_proj]
+    const float* wout;      // f32 [feat, d_in]
+    const float* bout;
+    const float* head_g;
+    const float* wl_bias;
+    float k_scale;
+    float* proj;            // [BL, n_proj]
+    float* gq;              // [BL, H*Nq*3] global query points
+    float* gk;              // [BL, H*Nq*3]
+    float* vcat;            // [B, H, L, c + 3Nv]  v | T_j v_p
+    float* z;               // [B, L, L, d_z]
+    float* logits;          // [B, H, L, L] (softmax in place)
+    float* ov;              // [B, H, L, c + 3Nv]
+    float* oz;              // [BL, H, d_z]
+    float* feat;            // [BL, feat]
+    float* out;             // [BL, d_in]
+};
+void launch_dense_ipa(const LayerDims& d, const DenseArgs& a, cudaStream_t stream);
+// Generic attention (attention_kernel.hpp): q, k [H, L, d_qk], v [H, L, d_v], key mask [L].
+void launch_naive_attention_f32(int H, int L, int dqk, int dv, const float* q, const float* k, const float* v,
+                                const uint8_t* mask, float* logits, float* out, cudaStream_t stream);
+bool flash_attention_f32_supported(int dv);
+void launch_flash_attention_f32(int H, int L, int dqk, int dv, const float* q, const float* k, const float* v,
+                                const uint8_t* mask, float* out, cudaStream_t stream);
+
 }  // namespace fipa_b200

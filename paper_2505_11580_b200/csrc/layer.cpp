@@ -494,7 +494,8 @@ void FlashIpaLayer::upload_weights() {
             for (std::size_t c = 0; c < din; ++c)
                 o[c * fld + r] = __float2bfloat16_rn(static_cast<float>(w_.w_out[r * din + c]));
         up(&d_wout_t_, o);
-    } else {
+    }
+    {  // fp32 copies: the f32 path, and the quadratic-memory arm (reference_forward) at any precision
         std::vector<float> t(wproj.begin(), wproj.end());
         up(&d_wproj_, t);
         std::vector<float> o(w_.w_out.begin(), w_.w_out.end());
@@ -788,6 +789,20 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
 void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
                                  const double* z2, const double* rot, const double* trans,
                                  const std::uint8_t* mask, double* out) {
+    run_host(B, L, s, z1, z2, rot, trans, mask, out, false);
+}
+
+void FlashIpaLayer::reference_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
+                                   const double* z2, const double* rot, const double* trans,
+                                   const std::uint8_t* mask, double* out) {
+    run_host(B, L, s, z1, z2, rot, trans, mask, out, true);
+}
+
+// Host buffers in, host buffers out (the reference calling convention): threaded float64 -> float32
+// conversion overlapped with the per-tensor copies, one device pass, copy back.
+void FlashIpaLayer::run_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
+                             const double* z2, const double* rot, const double* trans,
+                             const std::uint8_t* mask, double* out, bool dense) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -797,7 +812,7 @@ void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s
     const std::size_t n_s = BL * cfg_.d_in, n_z = BL * rdz, n_r = BL * 9, n_t = BL * 3;
     const std::size_t n_in = n_s + 2 * n_z + n_r + n_t, n_out = BL * cfg_.d_in;
     const std::size_t io_bytes = round_up((n_in + n_out) * 4 + BL, 256);
-    const std::size_t ws_bytes = workspace_size(B, L);
+    const std::size_t ws_bytes = dense ? reference_workspace_size(B, L) : workspace_size(B, L);
     if (h_stage_bytes_ < io_bytes) {
         if (h_stage_) cudaFreeHost(h_stage_);
         h_stage_ = nullptr;
@@ -824,15 +839,100 @@ void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s
     std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
     if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
     void* ws = static_cast<char*>(d_stage_) + io_bytes;
-    forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
-            dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
-            own_stream_);
+    if (dense) {
+        reference_forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
+                          dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
+                          own_stream_);
+    } else {
+        forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
+                dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
+                own_stream_);
+    }
     cuda_check(cudaMemcpyAsync(h + n_in, dbase + n_in, n_out * 4, cudaMemcpyDeviceToHost, own_stream_),
                "D2H");
     cuda_check(cudaStreamSynchronize(own_stream_), "forward");
     convert(out, h + n_in, n_out);
 }
 
+
+// ------------------------------------------------------------ quadratic-memory arm
+namespace {
+struct DenseLayout {
+    std::size_t proj, gq, gk, vcat, z, logits, ov, oz, feat, bytes;
+};
+DenseLayout dense_layout(const LayerDims& d, std::int64_t B, std::int64_t L) {
+    DenseLayout l{};
+    std::size_t off = 0;
+    auto take = [&](std::size_t floats) {
+        const std::size_t o = off;
+        off += round_up(floats * 4, 256);
+        return o;
+    };
+    const std::size_t BL = std::size_t(B) * L, H = d.heads, vw = d.c + 3 * d.n_value;
+    l.proj = take(BL * d.n_proj);
+    l.gq = take(BL * H * d.n_query * 3);
+    l.gk = take(BL * H * d.n_query * 3);
+    l.vcat = take(BL * H * vw);
+    l.z = take(BL * std::size_t(L) * d.d_z);
+    l.logits = take(BL * H * std::size_t(L));
+    l.ov = take(BL * H * vw);
+    l.oz = take(BL * H * d.d_z);
+    l.feat = take(BL * d.feat);
+    l.bytes = off;
+    return l;
+}
+}  // namespace
+
+std::size_t FlashIpaLayer::reference_workspace_size(std::int64_t B, std::int64_t L) const {
+    return dense_layout(dims_, B, L).bytes;
+}
+
+void FlashIpaLayer::reference_forward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                      const float* z2, const float* rot, const float* trans,
+                                      const std::uint8_t* mask, float* out, void* workspace,
+                                      std::size_t workspace_bytes, cudaStream_t stream) {
+    REQUIRE(B >= 1, "batch must be >= 1");
+    REQUIRE(L >= 1, "empty frame set");
+    REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
+    REQUIRE(B * L <= std::int64_t(1) << 31 && L <= 65535, "dense arm: B*L or L too large");
+    const DenseLayout lay = dense_layout(dims_, B, L);
+    REQUIRE(workspace != nullptr && workspace_bytes >= lay.bytes, "reference workspace too small: need ",
+            lay.bytes, " bytes");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (dirty_) {
+        std::lock_guard<std::mutex> lk(upload_mu_);
+        if (dirty_) upload_weights();
+    }
+    char* base = static_cast<char*>(workspace);
+    auto at = [&](std::size_t o) { return reinterpret_cast<float*>(base + o); };
+    DenseArgs a{};
+    a.B = int(B);
+    a.L = int(L);
+    a.s = s;
+    a.z1 = z1;
+    a.z2 = z2;
+    a.rot = rot;
+    a.trans = trans;
+    a.mask = mask;
+    a.wproj = d_wproj_;
+    a.wout = d_wout_;
+    a.bout = d_bout_;
+    a.head_g = d_head_g_;
+    a.wl_bias = d_wl_bias_;
+    a.k_scale = k_scale_;
+    a.proj = at(lay.proj);
+    a.gq = at(lay.gq);
+    a.gk = at(lay.gk);
+    a.vcat = at(lay.vcat);
+    a.z = at(lay.z);
+    a.logits = at(lay.logits);
+    a.ov = at(lay.ov);
+    a.oz = at(lay.oz);
+    a.feat = at(lay.feat);
+    a.out = out;
+    launch_dense_ipa(dims_, a, stream);
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
 
 void FlashIpaLayer::ensure_staging(std::size_t host_bytes, std::size_t dev_bytes) {
     if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");

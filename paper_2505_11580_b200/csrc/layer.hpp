@@ -152,6 +152,14 @@ public:
                       const std::uint8_t* mask, double* out);
     int launches_per_forward() const;
 
+    // Quadratic-memory arm (reference_forward, proj/src/ipa.cpp:244-310; dense.cu), fp32.
+    std::size_t reference_workspace_size(std::int64_t B, std::int64_t L) const;
+    void reference_forward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                           const float* rot, const float* trans, const std::uint8_t* mask, float* out,
+                           void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+    void reference_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
+                        const double* rot, const double* trans, const std::uint8_t* mask, double* out);
+
     void set_timing(bool on);
     std::vector<float> stage_times() const;
 
@@ -229,6 +237,8 @@ private:
     void* d_stage_ = nullptr;
     std::size_t d_stage_bytes_ = 0;
     void ensure_staging(std::size_t host_bytes, std::size_t dev_bytes);
+    void run_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
+                  const double* rot, const double* trans, const std::uint8_t* mask, double* out, bool dense);
     cudaStream_t own_stream_ = nullptr;
     // timing
     bool timing_ = false;

@@ -59,7 +59,8 @@ def test_c_abi_config_and_errors(fipa):
     assert lib.fipa_layer_create(ctypes.byref(cfg), ctypes.byref(handle)) == 0
     lib.fipa_layer_workspace_size.restype = ctypes.c_size_t
     assert lib.fipa_layer_workspace_size(handle, ctypes.c_int64(2), ctypes.c_int64(100)) > 0
-    assert lib.fipa_layer_forward_launches(handle) == 6
+    # fused projection+pack (proj_pack.cu) -> attention -> output GEMM (+ recentre, cast)
+    assert lib.fipa_layer_forward_launches(handle) == (6 if os.environ.get("FIPA_FUSED_PACK") == "0" else 5)
     lib.fipa_layer_destroy(handle)
 
 
@@ -134,3 +135,16 @@ def test_workspace_layout_is_consistent(fipa):
     mf = fipa.Model(**MAIN, precision="f32", enforce_head_cap=False)
     off32, _ = mf.workspace_layout(2, 64)
     assert off32[1] == -1  # no bf16 cast buffer on the fp32 path
+
+
+def test_quadratic_arm_workspace_is_quadratic_and_flash_linear(fipa):
+    """Memory model of the two arms (reference bench.cpp:151-155 estimate_reference_bytes and the
+    paper's Fig. 2): the dense arm's workspace grows as (d_z + H) L^2, the flash workspace as L."""
+    model = fipa.Model(**MAIN, precision="bf16", seed=0, enforce_head_cap=False)
+    L0 = 8192
+    d1, d2 = model.reference_workspace_size(1, L0), model.reference_workspace_size(1, 2 * L0)
+    f1, f2 = model.workspace_size(1, L0), model.workspace_size(1, 2 * L0)
+    assert 3.95 < d2 / d1 < 4.01
+    assert 1.9 < f2 / f1 < 2.01
+    quad = (MAIN["d_z"] + MAIN["heads"]) * (2 * L0) ** 2 * 4
+    assert 0.95 < quad / d2 <= 1.0

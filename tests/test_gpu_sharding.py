@@ -21,11 +21,12 @@ def _dev(batch):
     return t
 
 
-@pytest.mark.parametrize("G,B", [(2, 1), (4, 2)])
-def test_emulated_shards_match_unsharded_forward(fipa, G, B):
-    model = fipa.Model(**MAIN, precision="bf16", seed=3, enforce_head_cap=False)
+@pytest.mark.parametrize("G,B,rank", [(2, 1, 2), (4, 2, 2), (2, 1, 3)])
+def test_emulated_shards_match_unsharded_forward(fipa, G, B, rank):
+    shape = dict(MAIN, rank=rank)  # rank 3: the two-pass attention kernel reads the sharded keys
+    model = fipa.Model(**shape, precision="bf16", seed=3, enforce_head_cap=False)
     L = 128 * G
-    batch = make_batch(MAIN, B, L, seed=31, mask_frac=0.1, bf16=True)
+    batch = make_batch(shape, B, L, seed=31, mask_frac=0.1, bf16=True)
     ref_gpu, _, _ = gpu_forward_device(model, batch)
     t = _dev(batch)
     st = torch.cuda.current_stream().cuda_stream
@@ -60,8 +61,17 @@ def test_emulated_shards_match_unsharded_forward(fipa, G, B):
     torch.cuda.synchronize()
     got = torch.cat(outs, 1).cpu().numpy().astype(np.float64)
     assert rel_dev(ref_gpu, got) < 1e-3  # only the centroid's summation order differs
-    ref = oracle_forward(MAIN, oracle_weights_for(model, "bf16"), batch)
+    ref = oracle_forward(shape, oracle_weights_for(model, "bf16"), batch)
     assert rel_dev(ref, got) < BF16_TOL
+
+
+def test_nccl_world1_gradient_all_reduce_is_identity(fipa):
+    comm = fipa.Comm(1, 0, fipa.comm_unique_id(), 0)
+    buf = torch.randn(1 << 20, dtype=torch.float32, device="cuda")
+    ref = buf.clone()
+    comm.all_reduce_sum_f32(buf.data_ptr(), buf.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(buf, ref)
 
 
 def test_nccl_world1_sharded_forward_equals_forward(fipa):
