@@ -238,7 +238,7 @@ size_t fipa_naive_attention_workspace_size(int64_t H, int64_t L_) {
 }
 
 namespace {
-void check_attention_dims(int64_t H, int64_t L_, int64_t dqk, int64_t dv) {
+static void check_attention_dims(int64_t H, int64_t L_, int64_t dqk, int64_t dv) {
     if (H < 1 || dqk < 1 || dv < 1) throw fipa_b200::ValueError("attention operands need positive sizes");
     if (L_ < 1) throw fipa_b200::ValueError("attention operands need L >= 1");
     if (H > 65535 || L_ > (int64_t(1) << 31) / 64 || dqk > (1 << 20) || dv > (1 << 20))
