@@ -222,246 +222,255 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
 }
 
 constexpr int kUnpackRows = 8;
+constexpr int kUnpackMaxH = 16;
 
-// Block = 8 warps, warp w handles heads w, w+8, ... of kUnpackRows consecutive residues.  The
-// residue's 3*H accumulator rows (and the point columns of its projection row) arrive by bulk
-// copies into one of two shared-memory stages while the previous residue is being processed;
-// the dproj row is assembled in shared memory and written with 16-byte stores.  Cross-head sums
-// go through shared memory; d(w_l w_bias) and d(g) are flushed with one global atomic per entry
-// per block.
-__global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a, int stage_w) {
-    extern __shared__ __align__(16) float sm[];
-    const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
-    const int nw = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int off_q = 0, off_k = H * c, off_v = 2 * H * c;
+// Lifts^T (pack.cu / proj_pack.cu reversed), in two launches so each half runs at its own
+// occupancy:
+//  bwd_unpack_geo_kernel   block = one residue, warp per head, lane per point: frame-applied point
+//                          gradients -> dproj point columns; dR, dt reduced across heads in shared
+//                          memory -> drot, dt_c; per-residue dgamma -> dg_rows [BL, H].
+//  bwd_unpack_kernel       block streams kUnpackRows residues; every accumulator column of the
+//                          scalar and pair blocks is read by exactly one thread with coalesced
+//                          loads (no staging, all loads of a residue in flight at once):
+//                          scalar q | k (x w_l/sqrt(c) ln2) | v -> bf16 pairs of the dproj row;
+//                          pair e: dz1 = dz1_epi + sum_h dq[zq+e],
+//                          dz2 = sum_h (w_l w_bias[h, e % d_z] ln2 dk[zq+e] + dv[c+e]),
+//                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials);
+//                          dg += sum of dg_rows over the block's residues.
+__global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
+    __shared__ float s_geo[kUnpackMaxH][12];
+    const int H = d.heads, c = d.c, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
-    const int npts = d.n_proj - off_qp;                       // point columns of a projection row
-    const int npts_pad = (npts + 3) & ~3;
-    const int rdz_pad = (rdz + 3) & ~3;
-    // one residue: dq|dk|dv rows, points, z2, dz1_epi, geo_epi (12)
-    const int stage_floats = 3 * H * stage_w + npts_pad + 2 * rdz_pad + 12;
-    float* s_stage = sm;                                      // 2 x stage_floats
-    float* s_pq = s_stage + 2 * stage_floats;                 // H x rdz  query-side pair grads
-    float* s_pk = s_pq + H * rdz;                             // H x rdz  key+value-side pair grads
-    float* s_geo = s_pk + H * rdz;                            // H x 12
-    float* s_dwlb = s_geo + H * 12;                           // H x dz
-    float* s_dg = s_dwlb + H * dz;                            // H
-    float* s_wlb = s_dg + H;                                  // H x dz  w_l w_bias
-    __nv_bfloat16* s_dp = reinterpret_cast<__nv_bfloat16*>((reinterpret_cast<uintptr_t>(s_wlb + H * dz) + 15) & ~uintptr_t(15));
-    uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_dp + a.nproj_ld) + 7) & ~uintptr_t(7));
-    const int g0 = c + 3 * Nq, zq = d.zq, vpair = c + rdz;
+    const int g0 = c + 3 * Nq, vpair = c + rdz;
+    const int64_t row = blockIdx.x;
+    const int64_t acc_h = a.acc_ld;
+    const float* qrow = a.dq_acc + row * H * acc_h;
+    const float* krow = a.dk_acc + row * H * acc_h;
+    const float* vrow = a.dv_acc + row * H * acc_h;
+    __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+    float R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
+    const float* pr = a.proj + row * d.n_proj;  // pr[off_qp + ...] = local point columns
+    for (int h = warp; h < H; h += (blockDim.x >> 5)) {
+        const float* qa = qrow + h * acc_h;
+        const float* ka = krow + h * acc_h;
+        const float* va = vrow + h * acc_h;
+        // every load of this head first (one memory round trip): per-head scalars, the lane's
+        // query/key point (lanes < Nq) and value point (lanes < Nv), clamped to valid addresses
+        const int pq = min(lane, Nq - 1), pv = min(lane, Nv - 1);
+        const float g = __ldg(a.head_g + h);
+        const float cs = __ldg(ka + g0 + 18);
+        const float S1 = __ldg(qa + g0 + 20);  // sum_j dS_ij, as rounded for the MMAs
+        float kw[6], kt[9], vt[3], qp[3], qc[3], qt[6], kp[3], kc[3], vp[3], dV[3];
+#pragma unroll
+        for (int x = 0; x < 6; ++x) {
+            kw[x] = __ldg(ka + g0 + 9 + x);
+            qt[x] = __ldg(qa + g0 + x);
+        }
+#pragma unroll
+        for (int x = 0; x < 9; ++x) kt[x] = __ldg(ka + g0 + x);
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            vt[x] = __ldg(va + vpair + x);
+            qp[x] = __ldg(pr + off_qp + (h * Nq + pq) * 3 + x);
+            qc[x] = __ldg(qa + c + 3 * pq + x);
+            kp[x] = __ldg(pr + off_kp + (h * Nq + pq) * 3 + x);
+            kc[x] = __ldg(ka + c + 3 * pq + x);
+            vp[x] = __ldg(pr + off_vp + (h * Nv + pv) * 3 + x);
+            dV[x] = __ldg(va + vpair + 6 + 3 * pv + x);
+        }
+        float dW[3];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (kw[x] + kw[3 + x]);
+        float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dgh = 0.f;
+        if (lane < Nq) {
+            const int p = lane;
+            // query point: A = R q_p + t,  dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS B] - g A S1
+            // (subtracting g A S1 with the same rounded dS cancels the translation-sized common
+            // mode of the first term)
+            float gB[3], A[3], dA[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) gB[x] = qc[x] + qt[x] + qt[3 + x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                dA[x] = gB[x] - g * A[x] * S1;
+                dt[x] += dA[x];
+            }
+            // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
+            dgh += (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
+                   0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                dp[off_qp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dA[0] + R[3 + x] * dA[1] + R[6 + x] * dA[2]);
+#pragma unroll
+                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
+            }
+            // key point: B = R k_p + t
+            float B[3], dB[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) B[x] = R[3 * x] * kp[0] + R[3 * x + 1] * kp[1] + R[3 * x + 2] * kp[2] + t[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                dB[x] = g * kLn2 * kc[x] + dW[x] - g * B[x] * cs;
+                dt[x] -= g * B[x] * cs;
+            }
+            dgh += -0.5f * (B[0] * B[0] + B[1] * B[1] + B[2] * B[2]) * cs;
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                dp[off_kp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dB[0] + R[3 + x] * dB[1] + R[6 + x] * dB[2]);
+#pragma unroll
+                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
+            }
+        }
+        if (lane < Nv) {
+            const int p = lane;
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                dp[off_vp + (h * Nv + p) * 3 + x] = __float2bfloat16_rn(R[x] * dV[0] + R[3 + x] * dV[1] + R[6 + x] * dV[2]);
+#pragma unroll
+                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+                dt[x] += g * kLn2 * (kt[x] + kt[6 + x]) + float(Nq) * dW[x]  // key
+                         + vt[x];                                                // value
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
+        dgh = warp_sum(dgh);
+        if (lane < 12) s_geo[h][lane] = lane < 9 ? dR[lane] : dt[lane - 9];
+        if (lane == 0) a.dg_rows[row * H + h] = dgh;
+    }
+    __syncthreads();
+    if (tid < 12) {
+        float acc = __ldg(a.geo_epi + row * 12 + tid);
+        for (int h = 0; h < H; ++h) acc += s_geo[h][tid];
+        if (tid < 9) {
+            if (a.drot != nullptr) a.drot[row * 9 + tid] = acc;
+        } else {
+            a.dt_c[row * 3 + tid - 9] = acc;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z;
+    const int tid = threadIdx.x;
+    float* s_dwlb = sm;                 // H x dz
+    float* s_wlb = s_dwlb + H * dz;     // H x dz
+    const int zq = d.zq;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
     const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
     const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
-    const bool pts_bulk = ((off_qp * 4) & 15) == 0 && ((d.n_proj * 4) & 15) == 0 && ((npts * 4) & 15) == 0 &&
-                          ((rdz * 4) & 15) == 0;
-    // d(w_l w_bias) partials live in the head's warp-private slice; lanes of one step never share
-    // a d_z index when d_z >= 32, so plain adds suffice there
-    const bool dwlb_plain = dz >= 32;
-
-    auto issue = [&](int rr) {  // thread 0: stage residue row_begin + rr into buffer rr & 1
-        const int64_t row = row_begin + rr;
-        const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
-        float* st = s_stage + (rr & 1) * stage_floats;
-        uint64_t* bar = bars + (rr & 1);
-        (void)b;
-        (void)i;
-        // accumulators are residue-major [B, L, H, acc_ld]: one copy per tensor moves all heads
-        const uint32_t rbytes = H * stage_w * 4;
-        ptx::mbar_expect_tx(bar, 3 * rbytes + (pts_bulk ? (npts + 2 * rdz + 12) * 4 : 0));
-        const int64_t arow = row * H * a.acc_ld;
-        bulk_g2s(st, a.dq_acc + arow, rbytes, bar);
-        bulk_g2s(st + H * stage_w, a.dk_acc + arow, rbytes, bar);
-        bulk_g2s(st + 2 * H * stage_w, a.dv_acc + arow, rbytes, bar);
-        if (pts_bulk) {
-            bulk_g2s(st + 3 * H * stage_w, a.proj + row * d.n_proj + off_qp, npts * 4, bar);
-            bulk_g2s(st + 3 * H * stage_w + npts_pad, a.z2 + row * rdz, rdz * 4, bar);
-            bulk_g2s(st + 3 * H * stage_w + npts_pad + rdz_pad, a.dz1_epi + row * rdz, rdz * 4, bar);
-            bulk_g2s(st + 3 * H * stage_w + npts_pad + 2 * rdz_pad, a.geo_epi + row * 12, 48, bar);
-        }
-    };
-
-    if (threadIdx.x == 0) {
-        ptx::mbar_init(&bars[0], 1);
-        ptx::mbar_init(&bars[1], 1);
-        ptx::fence_mbar_init();
-        if (nrows > 0) issue(0);
+    const int64_t acc_h = a.acc_ld;     // accumulator rows are residue-major [BL, H, acc_ld]
+    const float kscale = a.k_scale * kLn2;
+    const int half_c = c / 2;
+    const bool pairs = (c % 2) == 0 && (a.acc_ld % 2) == 0 && (a.nproj_ld % 2) == 0;
+    const bool reg_dwlb = rdz <= static_cast<int>(blockDim.x);  // one pair column per thread
+    for (int e = tid; e < H * dz; e += blockDim.x) {
+        s_dwlb[e] = 0.f;
+        s_wlb[e] = a.wl_bias[e];
     }
-    for (int e = threadIdx.x; e < H * dz + H; e += blockDim.x) s_dwlb[e] = 0.f;
-    for (int e = threadIdx.x; e < H * dz; e += blockDim.x) s_wlb[e] = a.wl_bias[e];
     __syncthreads();
+    float pw[kUnpackMaxH];  // this thread's d(w_l w_bias) partials over the block's residues
+#pragma unroll
+    for (int h = 0; h < kUnpackMaxH; ++h) pw[h] = 0.f;
 
     for (int rr = 0; rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
-        // prefetch the next residue into the other stage (freed by the previous iteration's sync)
-        if (threadIdx.x == 0 && rr + 1 < nrows) issue(rr + 1);
-        float* st = s_stage + (rr & 1) * stage_floats;
-        if (!pts_bulk) {
-            for (int e = threadIdx.x; e < npts; e += blockDim.x) st[3 * H * stage_w + e] = a.proj[row * d.n_proj + off_qp + e];
-            for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
-                st[3 * H * stage_w + npts_pad + e] = a.z2[row * rdz + e];
-                st[3 * H * stage_w + npts_pad + rdz_pad + e] = a.dz1_epi[row * rdz + e];
-            }
-            if (threadIdx.x < 12) st[3 * H * stage_w + npts_pad + 2 * rdz_pad + threadIdx.x] = a.geo_epi[row * 12 + threadIdx.x];
-        }
-        float R[9], t[3];
+        const float* qrow = a.dq_acc + row * H * acc_h;
+        const float* krow = a.dk_acc + row * H * acc_h;
+        const float* vrow = a.dv_acc + row * H * acc_h;
+        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+        // ---- pair columns
+        for (int e = tid; e < rdz; e += blockDim.x) {
+            const int dd = e % dz;
+            const float z2v = __ldg(a.z2 + row * rdz + e);
+            float s1 = __ldg(a.dz1_epi + row * rdz + e), s2 = 0.f;
+            for (int h0 = 0; h0 < H; h0 += 8) {
+                // all 24 loads of the chunk issued before any use (the compiler otherwise waits
+                // on each head's load in turn)
+                float qq[8], kq[8], vq[8];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+                for (int u = 0; u < 8; ++u) {
+                    const int h = min(h0 + u, H - 1);
+                    qq[u] = __ldg(qrow + h * acc_h + zq + e);
+                    kq[u] = __ldg(krow + h * acc_h + zq + e);
+                    vq[u] = __ldg(vrow + h * acc_h + c + e);
+                }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
-        const float* z2 = st + 3 * H * stage_w + npts_pad;
-        const float* z1e = z2 + rdz_pad;           // dz1 of the output epilogue
-        const float* epi = z1e + rdz_pad;          // dR (9) | dt (3) of the output epilogue
-        const float* pr = st + 3 * H * stage_w - off_qp;  // pr[off_qp + ...] = point columns
-        if (!pts_bulk) __syncthreads();
-        ptx::mbar_wait(&bars[rr & 1], (rr >> 1) & 1);
-        __nv_bfloat16* dp = s_dp;
-        for (int h = warp; h < H; h += nw) {
-            const float* qa = st + (0 * H + h) * stage_w;
-            const float* ka = st + (1 * H + h) * stage_w;
-            const float* va = st + (2 * H + h) * stage_w;
-            // scalar channels (bf16 pairs into the staged dproj row)
-            for (int c2 = lane; 2 * c2 < c; c2 += 32) {
-                const int cc = 2 * c2;
-                const int o = h * c + cc;
-                const bool two = cc + 1 < c;
-                auto st2 = [&](int base, float x0, float x1) {
-                    if (two && ((base + o) & 1) == 0) {
-                        *reinterpret_cast<uint32_t*>(dp + base + o) = ptx_pack(x0, x1);
-                    } else {
-                        dp[base + o] = __float2bfloat16_rn(x0);
-                        if (two) dp[base + o + 1] = __float2bfloat16_rn(x1);
+                for (int u = 0; u < 8; ++u) {
+                    const int h = h0 + u;
+                    if (h < H) {
+                        const float k2 = kLn2 * kq[u];
+                        s1 += qq[u];
+                        s2 += s_wlb[h * dz + dd] * k2 + vq[u];
+                        if (reg_dwlb) pw[u + h0] = fmaf(k2, z2v, pw[u + h0]);
+                        else atomicAdd(&s_dwlb[h * dz + dd], k2 * z2v);
                     }
-                };
-                st2(off_q, qa[cc], two ? qa[cc + 1] : 0.f);
-                st2(off_k, a.k_scale * kLn2 * ka[cc], two ? a.k_scale * kLn2 * ka[cc + 1] : 0.f);
-                st2(off_v, va[cc], two ? va[cc + 1] : 0.f);
-            }
-            // pair factors
-            for (int e = lane; e < rdz; e += 32) {
-                const int dd = e % dz;
-                const float kq = kLn2 * ka[zq + e];
-                s_pq[h * rdz + e] = qa[zq + e];
-                s_pk[h * rdz + e] = s_wlb[h * dz + dd] * kq + va[c + e];
-                if (dwlb_plain) s_dwlb[h * dz + dd] += kq * z2[e];
-                else atomicAdd(&s_dwlb[h * dz + dd], kq * z2[e]);
-            }
-            // geometry: lane per point
-            const float g = a.head_g[h];
-            const float cs = ka[g0 + 18];
-            const float S1 = qa[g0 + 20];  // sum_j dS_ij, as rounded for the MMAs
-            float dW[3];
-#pragma unroll
-            for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (ka[g0 + 9 + x] + ka[g0 + 12 + x]);
-            float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dgh = 0.f;
-            if (lane < Nq) {
-                const int p = lane;
-                // query point: A = R q_p + t,  dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS B] - g A S1
-                // (S1 = 0 is not assumed: subtracting g A S1 with the same rounded dS cancels the
-                // translation-sized common mode of the first term)
-                float qp[3], gB[3], A[3], dA[3];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    qp[x] = pr[off_qp + (h * Nq + p) * 3 + x];
-                    gB[x] = qa[c + 3 * p + x] + qa[g0 + x] + qa[g0 + 3 + x];
                 }
-#pragma unroll
-                for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    dA[x] = gB[x] - g * A[x] * S1;
-                    dt[x] += dA[x];
-                }
-                // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
-                dgh += (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
-                       0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    dp[off_qp + (h * Nq + p) * 3 + x] =
-                        __float2bfloat16_rn(R[x] * dA[0] + R[3 + x] * dA[1] + R[6 + x] * dA[2]);
-#pragma unroll
-                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
-                }
-                // key point: B = R k_p + t
-                float kp[3], B[3], dB[3];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) kp[x] = pr[off_kp + (h * Nq + p) * 3 + x];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) B[x] = R[3 * x] * kp[0] + R[3 * x + 1] * kp[1] + R[3 * x + 2] * kp[2] + t[x];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    dB[x] = g * kLn2 * ka[c + 3 * p + x] + dW[x] - g * B[x] * cs;
-                    dt[x] -= g * B[x] * cs;
-                }
-                dgh += -0.5f * (B[0] * B[0] + B[1] * B[1] + B[2] * B[2]) * cs;
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    dp[off_kp + (h * Nq + p) * 3 + x] =
-                        __float2bfloat16_rn(R[x] * dB[0] + R[3 + x] * dB[1] + R[6 + x] * dB[2]);
-#pragma unroll
-                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
-                }
-            }
-            if (lane < Nv) {
-                const int p = lane;
-                float vp[3], dV[3];
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    vp[x] = pr[off_vp + (h * Nv + p) * 3 + x];
-                    dV[x] = va[vpair + 6 + 3 * p + x];
-                }
-#pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    dp[off_vp + (h * Nv + p) * 3 + x] =
-                        __float2bfloat16_rn(R[x] * dV[0] + R[3 + x] * dV[1] + R[6 + x] * dV[2]);
-#pragma unroll
-                    for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
-                }
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int x = 0; x < 3; ++x)
-                    dt[x] += g * kLn2 * (ka[g0 + x] + ka[g0 + 6 + x]) + float(Nq) * dW[x]   // key
-                             + va[vpair + x];                                                // value
-            }
-#pragma unroll
-            for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
-            dgh = warp_sum(dgh);
-            if (lane < 12) s_geo[h * 12 + lane] = lane < 9 ? dR[lane] : dt[lane - 9];
-            if (lane == 0) s_dg[h] += dgh;  // one warp per head
-            __syncwarp();
-        }
-        __syncthreads();
-        {
-            const uint4* src = reinterpret_cast<const uint4*>(s_dp);
-            uint4* dst = reinterpret_cast<uint4*>(a.dproj + row * a.nproj_ld);
-            for (int e = threadIdx.x; e < a.nproj_ld / 8; e += blockDim.x) dst[e] = src[e];
-        }
-        for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
-            float s1 = z1e[e], s2 = 0.f;
-            for (int h = 0; h < H; ++h) {
-                s1 += s_pq[h * rdz + e];
-                s2 += s_pk[h * rdz + e];
             }
             a.dz1[row * rdz + e] = s1;
             a.dz2[row * rdz + e] = s2;
         }
-        if (threadIdx.x < 12) {
-            float acc = 0.f;
-            for (int h = 0; h < H; ++h) acc += s_geo[h * 12 + threadIdx.x];
-            if (threadIdx.x < 9) {
-                if (a.drot != nullptr) a.drot[row * 9 + threadIdx.x] = acc + epi[threadIdx.x];
-            } else {
-                a.dt_c[row * 3 + threadIdx.x - 9] = acc + epi[threadIdx.x];
+        // ---- scalar columns (bf16 pairs)
+        if (pairs) {
+            constexpr int kBatch = 6;  // loads of kBatch iterations in flight before the stores
+            const int total = 3 * H * half_c;
+            for (int base = tid; base < total; base += kBatch * blockDim.x) {
+                float2 v[kBatch];
+                int dst[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int idx = min(base + u * static_cast<int>(blockDim.x), total - 1);
+                    const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
+                    const int h = rem / half_c, cc = 2 * (rem - h * half_c);
+                    const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
+                    v[u] = __ldg(reinterpret_cast<const float2*>(src));
+                    dst[u] = tsel * H * c + h * c + cc;
+                    if (tsel == 1) {
+                        v[u].x *= kscale;
+                        v[u].y *= kscale;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+                    if (base + u * static_cast<int>(blockDim.x) < total)
+                        *reinterpret_cast<uint32_t*>(dp + dst[u]) = ptx_pack(v[u].x, v[u].y);
+            }
+        } else {
+            for (int idx = tid; idx < 3 * H * c; idx += blockDim.x) {
+                const int tsel = idx / (H * c), rem = idx - tsel * (H * c);
+                const int h = rem / c, cc = rem - h * c;
+                const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
+                dp[tsel * H * c + h * c + cc] = __float2bfloat16_rn(__ldg(src) * (tsel == 1 ? kscale : 1.f));
             }
         }
-        __syncthreads();
+        for (int e = d.n_proj + tid; e < a.nproj_ld; e += blockDim.x) dp[e] = __float2bfloat16_rn(0.f);
     }
-    for (int e = threadIdx.x; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
-    for (int e = threadIdx.x; e < H; e += blockDim.x) atomicAdd(&a.dg[e], s_dg[e]);
+    if (reg_dwlb && tid < rdz) {
+#pragma unroll
+        for (int h = 0; h < kUnpackMaxH; ++h)
+            if (h < H) atomicAdd(&s_dwlb[h * dz + tid % dz], pw[h]);
+    }
+    __syncthreads();
+    for (int e = tid; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
+    if (tid < H) {
+        float acc = 0.f;
+        for (int rr = 0; rr < nrows; ++rr) acc += a.dg_rows[(row_begin + rr) * H + tid];
+        atomicAdd(&a.dg[tid], acc);
+    }
 }
 
 // dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 32 columns x 8 row
@@ -570,19 +579,14 @@ void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stre
 }
 
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
-    const int rdz = d.rank * d.d_z;
-    // a residue's H accumulator rows are staged whole (row stride acc_ld)
-    const int stage_w = a.acc_ld;
-    if (std::max(d.dqk_used, d.dv_used) > a.acc_ld || (a.acc_ld * 4) % 16)
-        throw std::invalid_argument("bwd_unpack: accumulator stride");
-    if (a.nproj_ld % 8 != 0) throw std::invalid_argument("bwd_unpack: dproj stride must be a multiple of 8");
-    const int npts = d.n_proj - 3 * d.heads * d.c;
-    const int stage_floats = 3 * d.heads * stage_w + ((npts + 3) & ~3) + 2 * ((rdz + 3) & ~3) + 12;
-    const size_t smem = sizeof(float) * (2 * stage_floats + 2 * d.heads * rdz + d.heads * 12 + 2 * d.heads * d.d_z +
-                                         d.heads) + 16 + 2 * size_t(a.nproj_ld) + 8 + 16;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (std::max(d.dqk_used, d.dv_used) > a.acc_ld) throw std::invalid_argument("bwd_unpack: accumulator stride");
+    if (d.heads > kUnpackMaxH) throw std::invalid_argument("bwd_unpack: at most 16 heads");
+    if (d.n_query > 32 || d.n_value > 32) throw std::invalid_argument("bwd_unpack: at most 32 points per head");
     const int64_t BL = int64_t(a.B) * a.L;
-    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a, stage_w);
+    bwd_unpack_geo_kernel<<<static_cast<unsigned>(BL), 32 * std::min(d.heads, 8), 0, stream>>>(d, a);
+    const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a);
 }
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,

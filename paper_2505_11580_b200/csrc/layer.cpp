@@ -553,6 +553,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dt_c = reinterpret_cast<float*>(take(BL * 3 * 4));
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
+        w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
     }
     w.bytes = off;
     return w;
@@ -578,9 +579,9 @@ bool FlashIpaLayer::backward_supported() const {
 }
 
 int FlashIpaLayer::launches_per_backward() const {
-    // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, attn Q, unpack, recenter, ds GEMM,
-    // dW_proj GEMM, scatter, two scale kernels (memsets are not kernels of ours)
-    return 13;
+    // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, attn Q, unpack (geometry + streaming),
+    // recenter, ds GEMM, dW_proj GEMM, scatter, two scale kernels (memsets are not kernels of ours)
+    return 14;
 }
 
 int FlashIpaLayer::launches_per_forward() const {
@@ -1081,6 +1082,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.drot = drot;
         a.dt_c = ws.dt_c;
         a.dg = ws.red;
+        a.dg_rows = ws.dg_rows;
         a.dwlb = ws.red + H;
         a.B = int(B);
         a.L = int(L);

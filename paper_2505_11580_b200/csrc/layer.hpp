@@ -188,6 +188,7 @@ public:
         float* geo_epi = nullptr;          // [BL, 12] dR | dt of the output epilogue
         float* dt_c = nullptr;             // [BL, 3]
         float* red = nullptr;              // [H + H d_z]  d(g) | d(w_l w_bias)
+        float* dg_rows = nullptr;          // [BL, H] per-residue dgamma terms (unpack scratch)
         float* dwproj = nullptr;           // [d_in, n_proj]
         std::size_t bytes = 0;
     };
