@@ -71,6 +71,8 @@ struct BwdParams {
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
     int acc_ld;
+    int acc_col0[2];   // first accumulator column each pair writes (dQ split over the pairs)
+    int b2_col0[2];    // first B2 column each pair streams
 };
 
 struct Bars {
@@ -79,6 +81,7 @@ struct Bars {
     uint64_t b2_full[kStages2], b2_empty[kStages2];
     uint64_t x_full, x_free, a_full, acc_full;
     uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
+    uint64_t dsin_full[2];                            // Q kernel: dS returned to the P pair
     uint32_t tmem_slot;
 };
 
@@ -192,12 +195,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ptx::mbar_init(&bars->x_full, 1);
         ptx::mbar_init(&bars->x_free, 16);
-        ptx::mbar_init(&bars->a_full, 16);
+        // Q kernel, P pair: the MMA operand (dS) arrives by copy; the odd CTA forwards its arrival
+        ptx::mbar_init(&bars->a_full, (!KV && role == 0) ? 1 : 16);
         ptx::mbar_init(&bars->acc_full, 1);
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->mma2_done[b], 1);
             ptx::mbar_init(&bars->pin_full[b], 1);
             ptx::mbar_init(&bars->pin_free[b], 1);
+            ptx::mbar_init(&bars->dsin_full[b], 1);
         }
         ptx::fence_mbar_init();
     }
@@ -235,16 +240,28 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
                 uint8_t* dst = sB2 + s * p.b2_stage;
                 const int row = n * kSlice;
+                const int col0 = p.b2_col0[role];
                 for (int x = 0; x < rd.nba; ++x)
                     ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s],
-                                         halfa * static_cast<int>(prank) + 64 * x, row, bh);
+                                         col0 + halfa * static_cast<int>(prank) + 64 * x, row, bh);
                 for (int x = 0; x < rd.nbb; ++x)
                     ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
-                                         rd.n2a + halfb * static_cast<int>(prank) + 64 * x, row, bh);
+                                         col0 + rd.n2a + halfb * static_cast<int>(prank) + 64 * x, row, bh);
             }
         }
     } else if (warp == 1) {
         // -------------------------------------------------- MMA issue (pair leaders)
+        if (!leader && !KV && role == 0 && has_mma2) {
+            // Q kernel, odd CTA of the P pair: forward the arrival of each returned dS tile to the
+            // leader (a bulk copy can only complete on a barrier of the destination CTA)
+            if (lane == 0) {
+                const uint32_t a_full_leader = ptx::mapa(&bars->a_full, crank & 2u);
+                for (int j = 0; j < ntiles; ++j) {
+                    ptx::mbar_wait(&bars->dsin_full[j & 1], (j >> 1) & 1);
+                    ptx::mbar_arrive_remote(a_full_leader);
+                }
+            }
+        }
         if (leader) {
             const uint32_t idesc1 = ptx::idesc_bf16(256, BN, false, false);
             const uint32_t idesc2a = ptx::idesc_bf16(256, rd.n2a > 0 ? rd.n2a : 16, false, true);
@@ -278,6 +295,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
+                    if (!KV && role == 0) ptx::mbar_wait(&bars->dsin_full[jj & 1], (jj >> 1) & 1);
                     ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
                     if (lane == 0) BTRACE(1, jj);
                     for (int h2 = 0; h2 < BN / kSlice; ++h2) {
@@ -385,6 +403,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait_cluster(&bars->pin_free[buf], ((j >> 1) - 1) & 1);
                     ptx::tc_fence_after();
                 }
+                // Q kernel: dS_j comes back into this buffer once the dS pair has it (the copy of
+                // P_j out of it has completed by then)
+                if (!KV && has_mma2 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->dsin_full[buf], BM * 128);
                 if (lane == 0) BTRACE(5, j);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -395,7 +416,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::fence_proxy_async_smem();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (has_mma2 && lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                if (KV && has_mma2 && lane == 0) ptx::mbar_arrive_remote(a_full_remote);
                 // all 128 rows written -> one bulk copy of the 16 KB tile into the dS pair
                 named_bar_sync(1, 256);
                 if (warp == 2 && lane == 0) {
@@ -431,6 +452,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
                 if (lane == 0) BTRACE(10, j);
+                if (!KV && p.role[0].n2 > 0) {
+                    // Q kernel: the P pair accumulates the other half of dQ from the same dS tile
+                    named_bar_sync(1, 256);
+                    if (warp == 2 && lane == 0)
+                        bulk_copy_s2cluster(ptx::mapa(abuf, crank - 2u), abuf, BM * 128,
+                                            ptx::mapa(&bars->dsin_full[buf], crank - 2u));
+                }
             }
         }
 
@@ -443,7 +471,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
             // residue-major [B, L, H, acc_ld]: the H rows of a residue are contiguous for bwd_unpack
             const int bb = bh / p.H, hh = bh - bb * p.H;
-            float* orow = out + ((static_cast<int64_t>(bb) * p.L + (grow < p.L ? grow : 0)) * p.H + hh) * p.acc_ld;
+            float* orow = out + ((static_cast<int64_t>(bb) * p.L + (grow < p.L ? grow : 0)) * p.H + hh) * p.acc_ld +
+                          p.acc_col0[role];
             for (int ch = lo; ch < hi; ++ch) {
                 uint32_t o[16];
                 ptx::tmem_ld16(tl + 16 * ch, o);
@@ -533,16 +562,24 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         launch<true>(d, a, p, maps, stream);
     }
     if (which & 2) {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
+        // dQ = dS.K_hat split over both pairs by columns: the P pair receives dS back from the
+        // dS pair and accumulates columns [0, nq0), the dS pair [nq0, dqk): one S (or dP) GEMM and
+        // half a dQ GEMM per pair and tile, instead of the P pair idling through the dS pair's two.
+        const int nq0 = (d.dqk_mma / 2 + 15) / 16 * 16;
         BwdParams p{};
         p.L = a.L;
         p.H = d.heads;
-        p.role[0] = make_role(d.dqk_mma, 0);
-        p.role[1] = make_role(d.dv_mma, d.dqk_mma);
+        p.role[0] = make_role(d.dqk_mma, nq0);
+        p.role[1] = make_role(d.dv_mma, d.dqk_mma - nq0);
         finish_params(p);
         p.lse = a.lse;
         p.Dvec = a.Dvec;
-        p.acc_out[0] = nullptr;
+        p.acc_out[0] = a.dq_acc;
         p.acc_out[1] = a.dq_acc;
+        p.acc_col0[0] = 0;
+        p.acc_col0[1] = nq0;
+        p.b2_col0[0] = 0;
+        p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
         const CUtensorMap maps[6] = {stat(a.qhat, nqk), tile(a.khat, nqk), slice(a.khat),
                                      stat(a.dohat, nv), tile(a.vhat, nv),  slice(a.khat)};
