@@ -49,7 +49,9 @@ constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
 constexpr int kStages1 = 2;
-constexpr int kStages2 = 3;  // 16-row B2 slices (3 x 8 KB: what is left next to two 16 KB P/dS buffers)
+constexpr int kMaxStages2 = 8;  // 16-row B2 slices: as many as fit beside the stationary tile, the
+                                // two P/dS buffers and the B1 ring (3 x 8 KB in the KV kernel,
+                                // 6 x 4 KB in the dQ kernel whose pairs stream half the columns)
 constexpr int kSlice = 16;
 constexpr int kSliceBox = kSlice * 128;
 constexpr uint32_t kXCol = 448;
@@ -66,7 +68,7 @@ struct RoleDims {
 struct BwdParams {
     int L, H;
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
-    int stat_bytes, b1_stage, b2_stage;
+    int stat_bytes, b1_stage, b2_stage, nst2;
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -78,7 +80,7 @@ struct BwdParams {
 struct Bars {
     uint64_t stat_full;
     uint64_t b1_full[kStages1], b1_empty[kStages1];
-    uint64_t b2_full[kStages2], b2_empty[kStages2];
+    uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
     uint64_t x_full, x_free, a_full, acc_full;
     uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
     uint64_t dsin_full[2];                            // Q kernel: dS returned to the P pair
@@ -94,7 +96,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.abuf = p.stat_bytes;
     l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
     l.b2 = l.b1 + kStages1 * p.b1_stage;
-    l.bars = l.b2 + kStages2 * p.b2_stage;
+    l.bars = l.b2 + p.nst2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
 }
@@ -189,7 +191,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->b1_full[s], 1);
             ptx::mbar_init(&bars->b1_empty[s], 1);
         }
-        for (int s = 0; s < kStages2; ++s) {
+        for (int s = 0; s < p.nst2; ++s) {
             ptx::mbar_init(&bars->b2_full[s], 1);
             ptx::mbar_init(&bars->b2_empty[s], 1);
         }
@@ -234,8 +236,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int stage_bytes = (rd.nba + rd.nbb) * kSliceBox;
             const int nslices = ntiles * (BN / kSlice);
             for (int n = 0; n < nslices; ++n) {
-                const int s = n % kStages2;
-                if (n >= kStages2) ptx::mbar_wait(&bars->b2_empty[s], ((n / kStages2) - 1) & 1);
+                const int s = n % p.nst2;
+                if (n >= p.nst2) ptx::mbar_wait(&bars->b2_empty[s], ((n / p.nst2) - 1) & 1);
                 BTRACE(12, n);
                 if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
                 uint8_t* dst = sB2 + s * p.b2_stage;
@@ -271,6 +273,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1_base = ptx::smem_u32(sB1);
             const uint32_t b2_base = ptx::smem_u32(sB2);
             const int k1_steps = rd.k1 / 16;
+            int s2 = 0, ph2 = 0;
             ptx::mbar_wait(&bars->stat_full, 0);
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
@@ -299,9 +302,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
                     if (lane == 0) BTRACE(1, jj);
                     for (int h2 = 0; h2 < BN / kSlice; ++h2) {
-                        const int n = jj * (BN / kSlice) + h2;
-                        const int s = n % kStages2;
-                        ptx::mbar_wait(&bars->b2_full[s], (n / kStages2) & 1);
+                        const int s = s2;
+                        ptx::mbar_wait(&bars->b2_full[s], ph2);
+                        if (++s2 == p.nst2) {  // ring position by counters: no division on the issue path
+                            s2 = 0;
+                            ph2 ^= 1;
+                        }
                         if (lane == 0 && h2 == BN / kSlice - 1) BTRACE(13, jj);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
@@ -511,6 +517,14 @@ void finish_params(BwdParams& p) {
     p.stat_bytes = nb1 * BM * 128;
     p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
+    p.nst2 = 2;
+    while (p.nst2 < kMaxStages2) {  // deepest B2 ring that fits
+        ++p.nst2;
+        if (smem_layout(p).total + 1024 > 232448) {
+            --p.nst2;
+            break;
+        }
+    }
 }
 
 template <bool KV>
