@@ -35,6 +35,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -48,7 +50,7 @@ namespace {
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
-constexpr int kStages1 = 2;
+constexpr int kMaxStages1 = 8;  // B1 ring: groups of kb1 128-byte column blocks of a 32-row tile half
 constexpr int kMaxStages2 = 8;  // 16-row B2 slices: as many as fit beside the stationary tile, the
                                 // two P/dS buffers and the B1 ring (3 x 8 KB in the KV kernel,
                                 // 6 x 4 KB in the dQ kernel whose pairs stream half the columns)
@@ -69,6 +71,7 @@ struct BwdParams {
     int L, H;
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
     int stat_bytes, b1_stage, b2_stage, nst2;
+    int kb1, nst1;     // B1 ring: column blocks per stage, stages
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -79,7 +82,7 @@ struct BwdParams {
 
 struct Bars {
     uint64_t stat_full;
-    uint64_t b1_full[kStages1], b1_empty[kStages1];
+    uint64_t b1_full[kMaxStages1], b1_empty[kMaxStages1];
     uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
     uint64_t x_full, x_free, a_full, acc_full;
     uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
@@ -95,7 +98,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.stat = 0;
     l.abuf = p.stat_bytes;
     l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
-    l.b2 = l.b1 + kStages1 * p.b1_stage;
+    l.b2 = l.b1 + p.nst1 * p.b1_stage;
     l.bars = l.b2 + p.nst2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
@@ -187,7 +190,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(mB1);
         if (has_mma2) ptx::tma_prefetch(mB2);
         ptx::mbar_init(&bars->stat_full, 1);
-        for (int s = 0; s < kStages1; ++s) {
+        for (int s = 0; s < p.nst1; ++s) {
             ptx::mbar_init(&bars->b1_full[s], 1);
             ptx::mbar_init(&bars->b1_empty[s], 1);
         }
@@ -219,14 +222,20 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
             ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
-            const int stage = rd.nb1 * 32 * 128;
+            const int nk1 = (rd.nb1 + p.kb1 - 1) / p.kb1;  // stages per tile
+            int s = 0, ph = 0, n = 0;
             for (int j = 0; j < ntiles; ++j) {
-                const int s = j % kStages1;
-                if (j >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((j / kStages1) - 1) & 1);
                 BTRACE(11, j);
-                if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
-                ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
-                                     j * BN + 32 * static_cast<int>(prank), 0, bh);
+                for (int u = 0; u < nk1; ++u, ++n) {
+                    if (n >= p.nst1) ptx::mbar_wait(&bars->b1_empty[s], ph ^ 1);
+                    if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * p.b1_stage);
+                    ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
+                                         j * BN + 32 * static_cast<int>(prank), u * p.kb1, bh);
+                    if (++s == p.nst1) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
             }
         }
     } else if (warp == 10) {
@@ -273,28 +282,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1_base = ptx::smem_u32(sB1);
             const uint32_t b2_base = ptx::smem_u32(sB2);
             const int k1_steps = rd.k1 / 16;
-            int s2 = 0, ph2 = 0;
+            const int nk1 = (rd.nb1 + p.kb1 - 1) / p.kb1;
+            int s1 = 0, ph1 = 0, s2 = 0, ph2 = 0;
             ptx::mbar_wait(&bars->stat_full, 0);
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
                     if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
                     if (lane == 0) BTRACE(2, j);
-                    const int s = j % kStages1;
-                    ptx::mbar_wait(&bars->b1_full[s], (j / kStages1) & 1);
-                    if (lane == 0) BTRACE(0, j);
-                    ptx::tc_fence_after();
-                    if (ptx::elect_one()) {
-                        const uint32_t bb = b1_base + s * p.b1_stage;
-                        for (int kk = 0; kk < k1_steps; ++kk) {
-                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
-                            const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
-                            const uint64_t db = ptx::sw128_desc(bb + blk * (32 * 128) + sub, 16, 1024);
-                            ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
+                    for (int u = 0; u < nk1; ++u) {
+                        ptx::mbar_wait(&bars->b1_full[s1], ph1);
+                        if (lane == 0 && u == 0) BTRACE(0, j);
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            const uint32_t bb = b1_base + s1 * p.b1_stage;
+                            const int k_lo = u * p.kb1 * 4, k_hi = min(k1_steps, (u + 1) * p.kb1 * 4);
+                            for (int kk = k_lo; kk < k_hi; ++kk) {
+                                const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
+                                const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
+                                const uint64_t db = ptx::sw128_desc(bb + (blk - u * p.kb1) * (32 * 128) + sub, 16, 1024);
+                                ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
+                            }
+                            ptx::mma_commit_2sm(&bars->b1_empty[s1], pair_mask);
+                            if (u == nk1 - 1) ptx::mma_commit_2sm(&bars->x_full, pair_mask);
                         }
-                        ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
-                        ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                        __syncwarp();
+                        if (++s1 == p.nst1) {
+                            s1 = 0;
+                            ph1 ^= 1;
+                        }
                     }
-                    __syncwarp();
                 }
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
@@ -511,20 +527,68 @@ RoleDims make_role(int k1, int n2) {
     return r;
 }
 
+// Ring plan: the stationary tile (128 rows x all column blocks) and the two P/dS buffers are
+// fixed; the rest of shared memory is split between the B1 ring (groups of kb1 column blocks of
+// the 32-row tile half) and the B2 ring (16-row slices).  Preference: the plan whose shallower
+// ring, in tiles of lead, is deepest (B1 moves nb1 blocks per tile, B2 four slices per tile).
 void finish_params(BwdParams& p) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
     p.stat_bytes = nb1 * BM * 128;
-    p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    p.nst2 = 2;
-    while (p.nst2 < kMaxStages2) {  // deepest B2 ring that fits
-        ++p.nst2;
-        if (smem_layout(p).total + 1024 > 232448) {
-            --p.nst2;
-            break;
+    int forced[3] = {0, 0, 0};
+    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d,%d", &forced[0], &forced[1], &forced[2]);
+    // measured at the north-star shape (B=8 L=1024): whole-tile B1 stages with a 6-deep B2 ring
+    // where they fit (dQ kernel), else 4-block B1 groups x 3 with 4 B2 slices (dK/dV kernel);
+    // deeper B2 rings with small B1 stages measured slower
+    if (forced[0] == 0) {
+        const int pref[][3] = {{nb1, 2, 6}, {4, 3, 4}, {nb1, 2, 3}};
+        for (const auto& c : pref) {
+            BwdParams q = p;
+            q.kb1 = std::min(c[0], nb1);
+            q.nst1 = c[1];
+            q.nst2 = c[2];
+            q.b1_stage = q.kb1 * 32 * 128;
+            if (smem_layout(q).total + 1024 <= 232448) {
+                p = q;
+                return;
+            }
         }
     }
+    double best = -1.0;
+    BwdParams bestp = p;
+    for (int kb1 = 1; kb1 <= nb1; ++kb1) {
+        for (int nst1 = 2; nst1 <= kMaxStages1; ++nst1) {
+            for (int nst2 = 2; nst2 <= kMaxStages2; ++nst2) {
+                BwdParams q = p;
+                q.kb1 = kb1;
+                q.nst1 = nst1;
+                q.nst2 = nst2;
+                q.b1_stage = kb1 * 32 * 128;
+                if (smem_layout(q).total + 1024 > 232448) continue;
+                if (forced[0] > 0 && (kb1 != forced[0] || nst1 != forced[1] || nst2 != forced[2])) continue;
+                if (nst1 * kb1 < std::min(nb1, 2 * kb1)) continue;  // at least two stages in flight
+                const int nk1 = (nb1 + kb1 - 1) / kb1;              // stages per tile
+                const double lead1 = double(nst1) / nk1;            // tiles of B1 in flight
+                const double lead2 = double(nst2) / (BN / kSlice);   // tiles of B2 in flight
+                // shallower ring first, then fewer barrier round trips per tile (larger stages)
+                const double score = std::min(lead1, lead2) * 100.0 + kb1;
+                if (score > best) {
+                    best = score;
+                    bestp = q;
+                }
+            }
+        }
+    }
+    if (best < 0.0) {
+        if (forced[0] > 0) {  // a forced plan that does not fit: fall back to the automatic choice
+            unsetenv("FIPA_BWD_RING");
+            finish_params(p);
+            return;
+        }
+        throw std::invalid_argument("attention backward: no ring plan fits shared memory");
+    }
+    p = bestp;
 }
 
 template <bool KV>
@@ -557,7 +621,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     const int nqk = (d.dqk_mma + 63) / 64, nv = (d.dv_mma + 63) / 64;
     auto ld_of = [&](const void* x) { return (x == a.vhat || x == a.dohat) ? d.dv_pad : d.dqk_pad; };
     auto stat = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), BM, nb); };
-    auto tile = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), 32, nb); };
+    auto tile = [&](const void* x, int kb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), 32, kb); };
     auto slice = [&](const void* x) { return make_map_3d_bf16(x, ld_of(x), a.L, BH, ld_of(x), 64, kSlice); };
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
@@ -571,8 +635,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.acc_out[0] = a.dv_acc;
         p.acc_out[1] = a.dk_acc;
         p.acc_ld = a.acc_ld;
-        const CUtensorMap maps[6] = {stat(a.khat, nqk), tile(a.qhat, nqk), slice(a.dohat),
-                                     stat(a.vhat, nv),  tile(a.dohat, nv), slice(a.qhat)};
+        const CUtensorMap maps[6] = {stat(a.khat, nqk), tile(a.qhat, p.kb1), slice(a.dohat),
+                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat)};
         launch<true>(d, a, p, maps, stream);
     }
     if (which & 2) {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
@@ -595,8 +659,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.b2_col0[0] = 0;
         p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
-        const CUtensorMap maps[6] = {stat(a.qhat, nqk), tile(a.khat, nqk), slice(a.khat),
-                                     stat(a.dohat, nv), tile(a.vhat, nv),  slice(a.khat)};
+        const CUtensorMap maps[6] = {stat(a.qhat, nqk), tile(a.khat, p.kb1), slice(a.khat),
+                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat)};
         launch<false>(d, a, p, maps, stream);
     }
 }
