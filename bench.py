@@ -571,8 +571,7 @@ def run_trunk(args, shape):
             "config": {"workload": f"{args.trunk}-layer FlashIPA trunk forward with per-layer backbone frame update, "
                                    f"B={B} L={L} per GPU (BASELINE cfg3)", "pass": "fwd", "model": "FlashIPA trunk",
                        "global_batch": B * world, "seq_len": L, "layers": args.trunk, "shape": shape,
-                       "parallelism": (f"dp{world} (samples sharded, weight-gradient all-reduce)" if train and world > 1
-                                       else f"dp{world} (independent samples)"),
+                       "parallelism": f"dp{world} (independent samples)",
                        "l2": "flushed (256 MiB write) before every timed step"},
             "attn_tflops_whole_trunk": tflops,
             "roofline": {"bound": "tensor", "kernel": "whole trunk step (attention-dominated)", "achieved": tflops,
