@@ -216,6 +216,44 @@ int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_local, int w
                             const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------ sharded training
+ * Rank r of G owns residues [r L, (r+1) L); L % 256 == 0 when G > 1.  The forward keeps the fp32
+ * O_hat / lse of the local queries and the gathered k_hat / v_hat; the backward computes dQ for
+ * the local queries and PARTIAL dK / dV for all G L keys, reduce-scatters them (fp32) to their
+ * owners, all-reduces the per-sample translation-gradient sums and the weight gradients.
+ * Reference counterpart: none (the reference is single-process and inference-only). */
+size_t fipa_layer_sharded_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_local, int world);
+int fipa_layer_forward_train_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_local, const float* s,
+                                     const float* z1, const float* z2, const float* rot, const float* trans,
+                                     const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+int fipa_layer_backward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_local, const float* s,
+                                const float* z1, const float* z2, const float* rot, const float* trans,
+                                const uint8_t* mask, const float* dout, float* ds, float* dz1, float* dz2, float* drot,
+                                float* dtrans, float* dweights, void* workspace, size_t workspace_bytes,
+                                void* stream);
+/* Collective-agnostic blocks of the same training step (a fipa_layer_train_workspace_size(B, L_local)
+ * workspace per rank):
+ *   forward:  shard_centroid_sums -> all-reduce -> shard_pack_train -> rank-major all-gather of
+ *             k/v -> shard_attend_train
+ *   backward: shard_backward(stage 1) -> reduce-scatter dk_part / dv_part ([G][B][L][H][448] f32,
+ *             rank-major) into dk_own / dv_own ([B][L][H][448]) -> shard_backward(stage 2) ->
+ *             all-reduce dt_sums [B*4] -> shard_backward(stage 3) -> all-reduce dweights. */
+int fipa_layer_shard_pack_train(fipa_layer* layer, int64_t B, int64_t L_local, const float* s, const float* z1,
+                                const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                                const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                                void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes);
+int fipa_layer_shard_attend_train(fipa_layer* layer, int64_t B, int64_t L_local, int world, const float* s,
+                                  const float* z1, const float* z2, const float* rot, const float* trans,
+                                  const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+int fipa_layer_shard_backward(fipa_layer* layer, int stage, int world, int64_t B, int64_t L_local, const float* s,
+                              const float* z1, const float* z2, const float* rot, const float* trans,
+                              const uint8_t* mask, const float* dout, const void* khat_all, const void* vhat_all,
+                              float* dk_part, float* dv_part, const float* dk_own, const float* dv_own,
+                              float* dt_sums, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                              float* dweights, void* workspace, size_t workspace_bytes, void* stream);
+
 /* -------------------------------------------------------------------------- trunk
  * BASELINE cfg3: n_layers FlashIPA layers with residual and per-layer backbone frame update
  * (FrameFlow-style; the reference has no trunk -- the definition is oracle/fipa_oracle.py

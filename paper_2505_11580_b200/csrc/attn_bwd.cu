@@ -68,7 +68,8 @@ struct RoleDims {
 };
 
 struct BwdParams {
-    int L, H;
+    int Lrow, Lcol, H, B;       // rows (keys in KV, queries in Q) / tile columns
+    int stat_chunk, col_chunk;  // rows per shard of the stationary / column operands (sharded keys)
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
     int stat_bytes, b1_stage, b2_stage, nst2;
     int kb1, nst1;     // B1 ring: column blocks per stage, stages
@@ -179,7 +180,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const RoleDims rd = p.role[role];
     const int bh = blockIdx.y;
     const int r0 = (blockIdx.x >> 2) * 256 + static_cast<int>(prank) * BM;  // first row of this CTA
-    const int ntiles = (p.L + BN - 1) / BN;
+    const int ntiles = (p.Lcol + BN - 1) / BN;
     const bool has_mma2 = rd.n2 > 0;
     const CUtensorMap* mStat = role ? &statD : &statP;
     const CUtensorMap* mB1 = role ? &b1D : &b1P;
@@ -221,7 +222,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         // ------------------------------------------- stationary tile + B1 tile producer
         if (lane == 0) {
             if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
-            ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
+            {
+                const int g = r0 / p.stat_chunk;  // rows past the end land in shard G: TMA zero fill
+                ptx::tma_load_5d_2sm(sStat, mStat, &bars->stat_full, 0, r0 - g * p.stat_chunk, 0, bh, g);
+            }
             const int nk1 = (rd.nb1 + p.kb1 - 1) / p.kb1;  // stages per tile
             int s = 0, ph = 0, n = 0;
             for (int j = 0; j < ntiles; ++j) {
@@ -229,8 +233,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < nk1; ++u, ++n) {
                     if (n >= p.nst1) ptx::mbar_wait(&bars->b1_empty[s], ph ^ 1);
                     if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * p.b1_stage);
-                    ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
-                                         j * BN + 32 * static_cast<int>(prank), u * p.kb1, bh);
+                    const int key = j * BN + 32 * static_cast<int>(prank);
+                    const int g = key / p.col_chunk;
+                    ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk,
+                                         u * p.kb1, bh, g);
                     if (++s == p.nst1) {
                         s = 0;
                         ph ^= 1;
@@ -251,13 +257,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
                 uint8_t* dst = sB2 + s * p.b2_stage;
                 const int row = n * kSlice;
+                const int g = row / p.col_chunk, rloc = row - g * p.col_chunk;
                 const int col0 = p.b2_col0[role];
                 for (int x = 0; x < rd.nba; ++x)
-                    ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s],
-                                         col0 + halfa * static_cast<int>(prank) + 64 * x, row, bh);
+                    ptx::tma_load_4d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s],
+                                         col0 + halfa * static_cast<int>(prank) + 64 * x, rloc, bh, g);
                 for (int x = 0; x < rd.nbb; ++x)
-                    ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
-                                         col0 + rd.n2a + halfb * static_cast<int>(prank) + 64 * x, row, bh);
+                    ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
+                                         col0 + rd.n2a + halfb * static_cast<int>(prank) + 64 * x, rloc, bh, g);
             }
         }
     } else if (warp == 1) {
@@ -363,11 +370,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t leader_rank = crank & 2u;
         const uint32_t x_free_remote = ptx::mapa(&bars->x_free, leader_rank);
         const uint32_t a_full_remote = ptx::mapa(&bars->a_full, leader_rank);
-        const int64_t vec_base = static_cast<int64_t>(bh) * p.L;
+        const int64_t vec_base = static_cast<int64_t>(bh) * (KV ? p.Lcol : p.Lrow);  // per-query vectors
         const int grow = r0 + row;  // global row (key in KV, query in Q)
         // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.
         float row_v = 0.f;
-        if (!KV && grow < p.L) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
+        if (!KV && grow < p.Lrow) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
                                                  : __ldg(p.Dvec + vec_base + grow);
         const uint32_t peer_rank = crank + 2u;  // P pair -> dS pair partner
 
@@ -381,11 +388,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             float cv[32];
             if (KV) {
                 if (role == 0) {
-                    load_vec32(p.lse + vec_base, c0, p.L, INFINITY, cv);
+                    load_vec32(p.lse + vec_base, c0, p.Lcol, INFINITY, cv);
 #pragma unroll
                     for (int k = 0; k < 32; ++k) cv[k] *= kL2E;
                 } else {
-                    load_vec32(p.Dvec + vec_base, c0, p.L, 0.f, cv);
+                    load_vec32(p.Dvec + vec_base, c0, p.Lcol, 0.f, cv);
                 }
             }
             ptx::mbar_wait(&bars->x_full, j & 1);
@@ -411,7 +418,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                         if (KV) {
                             pv[u] = ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
                         } else {
-                            pv[u] = c0 + k < p.L ? ptx::ex2(x - row_v) : 0.f;
+                            pv[u] = c0 + k < p.Lcol ? ptx::ex2(x - row_v) : 0.f;
                         }
                     }
                     pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);
@@ -493,13 +500,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
             // residue-major [B, L, H, acc_ld]: the H rows of a residue are contiguous for bwd_unpack
             const int bb = bh / p.H, hh = bh - bb * p.H;
-            float* orow = out + ((static_cast<int64_t>(bb) * p.L + (grow < p.L ? grow : 0)) * p.H + hh) * p.acc_ld +
+            // rank-major [G][B][chunk][H][acc_ld] (G = 1 unsharded: residue-major [B, L, H, acc_ld])
+            const int rr = grow < p.Lrow ? grow : 0;
+            const int g = rr / p.stat_chunk, gi = rr - g * p.stat_chunk;
+            float* orow = out + (((static_cast<int64_t>(g) * p.B + bb) * p.stat_chunk + gi) * p.H + hh) * p.acc_ld +
                           p.acc_col0[role];
             for (int ch = lo; ch < hi; ++ch) {
                 uint32_t o[16];
                 ptx::tmem_ld16(tl + 16 * ch, o);
                 ptx::tmem_wait_ld();
-                if (grow < p.L) {
+                if (grow < p.Lrow) {
                     float4* dst = reinterpret_cast<float4*>(orow + 16 * ch);
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
@@ -599,7 +609,7 @@ void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const 
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
     auto kern = attn_bwd_kernel<KV>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int clusters = (a.L + 255) / 256;
+    const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
     kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
 }
@@ -620,13 +630,29 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
     const int nqk = (d.dqk_mma + 63) / 64, nv = (d.dv_mma + 63) / 64;
     auto ld_of = [&](const void* x) { return (x == a.vhat || x == a.dohat) ? d.dv_pad : d.dqk_pad; };
-    auto stat = [&](const void* x, int nb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), BM, nb); };
-    auto tile = [&](const void* x, int kb) { return make_map_blocks_bf16(x, a.L, BH, ld_of(x), 32, kb); };
-    auto slice = [&](const void* x) { return make_map_3d_bf16(x, ld_of(x), a.L, BH, ld_of(x), 64, kSlice); };
+    // every operand through the sharded (rank-major) maps; local operands are one shard of L rows
+    const int Lk = a.Lk > 0 ? a.Lk : a.L, kc = a.kchunk > 0 ? a.kchunk : Lk;
+    const int G = (Lk + kc - 1) / kc;
+    if (G * kc != Lk || (G > 1 && kc % 256 != 0))
+        throw std::invalid_argument("attention backward: key shards must be equal and a multiple of 256 rows");
+    auto is_key = [&](const void* x) { return x == a.khat || x == a.vhat; };
+    auto chunk_of = [&](const void* x) { return is_key(x) ? kc : a.L; };
+    auto g_of = [&](const void* x) { return is_key(x) ? G : 1; };
+    auto stat = [&](const void* x, int nb) {
+        return make_map_blocks_bf16_sharded(x, chunk_of(x), BH, g_of(x), ld_of(x), BM, nb);
+    };
+    auto tile = [&](const void* x, int kb) {
+        return make_map_blocks_bf16_sharded(x, chunk_of(x), BH, g_of(x), ld_of(x), 32, kb);
+    };
+    auto slice = [&](const void* x) { return make_map_4d_bf16_sharded(x, ld_of(x), chunk_of(x), BH, g_of(x), 64, kSlice); };
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
-        p.L = a.L;
+        p.Lrow = Lk;  // rows = keys (all shards)
+        p.Lcol = a.L; // tile columns = local queries
+        p.stat_chunk = kc;
+        p.col_chunk = a.L;
         p.H = d.heads;
+        p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
         finish_params(p);
@@ -645,8 +671,12 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         // half a dQ GEMM per pair and tile, instead of the P pair idling through the dS pair's two.
         const int nq0 = (d.dqk_mma / 2 + 15) / 16 * 16;
         BwdParams p{};
-        p.L = a.L;
+        p.Lrow = a.L;  // rows = local queries
+        p.Lcol = Lk;   // tile columns = keys (all shards)
+        p.stat_chunk = a.L;
+        p.col_chunk = kc;
         p.H = d.heads;
+        p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, nq0);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma - nq0);
         finish_params(p);

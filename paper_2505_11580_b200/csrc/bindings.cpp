@@ -343,23 +343,72 @@ public:
     }
     py::tuple shard_pack(int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
                          uintptr_t trans, uintptr_t mask, uintptr_t sums, uintptr_t ws, size_t ws_bytes,
-                         uintptr_t stream) {
+                         uintptr_t stream, bool train) {
         auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
         void *k = nullptr, *v = nullptr;
         size_t kb = 0, vb = 0;
-        check(fipa_layer_shard_pack(layer_, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+        check((train ? fipa_layer_shard_pack_train : fipa_layer_shard_pack)(layer_, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
                                     reinterpret_cast<const uint8_t*>(mask), f(sums), reinterpret_cast<void*>(ws),
                                     ws_bytes, reinterpret_cast<void*>(stream), &k, &kb, &v, &vb));
         return py::make_tuple(reinterpret_cast<uintptr_t>(k), kb, reinterpret_cast<uintptr_t>(v), vb);
     }
     void shard_attend(int64_t B, int64_t L, int world, uintptr_t s, uintptr_t z1, uintptr_t z2, uintptr_t rot,
                       uintptr_t trans, uintptr_t mask, uintptr_t k_all, uintptr_t v_all, uintptr_t out, uintptr_t ws,
-                      size_t ws_bytes, uintptr_t stream) {
+                      size_t ws_bytes, uintptr_t stream, bool train) {
         auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
-        check(fipa_layer_shard_attend(layer_, B, L, world, f(s), f(z1), f(z2), f(rot), f(trans),
+        check((train ? fipa_layer_shard_attend_train : fipa_layer_shard_attend)(layer_, B, L, world, f(s), f(z1), f(z2), f(rot), f(trans),
                                       reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<const void*>(k_all),
                                       reinterpret_cast<const void*>(v_all), reinterpret_cast<float*>(out),
                                       reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream)));
+    }
+    void shard_backward(int stage, int world, int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2,
+                        uintptr_t rot, uintptr_t trans, uintptr_t mask, uintptr_t dout, uintptr_t k_all,
+                        uintptr_t v_all, uintptr_t dk_part, uintptr_t dv_part, uintptr_t dk_own, uintptr_t dv_own,
+                        uintptr_t dt_sums, uintptr_t ds, uintptr_t dz1, uintptr_t dz2, uintptr_t drot,
+                        uintptr_t dtrans, uintptr_t dweights, uintptr_t ws, size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_shard_backward(layer_, stage, world, B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                           reinterpret_cast<const uint8_t*>(mask), f(dout),
+                                           reinterpret_cast<const void*>(k_all), reinterpret_cast<const void*>(v_all),
+                                           f(dk_part), f(dv_part), f(dk_own), f(dv_own), f(dt_sums), f(ds), f(dz1),
+                                           f(dz2), f(drot), f(dtrans), f(dweights), reinterpret_cast<void*>(ws),
+                                           ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    size_t sharded_train_workspace_size(int64_t B, int64_t L, int world) const {
+        return fipa_layer_sharded_train_workspace_size(layer_, B, L, world);
+    }
+    void forward_train_sharded_device(Comm& comm, int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2,
+                                      uintptr_t rot, uintptr_t trans, uintptr_t mask, uintptr_t out, uintptr_t ws,
+                                      size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<const float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_forward_train_sharded(layer_, comm.get(), B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                                  reinterpret_cast<const uint8_t*>(mask), reinterpret_cast<float*>(out),
+                                                  reinterpret_cast<void*>(ws), ws_bytes, reinterpret_cast<void*>(stream));
+        }
+        check(rc);
+    }
+    void backward_sharded_device(Comm& comm, int64_t B, int64_t L, uintptr_t s, uintptr_t z1, uintptr_t z2,
+                                 uintptr_t rot, uintptr_t trans, uintptr_t mask, uintptr_t dout, uintptr_t ds,
+                                 uintptr_t dz1, uintptr_t dz2, uintptr_t drot, uintptr_t dtrans, uintptr_t dweights,
+                                 uintptr_t ws, size_t ws_bytes, uintptr_t stream) {
+        auto f = [](uintptr_t p) { return reinterpret_cast<float*>(p); };
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = fipa_layer_backward_sharded(layer_, comm.get(), B, L, f(s), f(z1), f(z2), f(rot), f(trans),
+                                             reinterpret_cast<const uint8_t*>(mask), f(dout), f(ds), f(dz1), f(dz2),
+                                             f(drot), f(dtrans), f(dweights), reinterpret_cast<void*>(ws), ws_bytes,
+                                             reinterpret_cast<void*>(stream));
+        }
+        check(rc);
     }
     size_t train_workspace_size(int64_t B, int64_t L) const { return fipa_layer_train_workspace_size(layer_, B, L); }
     uint64_t num_weights() const { return fipa_layer_num_weights(layer_); }
@@ -663,10 +712,26 @@ PYBIND11_MODULE(_fipa_b200, m) {
              py::arg("mask"), py::arg("sums"), py::arg("stream"))
         .def("shard_pack", &Model::shard_pack, py::arg("B"), py::arg("L"), py::arg("s"), py::arg("z1"),
              py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("sums"), py::arg("workspace"),
-             py::arg("workspace_bytes"), py::arg("stream"))
+             py::arg("workspace_bytes"), py::arg("stream"), py::arg("train") = false)
         .def("shard_attend", &Model::shard_attend, py::arg("B"), py::arg("L"), py::arg("world"), py::arg("s"),
              py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("k_all"),
-             py::arg("v_all"), py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+             py::arg("v_all"), py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"),
+             py::arg("train") = false)
+        .def("shard_backward", &Model::shard_backward, py::arg("stage"), py::arg("world"), py::arg("B"), py::arg("L"),
+             py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("dout"), py::arg("k_all"), py::arg("v_all"), py::arg("dk_part"), py::arg("dv_part"),
+             py::arg("dk_own"), py::arg("dv_own"), py::arg("dt_sums"), py::arg("ds"), py::arg("dz1"), py::arg("dz2"),
+             py::arg("drot"), py::arg("dtrans"), py::arg("dweights"), py::arg("workspace"),
+             py::arg("workspace_bytes"), py::arg("stream"))
+        .def("sharded_train_workspace_size", &Model::sharded_train_workspace_size, py::arg("B"), py::arg("L"),
+             py::arg("world"))
+        .def("forward_train_sharded_device", &Model::forward_train_sharded_device, py::arg("comm"), py::arg("B"),
+             py::arg("L"), py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
+        .def("backward_sharded_device", &Model::backward_sharded_device, py::arg("comm"), py::arg("B"), py::arg("L"),
+             py::arg("s"), py::arg("z1"), py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"),
+             py::arg("dout"), py::arg("ds"), py::arg("dz1"), py::arg("dz2"), py::arg("drot"), py::arg("dtrans"),
+             py::arg("dweights"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
         .def("train_workspace_size", &Model::train_workspace_size, py::arg("B"), py::arg("L"))
         .def("num_weights", &Model::num_weights)
         .def("forward_train_device", &Model::forward_train_device, py::arg("B"), py::arg("L"), py::arg("s"),

@@ -474,10 +474,10 @@ int fipa_layer_shard_centroid_sums(fipa_layer* layer, int64_t B, int64_t L_, con
     });
 }
 
-int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
-                          const float* z2, const float* rot, const float* trans, const uint8_t* mask,
-                          const float* sums, void* workspace, size_t workspace_bytes, void* stream,
-                          void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes) {
+static int shard_pack_impl(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                           const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                           const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                           void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes, bool train) {
     return guarded([&] {
         auto& impl = L(layer);
         if (sums == nullptr) throw fipa_b200::ValueError("null centroid sums");
@@ -486,7 +486,7 @@ int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_, const float*
         st.sums = sums;
         // out is not written in stage 1; any non-null pointer satisfies the argument check
         impl.forward(B, L_, s, z1, z2, rot, trans, mask, reinterpret_cast<float*>(workspace), workspace,
-                     workspace_bytes, static_cast<cudaStream_t>(stream), false, &st);
+                     workspace_bytes, static_cast<cudaStream_t>(stream), train, &st);
         const auto w = impl.carve(workspace, B, L_);
         const std::size_t BHL = std::size_t(B) * L_ * impl.dims().heads;
         if (khat) *khat = w.khat;
@@ -496,10 +496,10 @@ int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_, const float*
     });
 }
 
-int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_, int world, const float* s, const float* z1,
-                            const float* z2, const float* rot, const float* trans, const uint8_t* mask,
-                            const void* khat_all, const void* vhat_all, float* out, void* workspace,
-                            size_t workspace_bytes, void* stream) {
+static int shard_attend_impl(fipa_layer* layer, int64_t B, int64_t L_, int world, const float* s,
+                             const float* z1, const float* z2, const float* rot, const float* trans,
+                             const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
+                             void* workspace, size_t workspace_bytes, void* stream, bool train) {
     return guarded([&] {
         if (khat_all == nullptr || vhat_all == nullptr || world < 1) throw fipa_b200::ValueError("bad key shards");
         if (world > 1 && L_ % 64 != 0) throw fipa_b200::ValueError("query-row sharding needs L_local % 64 == 0");
@@ -509,7 +509,90 @@ int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_, int world,
         st.v_all = vhat_all;
         st.groups = world;
         L(layer).forward(B, L_, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes,
-                         static_cast<cudaStream_t>(stream), false, &st);
+                         static_cast<cudaStream_t>(stream), train, &st);
+    });
+}
+
+int fipa_layer_shard_pack(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                          const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                          const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                          void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes) {
+    return shard_pack_impl(layer, B, L_, s, z1, z2, rot, trans, mask, sums, workspace, workspace_bytes, stream, khat,
+                           k_bytes, vhat, v_bytes, false);
+}
+
+int fipa_layer_shard_attend(fipa_layer* layer, int64_t B, int64_t L_, int world, const float* s, const float* z1,
+                            const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                            const void* khat_all, const void* vhat_all, float* out, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    return shard_attend_impl(layer, B, L_, world, s, z1, z2, rot, trans, mask, khat_all, vhat_all, out, workspace,
+                             workspace_bytes, stream, false);
+}
+
+int fipa_layer_shard_pack_train(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                                const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                                const float* sums, void* workspace, size_t workspace_bytes, void* stream,
+                                void** khat, size_t* k_bytes, void** vhat, size_t* v_bytes) {
+    return shard_pack_impl(layer, B, L_, s, z1, z2, rot, trans, mask, sums, workspace, workspace_bytes, stream, khat,
+                           k_bytes, vhat, v_bytes, true);
+}
+
+int fipa_layer_shard_attend_train(fipa_layer* layer, int64_t B, int64_t L_, int world, const float* s,
+                                  const float* z1, const float* z2, const float* rot, const float* trans,
+                                  const uint8_t* mask, const void* khat_all, const void* vhat_all, float* out,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+    return shard_attend_impl(layer, B, L_, world, s, z1, z2, rot, trans, mask, khat_all, vhat_all, out, workspace,
+                             workspace_bytes, stream, true);
+}
+
+int fipa_layer_shard_backward(fipa_layer* layer, int stage, int world, int64_t B, int64_t L_, const float* s,
+                              const float* z1, const float* z2, const float* rot, const float* trans,
+                              const uint8_t* mask, const float* dout, const void* khat_all, const void* vhat_all,
+                              float* dk_part, float* dv_part, const float* dk_own, const float* dv_own,
+                              float* dt_sums, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                              float* dweights, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        if (world < 1) throw fipa_b200::ValueError("world must be >= 1");
+        fipa_b200::BwdShard sh;
+        sh.stage = stage;
+        sh.groups = world;
+        sh.k_all = khat_all;
+        sh.v_all = vhat_all;
+        sh.dk_part = dk_part;
+        sh.dv_part = dv_part;
+        sh.dk_own = dk_own;
+        sh.dv_own = dv_own;
+        sh.dt_sums = dt_sums;
+        L(layer).backward(B, L_, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+                          workspace_bytes, static_cast<cudaStream_t>(stream), &sh);
+    });
+}
+
+size_t fipa_layer_sharded_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L_, int world) {
+    if (layer == nullptr || B < 1 || L_ < 1 || world < 1) return 0;
+    return layer->impl->sharded_train_workspace_size(B, L_, world);
+}
+
+int fipa_layer_forward_train_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_, const float* s,
+                                     const float* z1, const float* z2, const float* rot, const float* trans,
+                                     const uint8_t* mask, float* out, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+    return guarded([&] {
+        if (comm == nullptr) throw fipa_b200::ValueError("null fipa_comm");
+        L(layer).forward_train_sharded(comm->impl, B, L_, s, z1, z2, rot, trans, mask, out, workspace,
+                                       workspace_bytes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_layer_backward_sharded(fipa_layer* layer, fipa_comm* comm, int64_t B, int64_t L_, const float* s,
+                                const float* z1, const float* z2, const float* rot, const float* trans,
+                                const uint8_t* mask, const float* dout, float* ds, float* dz1, float* dz2, float* drot,
+                                float* dtrans, float* dweights, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+    return guarded([&] {
+        if (comm == nullptr) throw fipa_b200::ValueError("null fipa_comm");
+        L(layer).backward_sharded(comm->impl, B, L_, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans,
+                                  dweights, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -29,6 +29,8 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -51,8 +53,10 @@ const NcclApi& nccl() {
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
         api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+        api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
-        if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.AllReduce) {
+        if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.AllReduce ||
+            !api.ReduceScatter) {
             err = "NCCL library lacks required symbols";
             api.handle = nullptr;
         }
@@ -104,11 +108,16 @@ void Comm::all_gather_bytes(const void* send, void* recv, std::size_t bytes, cud
                "ncclAllGather");
 }
 
+void Comm::reduce_scatter_sum_f32(const float* send, float* recv, std::size_t n, cudaStream_t stream) {
+    nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), stream),
+               "ncclReduceScatter");
+}
+
 // ---------------------------------------------------------------- sharded forward
 FlashIpaLayer::ShardedWorkspace FlashIpaLayer::carve_sharded(void* base, std::int64_t B, std::int64_t L,
-                                                            int groups) const {
+                                                            int groups, bool train) const {
     ShardedWorkspace w;
-    w.local = carve(base, B, L);
+    w.local = carve(base, B, L, train);
     std::size_t off = (w.local.bytes + 255) / 256 * 256;
     auto take = [&](std::size_t bytes) {
         char* p = reinterpret_cast<char*>(reinterpret_cast<std::uintptr_t>(base) + off);
@@ -121,8 +130,81 @@ FlashIpaLayer::ShardedWorkspace FlashIpaLayer::carve_sharded(void* base, std::in
     w.k_all = take(w.kv_bytes * groups);
     w.v_all = take(w.v_bytes * groups);
     w.sums = reinterpret_cast<float*>(take(std::size_t(B) * 4 * 4));
+    if (train) {
+        const std::size_t part = std::size_t(groups) * BHL * kAccLd * 4;
+        w.dk_part = reinterpret_cast<float*>(take(part));
+        w.dv_part = reinterpret_cast<float*>(take(part));
+        w.dt_sums = reinterpret_cast<float*>(take(std::size_t(B) * 4 * 4));
+    }
     w.bytes = off;
     return w;
+}
+
+std::size_t FlashIpaLayer::sharded_train_workspace_size(std::int64_t B, std::int64_t L, int groups) const {
+    return carve_sharded(nullptr, B, L, groups, true).bytes;
+}
+
+// Sharded training step.  Forward as forward_sharded with the training buffers (fp32 O_hat, lse)
+// kept; the gathered k_hat / v_hat stay in the workspace for the backward.
+void FlashIpaLayer::forward_train_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s,
+                                          const float* z1, const float* z2, const float* rot,
+                                          const float* trans, const std::uint8_t* mask, float* out,
+                                          void* workspace, std::size_t workspace_bytes, cudaStream_t stream) {
+    const int G = comm.world();
+    if (G > 1 && L % 256 != 0) throw ValueError("sharded training needs L_local % 256 == 0");
+    const ShardedWorkspace ws = carve_sharded(workspace, B, L, G, true);
+    if (workspace == nullptr || workspace_bytes < ws.bytes)
+        throw ValueError("sharded train workspace too small: need " + std::to_string(ws.bytes) + " bytes");
+    launch_centroid_sums(trans, mask, ws.sums, int(B), int(L), stream);
+    comm.all_reduce_sum_f32(ws.sums, std::size_t(B) * 4, stream);
+    ShardStage st;
+    st.stage = 1;
+    st.sums = ws.sums;
+    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, true, &st);
+    comm.all_gather_bytes(ws.local.khat, ws.k_all, ws.kv_bytes, stream);
+    comm.all_gather_bytes(ws.local.vhat, ws.v_all, ws.v_bytes, stream);
+    st.stage = 2;
+    st.k_all = ws.k_all;
+    st.v_all = ws.v_all;
+    st.groups = G;
+    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, true, &st);
+}
+
+// Backward of the sharded step: the three BwdShard stages joined by a reduce-scatter of the partial
+// key gradients (fp32, 2 x G x B L H 448 floats per rank), an all-reduce of the translation-gradient
+// sums (4 floats per sample) and an all-reduce of the weight gradients.
+void FlashIpaLayer::backward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s,
+                                     const float* z1, const float* z2, const float* rot, const float* trans,
+                                     const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
+                                     float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
+                                     std::size_t workspace_bytes, cudaStream_t stream) {
+    const int G = comm.world();
+    const ShardedWorkspace ws = carve_sharded(workspace, B, L, G, true);
+    if (workspace == nullptr || workspace_bytes < ws.bytes)
+        throw ValueError("sharded train workspace too small: need " + std::to_string(ws.bytes) + " bytes");
+    BwdShard sh;
+    sh.groups = G;
+    sh.k_all = ws.k_all;
+    sh.v_all = ws.v_all;
+    sh.dk_part = ws.dk_part;
+    sh.dv_part = ws.dv_part;
+    sh.stage = 1;
+    backward(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+             ws.local.bytes, stream, &sh);
+    const std::size_t n = std::size_t(B) * L * dims_.heads * kAccLd;
+    comm.reduce_scatter_sum_f32(ws.dk_part, ws.local.dk_acc, n, stream);
+    comm.reduce_scatter_sum_f32(ws.dv_part, ws.local.dv_acc, n, stream);
+    sh.stage = 2;
+    sh.dk_own = ws.local.dk_acc;
+    sh.dv_own = ws.local.dv_acc;
+    sh.dt_sums = ws.dt_sums;
+    backward(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+             ws.local.bytes, stream, &sh);
+    comm.all_reduce_sum_f32(ws.dt_sums, std::size_t(B) * 4, stream);
+    sh.stage = 3;
+    backward(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+             ws.local.bytes, stream, &sh);
+    comm.all_reduce_sum_f32(dweights, num_weights(), stream);
 }
 
 std::size_t FlashIpaLayer::sharded_workspace_size(std::int64_t B, std::int64_t L, int groups) const {

@@ -134,7 +134,11 @@ struct AttnBwdArgs {
     float* dk_acc;               //                  = dS^T . Q_hat
     float* dv_acc;               //                  = P^T . dO_hat
     int acc_ld;
-    int B, L;
+    int B, L;                    // L = local query rows
+    // Query-row sharding: khat / vhat hold all Lk = G*kchunk keys gathered rank-major
+    // [G][B*H][kchunk][pad]; dk_acc / dv_acc then receive PARTIAL sums for all keys, rank-major
+    // [G][B][kchunk][H][acc_ld] (ready for a reduce-scatter).  0 = unsharded (Lk = L).
+    int Lk = 0, kchunk = 0;
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both
@@ -220,7 +224,9 @@ void launch_trunk_update(float* s, const float* ipa_out, const float* w_bb, cons
 // Query-row sharding: per-sample {sum x, sum y, sum z, count} of valid local translations, and
 // recentring with (all-reduced) global sums.
 void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, int B, int L, cudaStream_t stream);
-void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream);
+// out = trans - sum/count per sample; rows with zero_masked[row] == 0 are written as 0 when given.
+void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream,
+                               const uint8_t* zero_masked = nullptr);
 // Subtract each sample's translation centroid (exact: the layer is invariant to it).
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream);

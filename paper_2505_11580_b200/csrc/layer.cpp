@@ -630,8 +630,8 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
     REQUIRE(!train || backward_supported(),
             "training (forward_train/backward) needs precision='bf16' and lifted widths <= 448");
-    REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && bf16_attention_supported(dims_) && !train),
-            "query-row sharding needs precision='bf16' (inference forward)");
+    REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && bf16_attention_supported(dims_)),
+            "query-row sharding needs precision='bf16'");
     const bool do_pack = shard == nullptr || shard->stage == 1;
     const bool do_attend = shard == nullptr || shard->stage == 2;
     const Workspace ws = carve(workspace, B, L, train);
@@ -959,7 +959,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
                              const float* z2, const float* rot, const float* trans,
                              const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
                              float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
-                             std::size_t workspace_bytes, cudaStream_t stream) {
+                             std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && dout && ds && dz1 && dz2 && dweights,
@@ -983,9 +983,23 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
     float* db_out = dweights + woff[9];
 
     auto mark = [&](int i) {
-        if (timing_) cuda_check(cudaEventRecord(evb_[i], stream), "cudaEventRecord");
+        if (timing_ && shard == nullptr) cuda_check(cudaEventRecord(evb_[i], stream), "cudaEventRecord");
     };
+    const int G = shard ? shard->groups : 1;
+    if (shard != nullptr) {
+        REQUIRE(shard->stage >= 1 && shard->stage <= 3, "backward shard stage must be 1, 2 or 3");
+        REQUIRE(G == 1 || L % 256 == 0, "sharded backward needs L_local % 256 == 0");
+        REQUIRE(shard->stage != 1 || (shard->k_all && shard->v_all && shard->dk_part && shard->dv_part),
+                "backward shard stage 1 needs the gathered keys and the partial-gradient buffers");
+        REQUIRE(shard->stage != 2 || (shard->dk_own && shard->dv_own && shard->dt_sums),
+                "backward shard stage 2 needs the reduced key gradients and a dt_sums buffer");
+        REQUIRE(shard->stage != 3 || shard->dt_sums, "backward shard stage 3 needs the global dt_sums");
+    }
+    const bool st1 = shard == nullptr || shard->stage == 1;
+    const bool st2 = shard == nullptr || shard->stage == 2;
+    const bool st3 = shard == nullptr || shard->stage == 3;
     mark(0);
+    if (st1) {
     cuda_check(cudaMemsetAsync(dw_out, 0, (woff[10] - woff[8]) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.red, 0, (H + std::size_t(H) * d.d_z) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.dwproj, 0, std::size_t(d.d_in) * d.n_proj * 4, stream), "memset");
@@ -1055,16 +1069,26 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.acc_ld = kAccLd;
         a.B = int(B);
         a.L = int(L);
+        if (shard != nullptr) {  // local queries against all G shards' keys; partial dK / dV
+            a.khat = static_cast<const __nv_bfloat16*>(shard->k_all);
+            a.vhat = static_cast<const __nv_bfloat16*>(shard->v_all);
+            a.Lk = int(L) * G;
+            a.kchunk = int(L);
+            a.dk_acc = shard->dk_part;
+            a.dv_acc = shard->dv_part;
+        }
         launch_attn_bwd(d, a, stream, 1);
         mark(5);
         launch_attn_bwd(d, a, stream, 2);
     }
     mark(6);
+    }  // stage 1
+    if (st2) {
     {
         BwdUnpackArgs a{};
         a.dq_acc = ws.dq_acc;
-        a.dk_acc = ws.dk_acc;
-        a.dv_acc = ws.dv_acc;
+        a.dk_acc = shard ? shard->dk_own : ws.dk_acc;
+        a.dv_acc = shard ? shard->dv_own : ws.dv_acc;
         a.acc_ld = kAccLd;
         a.proj = ws.proj;
         a.rot = rot;
@@ -1089,7 +1113,17 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         launch_bwd_unpack(d, a, stream);
     }
     mark(7);
-    if (dtrans != nullptr) launch_bwd_recenter(ws.dt_c, mask, dtrans, int(B), int(L), stream);
+    if (shard != nullptr) launch_centroid_sums(ws.dt_c, mask, shard->dt_sums, int(B), int(L), stream);
+    }  // stage 2
+    if (st3) {
+    if (dtrans != nullptr) {
+        if (shard != nullptr) {  // dt = mask (dt_c - mean over the valid rows of ALL shards)
+            launch_recenter_with_sums(ws.dt_c, shard->dt_sums, dtrans, int(B), int(L), stream,
+                                      mask != nullptr ? mask : nullptr);
+        } else {
+            launch_bwd_recenter(ws.dt_c, mask, dtrans, int(B), int(L), stream);
+        }
+    }
     mark(8);
     {  // ds = dproj . W^T
         GemmArgs g;
@@ -1140,6 +1174,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
     launch_scale_vec(ws.red + H, d_bwd_scale_ + H, 1, dw_bias, H * d.d_z, stream);
     launch_scale_vec(ws.red, d_bwd_scale_, H, dgamma, H, stream);
     mark(11);
+    }  // stage 3
     if (timing_) bwd_timed_once_ = true;
     cuda_check(cudaGetLastError(), "backward launch");
 }

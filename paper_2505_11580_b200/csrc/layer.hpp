@@ -90,6 +90,8 @@ public:
     int rank() const { return rank_; }
     void all_reduce_sum_f32(float* buf, std::size_t n, cudaStream_t stream);
     void all_gather_bytes(const void* send, void* recv, std::size_t bytes, cudaStream_t stream);
+    // recv[n] = sum over ranks of send[rank_ * n .. ], send holding world() blocks of n floats
+    void reduce_scatter_sum_f32(const float* send, float* recv, std::size_t n, cudaStream_t stream);
 
 private:
     int world_, rank_, device_;
@@ -106,6 +108,27 @@ struct ShardStage {
     const void* k_all = nullptr;   // stage 2
     const void* v_all = nullptr;
     int groups = 1;
+};
+
+// Stage of the query-row-sharded backward (rank r owns residues [r L, (r+1) L) of G L):
+//   1: dOut -> dfeat, dw_out, prep, attention backward against the GATHERED keys: dQ for the local
+//      queries, PARTIAL dK/dV for all keys -> dk_part / dv_part [G][B][L][H][448] (rank-major)
+//   -- caller: reduce-scatter (sum) dk_part / dv_part -> this rank's keys (dk_own / dv_own)
+//   2: unpack with dk_own / dv_own -> dz1, dz2, drot; per-sample sums of the recentred-translation
+//      gradient -> dt_sums [B,4] (local)
+//   -- caller: all-reduce dt_sums
+//   3: dtrans (recentring with the global sums), ds, weight gradients (local)
+//   -- caller: all-reduce the weight gradients
+struct BwdShard {
+    int stage = 1;
+    int groups = 1;
+    const void* k_all = nullptr;  // gathered k_hat / v_hat [G][B*H][L][pad] (stage 1)
+    const void* v_all = nullptr;
+    float* dk_part = nullptr;     // stage 1 outputs
+    float* dv_part = nullptr;
+    const float* dk_own = nullptr;  // stage 2 inputs
+    const float* dv_own = nullptr;
+    float* dt_sums = nullptr;     // stage 2 output (local) / stage 3 input (global)
 };
 
 class FlashIpaLayer {
@@ -138,7 +161,8 @@ public:
     void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                   const float* rot, const float* trans, const std::uint8_t* mask, const float* dout,
                   float* ds, float* dz1, float* dz2, float* drot, float* dtrans, float* dweights,
-                  void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+                  void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
+                  const BwdShard* shard = nullptr);
     void grad_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
                    const double* rot, const double* trans, const std::uint8_t* mask, const double* dout,
                    double* out, double* ds, double* dz1, double* dz2, double* drot, double* dtrans,
@@ -203,10 +227,22 @@ public:
         void* k_all = nullptr;
         void* v_all = nullptr;
         float* sums = nullptr;
+        float* dk_part = nullptr;  // training: [G][B][L][H][448] partial key gradients
+        float* dv_part = nullptr;
+        float* dt_sums = nullptr;  // training: [B,4]
         std::size_t kv_bytes = 0, v_bytes = 0, bytes = 0;
     };
-    ShardedWorkspace carve_sharded(void* base, std::int64_t B, std::int64_t L, int groups) const;
+    ShardedWorkspace carve_sharded(void* base, std::int64_t B, std::int64_t L, int groups, bool train = false) const;
     std::size_t sharded_workspace_size(std::int64_t B, std::int64_t L, int groups) const;
+    // Sharded training (NCCL): forward keeps the gathered keys in the workspace for the backward.
+    std::size_t sharded_train_workspace_size(std::int64_t B, std::int64_t L, int groups) const;
+    void forward_train_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                               const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                               float* out, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+    void backward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                          const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                          const float* dout, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                          float* dweights, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
     void forward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
                          const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
                          float* out, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);

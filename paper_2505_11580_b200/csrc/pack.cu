@@ -590,13 +590,14 @@ __global__ void centroid_sums_kernel(const float* __restrict__ trans, const uint
 }
 
 __global__ void recenter_with_sums_kernel(const float* __restrict__ trans, const float* __restrict__ sums,
-                                          float* __restrict__ out, int L) {
+                                          const uint8_t* __restrict__ zero_masked, float* __restrict__ out, int L) {
     const int b = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= L) return;
     const float n = sums[b * 4 + 3] > 0.f ? sums[b * 4 + 3] : 1.f;
     const int64_t r = (int64_t(b) * L + i) * 3;
-    for (int x = 0; x < 3; ++x) out[r + x] = trans[r + x] - sums[b * 4 + x] / n;
+    const bool zero = zero_masked != nullptr && zero_masked[int64_t(b) * L + i] == 0;
+    for (int x = 0; x < 3; ++x) out[r + x] = zero ? 0.f : trans[r + x] - sums[b * 4 + x] / n;
 }
 
 // Trunk step (BASELINE cfg3, oracle/fipa_oracle.py trunk_forward): s <- s + ipa_out, then the
@@ -655,9 +656,10 @@ void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, 
     centroid_sums_kernel<<<B, 256, 0, stream>>>(trans, mask, sums, L);
 }
 
-void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream) {
+void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream,
+                               const uint8_t* zero_masked) {
     dim3 grid((L + 255) / 256, B);
-    recenter_with_sums_kernel<<<grid, 256, 0, stream>>>(trans, sums, out, L);
+    recenter_with_sums_kernel<<<grid, 256, 0, stream>>>(trans, sums, zero_masked, out, L);
 }
 
 void launch_pack(const LayerDims& d, const PackArgs& a, cudaStream_t stream) {
