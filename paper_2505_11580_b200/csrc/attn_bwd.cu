@@ -50,10 +50,8 @@ namespace {
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
-constexpr int kMaxStages1 = 8;  // B1 ring: groups of kb1 128-byte column blocks of a 32-row tile half
-constexpr int kMaxStages2 = 8;  // 16-row B2 slices: as many as fit beside the stationary tile, the
-                                // two P/dS buffers and the B1 ring (3 x 8 KB in the KV kernel,
-                                // 6 x 4 KB in the dQ kernel whose pairs stream half the columns)
+constexpr int kStages1 = 2;     // B1 ring: whole 32-row tile halves
+constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
 constexpr int kSlice = 16;
 constexpr int kSliceBox = kSlice * 128;
 constexpr uint32_t kXCol = 448;
@@ -70,9 +68,11 @@ struct RoleDims {
 struct BwdParams {
     int Lrow, Lcol, H, B;       // rows (keys in KV, queries in Q) / tile columns
     int stat_chunk, col_chunk;  // rows per shard of the stationary / column operands (sharded keys)
+    int stat_sharded, col_sharded;  // 1: operand read through the 5-D / 4-D rank-major maps (measured
+                                    // ~10% slower per box than the unsharded 4-D / 3-D maps)
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
     int stat_bytes, b1_stage, b2_stage, nst2;
-    int kb1, nst1;     // B1 ring: column blocks per stage, stages
+    int kb1;           // column blocks per B1 stage (= nb1: whole tiles)
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -83,7 +83,7 @@ struct BwdParams {
 
 struct Bars {
     uint64_t stat_full;
-    uint64_t b1_full[kMaxStages1], b1_empty[kMaxStages1];
+    uint64_t b1_full[kStages1], b1_empty[kStages1];
     uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
     uint64_t x_full, x_free, a_full, acc_full;
     uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
@@ -99,7 +99,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.stat = 0;
     l.abuf = p.stat_bytes;
     l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
-    l.b2 = l.b1 + p.nst1 * p.b1_stage;
+    l.b2 = l.b1 + kStages1 * p.b1_stage;
     l.bars = l.b2 + p.nst2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
@@ -154,7 +154,9 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
     }
 }
 
-template <bool KV>
+// NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
+// and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
+template <bool KV, int NST2>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
@@ -191,7 +193,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(mB1);
         if (has_mma2) ptx::tma_prefetch(mB2);
         ptx::mbar_init(&bars->stat_full, 1);
-        for (int s = 0; s < p.nst1; ++s) {
+        for (int s = 0; s < kStages1; ++s) {
             ptx::mbar_init(&bars->b1_full[s], 1);
             ptx::mbar_init(&bars->b1_empty[s], 1);
         }
@@ -222,49 +224,64 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         // ------------------------------------------- stationary tile + B1 tile producer
         if (lane == 0) {
             if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
-            {
+            if (p.stat_sharded) {
                 const int g = r0 / p.stat_chunk;  // rows past the end land in shard G: TMA zero fill
                 ptx::tma_load_5d_2sm(sStat, mStat, &bars->stat_full, 0, r0 - g * p.stat_chunk, 0, bh, g);
+            } else {
+                ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
             }
-            const int nk1 = (rd.nb1 + p.kb1 - 1) / p.kb1;  // stages per tile
-            int s = 0, ph = 0, n = 0;
+            const int stage = rd.nb1 * 32 * 128;
             for (int j = 0; j < ntiles; ++j) {
+                const int s = j % kStages1;
+                if (j >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((j / kStages1) - 1) & 1);
                 BTRACE(11, j);
-                for (int u = 0; u < nk1; ++u, ++n) {
-                    if (n >= p.nst1) ptx::mbar_wait(&bars->b1_empty[s], ph ^ 1);
-                    if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * p.b1_stage);
-                    const int key = j * BN + 32 * static_cast<int>(prank);
+                if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
+                const int key = j * BN + 32 * static_cast<int>(prank);
+                if (p.col_sharded) {
                     const int g = key / p.col_chunk;
-                    ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk,
-                                         u * p.kb1, bh, g);
-                    if (++s == p.nst1) {
-                        s = 0;
-                        ph ^= 1;
-                    }
+                    ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk, 0,
+                                         bh, g);
+                } else {
+                    ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key, 0, bh);
                 }
             }
         }
     } else if (warp == 10) {
         // ------------------------------------------------------------ B2 slice producer
         if (lane == 0 && has_mma2) {
+            // the refill of a slice sits on the critical path: no division or branching between the
+            // empty-barrier wait and the TMA issues (slot / phase by counters, columns precomputed)
             const int halfa = rd.n2a / 2, halfb = rd.n2b / 2;
             const int stage_bytes = (rd.nba + rd.nbb) * kSliceBox;
             const int nslices = ntiles * (BN / kSlice);
+            const int col_a = p.b2_col0[role] + halfa * static_cast<int>(prank);
+            const int col_b = p.b2_col0[role] + rd.n2a + halfb * static_cast<int>(prank);
+            int g = 0, rloc = 0;
             for (int n = 0; n < nslices; ++n) {
-                const int s = n % p.nst2;
-                if (n >= p.nst2) ptx::mbar_wait(&bars->b2_empty[s], ((n / p.nst2) - 1) & 1);
+                const int s = n % NST2;
+                if (n >= NST2) ptx::mbar_wait(&bars->b2_empty[s], ((n / NST2) - 1) & 1);
                 BTRACE(12, n);
                 if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
                 uint8_t* dst = sB2 + s * p.b2_stage;
-                const int row = n * kSlice;
-                const int g = row / p.col_chunk, rloc = row - g * p.col_chunk;
-                const int col0 = p.b2_col0[role];
-                for (int x = 0; x < rd.nba; ++x)
-                    ptx::tma_load_4d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s],
-                                         col0 + halfa * static_cast<int>(prank) + 64 * x, rloc, bh, g);
-                for (int x = 0; x < rd.nbb; ++x)
-                    ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
-                                         col0 + rd.n2a + halfb * static_cast<int>(prank) + 64 * x, rloc, bh, g);
+                if (p.col_sharded) {
+                    for (int x = 0; x < rd.nba; ++x)
+                        ptx::tma_load_4d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, rloc, bh, g);
+                    for (int x = 0; x < rd.nbb; ++x)
+                        ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s], col_b + 64 * x,
+                                             rloc, bh, g);
+                } else {
+                    const int row = n * kSlice;
+                    for (int x = 0; x < rd.nba; ++x)
+                        ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, row, bh);
+                    for (int x = 0; x < rd.nbb; ++x)
+                        ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s], col_b + 64 * x,
+                                             row, bh);
+                }
+                rloc += kSlice;  // shard-local row of the next slice
+                if (rloc >= p.col_chunk) {
+                    rloc -= p.col_chunk;
+                    ++g;
+                }
             }
         }
     } else if (warp == 1) {
@@ -289,35 +306,28 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1_base = ptx::smem_u32(sB1);
             const uint32_t b2_base = ptx::smem_u32(sB2);
             const int k1_steps = rd.k1 / 16;
-            const int nk1 = (rd.nb1 + p.kb1 - 1) / p.kb1;
-            int s1 = 0, ph1 = 0, s2 = 0, ph2 = 0;
+            (void)0;
             ptx::mbar_wait(&bars->stat_full, 0);
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
                     if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
                     if (lane == 0) BTRACE(2, j);
-                    for (int u = 0; u < nk1; ++u) {
-                        ptx::mbar_wait(&bars->b1_full[s1], ph1);
-                        if (lane == 0 && u == 0) BTRACE(0, j);
-                        ptx::tc_fence_after();
-                        if (ptx::elect_one()) {
-                            const uint32_t bb = b1_base + s1 * p.b1_stage;
-                            const int k_lo = u * p.kb1 * 4, k_hi = min(k1_steps, (u + 1) * p.kb1 * 4);
-                            for (int kk = k_lo; kk < k_hi; ++kk) {
-                                const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
-                                const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
-                                const uint64_t db = ptx::sw128_desc(bb + (blk - u * p.kb1) * (32 * 128) + sub, 16, 1024);
-                                ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
-                            }
-                            ptx::mma_commit_2sm(&bars->b1_empty[s1], pair_mask);
-                            if (u == nk1 - 1) ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                    const int s = j % kStages1;
+                    ptx::mbar_wait(&bars->b1_full[s], (j / kStages1) & 1);
+                    if (lane == 0) BTRACE(0, j);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t bb = b1_base + s * p.b1_stage;
+                        for (int kk = 0; kk < k1_steps; ++kk) {
+                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
+                            const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
+                            const uint64_t db = ptx::sw128_desc(bb + blk * (32 * 128) + sub, 16, 1024);
+                            ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
                         }
-                        __syncwarp();
-                        if (++s1 == p.nst1) {
-                            s1 = 0;
-                            ph1 ^= 1;
-                        }
+                        ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
+                        ptx::mma_commit_2sm(&bars->x_full, pair_mask);
                     }
+                    __syncwarp();
                 }
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
@@ -325,12 +335,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
                     if (lane == 0) BTRACE(1, jj);
                     for (int h2 = 0; h2 < BN / kSlice; ++h2) {
-                        const int s = s2;
-                        ptx::mbar_wait(&bars->b2_full[s], ph2);
-                        if (++s2 == p.nst2) {  // ring position by counters: no division on the issue path
-                            s2 = 0;
-                            ph2 ^= 1;
-                        }
+                        const int n = jj * (BN / kSlice) + h2;
+                        const int s = n % NST2;
+                        ptx::mbar_wait(&bars->b2_full[s], (n / NST2) & 1);
                         if (lane == 0 && h2 == BN / kSlice - 1) BTRACE(13, jj);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
@@ -537,81 +544,43 @@ RoleDims make_role(int k1, int n2) {
     return r;
 }
 
-// Ring plan: the stationary tile (128 rows x all column blocks) and the two P/dS buffers are
-// fixed; the rest of shared memory is split between the B1 ring (groups of kb1 column blocks of
-// the 32-row tile half) and the B2 ring (16-row slices).  Preference: the plan whose shallower
-// ring, in tiles of lead, is deepest (B1 moves nb1 blocks per tile, B2 four slices per tile).
+// Ring plan: the stationary tile (128 rows x all column blocks), the two P/dS buffers and the B1
+// ring (two whole 32-row tile halves) are fixed; the B2 ring of 16-row slices takes what is left,
+// as a compile-time depth of 6 (the dQ kernel, whose pairs stream half the columns, 4 KB slices)
+// or 3 (the dK/dV kernel, 8 KB slices).  Whole-tile B1 stages measured faster than column-block
+// groups with a deeper B2 ring (dK/dV 0.405 vs 0.439 ms at B=8 L=1024, same-box A/B).
 void finish_params(BwdParams& p) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
     p.stat_bytes = nb1 * BM * 128;
+    p.kb1 = nb1;
+    p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    int forced[3] = {0, 0, 0};
-    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d,%d", &forced[0], &forced[1], &forced[2]);
-    // measured at the north-star shape (B=8 L=1024): whole-tile B1 stages with a 6-deep B2 ring
-    // where they fit (dQ kernel), else 4-block B1 groups x 3 with 4 B2 slices (dK/dV kernel);
-    // deeper B2 rings with small B1 stages measured slower
-    if (forced[0] == 0) {
-        const int pref[][3] = {{nb1, 2, 6}, {4, 3, 4}, {nb1, 2, 3}};
-        for (const auto& c : pref) {
-            BwdParams q = p;
-            q.kb1 = std::min(c[0], nb1);
-            q.nst1 = c[1];
-            q.nst2 = c[2];
-            q.b1_stage = q.kb1 * 32 * 128;
-            if (smem_layout(q).total + 1024 <= 232448) {
-                p = q;
-                return;
-            }
-        }
+    for (int depth : {6, 3, 2}) {
+        p.nst2 = depth;
+        if (smem_layout(p).total + 1024 <= 232448) return;
     }
-    double best = -1.0;
-    BwdParams bestp = p;
-    for (int kb1 = 1; kb1 <= nb1; ++kb1) {
-        for (int nst1 = 2; nst1 <= kMaxStages1; ++nst1) {
-            for (int nst2 = 2; nst2 <= kMaxStages2; ++nst2) {
-                BwdParams q = p;
-                q.kb1 = kb1;
-                q.nst1 = nst1;
-                q.nst2 = nst2;
-                q.b1_stage = kb1 * 32 * 128;
-                if (smem_layout(q).total + 1024 > 232448) continue;
-                if (forced[0] > 0 && (kb1 != forced[0] || nst1 != forced[1] || nst2 != forced[2])) continue;
-                if (nst1 * kb1 < std::min(nb1, 2 * kb1)) continue;  // at least two stages in flight
-                const int nk1 = (nb1 + kb1 - 1) / kb1;              // stages per tile
-                const double lead1 = double(nst1) / nk1;            // tiles of B1 in flight
-                const double lead2 = double(nst2) / (BN / kSlice);   // tiles of B2 in flight
-                // shallower ring first, then fewer barrier round trips per tile (larger stages)
-                const double score = std::min(lead1, lead2) * 100.0 + kb1;
-                if (score > best) {
-                    best = score;
-                    bestp = q;
-                }
-            }
-        }
-    }
-    if (best < 0.0) {
-        if (forced[0] > 0) {  // a forced plan that does not fit: fall back to the automatic choice
-            unsetenv("FIPA_BWD_RING");
-            finish_params(p);
-            return;
-        }
-        throw std::invalid_argument("attention backward: no ring plan fits shared memory");
-    }
-    p = bestp;
+}
+
+template <bool KV, int NST2>
+void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
+                  cudaStream_t stream) {
+    const Layout lay = smem_layout(p);
+    const int smem = lay.total + 1024;
+    if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
+    auto kern = attn_bwd_kernel<KV, NST2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int clusters = (p.Lrow + 255) / 256;
+    dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
+    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
 }
 
 template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
-    const Layout lay = smem_layout(p);
-    const int smem = lay.total + 1024;
-    if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
-    auto kern = attn_bwd_kernel<KV>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int clusters = (p.Lrow + 255) / 256;
-    dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
-    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
+    if (p.nst2 == 6) launch_depth<KV, 6>(d, a, p, maps, stream);
+    else if (p.nst2 == 3) launch_depth<KV, 3>(d, a, p, maps, stream);
+    else launch_depth<KV, 2>(d, a, p, maps, stream);
 }
 
 }  // namespace
@@ -637,20 +606,27 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         throw std::invalid_argument("attention backward: key shards must be equal and a multiple of 256 rows");
     auto is_key = [&](const void* x) { return x == a.khat || x == a.vhat; };
     auto chunk_of = [&](const void* x) { return is_key(x) ? kc : a.L; };
-    auto g_of = [&](const void* x) { return is_key(x) ? G : 1; };
+    auto sharded = [&](const void* x) { return is_key(x) && G > 1; };
     auto stat = [&](const void* x, int nb) {
-        return make_map_blocks_bf16_sharded(x, chunk_of(x), BH, g_of(x), ld_of(x), BM, nb);
+        return sharded(x) ? make_map_blocks_bf16_sharded(x, kc, BH, G, ld_of(x), BM, nb)
+                          : make_map_blocks_bf16(x, chunk_of(x), BH, ld_of(x), BM, nb);
     };
     auto tile = [&](const void* x, int kb) {
-        return make_map_blocks_bf16_sharded(x, chunk_of(x), BH, g_of(x), ld_of(x), 32, kb);
+        return sharded(x) ? make_map_blocks_bf16_sharded(x, kc, BH, G, ld_of(x), 32, kb)
+                          : make_map_blocks_bf16(x, chunk_of(x), BH, ld_of(x), 32, kb);
     };
-    auto slice = [&](const void* x) { return make_map_4d_bf16_sharded(x, ld_of(x), chunk_of(x), BH, g_of(x), 64, kSlice); };
+    auto slice = [&](const void* x) {
+        return sharded(x) ? make_map_4d_bf16_sharded(x, ld_of(x), kc, BH, G, 64, kSlice)
+                          : make_map_3d_bf16(x, ld_of(x), chunk_of(x), BH, ld_of(x), 64, kSlice);
+    };
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
         p.Lrow = Lk;  // rows = keys (all shards)
         p.Lcol = a.L; // tile columns = local queries
         p.stat_chunk = kc;
         p.col_chunk = a.L;
+        p.stat_sharded = G > 1;
+        p.col_sharded = 0;
         p.H = d.heads;
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
@@ -675,6 +651,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.Lcol = Lk;   // tile columns = keys (all shards)
         p.stat_chunk = a.L;
         p.col_chunk = kc;
+        p.stat_sharded = 0;
+        p.col_sharded = G > 1;
         p.H = d.heads;
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, nq0);
