@@ -50,7 +50,7 @@ namespace {
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
-constexpr int kStages1 = 2;     // B1 ring: whole 32-row tile halves
+constexpr int kMaxStages1 = 2;  // B1 ring: whole 32-row tile halves
 constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
 constexpr int kSlice = 16;
 constexpr int kSliceBox = kSlice * 128;
@@ -73,6 +73,7 @@ struct BwdParams {
     RoleDims role[2];  // 0 = P pair, 1 = dS pair
     int stat_bytes, b1_stage, b2_stage, nst2;
     int kb1;           // column blocks per B1 stage (= nb1: whole tiles)
+    int nst1;          // B1 ring depth (1 or 2)
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -83,7 +84,7 @@ struct BwdParams {
 
 struct Bars {
     uint64_t stat_full;
-    uint64_t b1_full[kStages1], b1_empty[kStages1];
+    uint64_t b1_full[kMaxStages1], b1_empty[kMaxStages1];
     uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
     uint64_t x_full, x_free, a_full, acc_full;
     uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
@@ -99,7 +100,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.stat = 0;
     l.abuf = p.stat_bytes;
     l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
-    l.b2 = l.b1 + kStages1 * p.b1_stage;
+    l.b2 = l.b1 + p.nst1 * p.b1_stage;
     l.bars = l.b2 + p.nst2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
@@ -156,7 +157,7 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
 
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
-template <bool KV, int NST2>
+template <bool KV, int kStages1, int NST2>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
@@ -544,11 +545,10 @@ RoleDims make_role(int k1, int n2) {
     return r;
 }
 
-// Ring plan: the stationary tile (128 rows x all column blocks), the two P/dS buffers and the B1
-// ring (two whole 32-row tile halves) are fixed; the B2 ring of 16-row slices takes what is left,
-// as a compile-time depth of 6 (the dQ kernel, whose pairs stream half the columns, 4 KB slices)
-// or 3 (the dK/dV kernel, 8 KB slices).  Whole-tile B1 stages measured faster than column-block
-// groups with a deeper B2 ring (dK/dV 0.405 vs 0.439 ms at B=8 L=1024, same-box A/B).
+// Ring plan: the stationary tile (128 rows x all column blocks) and the two P/dS buffers are
+// fixed; whole 32-row B1 tile halves (1 or 2 stages) and 16-row B2 slices (compile-time depth)
+// share the rest: dQ kernel (2, 6 x 4 KB), dK/dV kernel (1, 6 x 8 KB).  Whole-tile B1 stages
+// measured faster than column-block groups (dK/dV 0.406 vs 0.439 ms at B=8 L=1024, same-box A/B).
 void finish_params(BwdParams& p) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
@@ -556,19 +556,32 @@ void finish_params(BwdParams& p) {
     p.kb1 = nb1;
     p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    for (int depth : {6, 3, 2}) {
-        p.nst2 = depth;
+    int forced[2] = {0, 0};  // FIPA_BWD_RING="nst1,nst2": tuning experiments
+    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d", &forced[0], &forced[1]);
+    if (forced[0] > 0) {
+        p.nst1 = forced[0];
+        p.nst2 = forced[1];
+        if (smem_layout(p).total + 1024 <= 232448 &&
+            ((p.nst1 == 2 && (p.nst2 == 6 || p.nst2 == 3 || p.nst2 == 2)) || (p.nst1 == 1 && p.nst2 == 6)))
+            return;
+    }
+    // (B1 stages, B2 stages), preferred first: a 6-deep B2 ring beats the second B1 stage
+    // (dK/dV kernel 0.406 with (1, 6) vs 0.416 ms with (2, 3))
+    const int plans[][2] = {{2, 6}, {1, 6}, {2, 3}, {2, 2}};
+    for (const auto& pl : plans) {
+        p.nst1 = pl[0];
+        p.nst2 = pl[1];
         if (smem_layout(p).total + 1024 <= 232448) return;
     }
 }
 
-template <bool KV, int NST2>
+template <bool KV, int NS1, int NST2>
 void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
                   cudaStream_t stream) {
     const Layout lay = smem_layout(p);
     const int smem = lay.total + 1024;
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
-    auto kern = attn_bwd_kernel<KV, NST2>;
+    auto kern = attn_bwd_kernel<KV, NS1, NST2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
@@ -578,9 +591,10 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
 template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
-    if (p.nst2 == 6) launch_depth<KV, 6>(d, a, p, maps, stream);
-    else if (p.nst2 == 3) launch_depth<KV, 3>(d, a, p, maps, stream);
-    else launch_depth<KV, 2>(d, a, p, maps, stream);
+    if (p.nst1 == 1) launch_depth<KV, 1, 6>(d, a, p, maps, stream);
+    else if (p.nst2 == 6) launch_depth<KV, 2, 6>(d, a, p, maps, stream);
+    else if (p.nst2 == 3) launch_depth<KV, 2, 3>(d, a, p, maps, stream);
+    else launch_depth<KV, 2, 2>(d, a, p, maps, stream);
 }
 
 }  // namespace
