@@ -87,11 +87,14 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: through NVML every 2 ms when
+    the bindings are importable (nvidia_ml_py), else nvidia-smi every 200 ms."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index):
         self.index = index
@@ -99,7 +102,28 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        while not self._stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = get_reasons(h)
+            self.rows.append([str(sm), str(mx)] + ["Active" if bits & b else "Not Active" for b in self.BITS])
+            self._stop.wait(0.002)
+
     def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            try:
+                self._run_nvml(nv)
+                return
+            finally:
+                nv.nvmlShutdown()
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
