@@ -74,6 +74,7 @@ struct BwdParams {
     int stat_bytes, b1_stage, b2_stage, nst2;
     int kb1;           // column blocks per B1 stage (= nb1: whole tiles)
     int nst1;          // B1 ring depth (1 or 2)
+    int nab;           // P / dS exchange buffers (2 or 3)
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -87,8 +88,8 @@ struct Bars {
     uint64_t b1_full[kMaxStages1], b1_empty[kMaxStages1];
     uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
     uint64_t x_full, x_free, a_full, acc_full;
-    uint64_t mma2_done[2], pin_full[2], pin_free[2];  // per P / dS buffer
-    uint64_t dsin_full[2];                            // Q kernel: dS returned to the P pair
+    uint64_t mma2_done[3], pin_full[3], pin_free[3];  // per P / dS exchange buffer (2 or 3)
+    uint64_t dsin_full[3];                            // Q kernel: dS returned to the P pair
     uint32_t tmem_slot;
 };
 
@@ -99,7 +100,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     Layout l{};
     l.stat = 0;
     l.abuf = p.stat_bytes;
-    l.b1 = l.abuf + 2 * BM * 128;  // two P (P pair) / received-P-then-dS (dS pair) buffers
+    l.b1 = l.abuf + p.nab * BM * 128;  // P (P pair) / received-P-then-dS (dS pair) exchange buffers
     l.b2 = l.b1 + p.nst1 * p.b1_stage;
     l.bars = l.b2 + p.nst2 * p.b2_stage;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
@@ -157,7 +158,7 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
 
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
-template <bool KV, int kStages1, int NST2>
+template <bool KV, int kStages1, int NST2, int NAB>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
@@ -207,7 +208,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         // Q kernel, P pair: the MMA operand (dS) arrives by copy; the odd CTA forwards its arrival
         ptx::mbar_init(&bars->a_full, (!KV && role == 0) ? 1 : 16);
         ptx::mbar_init(&bars->acc_full, 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 3; ++b) {
             ptx::mbar_init(&bars->mma2_done[b], 1);
             ptx::mbar_init(&bars->pin_full[b], 1);
             ptx::mbar_init(&bars->pin_free[b], 1);
@@ -293,7 +294,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             if (lane == 0) {
                 const uint32_t a_full_leader = ptx::mapa(&bars->a_full, crank & 2u);
                 for (int j = 0; j < ntiles; ++j) {
-                    ptx::mbar_wait(&bars->dsin_full[j & 1], (j >> 1) & 1);
+                    ptx::mbar_wait(&bars->dsin_full[j % NAB], (j / NAB) & 1);
                     ptx::mbar_arrive_remote(a_full_leader);
                 }
             }
@@ -332,7 +333,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
-                    if (!KV && role == 0) ptx::mbar_wait(&bars->dsin_full[jj & 1], (jj >> 1) & 1);
+                    if (!KV && role == 0) ptx::mbar_wait(&bars->dsin_full[jj % NAB], (jj / NAB) & 1);
                     ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
                     if (lane == 0) BTRACE(1, jj);
                     for (int h2 = 0; h2 < BN / kSlice; ++h2) {
@@ -344,7 +345,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                         if (ptx::elect_one()) {
                             for (int kk = 0; kk < kSlice / 16; ++kk) {
                                 const uint64_t da = ptx::sw128_desc(
-                                    a_base + (jj & 1) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32, 16, 1024);
+                                    a_base + (jj % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32, 16, 1024);
                                 const uint32_t vb = b2_base + s * p.b2_stage + kk * 2048;
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
                                 ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kSliceBox, 1024), idesc2a, acc);
@@ -360,8 +361,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     if (ptx::elect_one()) {
                         // P pair: its P buffer is free again.  dS pair: the received-P buffer
                         // is free -> the P pair may send the next tile.
-                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done[jj & 1], pair_mask);
-                        else ptx::mma_commit_2sm(&bars->pin_free[jj & 1], 0x3);
+                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done[jj % NAB], pair_mask);
+                        else ptx::mma_commit_2sm(&bars->pin_free[jj % NAB], 0x3);
                         if (j == ntiles) ptx::mma_commit_2sm(&bars->acc_full, pair_mask);
                     }
                     __syncwarp();
@@ -388,7 +389,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
 
         for (int j = 0; j < ntiles; ++j) {
             const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
-            const int buf = j & 1;
+            const int buf = j % NAB;
             uint8_t* abuf = sA + buf * (BM * 128);
             uint8_t* arow = abuf + row * 128;
             if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full[buf], BM * 128);
@@ -435,9 +436,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 // Buffer `buf` held P_{j-2}: free once the local dV MMA of tile j-2 (KV) and the dS
                 // pair's MMA of tile j-2 (which implies the copy of P_{j-2} landed) are done; the
                 // latter also frees the dS pair's buffer `buf` for the copy of P_j.
-                if (j >= 2) {
-                    if (has_mma2) ptx::mbar_wait(&bars->mma2_done[buf], ((j >> 1) - 1) & 1);
-                    ptx::mbar_wait_cluster(&bars->pin_free[buf], ((j >> 1) - 1) & 1);
+                if (j >= NAB) {
+                    if (has_mma2) ptx::mbar_wait(&bars->mma2_done[buf], ((j / NAB) - 1) & 1);
+                    ptx::mbar_wait_cluster(&bars->pin_free[buf], ((j / NAB) - 1) & 1);
                     ptx::tc_fence_after();
                 }
                 // Q kernel: dS_j comes back into this buffer once the dS pair has it (the copy of
@@ -461,7 +462,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     BTRACE(7, j);
                 }
             } else {
-                ptx::mbar_wait_cluster(&bars->pin_full[buf], (j >> 1) & 1);
+                ptx::mbar_wait_cluster(&bars->pin_full[buf], (j / NAB) & 1);
                 if (lane == 0) BTRACE(9, j);
                 uint4 pin[4];
 #pragma unroll
@@ -549,39 +550,41 @@ RoleDims make_role(int k1, int n2) {
 // fixed; whole 32-row B1 tile halves (1 or 2 stages) and 16-row B2 slices (compile-time depth)
 // share the rest: dQ kernel (2, 6 x 4 KB), dK/dV kernel (1, 6 x 8 KB).  Whole-tile B1 stages
 // measured faster than column-block groups (dK/dV 0.406 vs 0.439 ms at B=8 L=1024, same-box A/B).
-void finish_params(BwdParams& p) {
+void finish_params(BwdParams& p, bool kv) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
     p.stat_bytes = nb1 * BM * 128;
     p.kb1 = nb1;
     p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    int forced[2] = {0, 0};  // FIPA_BWD_RING="nst1,nst2": tuning experiments
-    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d", &forced[0], &forced[1]);
-    if (forced[0] > 0) {
-        p.nst1 = forced[0];
-        p.nst2 = forced[1];
-        if (smem_layout(p).total + 1024 <= 232448 &&
-            ((p.nst1 == 2 && (p.nst2 == 6 || p.nst2 == 3 || p.nst2 == 2)) || (p.nst1 == 1 && p.nst2 == 6)))
-            return;
+    int forced[3] = {0, 0, 0};  // FIPA_BWD_RING="nst1,nst2,nab": tuning experiments
+    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d,%d", &forced[0], &forced[1], &forced[2]);
+    // (B1 stages, B2 stages, exchange buffers), preferred first.  Measured (B=8 L=1024, same box):
+    // dK/dV kernel (1,6,2) 0.392 ms vs (1,4,3) 0.397; dQ kernel (1,4,3) 0.349 vs (2,6,2) 0.358.
+    const int plans_kv[][3] = {{2, 6, 2}, {1, 6, 2}, {2, 3, 2}, {2, 2, 2}, {1, 4, 3}, {1, 6, 3}};
+    const int plans_q[][3] = {{1, 4, 3}, {2, 6, 2}, {1, 6, 2}, {2, 3, 2}, {2, 2, 2}, {1, 6, 3}};
+    const auto& plans = kv ? plans_kv : plans_q;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (const auto& pl : plans) {
+            if (pass == 0 && forced[0] > 0 && (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2]))
+                continue;
+            if (pass == 0 && forced[0] == 0) break;
+            p.nst1 = pl[0];
+            p.nst2 = pl[1];
+            p.nab = pl[2];
+            if (smem_layout(p).total + 1024 <= 232448) return;
+        }
     }
-    // (B1 stages, B2 stages), preferred first: a 6-deep B2 ring beats the second B1 stage
-    // (dK/dV kernel 0.406 with (1, 6) vs 0.416 ms with (2, 3))
-    const int plans[][2] = {{2, 6}, {1, 6}, {2, 3}, {2, 2}};
-    for (const auto& pl : plans) {
-        p.nst1 = pl[0];
-        p.nst2 = pl[1];
-        if (smem_layout(p).total + 1024 <= 232448) return;
-    }
+    throw std::invalid_argument("attention backward: no ring plan fits shared memory");
 }
 
-template <bool KV, int NS1, int NST2>
+template <bool KV, int NS1, int NST2, int NAB>
 void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
                   cudaStream_t stream) {
     const Layout lay = smem_layout(p);
     const int smem = lay.total + 1024;
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
-    auto kern = attn_bwd_kernel<KV, NS1, NST2>;
+    auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
@@ -591,10 +594,18 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
 template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
-    if (p.nst1 == 1) launch_depth<KV, 1, 6>(d, a, p, maps, stream);
-    else if (p.nst2 == 6) launch_depth<KV, 2, 6>(d, a, p, maps, stream);
-    else if (p.nst2 == 3) launch_depth<KV, 2, 3>(d, a, p, maps, stream);
-    else launch_depth<KV, 2, 2>(d, a, p, maps, stream);
+    if (p.nab == 3) {
+        if (p.nst2 == 4) launch_depth<KV, 1, 4, 3>(d, a, p, maps, stream);
+        else launch_depth<KV, 1, 6, 3>(d, a, p, maps, stream);
+    } else if (p.nst1 == 1) {
+        launch_depth<KV, 1, 6, 2>(d, a, p, maps, stream);
+    } else if (p.nst2 == 6) {
+        launch_depth<KV, 2, 6, 2>(d, a, p, maps, stream);
+    } else if (p.nst2 == 3) {
+        launch_depth<KV, 2, 3, 2>(d, a, p, maps, stream);
+    } else {
+        launch_depth<KV, 2, 2, 2>(d, a, p, maps, stream);
+    }
 }
 
 }  // namespace
@@ -604,7 +615,11 @@ bool attn_bwd_supported(const LayerDims& d) {
     BwdParams p{};
     p.role[0] = make_role(d.dqk_mma, d.dv_mma);
     p.role[1] = make_role(d.dv_mma, d.dqk_mma);
-    finish_params(p);
+    try {
+        finish_params(p, true);
+    } catch (const std::invalid_argument&) {
+        return false;
+    }
     return smem_layout(p).total + 1024 <= 232448;
 }
 
@@ -645,7 +660,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
-        finish_params(p);
+        finish_params(p, true);
         p.lse = a.lse;
         p.Dvec = a.Dvec;
         p.acc_out[0] = a.dv_acc;
@@ -671,7 +686,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, nq0);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma - nq0);
-        finish_params(p);
+        finish_params(p, false);
         p.lse = a.lse;
         p.Dvec = a.Dvec;
         p.acc_out[0] = a.dq_acc;
