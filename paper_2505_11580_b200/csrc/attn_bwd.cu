@@ -308,7 +308,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1_base = ptx::smem_u32(sB1);
             const uint32_t b2_base = ptx::smem_u32(sB2);
             const int k1_steps = rd.k1 / 16;
-            (void)0;
+            // descriptors advance by 64-bit adds of (byte offset >> 4): the issue thread's work per
+            // MMA is a couple of integer ops (it is on the critical path with ~35 MMAs per tile)
+            const uint64_t d_stat = ptx::sw128_desc(stat_base, 16, 1024);
+            const uint64_t d_b1 = ptx::sw128_desc(b1_base, 16, 1024);
+            const uint64_t d_a = ptx::sw128_desc(a_base, 16, 1024);
+            const uint64_t d_b2 = ptx::sw128_desc(b2_base, kSliceBox, 1024);
             ptx::mbar_wait(&bars->stat_full, 0);
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
@@ -319,12 +324,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     if (lane == 0) BTRACE(0, j);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t bb = b1_base + s * p.b1_stage;
-                        for (int kk = 0; kk < k1_steps; ++kk) {
-                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
-                            const uint64_t da = ptx::sw128_desc(stat_base + blk * (BM * 128) + sub, 16, 1024);
-                            const uint64_t db = ptx::sw128_desc(bb + blk * (32 * 128) + sub, 16, 1024);
-                            ptx::mma2_ss(tmem + kXCol, da, db, idesc1, kk != 0);
+                        const uint64_t db0 = d_b1 + static_cast<uint64_t>((s * p.b1_stage) >> 4);
+                        for (int blk = 0; 4 * blk < k1_steps; ++blk) {
+                            const uint64_t da_b = d_stat + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
+                            const uint64_t db_b = db0 + static_cast<uint64_t>((blk * (32 * 128)) >> 4);
+#pragma unroll
+                            for (int sub = 0; sub < 4; ++sub) {
+                                if (4 * blk + sub < k1_steps)
+                                    ptx::mma2_ss(tmem + kXCol, da_b + 2 * sub, db_b + 2 * sub, idesc1,
+                                                 (blk | sub) != 0);
+                            }
                         }
                         ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
                         ptx::mma_commit_2sm(&bars->x_full, pair_mask);
@@ -343,15 +352,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                         if (lane == 0 && h2 == BN / kSlice - 1) BTRACE(13, jj);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
+#pragma unroll
                             for (int kk = 0; kk < kSlice / 16; ++kk) {
-                                const uint64_t da = ptx::sw128_desc(
-                                    a_base + (jj % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32, 16, 1024);
-                                const uint32_t vb = b2_base + s * p.b2_stage + kk * 2048;
+                                const uint64_t da = d_a + static_cast<uint64_t>(
+                                    ((jj % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32) >> 4);
+                                const uint64_t db = d_b2 + static_cast<uint64_t>((s * p.b2_stage + kk * 2048) >> 4);
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
-                                ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kSliceBox, 1024), idesc2a, acc);
+                                ptx::mma2_ss(tmem, da, db, idesc2a, acc);
                                 if (rd.n2b > 0)
-                                    ptx::mma2_ss(tmem + rd.n2a, da,
-                                                 ptx::sw128_desc(vb + rd.nba * kSliceBox, kSliceBox, 1024),
+                                    ptx::mma2_ss(tmem + rd.n2a, da, db + static_cast<uint64_t>((rd.nba * kSliceBox) >> 4),
                                                  idesc2b, acc);
                             }
                             ptx::mma_commit_2sm(&bars->b2_empty[s], pair_mask);
