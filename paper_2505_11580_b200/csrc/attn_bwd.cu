@@ -50,7 +50,7 @@ namespace {
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
-constexpr int kMaxStages1 = 2;  // B1 ring: whole 32-row tile halves
+constexpr int kMaxStages1 = 3;  // B1 ring: whole 32-row tile halves, or groups of KB1 column blocks
 constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
 constexpr int kSlice = 16;
 constexpr int kSliceBox = kSlice * 128;
@@ -158,7 +158,7 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
 
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
-template <bool KV, int kStages1, int NST2, int NAB>
+template <bool KV, int kStages1, int NST2, int NAB, int KB1>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
@@ -232,19 +232,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
                 ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
             }
-            const int stage = rd.nb1 * 32 * 128;
+            const int nk1 = KB1 ? (rd.nb1 + KB1 - 1) / KB1 : 1;  // B1 stages per tile
+            const int stage = (KB1 ? KB1 : rd.nb1) * 32 * 128;
             for (int j = 0; j < ntiles; ++j) {
-                const int s = j % kStages1;
-                if (j >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((j / kStages1) - 1) & 1);
                 BTRACE(11, j);
-                if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
                 const int key = j * BN + 32 * static_cast<int>(prank);
-                if (p.col_sharded) {
-                    const int g = key / p.col_chunk;
-                    ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk, 0,
-                                         bh, g);
-                } else {
-                    ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key, 0, bh);
+                const int g = p.col_sharded ? key / p.col_chunk : 0;
+                for (int u = 0; u < nk1; ++u) {
+                    const int n = j * nk1 + u;
+                    const int s = n % kStages1;
+                    if (n >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((n / kStages1) - 1) & 1);
+                    if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
+                    if (p.col_sharded) {
+                        ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk,
+                                             u * KB1, bh, g);
+                    } else {
+                        ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key, u * KB1, bh);
+                    }
                 }
             }
         }
@@ -319,26 +323,31 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 if (j < ntiles) {
                     if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
                     if (lane == 0) BTRACE(2, j);
-                    const int s = j % kStages1;
-                    ptx::mbar_wait(&bars->b1_full[s], (j / kStages1) & 1);
-                    if (lane == 0) BTRACE(0, j);
-                    ptx::tc_fence_after();
-                    if (ptx::elect_one()) {
-                        const uint64_t db0 = d_b1 + static_cast<uint64_t>((s * p.b1_stage) >> 4);
-                        for (int blk = 0; 4 * blk < k1_steps; ++blk) {
-                            const uint64_t da_b = d_stat + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
-                            const uint64_t db_b = db0 + static_cast<uint64_t>((blk * (32 * 128)) >> 4);
+                    const int nk1 = KB1 ? (rd.nb1 + KB1 - 1) / KB1 : 1;
+                    for (int u = 0; u < nk1; ++u) {
+                        const int n = j * nk1 + u;
+                        const int s = n % kStages1;
+                        ptx::mbar_wait(&bars->b1_full[s], (n / kStages1) & 1);
+                        if (lane == 0 && u == 0) BTRACE(0, j);
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            const uint64_t db0 = d_b1 + static_cast<uint64_t>((s * p.b1_stage) >> 4);
+                            const int b_lo = u * KB1, b_hi = KB1 ? min(rd.nb1, (u + 1) * KB1) : rd.nb1;
+                            for (int blk = b_lo; blk < b_hi; ++blk) {
+                                const uint64_t da_b = d_stat + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
+                                const uint64_t db_b = db0 + static_cast<uint64_t>(((blk - b_lo) * (32 * 128)) >> 4);
 #pragma unroll
-                            for (int sub = 0; sub < 4; ++sub) {
-                                if (4 * blk + sub < k1_steps)
-                                    ptx::mma2_ss(tmem + kXCol, da_b + 2 * sub, db_b + 2 * sub, idesc1,
-                                                 (blk | sub) != 0);
+                                for (int sub = 0; sub < 4; ++sub) {
+                                    if (4 * blk + sub < k1_steps)
+                                        ptx::mma2_ss(tmem + kXCol, da_b + 2 * sub, db_b + 2 * sub, idesc1,
+                                                     (blk | sub) != 0);
+                                }
                             }
+                            ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
+                            if (u == nk1 - 1) ptx::mma_commit_2sm(&bars->x_full, pair_mask);
                         }
-                        ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
-                        ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                        __syncwarp();
                     }
-                    __syncwarp();
                 }
                 if (j > 0 && has_mma2) {
                     const int jj = j - 1;
@@ -566,34 +575,41 @@ void finish_params(BwdParams& p, bool kv) {
     p.kb1 = nb1;
     p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    int forced[3] = {0, 0, 0};  // FIPA_BWD_RING="nst1,nst2,nab": tuning experiments
-    if (const char* e = std::getenv("FIPA_BWD_RING")) std::sscanf(e, "%d,%d,%d", &forced[0], &forced[1], &forced[2]);
+    int forced[4] = {0, 0, 0, 0};  // FIPA_BWD_RING="nst1,nst2,nab,kb1": tuning experiments
+    if (const char* e = std::getenv("FIPA_BWD_RING"))
+        std::sscanf(e, "%d,%d,%d,%d", &forced[0], &forced[1], &forced[2], &forced[3]);
     // (B1 stages, B2 stages, exchange buffers), preferred first.  Measured (B=8 L=1024, same box):
     // dK/dV kernel (1,6,2) 0.392 ms vs (1,4,3) 0.397; dQ kernel (1,4,3) 0.349 vs (2,6,2) 0.358.
-    const int plans_kv[][3] = {{2, 6, 2}, {1, 6, 2}, {2, 3, 2}, {2, 2, 2}, {1, 4, 3}, {1, 6, 3}};
-    const int plans_q[][3] = {{1, 4, 3}, {2, 6, 2}, {1, 6, 2}, {2, 3, 2}, {2, 2, 2}, {1, 6, 3}};
+    // (kb1 = 0: whole-tile B1 stages)
+    const int plans_kv[][4] = {{2, 6, 2, 0}, {1, 6, 2, 0}, {2, 3, 2, 0}, {2, 2, 2, 0}, {1, 4, 3, 0}, {1, 6, 3, 0},
+                               {3, 4, 2, 4}};
+    const int plans_q[][4] = {{1, 4, 3, 0}, {2, 6, 2, 0}, {1, 6, 2, 0}, {2, 3, 2, 0}, {2, 2, 2, 0}, {1, 6, 3, 0},
+                              {3, 4, 2, 4}};
     const auto& plans = kv ? plans_kv : plans_q;
     for (int pass = 0; pass < 2; ++pass) {
         for (const auto& pl : plans) {
-            if (pass == 0 && forced[0] > 0 && (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2]))
+            if (pass == 0 && forced[0] > 0 &&
+                (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2] || pl[3] != forced[3]))
                 continue;
             if (pass == 0 && forced[0] == 0) break;
             p.nst1 = pl[0];
             p.nst2 = pl[1];
             p.nab = pl[2];
+            p.kb1 = pl[3] ? pl[3] : nb1;
+            p.b1_stage = p.kb1 * 32 * 128;
             if (smem_layout(p).total + 1024 <= 232448) return;
         }
     }
     throw std::invalid_argument("attention backward: no ring plan fits shared memory");
 }
 
-template <bool KV, int NS1, int NST2, int NAB>
+template <bool KV, int NS1, int NST2, int NAB, int KB1 = 0>
 void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
                   cudaStream_t stream) {
     const Layout lay = smem_layout(p);
     const int smem = lay.total + 1024;
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
-    auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB>;
+    auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB, KB1>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
@@ -603,7 +619,9 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
 template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
-    if (p.nab == 3) {
+    if (p.kb1 == 4 && p.nst1 == 3) {
+        launch_depth<KV, 3, 4, 2, 4>(d, a, p, maps, stream);
+    } else if (p.nab == 3) {
         if (p.nst2 == 4) launch_depth<KV, 1, 4, 3>(d, a, p, maps, stream);
         else launch_depth<KV, 1, 6, 3>(d, a, p, maps, stream);
     } else if (p.nst1 == 1) {

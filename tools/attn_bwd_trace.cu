@@ -53,10 +53,10 @@ int main(int argc, char** argv) {
     const long long t0 = T(0, 1, 0, 0);
     const int nt = (L + 63) / 64;
     for (int cta : {0, 2}) {
-        printf("leader cta%d: tile xfree_ok mma1_issue a_full_ok(mma2 issue) b2_last_full | b1_issue b2_issue(2j)\n", cta);
+        printf("leader cta%d: tile xfree_ok mma1_issue a_full_ok(mma2 issue) b2_last_full | b1_issue b2_issue(4j)\n", cta);
         for (int j = 0; j < nt && j < 64; ++j)
             printf("  %3d %8lld %8lld %8lld %8lld | %8lld %8lld\n", j, T(cta,1,2,j)-t0, T(cta,1,0,j)-t0, T(cta,1,1,j)-t0,
-                   T(cta,1,13,j)-t0, T(cta,0,11,j)-t0, T(cta,10,12,2*j)-t0);
+                   T(cta,1,13,j)-t0, T(cta,0,11,j)-t0, T(cta,10,12,4*j)-t0);
     }
     printf("P cta0 w2: tile x_full p_done mma2done_ok pin_free_ok\n");
     for (int j = 0; j < nt && j < 64; ++j)
