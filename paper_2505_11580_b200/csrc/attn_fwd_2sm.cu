@@ -353,6 +353,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t p_base = ptx::smem_u32(sP);
             const uint32_t k_base = ptx::smem_u32(sK);
             const uint32_t v_base = ptx::smem_u32(sV);
+            // descriptors advance by 64-bit adds of (byte offset >> 4)
+            const uint64_t d_q = ptx::sw128_desc(q_base, 16, 1024);
+            const uint64_t d_k = ptx::sw128_desc(k_base, 16, 1024);
+            const uint64_t d_p = ptx::sw128_desc(p_base, 16, 1024);
+            const uint64_t d_v = ptx::sw128_desc(v_base, kVBoxBytes, 1024);
             ptx::mbar_wait(&bars->q_full, 0);
             for (int j = 0; j <= ntiles; ++j) {
                 if (j < ntiles) {
@@ -363,12 +368,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (lane == 0) FIPA_TRACE(0, j);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t kb = k_base + ks * lay.kstage;
-                        for (int kk = 0; kk < qk_steps; ++kk) {
-                            const uint32_t blk = kk >> 2, sub = (kk & 3) * 32;
-                            const uint64_t da = ptx::sw128_desc(q_base + blk * (BM * 128) + sub, 16, 1024);
-                            const uint64_t db = ptx::sw128_desc(kb + blk * (32 * 128) + sub, 16, 1024);
-                            ptx::mma2_ss(tmem + kSCol, da, db, idesc_qk, kk != 0);
+                        const uint64_t dk0 = d_k + static_cast<uint64_t>((ks * lay.kstage) >> 4);
+                        for (int blk = 0; 4 * blk < qk_steps; ++blk) {
+                            const uint64_t da_b = d_q + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
+                            const uint64_t db_b = dk0 + static_cast<uint64_t>((blk * (32 * 128)) >> 4);
+#pragma unroll
+                            for (int sub = 0; sub < 4; ++sub)
+                                if (4 * blk + sub < qk_steps)
+                                    ptx::mma2_ss(tmem + kSCol, da_b + 2 * sub, db_b + 2 * sub, idesc_qk, (blk | sub) != 0);
                         }
                         ptx::mma_commit_2sm(&bars->k_empty[ks], 0x3);
                         ptx::mma_commit_2sm(&bars->s_full, 0x3);
@@ -386,14 +393,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (lane == 0 && h2 == 0) FIPA_TRACE(1, jj);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
+#pragma unroll
                             for (int kk = 0; kk < kVKeys / 16; ++kk) {
-                                const uint64_t da = ptx::sw128_desc(p_base + (2 * h2 + kk) * 32, 16, 1024);
-                                const uint32_t vb = v_base + vs * lay.vstage + kk * 2048;
+                                const uint64_t da = d_p + static_cast<uint64_t>(((2 * h2 + kk) * 32) >> 4);
+                                const uint64_t db = d_v + static_cast<uint64_t>((vs * lay.vstage + kk * 2048) >> 4);
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
-                                ptx::mma2_ss(tmem, da, ptx::sw128_desc(vb, kVBoxBytes, 1024), idesc_pv1, acc);
+                                ptx::mma2_ss(tmem, da, db, idesc_pv1, acc);
                                 if (p.n2 > 0)
-                                    ptx::mma2_ss(tmem + p.n1, da,
-                                                 ptx::sw128_desc(vb + p.nb1 * kVBoxBytes, kVBoxBytes, 1024),
+                                    ptx::mma2_ss(tmem + p.n1, da, db + static_cast<uint64_t>((p.nb1 * kVBoxBytes) >> 4),
                                                  idesc_pv2, acc);
                             }
                             ptx::mma_commit_2sm(&bars->v_empty[vs], 0x3);
