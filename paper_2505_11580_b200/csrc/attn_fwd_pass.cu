@@ -15,8 +15,10 @@
 //   * K streams through a ring of 128-byte column-block groups (kb blocks x 32 keys per CTA)
 //     instead of whole tiles; V slices are 16 or 32 keys.  Ring depths are chosen on the host
 //     from the shared-memory budget.
-// TMEM: S [0,64) | partial pair aggregate [64, 64+d_z) | O1 [64+d_z, ...) ; O0 [512-N0, 512)
-// (O0 may overlap the aggregate only in its scalar columns, which are consumed first).
+// TMEM: S [0,64) | P [64,96) (bf16 pairs, the A operand of the P.V MMAs: no shared-memory P tile,
+// which leaves that 16 KB to the operand rings) | partial pair aggregate (bf16 pairs) [96, 96+d_z/2)
+// | O1 [96+d_z/2, ...) ; O0 [512-N0, 512) (O0 may overlap the aggregate only in its scalar columns,
+// which are consumed first).
 //
 // Warps (352 threads per CTA): w0 Q/K producer, w1 TMEM alloc (+ MMA issue on the even CTA),
 // w2..w9 softmax + epilogue (quadrant w%4, key half (w-2)/4), w10 V producer.
@@ -41,7 +43,8 @@ constexpr int BM = 128;  // query rows per CTA (256 per pair)
 constexpr int BN = 64;   // keys per tile
 constexpr int kThreads = 352;
 constexpr int kMaxPoints = 14;
-constexpr uint32_t kOz = 64;  // TMEM column of the partial pair aggregate
+constexpr uint32_t kPc = 64;   // TMEM column of the bf16 P tile (64 keys = 32 columns)
+constexpr uint32_t kOz = 96;   // TMEM column of the bf16-packed partial pair aggregate (d_z / 2 columns)
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kSmemLimit = 232448;
 
@@ -76,8 +79,8 @@ __host__ __device__ inline Layout smem_layout(int n_qkb, int kb, int kst, int vk
     l.kstage = kb * 32 * 128;
     l.vstage = vboxes * vkeys * 128;
     l.q = 0;
-    l.p = n_qkb * BM * 128;
-    l.k = l.p + BM * 128;
+    l.p = 0;  // (P lives in TMEM)
+    l.k = n_qkb * BM * 128;
     l.v = l.k + kst * l.kstage;
     l.xch = l.v + vst * l.vstage;
     l.bars = l.xch + 2 * 2 * BM * 4;
@@ -114,7 +117,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int vboxes = max(p.boxa[0] + p.boxb[0], p.boxa[1] + p.boxb[1]);
     const Layout lay = smem_layout(p.n_qkb, p.kb, p.kst, p.vkeys, p.vst, vboxes);
     uint8_t* sQ = smem + lay.q;
-    uint8_t* sP = smem + lay.p;
     uint8_t* sK = smem + lay.k;
     uint8_t* sV = smem + lay.v;
     Bars* bars = reinterpret_cast<Bars*>(smem + lay.bars);
@@ -203,7 +205,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (leader) {
             const uint32_t idesc_qk = ptx::idesc_bf16(256, BN, false, false);
             const uint32_t q_base = ptx::smem_u32(sQ);
-            const uint32_t p_base = ptx::smem_u32(sP);
             const uint32_t k_base = ptx::smem_u32(sK);
             const uint32_t v_base = ptx::smem_u32(sV);
             ptx::mbar_wait(&bars->q_full, 0);
@@ -212,6 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int ks = 0, kph = 0, vs = 0, vph = 0;
             const uint64_t dq0 = ptx::sw128_desc(q_base, 16, 1024);
             const uint64_t dk0 = ptx::sw128_desc(k_base, 16, 1024);
+            const uint64_t dv0 = ptx::sw128_desc(v_base, p.vkeys * 128, 1024);
             for (int t = 0, ps_prev = 0, jj = -1; t <= T; ++t) {
                 if (t < T) {
                     if (t > 0) ptx::mbar_wait_cluster(&bars->s_free, (t - 1) & 1);
@@ -256,15 +258,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         ptx::mbar_wait(&bars->v_full[vs], vph);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
-                            const uint32_t vb0 = v_base + vs * lay.vstage;
+                            const uint64_t db0 = dv0 + static_cast<uint64_t>((vs * lay.vstage) >> 4);
                             for (int kk = 0; kk < p.vkeys / 16; ++kk) {
-                                const uint64_t da =
-                                    ptx::sw128_desc(p_base + (h2 * (p.vkeys / 16) + kk) * 32, 16, 1024);
-                                const uint32_t vb = vb0 + kk * 2048;
+                                // A = P from TMEM: 16 keys = 8 columns of bf16 pairs
+                                const uint32_t a_tm = tmem + kPc + (h2 * (p.vkeys / 16) + kk) * 8;
+                                const uint64_t db = db0 + static_cast<uint64_t>((kk * 2048) >> 4);
                                 const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
-                                ptx::mma2_ss(oa, da, ptx::sw128_desc(vb, boxb, 1024), idesc_a, acc);
+                                ptx::mma2_ts(oa, a_tm, db, idesc_a, acc);
                                 if (two)
-                                    ptx::mma2_ss(obb, da, ptx::sw128_desc(vb + p.boxa[ps] * boxb, boxb, 1024),
+                                    ptx::mma2_ts(obb, a_tm, db + static_cast<uint64_t>((p.boxa[ps] * boxb) >> 4),
                                                  idesc_b, acc);
                             }
                             ptx::mma_commit_2sm(&bars->v_empty[vs], 0x3);
@@ -293,7 +295,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t s_free_remote = ptx::mapa(&bars->s_free, 0);
         const uint32_t p_full_remote = ptx::mapa(&bars->p_full, 0);
         float* xch = reinterpret_cast<float*>(smem + lay.xch);  // [2 parity][2 half][128 rows]
-        uint8_t* prow = sP + row * 128;
         const int H = p.H, b = bh / H, h = bh % H;
         const int qi = q0 + row;
         const bool ok = qi < p.L;
@@ -423,21 +424,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int e = 0; e < 16; ++e) acc[e] = fmaf(z[e], __uint_as_float(o[e]), acc[e]);
                     }
-                    uint32_t o[16];
+                    uint32_t o[8];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(acc[e] * inv_l);
-                    ptx::tmem_st16(tl + kOz + d0, o);
+                    for (int e = 0; e < 8; ++e) o[e] = ptx::pack_bf16x2(acc[2 * e] * inv_l, acc[2 * e + 1] * inv_l);
+                    ptx::tmem_st8(tl + kOz + d0 / 2, o);
                 }
                 ptx::tmem_wait_st();
             }
-            // P row half in the SWIZZLE_128B K-major layout
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int chunk = 4 * half + k;
-                const uint4 v = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                *reinterpret_cast<uint4*>(prow + ((chunk ^ (row & 7)) << 4)) = v;
-            }
-            ptx::fence_proxy_async_smem();
+            // P row half into TMEM (bf16 pairs): the A operand of this tile's P.V MMAs
+            ptx::tmem_st16(tl + kPc + 16 * half, pk);
+            ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_remote(p_full_remote);
@@ -489,9 +485,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int d0 = 16 * ch;
             float acc[16];
             {
-                uint32_t o[16];
-                ptx::tmem_ld16(tl + kOz + d0, o);
+                uint32_t o8[8];
+                ptx::tmem_ld8(tl + kOz + d0 / 2, o8);
                 ptx::tmem_wait_ld();
+                uint32_t o[16];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    o[2 * e] = o8[e] << 16;              // low bf16 -> float bits
+                    o[2 * e + 1] = o8[e] & 0xFFFF0000u;  // high bf16
+                }
 #pragma unroll
                 for (int e = 0; e < 16; ++e) acc[e] = 0.f;
                 for (int rho = p.rho_a; rho < p.rank; ++rho) {
@@ -550,23 +552,26 @@ bool make_plan(const LayerDims& d, PassParams& p, Layout& lay) {
         return false;
     // largest rho_a with pass-0 width N0 = c + rho_a*d_z inside TMEM beside S and the aggregate
     int rho_a = -1;
+    // TS MMAs (A = P from TMEM) need N % 32 == 0: both passes are padded to 32 columns
+    auto up32 = [](int x) { return (x + 31) / 32 * 32; };
+    if (dz % 32 != 0) return false;
     for (int ra = r; ra >= 0; --ra) {
-        const int N0 = c + ra * dz, N1 = d.dv_mma - N0;
-        const int ob0 = 512 - N0, ob1 = static_cast<int>(kOz) + dz;
-        if (N0 < 16 || N1 < 16 || N0 > 448) continue;
-        if (ob0 < 64 || ob0 + c < static_cast<int>(kOz) + dz) continue;  // aggregate overlaps scalar cols only
-        if (ob1 + N1 > 512) continue;
+        const int N0 = c + ra * dz, N1 = up32(d.dv_mma - N0);
+        const int ob0 = 512 - N0, ob1 = static_cast<int>(kOz) + dz / 2;
+        if (N0 < 32 || N0 % 32 != 0 || N1 < 32 || N0 > 448) continue;
+        if (ob0 < static_cast<int>(kPc) + 32 || ob0 + c < ob1) continue;  // aggregate overlaps scalar cols only
+        if (ob1 + N1 > 512 || N0 + N1 > d.dv_pad) continue;
         rho_a = ra;
         break;
     }
     if (rho_a < 0) return false;
     p.rho_a = rho_a;
     p.N[0] = c + rho_a * dz;
-    p.N[1] = d.dv_mma - p.N[0];
+    p.N[1] = up32(d.dv_mma - p.N[0]);
     p.vcol0[0] = 0;
     p.vcol0[1] = p.N[0];
     p.ob[0] = 512 - p.N[0];
-    p.ob[1] = static_cast<int>(kOz) + dz;
+    p.ob[1] = static_cast<int>(kOz) + dz / 2;
     for (int ps = 0; ps < 2; ++ps) {
         p.na[ps] = std::min(p.N[ps], 256);
         p.nb[ps] = p.N[ps] - p.na[ps];
@@ -579,8 +584,8 @@ bool make_plan(const LayerDims& d, PassParams& p, Layout& lay) {
     const int vboxes = std::max(p.boxa[0] + p.boxb[0], p.boxa[1] + p.boxb[1]);
     // ring depths, preferred first: bytes in flight and few, large K stages (each stage costs a
     // barrier round trip; 4 KB stages measured 1.3x slower than 12 KB ones at rank 3)
-    const int cand[][4] = {{3, 3, 32, 2}, {4, 2, 32, 2}, {3, 2, 32, 2}, {2, 3, 32, 2}, {2, 2, 32, 2},
-                           {2, 2, 16, 3}, {2, 2, 16, 2}, {1, 4, 16, 2}, {1, 3, 16, 2}, {1, 2, 16, 2}};
+    const int cand[][4] = {{4, 3, 32, 2}, {3, 3, 32, 2}, {4, 2, 32, 2}, {3, 2, 32, 2}, {2, 3, 32, 2}, {3, 2, 16, 3}, {3, 2, 16, 2},
+                           {2, 2, 32, 2}, {2, 2, 16, 3}, {2, 2, 16, 2}, {1, 4, 16, 2}, {1, 3, 16, 2}, {1, 2, 16, 2}};
     int forced[4] = {0, 0, 0, 0};
     if (const char* e = std::getenv("FIPA_PASS_RING"))  // "kb,kst,vkeys,vst" (tuning experiments)
         std::sscanf(e, "%d,%d,%d,%d", &forced[0], &forced[1], &forced[2], &forced[3]);
