@@ -259,7 +259,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap mapQ,
                         const __grid_constant__ CUtensorMap mapK,
                         const __grid_constant__ CUtensorMap mapV,
-                        const __grid_constant__ CUtensorMap mapZ, Attn2Params p) {
+                        const __grid_constant__ CUtensorMap mapZ,
+                        const __grid_constant__ CUtensorMap mapO, Attn2Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -525,34 +526,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int qi = q0 + row;
         if (half == 0 && qi < p.L)
             p.lse[static_cast<int64_t>(bh) * p.L + qi] = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+        uint8_t* zs = smem + epilogue_smem(p.seg);
+        // z1 rows by TMA (all MMAs are complete, so the Q/K/V/P regions are free), issued before the
+        // O_hat save when the save's staging chunks [0, 64 KB) stay clear of the z1 region
+        const bool z_early = epilogue_smem(p.seg) >= 4 * BM * 128;
+        auto issue_z1 = [&]() {
+            if (p.z1_tma && warp == 2 && lane == 0) {
+                ptx::mbar_expect_tx(&bars->z_full, BM * p.rank * p.d_z * 4);
+                ptx::tma_load_3d(zs, &mapZ, &bars->z_full, 0, (bh / p.H) * p.L + q0, 0);
+            }
+        };
+        if (z_early || p.o_save == nullptr) issue_z1();
         if (p.o_save != nullptr) {
             // Training: keep the normalised O_hat row in fp32 for bwd_prep.  D = rowsum(dO*O) is
             // compared against dP = dO.V_j^T of the (often near one-hot) attended keys, where
             // dP - D is a small difference: a bf16 O would put its 2^-9 rounding straight into dS.
-            // tcgen05.ld is warp-collective: load first, store only rows inside the sequence.
-            const int n16 = p.dv_mma / 16;
-            const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
-            // residue-major [B, L, H, dv_pad]: bwd_prep stages a residue's H rows with one copy
+            // Residue-major [B, L, H, dv_pad] (bwd_prep stages a residue's H rows with one copy),
+            // written as 32-column x 128-row TMA tensor stores from four rotating 16 KB
+            // 128-byte-swizzled shared-memory chunks (the feature-staging region, free until the
+            // fused epilogue): coalesced full-line writes, rows past L clipped by the map.
             const int ob = bh / p.H, oh = bh - ob * p.H;
-            float* orow = p.o_save + ((static_cast<int64_t>(ob) * p.L + (qi < p.L ? qi : 0)) * p.H + oh) * p.dv_pad;
-            for (int ch = lo; ch < hi; ++ch) {
+            const int nchunks = (p.dv_mma + 31) / 32;
+            for (int ch = 0; ch < nchunks; ++ch) {
+                uint8_t* cb = smem + (ch & 3) * (BM * 128);
+                if (ch >= 4) {
+                    if (warp == 2 && lane == 0) ptx::bulk_wait_group_read<3>();  // chunk ch-4's store has read cb
+                    named_bar_sync(1, 256);
+                }
+                const int c0 = 32 * ch + 16 * half;
                 uint32_t o[16];
-                ptx::tmem_ld16(tl + 16 * ch, o);
-                ptx::tmem_wait_ld();
-                if (qi < p.L) {
-                    float4* dst = reinterpret_cast<float4*>(orow + 16 * ch);
+                if (c0 < p.dv_mma) {  // warp-uniform
+                    ptx::tmem_ld16(tl + c0, o);
+                    ptx::tmem_wait_ld();
+                } else {
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4)
-                        dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
-                                              __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
+                    for (int e = 0; e < 16; ++e) o[e] = 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    *reinterpret_cast<float4*>(cb + row * 128 + (((4 * half + k) ^ (row & 7)) << 4)) =
+                        make_float4(__uint_as_float(o[4 * k]) * inv_l, __uint_as_float(o[4 * k + 1]) * inv_l,
+                                    __uint_as_float(o[4 * k + 2]) * inv_l, __uint_as_float(o[4 * k + 3]) * inv_l);
+                ptx::fence_proxy_async_smem();
+                named_bar_sync(1, 256);
+                if (warp == 2 && lane == 0) {
+                    ptx::tma_store_4d(&mapO, cb, 32 * ch, oh, q0, ob);
+                    ptx::bulk_commit_group();
                 }
             }
-        }
-        uint8_t* zs = smem + epilogue_smem(p.seg);
-        if (p.z1_tma && warp == 2 && lane == 0) {
-            // All MMAs are complete (o_full), so the Q/K/V/P regions are free for the z1 rows.
-            ptx::mbar_expect_tx(&bars->z_full, BM * p.rank * p.d_z * 4);
-            ptx::tma_load_3d(zs, &mapZ, &bars->z_full, 0, (bh / p.H) * p.L + q0, 0);
+            if (warp == 2 && lane == 0) ptx::bulk_wait_group_read<0>();  // staging free for the epilogue
+            named_bar_sync(1, 256);
+            if (!z_early) issue_z1();
         }
         fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full);
         if (lane == 0) FIPA_TRACE(9, 1);
@@ -620,10 +644,15 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
                                       : mapV;
     const Layout lay = smem_layout(p.n_qkb, p.nb1, p.nb2);
     const int smem = lay.total + 1024;
+    if (a.o_save != nullptr && d.dv_pad % 32 != 0)
+        throw std::invalid_argument("attention: O_hat rows must be a multiple of 32 floats");
+    const CUtensorMap mapO = a.o_save != nullptr
+                                 ? make_map_4d_f32(a.o_save, d.dv_pad, d.heads, a.L, a.B, 32, 1, BM, 1)
+                                 : mapV;
     cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int qtiles = (a.L + BM - 1) / BM;
     dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(BH));
-    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, p);
+    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, mapO, p);
 }
 
 }  // namespace fipa_b200
