@@ -503,15 +503,20 @@ __global__ void __launch_bounds__(256) bwd_dout_kernel(const float* __restrict__
 
 // Scatter the fused projection-weight gradient [d_in, n_proj] into the reference tensors
 // w_q | w_k | w_v | w_qp | w_kp | w_vp (each [d_in, width], concatenated in `dst`).
+// Scatter the fused projection-weight gradient [d_in, n_proj] into the reference tensors
+// w_q | w_k | w_v | w_qp | w_kp | w_vp (each [d_in, width], concatenated in `dst`).  One block per
+// source row: coalesced row read, per-column segment lookup with 32-bit arithmetic.
 __global__ void scatter_proj_grad_kernel(const float* __restrict__ src, int d_in, int n_proj, ScatterCols seg,
                                          float* __restrict__ dst) {
-    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= static_cast<int64_t>(d_in) * n_proj) return;
-    int i = 0;
-    while (i < 5 && e >= seg.dst_off[i + 1]) ++i;
-    const int64_t local = e - seg.dst_off[i];
-    const int r = static_cast<int>(local / seg.width[i]), c = static_cast<int>(local % seg.width[i]);
-    dst[e] = src[static_cast<int64_t>(r) * n_proj + seg.col0[i] + c];
+    const int r = blockIdx.x;
+    const float* srow = src + static_cast<int64_t>(r) * n_proj;
+    for (int c = threadIdx.x; c < n_proj; c += blockDim.x) {
+        int i = 0;
+#pragma unroll
+        for (int k = 1; k < 6; ++k) i += c >= seg.col0[k] ? 1 : 0;
+        const int cc = c - seg.col0[i];
+        dst[seg.dst_off[i] + static_cast<int64_t>(r) * seg.width[i] + cc] = srow[c];
+    }
 }
 
 __global__ void bwd_recenter_kernel(const float* __restrict__ dtc, const uint8_t* __restrict__ mask,
@@ -598,8 +603,7 @@ void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out,
 
 void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
                               cudaStream_t stream) {
-    const int64_t n = int64_t(d_in) * n_proj;
-    scatter_proj_grad_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(src, d_in, n_proj, seg, dst);
+    scatter_proj_grad_kernel<<<static_cast<unsigned>(d_in), 256, 0, stream>>>(src, d_in, n_proj, seg, dst);
 }
 
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {
