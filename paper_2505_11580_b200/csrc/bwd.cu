@@ -473,31 +473,61 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpa
     }
 }
 
-// dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 32 columns x 8 row
-// groups; each thread strides rows, partial sums reduced in shared memory, one atomic per column.
+// dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 64 columns x 128 rows:
+// 16 threads cover a row's 64 columns with float4 loads (256 B contiguous), 16 row lanes stride the
+// rows with all their loads independent; column partials reduced in shared memory, one atomic per
+// column and block.
 __global__ void __launch_bounds__(256) bwd_dout_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ mask,
                                                        __nv_bfloat16* __restrict__ out, int ld_out, float* __restrict__ db,
                                                        int64_t rows, int cols, int rows_per_block) {
-    __shared__ float red[8][33];
-    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
-    const int col = blockIdx.x * 32 + cx;
+    __shared__ float red[16][65];
+    const int cq = threadIdx.x & 15, ry = threadIdx.x >> 4;
+    const int col = blockIdx.x * 64 + 4 * cq;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
     const int64_t r1 = min(rows, r0 + rows_per_block);
-    float acc = 0.f;
+    const bool vec = col + 4 <= cols && (cols & 3) == 0 && (ld_out & 3) == 0;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     if (col < cols) {
-        for (int64_t r = r0 + ry; r < r1; r += 8) {
+#pragma unroll 4
+        for (int64_t r = r0 + ry; r < r1; r += 16) {
             const bool ok = mask == nullptr || mask[r] != 0;
-            const float v = ok ? dout[r * cols + col] : 0.f;
-            out[r * ld_out + col] = __float2bfloat16_rn(v);
-            acc += v;
+            float v[4];
+            if (vec) {
+                const float4 f = ok ? __ldg(reinterpret_cast<const float4*>(dout + r * cols + col))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[0] = f.x;
+                v[1] = f.y;
+                v[2] = f.z;
+                v[3] = f.w;
+                uint2 w;
+                w.x = ptx_pack(v[0], v[1]);
+                w.y = ptx_pack(v[2], v[3]);
+                *reinterpret_cast<uint2*>(out + r * ld_out + col) = w;
+            } else {
+                for (int e = 0; e < 4; ++e) {
+                    v[e] = (ok && col + e < cols) ? dout[r * cols + col + e] : 0.f;
+                    if (col + e < cols) out[r * ld_out + col + e] = __float2bfloat16_rn(v[e]);
+                }
+            }
+            a0 += v[0];
+            a1 += v[1];
+            a2 += v[2];
+            a3 += v[3];
         }
     }
-    red[ry][cx] = acc;
+    red[ry][4 * cq] = a0;
+    red[ry][4 * cq + 1] = a1;
+    red[ry][4 * cq + 2] = a2;
+    red[ry][4 * cq + 3] = a3;
     __syncthreads();
-    if (ry == 0 && col < cols) {
-        float sum = 0.f;
-        for (int k = 0; k < 8; ++k) sum += red[k][cx];
-        atomicAdd(&db[col], sum);
+    if (threadIdx.x < 64) {
+        const int c = blockIdx.x * 64 + threadIdx.x;
+        if (c < cols) {
+            float sum = 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum += red[k][threadIdx.x];
+            atomicAdd(&db[c], sum);
+        }
     }
 }
 
@@ -597,7 +627,7 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
                      int64_t rows, int cols, cudaStream_t stream) {
     const int rpb = 128;
-    dim3 grid((cols + 31) / 32, static_cast<unsigned>((rows + rpb - 1) / rpb));
+    dim3 grid((cols + 63) / 64, static_cast<unsigned>((rows + rpb - 1) / rpb));
     bwd_dout_kernel<<<grid, 256, 0, stream>>>(dout, mask, out, ld_out, db, rows, cols, rpb);
 }
 
