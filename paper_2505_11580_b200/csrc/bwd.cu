@@ -237,130 +237,128 @@ constexpr int kUnpackMaxH = 16;
 //                          dz2 = sum_h (w_l w_bias[h, e % d_z] ln2 dk[zq+e] + dv[c+e]),
 //                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials);
 //                          dg += sum of dg_rows over the block's residues.
-__global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
-    __shared__ float s_geo[kUnpackMaxH][12];
+__global__ void __launch_bounds__(256) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
+    // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
+    // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
+    // heads with one warp reduction; per-head dgamma terms go through shared memory.
+    __shared__ float s_dg[8][kUnpackMaxH];
     const int H = d.heads, c = d.c, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
     const int g0 = c + 3 * Nq, vpair = c + rdz;
-    const int64_t row = blockIdx.x;
+    const int64_t BL = static_cast<int64_t>(a.B) * a.L;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (lane < kUnpackMaxH) s_dg[warp][lane] = 0.f;
+    __syncwarp();
+    if (row >= BL) return;
     const int64_t acc_h = a.acc_ld;
     const float* qrow = a.dq_acc + row * H * acc_h;
     const float* krow = a.dk_acc + row * H * acc_h;
     const float* vrow = a.dv_acc + row * H * acc_h;
     __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+    const float* pr = a.proj + row * d.n_proj;
     float R[9], t[3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
 #pragma unroll
     for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
-    const float* pr = a.proj + row * d.n_proj;  // pr[off_qp + ...] = local point columns
-    for (int h = warp; h < H; h += (blockDim.x >> 5)) {
+    float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
+    // ---- query / key points: task = (head, point)
+    for (int task = lane; task < H * Nq; task += 32) {
+        const int h = task / Nq, p = task - h * Nq;
         const float* qa = qrow + h * acc_h;
         const float* ka = krow + h * acc_h;
-        const float* va = vrow + h * acc_h;
-        // every load of this head first (one memory round trip): per-head scalars, the lane's
-        // query/key point (lanes < Nq) and value point (lanes < Nv), clamped to valid addresses
-        const int pq = min(lane, Nq - 1), pv = min(lane, Nv - 1);
         const float g = __ldg(a.head_g + h);
         const float cs = __ldg(ka + g0 + 18);
         const float S1 = __ldg(qa + g0 + 20);  // sum_j dS_ij, as rounded for the MMAs
-        float kw[6], kt[9], vt[3], qp[3], qc[3], qt[6], kp[3], kc[3], vp[3], dV[3];
-#pragma unroll
-        for (int x = 0; x < 6; ++x) {
-            kw[x] = __ldg(ka + g0 + 9 + x);
-            qt[x] = __ldg(qa + g0 + x);
-        }
-#pragma unroll
-        for (int x = 0; x < 9; ++x) kt[x] = __ldg(ka + g0 + x);
+        float qp[3], gB[3], kp[3], kc[3], dW[3];
 #pragma unroll
         for (int x = 0; x < 3; ++x) {
-            vt[x] = __ldg(va + vpair + x);
-            qp[x] = __ldg(pr + off_qp + (h * Nq + pq) * 3 + x);
-            qc[x] = __ldg(qa + c + 3 * pq + x);
-            kp[x] = __ldg(pr + off_kp + (h * Nq + pq) * 3 + x);
-            kc[x] = __ldg(ka + c + 3 * pq + x);
-            vp[x] = __ldg(pr + off_vp + (h * Nv + pv) * 3 + x);
-            dV[x] = __ldg(va + vpair + 6 + 3 * pv + x);
+            qp[x] = __ldg(pr + off_qp + (h * Nq + p) * 3 + x);
+            gB[x] = __ldg(qa + c + 3 * p + x) + __ldg(qa + g0 + x) + __ldg(qa + g0 + 3 + x);
+            kp[x] = __ldg(pr + off_kp + (h * Nq + p) * 3 + x);
+            kc[x] = __ldg(ka + c + 3 * p + x);
+            dW[x] = g * kLn2 * (__ldg(ka + g0 + 9 + x) + __ldg(ka + g0 + 12 + x));
         }
-        float dW[3];
+        // query point: A = R q_p + t,  dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS B] - g A S1
+        // (subtracting g A S1 with the same rounded dS cancels the translation-sized common mode)
+        float A[3], dA[3], B[3], dB[3];
 #pragma unroll
-        for (int x = 0; x < 3; ++x) dW[x] = g * kLn2 * (kw[x] + kw[3 + x]);
-        float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f}, dgh = 0.f;
-        if (lane < Nq) {
-            const int p = lane;
-            // query point: A = R q_p + t,  dA = g sum_j dS_ij (B_jp - A) = [g sum_j dS B] - g A S1
-            // (subtracting g A S1 with the same rounded dS cancels the translation-sized common
-            // mode of the first term)
-            float gB[3], A[3], dA[3];
+        for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
 #pragma unroll
-            for (int x = 0; x < 3; ++x) gB[x] = qc[x] + qt[x] + qt[3 + x];
-#pragma unroll
-            for (int x = 0; x < 3; ++x) A[x] = R[3 * x] * qp[0] + R[3 * x + 1] * qp[1] + R[3 * x + 2] * qp[2] + t[x];
-#pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                dA[x] = gB[x] - g * A[x] * S1;
-                dt[x] += dA[x];
-            }
-            // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
-            dgh += (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
-                   0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
-#pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                dp[off_qp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dA[0] + R[3 + x] * dA[1] + R[6 + x] * dA[2]);
-#pragma unroll
-                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
-            }
-            // key point: B = R k_p + t
-            float B[3], dB[3];
-#pragma unroll
-            for (int x = 0; x < 3; ++x) B[x] = R[3 * x] * kp[0] + R[3 * x + 1] * kp[1] + R[3 * x + 2] * kp[2] + t[x];
-#pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                dB[x] = g * kLn2 * kc[x] + dW[x] - g * B[x] * cs;
-                dt[x] -= g * B[x] * cs;
-            }
-            dgh += -0.5f * (B[0] * B[0] + B[1] * B[1] + B[2] * B[2]) * cs;
-#pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                dp[off_kp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dB[0] + R[3 + x] * dB[1] + R[6 + x] * dB[2]);
-#pragma unroll
-                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
-            }
+        for (int x = 0; x < 3; ++x) {
+            dA[x] = gB[x] - g * A[x] * S1;
+            dt[x] += dA[x];
         }
-        if (lane < Nv) {
-            const int p = lane;
+        // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
+        float dgh = (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
+                    0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
 #pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                dp[off_vp + (h * Nv + p) * 3 + x] = __float2bfloat16_rn(R[x] * dV[0] + R[3 + x] * dV[1] + R[6 + x] * dV[2]);
+        for (int x = 0; x < 3; ++x) {
+            dp[off_qp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dA[0] + R[3 + x] * dA[1] + R[6 + x] * dA[2]);
 #pragma unroll
-                for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
-            }
+            for (int y = 0; y < 3; ++y) dR[3 * x + y] += dA[x] * qp[y];
         }
-        if (lane == 0) {
+        // key point: B = R k_p + t
 #pragma unroll
-            for (int x = 0; x < 3; ++x)
-                dt[x] += g * kLn2 * (kt[x] + kt[6 + x]) + float(Nq) * dW[x]  // key
-                         + vt[x];                                                // value
+        for (int x = 0; x < 3; ++x) B[x] = R[3 * x] * kp[0] + R[3 * x + 1] * kp[1] + R[3 * x + 2] * kp[2] + t[x];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            dB[x] = g * kLn2 * kc[x] + dW[x] - g * B[x] * cs;
+            dt[x] -= g * B[x] * cs;
         }
+        dgh += -0.5f * (B[0] * B[0] + B[1] * B[1] + B[2] * B[2]) * cs;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+        for (int x = 0; x < 3; ++x) {
+            dp[off_kp + (h * Nq + p) * 3 + x] = __float2bfloat16_rn(R[x] * dB[0] + R[3 + x] * dB[1] + R[6 + x] * dB[2]);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
-        dgh = warp_sum(dgh);
-        if (lane < 12) s_geo[h][lane] = lane < 9 ? dR[lane] : dt[lane - 9];
-        if (lane == 0) a.dg_rows[row * H + h] = dgh;
+            for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
+        }
+        atomicAdd(&s_dg[warp][h], dgh);
     }
-    __syncthreads();
-    if (tid < 12) {
-        float acc = __ldg(a.geo_epi + row * 12 + tid);
-        for (int h = 0; h < H; ++h) acc += s_geo[h][tid];
-        if (tid < 9) {
-            if (a.drot != nullptr) a.drot[row * 9 + tid] = acc;
+    // ---- value points
+    for (int task = lane; task < H * Nv; task += 32) {
+        const int h = task / Nv, p = task - h * Nv;
+        const float* va = vrow + h * acc_h;
+        float vp[3], dV[3];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            vp[x] = __ldg(pr + off_vp + (h * Nv + p) * 3 + x);
+            dV[x] = __ldg(va + vpair + 6 + 3 * p + x);
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            dp[off_vp + (h * Nv + p) * 3 + x] = __float2bfloat16_rn(R[x] * dV[0] + R[3 + x] * dV[1] + R[6 + x] * dV[2]);
+#pragma unroll
+            for (int y = 0; y < 3; ++y) dR[3 * x + y] += dV[x] * vp[y];
+        }
+    }
+    // ---- per-head translation terms (key frame columns, value translation columns)
+    for (int h = lane; h < H; h += 32) {
+        const float* ka = krow + h * acc_h;
+        const float* va = vrow + h * acc_h;
+        const float g = __ldg(a.head_g + h);
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            const float dW = g * kLn2 * (__ldg(ka + g0 + 9 + x) + __ldg(ka + g0 + 12 + x));
+            dt[x] += g * kLn2 * (__ldg(ka + g0 + x) + __ldg(ka + g0 + 6 + x)) + float(Nq) * dW  // key
+                     + __ldg(va + vpair + x);                                                   // value
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
+    if (lane < 12) {
+        const float v = (lane < 9 ? dR[lane] : dt[lane - 9]) + __ldg(a.geo_epi + row * 12 + lane);
+        if (lane < 9) {
+            if (a.drot != nullptr) a.drot[row * 9 + lane] = v;
         } else {
-            a.dt_c[row * 3 + tid - 9] = acc;
+            a.dt_c[row * 3 + lane - 9] = v;
         }
     }
+    __syncwarp();
+    if (lane < H) a.dg_rows[row * H + lane] = s_dg[warp][lane];
 }
 
 __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
@@ -618,7 +616,7 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     if (d.heads > kUnpackMaxH) throw std::invalid_argument("bwd_unpack: at most 16 heads");
     if (d.n_query > 32 || d.n_value > 32) throw std::invalid_argument("bwd_unpack: at most 32 points per head");
     const int64_t BL = int64_t(a.B) * a.L;
-    bwd_unpack_geo_kernel<<<static_cast<unsigned>(BL), 32 * std::min(d.heads, 8), 0, stream>>>(d, a);
+    bwd_unpack_geo_kernel<<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a);
