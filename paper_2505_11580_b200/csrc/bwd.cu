@@ -82,7 +82,10 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
         bulk_g2s(s_o, a.ohat + row * H * d.dv_pad, H * o_bytes, bar);  // residue-major O_hat rows
     }
     for (int e = threadIdx.x; e < rdz; e += blockDim.x) s_z1[e] = a.z1[row * rdz + e];
-    for (int e = threadIdx.x; e < nw * (rdz + 12); e += blockDim.x) s_pair[e] = 0.f;  // s_pair + s_geo
+    // s_pair needs no clearing when every warp owns exactly one head (its slice is overwritten)
+    const bool one_head = H <= nw;
+    for (int e = threadIdx.x; e < (one_head ? 0 : nw * rdz) + nw * 12; e += blockDim.x)
+        s_pair[(one_head ? nw * rdz : 0) + e] = 0.f;  // s_pair (several heads per warp) + s_geo
     float R[9], t[3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
@@ -146,7 +149,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
                 const float4 ov = *reinterpret_cast<const float4*>(o + c + e);
                 const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
                 Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
-                float4 ps = *reinterpret_cast<float4*>(pair_s + e);  // warp-private slice
+                float4 ps = one_head ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                     : *reinterpret_cast<float4*>(pair_s + e);  // warp-private slice
                 ps.x += ov.x * dpc.x;
                 ps.y += ov.y * dpc.y;
                 ps.z += ov.z * dpc.z;
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
                     const int e = col - c;
                     const float dpc = df[e % dz];
                     v[u] = s_z1[e] * dpc;
-                    pair_s[e] += oo[u] * dpc;  // warp-private slice, one lane per e
+                    pair_s[e] = (one_head ? 0.f : pair_s[e]) + oo[u] * dpc;  // warp-private slice, one lane per e
                 } else if (col < vpts) {
                     v[u] = ds[(col - vpair) % 3];
                 } else if (col < vend) {
@@ -211,7 +215,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     }
     for (int e = threadIdx.x; e < rdz; e += blockDim.x) {
         float acc = 0.f;
-        for (int w = 0; w < nw; ++w) acc += s_pair[w * rdz + e];
+        const int nslices = one_head ? H : nw;  // (one head per warp: only the first H slices are written)
+        for (int w = 0; w < nslices; ++w) acc += s_pair[w * rdz + e];
         a.dz1_epi[row * rdz + e] = acc;
     }
     if (threadIdx.x < 12) {
