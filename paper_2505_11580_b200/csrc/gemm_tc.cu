@@ -30,7 +30,8 @@ struct GemmCfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStageC = 4 * 2 * 32 * 128;  // fp32 output staging: 4 warps x 2 x (32 rows x 128 B)
+    static constexpr int kSmem = kStages * kStageBytes + kStageC + 1024 /*align*/ + 256 /*barriers*/;
     static_assert(2 * BN <= 512, "double-buffered accumulator must fit TMEM");
 };
 
@@ -39,6 +40,7 @@ struct EpiParams {
     int64_t ldc;
     int M, N, K;
     bool out_bf16, accumulate;
+    bool tma_c;  // plain fp32 C: 32x32 chunks staged in shared memory and written by TMA stores
     int split_k;
     float alpha;
     const float* bias;
@@ -51,13 +53,15 @@ struct EpiParams {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
-                     const __grid_constant__ CUtensorMap mapB, EpiParams p) {
+                     const __grid_constant__ CUtensorMap mapB,
+                     const __grid_constant__ CUtensorMap mapC, EpiParams p) {
     using Cfg = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* tiles = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+    uint8_t* stage_c = smem + Cfg::kStages * Cfg::kStageBytes;  // [4 warps][2][32 rows][128 B]
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage_c + Cfg::kStageC);
     uint64_t* empty = full + Cfg::kStages;
     uint64_t* acc_full = empty + Cfg::kStages;   // [2]
     uint64_t* acc_empty = acc_full + 2;          // [2]
@@ -159,6 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
         const int quad = warp & 3;
+        uint8_t* my_stage = stage_c + quad * (2 * 32 * 128);
+        int nstore = 0;  // TMA stores issued by this warp (staging buffer = nstore & 1)
         int lu = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
             int m0, n0, kb0, nk;
@@ -173,9 +179,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t r[32];
                 ptx::tmem_ld32(tmem + buf * BN + (uint32_t(quad * 32) << 16) + c0, r);
                 ptx::tmem_wait_ld();
-                if (!row_ok || nk <= 0) continue;
                 const int col0 = n0 + c0;
-                if (col0 >= p.N) continue;
+                if (p.tma_c) {
+                    // warp-collective path: rows past M are clipped by the TMA store; nk == 0 (an
+                    // empty split) cannot occur without split-K
+                    if (col0 >= p.N || m0 + quad * 32 >= p.M) continue;
+                } else {
+                    if (!row_ok || nk <= 0) continue;
+                    if (col0 >= p.N) continue;
+                }
                 if (p.split_k > 1) {
                     float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
                     if (col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
@@ -196,6 +208,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int col = col0 + i;
                     if (p.bias != nullptr && col < p.N) x += p.bias[col];
                     v[i] = zero_row ? 0.0f : x;
+                }
+                if (p.tma_c) {
+                    // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
+                    uint8_t* sb = my_stage + (nstore & 1) * (32 * 128);
+                    if (nstore >= 2 && lane == 0) ptx::bulk_wait_group_read<1>();  // buffer's last store has read it
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<float4*>(sb + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&mapC, sb, col0, m0 + quad * 32);
+                        ptx::bulk_commit_group();
+                    }
+                    ++nstore;
+                    continue;
                 }
                 const size_t esz = p.out_bf16 ? 2 : 4;
                 const bool full_chunk = col0 + 32 <= p.N &&
@@ -239,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&acc_empty[buf]);
         }
+        if (p.tma_c && lane == 0) ptx::bulk_wait_group_read<0>();
     }
 
     ptx::tc_fence_before();
@@ -255,7 +286,11 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
                                   : make_map_2d_bf16(a.A, a.M, a.K, a.lda, 64, BM);
     const CUtensorMap mapB = B_MN ? make_map_2d_bf16(a.B, a.K, a.N, a.ldb, 64, BK)
                                   : make_map_2d_bf16(a.B, a.N, a.K, a.ldb, 64, BN);
-    EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, std::max(1, a.split_k), a.alpha, a.bias, a.row_mask};
+    const bool tma_c = !a.out_bf16 && !a.accumulate && a.split_k <= 1 && (a.ldc * 4) % 16 == 0 &&
+                       (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+    EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, tma_c, std::max(1, a.split_k), a.alpha, a.bias,
+                a.row_mask};
+    const CUtensorMap mapC = tma_c ? make_map_2d_f32(a.C, a.M, a.N, a.ldc, 32, 32) : mapA;
     auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
@@ -271,7 +306,7 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
         if (sms <= 0) sms = 148;
     }
     dim3 grid(static_cast<unsigned>(std::min(units, sms)));
-    kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, p);
+    kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, mapC, p);
 }
 
 }  // namespace

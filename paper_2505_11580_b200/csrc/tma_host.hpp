@@ -142,6 +142,23 @@ inline CUtensorMap make_map_4d_bf16_sharded(const void* base, uint64_t ld, uint6
     return m;
 }
 
+// fp32 matrix [rows, cols] (row stride ld elements), box {box_cols (<= 32: 128 B), box_rows}, SWIZZLE_128B.
+inline CUtensorMap make_map_2d_f32(const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_cols,
+                                   uint32_t box_rows) {
+    CUtensorMap m{};
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 4};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(2d f32) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 // fp32 [d3][d2][d1][d0] (d0 contiguous), box {box0, box1, box2, box3}, SWIZZLE_128B (box0 * 4 <= 128).
 inline CUtensorMap make_map_4d_f32(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
                                    uint32_t box0, uint32_t box1, uint32_t box2, uint32_t box3) {
