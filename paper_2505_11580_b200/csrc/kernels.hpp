@@ -84,7 +84,8 @@ struct ProjPackArgs {
     const float* head_g;
     const float* wl_bias;
     float k_scale;
-    float* proj;                   // [BL, n_proj]: only the point columns are written
+    float* proj;                   // [BL, n_proj]: only the point columns are written (write_points)
+    bool write_points = true;      // the backward reads them; inference may skip
     float* colbias;
     __nv_bfloat16* qhat;
     __nv_bfloat16* khat;

@@ -36,6 +36,7 @@ constexpr float kMaskedBias = -1.0e30f;
 struct PPParams {
     int M, L, H, c, Nq, Nv, dz, rdz, NH, N1, N2, nk;
     int dqk_used, dqk_pad, dv_used, dv_pad, zq, n_proj, chunk_ok;
+    int write_points;  // training: raw point columns into proj for the backward
     const float* z1;
     const float* z2;
     const float* rot;
@@ -50,6 +51,20 @@ struct PPParams {
     __nv_bfloat16* khat;
     __nv_bfloat16* vhat;
 };
+
+// Optional timestamps of CTA (0, 0) for pipeline analysis (tools/proj_pack_trace.cu).
+#ifdef FIPA_PP_TRACE
+__device__ long long g_pp_trace[10 * 16];  // [warp][event]
+#define PPTRACE(ev)                                                                                   \
+    do {                                                                                              \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0)                           \
+            g_pp_trace[(threadIdx.x >> 5) * 16 + (ev)] = clock64();                                   \
+    } while (0)
+#else
+#define PPTRACE(ev) \
+    do {            \
+    } while (0)
+#endif
 
 __device__ __forceinline__ float bf_hi(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ float bf_lo(float x) { return x - __bfloat162float(__float2bfloat16_rn(x)); }
@@ -79,6 +94,43 @@ __device__ __forceinline__ void stage_put8(uint8_t* tile, int row, int col, cons
     w.z = ptx::pack_bf16x2(v[4], v[5]);
     w.w = ptx::pack_bf16x2(v[6], v[7]);
     *reinterpret_cast<uint4*>(p) = w;
+}
+
+// Frame-apply up to MAXP points held in TMEM registers u[32] | w[16] (x, y, z interleaved); every
+// index is a compile-time constant so the arrays stay in registers.
+template <int MAXP>
+__device__ __forceinline__ void rotate_points(const uint32_t* u, const uint32_t* w, int n, const float* R, float* out) {
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q) {
+        if (q < n) {
+            const float x = __uint_as_float(3 * q < 32 ? u[3 * q] : w[3 * q - 32]);
+            const float y = __uint_as_float(3 * q + 1 < 32 ? u[3 * q + 1] : w[3 * q + 1 - 32]);
+            const float z = __uint_as_float(3 * q + 2 < 32 ? u[3 * q + 2] : w[3 * q + 2 - 32]);
+            out[3 * q] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z));
+            out[3 * q + 1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z));
+            out[3 * q + 2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z));
+        }
+    }
+}
+// Raw point columns (training only) into the projection row: float4 stores where aligned.
+__device__ __forceinline__ void store_points(float* dst, const uint32_t* u, const uint32_t* w, int n) {
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (n & 3) == 0) {
+#pragma unroll
+        for (int e4 = 0; e4 < 12; ++e4) {
+            if (4 * e4 < n) {
+                float4 f;
+                f.x = __uint_as_float(4 * e4 < 32 ? u[4 * e4] : w[4 * e4 - 32]);
+                f.y = __uint_as_float(4 * e4 + 1 < 32 ? u[4 * e4 + 1] : w[4 * e4 + 1 - 32]);
+                f.z = __uint_as_float(4 * e4 + 2 < 32 ? u[4 * e4 + 2] : w[4 * e4 + 2 - 32]);
+                f.w = __uint_as_float(4 * e4 + 3 < 32 ? u[4 * e4 + 3] : w[4 * e4 + 3 - 32]);
+                reinterpret_cast<float4*>(dst)[e4] = f;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 48; ++e)
+            if (e < n) dst[e] = __uint_as_float(e < 32 ? u[e] : w[e - 32]);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -116,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
+        PPTRACE(0);
         if (lane == 0) {
             for (int kb = 0; kb < p.nk; ++kb) {
                 const int s = kb % kStages;
@@ -149,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mma_commit(done);
         }
+        PPTRACE(1);
     } else {
         // ---------------------------------------------------------------- epilogue
         const int quad = warp & 3;
@@ -168,40 +222,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 3; ++k) t[k] = __ldg(p.trans + int64_t(rowc) * 3 + k);
         const bool valid = p.mask == nullptr || p.mask[rowc] != 0;
         const float g = p.head_g[h];
+        {  // warm L2 with this row's pair factors (phase B reads them) while the GEMM runs
+            const char* z1r = reinterpret_cast<const char*>(p.z1 + int64_t(rowc) * rdz);
+            const char* z2r = reinterpret_cast<const char*>(p.z2 + int64_t(rowc) * rdz);
+            for (int o = 128 * half; o < rdz * 4; o += 256) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(z1r + o));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(z2r + o));
+            }
+        }
+        PPTRACE(0);
         ptx::mbar_wait(done, 0);
         ptx::tc_fence_after();
+        PPTRACE(1);
 
-        // points: raw (written back for the backward) and frame-rotated (geometry half only)
+        // points: frame-rotated (geometry half only); raw copies into proj when training
         float rq[3 * kMaxQ], rk[3 * kMaxQ], rv[3 * kMaxV];
         if (half == 1) {
             float* prow = p.proj + int64_t(rowc) * p.n_proj;
             const int oq = 3 * p.H * c + h * 3 * Nq, okp = oq + 3 * p.H * Nq, ov = 3 * p.H * c + 6 * p.H * Nq + h * 3 * Nv;
-#pragma unroll
-            for (int part = 0; part < 3; ++part) {
-                const int col = part == 0 ? cqp : part == 1 ? ckp : cvp;
-                const int n = part == 2 ? 3 * Nv : 3 * Nq;  // <= 36
-                uint32_t u[32], w[16];
-                ptx::tmem_ld32(tl + col, u);
-                ptx::tmem_ld16(tl + col + 32, w);
-                ptx::tmem_wait_ld();
-                if (ok) {
-                    float* dst = prow + (part == 0 ? oq : part == 1 ? okp : ov);
-                    for (int e = 0; e < n; ++e) dst[e] = __uint_as_float(e < 32 ? u[e] : w[e - 32]);
-                }
-                float* outp = part == 0 ? rq : part == 1 ? rk : rv;
-                const int cap = part == 2 ? kMaxV : kMaxQ;
-#pragma unroll
-                for (int q = 0; q < kMaxV; ++q) {
-                    if (q < cap && 3 * q < n) {
-                        const float x = __uint_as_float(3 * q < 32 ? u[3 * q] : w[3 * q - 32]);
-                        const float y = __uint_as_float(3 * q + 1 < 32 ? u[3 * q + 1] : w[3 * q + 1 - 32]);
-                        const float z = __uint_as_float(3 * q + 2 < 32 ? u[3 * q + 2] : w[3 * q + 2 - 32]);
-                        outp[3 * q] = fmaf(R[0], x, fmaf(R[1], y, R[2] * z));
-                        outp[3 * q + 1] = fmaf(R[3], x, fmaf(R[4], y, R[5] * z));
-                        outp[3 * q + 2] = fmaf(R[6], x, fmaf(R[7], y, R[8] * z));
-                    }
-                }
-            }
+            uint32_t u[32], w[16];
+            ptx::tmem_ld32(tl + cqp, u);
+            ptx::tmem_ld16(tl + cqp + 32, w);
+            ptx::tmem_wait_ld();
+            rotate_points<kMaxQ>(u, w, Nq, R, rq);
+            if (p.write_points && ok) store_points(prow + oq, u, w, 3 * Nq);
+            ptx::tmem_ld32(tl + ckp, u);
+            ptx::tmem_ld16(tl + ckp + 32, w);
+            ptx::tmem_wait_ld();
+            rotate_points<kMaxQ>(u, w, Nq, R, rk);
+            if (p.write_points && ok) store_points(prow + okp, u, w, 3 * Nq);
+            ptx::tmem_ld32(tl + cvp, u);
+            ptx::tmem_ld16(tl + cvp + 32, w);
+            ptx::tmem_wait_ld();
+            rotate_points<kMaxV>(u, w, Nv, R, rv);
+            if (p.write_points && ok) store_points(prow + ov, u, w, 3 * Nv);
         }
         float qb[3] = {0.f, 0.f, 0.f}, W[3] = {0.f, 0.f, 0.f}, kn = 0.f;
 #pragma unroll
@@ -225,8 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // derived from TMEM and the frame.  Phase B (warp-cooperative, lanes across columns): the
         // pair-factor columns, straight from coalesced z1 / z2 row loads.
         const float* wbh = p.wl_bias + h * p.dz;
+        PPTRACE(2);
         for (int tsel = 0; tsel < 3; ++tsel) {
             uint8_t* tile = tiles + (tsel & 1) * tile_bytes;
+            PPTRACE(3 + 4 * tsel);
             if (tsel == 2) {
                 // tile 0 is reused: tensor 0's TMA stores must have read it (tensor 1's may fly)
                 if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -253,10 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // rotated points, the 21 translation / bias columns and the zq padding
                 const float gs = tsel == 0 ? kL2E : g;
                 const float* pts = tsel == 0 ? rq : rk;
-#pragma unroll
-                for (int e = 0; e < 3 * kMaxQ; ++e)
-                    if (e < 3 * Nq) stage_put(tile, r, c + e, gs * pts[e]);
-                for (int e = 0; e < zq - g0; ++e) {
+                // translation / bias column e of the [g0, zq) block (q_hat if tsel == 0, else k_hat)
+                auto tcolv = [&](int e) -> float {
                     const int x = e % 3;
                     float qv, kv;
                     if (e < 9) {
@@ -274,21 +328,60 @@ __global__ void __launch_bounds__(kThreads, 1)
                         qv = 0.f;
                         kv = e == 20 ? 1.0f : 0.f;
                     }
-                    stage_put(tile, r, g0 + e, tsel == 0 ? qv : kv);
+                    return tsel == 0 ? qv : kv;
+                };
+                if (3 * Nq == 3 * kMaxQ && c % 8 == 0 && zq - g0 == 24 && p.dqk_used % 8 == 0) {
+                    // 16-byte stores: 3 point chunks, 3 translation chunks, the pad chunks
+#pragma unroll
+                    for (int k8 = 0; k8 < 3; ++k8) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v8[e] = gs * pts[8 * k8 + e];
+                        stage_put8(tile, r, c + 8 * k8, v8);
+                    }
+#pragma unroll
+                    for (int k8 = 0; k8 < 3; ++k8) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v8[e] = tcolv(8 * k8 + e);
+                        stage_put8(tile, r, g0 + 8 * k8, v8);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v8[e] = 0.f;
+                    for (int e = p.dqk_used; e < width; e += 8) stage_put8(tile, r, e, v8);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 3 * kMaxQ; ++e)
+                        if (e < 3 * Nq) stage_put(tile, r, c + e, gs * pts[e]);
+                    for (int e = 0; e < zq - g0; ++e) stage_put(tile, r, g0 + e, tcolv(e));
+                    for (int e = p.dqk_used; e < width; ++e) stage_put(tile, r, e, 0.f);
                 }
-                for (int e = p.dqk_used; e < width; ++e) stage_put(tile, r, e, 0.f);
             } else {
                 const int vp = c + rdz;
+                // [t hi (3) | t lo (3) | R v_p (3 Nv) | 0 ...] from column vp to the row end
+                auto vcolv = [&](int e) -> float {
+                    if (e < 3) return bf_hi(t[e]);
+                    if (e < 6) return bf_lo(t[e - 3]);
+                    return e - 6 < 3 * Nv ? rv[e - 6] : 0.f;
+                };
+                if (vp % 8 == 0 && width - vp == 64) {
 #pragma unroll
-                for (int x = 0; x < 3; ++x) {
-                    stage_put(tile, r, vp + x, bf_hi(t[x]));
-                    stage_put(tile, r, vp + 3 + x, bf_lo(t[x]));
+                    for (int k8 = 0; k8 < 8; ++k8) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v8[e] = (8 * k8 + e < 6 + 3 * kMaxV) ? vcolv(8 * k8 + e) : 0.f;
+                        stage_put8(tile, r, vp + 8 * k8, v8);
+                    }
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        stage_put(tile, r, vp + x, bf_hi(t[x]));
+                        stage_put(tile, r, vp + 3 + x, bf_lo(t[x]));
+                    }
+#pragma unroll
+                    for (int e = 0; e < 3 * kMaxV; ++e)
+                        if (e < 3 * Nv) stage_put(tile, r, vp + 6 + e, rv[e]);
+                    for (int e = p.dv_used; e < width; ++e) stage_put(tile, r, e, 0.f);
                 }
-#pragma unroll
-                for (int e = 0; e < 3 * kMaxV; ++e)
-                    if (e < 3 * Nv) stage_put(tile, r, vp + 6 + e, rv[e]);
-                for (int e = p.dv_used; e < width; ++e) stage_put(tile, r, e, 0.f);
             }
+            PPTRACE(4 + 4 * tsel);
             // ---- phase B: pair factors, warp covers rows quad*32 + half*16 .. +16, lane = 8-column chunk
             {
                 const float* zsrc = tsel == 0 ? p.z1 : p.z2;
@@ -325,8 +418,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            PPTRACE(5 + 4 * tsel);
             ptx::fence_proxy_async_smem();
             named_sync(1, 256);
+            PPTRACE(6 + 4 * tsel);
             const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
             if (p.chunk_ok) {
                 // 32-row chunks never straddle two samples (L % 32 == 0): TMA stores, one thread
@@ -350,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        PPTRACE(15);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -392,6 +488,7 @@ void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t st
     p.zq = d.zq;
     p.n_proj = d.n_proj;
     p.chunk_ok = (a.L % 32) == 0 ? 1 : 0;
+    p.write_points = a.write_points ? 1 : 0;
     p.z1 = a.z1;
     p.z2 = a.z2;
     p.rot = a.rot;
