@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
                                                   __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha));
                     } else {
-                        for (int i = 0; i < 32 && col0 + i < p.N; ++i) atomicAdd(out + i, __uint_as_float(r[i]) * p.alpha);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)  // compile-time indices keep r[] in registers
+                            if (col0 + i < p.N) atomicAdd(out + i, __uint_as_float(r[i]) * p.alpha);
                     }
                     continue;
                 }
@@ -244,7 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             o4[q] = w;
                         }
                     } else {
-                        for (int i = 0; i < 32 && col0 + i < p.N; ++i) out[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < p.N) out[i] = __float2bfloat16_rn(v[i]);
                     }
                 } else {
                     float* out = reinterpret_cast<float*>(p.C) + int64_t(row) * p.ldc + col0;
@@ -260,8 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             o4[q] = w;
                         }
                     } else {
-                        for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-                            out[i] = p.accumulate ? out[i] + v[i] : v[i];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < p.N) out[i] = p.accumulate ? out[i] + v[i] : v[i];
                     }
                 }
             }
