@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
             }
             for (int col = vpair + lane; col < d.dv_pad; col += 32) {
                 float v = 0.f;
-                if (col < vpts) v = ds[(col - vpair) % 3];
+                if (col < vpts) {
+                    const int x = (col - vpair) % 3;  // select, not an indexed load: keeps ds[] in registers
+                    v = x == 0 ? ds[0] : (x == 1 ? ds[1] : ds[2]);
+                }
                 else if (col < vend) v = dopt_s[col - vpts];
                 v = bfr(v);
                 out[col] = __float2bfloat16_rn(v);
@@ -182,7 +185,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
                     v[u] = s_z1[e] * dpc;
                     pair_s[e] = (one_head ? 0.f : pair_s[e]) + oo[u] * dpc;  // warp-private slice, one lane per e
                 } else if (col < vpts) {
-                    v[u] = ds[(col - vpair) % 3];
+                    const int x = (col - vpair) % 3;
+                    v[u] = x == 0 ? ds[0] : (x == 1 ? ds[1] : ds[2]);
                 } else if (col < vend) {
                     v[u] = dopt_s[col - vpts];
                 } else {
