@@ -39,7 +39,14 @@ int main(int argc, char** argv) {
     cudaMemset(z1, 0, BL * 256 * 4);
     cudaMemset(rot, 0, BL * 9 * 4);
     cudaMemset(trans, 0, BL * 3 * 4);
-    AttnArgs a{q, k, v, nullptr, z1, rot, trans, feat, lse, B, L};
+    AttnArgs a{};
+    a.qhat = q; a.khat = k; a.vhat = v; a.colbias = nullptr; a.z1 = z1; a.rot = rot; a.trans = trans;
+    a.feat = feat; a.lse = lse; a.B = B; a.L = L;
+    if (argc > 3 && atoi(argv[3]) != 0) {  // training forward: also save the fp32 O_hat
+        float* o;
+        cudaMalloc(&o, BL * d.heads * d.dv_pad * 4);
+        a.o_save = o;
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
