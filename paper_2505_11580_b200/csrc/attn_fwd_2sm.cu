@@ -150,9 +150,136 @@ __device__ __forceinline__ void load_z16_smem(const uint8_t* zs, int row, int f,
     }
 }
 
+// Points block of one row (half 0), branch-free over kMaxPoints so the independent points
+// interleave: local = R_i^T (g - t_i) (proj/src/geometry.cpp:70-76) and |local|, as bf16 pairs.
+__device__ __forceinline__ void epilogue_points(uint32_t tl_pts, float inv_l, int Nv, const float* Rm,
+                                                const float* tv, __nv_bfloat16* fp, bool ok) {
+    uint32_t o[48];  // warp-collective TMEM loads: every lane, rows past L included
+    ptx::tmem_ld16(tl_pts, o);
+    ptx::tmem_ld16(tl_pts + 16, o + 16);
+    ptx::tmem_ld16(tl_pts + 32, o + 32);
+    ptx::tmem_wait_ld();
+    if (!ok) return;
+    float tg[3];
+#pragma unroll
+    for (int y = 0; y < 3; ++y) tg[y] = (__uint_as_float(o[y]) + __uint_as_float(o[3 + y])) * inv_l - tv[y];
+    float v[3 * kMaxPoints], nrm[kMaxPoints];
+#pragma unroll
+    for (int pt = 0; pt < kMaxPoints; ++pt) {
+        const float gx = fmaf(__uint_as_float(o[6 + 3 * pt]), inv_l, tg[0]);
+        const float gy = fmaf(__uint_as_float(o[7 + 3 * pt]), inv_l, tg[1]);
+        const float gz = fmaf(__uint_as_float(o[8 + 3 * pt]), inv_l, tg[2]);
+        const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
+        const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));
+        const float lz = fmaf(Rm[2], gx, fmaf(Rm[5], gy, Rm[8] * gz));
+        v[3 * pt] = lx;
+        v[3 * pt + 1] = ly;
+        v[3 * pt + 2] = lz;
+        const float n2 = fmaf(lx, lx, fmaf(ly, ly, lz * lz));
+        nrm[pt] = n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
+    }
+    // [x0 y0 z0 x1 ... | n0 n1 ...]: 3*Nv coordinates then Nv norms
+    const int nc = 3 * Nv;
+    if ((reinterpret_cast<uintptr_t>(fp) & 3) != 0) {
+#pragma unroll
+        for (int e = 0; e < 3 * kMaxPoints; ++e)
+            if (e < nc) fp[e] = __float2bfloat16_rn(v[e]);
+#pragma unroll
+        for (int pt = 0; pt < kMaxPoints; ++pt)
+            if (pt < Nv) fp[nc + pt] = __float2bfloat16_rn(nrm[pt]);
+        return;
+    }
+    uint32_t* fp2 = reinterpret_cast<uint32_t*>(fp);
+#pragma unroll
+    for (int e = 0; e < 3 * kMaxPoints / 2; ++e) {
+        if (2 * e + 1 < nc) {
+            fp2[e] = ptx::pack_bf16x2(v[2 * e], v[2 * e + 1]);
+        } else if (2 * e < nc) {
+            fp[2 * e] = __float2bfloat16_rn(v[2 * e]);
+        }
+    }
+    if ((nc & 1) == 0) {
+#pragma unroll
+        for (int i = 0; i < kMaxPoints / 2; ++i) {
+            if (2 * i + 1 < Nv) {
+                fp2[nc / 2 + i] = ptx::pack_bf16x2(nrm[2 * i], nrm[2 * i + 1]);
+            } else if (2 * i < Nv) {
+                fp[nc + 2 * i] = __float2bfloat16_rn(nrm[2 * i]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int pt = 0; pt < kMaxPoints; ++pt)
+            if (pt < Nv) fp[nc + pt] = __float2bfloat16_rn(nrm[pt]);
+    }
+}
+
+// Scalar and pair blocks of one row for c = d_z = 128 and z1 staged in shared memory: each half
+// owns four 16-column chunks of each block, every loop trip count and index compile-time, four
+// TMEM loads in flight per wait.
+__device__ __forceinline__ void put16_vec(__nv_bfloat16* dst, const float* x) {
+    uint4 w0, w1;
+    w0.x = ptx::pack_bf16x2(x[0], x[1]);
+    w0.y = ptx::pack_bf16x2(x[2], x[3]);
+    w0.z = ptx::pack_bf16x2(x[4], x[5]);
+    w0.w = ptx::pack_bf16x2(x[6], x[7]);
+    w1.x = ptx::pack_bf16x2(x[8], x[9]);
+    w1.y = ptx::pack_bf16x2(x[10], x[11]);
+    w1.z = ptx::pack_bf16x2(x[12], x[13]);
+    w1.w = ptx::pack_bf16x2(x[14], x[15]);
+    reinterpret_cast<uint4*>(dst)[0] = w0;
+    reinterpret_cast<uint4*>(dst)[1] = w1;
+}
+
+__device__ __forceinline__ void epilogue_scalar128(uint32_t tl, float inv_l, int half, __nv_bfloat16* frow) {
+    uint32_t o[4][16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ptx::tmem_ld16(tl + 64 * half + 16 * k, o[k]);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(o[k][e]) * inv_l;
+        put16_vec(frow + 128 + 64 * half + 16 * k, x);
+    }
+}
+
+template <int RANK>
+__device__ __forceinline__ void epilogue_pair128(uint32_t tl, float inv_l, int half, int row, const uint8_t* zs,
+                                                 __nv_bfloat16* frow) {
+    constexpr int CB = 4 / RANK;  // chunks per TMEM wait
+#pragma unroll
+    for (int b0 = 0; b0 < 4; b0 += CB) {
+        uint32_t o[CB][RANK][16];
+#pragma unroll
+        for (int k = 0; k < CB; ++k)
+#pragma unroll
+            for (int r = 0; r < RANK; ++r) ptx::tmem_ld16(tl + 128 + r * 128 + 64 * half + 16 * (b0 + k), o[k][r]);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < CB; ++k) {
+            const int d0 = 64 * half + 16 * (b0 + k);
+            float acc[16];
+#pragma unroll
+            for (int r = 0; r < RANK; ++r) {
+                float z[16];
+                load_z16_smem(zs, row, r * 128 + d0, z);
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    acc[e] = r == 0 ? z[e] * __uint_as_float(o[k][r][e]) : fmaf(z[e], __uint_as_float(o[k][r][e]), acc[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] *= inv_l;
+            put16_vec(frow + d0, acc);
+        }
+    }
+}
+
 __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl, float inv_l,
                                                int row, int q0, int bh, uint8_t* smem, int half,
-                                               const uint8_t* zs, uint64_t* z_full) {
+                                               const uint8_t* zs, uint64_t* z_full, const float* Rm,
+                                               const float* tv) {
     const int seg = p.seg, sst = (seg + 7) / 8 * 8 + 8;
     __nv_bfloat16* fst = reinterpret_cast<__nv_bfloat16*>(smem);
     __nv_bfloat16* frow = fst + row * sst;
@@ -163,89 +290,159 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
     const int c = p.c, dz = p.d_z, Nv = p.n_value;
     const int base = c + p.rank * dz;
 
-    // scalar aggregate -> [d_z, d_z + c): 16-column chunks split between the halves
+    // 16 bf16 of a feature row as two 16-byte shared-memory stores where aligned
+    const bool vrow = (c % 16) == 0 && (dz % 16) == 0 && (sst % 8) == 0;
+    auto put16 = [&](int col, const float* x, int n) {
+        if (vrow) {
+            uint4 w0, w1;
+            w0.x = ptx::pack_bf16x2(x[0], x[1]);
+            w0.y = ptx::pack_bf16x2(x[2], x[3]);
+            w0.z = ptx::pack_bf16x2(x[4], x[5]);
+            w0.w = ptx::pack_bf16x2(x[6], x[7]);
+            w1.x = ptx::pack_bf16x2(x[8], x[9]);
+            w1.y = ptx::pack_bf16x2(x[10], x[11]);
+            w1.z = ptx::pack_bf16x2(x[12], x[13]);
+            w1.w = ptx::pack_bf16x2(x[14], x[15]);
+            reinterpret_cast<uint4*>(frow + col)[0] = w0;
+            reinterpret_cast<uint4*>(frow + col)[1] = w1;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if (e < n) frow[col + e] = __float2bfloat16_rn(x[e]);
+        }
+    };
+
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 0);
+    const bool fast = c == 128 && dz == 128 && (p.rank == 1 || p.rank == 2) && zs != nullptr;
+    if (fast) {
+        epilogue_scalar128(tl, inv_l, half, frow);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 1);
+        if (half == 0) epilogue_points(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 2);
+        ptx::mbar_wait(z_full, 0);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 3);
+        if (p.rank == 1) {
+            epilogue_pair128<1>(tl, inv_l, half, row, zs, frow);
+        } else {
+            epilogue_pair128<2>(tl, inv_l, half, row, zs, frow);
+        }
+    } else {
+    // scalar aggregate -> [d_z, d_z + c): 16-column chunks split between the halves, four TMEM
+    // loads in flight per wait (a TMEM load costs ~0.5k cycles of latency)
     const int nsc = (c + 15) / 16;
-    for (int ch = half ? (nsc + 1) / 2 : 0; ch < (half ? nsc : (nsc + 1) / 2); ++ch) {
-        const int c0 = 16 * ch;
-        uint32_t o[16];
-        ptx::tmem_ld16(tl + c0, o);
+    const int sc_lo = half ? (nsc + 1) / 2 : 0, sc_hi = half ? nsc : (nsc + 1) / 2;
+    for (int ch0 = sc_lo; ch0 < sc_hi; ch0 += 4) {
+        uint32_t o[64];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ch0 + k < sc_hi) ptx::tmem_ld16(tl + 16 * (ch0 + k), o + 16 * k);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-            if (c0 + e < c) frow[dz + c0 + e] = __float2bfloat16_rn(__uint_as_float(o[e]) * inv_l);
-    }
-    // points (half 0), all in registers: local = R_i^T (g - t_i)   (proj/src/geometry.cpp:70-76)
-    if (half == 0) {
-        uint32_t o[48];
-        ptx::tmem_ld16(tl + base, o);
-        ptx::tmem_ld16(tl + base + 16, o + 16);
-        ptx::tmem_ld16(tl + base + 32, o + 32);
-        ptx::tmem_wait_ld();
-        if (ok) {
-            const float* R = p.rot + grow * 9;
-            const float* t = p.trans + grow * 3;
-            float Rm[9], tg[3];
+        for (int k = 0; k < 4; ++k) {
+            if (ch0 + k < sc_hi) {
+                float x[16];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) Rm[k] = __ldg(R + k);
-#pragma unroll
-            for (int y = 0; y < 3; ++y)
-                tg[y] = (__uint_as_float(o[y]) + __uint_as_float(o[3 + y])) * inv_l - __ldg(t + y);
-            __nv_bfloat16* fp = frow + dz + c;
-#pragma unroll
-            for (int pt = 0; pt < kMaxPoints; ++pt) {
-                if (pt < Nv) {
-                    const float gx = __uint_as_float(o[6 + 3 * pt]) * inv_l + tg[0];
-                    const float gy = __uint_as_float(o[7 + 3 * pt]) * inv_l + tg[1];
-                    const float gz = __uint_as_float(o[8 + 3 * pt]) * inv_l + tg[2];
-                    const float lx = fmaf(Rm[0], gx, fmaf(Rm[3], gy, Rm[6] * gz));
-                    const float ly = fmaf(Rm[1], gx, fmaf(Rm[4], gy, Rm[7] * gz));
-                    const float lz = fmaf(Rm[2], gx, fmaf(Rm[5], gy, Rm[8] * gz));
-                    fp[3 * pt] = __float2bfloat16_rn(lx);
-                    fp[3 * pt + 1] = __float2bfloat16_rn(ly);
-                    fp[3 * pt + 2] = __float2bfloat16_rn(lz);
-                    fp[3 * Nv + pt] = __float2bfloat16_rn(sqrtf(lx * lx + ly * ly + lz * lz));
-                }
+                for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(o[16 * k + e]) * inv_l;
+                put16(dz + 16 * (ch0 + k), x, c - 16 * (ch0 + k));
             }
         }
     }
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 1);
+    // points (half 0), all in registers: local = R_i^T (g - t_i)   (proj/src/geometry.cpp:70-76)
+    if (half == 0) epilogue_points(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
     // pair contraction -> [0, d_z): 16-column chunks split between the halves
     const float* z1r = p.z1 + grow * (p.rank * dz);
     const bool vec = (reinterpret_cast<uintptr_t>(z1r) & 15) == 0;
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 2);
     if (zs != nullptr) ptx::mbar_wait(z_full, 0);
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 3);
     const int npc = (dz + 15) / 16;
-    for (int ch = half ? (npc + 1) / 2 : 0; ch < (half ? npc : (npc + 1) / 2); ++ch) {
-        const int d0 = 16 * ch;
-        float acc[16];
+    const int pc_lo = half ? (npc + 1) / 2 : 0, pc_hi = half ? npc : (npc + 1) / 2;
+    if (p.rank <= 2) {
+        // two chunks x both ranks: four TMEM loads in flight per wait
+        for (int ch0 = pc_lo; ch0 < pc_hi; ch0 += 2) {
+            uint32_t o[2][2][16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-        for (int rho = 0; rho < p.rank; ++rho) {
-            float z[16];
-            if (zs != nullptr) {
-                load_z16_smem(zs, row, rho * dz + d0, z);
-            } else {
-                load_z16_global(z1r + rho * dz + d0, vec, dz - d0, z);
-            }
-            uint32_t o[16];
-            ptx::tmem_ld16(tl + c + rho * dz + d0, o);
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (ch0 + k < pc_hi && r < p.rank) ptx::tmem_ld16(tl + c + r * dz + 16 * (ch0 + k), o[k][r]);
             ptx::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) acc[e] = fmaf(z[e], __uint_as_float(o[e]), acc[e]);
-        }
+            for (int k = 0; k < 2; ++k) {
+                if (ch0 + k < pc_hi) {
+                    const int d0 = 16 * (ch0 + k);
+                    float acc[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-            if (d0 + e < dz) frow[d0 + e] = __float2bfloat16_rn(acc[e] * inv_l);
+                    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        if (r < p.rank) {
+                            float z[16];
+                            if (zs != nullptr) {
+                                load_z16_smem(zs, row, r * dz + d0, z);
+                            } else {
+                                load_z16_global(z1r + r * dz + d0, vec, dz - d0, z);
+                            }
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) acc[e] = fmaf(z[e], __uint_as_float(o[k][r][e]), acc[e]);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) acc[e] *= inv_l;
+                    put16(d0, acc, dz - d0);
+                }
+            }
+        }
+    } else {
+        constexpr int kMaxRank = 4;
+        for (int ch = pc_lo; ch < pc_hi; ++ch) {
+            const int d0 = 16 * ch;
+            float acc[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+            for (int r0 = 0; r0 < p.rank; r0 += kMaxRank) {
+                uint32_t o[kMaxRank][16];  // every rank's TMEM chunk in flight before one wait
+#pragma unroll
+                for (int k = 0; k < kMaxRank; ++k)
+                    if (r0 + k < p.rank) ptx::tmem_ld16(tl + c + (r0 + k) * dz + d0, o[k]);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < kMaxRank; ++k) {
+                    if (r0 + k < p.rank) {
+                        float z[16];
+                        if (zs != nullptr) {
+                            load_z16_smem(zs, row, (r0 + k) * dz + d0, z);
+                        } else {
+                            load_z16_global(z1r + (r0 + k) * dz + d0, vec, dz - d0, z);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) acc[e] = fmaf(z[e], __uint_as_float(o[k][e]), acc[e]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] *= inv_l;
+            put16(d0, acc, dz - d0);
+        }
     }
-    named_bar_sync(1, 256);
-    const int tid = threadIdx.x - 64;  // 0..255 over warps 2..9
+    }  // generic shapes
     const int rows = min(BM, p.L - q0);
-    if (rows <= 0) return;
     __nv_bfloat16* gout = p.feat_out + (static_cast<int64_t>(b) * p.L + q0) * p.feat_ld + h * seg;
-    if (seg % 8 == 0 && p.feat_ld % 8 == 0 && ((h * seg) % 8) == 0) {
-        const int per_row = seg / 8;
-        for (int e = tid; e < rows * per_row; e += 256) {
-            const int r = e / per_row, k = e - r * per_row;
-            *reinterpret_cast<uint4*>(gout + static_cast<int64_t>(r) * p.feat_ld + 8 * k) =
-                *reinterpret_cast<const uint4*>(fst + r * sst + 8 * k);
+    const bool bulk = (seg * 2) % 16 == 0 && (p.feat_ld * 2) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(gout) & 15) == 0;
+    if (bulk) ptx::fence_proxy_async_smem();  // row visible to the bulk-copy engine
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 4);
+    named_bar_sync(1, 256);
+    if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 5);
+    if (rows <= 0) return;
+    const int tid = threadIdx.x - 64;  // 0..255 over warps 2..9
+    if (bulk) {
+        // one contiguous seg-wide bf16 row segment per query row, by the bulk-copy engine
+        if (tid < rows) {
+            ptx::bulk_store_s2g(gout + static_cast<int64_t>(tid) * p.feat_ld, fst + tid * sst, seg * 2);
+            ptx::bulk_commit_group();
+            ptx::bulk_wait_group_read<0>();  // shared memory stays valid until read
         }
     } else {
         for (int e = tid; e < rows * seg; e += 256) {
@@ -519,6 +716,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         lb[half * 128 + row] = l;
         named_bar_sync(2 + quad, 64);
         l += lb[(half ^ 1) * 128 + row];
+        // residue frame for the point epilogue, fetched while the last PV MMAs run
+        float Rm[9], tv[3];
+        {
+            const int qi = q0 + row;
+            const int64_t g = static_cast<int64_t>(bh / p.H) * p.L + (qi < p.L ? qi : 0);
+            if (half == 0) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) Rm[k] = __ldg(p.rot + g * 9 + k);
+#pragma unroll
+                for (int y = 0; y < 3; ++y) tv[y] = __ldg(p.trans + g * 3 + y);
+            }
+        }
         ptx::mbar_wait(&bars->o_full, 0);
         if (lane == 0) FIPA_TRACE(9, 0);
         ptx::tc_fence_after();
@@ -578,7 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 256);
             if (!z_early) issue_z1();
         }
-        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full);
+        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full, Rm, tv);
         if (lane == 0) FIPA_TRACE(9, 1);
     }
 

@@ -79,5 +79,10 @@ int main(int argc, char** argv) {
                        T(cta,w,13,j)-t0, j ? T(cta,w,3,j)-t0 : 0, T(cta,w,14,j)-t0, T(cta,w,4,j)-t0);
         }
     printf("o_full %lld  end %lld\n", T(0,2,9,0)-t0, T(0,2,9,1)-t0);
+    for (int cta = 0; cta < 2; ++cta)
+        for (int w = 2; w < 10; ++w)
+            printf("epi cta%d w%d: pre %6lld scalar %6lld points %6lld zwait %6lld pair %6lld bar %6lld store %6lld\n", cta, w,
+                   T(cta,w,15,0)-T(cta,w,9,0), T(cta,w,15,1)-T(cta,w,15,0), T(cta,w,15,2)-T(cta,w,15,1), T(cta,w,15,3)-T(cta,w,15,2),
+                   T(cta,w,15,4)-T(cta,w,15,3), T(cta,w,15,5)-T(cta,w,15,4), T(cta,w,9,1)-T(cta,w,15,5));
     return 0;
 }
