@@ -63,6 +63,7 @@ struct Attn2Params {
     float* lse;
     float* o_save;  // [BH, L, dv_pad] normalised O_hat (fp32) for the backward, or null
     int dv_pad;
+    int feat_tma;  // feature blocks written by per-warp TMA stores (fast epilogue shapes)
 };
 
 struct Bars {
@@ -90,7 +91,10 @@ __host__ __device__ inline Layout smem_layout(int n_qkb, int nb1, int nb2) {
     return l;
 }
 __host__ __device__ constexpr int epilogue_smem(int seg) {
-    return (BM * ((seg + 7) / 8 * 8 + 8) * 2 + 1023) / 1024 * 1024;
+    // row-major staging rows of (seg rounded to 8) + 8 bf16, or 64-column swizzled blocks
+    return (BM * ((seg + 7) / 8 * 8 + 8) * 2 + 1023) / 1024 * 1024 > (seg + 63) / 64 * BM * 128
+               ? (BM * ((seg + 7) / 8 * 8 + 8) * 2 + 1023) / 1024 * 1024
+               : (seg + 63) / 64 * BM * 128;
 }
 
 // Optional per-event timestamps of clusters (0,0) for pipeline analysis (tools/attn_trace2.cu).
@@ -152,8 +156,10 @@ __device__ __forceinline__ void load_z16_smem(const uint8_t* zs, int row, int f,
 
 // Points block of one row (half 0), branch-free over kMaxPoints so the independent points
 // interleave: local = R_i^T (g - t_i) (proj/src/geometry.cpp:70-76) and |local|, as bf16 pairs.
+template <bool SW>
 __device__ __forceinline__ void epilogue_points(uint32_t tl_pts, float inv_l, int Nv, const float* Rm,
-                                                const float* tv, __nv_bfloat16* fp, bool ok) {
+                                                const float* tv, __nv_bfloat16* fp, bool ok,
+                                                uint8_t* blk = nullptr, int row = 0) {
     uint32_t o[48];  // warp-collective TMEM loads: every lane, rows past L included
     ptx::tmem_ld16(tl_pts, o);
     ptx::tmem_ld16(tl_pts + 16, o + 16);
@@ -180,6 +186,19 @@ __device__ __forceinline__ void epilogue_points(uint32_t tl_pts, float inv_l, in
     }
     // [x0 y0 z0 x1 ... | n0 n1 ...]: 3*Nv coordinates then Nv norms
     const int nc = 3 * Nv;
+    if (SW) {  // Nv even: bf16 pairs into the swizzled staging block (element e in chunk e / 8)
+        auto put2 = [&](int e, float x0, float x1) {
+            *reinterpret_cast<uint32_t*>(blk + row * 128 + ((((e >> 3) ^ (row & 7))) << 4) + ((2 * e) & 15)) =
+                ptx::pack_bf16x2(x0, x1);
+        };
+#pragma unroll
+        for (int e = 0; e < 3 * kMaxPoints / 2; ++e)
+            if (2 * e + 1 < nc) put2(2 * e, v[2 * e], v[2 * e + 1]);
+#pragma unroll
+        for (int i = 0; i < kMaxPoints / 2; ++i)
+            if (2 * i + 1 < Nv) put2(nc + 2 * i, nrm[2 * i], nrm[2 * i + 1]);
+        return;
+    }
     if ((reinterpret_cast<uintptr_t>(fp) & 3) != 0) {
 #pragma unroll
         for (int e = 0; e < 3 * kMaxPoints; ++e)
@@ -231,7 +250,28 @@ __device__ __forceinline__ void put16_vec(__nv_bfloat16* dst, const float* x) {
     reinterpret_cast<uint4*>(dst)[1] = w1;
 }
 
-__device__ __forceinline__ void epilogue_scalar128(uint32_t tl, float inv_l, int half, __nv_bfloat16* frow) {
+// 16 bf16 into a 128-byte-swizzled [128 rows][64 cols] staging block (TMA store layout) at column
+// col (col % 16 == 0): 16-byte chunk j of row r sits at r * 128 + ((j ^ (r & 7)) << 4)
+__device__ __forceinline__ void put16_sw(uint8_t* blk, int row, int col, const float* x) {
+    uint4 w0, w1;
+    w0.x = ptx::pack_bf16x2(x[0], x[1]);
+    w0.y = ptx::pack_bf16x2(x[2], x[3]);
+    w0.z = ptx::pack_bf16x2(x[4], x[5]);
+    w0.w = ptx::pack_bf16x2(x[6], x[7]);
+    w1.x = ptx::pack_bf16x2(x[8], x[9]);
+    w1.y = ptx::pack_bf16x2(x[10], x[11]);
+    w1.z = ptx::pack_bf16x2(x[12], x[13]);
+    w1.w = ptx::pack_bf16x2(x[14], x[15]);
+    const int j = col >> 3;
+    *reinterpret_cast<uint4*>(blk + row * 128 + ((j ^ (row & 7)) << 4)) = w0;
+    *reinterpret_cast<uint4*>(blk + row * 128 + (((j + 1) ^ (row & 7)) << 4)) = w1;
+}
+
+// SW: write into the swizzled staging block `blk` (columns relative to the block) instead of
+// the row-major feature row `frow`
+template <bool SW>
+__device__ __forceinline__ void epilogue_scalar128(uint32_t tl, float inv_l, int half, int row,
+                                                   __nv_bfloat16* frow, uint8_t* blk) {
     uint32_t o[4][16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) ptx::tmem_ld16(tl + 64 * half + 16 * k, o[k]);
@@ -241,13 +281,17 @@ __device__ __forceinline__ void epilogue_scalar128(uint32_t tl, float inv_l, int
         float x[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(o[k][e]) * inv_l;
-        put16_vec(frow + 128 + 64 * half + 16 * k, x);
+        if (SW) {
+            put16_sw(blk, row, 16 * k, x);
+        } else {
+            put16_vec(frow + 128 + 64 * half + 16 * k, x);
+        }
     }
 }
 
-template <int RANK>
+template <int RANK, bool SW>
 __device__ __forceinline__ void epilogue_pair128(uint32_t tl, float inv_l, int half, int row, const uint8_t* zs,
-                                                 __nv_bfloat16* frow) {
+                                                 __nv_bfloat16* frow, uint8_t* blk) {
     constexpr int CB = 4 / RANK;  // chunks per TMEM wait
 #pragma unroll
     for (int b0 = 0; b0 < 4; b0 += CB) {
@@ -271,7 +315,11 @@ __device__ __forceinline__ void epilogue_pair128(uint32_t tl, float inv_l, int h
             }
 #pragma unroll
             for (int e = 0; e < 16; ++e) acc[e] *= inv_l;
-            put16_vec(frow + d0, acc);
+            if (SW) {
+                put16_sw(blk, row, 16 * (b0 + k), acc);
+            } else {
+                put16_vec(frow + d0, acc);
+            }
         }
     }
 }
@@ -279,7 +327,8 @@ __device__ __forceinline__ void epilogue_pair128(uint32_t tl, float inv_l, int h
 __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl, float inv_l,
                                                int row, int q0, int bh, uint8_t* smem, int half,
                                                const uint8_t* zs, uint64_t* z_full, const float* Rm,
-                                               const float* tv) {
+                                               const float* tv, const CUtensorMap* map_f,
+                                               const CUtensorMap* map_fp) {
     const int seg = p.seg, sst = (seg + 7) / 8 * 8 + 8;
     __nv_bfloat16* fst = reinterpret_cast<__nv_bfloat16*>(smem);
     __nv_bfloat16* frow = fst + row * sst;
@@ -314,17 +363,54 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
 
     if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 0);
     const bool fast = c == 128 && dz == 128 && (p.rank == 1 || p.rank == 2) && zs != nullptr;
-    if (fast) {
-        epilogue_scalar128(tl, inv_l, half, frow);
+    if (p.feat_tma) {
+        // c = d_z = 128, z1 staged, Nv even: each warp stages its 32 rows of a 64-column block
+        // swizzled and writes it with one TMA store as soon as the block is complete, so the
+        // feature writes overlap the rest of the epilogue: blocks [pair lo|pair hi|scalar lo|
+        // scalar hi|points] of 16 KB each
+        const int r0 = row & ~31;
+        auto store_box = [&](int cb, const CUtensorMap* map, int col) {
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                ptx::tma_store_3d(map, smem + cb * (BM * 128) + r0 * 128, h * seg + col, q0 + r0, b);
+                ptx::bulk_commit_group();
+            }
+        };
+        epilogue_scalar128<true>(tl, inv_l, half, row, frow, smem + (2 + half) * (BM * 128));
+        store_box(2 + half, map_f, 128 + 64 * half);
         if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 1);
-        if (half == 0) epilogue_points(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
+        if (half == 0) {
+            epilogue_points<true>(tl + base, inv_l, Nv, Rm, tv, nullptr, ok, smem + 4 * (BM * 128), row);
+            store_box(4, map_fp, 256);
+        }
         if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 2);
         ptx::mbar_wait(z_full, 0);
         if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 3);
         if (p.rank == 1) {
-            epilogue_pair128<1>(tl, inv_l, half, row, zs, frow);
+            epilogue_pair128<1, true>(tl, inv_l, half, row, zs, frow, smem + half * (BM * 128));
         } else {
-            epilogue_pair128<2>(tl, inv_l, half, row, zs, frow);
+            epilogue_pair128<2, true>(tl, inv_l, half, row, zs, frow, smem + half * (BM * 128));
+        }
+        store_box(half, map_f, 64 * half);
+        if ((threadIdx.x & 31) == 0) {
+            FIPA_TRACE(15, 4);
+            FIPA_TRACE(15, 5);
+            ptx::bulk_wait_group_read<0>();  // staging read before the CTA exits
+        }
+        return;
+    }
+    if (fast) {
+        epilogue_scalar128<false>(tl, inv_l, half, row, frow, nullptr);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 1);
+        if (half == 0) epilogue_points<false>(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 2);
+        ptx::mbar_wait(z_full, 0);
+        if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 3);
+        if (p.rank == 1) {
+            epilogue_pair128<1, false>(tl, inv_l, half, row, zs, frow, nullptr);
+        } else {
+            epilogue_pair128<2, false>(tl, inv_l, half, row, zs, frow, nullptr);
         }
     } else {
     // scalar aggregate -> [d_z, d_z + c): 16-column chunks split between the halves, four TMEM
@@ -349,7 +435,7 @@ __device__ __forceinline__ void fused_epilogue(const Attn2Params& p, uint32_t tl
     }
     if ((threadIdx.x & 31) == 0) FIPA_TRACE(15, 1);
     // points (half 0), all in registers: local = R_i^T (g - t_i)   (proj/src/geometry.cpp:70-76)
-    if (half == 0) epilogue_points(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
+    if (half == 0) epilogue_points<false>(tl + base, inv_l, Nv, Rm, tv, frow + dz + c, ok);
     // pair contraction -> [0, d_z): 16-column chunks split between the halves
     const float* z1r = p.z1 + grow * (p.rank * dz);
     const bool vec = (reinterpret_cast<uintptr_t>(z1r) & 15) == 0;
@@ -457,7 +543,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap mapK,
                         const __grid_constant__ CUtensorMap mapV,
                         const __grid_constant__ CUtensorMap mapZ,
-                        const __grid_constant__ CUtensorMap mapO, Attn2Params p) {
+                        const __grid_constant__ CUtensorMap mapO,
+                        const __grid_constant__ CUtensorMap mapF,   // features [B][L][feat_ld], box {64, 32, 1}
+                        const __grid_constant__ CUtensorMap mapFP,  // same, box {4 n_value, 32, 1}
+                        Attn2Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -482,6 +571,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(&mapK);
         ptx::tma_prefetch(&mapV);
         if (p.z1_tma) ptx::tma_prefetch(&mapZ);
+        if (p.feat_tma) {
+            ptx::tma_prefetch(&mapF);
+            ptx::tma_prefetch(&mapFP);
+        }
         ptx::mbar_init(&bars->q_full, 1);
         for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(&bars->k_full[s], 1);
@@ -787,7 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 256);
             if (!z_early) issue_z1();
         }
-        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full, Rm, tv);
+        fused_epilogue(p, tl, inv_l, row, q0, bh, smem, half, p.z1_tma ? zs : nullptr, &bars->z_full, Rm, tv, &mapF, &mapFP);
         if (lane == 0) FIPA_TRACE(9, 1);
     }
 
@@ -861,7 +954,17 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int qtiles = (a.L + BM - 1) / BM;
     dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(BH));
-    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, mapO, p);
+    // fast epilogue with per-warp TMA feature stores: c = d_z = 128, rank 1-2, z1 staged,
+    // even n_value (points block a whole number of 16-byte chunks), 16-byte aligned rows
+    p.feat_tma = (d.c == 128 && d.d_z == 128 && (d.rank == 1 || d.rank == 2) && p.z1_tma && d.n_value % 2 == 0 &&
+                  d.n_value <= kMaxPoints && d.seg == 256 + 4 * d.n_value && (d.feat_ld * 2) % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(a.feat) & 15) == 0)
+                     ? 1
+                     : 0;
+    const CUtensorMap mapF = p.feat_tma ? make_map_3d_bf16(a.feat, d.feat, a.L, a.B, d.feat_ld, 64, 32) : mapV;
+    const CUtensorMap mapFP =
+        p.feat_tma ? make_map_3d_bf16(a.feat, d.feat, a.L, a.B, d.feat_ld, 4 * d.n_value, 32) : mapV;
+    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, mapO, mapF, mapFP, p);
 }
 
 }  // namespace fipa_b200
