@@ -81,6 +81,7 @@ struct BwdParams {
     int acc_ld;
     int acc_col0[2];   // first accumulator column each pair writes (dQ split over the pairs)
     int b2_col0[2];    // first B2 column each pair streams
+    int ds_store;      // KV kernel: dS tiles also written to global [BH][Lk][ds_ld] (bf16) for dQ
 };
 
 struct Bars {
@@ -163,7 +164,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
                     const __grid_constant__ CUtensorMap b1D, const __grid_constant__ CUtensorMap b2D,
-                    BwdParams p) {
+                    const __grid_constant__ CUtensorMap mapDS, BwdParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -211,7 +212,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         for (int b = 0; b < 3; ++b) {
             ptx::mbar_init(&bars->mma2_done[b], 1);
             ptx::mbar_init(&bars->pin_full[b], 1);
-            ptx::mbar_init(&bars->pin_free[b], 1);
+            // materialised dS: the buffer is also released by the dS CTA once its TMA store has read it
+            ptx::mbar_init(&bars->pin_free[b], (KV && p.ds_store) ? 2 : 1);
             ptx::mbar_init(&bars->dsin_full[b], 1);
         }
         ptx::fence_mbar_init();
@@ -480,6 +482,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     BTRACE(7, j);
                 }
             } else {
+                if (KV && p.ds_store && j > 0 && warp == 2 && lane == 0) {
+                    // dS_{j-1}'s store has read its buffer: release it to the P pair
+                    ptx::bulk_wait_group_read<0>();
+                    ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(j - 1) % NAB], crank - 2u));
+                }
                 ptx::mbar_wait_cluster(&bars->pin_full[buf], (j / NAB) & 1);
                 if (lane == 0) BTRACE(9, j);
                 uint4 pin[4];
@@ -508,6 +515,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
                 if (lane == 0) BTRACE(10, j);
+                if (KV && p.ds_store) {
+                    // the whole 128-key x 64-query dS tile (already in the 128-byte-swizzled
+                    // K-major layout of the TMA box) -> dS[bh][key][query] for the dQ GEMM
+                    named_bar_sync(1, 256);
+                    if (warp == 2 && lane == 0) {
+                        ptx::tma_store_3d(&mapDS, abuf, j * BN, r0, bh);
+                        ptx::bulk_commit_group();
+                    }
+                }
                 if (!KV && p.role[0].n2 > 0) {
                     // Q kernel: the P pair accumulates the other half of dQ from the same dS tile
                     named_bar_sync(1, 256);
@@ -518,6 +534,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
 
+        if (KV && p.ds_store && role == 1 && warp == 2 && lane == 0) {
+            ptx::bulk_wait_group_read<0>();  // last dS store done reading before the CTA exits
+            if (ntiles > 0) ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(ntiles - 1) % NAB], crank - 2u));
+        }
         // ------------------------------------------------------------- epilogue
         float* out = p.acc_out[role];
         if (has_mma2 && out != nullptr) {
@@ -613,7 +633,7 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
-    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
+    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
 }
 
 template <bool KV>
@@ -693,9 +713,37 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.acc_out[0] = a.dv_acc;
         p.acc_out[1] = a.dk_acc;
         p.acc_ld = a.acc_ld;
-        const CUtensorMap maps[6] = {stat(a.khat, nqk), tile(a.qhat, p.kb1), slice(a.dohat),
-                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat)};
+        p.ds_store = a.ds != nullptr ? 1 : 0;
+        if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < a.L))
+            throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= L, % 8");
+        const CUtensorMap m0 = stat(a.khat, nqk);
+        const CUtensorMap maps[7] = {m0, tile(a.qhat, p.kb1), slice(a.dohat),
+                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat),
+                                     p.ds_store ? make_map_3d_bf16(a.ds, a.L, a.L, BH, a.ds_ld, 64, BM) : m0};
         launch<true>(d, a, p, maps, stream);
+    }
+    if ((which & 2) && a.ds != nullptr) {
+        // dQ from the materialised dS: per (sample, head) dQ_acc[q, :] = sum_key dS[key, q] K_hat[key, :],
+        // one batched tcgen05 GEMM (both operands MN-major) straight into the residue-major
+        // [B, L, H, acc_ld] accumulator -- no second pass over S, dP and the softmax
+        GemmArgs g{};
+        g.A = a.ds;
+        g.lda = a.ds_ld;
+        g.a_mn_major = true;
+        g.B = a.khat;
+        g.ldb = d.dqk_pad;
+        g.b_mn_major = true;
+        g.C = a.dq_acc;
+        g.ldc = int64_t(d.heads) * a.acc_ld;
+        g.ldc_h = a.acc_ld;
+        g.ldc_b = int64_t(a.L) * d.heads * a.acc_ld;
+        g.M = a.L;
+        g.N = d.dqk_mma;
+        g.K = a.L;
+        g.batch = static_cast<int>(BH);
+        g.batch_h = d.heads;
+        launch_gemm_bf16(g, stream);
+        which &= ~2;
     }
     if (which & 2) {  // Q kernel: P pair Q_hat/K_hat ; dS pair dO_hat/V_hat/K_hat -> dQ
         // dQ = dS.K_hat split over both pairs by columns: the P pair receives dS back from the
@@ -723,8 +771,9 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.b2_col0[0] = 0;
         p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
-        const CUtensorMap maps[6] = {stat(a.qhat, nqk), tile(a.khat, p.kb1), slice(a.khat),
-                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat)};
+        const CUtensorMap q0map = stat(a.qhat, nqk);
+        const CUtensorMap maps[7] = {q0map, tile(a.khat, p.kb1), slice(a.khat),
+                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat), q0map};
         launch<false>(d, a, p, maps, stream);
     }
 }

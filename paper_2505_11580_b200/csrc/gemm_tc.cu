@@ -45,6 +45,7 @@ struct EpiParams {
     float alpha;
     const float* bias;
     const uint8_t* row_mask;
+    int batch, batch_h;  // batched products (see GemmArgs)
 };
 
 // Persistent: each CTA walks work units u = blockIdx.x, += gridDim.x over (split, m-tile, n-tile).
@@ -71,9 +72,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = ptx::lane_id();
     const int n_tiles_n = (p.N + BN - 1) / BN;
     const int n_tiles_m = (p.M + BM - 1) / BM;
-    const int units = n_tiles_n * n_tiles_m * p.split_k;
+    const int per_batch = n_tiles_n * n_tiles_m * p.split_k;
+    const int units = per_batch * p.batch;
     const int nk_all = (p.K + BK - 1) / BK;
     auto unit_coords = [&](int u, int& m0, int& n0, int& kb0, int& nk) {
+        u -= (u / per_batch) * per_batch;
         const int z = u / (n_tiles_n * n_tiles_m);
         const int r = u - z * (n_tiles_n * n_tiles_m);
         m0 = (r / n_tiles_n) * BM;
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int m0, n0, kb0, nk;
                 unit_coords(u, m0, n0, kb0, nk);
+                const int zb = u / per_batch;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % Cfg::kStages;
                     if (it >= Cfg::kStages) ptx::mbar_wait(&empty[s], ((it / Cfg::kStages) - 1) & 1);
@@ -117,15 +121,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int kc = (kb0 + kb) * BK;
                     if (A_MN) {
                         for (int mb = 0; mb < BM / 64; ++mb)
-                            ptx::tma_load_2d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kc);
+                            ptx::tma_load_3d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kc, zb);
                     } else {
-                        ptx::tma_load_2d(sa, &mapA, &full[s], kc, m0);
+                        ptx::tma_load_3d(sa, &mapA, &full[s], kc, m0, zb);
                     }
                     if (B_MN) {
                         for (int nb = 0; nb < BN / 64; ++nb)
-                            ptx::tma_load_2d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kc);
+                            ptx::tma_load_3d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kc, zb);
                     } else {
-                        ptx::tma_load_2d(sb, &mapB, &full[s], kc, n0);
+                        ptx::tma_load_3d(sb, &mapB, &full[s], kc, n0, zb);
                     }
                 }
             }
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int m0, n0, kb0, nk;
             unit_coords(u, m0, n0, kb0, nk);
             const int buf = lu & 1;
+            const int zb = u / per_batch, zh = zb % p.batch_h, zo = zb / p.batch_h;
             ptx::mbar_wait(&acc_full[buf], (lu >> 1) & 1);
             ptx::tc_fence_after();
             const int row = m0 + quad * 32 + lane;
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        ptx::tma_store_2d(&mapC, sb, col0, m0 + quad * 32);
+                        ptx::tma_store_4d(&mapC, sb, col0, zh, m0 + quad * 32, zo);
                         ptx::bulk_commit_group();
                     }
                     ++nstore;
@@ -287,22 +292,35 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
     using Cfg = GemmCfg<BN>;
     // TMA maps: K-major operands are [rows=M|N, cols=K] with box {64, rows-per-tile};
     // MN-major operands are [rows=K, cols=M|N] with box {64, BK}.
-    const CUtensorMap mapA = A_MN ? make_map_2d_bf16(a.A, a.K, a.M, a.lda, 64, BK)
-                                  : make_map_2d_bf16(a.A, a.M, a.K, a.lda, 64, BM);
-    const CUtensorMap mapB = B_MN ? make_map_2d_bf16(a.B, a.K, a.N, a.ldb, 64, BK)
-                                  : make_map_2d_bf16(a.B, a.N, a.K, a.ldb, 64, BN);
+    // TMA maps (dim 2 = batch, dense stacks): K-major operands are [rows=M|N, cols=K] with box
+    // {64, rows-per-tile}; MN-major operands are [rows=K, cols=M|N] with box {64, BK}.
+    const uint64_t nb = static_cast<uint64_t>(std::max(1, a.batch));
+    const CUtensorMap mapA = A_MN ? make_map_3d_bf16(a.A, a.M, a.K, nb, a.lda, 64, BK)
+                                  : make_map_3d_bf16(a.A, a.K, a.M, nb, a.lda, 64, BM);
+    const CUtensorMap mapB = B_MN ? make_map_3d_bf16(a.B, a.N, a.K, nb, a.ldb, 64, BK)
+                                  : make_map_3d_bf16(a.B, a.K, a.N, nb, a.ldb, 64, BN);
     const bool tma_c = !a.out_bf16 && !a.accumulate && a.split_k <= 1 && (a.ldc * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+    const int bh = std::max(1, a.batch_h);
     EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, tma_c, std::max(1, a.split_k), a.alpha, a.bias,
-                a.row_mask};
-    const CUtensorMap mapC = tma_c ? make_map_2d_f32(a.C, a.M, a.N, a.ldc, 32, 32) : mapA;
+                a.row_mask, static_cast<int>(nb), bh};
+    // C as [batch / batch_h][M][batch_h][N]: box {32 cols, 1, 32 rows, 1} (the 2-D 32 x 32 box)
+    CUtensorMap mapC = mapA;
+    if (tma_c) {
+        const uint64_t cd[4] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(bh), static_cast<uint64_t>(a.M),
+                                nb / bh};
+        const uint64_t cs[3] = {static_cast<uint64_t>(nb > 1 ? a.ldc_h : a.ldc) * 4, static_cast<uint64_t>(a.ldc) * 4,
+                                static_cast<uint64_t>(nb > 1 ? a.ldc_b : int64_t(a.M) * a.ldc) * 4};
+        const uint32_t cb[4] = {32, 1, 32, 1};
+        mapC = make_map_4d_f32_strided(a.C, cd, cs, cb);
+    }
     auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         configured = true;
     }
-    const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k);
+    const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k) * static_cast<int>(nb);
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
@@ -325,6 +343,10 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
     if (a.accumulate && a.out_bf16) throw std::invalid_argument("gemm: accumulate needs fp32 C");
     if (a.split_k > 1 && (a.out_bf16 || a.bias || a.row_mask))
         throw std::invalid_argument("gemm: split-K accumulates plain fp32 C");
+    if (a.batch > 1 && (a.out_bf16 || a.accumulate || a.split_k > 1 || a.row_mask || (a.ldc * 4) % 16 != 0 ||
+                        (a.ldc_h * 4) % 16 != 0 || (a.ldc_b * 4) % 16 != 0 || a.batch % std::max(1, a.batch_h) != 0 ||
+                        (reinterpret_cast<uintptr_t>(a.C) & 15) != 0))
+        throw std::invalid_argument("gemm: batched products write plain, 16-byte aligned fp32 C");
     const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512);
     const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);
     if (wide) {

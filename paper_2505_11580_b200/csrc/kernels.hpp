@@ -29,6 +29,11 @@ struct GemmArgs {
     float alpha = 1.0f;
     const float* bias = nullptr;        // [N] or null
     const uint8_t* row_mask = nullptr;  // [M] or null: rows with 0 are written as 0
+    // Batched: `batch` independent products z = 0..batch-1 over dense operand stacks (A_z at
+    // A + z * (rows of A) * lda, likewise B); C_z at C + (z / batch_h) * ldc_b + (z % batch_h) * ldc_h
+    // (plain fp32 C only: no accumulate / split-K / row mask)
+    int batch = 1, batch_h = 1;
+    int64_t ldc_h = 0, ldc_b = 0;
 };
 void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 
@@ -140,6 +145,10 @@ struct AttnBwdArgs {
     // [G][B*H][kchunk][pad]; dk_acc / dv_acc then receive PARTIAL sums for all keys, rank-major
     // [G][B][kchunk][H][acc_ld] (ready for a reduce-scatter).  0 = unsharded (Lk = L).
     int Lk = 0, kchunk = 0;
+    // Optional materialised dS [B*H][L keys][ds_ld] (bf16, unsharded only): the dK/dV kernel
+    // stores its dS tiles there and dQ becomes one batched GEMM dS^T . K_hat (which & 2).
+    __nv_bfloat16* ds = nullptr;
+    int ds_ld = 0;
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both

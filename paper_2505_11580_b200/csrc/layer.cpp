@@ -554,9 +554,20 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
         w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
+        if (materialize_ds(B, L, d.heads)) {
+            w.ds_ld = static_cast<int>(round_up(static_cast<std::size_t>(L), 8));
+            w.ds = reinterpret_cast<__nv_bfloat16*>(take(BHL * w.ds_ld * 2));
+        }
     }
     w.bytes = off;
     return w;
+}
+
+bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L, int heads) {
+    const double bytes = double(B) * heads * double(L) * double((L + 7) / 8 * 8) * 2.0;
+    if (L > 2048 || bytes > double(1u << 30)) return false;
+    if (const char* e = std::getenv("FIPA_BWD_DS")) return std::atoi(e) != 0;
+    return true;
 }
 
 std::size_t FlashIpaLayer::workspace_size(std::int64_t B, std::int64_t L) const {
@@ -1076,6 +1087,9 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
             a.kchunk = int(L);
             a.dk_acc = shard->dk_part;
             a.dv_acc = shard->dv_part;
+        } else if (ws.ds != nullptr) {
+            a.ds = ws.ds;
+            a.ds_ld = ws.ds_ld;
         }
         launch_attn_bwd(d, a, stream, 1);
         mark(5);

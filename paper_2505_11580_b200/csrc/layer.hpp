@@ -157,6 +157,10 @@ public:
     // sum(out * dout) w.r.t. the inputs (fp32, any of drot/dtrans may be null) and the weights
     // (fp32, reference order w_q..b_out concatenated, num_weights() values).
     std::size_t train_workspace_size(std::int64_t B, std::int64_t L) const;
+    // Short-sequence backward: the dK/dV kernel also writes dS (bf16, B*H*L^2*2 bytes of the
+    // training workspace) and dQ is one batched GEMM instead of a second attention pass.  Used
+    // for L <= 2048 and at most 1 GiB of dS; FIPA_BWD_DS=0 / 1 forces it off / on (within that cap).
+    static bool materialize_ds(std::int64_t B, std::int64_t L, int heads);
     std::size_t num_weights() const;
     void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                   const float* rot, const float* trans, const std::uint8_t* mask, const float* dout,
@@ -213,6 +217,8 @@ public:
         float* dt_c = nullptr;             // [BL, 3]
         float* red = nullptr;              // [H + H d_z]  d(g) | d(w_l w_bias)
         float* dg_rows = nullptr;          // [BL, H] per-residue dgamma terms (unpack scratch)
+        __nv_bfloat16* ds = nullptr;       // [BH, L, ds_ld] materialised dS (short sequences, or null)
+        int ds_ld = 0;
         float* dwproj = nullptr;           // [d_in, n_proj]
         std::size_t bytes = 0;
     };

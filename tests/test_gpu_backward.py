@@ -49,6 +49,28 @@ def test_backward_main_shape(fipa, L):
     _check(fipa, MAIN, 2, L, seed=10 + L, mask_frac=0.1)
 
 
+@pytest.mark.parametrize("ds", ["0", "1"])
+def test_backward_both_dq_paths(fipa, monkeypatch, ds):
+    """dQ by the streaming attention kernel (FIPA_BWD_DS=0) and by the batched GEMM over the
+    dS the dK/dV kernel materialises (=1, the default for L <= 2048) -- each against the oracle."""
+    monkeypatch.setenv("FIPA_BWD_DS", ds)
+    _check(fipa, MAIN, 2, 257, seed=31, mask_frac=0.1)
+
+
+def test_dq_paths_agree(fipa, monkeypatch):
+    """Same dS values either way (same formula, same bf16 rounding); only the fp32 summation
+    order of dQ differs, so the gradients agree far inside the oracle gate."""
+    model = _model(fipa, MAIN, 13)
+    batch = make_batch(MAIN, 2, 320, seed=13, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(13).standard_normal((2, 320, MAIN["d_in"]))
+    got = {}
+    for ds in ("0", "1"):
+        monkeypatch.setenv("FIPA_BWD_DS", ds)
+        _, got[ds], _, _ = gpu_train_device(model, batch, dout)
+    for n in GRADS:
+        assert rel_dev(got["0"][n], got["1"][n]) < 1e-4, n
+
+
 def test_backward_tiny_shape(fipa):
     _check(fipa, TINY, 3, 37, seed=3, mask_frac=0.2)
 
@@ -86,9 +108,12 @@ def test_training_forward_matches_inference_forward(fipa):
     assert np.array_equal(out_inf, out_tr)
 
 
-def test_attention_backward_stage_parity(fipa):
+@pytest.mark.parametrize("ds", ["0", "1"])
+def test_attention_backward_stage_parity(fipa, monkeypatch, ds):
     """dO_hat, D and the three attention accumulators against the layout emulation
-    (tests/bwd_emulation.py) fed the device's own q/k/v_hat, O_hat and lse."""
+    (tests/bwd_emulation.py) fed the device's own q/k/v_hat, O_hat and lse; dQ from both the
+    streaming kernel and the materialised-dS GEMM."""
+    monkeypatch.setenv("FIPA_BWD_DS", ds)
     B, L = 1, 160
     shape = MAIN
     model = _model(fipa, shape, 8)
