@@ -487,7 +487,7 @@ def run_ours(args, shape):
             "attn_bwd_tflops": achieved_bwd,
             "stage_ms": stage_ms,
             "roofline": roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus,
-                                       peak_kind, traffic),
+                                       peak_kind, traffic, ds_mode=ds_mode(B, L, shape["heads"])),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (model.forward_launches() + (model.backward_launches() if train else 0)) * args.steps,
@@ -499,7 +499,15 @@ def run_ours(args, shape):
     return 0
 
 
-def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus, peak_kind, traffic):
+def ds_mode(B, L, H):
+    """Whether the backward materialises dS (layer.hpp FlashIpaLayer::materialize_ds)."""
+    if L > 2048 or B * H * L * ((L + 7) // 8 * 8) * 2 > (1 << 30):
+        return False
+    return os.environ.get("FIPA_BWD_DS", "1") != "0"
+
+
+def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus, peak_kind, traffic,
+                   ds_mode=False):
     """Roofline of the dominant attention kernel(s) of the step (tensor-bound)."""
     fwd = {"bound": "tensor", "kernel": "attn_fwd_2sm_kernel", "achieved": achieved, "peak": peak,
            "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
@@ -518,7 +526,10 @@ def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak,
                 bwd_traffic = json.load(f).get("dram_bytes_per_backward")
         except Exception:
             bwd_traffic = None
-    return {"bound": "tensor", "kernel": "attn_bwd_kernel<true> + attn_bwd_kernel<false> (dK/dV + dQ)",
+    # dQ path: layer.hpp FlashIpaLayer::materialize_ds (L <= 2048, dS <= 1 GiB, FIPA_BWD_DS override)
+    kernel = ("attn_bwd_kernel<true> (dK/dV, stores dS) + batched dQ GEMM gemm_bf16_kernel<256,MN,MN>"
+              if ds_mode else "attn_bwd_kernel<true> + attn_bwd_kernel<false> (dK/dV + dQ)")
+    return {"bound": "tensor", "kernel": kernel,
             "achieved": achieved_bwd, "peak": peak, "unit": "TFLOP/s", "frac": achieved_bwd / peak,
             "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})", "traffic": bwd_traffic,
             "algorithmic": f"2*B*H*L^2*(3*D_qk+2*D_v) = {bflops:.4g} FLOP per backward",

@@ -347,7 +347,9 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
                         (a.ldc_h * 4) % 16 != 0 || (a.ldc_b * 4) % 16 != 0 || a.batch % std::max(1, a.batch_h) != 0 ||
                         (reinterpret_cast<uintptr_t>(a.C) & 15) != 0))
         throw std::invalid_argument("gemm: batched products write plain, 16-byte aligned fp32 C");
-    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512);
+    // 256-wide tiles halve the shared-memory traffic per MMA (A is re-read per N tile); batched
+    // products with N in (256, 512] (dQ: N = 432) cover N with two of them
+    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512) || (a.batch > 1 && a.N > 256 && a.N <= 512);
     const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);
     if (wide) {
         switch (sel) {

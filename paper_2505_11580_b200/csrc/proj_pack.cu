@@ -144,6 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + kStages;
     uint64_t* done = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tile_ready = done + 2;  // [2] staging tile complete (one arrive per epilogue warp)
+    uint64_t* tile_free = done + 4;   // tile 0 read by tensor 0's stores (tensor 2 may overwrite it)
     uint8_t* ring = smem + 1024;
     // two output staging tiles (alternating tensors) reuse the ring once the MMAs are done
     uint8_t* tiles = ring;
@@ -159,6 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(done, 1);
+        ptx::mbar_init(&tile_ready[0], 8);
+        ptx::mbar_init(&tile_ready[1], 8);
+        ptx::mbar_init(tile_free, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
@@ -178,6 +183,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
                 ptx::tma_load_2d(sa + a_bytes, &mapB, &full[s], kb * BK, h * p.NH);
                 ptx::tma_load_2d(sa + a_bytes + (p.NH / 2) * 128, &mapB, &full[s], kb * BK, h * p.NH + p.NH / 2);
+            }
+            if (p.chunk_ok) {
+                // output stores: this otherwise idle thread issues every tile's TMA stores, so the
+                // epilogue warps go on building the next tensor while the previous one drains
+                // (issuing from the epilogue warps stalled them ~5k cycles per tensor on the
+                // store queue)
+                for (int tsel = 0; tsel < 3; ++tsel) {
+                    const int tb = tsel & 1;
+                    ptx::mbar_wait(&tile_ready[tb], (tsel >> 1) & 1);
+                    const uint8_t* tile = tiles + tb * tile_bytes;
+                    const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
+                    const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
+                    // 32-row chunks never straddle two samples (L % 32 == 0)
+                    for (int ch = 0; ch < BM / 32; ++ch) {
+                        const int rr = m0 + ch * 32;
+                        if (rr >= p.M) break;
+                        const int cb_ = rr / p.L, ci = rr - cb_ * p.L;
+                        for (int blk = 0; blk < width / 64; ++blk)
+                            tma_store_3d(map, tile + blk * (BM * 128) + ch * 32 * 128, blk * 64, ci, cb_ * p.H + h);
+                    }
+                    bulk_commit();
+                    if (tsel == 1) {
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // tensor 0 read
+                        ptx::mbar_arrive(tile_free);
+                    }
+                }
+                bulk_wait_read0();  // staging read before the CTA exits
             }
         }
     } else if (warp == 1) {
@@ -284,25 +316,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* tile = tiles + (tsel & 1) * tile_bytes;
             PPTRACE(3 + 4 * tsel);
             if (tsel == 2) {
-                // tile 0 is reused: tensor 0's TMA stores must have read it (tensor 1's may fly)
-                if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                named_sync(1, 256);
+                // tile 0 is reused: tensor 0's stores (or row copies) must have read it
+                if (p.chunk_ok) {
+                    ptx::mbar_wait(tile_free, 0);
+                } else {
+                    named_sync(1, 256);
+                }
             }
             const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
             float v8[8];
             // ---- phase A, half 0: [0, c) scalar channels from TMEM, 16 per load
             const float sc = tsel == 0 ? kL2E : tsel == 1 ? p.k_scale : 1.f;
             const int tcol = tsel == 0 ? cq : tsel == 1 ? ck : cv;
-            for (int c0 = 0; c0 < (half == 0 ? c : 0); c0 += 16) {
-                uint32_t u[16];
-                ptx::tmem_ld16(tl + tcol + c0, u);
-                ptx::tmem_wait_ld();
+            if (half == 0 && c % 32 == 0) {
+                // two TMEM loads in flight per wait (each round trip costs ~0.5k cycles; four
+                // spill at this kernel's 168-register cap)
+                for (int c0 = 0; c0 < c; c0 += 32) {
+                    uint32_t u[2][16];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[e]);
-                stage_put8(tile, r, c0, v8);
+                    for (int k = 0; k < 2; ++k) ptx::tmem_ld16(tl + tcol + c0 + 16 * k, u[k]);
+                    ptx::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[8 + e]);
-                stage_put8(tile, r, c0 + 8, v8);
+                    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[k][e]);
+                        stage_put8(tile, r, c0 + 16 * k, v8);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[k][8 + e]);
+                        stage_put8(tile, r, c0 + 16 * k + 8, v8);
+                    }
+                }
+            } else {
+                for (int c0 = 0; c0 < (half == 0 ? c : 0); c0 += 16) {
+                    uint32_t u[16];
+                    ptx::tmem_ld16(tl + tcol + c0, u);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[e]);
+                    stage_put8(tile, r, c0, v8);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v8[e] = sc * __uint_as_float(u[8 + e]);
+                    stage_put8(tile, r, c0 + 8, v8);
+                }
             }
             if (half == 0) {
             } else if (tsel < 2) {
@@ -419,23 +474,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             PPTRACE(5 + 4 * tsel);
-            ptx::fence_proxy_async_smem();
-            named_sync(1, 256);
-            PPTRACE(6 + 4 * tsel);
-            const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
             if (p.chunk_ok) {
-                // 32-row chunks never straddle two samples (L % 32 == 0): TMA stores, one thread
-                if (warp == 2 && lane == 0) {
-                    for (int ch = 0; ch < BM / 32; ++ch) {
-                        const int rr = m0 + ch * 32;
-                        if (rr >= p.M) break;
-                        const int cb_ = rr / p.L, ci = rr - cb_ * p.L;
-                        for (int blk = 0; blk < width / 64; ++blk)
-                            tma_store_3d(map, tile + blk * (BM * 128) + ch * 32 * 128, blk * 64, ci, cb_ * p.H + h);
-                    }
-                    bulk_commit();
-                }
-            } else if (ok && half == 0) {
+                ptx::fence_proxy_async_smem();  // rows visible to the TMA stores of warp 0
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tile_ready[tsel & 1]);
+                PPTRACE(6 + 4 * tsel);
+            } else {
+                named_sync(1, 256);
+                PPTRACE(6 + 4 * tsel);
+            }
+            if (!p.chunk_ok && ok && half == 0) {
                 // generic shapes: each thread copies its own row (16-byte chunks, un-swizzled)
                 __nv_bfloat16* dst = (tsel == 0 ? p.qhat : tsel == 1 ? p.khat : p.vhat) + hrow * width;
                 for (int ch8 = 0; ch8 < width / 8; ++ch8) {
@@ -444,7 +492,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-        if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         PPTRACE(15);
     }
     ptx::tc_fence_before();
