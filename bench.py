@@ -27,6 +27,10 @@ import sys
 import threading
 import time
 
+# NCCL's "NCCL version ..." banner goes to stdout, ahead of the one JSON line rank 0 prints
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
