@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) bwd_unpack_geo_kernel(LayerDims d, BwdUnp
     if (lane < H) a.dg_rows[row * H + lane] = s_dg[warp][lane];
 }
 
-__global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+__global__ void __launch_bounds__(256, 3) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z;
     const int tid = threadIdx.x;
@@ -378,8 +378,7 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpa
     float* s_wlb = s_dwlb + H * dz;     // H x dz
     const int zq = d.zq;
     const int64_t BL = static_cast<int64_t>(a.B) * a.L;
-    const int64_t row_begin = static_cast<int64_t>(blockIdx.x) * kUnpackRows;
-    const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
+    const int64_t ngroups = (BL + kUnpackRows - 1) / kUnpackRows;
     const int64_t acc_h = a.acc_ld;     // accumulator rows are residue-major [BL, H, acc_ld]
     const float kscale = a.k_scale * kLn2;
     const int half_c = c / 2;
@@ -394,7 +393,66 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpa
 #pragma unroll
     for (int h = 0; h < kUnpackMaxH; ++h) pw[h] = 0.f;
 
-    for (int rr = 0; rr < nrows; ++rr) {
+    // Fast path (H <= 8, one pair column per thread, a row's scalar columns in kBatchF float2 per
+    // thread): ALL of a row's loads -- 24 pair-column loads and the scalar float2 loads -- are
+    // issued before any use, so each row costs one memory latency instead of two.
+    constexpr int kBatchF = 6;
+    const bool fast = H <= 8 && reg_dwlb && pairs && rdz == static_cast<int>(blockDim.x) &&
+                      3 * H * half_c <= kBatchF * static_cast<int>(blockDim.x);
+    // persistent: groups of kUnpackRows residues strided over a grid of (SMs x resident blocks)
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t row_begin = grp * kUnpackRows;
+    const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
+    for (int rr = 0; fast && rr < nrows; ++rr) {
+        const int64_t row = row_begin + rr;
+        const float* qrow = a.dq_acc + row * H * acc_h;
+        const float* krow = a.dk_acc + row * H * acc_h;
+        const float* vrow = a.dv_acc + row * H * acc_h;
+        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
+        const int e = tid, dd = e % dz;
+        const float z2v = __ldg(a.z2 + row * rdz + e);
+        float s1 = __ldg(a.dz1_epi + row * rdz + e), s2 = 0.f;
+        float qq[8], kq[8], vq[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int h = min(u, H - 1);
+            qq[u] = __ldg(qrow + h * acc_h + zq + e);
+            kq[u] = __ldg(krow + h * acc_h + zq + e);
+            vq[u] = __ldg(vrow + h * acc_h + c + e);
+        }
+        const int total = 3 * H * half_c;
+        float2 v[kBatchF];
+#pragma unroll
+        for (int u = 0; u < kBatchF; ++u) {
+            const int idx = min(tid + u * static_cast<int>(blockDim.x), total - 1);
+            const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
+            const int h = rem / half_c, cc = 2 * (rem - h * half_c);
+            const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
+            v[u] = __ldg(reinterpret_cast<const float2*>(src));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u < H) {
+                const float k2 = kLn2 * kq[u];
+                s1 += qq[u];
+                s2 += s_wlb[u * dz + dd] * k2 + vq[u];
+                pw[u] = fmaf(k2, z2v, pw[u]);
+            }
+        }
+        a.dz1[row * rdz + e] = s1;
+        a.dz2[row * rdz + e] = s2;
+#pragma unroll
+        for (int u = 0; u < kBatchF; ++u) {
+            const int idx = tid + u * static_cast<int>(blockDim.x);
+            if (idx < total) {
+                // dproj column of the same (tensor, head, channel pair): idx * 2 in [q | k | v] order
+                const float sc = idx >= H * half_c && idx < 2 * H * half_c ? kscale : 1.f;
+                *reinterpret_cast<uint32_t*>(dp + 2 * idx) = ptx_pack(v[u].x * sc, v[u].y * sc);
+            }
+        }
+        for (int x = d.n_proj + tid; x < a.nproj_ld; x += blockDim.x) dp[x] = __float2bfloat16_rn(0.f);
+    }
+    for (int rr = 0; !fast && rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
         const float* qrow = a.dq_acc + row * H * acc_h;
         const float* krow = a.dk_acc + row * H * acc_h;
@@ -466,6 +524,7 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpa
         }
         for (int e = d.n_proj + tid; e < a.nproj_ld; e += blockDim.x) dp[e] = __float2bfloat16_rn(0.f);
     }
+    }  // groups
     if (reg_dwlb && tid < rdz) {
 #pragma unroll
         for (int h = 0; h < kUnpackMaxH; ++h)
@@ -475,7 +534,9 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_kernel(LayerDims d, BwdUnpa
     for (int e = tid; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
     if (tid < H) {
         float acc = 0.f;
-        for (int rr = 0; rr < nrows; ++rr) acc += a.dg_rows[(row_begin + rr) * H + tid];
+        for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x)
+            for (int64_t row = grp * kUnpackRows; row < BL && row < (grp + 1) * kUnpackRows; ++row)
+                acc += a.dg_rows[row * H + tid];
         atomicAdd(&a.dg[tid], acc);
     }
 }
@@ -628,7 +689,16 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     bwd_unpack_geo_kernel<<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    bwd_unpack_kernel<<<static_cast<unsigned>((BL + kUnpackRows - 1) / kUnpackRows), 256, smem, stream>>>(d, a);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
+    const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 3);  // 3 resident blocks per SM
+    bwd_unpack_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(d, a);
 }
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
