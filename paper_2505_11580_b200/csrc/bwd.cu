@@ -38,6 +38,13 @@ __device__ __forceinline__ uint32_t ptx_pack(float lo, float hi) {
 
 __device__ __forceinline__ float bfr(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
+// four consecutive bf16 (8-byte aligned) as floats
+__device__ __forceinline__ float4 ld4_bf16(const __nv_bfloat16* p) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                       __uint_as_float(w.y & 0xffff0000u));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -61,8 +68,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nv = d.n_value;
     const int nw = blockDim.x >> 5;
-    float* s_df = sm;                               // feat_ld   dfeat row
-    float* s_o = s_df + d.feat_ld;                  // H x dv_pad  O_hat rows
+    __nv_bfloat16* s_df = reinterpret_cast<__nv_bfloat16*>(sm);  // feat_ld   dfeat row (bf16)
+    float* s_o = sm + d.feat_ld / 2;                // H x dv_pad  O_hat rows (feat_ld % 8 == 0)
     float* s_z1 = s_o + H * d.dv_pad;               // rdz
     float* s_pair = s_z1 + ((rdz + 3) & ~3);        // nw x rdz   per-warp dz1 partials
     float* s_geo = s_pair + nw * rdz;               // nw x 12    per-warp dR (9) | dt (3)
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     if (threadIdx.x == 0) {
         ptx::mbar_init(bar, 1);
         ptx::fence_mbar_init();
-        const uint32_t df_bytes = d.feat_ld * 4, o_bytes = d.dv_pad * 4;
+        const uint32_t df_bytes = d.feat_ld * 2, o_bytes = d.dv_pad * 4;
         ptx::mbar_expect_tx(bar, df_bytes + H * o_bytes);
         bulk_g2s(s_df, a.dfeat + row * d.feat_ld, df_bytes, bar);
         bulk_g2s(s_o, a.ohat + row * H * d.dv_pad, H * o_bytes, bar);  // residue-major O_hat rows
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     for (int h = warp; h < H; h += nw) {
         const int64_t hrow = (static_cast<int64_t>(b) * H + h) * a.L + i;
         const float* o = s_o + h * d.dv_pad;
-        const float* df = s_df + h * d.seg;
+        const __nv_bfloat16* df = s_df + h * d.seg;
         float ds[3] = {0.f, 0.f, 0.f};
         if (lane < Nv) {
             const int p = lane;
@@ -112,10 +119,10 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
 #pragma unroll
             for (int x = 0; x < 3; ++x) loc[x] = R[x] * y[0] + R[3 + x] * y[1] + R[6 + x] * y[2];
             const float nrm = sqrtf(loc[0] * loc[0] + loc[1] * loc[1] + loc[2] * loc[2]);
-            const float sc = nrm > 0.f ? df[dz + c + 3 * Nv + p] / nrm : 0.f;
+            const float sc = nrm > 0.f ? __bfloat162float(df[dz + c + 3 * Nv + p]) / nrm : 0.f;
             float dl[3];
 #pragma unroll
-            for (int x = 0; x < 3; ++x) dl[x] = df[dz + c + 3 * p + x] + sc * loc[x];
+            for (int x = 0; x < 3; ++x) dl[x] = __bfloat162float(df[dz + c + 3 * p + x]) + sc * loc[x];
 #pragma unroll
             for (int x = 0; x < 3; ++x) {
                 ds[x] = R[3 * x] * dl[0] + R[3 * x + 1] * dl[1] + R[3 * x + 2] * dl[2];
@@ -136,7 +143,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
         if (vec) {
             // segment-wise, 4 columns per lane step: [dv | z1 (.) d(pair) | sum dg x2 | dg_p | 0]
             for (int j = lane; 4 * j < c; j += 32) {
-                const float4 dv = *reinterpret_cast<const float4*>(df + dz + 4 * j);
+                const float4 dv = ld4_bf16(df + dz + 4 * j);
                 const float4 ov = *reinterpret_cast<const float4*>(o + 4 * j);
                 const float v0 = bfr(dv.x), v1 = bfr(dv.y), v2 = bfr(dv.z), v3 = bfr(dv.w);
                 Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
             for (int j = lane; 4 * j < rdz; j += 32) {
                 const int e = 4 * j;
                 const float4 zz = *reinterpret_cast<const float4*>(s_z1 + e);
-                const float4 dpc = *reinterpret_cast<const float4*>(df + e % dz);
+                const float4 dpc = ld4_bf16(df + e % dz);
                 const float4 ov = *reinterpret_cast<const float4*>(o + c + e);
                 const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
                 Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
@@ -178,10 +185,10 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
             for (int u = 0; u < 4; ++u) {
                 const int col = 4 * c4 + u;
                 if (col < c) {
-                    v[u] = df[dz + col];
+                    v[u] = __bfloat162float(df[dz + col]);
                 } else if (col < vpair) {
                     const int e = col - c;
-                    const float dpc = df[e % dz];
+                    const float dpc = __bfloat162float(df[e % dz]);
                     v[u] = s_z1[e] * dpc;
                     pair_s[e] = (one_head ? 0.f : pair_s[e]) + oo[u] * dpc;  // warp-private slice, one lane per e
                 } else if (col < vpts) {
@@ -672,7 +679,7 @@ __global__ void scale_vec_kernel(const float* in, const float* scale, int period
 
 void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
-    if ((d.feat_ld * 4) % 16 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
+    if (d.feat_ld % 8 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
         throw std::invalid_argument("bwd_prep: row strides must be multiples of 16 bytes");
     const size_t smem = sizeof(float) * (d.feat_ld + d.heads * d.dv_pad + ((rdz + 3) & ~3) +
                                          8 * (rdz + 12 + 3 * d.n_value)) +

@@ -155,7 +155,7 @@ bool attn_bwd_supported(const LayerDims& d);
 void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream, int which = 3);
 
 struct BwdPrepArgs {
-    const float* dfeat;           // [BL, feat_ld] dOut . w_out^T
+    const __nv_bfloat16* dfeat;   // [BL, feat_ld] dOut . w_out^T (bf16)
     const float* ohat;            // [B, L, H, dv_pad] fp32 (residue-major), saved by the forward
     const float* z1;              // [BL, r*d_z]
     const float* rot;             // [BL, 9]

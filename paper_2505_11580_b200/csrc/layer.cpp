@@ -541,7 +541,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         const std::size_t rdz = std::size_t(d.rank) * d.d_z;
         w.o_hat = reinterpret_cast<float*>(take(BHL * d.dv_pad * 4));
         w.dout_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
-        w.dfeat = reinterpret_cast<float*>(take(BL * d.feat_ld * 4));
+        w.dfeat = reinterpret_cast<__nv_bfloat16*>(take(BL * d.feat_ld * 2));
         w.do_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));
         w.Dvec = reinterpret_cast<float*>(take(BHL * 4));
         w.dq_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
@@ -1026,6 +1026,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         g.b_mn_major = true;
         g.C = ws.dfeat;
         g.ldc = d.feat_ld;
+        g.out_bf16 = true;
         g.M = BL;
         g.N = d.feat;
         g.K = d.d_in;

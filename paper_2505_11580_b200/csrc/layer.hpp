@@ -205,7 +205,7 @@ public:
         // training extras (carve(..., train = true))
         float* o_hat = nullptr;            // [BH, L, dv_pad] fp32
         __nv_bfloat16* dout_bf16 = nullptr; // [BL, din_ld]
-        float* dfeat = nullptr;            // [BL, feat_ld]
+        __nv_bfloat16* dfeat = nullptr;    // [BL, feat_ld] (bf16: prep rounds dO_hat to bf16 anyway)
         __nv_bfloat16* do_hat = nullptr;   // [BH, L, dv_pad]
         float* Dvec = nullptr;             // [BH, L]
         float* dq_acc = nullptr;           // [BH, L, acc_ld]
