@@ -141,29 +141,32 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
         __nv_bfloat16* out = s_out + h * d.dv_pad;
         float Dp = 0.f;
         if (vec) {
-            // segment-wise, 4 columns per lane step: [dv | z1 (.) d(pair) | sum dg x2 | dg_p | 0]
+            // segment-wise, 4 columns per lane step: [dv | z1 (.) d(pair) | sum dg x2 | dg_p | 0],
+            // written straight to the global dO_hat row (8-byte stores, coalesced across the warp)
+            __nv_bfloat16* gout = a.dohat + hrow * d.dv_pad;
             for (int j = lane; 4 * j < c; j += 32) {
                 const float4 dv = ld4_bf16(df + dz + 4 * j);
                 const float4 ov = *reinterpret_cast<const float4*>(o + 4 * j);
-                const float v0 = bfr(dv.x), v1 = bfr(dv.y), v2 = bfr(dv.z), v3 = bfr(dv.w);
-                Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
-                *reinterpret_cast<uint2*>(out + 4 * j) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+                Dp += dv.x * ov.x + dv.y * ov.y + dv.z * ov.z + dv.w * ov.w;
+                *reinterpret_cast<uint2*>(gout + 4 * j) = make_uint2(ptx_pack(dv.x, dv.y), ptx_pack(dv.z, dv.w));
             }
-            for (int j = lane; 4 * j < rdz; j += 32) {
-                const int e = 4 * j;
-                const float4 zz = *reinterpret_cast<const float4*>(s_z1 + e);
-                const float4 dpc = ld4_bf16(df + e % dz);
-                const float4 ov = *reinterpret_cast<const float4*>(o + c + e);
-                const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
-                Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
-                float4 ps = one_head ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                     : *reinterpret_cast<float4*>(pair_s + e);  // warp-private slice
-                ps.x += ov.x * dpc.x;
-                ps.y += ov.y * dpc.y;
-                ps.z += ov.z * dpc.z;
-                ps.w += ov.w * dpc.w;
-                *reinterpret_cast<float4*>(pair_s + e) = ps;
-                *reinterpret_cast<uint2*>(out + c + 4 * j) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+            for (int rho = 0; rho < d.rank; ++rho) {  // pair block rho: d(pair) columns repeat per rank
+                for (int j = lane; 4 * j < dz; j += 32) {
+                    const int e = rho * dz + 4 * j;
+                    const float4 zz = *reinterpret_cast<const float4*>(s_z1 + e);
+                    const float4 dpc = ld4_bf16(df + 4 * j);
+                    const float4 ov = *reinterpret_cast<const float4*>(o + c + e);
+                    const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
+                    Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
+                    float4 ps = one_head ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                         : *reinterpret_cast<float4*>(pair_s + e);  // warp-private slice
+                    ps.x += ov.x * dpc.x;
+                    ps.y += ov.y * dpc.y;
+                    ps.z += ov.z * dpc.z;
+                    ps.w += ov.w * dpc.w;
+                    *reinterpret_cast<float4*>(pair_s + e) = ps;
+                    *reinterpret_cast<uint2*>(gout + c + e) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+                }
             }
             for (int col = vpair + lane; col < d.dv_pad; col += 32) {
                 float v = 0.f;
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
                 }
                 else if (col < vend) v = dopt_s[col - vpts];
                 v = bfr(v);
-                out[col] = __float2bfloat16_rn(v);
+                gout[col] = __float2bfloat16_rn(v);
                 if (col < d.dv_used) Dp += v * o[col];
             }
         } else {
@@ -218,8 +221,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
     if (lane < 12) s_geo[warp * 12 + lane] = lane < 9 ? dR[lane] : dt[lane - 9];
     __syncthreads();
-    const int per_row = d.dv_pad / 8;  // 16-byte chunks per dO_hat row
-    for (int e = threadIdx.x; e < H * per_row; e += blockDim.x) {
+    const int per_row = d.dv_pad / 8;  // 16-byte chunks per dO_hat row (staged rows: generic shapes)
+    for (int e = threadIdx.x; !vec && e < H * per_row; e += blockDim.x) {
         const int h = e / per_row, k = e - h * per_row;
         reinterpret_cast<uint4*>(a.dohat + ((static_cast<int64_t>(b) * H + h) * a.L + i) * d.dv_pad)[k] =
             reinterpret_cast<const uint4*>(s_out + h * d.dv_pad)[k];
