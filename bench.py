@@ -505,7 +505,7 @@ def run_ours(args, shape):
 
 def ds_mode(B, L, H):
     """Whether the backward materialises dS (layer.hpp FlashIpaLayer::materialize_ds)."""
-    if L > 2048 or B * H * L * ((L + 7) // 8 * 8) * 2 > (1 << 30):
+    if L > 2048 or B * H * L * ((L + 63) // 64 * 64) * 2 > (1 << 30):
         return False
     return os.environ.get("FIPA_BWD_DS", "1") != "0"
 

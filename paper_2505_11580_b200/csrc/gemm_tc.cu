@@ -46,6 +46,7 @@ struct EpiParams {
     const float* bias;
     const uint8_t* row_mask;
     int batch, batch_h;  // batched products (see GemmArgs)
+    int a_blk, b_blk;    // MN-major operand loaded as ONE 4-D box of 64-column blocks (ld % 64 == 0)
 };
 
 // Persistent: each CTA walks work units u = blockIdx.x, += gridDim.x over (split, m-tile, n-tile).
@@ -119,13 +120,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sb = sa + Cfg::kABytes;
                     ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
                     const int kc = (kb0 + kb) * BK;
-                    if (A_MN) {
+                    // (the TMA engine costs ~100 cycles per box: one box per operand and stage)
+                    if (A_MN && p.a_blk) {
+                        ptx::tma_load_4d(sa, &mapA, &full[s], 0, kc, m0 / 64, zb);
+                    } else if (A_MN) {
                         for (int mb = 0; mb < BM / 64; ++mb)
                             ptx::tma_load_3d(sa + mb * 64 * 128, &mapA, &full[s], m0 + mb * 64, kc, zb);
                     } else {
                         ptx::tma_load_3d(sa, &mapA, &full[s], kc, m0, zb);
                     }
-                    if (B_MN) {
+                    if (B_MN && p.b_blk) {
+                        ptx::tma_load_4d(sb, &mapB, &full[s], 0, kc, n0 / 64, zb);
+                    } else if (B_MN) {
                         for (int nb = 0; nb < BN / 64; ++nb)
                             ptx::tma_load_3d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kc, zb);
                     } else {
@@ -295,15 +301,21 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
     // TMA maps (dim 2 = batch, dense stacks): K-major operands are [rows=M|N, cols=K] with box
     // {64, rows-per-tile}; MN-major operands are [rows=K, cols=M|N] with box {64, BK}.
     const uint64_t nb = static_cast<uint64_t>(std::max(1, a.batch));
-    const CUtensorMap mapA = A_MN ? make_map_3d_bf16(a.A, a.M, a.K, nb, a.lda, 64, BK)
-                                  : make_map_3d_bf16(a.A, a.K, a.M, nb, a.lda, 64, BM);
-    const CUtensorMap mapB = B_MN ? make_map_3d_bf16(a.B, a.N, a.K, nb, a.ldb, 64, BK)
-                                  : make_map_3d_bf16(a.B, a.K, a.N, nb, a.ldb, 64, BN);
+    // MN-major operands whose row stride is a whole number of 64-column blocks (and covers the
+    // tile's columns) come in as ONE 4-D box {64, BK, tile/64 blocks} per stage
+    const bool a_blk = A_MN && a.lda % 64 == 0 && a.lda >= a.M;
+    const bool b_blk = B_MN && a.ldb % 64 == 0 && a.ldb >= a.N;
+    const CUtensorMap mapA = a_blk  ? make_map_blocks_bf16(a.A, a.K, nb, a.lda, BK, BM / 64)
+                             : A_MN ? make_map_3d_bf16(a.A, a.M, a.K, nb, a.lda, 64, BK)
+                                    : make_map_3d_bf16(a.A, a.K, a.M, nb, a.lda, 64, BM);
+    const CUtensorMap mapB = b_blk  ? make_map_blocks_bf16(a.B, a.K, nb, a.ldb, BK, BN / 64)
+                             : B_MN ? make_map_3d_bf16(a.B, a.N, a.K, nb, a.ldb, 64, BK)
+                                    : make_map_3d_bf16(a.B, a.K, a.N, nb, a.ldb, 64, BN);
     const bool tma_c = !a.out_bf16 && !a.accumulate && a.split_k <= 1 && (a.ldc * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
     const int bh = std::max(1, a.batch_h);
     EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, tma_c, std::max(1, a.split_k), a.alpha, a.bias,
-                a.row_mask, static_cast<int>(nb), bh};
+                a.row_mask, static_cast<int>(nb), bh, a_blk ? 1 : 0, b_blk ? 1 : 0};
     // C as [batch / batch_h][M][batch_h][N]: box {32 cols, 1, 32 rows, 1} (the 2-D 32 x 32 box)
     CUtensorMap mapC = mapA;
     if (tma_c) {

@@ -555,7 +555,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
         w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
         if (materialize_ds(B, L, d.heads)) {
-            w.ds_ld = static_cast<int>(round_up(static_cast<std::size_t>(L), 8));
+            w.ds_ld = static_cast<int>(round_up(static_cast<std::size_t>(L), 64));  // whole 64-column blocks
             w.ds = reinterpret_cast<__nv_bfloat16*>(take(BHL * w.ds_ld * 2));
         }
     }
@@ -564,7 +564,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
 }
 
 bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L, int heads) {
-    const double bytes = double(B) * heads * double(L) * double((L + 7) / 8 * 8) * 2.0;
+    const double bytes = double(B) * heads * double(L) * double((L + 63) / 64 * 64) * 2.0;
     if (L > 2048 || bytes > double(1u << 30)) return false;
     if (const char* e = std::getenv("FIPA_BWD_DS")) return std::atoi(e) != 0;
     return true;
