@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) bwd_unpack_geo_kernel(LayerDims d, BwdUnp
     if (lane < H) a.dg_rows[row * H + lane] = s_dg[warp][lane];
 }
 
-__global__ void __launch_bounds__(256, 3) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+__global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z;
     const int tid = threadIdx.x;
@@ -413,54 +413,67 @@ __global__ void __launch_bounds__(256, 3) bwd_unpack_kernel(LayerDims d, BwdUnpa
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t row_begin = grp * kUnpackRows;
     const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
-    for (int rr = 0; fast && rr < nrows; ++rr) {
-        const int64_t row = row_begin + rr;
+    struct RowLoads {
+        float qq[8], kq[8], vq[8];
+        float2 v[kBatchF];
+        float z2v, s1;
+    };
+    const int total = 3 * H * half_c;
+    auto load_row = [&](int64_t row, RowLoads& L) {
         const float* qrow = a.dq_acc + row * H * acc_h;
         const float* krow = a.dk_acc + row * H * acc_h;
         const float* vrow = a.dv_acc + row * H * acc_h;
-        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
-        const int e = tid, dd = e % dz;
-        const float z2v = __ldg(a.z2 + row * rdz + e);
-        float s1 = __ldg(a.dz1_epi + row * rdz + e), s2 = 0.f;
-        float qq[8], kq[8], vq[8];
+        L.z2v = __ldg(a.z2 + row * rdz + tid);
+        L.s1 = __ldg(a.dz1_epi + row * rdz + tid);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int h = min(u, H - 1);
-            qq[u] = __ldg(qrow + h * acc_h + zq + e);
-            kq[u] = __ldg(krow + h * acc_h + zq + e);
-            vq[u] = __ldg(vrow + h * acc_h + c + e);
+            L.qq[u] = __ldg(qrow + h * acc_h + zq + tid);
+            L.kq[u] = __ldg(krow + h * acc_h + zq + tid);
+            L.vq[u] = __ldg(vrow + h * acc_h + c + tid);
         }
-        const int total = 3 * H * half_c;
-        float2 v[kBatchF];
 #pragma unroll
         for (int u = 0; u < kBatchF; ++u) {
             const int idx = min(tid + u * static_cast<int>(blockDim.x), total - 1);
             const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
             const int h = rem / half_c, cc = 2 * (rem - h * half_c);
             const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
-            v[u] = __ldg(reinterpret_cast<const float2*>(src));
+            L.v[u] = __ldg(reinterpret_cast<const float2*>(src));
         }
+    };
+    auto finish_row = [&](int64_t row, const RowLoads& L) {
+        const int dd = tid % dz;
+        float s1 = L.s1, s2 = 0.f;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (u < H) {
-                const float k2 = kLn2 * kq[u];
-                s1 += qq[u];
-                s2 += s_wlb[u * dz + dd] * k2 + vq[u];
-                pw[u] = fmaf(k2, z2v, pw[u]);
+                const float k2 = kLn2 * L.kq[u];
+                s1 += L.qq[u];
+                s2 += s_wlb[u * dz + dd] * k2 + L.vq[u];
+                pw[u] = fmaf(k2, L.z2v, pw[u]);
             }
         }
-        a.dz1[row * rdz + e] = s1;
-        a.dz2[row * rdz + e] = s2;
+        a.dz1[row * rdz + tid] = s1;
+        a.dz2[row * rdz + tid] = s2;
+        __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
 #pragma unroll
         for (int u = 0; u < kBatchF; ++u) {
             const int idx = tid + u * static_cast<int>(blockDim.x);
             if (idx < total) {
                 // dproj column of the same (tensor, head, channel pair): idx * 2 in [q | k | v] order
                 const float sc = idx >= H * half_c && idx < 2 * H * half_c ? kscale : 1.f;
-                *reinterpret_cast<uint32_t*>(dp + 2 * idx) = ptx_pack(v[u].x * sc, v[u].y * sc);
+                *reinterpret_cast<uint32_t*>(dp + 2 * idx) = ptx_pack(L.v[u].x * sc, L.v[u].y * sc);
             }
         }
         for (int x = d.n_proj + tid; x < a.nproj_ld; x += blockDim.x) dp[x] = __float2bfloat16_rn(0.f);
+    };
+    // two residues' loads in flight per thread before either is used
+    for (int rr = 0; fast && rr < nrows; rr += 2) {
+        RowLoads L0, L1;
+        load_row(row_begin + rr, L0);
+        if (rr + 1 < nrows) load_row(row_begin + rr + 1, L1);
+        finish_row(row_begin + rr, L0);
+        if (rr + 1 < nrows) finish_row(row_begin + rr + 1, L1);
     }
     for (int rr = 0; !fast && rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
@@ -707,7 +720,7 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
         if (sms <= 0) sms = 148;
     }
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
-    const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 3);  // 3 resident blocks per SM
+    const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 2);  // 2 resident blocks per SM
     bwd_unpack_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(d, a);
 }
 
