@@ -552,16 +552,24 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int g = rr / p.stat_chunk, gi = rr - g * p.stat_chunk;
             float* orow = out + (((static_cast<int64_t>(g) * p.B + bb) * p.stat_chunk + gi) * p.H + hh) * p.acc_ld +
                           p.acc_col0[role];
-            for (int ch = lo; ch < hi; ++ch) {
-                uint32_t o[16];
-                ptx::tmem_ld16(tl + 16 * ch, o);
+            // four TMEM loads in flight per wait (one round trip costs ~0.5k cycles)
+            for (int ch0 = lo; ch0 < hi; ch0 += 4) {
+                uint32_t o[4][16];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (ch0 + k < hi) ptx::tmem_ld16(tl + 16 * (ch0 + k), o[k]);
                 ptx::tmem_wait_ld();
                 if (grow < p.Lrow) {
-                    float4* dst = reinterpret_cast<float4*>(orow + 16 * ch);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        dst[q] = make_float4(__uint_as_float(o[4 * q]), __uint_as_float(o[4 * q + 1]),
-                                             __uint_as_float(o[4 * q + 2]), __uint_as_float(o[4 * q + 3]));
+                    for (int k = 0; k < 4; ++k) {
+                        if (ch0 + k < hi) {
+                            float4* dst = reinterpret_cast<float4*>(orow + 16 * (ch0 + k));
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                dst[q] = make_float4(__uint_as_float(o[k][4 * q]), __uint_as_float(o[k][4 * q + 1]),
+                                                     __uint_as_float(o[k][4 * q + 2]), __uint_as_float(o[k][4 * q + 3]));
+                        }
+                    }
                 }
             }
         }
