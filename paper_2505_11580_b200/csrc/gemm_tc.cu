@@ -141,34 +141,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
-            int it = 0, lu = 0;  // k-block counter, local unit counter
-            for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
-                int m0, n0, kb0, nk;
-                unit_coords(u, m0, n0, kb0, nk);
-                const int buf = lu & 1;
-                if (lu >= 2) ptx::mbar_wait(&acc_empty[buf], ((lu >> 1) - 1) & 1);
+        // The whole warp runs the loop and one elected lane issues (warp-uniform descriptors in
+        // uniform registers; a lane-0-only loop paid ~45 cycles of R2UR per MMA, which left the
+        // N=128 MMAs issue-bound); descriptors advance by 64-bit adds of (byte offset >> 4).
+        constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+        const uint32_t tiles_u32 = ptx::smem_u32(tiles);
+        const uint64_t da0 = A_MN ? ptx::sw128_desc(tiles_u32, 64 * 128, 1024) : ptx::sw128_desc(tiles_u32, 16, 1024);
+        const uint64_t db0 = B_MN ? ptx::sw128_desc(tiles_u32 + Cfg::kABytes, 64 * 128, 1024)
+                                  : ptx::sw128_desc(tiles_u32 + Cfg::kABytes, 16, 1024);
+        constexpr uint64_t kStepA = A_MN ? (2048 >> 4) : (32 >> 4);  // one 16-deep K step
+        constexpr uint64_t kStepB = B_MN ? (2048 >> 4) : (32 >> 4);
+        int it = 0, lu = 0;  // k-block counter, local unit counter
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
+            int m0, n0, kb0, nk;
+            unit_coords(u, m0, n0, kb0, nk);
+            const int buf = lu & 1;
+            if (lu >= 2) ptx::mbar_wait(&acc_empty[buf], ((lu >> 1) - 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t acc = tmem + buf * BN;
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % Cfg::kStages;
+                ptx::mbar_wait(&full[s], (it / Cfg::kStages) & 1);
                 ptx::tc_fence_after();
-                const uint32_t acc = tmem + buf * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % Cfg::kStages;
-                    ptx::mbar_wait(&full[s], (it / Cfg::kStages) & 1);
-                    ptx::tc_fence_after();
-                    const uint32_t sa = ptx::smem_u32(tiles + s * Cfg::kStageBytes);
-                    const uint32_t sb = sa + Cfg::kABytes;
+                if (ptx::elect_one()) {
+                    const uint64_t so = static_cast<uint64_t>((s * Cfg::kStageBytes) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t da = A_MN ? ptx::sw128_desc(sa + kk * 2048, 64 * 128, 1024)
-                                                 : ptx::sw128_desc(sa + kk * 32, 16, 1024);
-                        const uint64_t db = B_MN ? ptx::sw128_desc(sb + kk * 2048, 64 * 128, 1024)
-                                                 : ptx::sw128_desc(sb + kk * 32, 16, 1024);
-                        ptx::mma_ss(acc, da, db, idesc, (kb | kk) != 0);
-                    }
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        ptx::mma_ss(acc, da0 + so + kk * kStepA, db0 + so + kk * kStepB, idesc, (kb | kk) != 0);
                     ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&acc_full[buf]);
+                __syncwarp();
             }
+            if (ptx::elect_one()) ptx::mma_commit(&acc_full[buf]);
+            __syncwarp();
         }
     } else {
         // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
