@@ -26,11 +26,15 @@ constexpr int kThreads = 192;
 
 template <int BN>
 struct GemmCfg {
+    // Output staging buffers per epilogue warp: 2 keep up once the epilogue math is branch-free
+    // (tools/gemm_bench.cu: 4 buffers at the cost of ring stages measured no faster on the
+    // short-K shapes and 13% slower on a square 8192^3 product).
     static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kCBuf = 2;
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStageC = 4 * 2 * 32 * 128;  // fp32 output staging: 4 warps x 2 x (32 rows x 128 B)
+    static constexpr int kStageC = 4 * kCBuf * 32 * 128;  // fp32 output staging: 4 warps x kCBuf x (32 rows x 128 B)
     static constexpr int kSmem = kStages * kStageBytes + kStageC + 1024 /*align*/ + 256 /*barriers*/;
     static_assert(2 * BN <= 512, "double-buffered accumulator must fit TMEM");
 };
@@ -48,6 +52,18 @@ struct EpiParams {
     int batch, batch_h;  // batched products (see GemmArgs)
     int a_blk, b_blk;    // MN-major operand loaded as ONE 4-D box of 64-column blocks (ld % 64 == 0)
 };
+
+#ifdef FIPA_GEMM_TRACE
+__device__ long long g_gemm_trace[2][8][24];  // [epilogue warp 2 | MMA warp][unit][event], CTA 0
+#define GTRACE(w, u, ev)                                                              \
+    do {                                                                              \
+        if (blockIdx.x == 0 && (u) < 8 && (ev) < 24) g_gemm_trace[w][u][ev] = clock64(); \
+    } while (0)
+#else
+#define GTRACE(w, u, ev) \
+    do {                 \
+    } while (0)
+#endif
 
 // Persistent: each CTA walks work units u = blockIdx.x, += gridDim.x over (split, m-tile, n-tile).
 // The smem ring runs continuously across units; the accumulator is double-buffered in TMEM
@@ -156,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             int m0, n0, kb0, nk;
             unit_coords(u, m0, n0, kb0, nk);
             const int buf = lu & 1;
+            if (lane == 0) GTRACE(1, lu, 0);
             if (lu >= 2) ptx::mbar_wait(&acc_empty[buf], ((lu >> 1) - 1) & 1);
+            if (lane == 0) GTRACE(1, lu, 1);
             ptx::tc_fence_after();
             const uint32_t acc = tmem + buf * BN;
             for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -174,19 +192,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (ptx::elect_one()) ptx::mma_commit(&acc_full[buf]);
             __syncwarp();
+            if (lane == 0) GTRACE(1, lu, 2);
         }
     } else {
         // Epilogue: warp w reads TMEM lanes [32*(w%4), +32); thread = one output row.
         const int quad = warp & 3;
-        uint8_t* my_stage = stage_c + quad * (2 * 32 * 128);
-        int nstore = 0;  // TMA stores issued by this warp (staging buffer = nstore & 1)
+        uint8_t* my_stage = stage_c + quad * (Cfg::kCBuf * 32 * 128);
+        int nstore = 0;  // TMA stores issued by this warp (staging buffer = nstore % kCBuf)
         int lu = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
             int m0, n0, kb0, nk;
             unit_coords(u, m0, n0, kb0, nk);
             const int buf = lu & 1;
             const int zb = u / per_batch, zh = zb % p.batch_h, zo = zb / p.batch_h;
+            if (warp == 2 && lane == 0) GTRACE(0, lu, 0);
             ptx::mbar_wait(&acc_full[buf], (lu >> 1) & 1);
+            if (warp == 2 && lane == 0) GTRACE(0, lu, 1);
             ptx::tc_fence_after();
             const int row = m0 + quad * 32 + lane;
             const bool row_ok = row < p.M;
@@ -195,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t r[32];
                 ptx::tmem_ld32(tmem + buf * BN + (uint32_t(quad * 32) << 16) + c0, r);
                 ptx::tmem_wait_ld();
+                if (warp == 2 && lane == 0) GTRACE(0, lu, 2 + 2 * (c0 / 32));
                 const int col0 = n0 + c0;
                 if (p.tma_c) {
                     // warp-collective path: rows past M are clipped by the TMA store; nk == 0 (an
@@ -219,18 +241,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     continue;
                 }
+                // (a per-element `bias != null && col < N` test compiled to 32 dependent branches,
+                // ~2k cycles per chunk: tools/gemm_trace.cu; the bias test is uniform, hoist it)
                 float v[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float x = __uint_as_float(r[i]) * p.alpha;
-                    const int col = col0 + i;
-                    if (p.bias != nullptr && col < p.N) x += p.bias[col];
-                    v[i] = zero_row ? 0.0f : x;
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+                if (p.bias != nullptr) {
+                    if (col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(p.bias + col0) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 bq = __ldg(reinterpret_cast<const float4*>(p.bias + col0) + q);
+                            v[4 * q] += bq.x;
+                            v[4 * q + 1] += bq.y;
+                            v[4 * q + 2] += bq.z;
+                            v[4 * q + 3] += bq.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < p.N) v[i] += __ldg(p.bias + col0 + i);
+                    }
+                }
+                if (zero_row) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.0f;
                 }
                 if (p.tma_c) {
                     // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
-                    uint8_t* sb = my_stage + (nstore & 1) * (32 * 128);
-                    if (nstore >= 2 && lane == 0) ptx::bulk_wait_group_read<1>();  // buffer's last store has read it
+                    uint8_t* sb = my_stage + (nstore % Cfg::kCBuf) * (32 * 128);
+                    if (nstore >= Cfg::kCBuf && lane == 0)
+                        ptx::bulk_wait_group_read<Cfg::kCBuf - 1>();  // buffer's last store has read it
                     __syncwarp();
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
@@ -241,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) {
                         ptx::tma_store_4d(&mapC, sb, col0, zh, m0 + quad * 32, zo);
                         ptx::bulk_commit_group();
+                        if (warp == 2) GTRACE(0, lu, 3 + 2 * (c0 / 32));
                     }
                     ++nstore;
                     continue;
