@@ -267,27 +267,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         PPTRACE(1);
 
-        // points: frame-rotated (geometry half only); raw copies into proj when training
+        // points: frame-rotated (geometry half only); the raw copies into proj (training) go out
+        // after the three tensors
         float rq[3 * kMaxQ], rk[3 * kMaxQ], rv[3 * kMaxV];
         if (half == 1) {
-            float* prow = p.proj + int64_t(rowc) * p.n_proj;
-            const int oq = 3 * p.H * c + h * 3 * Nq, okp = oq + 3 * p.H * Nq, ov = 3 * p.H * c + 6 * p.H * Nq + h * 3 * Nv;
             uint32_t u[32], w[16];
             ptx::tmem_ld32(tl + cqp, u);
             ptx::tmem_ld16(tl + cqp + 32, w);
             ptx::tmem_wait_ld();
             rotate_points<kMaxQ>(u, w, Nq, R, rq);
-            if (p.write_points && ok) store_points(prow + oq, u, w, 3 * Nq);
             ptx::tmem_ld32(tl + ckp, u);
             ptx::tmem_ld16(tl + ckp + 32, w);
             ptx::tmem_wait_ld();
             rotate_points<kMaxQ>(u, w, Nq, R, rk);
-            if (p.write_points && ok) store_points(prow + okp, u, w, 3 * Nq);
             ptx::tmem_ld32(tl + cvp, u);
             ptx::tmem_ld16(tl + cvp + 32, w);
             ptx::tmem_wait_ld();
             rotate_points<kMaxV>(u, w, Nv, R, rv);
-            if (p.write_points && ok) store_points(prow + ov, u, w, 3 * Nv);
         }
         float qb[3] = {0.f, 0.f, 0.f}, W[3] = {0.f, 0.f, 0.f}, kn = 0.f;
 #pragma unroll
@@ -490,6 +486,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint8_t* src = tile + (ch8 >> 3) * (BM * 128) + r * 128 + (((ch8 & 7) ^ (r & 7)) << 4);
                     reinterpret_cast<uint4*>(dst)[ch8] = *reinterpret_cast<const uint4*>(src);
                 }
+            }
+        }
+        // raw point columns for the backward, after the three tensors: their scattered global
+        // stores no longer compete with the staging-tile writes of tensor 0 (TMEM still holds them)
+        if (half == 1 && p.write_points) {
+            float* prow = p.proj + int64_t(rowc) * p.n_proj;
+            const int oq = 3 * p.H * c + h * 3 * Nq, okp = oq + 3 * p.H * Nq, ov = 3 * p.H * c + 6 * p.H * Nq + h * 3 * Nv;
+            const int cols[3] = {cqp, ckp, cvp}, offs[3] = {oq, okp, ov}, ns[3] = {3 * Nq, 3 * Nq, 3 * Nv};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                uint32_t u[32], w[16];
+                ptx::tmem_ld32(tl + cols[k], u);
+                ptx::tmem_ld16(tl + cols[k] + 32, w);
+                ptx::tmem_wait_ld();
+                if (ok) store_points(prow + offs[k], u, w, ns[k]);
             }
         }
         PPTRACE(15);
