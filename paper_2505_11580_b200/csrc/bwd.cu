@@ -737,7 +737,7 @@ void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const Scat
 }
 
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {
-    bwd_recenter_kernel<<<B, 256, 0, stream>>>(dt_c, mask, dt, L);
+    bwd_recenter_kernel<<<B, 1024, 0, stream>>>(dt_c, mask, dt, L);
 }
 
 void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream) {

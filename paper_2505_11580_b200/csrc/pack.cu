@@ -699,7 +699,7 @@ void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, in
 
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream) {
-    recenter_kernel<<<B, 256, 0, stream>>>(trans, mask, out, L);
+    recenter_kernel<<<B, 1024, 0, stream>>>(trans, mask, out, L);  // one block per sample: all of L in one pass
 }
 
 }  // namespace fipa_b200
