@@ -256,7 +256,7 @@ constexpr int kUnpackMaxH = 16;
 //                          dz2 = sum_h (w_l w_bias[h, e % d_z] ln2 dk[zq+e] + dv[c+e]),
 //                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials);
 //                          dg += sum of dg_rows over the block's residues.
-__global__ void __launch_bounds__(256) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
+__global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
     // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
     // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
     // heads with one warp reduction; per-head dgamma terms go through shared memory.
