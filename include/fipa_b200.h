@@ -175,7 +175,8 @@ int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L, const double* 
 /* Byte offsets of the training intermediates in a train workspace, -1 when absent:
  *   0 o_hat (f32 [B,L,H,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
  *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B,L,H,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
- *   7 dfeat (f32 [B*L,feat_ld]).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.  Returns 8. */
+ *   7 dfeat (bf16 [B*L,feat_ld]).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.  Returns 8.
+ * Every slot is present in a train workspace (none is -1). */
 int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
                                       int64_t* dims);
 int fipa_layer_backward_launches(const fipa_layer* layer);
@@ -297,6 +298,24 @@ int fipa_build_factors_host(int64_t rows, uint64_t f, const double* features, ui
 
 /* Number of kernels fipa_layer_forward launches per call for this configuration. */
 int fipa_layer_forward_launches(const fipa_layer* layer);
+
+/* Kernel-selection / tuning knobs of a layer.  Fixed per layer: seeded once at creation from
+ * the FIPA_* environment variables named below (A/B experiments; defaults = the measured-best
+ * choices), changed only by fipa_layer_set_tuning -- never read on the launch path.  Not
+ * thread-safe against concurrent compute calls on the same layer.
+ *   attn_impl  inference attention kernel: 0 automatic, 1 CTA pair, 2 two-pass, 3 single CTA
+ *              (FIPA_ATTN_IMPL = pair | pass | 1sm; a sharded forward never takes 3)
+ *   fused_pack 1: fused projection + pack kernel (FIPA_FUSED_PACK=0 -> GEMM + pack kernel)
+ *   bwd_ds     materialised-dS backward: -1 automatic (L <= 2048, dS <= 1 GiB), 0 off, 1 on
+ *              within that cap (FIPA_BWD_DS)
+ *   bwd_ring   attention-backward ring plan {nst1, nst2, nab, kb1}, zeros = automatic (FIPA_BWD_RING)
+ *   pass_ring  two-pass attention rings {kb, kst, vkeys, vst}, zeros = automatic (FIPA_PASS_RING) */
+typedef struct fipa_tuning {
+    int32_t attn_impl, fused_pack, bwd_ds;
+    int32_t bwd_ring[4], pass_ring[4];
+} fipa_tuning;
+int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
+int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);
 
 /* Optional per-stage device timing (CUDA events on the forward's stream).  After enabling,
  * every forward records stage times; fipa_layer_stage_times copies up to n values (ms) in the

@@ -596,16 +596,16 @@ RoleDims make_role(int k1, int n2) {
 // fixed; whole 32-row B1 tile halves (1 or 2 stages) and 16-row B2 slices (compile-time depth)
 // share the rest: dQ kernel (2, 6 x 4 KB), dK/dV kernel (1, 6 x 8 KB).  Whole-tile B1 stages
 // measured faster than column-block groups (dK/dV 0.406 vs 0.439 ms at B=8 L=1024, same-box A/B).
-void finish_params(BwdParams& p, bool kv) {
+void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
     p.stat_bytes = nb1 * BM * 128;
     p.kb1 = nb1;
     p.b1_stage = nb1 * 32 * 128;
     p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    int forced[4] = {0, 0, 0, 0};  // FIPA_BWD_RING="nst1,nst2,nab,kb1": tuning experiments
-    if (const char* e = std::getenv("FIPA_BWD_RING"))
-        std::sscanf(e, "%d,%d,%d,%d", &forced[0], &forced[1], &forced[2], &forced[3]);
+    int forced[4] = {0, 0, 0, 0};  // AttnBwdArgs::ring (Tuning::bwd_ring): tuning experiments
+    if (ring != nullptr)
+        for (int i = 0; i < 4; ++i) forced[i] = ring[i];
     // (B1 stages, B2 stages, exchange buffers), preferred first.  Measured (B=8 L=1024, same box):
     // dK/dV kernel (1,6,2) 0.392 ms vs (1,4,3) 0.397; dQ kernel (1,4,3) 0.349 vs (2,6,2) 0.358.
     // (kb1 = 0: whole-tile B1 stages)
@@ -715,7 +715,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
-        finish_params(p, true);
+        finish_params(p, true, a.ring);
         p.lse = a.lse;
         p.Dvec = a.Dvec;
         p.acc_out[0] = a.dv_acc;
@@ -769,7 +769,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.B = a.B;
         p.role[0] = make_role(d.dqk_mma, nq0);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma - nq0);
-        finish_params(p, false);
+        finish_params(p, false, a.ring);
         p.lse = a.lse;
         p.Dvec = a.Dvec;
         p.acc_out[0] = a.dq_acc;

@@ -544,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // Host-side plan: value split, TMEM columns, ring depths that fit shared memory.
-bool make_plan(const LayerDims& d, PassParams& p, Layout& lay) {
+bool make_plan(const LayerDims& d, PassParams& p, Layout& lay, const int* ring = nullptr) {
     p = PassParams{};
     const int c = d.c, dz = d.d_z, r = d.rank;
     if (c % 16 != 0 || dz % 16 != 0 || r < 1 || 3 * d.n_value + 6 > 48 || d.dqk_pad % 64 != 0 ||
@@ -586,9 +586,9 @@ bool make_plan(const LayerDims& d, PassParams& p, Layout& lay) {
     // barrier round trip; 4 KB stages measured 1.3x slower than 12 KB ones at rank 3)
     const int cand[][4] = {{4, 3, 32, 2}, {3, 3, 32, 2}, {4, 2, 32, 2}, {3, 2, 32, 2}, {2, 3, 32, 2}, {3, 2, 16, 3}, {3, 2, 16, 2},
                            {2, 2, 32, 2}, {2, 2, 16, 3}, {2, 2, 16, 2}, {1, 4, 16, 2}, {1, 3, 16, 2}, {1, 2, 16, 2}};
-    int forced[4] = {0, 0, 0, 0};
-    if (const char* e = std::getenv("FIPA_PASS_RING"))  // "kb,kst,vkeys,vst" (tuning experiments)
-        std::sscanf(e, "%d,%d,%d,%d", &forced[0], &forced[1], &forced[2], &forced[3]);
+    int forced[4] = {0, 0, 0, 0};  // AttnArgs::pass_ring (Tuning::pass_ring): tuning experiments
+    if (ring != nullptr)
+        for (int i = 0; i < 4; ++i) forced[i] = ring[i];
     for (const auto& cd0 : cand) {
         const int* cd = forced[0] > 0 ? forced : cd0;
         if (cd[1] > 4 || cd[3] > 4) return false;
@@ -617,7 +617,7 @@ bool attn_fwd_pass_supported(const LayerDims& d) {
 void launch_attn_fwd_pass(const LayerDims& d, const AttnArgs& a, cudaStream_t stream) {
     PassParams p;
     Layout lay;
-    if (!make_plan(d, p, lay))
+    if (!make_plan(d, p, lay, a.pass_ring))
         throw std::invalid_argument("tcgen05 two-pass attention: lifted widths unsupported (use precision='f32')");
     if (a.o_save != nullptr) throw std::invalid_argument("two-pass attention: no training forward (O_hat save)");
     p.L = a.L;

@@ -505,6 +505,43 @@ public:
         return py::make_tuple(out, g);
     }
     void set_timing(bool on) { check(fipa_layer_set_timing(layer_, on ? 1 : 0)); }
+    py::dict tuning() const {
+        fipa_tuning t{};
+        check(fipa_layer_get_tuning(layer_, &t));
+        static const char* attn[4] = {"auto", "pair", "pass", "1sm"};
+        py::dict d;
+        d["attn_impl"] = attn[t.attn_impl];
+        d["fused_pack"] = t.fused_pack != 0;
+        d["bwd_ds"] = t.bwd_ds;
+        d["bwd_ring"] = std::vector<int>(t.bwd_ring, t.bwd_ring + 4);
+        d["pass_ring"] = std::vector<int>(t.pass_ring, t.pass_ring + 4);
+        return d;
+    }
+    // Keyword-wise update of the layer's tuning knobs (fipa_layer_set_tuning); None keeps a value.
+    void set_tuning(py::object attn_impl, py::object fused_pack, py::object bwd_ds, py::object bwd_ring,
+                    py::object pass_ring) {
+        fipa_tuning t{};
+        check(fipa_layer_get_tuning(layer_, &t));
+        if (!attn_impl.is_none()) {
+            const std::string v = attn_impl.cast<std::string>();
+            if (v == "auto") t.attn_impl = 0;
+            else if (v == "pair") t.attn_impl = 1;
+            else if (v == "pass") t.attn_impl = 2;
+            else if (v == "1sm") t.attn_impl = 3;
+            else throw py::value_error("attn_impl must be 'auto', 'pair', 'pass' or '1sm'");
+        }
+        if (!fused_pack.is_none()) t.fused_pack = fused_pack.cast<bool>() ? 1 : 0;
+        if (!bwd_ds.is_none()) t.bwd_ds = bwd_ds.cast<int>();
+        auto ring = [](py::object o, int32_t* dst) {
+            if (o.is_none()) return;
+            const auto v = o.cast<std::vector<int>>();
+            if (v.size() != 4) throw py::value_error("ring plans have 4 entries");
+            for (int i = 0; i < 4; ++i) dst[i] = v[i];
+        };
+        ring(bwd_ring, t.bwd_ring);
+        ring(pass_ring, t.pass_ring);
+        check(fipa_layer_set_tuning(layer_, &t));
+    }
     std::vector<float> stage_times() const {
         std::vector<float> t(16);
         t.resize(fipa_layer_stage_times(layer_, t.data(), 16));
@@ -746,6 +783,9 @@ PYBIND11_MODULE(_fipa_b200, m) {
              py::arg("rotations"), py::arg("translations"), py::arg("dout"), py::arg("mask") = py::none(),
              "Forward + backward (gradient of sum(out * dout)) on the GPU")
         .def("set_timing", &Model::set_timing, py::arg("enable"))
+        .def("tuning", &Model::tuning)
+        .def("set_tuning", &Model::set_tuning, py::arg("attn_impl") = py::none(), py::arg("fused_pack") = py::none(),
+             py::arg("bwd_ds") = py::none(), py::arg("bwd_ring") = py::none(), py::arg("pass_ring") = py::none())
         .def("stage_times", &Model::stage_times)
         .def("bwd_stage_times", &Model::bwd_stage_times)
         .def_property_readonly("precision", &Model::precision)

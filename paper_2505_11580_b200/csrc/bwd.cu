@@ -245,9 +245,11 @@ constexpr int kUnpackMaxH = 16;
 
 // Lifts^T (pack.cu / proj_pack.cu reversed), in two launches so each half runs at its own
 // occupancy:
-//  bwd_unpack_geo_kernel   block = one residue, warp per head, lane per point: frame-applied point
-//                          gradients -> dproj point columns; dR, dt reduced across heads in shared
-//                          memory -> drot, dt_c; per-residue dgamma -> dg_rows [BL, H].
+//  bwd_unpack_geo_kernel   block = 8 residues, one warp per residue with lanes over (head, point)
+//                          tasks: frame-applied point gradients -> dproj point columns; dR, dt
+//                          summed over the residue's heads by one warp reduction -> drot, dt_c;
+//                          per-residue dgamma terms -> dg_rows [BL, H] (via shared memory).
+//                          (launch bounds 256 x 4 cap it at 64 registers; ptxas -v: no spills)
 //  bwd_unpack_kernel       block streams kUnpackRows residues; every accumulator column of the
 //                          scalar and pair blocks is read by exactly one thread with coalesced
 //                          loads (no staging, all loads of a residue in flight at once):
@@ -310,7 +312,10 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
             dt[x] += dA[x];
         }
         // d/dg of -g/2 |A - B|^2 summed with dS: A.(sum_j dS B) - |A|^2 S1 / 2 (+ key part)
-        float dgh = (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) / g -
+        // gB carries the factor g; a head whose g rounds to 0 (very negative gamma_raw) has
+        // gB == 0 too, and its term is taken as 0 instead of 0/0
+        const float inv_g = g != 0.f ? 1.f / g : 0.f;
+        float dgh = (A[0] * gB[0] + A[1] * gB[1] + A[2] * gB[2]) * inv_g -
                     0.5f * (A[0] * A[0] + A[1] * A[1] + A[2] * A[2]) * S1;
 #pragma unroll
         for (int x = 0; x < 3; ++x) {
@@ -712,13 +717,7 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     bwd_unpack_geo_kernel<<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = device_sm_count();
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
     const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 2);  // 2 resident blocks per SM
     bwd_unpack_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(d, a);

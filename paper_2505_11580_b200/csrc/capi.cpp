@@ -341,6 +341,37 @@ int fipa_layer_forward_launches(const fipa_layer* layer) {
     return layer ? layer->impl->launches_per_forward() : 0;
 }
 
+int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
+    return guarded([&] {
+        if (layer == nullptr || out == nullptr) throw fipa_b200::ValueError("null layer or tuning");
+        const auto& t = layer->impl->tuning();
+        out->attn_impl = static_cast<int32_t>(t.attn);
+        out->fused_pack = t.fused_pack ? 1 : 0;
+        out->bwd_ds = t.bwd_ds;
+        for (int i = 0; i < 4; ++i) {
+            out->bwd_ring[i] = t.bwd_ring[i];
+            out->pass_ring[i] = t.pass_ring[i];
+        }
+    });
+}
+
+int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in) {
+    return guarded([&] {
+        if (layer == nullptr || in == nullptr) throw fipa_b200::ValueError("null layer or tuning");
+        if (in->attn_impl < 0 || in->attn_impl > 3) throw fipa_b200::ValueError("tuning: attn_impl must be 0..3");
+        if (in->bwd_ds < -1 || in->bwd_ds > 1) throw fipa_b200::ValueError("tuning: bwd_ds must be -1, 0 or 1");
+        fipa_b200::Tuning t;
+        t.attn = static_cast<fipa_b200::Tuning::Attn>(in->attn_impl);
+        t.fused_pack = in->fused_pack != 0;
+        t.bwd_ds = in->bwd_ds;
+        for (int i = 0; i < 4; ++i) {
+            t.bwd_ring[i] = in->bwd_ring[i];
+            t.pass_ring[i] = in->pass_ring[i];
+        }
+        L(layer).set_tuning(t);
+    });
+}
+
 int fipa_layer_set_timing(fipa_layer* layer, int enable) {
     return guarded([&] { L(layer).set_timing(enable != 0); });
 }

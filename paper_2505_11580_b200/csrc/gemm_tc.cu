@@ -373,19 +373,9 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
         mapC = make_map_4d_f32_strided(a.C, cd, cs, cb);
     }
     auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-        configured = true;
-    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);  // per device
     const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k) * static_cast<int>(nb);
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = device_sm_count();
     dim3 grid(static_cast<unsigned>(std::min(units, sms)));
     kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, mapC, p);
 }

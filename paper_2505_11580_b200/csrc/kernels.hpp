@@ -8,6 +8,10 @@
 
 namespace fipa_b200 {
 
+// SM count of the current device (cached per device, thread-safe); grids of the persistent
+// kernels are sized from it.
+int device_sm_count();
+
 // ------------------------------------------------------------------ GEMM
 // C[M,N] = alpha * A[M,K] . B[K,N] (+ bias[N]) (+ beta*C), rows with row_mask==0 zeroed.
 //   a_mn_major = false: A stored row-major [M, K] (lda >= K)
@@ -116,6 +120,7 @@ struct AttnArgs {
     // Keys (query-row sharding): khat/vhat hold Lk keys as kgroups shards of kchunk rows,
     // [kgroups][B*H][kchunk][pad] (shard g = keys g*kchunk ..).  0 = unsharded (Lk = L).
     int Lk = 0, kchunk = 0;
+    int pass_ring[4] = {0, 0, 0, 0};  // two-pass kernel: forced ring (kb, kst, vkeys, vst), 0 = automatic
 };
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
 // inverse frame / norms) writing bf16 features.
@@ -149,6 +154,7 @@ struct AttnBwdArgs {
     // stores its dS tiles there and dQ becomes one batched GEMM dS^T . K_hat (which & 2).
     __nv_bfloat16* ds = nullptr;
     int ds_ld = 0;
+    int ring[4] = {0, 0, 0, 0};  // forced ring plan (nst1, nst2, nab, kb1), 0 = automatic
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both

@@ -65,23 +65,14 @@ void convert(D* dst, const S* src, std::size_t n) {
     });
 }
 
-// CTA-pair attention unless FIPA_ATTN_IMPL=1sm forces the single-CTA kernel.
-// Fused projection+pack unless FIPA_FUSED_PACK=0 (the unfused GEMM + pack path stays for the
-// fp32 path, unsupported shapes and A/B checks).
-bool fused_pack_enabled() {
-    const char* e = std::getenv("FIPA_FUSED_PACK");
-    return e == nullptr || std::string(e) != "0";
-}
-
 // Inference attention kernel: the CTA-pair kernel where its budget allows, the two-pass pair
-// kernel for wider lifted rows (rank 3-4), else the single-CTA kernel.  FIPA_ATTN_IMPL=1sm /
-// =pass force the alternatives (A/B checks).
+// kernel for wider lifted rows (rank 3-4), else the single-CTA kernel.  Tuning::attn forces an
+// alternative (A/B checks); the single-CTA kernel does not read sharded keys, so a sharded
+// forward never takes it.
 enum class AttnImpl { pair, pass, one_sm };
-AttnImpl attention_impl(const LayerDims& d) {
-    const char* e = std::getenv("FIPA_ATTN_IMPL");
-    const std::string v = e ? std::string(e) : std::string();
-    if (v == "1sm") return AttnImpl::one_sm;
-    if (v == "pass" && attn_fwd_pass_supported(d)) return AttnImpl::pass;
+AttnImpl attention_impl(const LayerDims& d, Tuning::Attn forced, bool sharded) {
+    if (forced == Tuning::Attn::one_sm && !sharded) return AttnImpl::one_sm;
+    if (forced == Tuning::Attn::pass && attn_fwd_pass_supported(d)) return AttnImpl::pass;
     if (attn_fwd_2sm_supported(d)) return AttnImpl::pair;
     if (attn_fwd_pass_supported(d)) return AttnImpl::pass;
     return AttnImpl::one_sm;
@@ -138,6 +129,22 @@ double softplus(double x) {  // proj/src/ipa.cpp:25-27
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ Tuning
+Tuning Tuning::from_env() {
+    Tuning t;
+    if (const char* e = std::getenv("FIPA_ATTN_IMPL")) {
+        const std::string v(e);
+        t.attn = v == "1sm" ? Attn::one_sm : v == "pass" ? Attn::pass : v == "pair" ? Attn::pair : Attn::automatic;
+    }
+    if (const char* e = std::getenv("FIPA_FUSED_PACK")) t.fused_pack = std::string(e) != "0";
+    if (const char* e = std::getenv("FIPA_BWD_DS")) t.bwd_ds = std::atoi(e) != 0 ? 1 : 0;
+    if (const char* e = std::getenv("FIPA_BWD_RING"))
+        std::sscanf(e, "%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3]);
+    if (const char* e = std::getenv("FIPA_PASS_RING"))
+        std::sscanf(e, "%d,%d,%d,%d", &t.pass_ring[0], &t.pass_ring[1], &t.pass_ring[2], &t.pass_ring[3]);
+    return t;
+}
 
 // ------------------------------------------------------------------ Config
 void Config::validate() const {
@@ -554,7 +561,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
         w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
-        if (materialize_ds(B, L, d.heads)) {
+        if (materialize_ds(B, L)) {
             w.ds_ld = static_cast<int>(round_up(static_cast<std::size_t>(L), 64));  // whole 64-column blocks
             w.ds = reinterpret_cast<__nv_bfloat16*>(take(BHL * w.ds_ld * 2));
         }
@@ -563,11 +570,10 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     return w;
 }
 
-bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L, int heads) {
-    const double bytes = double(B) * heads * double(L) * double((L + 63) / 64 * 64) * 2.0;
+bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L) const {
+    const double bytes = double(B) * dims_.heads * double(L) * double((L + 63) / 64 * 64) * 2.0;
     if (L > 2048 || bytes > double(1u << 30)) return false;
-    if (const char* e = std::getenv("FIPA_BWD_DS")) return std::atoi(e) != 0;
-    return true;
+    return tuning_.bwd_ds != 0;
 }
 
 std::size_t FlashIpaLayer::workspace_size(std::int64_t B, std::int64_t L) const {
@@ -598,7 +604,7 @@ int FlashIpaLayer::launches_per_backward() const {
 int FlashIpaLayer::launches_per_forward() const {
     if (cfg_.precision != Precision::bf16) return 5;
     // recenter, cast, [fused projection+pack | projection GEMM, pack], attention, output GEMM
-    return (proj_pack_supported(dims_) && fused_pack_enabled()) ? 5 : 6;
+    return (proj_pack_supported(dims_) && tuning_.fused_pack) ? 5 : 6;
 }
 
 void FlashIpaLayer::set_timing(bool on) {
@@ -665,7 +671,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         launch_recenter_with_sums(trans, shard->sums, ws.trans_c, int(B), int(L), stream);
     }
     mark(1);
-    if (do_pack && d_wheads_ != nullptr && fused_pack_enabled()) {
+    if (do_pack && d_wheads_ != nullptr && tuning_.fused_pack) {
         // fused projection GEMM + frame application + packing (proj_pack.cu)
         launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
         mark(2);
@@ -753,7 +759,8 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
             aa.Lk = int(L) * shard->groups;
             aa.kchunk = int(L);
         }
-        const AttnImpl impl = train ? AttnImpl::pair : attention_impl(d);
+        for (int i = 0; i < 4; ++i) aa.pass_ring[i] = tuning_.pass_ring[i];
+        const AttnImpl impl = train ? AttnImpl::pair : attention_impl(d, tuning_.attn, shard != nullptr);
         if (impl == AttnImpl::pair) {
             launch_attn_fwd_2sm(d, aa, stream);
         } else if (impl == AttnImpl::pass) {
@@ -817,6 +824,7 @@ void FlashIpaLayer::run_host(std::int64_t B, std::int64_t L, const double* s, co
                              const std::uint8_t* mask, double* out, bool dense) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
+    std::lock_guard<std::mutex> host_lock(host_mu_);  // one staging set per layer
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");
     const std::size_t BL = std::size_t(B) * L;
@@ -1081,6 +1089,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.acc_ld = kAccLd;
         a.B = int(B);
         a.L = int(L);
+        for (int i = 0; i < 4; ++i) a.ring[i] = tuning_.bwd_ring[i];
         if (shard != nullptr) {  // local queries against all G shards' keys; partial dK / dV
             a.khat = static_cast<const __nv_bfloat16*>(shard->k_all);
             a.vhat = static_cast<const __nv_bfloat16*>(shard->v_all);
@@ -1200,6 +1209,7 @@ void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, c
                               double* dz1, double* dz2, double* drot, double* dtrans, double* dweights) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
+    std::lock_guard<std::mutex> host_lock(host_mu_);  // one staging set per layer
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const std::size_t BL = std::size_t(B) * L;
     const std::size_t rdz = cfg_.rank * cfg_.d_z;

@@ -56,6 +56,20 @@ struct Config {
     LayerDims dims() const;
 };
 
+// Kernel-selection and tuning knobs.  Fixed per layer: set at creation (defaults = the measured
+// best choices; the FIPA_* environment variables below seed them ONCE, for A/B experiments) and
+// changed only through FlashIpaLayer::set_tuning -- the launch path never reads the environment.
+struct Tuning {
+    enum class Attn { automatic = 0, pair = 1, pass = 2, one_sm = 3 };
+    Attn attn = Attn::automatic;  // FIPA_ATTN_IMPL = pair | pass | 1sm (inference forward only)
+    bool fused_pack = true;       // FIPA_FUSED_PACK = 0: projection GEMM + separate pack kernel
+    int bwd_ds = -1;              // FIPA_BWD_DS: -1 automatic (L <= 2048 and dS <= 1 GiB), 0 off,
+                                  // 1 on (within the same cap)
+    int bwd_ring[4] = {0, 0, 0, 0};   // FIPA_BWD_RING  "nst1,nst2,nab,kb1" (0 = automatic)
+    int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
+    static Tuning from_env();
+};
+
 // Master weights in the reference layout, kept in float64 on the host.
 struct HostWeights {
     std::vector<double> w_q, w_k, w_v, w_qp, w_kp, w_vp, w_bias, gamma_raw, w_out, b_out;
@@ -159,8 +173,11 @@ public:
     std::size_t train_workspace_size(std::int64_t B, std::int64_t L) const;
     // Short-sequence backward: the dK/dV kernel also writes dS (bf16, B*H*L^2*2 bytes of the
     // training workspace) and dQ is one batched GEMM instead of a second attention pass.  Used
-    // for L <= 2048 and at most 1 GiB of dS; FIPA_BWD_DS=0 / 1 forces it off / on (within that cap).
-    static bool materialize_ds(std::int64_t B, std::int64_t L, int heads);
+    // for L <= 2048 and at most 1 GiB of dS; Tuning::bwd_ds = 0 / 1 forces it off / on (within that cap).
+    bool materialize_ds(std::int64_t B, std::int64_t L) const;
+    const Tuning& tuning() const { return tuning_; }
+    // Not thread-safe against concurrent calls on the same layer (like weight mutation).
+    void set_tuning(const Tuning& t) { tuning_ = t; }
     std::size_t num_weights() const;
     void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                   const float* rot, const float* trans, const std::uint8_t* mask, const float* dout,
@@ -259,6 +276,7 @@ private:
 
     Config cfg_;
     LayerDims dims_{};
+    Tuning tuning_ = Tuning::from_env();
     HostWeights w_;
     int device_ = 0;
     // device weights
@@ -274,7 +292,9 @@ private:
     float k_scale_ = 0.f;
     bool dirty_ = true;
     std::mutex upload_mu_;
-    // host-path staging (forward_host)
+    // host-path staging (forward_host / reference_host / grad_host), guarded by host_mu_: the
+    // host entry points release the GIL and may be called concurrently on one layer
+    std::mutex host_mu_;
     void* h_stage_ = nullptr;
     std::size_t h_stage_bytes_ = 0;
     void* d_stage_ = nullptr;

@@ -67,14 +67,22 @@ def pack(cfg: fo.IpaConfig, w, s, z1, z2, rot, trans_c, mask):
     return dict(q_hat=q_hat, k_hat=k_hat, v_hat=v_hat, proj=(q, k, v, qp, kp, vp), g=g[:, 0, 0])
 
 
+BLOCK = 512  # query rows per block: O(BLOCK * L) memory, BLAS matmuls (scales to L = 4096+)
+
+
 def attention(q_hat, k_hat, v_hat, L):
     """Forward in log2 units: P = 2^(S - m) / l; returns O_hat (normalised) and natural LSE."""
-    s2 = np.einsum("hid,hjd->hij", q_hat, k_hat)
-    m = s2.max(-1, keepdims=True)
-    p = np.exp2(s2 - m)
-    l = p.sum(-1, keepdims=True)
-    o = np.einsum("hij,hjd->hid", p / l, v_hat)
-    lse = (m + np.log2(l))[..., 0] * LN2
+    H = q_hat.shape[0]
+    o = np.empty((H, q_hat.shape[1], v_hat.shape[-1]))
+    lse = np.empty((H, q_hat.shape[1]))
+    for h in range(H):
+        for a in range(0, q_hat.shape[1], BLOCK):
+            s2 = q_hat[h, a:a + BLOCK] @ k_hat[h].T
+            m = s2.max(-1, keepdims=True)
+            p = np.exp2(s2 - m)
+            l = p.sum(-1, keepdims=True)
+            o[h, a:a + BLOCK] = (p / l) @ v_hat[h]
+            lse[h, a:a + BLOCK] = (m + np.log2(l))[..., 0] * LN2
     return o, lse
 
 
@@ -116,13 +124,18 @@ def prep(cfg, dfeat, o_hat, z1, rot, ep):
 
 def attention_backward(q_hat, k_hat, v_hat, lse, do_hat, D):
     """attn_bwd kernels: dS in natural-logit units; accumulators against the stored rows."""
-    s2 = np.einsum("hid,hjd->hij", q_hat, k_hat)
-    p = np.exp2(s2 - (lse / LN2)[..., None])
-    dp = np.einsum("hid,hjd->hij", do_hat, v_hat)
-    ds = p * (dp - D[..., None])
-    dv_acc = np.einsum("hij,hid->hjd", p, do_hat)
-    dq_acc = np.einsum("hij,hjd->hid", ds, k_hat)
-    dk_acc = np.einsum("hij,hid->hjd", ds, q_hat)
+    H, Lq = q_hat.shape[:2]
+    dq_acc = np.empty((H, Lq, k_hat.shape[-1]))
+    dk_acc = np.zeros((H, k_hat.shape[1], q_hat.shape[-1]))
+    dv_acc = np.zeros((H, v_hat.shape[1], do_hat.shape[-1]))
+    for h in range(H):
+        for a in range(0, Lq, BLOCK):
+            b = slice(a, a + BLOCK)
+            p = np.exp2(q_hat[h, b] @ k_hat[h].T - (lse[h, b] / LN2)[:, None])
+            ds = p * (do_hat[h, b] @ v_hat[h].T - D[h, b][:, None])
+            dv_acc[h] += p.T @ do_hat[h, b]
+            dq_acc[h, b] = ds @ k_hat[h]
+            dk_acc[h] += ds.T @ q_hat[h, b]
     return dq_acc, dk_acc, dv_acc
 
 

@@ -151,6 +151,34 @@ def oracle_backward(shape, w, batch, dout):
     return out
 
 
+def emulated_backward(shape, w, batch, dout):
+    """Oracle-equivalent forward output + gradients at large L: tests/bwd_emulation.py run with
+    EXACT_SPLIT (the lifted-row restatement of fipa_oracle.flash_ipa_backward, equal to it within
+    1e-14 -- tests/test_bwd_layout.py pins it on the CPU), query-blocked BLAS matmuls and O(L) memory
+    per block, so L = 4096 finishes in seconds where the dense oracle needs O(L^2 d_z) memory.
+    Returns (out [B,L,d_in], grads stacked like oracle_backward)."""
+    import bwd_emulation as be
+
+    cfg = oracle_cfg(shape)
+    prev = be.EXACT_SPLIT
+    be.EXACT_SPLIT = True
+    try:
+        outs, res = [], []
+        for b in range(batch["s"].shape[0]):
+            args = [batch[k][b] for k in ("s", "z1", "z2", "rot", "trans", "mask")]
+            g, inter = be.backward(cfg, w, *args, dout[b])
+            m = np.asarray(batch["mask"][b], bool)
+            out = inter["feat"] @ w["w_out"] + w["b_out"] if inter else np.zeros_like(batch["s"][b])
+            outs.append(np.where(m[:, None], out, 0.0))
+            res.append(g)
+    finally:
+        be.EXACT_SPLIT = prev
+    grads = {k: np.stack([r[k] for r in res]) for k in ("s", "z1", "z2", "rot", "trans")}
+    for n in fo.WEIGHT_NAMES:
+        grads[n] = sum(r[n] for r in res)
+    return np.stack(outs), grads
+
+
 def gpu_train_device(model, batch, dout):
     """forward_train + backward through the C ABI over torch-owned device buffers.
     Returns (out, grads, workspace, layouts)."""

@@ -33,3 +33,21 @@ def test_emulated_device_backward_matches_oracle(shape, L, scale, mask_frac, mon
     got, _ = be.backward(cfg, w, p.s, p.z1, p.z2, p.rot, p.trans, p.mask, dout)
     for n in ref:
         assert fo.rel_dev(ref[n], got[n]) < 2e-3, n
+
+
+def test_large_L_checker_matches_oracle():
+    """helpers.emulated_backward -- the checker the L >= 1024 GPU parity tests use (query-blocked,
+    O(L) memory) -- against the dense oracle forward and backward at the north-star shape."""
+    from helpers import MAIN, emulated_backward, make_batch, oracle_backward, oracle_forward
+
+    cfg = fo.IpaConfig(**MAIN, enforce_head_cap=False)
+    w = fo.init_weights(cfg, 1)
+    w["gamma_raw"] = np.linspace(-0.6, 0.9, cfg.heads)
+    batch = make_batch(MAIN, 2, 600, seed=3, mask_frac=0.1, bf16=True)  # > one 512-row block
+    batch["mask"][1, :] = False  # a fully masked sample
+    dout = np.random.default_rng(4).standard_normal((2, 600, cfg.d_in))
+    out, g = emulated_backward(MAIN, w, batch, dout)
+    assert fo.rel_dev(oracle_forward(MAIN, w, batch), out) < 1e-12
+    ref = oracle_backward(MAIN, w, batch, dout)
+    for n in ref:
+        assert fo.rel_dev(ref[n], g[n]) < 1e-10, n

@@ -28,8 +28,11 @@ def _model(fipa, shape, seed=0):
     return m
 
 
-def _check(fipa, shape, B, L, seed, mask_frac=0.0, scale=1.0, tol=BF16_TOL, tol_logit=None):
+def _check(fipa, shape, B, L, seed, mask_frac=0.0, scale=1.0, tol=BF16_TOL, tol_logit=None, bwd_ds=None,
+           samples=None):
     model = _model(fipa, shape, seed)
+    if bwd_ds is not None:
+        model.set_tuning(bwd_ds=bwd_ds)
     w = oracle_weights_for(model, "bf16")
     batch = make_batch(shape, B, L, seed=seed, translation_scale=scale, mask_frac=mask_frac, bf16=True)
     dout = np.random.default_rng(seed + 1).standard_normal((B, L, shape["d_in"]))
@@ -49,26 +52,25 @@ def test_backward_main_shape(fipa, L):
     _check(fipa, MAIN, 2, L, seed=10 + L, mask_frac=0.1)
 
 
-@pytest.mark.parametrize("ds", ["0", "1"])
-def test_backward_both_dq_paths(fipa, monkeypatch, ds):
-    """dQ by the streaming attention kernel (FIPA_BWD_DS=0) and by the batched GEMM over the
+@pytest.mark.parametrize("ds", [0, 1])
+def test_backward_both_dq_paths(fipa, ds):
+    """dQ by the streaming attention kernel (bwd_ds=0) and by the batched GEMM over the
     dS the dK/dV kernel materialises (=1, the default for L <= 2048) -- each against the oracle."""
-    monkeypatch.setenv("FIPA_BWD_DS", ds)
-    _check(fipa, MAIN, 2, 257, seed=31, mask_frac=0.1)
+    _check(fipa, MAIN, 2, 257, seed=31, mask_frac=0.1, bwd_ds=ds)
 
 
-def test_dq_paths_agree(fipa, monkeypatch):
+def test_dq_paths_agree(fipa):
     """Same dS values either way (same formula, same bf16 rounding); only the fp32 summation
     order of dQ differs, so the gradients agree far inside the oracle gate."""
     model = _model(fipa, MAIN, 13)
     batch = make_batch(MAIN, 2, 320, seed=13, mask_frac=0.1, bf16=True)
     dout = np.random.default_rng(13).standard_normal((2, 320, MAIN["d_in"]))
     got = {}
-    for ds in ("0", "1"):
-        monkeypatch.setenv("FIPA_BWD_DS", ds)
+    for ds in (0, 1):
+        model.set_tuning(bwd_ds=ds)
         _, got[ds], _, _ = gpu_train_device(model, batch, dout)
     for n in GRADS:
-        assert rel_dev(got["0"][n], got["1"][n]) < 1e-4, n
+        assert rel_dev(got[0][n], got[1][n]) < 1e-4, n
 
 
 def test_backward_tiny_shape(fipa):
@@ -108,15 +110,15 @@ def test_training_forward_matches_inference_forward(fipa):
     assert np.array_equal(out_inf, out_tr)
 
 
-@pytest.mark.parametrize("ds", ["0", "1"])
-def test_attention_backward_stage_parity(fipa, monkeypatch, ds):
+@pytest.mark.parametrize("ds", [0, 1])
+def test_attention_backward_stage_parity(fipa, ds):
     """dO_hat, D and the three attention accumulators against the layout emulation
     (tests/bwd_emulation.py) fed the device's own q/k/v_hat, O_hat and lse; dQ from both the
     streaming kernel and the materialised-dS GEMM."""
-    monkeypatch.setenv("FIPA_BWD_DS", ds)
     B, L = 1, 160
     shape = MAIN
     model = _model(fipa, shape, 8)
+    model.set_tuning(bwd_ds=ds)
     batch = make_batch(shape, B, L, seed=8, mask_frac=0.1, bf16=True)
     dout = np.random.default_rng(9).standard_normal((B, L, shape["d_in"]))
     _, _, ws, ((off, dims), (toff, tdims)) = gpu_train_device(model, batch, dout)
@@ -151,3 +153,52 @@ def test_flash_grad_host_api_matches_device(fipa):
     for n, m in (("s", "s"), ("z1", "z1"), ("rot", "rotations"), ("trans", "translations"), ("w_q", "w_q"),
                  ("gamma_raw", "gamma_raw"), ("w_out", "w_out")):
         assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
+
+
+def _check_large(fipa, B, L, seed, mask_frac, bwd_ds=None, oracle_samples=()):
+    """Large-L parity: forward output and all 15 gradients against the oracle-equivalent blocked
+    emulation (helpers.emulated_backward: EXACT_SPLIT lifted restatement of the oracle backward,
+    equal to it within 1e-14), plus the dense f64 oracle itself on `oracle_samples` (per-sample
+    input gradients; weight gradients are batch sums and come from the emulation)."""
+    from helpers import emulated_backward
+
+    model = _model(fipa, MAIN, seed)
+    if bwd_ds is not None:
+        model.set_tuning(bwd_ds=bwd_ds)
+    w = oracle_weights_for(model, "bf16")
+    batch = make_batch(MAIN, B, L, seed=seed, mask_frac=mask_frac, bf16=True)
+    dout = np.random.default_rng(seed + 1).standard_normal((B, L, MAIN["d_in"]))
+    out, g, _, _ = gpu_train_device(model, batch, dout)
+    ref_out, ref = emulated_backward(MAIN, w, batch, dout)
+    assert rel_dev(ref_out, out) < BF16_TOL
+    errs = {n: rel_dev(ref[n], g[n]) for n in GRADS}
+    bad = {n: e for n, e in errs.items() if not (np.isfinite(e) and e < BF16_TOL)}
+    assert not bad, f"gradients off: {bad} (all: {errs})"
+    for b in oracle_samples:
+        one = {k: batch[k][b:b + 1] for k in batch}
+        ro = oracle_backward(MAIN, w, one, dout[b:b + 1])
+        for n in ("s", "z1", "z2", "rot", "trans"):
+            assert rel_dev(ro[n][0], g[n][b]) < BF16_TOL, (b, n)
+            assert rel_dev(ro[n][0], ref[n][b]) < 1e-10, (b, n)  # the emulation is the oracle
+    return errs
+
+
+def test_backward_bench_config(fipa):
+    """Exactly the benched workload (bench.py default, BASELINE cfg2): B=8, L=1024, 10% masked
+    residues, fwd+bwd through the materialised-dS path (its default at L <= 2048): ~7 waves of
+    4-CTA clusters.  All 15 gradients; the dense oracle on samples 0 and 5."""
+    _check_large(fipa, 8, 1024, seed=1234, mask_frac=0.1, oracle_samples=(0, 5))
+
+
+@pytest.mark.parametrize("ds", [0, 1])
+def test_backward_L2048(fipa, ds):
+    """L = 2048, the largest materialised-dS length, and the streaming dQ kernel at the same size."""
+    _check_large(fipa, 1, 2048, seed=2048, mask_frac=0.1, bwd_ds=ds)
+
+
+def test_backward_L4096_streaming_dq(fipa):
+    """L = 4096: beyond the materialised-dS cap, so the streaming dQ attention kernel runs (the
+    path every L > 2048 and all sharded training takes)."""
+    model = _model(fipa, MAIN, 0)
+    assert model.tuning()["bwd_ds"] == -1
+    _check_large(fipa, 1, 4096, seed=4096, mask_frac=0.05)

@@ -169,12 +169,13 @@ def test_reference_model_defaults_roundtrip(fipa, tmp_path):
     assert np.array_equal(other.flash(*args), got)
 
 
-@pytest.mark.parametrize("impl", ["1sm", "2sm", "pass"])
-def test_attention_kernels_agree(fipa, impl, monkeypatch):
+@pytest.mark.parametrize("impl", ["1sm", "pair", "pass"])
+def test_attention_kernels_agree(fipa, impl):
     """The tcgen05 attention kernels (single CTA, CTA pair, two-pass CTA pair) against the oracle at the
-    north-star shape, ragged L with masked keys (FIPA_ATTN_IMPL selects the kernel)."""
-    monkeypatch.setenv("FIPA_ATTN_IMPL", impl)
+    north-star shape, ragged L with masked keys (Model.set_tuning(attn_impl=...) selects the kernel)."""
     model = _model(fipa, MAIN, "bf16", seed=21)
+    model.set_tuning(attn_impl=impl)
+    assert model.tuning()["attn_impl"] == impl
     w = oracle_weights_for(model, "bf16")
     batch = make_batch(MAIN, 2, 389, seed=4242, mask_frac=0.15, bf16=True)
     got = model.flash(batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"], mask=batch["mask"])
@@ -235,3 +236,16 @@ def test_wide_rank_se3_invariance(fipa, rank):
     moved = move_frames(batch, g_rot, g_t)
     got2 = model.flash(moved["s"], moved["z1"], moved["z2"], moved["rot"], moved["trans"])
     assert rel_dev(got, got2) < BF16_TOL
+
+
+def test_forward_bench_config_all_rows(fipa):
+    """Inference forward at the benched workload (B=8, L=1024: ~3.5 waves of CTA pairs), every row
+    of every sample against the oracle-equivalent blocked checker (helpers.emulated_backward)."""
+    from helpers import emulated_backward
+
+    model = _model(fipa, MAIN, "bf16", seed=23)
+    w = oracle_weights_for(model, "bf16")
+    batch = make_batch(MAIN, 8, 1024, seed=99, mask_frac=0.1, bf16=True)
+    got, _, _ = gpu_forward_device(model, batch)
+    ref, _ = emulated_backward(MAIN, w, batch, np.zeros((8, 1024, MAIN["d_in"])))
+    assert rel_dev(ref, got) < BF16_TOL

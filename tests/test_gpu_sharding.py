@@ -92,14 +92,17 @@ def test_nccl_world1_sharded_forward_equals_forward(fipa):
     assert rel_dev(ref_gpu, out.cpu().numpy().astype(np.float64)) < 1e-3
 
 
-def test_emulated_sharded_training_matches_unsharded(fipa):
+@pytest.mark.parametrize("n", [256, 1024])
+def test_emulated_sharded_training_matches_unsharded(fipa, n):
     """Query-row-sharded training step for G=2 ranks emulated on one GPU through the
     collective-agnostic C-ABI blocks: all-reduce of centroid sums, all-gather of packed keys,
     reduce-scatter of the partial key gradients, all-reduce of the translation-gradient sums and of
-    the weight gradients.  Output and every gradient must match the unsharded training step."""
-    from helpers import gpu_train_device
+    the weight gradients.  Output and every gradient must match the unsharded training step (which
+    at L = 2048 takes the materialised-dS path, while the shards run the streaming dQ kernel), and
+    at L_local = 1024 the oracle-equivalent checker as well."""
+    from helpers import emulated_backward, gpu_train_device
 
-    G, B, n = 2, 1, 256
+    G, B = 2, 1
     L = G * n
     model = fipa.Model(**MAIN, precision="bf16", seed=12, enforce_head_cap=False)
     batch = make_batch(MAIN, B, L, seed=57, mask_frac=0.1, bf16=True)
@@ -180,6 +183,16 @@ def test_emulated_sharded_training_matches_unsharded(fipa):
     dw = sum(sh["dw"] for sh in ranks).cpu().numpy().astype(np.float64)  # all-reduce
     ref_w = np.concatenate([ref_g[nm].ravel() for nm in fo.WEIGHT_NAMES])
     assert rel_dev(ref_w, dw) < 5e-3
+    if n >= 1024:
+        eo, eg = emulated_backward(MAIN, oracle_weights_for(model, "bf16"), batch, dout)
+        assert rel_dev(eo, out) < BF16_TOL
+        for k, name in (("ds", "s"), ("dz1", "z1"), ("dz2", "z2"), ("drot", "rot"), ("dtrans", "trans")):
+            assert rel_dev(eg[name], cat(k).reshape(eg[name].shape)) < BF16_TOL, k
+        o = 0
+        for nm in fo.WEIGHT_NAMES:
+            size = eg[nm].size
+            assert rel_dev(eg[nm].ravel(), dw[o:o + size]) < BF16_TOL, nm
+            o += size
 
 
 def test_nccl_world1_sharded_training_equals_training(fipa):
