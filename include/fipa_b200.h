@@ -100,6 +100,13 @@ int fipa_layer_forward(fipa_layer* layer, int64_t B, int64_t L, const float* s, 
                        const float* z2, const float* rot, const float* trans, const uint8_t* mask,
                        float* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The reference's `fully_masked` output of flash_ipa_forward (include/fipa/flash_ipa.hpp:53-57,
+ * src/flash_ipa.cpp:156-158): flags [B,L] uint8 (device), 1 on every row of a sample that has no
+ * valid residue (mask NULL = all valid: all flags 0).  Enqueued on `stream`. */
+int fipa_fully_masked(int64_t B, int64_t L, const uint8_t* mask, uint8_t* flags, void* stream);
+/* Same over host buffers (synchronous, current device). */
+int fipa_fully_masked_host(int64_t B, int64_t L, const uint8_t* mask, uint8_t* flags);
+
 /* Same forward over HOST float64 buffers (the reference / Python calling convention): copies in,
  * runs on an internal stream, copies out, synchronises. */
 int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L, const double* s,
@@ -287,6 +294,11 @@ int fipa_trunk_forward_launches(const fipa_trunk* trunk);
  * precision FIPA_PREC_BF16 uses the tcgen05 GEMM, otherwise fp32. */
 int fipa_knn_distogram(int64_t B, int64_t L, const float* trans, uint64_t k, uint64_t n_bins, double d_min,
                        double d_max, uint64_t pe_dim, float* out, void* stream);
+/* Same over float64 device buffers: the translations are never rounded, so the neighbour choice
+ * and bins are bit-exact with the reference's float64 path (pair_features.cpp:29-45);
+ * fipa_knn_distogram_host runs this variant. */
+int fipa_knn_distogram_f64(int64_t B, int64_t L, const double* trans, uint64_t k, uint64_t n_bins, double d_min,
+                           double d_max, uint64_t pe_dim, double* out, void* stream);
 int fipa_knn_distogram_host(int64_t B, int64_t L, const double* trans, uint64_t k, uint64_t n_bins, double d_min,
                             double d_max, uint64_t pe_dim, double* out);
 size_t fipa_build_factors_workspace_size(int64_t rows, uint64_t f, uint64_t n);

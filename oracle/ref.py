@@ -173,3 +173,52 @@ def build_factors(features, r, d_z, w1, w2):
     _check(lib().ref_build_factors(ctypes.c_uint64(L), ctypes.c_uint64(f), _dp(features), ctypes.c_uint64(r),
                                    ctypes.c_uint64(d_z), _dp(w1), _dp(w2), _dp(z1), _dp(z2)))
     return z1, z2
+
+
+# ------------------------------------------------------------ report / fit schema (f4)
+def fit_polynomial(points):
+    """bench.cpp:103-149 -> (a, b, r^2); NumericError -> ArithmeticError."""
+    L = np.ascontiguousarray([p[0] for p in points], dtype=np.float64)
+    y = np.ascontiguousarray([p[1] for p in points], dtype=np.float64)
+    out = np.zeros(3)
+    _check(lib().ref_fit_polynomial(ctypes.c_uint64(len(L)), _dp(L), _dp(y), _dp(out)))
+    return float(out[0]), float(out[1]), float(out[2])
+
+
+def _text(call):
+    need = ctypes.c_uint64(0)
+    _check(call(None, ctypes.c_uint64(0), ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value + 1)
+    _check(call(buf, ctypes.c_uint64(need.value + 1), ctypes.byref(need)))
+    return buf.value.decode()
+
+
+def report_text(report, fmt):
+    """report_to_csv / report_to_json (model_io.cpp:200-243) of a report.RunReport-shaped object."""
+    U, P, Dp, Ip, S = ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), _D, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p
+    lib().ref_report_text.argtypes = [ctypes.c_int, S, S, U, S, P, P, Ip, P, Dp, U, S, S, Dp, U, S, Dp, Ip, U, S,
+                                      ctypes.c_char_p, U, P]
+    recs, fits, checks = report.records, report.fits, report.checks
+    u64 = lambda xs: (ctypes.c_uint64 * max(1, len(xs)))(*xs)  # noqa: E731
+    dbl = lambda xs: (ctypes.c_double * max(1, len(xs)))(*xs)  # noqa: E731
+    i32 = lambda xs: (ctypes.c_int * max(1, len(xs)))(*xs)  # noqa: E731
+    j = lambda xs: "\n".join(xs).encode()  # noqa: E731
+    args = (ctypes.c_int(0 if fmt == "csv" else 1), report.command.encode(), report.config_echo.encode(),
+            ctypes.c_uint64(len(recs)), j([r.arm for r in recs]), u64([r.length for r in recs]),
+            u64([r.seed for r in recs]), i32([0 if r.precision == "f32" else 1 for r in recs]),
+            u64([r.peak_bytes for r in recs]), dbl([r.seconds for r in recs]), ctypes.c_uint64(len(fits)),
+            j([f.arm for f in fits]), j([f.metric for f in fits]),
+            dbl([v for f in fits for v in (f.quadratic, f.linear, f.r_squared)]), ctypes.c_uint64(len(checks)),
+            j([c.name for c in checks]), dbl([v for c in checks for v in (c.value, c.tolerance)]),
+            i32([1 if c.passed else 0 for c in checks]), ctypes.c_uint64(len(report.notes)), j(report.notes))
+    return _text(lambda b, cap, need: lib().ref_report_text(*args, b, cap, need))
+
+
+def parse_records_csv_text(path):
+    """parse_records_csv (model_io.cpp:260-306), returned re-serialised by report_to_csv."""
+    return _text(lambda b, cap, need: lib().ref_parse_records_csv(str(path).encode(), b, cap, need))
+
+
+def config_json(path=""):
+    """config_to_json(load_config(path)) (model_io.cpp:308-405)."""
+    return _text(lambda b, cap, need: lib().ref_config_json(str(path).encode(), b, cap, need))

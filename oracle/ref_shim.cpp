@@ -16,17 +16,22 @@
 //   gaussian / Rng              proj/src/tensor.cpp:286-290, proj/src/rng.cpp:11-41
 //   knn_distogram / positional_encoding / build_factors
 //                               proj/src/pair_features.cpp:10-97
+//   fit_polynomial              proj/src/bench.cpp:103-149
+//   report_to_csv / report_to_json / parse_records_csv / load_config + config_to_json
+//                               proj/src/model_io.cpp:198-405
 //
 // Status codes mirror the product C-ABI: 0 ok, 1 ValueError, 2 NumericError,
 // 3 IoError, 9 other.
 
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <string>
 #include <vector>
 
 #include "fipa/attention_kernel.hpp"
+#include "fipa/bench.hpp"
 #include "fipa/error.hpp"
 #include "fipa/flash_ipa.hpp"
 #include "fipa/geometry.hpp"
@@ -304,6 +309,107 @@ int ref_build_factors(std::uint64_t L, std::uint64_t f, const double* feat, std:
         to_ptr(fp.z1, z1);
         to_ptr(fp.z2, z2);
     });
+}
+
+// ---------------------------------------------------------------- report / fit schema (f4)
+// Strings cross as '\n'-joined lists; text results are copied into buf (cap bytes, NUL-terminated)
+// and *need receives the full length.
+
+// y = a L^2 + b L least squares (bench.cpp:103-149): out = {a, b, r^2}
+int ref_fit_polynomial(std::uint64_t n, const double* L, const double* y, double* out) {
+    return guarded([&] {
+        std::vector<std::pair<double, double>> pts;
+        for (std::uint64_t i = 0; i < n; ++i) pts.emplace_back(L[i], y[i]);
+        const FitCoefficients f = fit_polynomial(pts);
+        out[0] = f.quadratic;
+        out[1] = f.linear;
+        out[2] = f.r_squared;
+    });
+}
+
+namespace {
+std::vector<std::string> split_lines(const char* s, std::uint64_t n) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (const char* p = s ? s : ""; *p; ++p) {
+        if (*p == '\n') {
+            out.push_back(cur);
+            cur.clear();
+        } else {
+            cur.push_back(*p);
+        }
+    }
+    if (!cur.empty() || out.size() < n) out.push_back(cur);
+    out.resize(n);
+    return out;
+}
+
+void put_text(const std::string& t, char* buf, std::uint64_t cap, std::uint64_t* need) {
+    *need = t.size();
+    if (buf != nullptr && cap > 0) {
+        const std::size_t m = std::min<std::size_t>(t.size(), cap - 1);
+        std::memcpy(buf, t.data(), m);
+        buf[m] = '\0';
+    }
+}
+
+// records: arms '\n'-joined; prec 0 = f32, 1 = f64
+RunReport make_report(const char* command, const char* config_echo, std::uint64_t n, const char* arms,
+                      const std::uint64_t* lengths, const std::uint64_t* seeds, const int* prec,
+                      const std::uint64_t* peak, const double* secs, std::uint64_t nf, const char* fit_arms,
+                      const char* fit_metrics, const double* fit_vals, std::uint64_t nc, const char* check_names,
+                      const double* check_vals, const int* check_pass, std::uint64_t nn, const char* notes) {
+    RunReport r;
+    r.command = command ? command : "";
+    r.config_echo = config_echo ? config_echo : "";
+    const auto a = split_lines(arms, n);
+    for (std::uint64_t i = 0; i < n; ++i) {
+        RunRecord rec;
+        rec.arm = a[i];
+        rec.length = lengths[i];
+        rec.seed = seeds[i];
+        rec.precision = prec[i] == 0 ? Precision::f32 : Precision::f64;
+        rec.peak_bytes = peak[i];
+        rec.seconds = secs[i];
+        r.records.push_back(rec);
+    }
+    const auto fa = split_lines(fit_arms, nf), fm = split_lines(fit_metrics, nf);
+    for (std::uint64_t i = 0; i < nf; ++i)
+        r.fits.push_back(FitSummary{fa[i], fm[i], fit_vals[3 * i], fit_vals[3 * i + 1], fit_vals[3 * i + 2]});
+    const auto cn = split_lines(check_names, nc);
+    for (std::uint64_t i = 0; i < nc; ++i)
+        r.checks.push_back(CheckOutcome{cn[i], check_vals[2 * i], check_vals[2 * i + 1], check_pass[i] != 0});
+    r.notes = split_lines(notes, nn);
+    return r;
+}
+}  // namespace
+
+// format 0 = csv, 1 = json (model_io.cpp:200-243)
+int ref_report_text(int format, const char* command, const char* config_echo, std::uint64_t n, const char* arms,
+                    const std::uint64_t* lengths, const std::uint64_t* seeds, const int* prec,
+                    const std::uint64_t* peak, const double* secs, std::uint64_t nf, const char* fit_arms,
+                    const char* fit_metrics, const double* fit_vals, std::uint64_t nc, const char* check_names,
+                    const double* check_vals, const int* check_pass, std::uint64_t nn, const char* notes, char* buf,
+                    std::uint64_t cap, std::uint64_t* need) {
+    return guarded([&] {
+        const RunReport r = make_report(command, config_echo, n, arms, lengths, seeds, prec, peak, secs, nf, fit_arms,
+                                        fit_metrics, fit_vals, nc, check_names, check_vals, check_pass, nn, notes);
+        put_text(format == 0 ? report_to_csv(r) : report_to_json(r), buf, cap, need);
+    });
+}
+
+// parse_records_csv (model_io.cpp:260-306) re-serialised as its CSV (records only)
+int ref_parse_records_csv(const char* path, char* buf, std::uint64_t cap, std::uint64_t* need) {
+    return guarded([&] {
+        RunReport r;
+        r.records = parse_records_csv(path);
+        put_text(report_to_csv(r), buf, cap, need);
+    });
+}
+
+// config_to_json(load_config(path)) (model_io.cpp:308-405); path "" = defaults
+int ref_config_json(const char* path, char* buf, std::uint64_t cap, std::uint64_t* need) {
+    return guarded([&] { put_text(config_to_json(load_config(path ? path : "")), buf, cap, need); });
 }
 
 }  // extern "C"

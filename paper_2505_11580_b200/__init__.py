@@ -32,7 +32,7 @@ except ImportError:
 
 try:
     from ._fipa_b200 import (Comm, Model, Trunk, build_factors, comm_unique_id,  # noqa: F401  (native, in-tree)
-                             flash_attention, knn_distogram, naive_attention)
+                             flash_attention, fully_masked, knn_distogram, naive_attention)
 except ImportError as exc:  # fail loudly: the product has no Python fallback
     raise ImportError(
         "paper_2505_11580_b200 native extension is not built; run "
@@ -41,5 +41,5 @@ except ImportError as exc:  # fail loudly: the product has no Python fallback
 
 LIB_PATH = os.path.join(_HERE, "libfipa_b200.so")
 
-__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "knn_distogram", "build_factors", "flash_attention",
+__all__ = ["Model", "Trunk", "Comm", "comm_unique_id", "fully_masked", "knn_distogram", "build_factors", "flash_attention",
            "naive_attention", "LIB_PATH"]

@@ -633,6 +633,26 @@ private:
     std::string precision_name_;
 };
 
+// fully_masked(mask [L] or [B, L]) -> bool array of the same shape: the reference's
+// flash_ipa_forward `fully_masked` output (proj/src/flash_ipa.cpp:156-158), on the GPU.
+py::array_t<bool> fully_masked(const py::object& mask_obj) {
+    py::array_t<uint8_t, py::array::c_style | py::array::forcecast> mask(mask_obj);
+    if (mask.ndim() != 1 && mask.ndim() != 2) throw FipaValueError("mask must be [L] or [B, L]");
+    const int64_t B = mask.ndim() == 2 ? mask.shape(0) : 1;
+    const int64_t L = mask.shape(mask.ndim() - 1);
+    std::vector<uint8_t> flags(size_t(B) * size_t(L));
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = fipa_fully_masked_host(B, L, mask.data(), flags.data());
+    }
+    check(rc);
+    py::array_t<bool> out(std::vector<py::ssize_t>(mask.shape(), mask.shape() + mask.ndim()));
+    bool* o = out.mutable_data();
+    for (size_t e = 0; e < flags.size(); ++e) o[e] = flags[e] != 0;
+    return out;
+}
+
 // knn_distogram(translations, k=20, n_bins=22, d_min=2.0, d_max=22.0, pe_dim=16) -> [.., L, k, n_bins+pe_dim]
 py::array_t<double> knn_distogram(const DArr& trans, uint64_t k, uint64_t n_bins, double d_min, double d_max,
                                   uint64_t pe_dim) {
@@ -681,6 +701,9 @@ PYBIND11_MODULE(_fipa_b200, m) {
     py::register_exception<FipaIoError>(m, "FipaIoError", PyExc_IOError);
     py::register_exception<FipaCudaError>(m, "FipaCudaError", PyExc_RuntimeError);
     py::register_exception<FipaCommError>(m, "FipaCommError", PyExc_RuntimeError);
+    m.def("fully_masked", &fully_masked, py::arg("mask"),
+          "Per-row flags of the reference flash_ipa_forward `fully_masked` output (rows of a sample with no valid "
+          "residue), on the GPU");
     m.def("knn_distogram", &knn_distogram, py::arg("translations"), py::arg("k") = 20, py::arg("n_bins") = 22,
           py::arg("d_min") = 2.0, py::arg("d_max") = 22.0, py::arg("pe_dim") = 16,
           "k-NN distogram + offset encoding of each residue (reference knn_distogram), on the GPU");

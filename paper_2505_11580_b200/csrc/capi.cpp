@@ -200,6 +200,32 @@ int fipa_layer_forward(fipa_layer* layer, int64_t B, int64_t L_, const float* s,
     });
 }
 
+int fipa_fully_masked(int64_t B, int64_t L_, const uint8_t* mask, uint8_t* flags, void* stream) {
+    return guarded([&] {
+        if (B < 1 || L_ < 1) throw fipa_b200::ValueError("empty frame set");
+        if (flags == nullptr) throw fipa_b200::ValueError("null flags buffer");
+        fipa_b200::launch_fully_masked(mask, flags, int(B), int(L_), static_cast<cudaStream_t>(stream));
+        fipa_b200::cuda_check(cudaGetLastError(), "fully_masked launch");
+    });
+}
+
+int fipa_fully_masked_host(int64_t B, int64_t L_, const uint8_t* mask, uint8_t* flags) {
+    return guarded([&] {
+        if (B < 1 || L_ < 1) throw fipa_b200::ValueError("empty frame set");
+        if (flags == nullptr) throw fipa_b200::ValueError("null flags buffer");
+        const size_t n = size_t(B) * size_t(L_);
+        uint8_t* d = nullptr;
+        fipa_b200::cuda_check(cudaMalloc(&d, 2 * n), "cudaMalloc");
+        struct Free {
+            uint8_t* p;
+            ~Free() { cudaFree(p); }
+        } guard{d};
+        if (mask) fipa_b200::cuda_check(cudaMemcpy(d, mask, n, cudaMemcpyHostToDevice), "H2D");
+        fipa_b200::launch_fully_masked(mask ? d : nullptr, d + n, int(B), int(L_), nullptr);
+        fipa_b200::cuda_check(cudaMemcpy(flags, d + n, n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
 int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L_, const double* s,
                             const double* z1, const double* z2, const double* rot,
                             const double* trans, const uint8_t* mask, double* out) {
@@ -697,6 +723,14 @@ extern "C" {
 
 int fipa_knn_distogram(int64_t B, int64_t L_, const float* trans, uint64_t k, uint64_t n_bins, double d_min,
                        double d_max, uint64_t pe_dim, float* out, void* stream) {
+    return guarded([&] {
+        fipa_b200::knn_distogram(B, L_, trans, knn_spec(k, n_bins, d_min, d_max, pe_dim), out,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fipa_knn_distogram_f64(int64_t B, int64_t L_, const double* trans, uint64_t k, uint64_t n_bins, double d_min,
+                           double d_max, uint64_t pe_dim, double* out, void* stream) {
     return guarded([&] {
         fipa_b200::knn_distogram(B, L_, trans, knn_spec(k, n_bins, d_min, d_max, pe_dim), out,
                                  static_cast<cudaStream_t>(stream));

@@ -226,6 +226,9 @@ size_t knn_smem_bytes(const KnnSpec& spec);
 // trans [B, L, 3] -> out [B, L, k, n_bins + pe_dim]; d_freq [pe_dim/2] = 10000^(-2p/pe_dim)
 void launch_knn_distogram(const float* trans, int B, int L, const KnnSpec& spec, const double* d_freq, float* out,
                           cudaStream_t stream);
+// float64 translations and features end to end (the reference's f64 API: no rounding before the distance)
+void launch_knn_distogram(const double* trans, int B, int L, const KnnSpec& spec, const double* d_freq, double* out,
+                          cudaStream_t stream);
 // w [K, N] fp32 row-major -> wt [N, ld] bf16 (K-major B operand), pad columns zeroed
 void launch_transpose_to_bf16(const float* w, int K, int N, __nv_bfloat16* wt, int ld, cudaStream_t stream);
 
@@ -243,6 +246,8 @@ void launch_centroid_sums(const float* trans, const uint8_t* mask, float* sums, 
 // out = trans - sum/count per sample; rows with zero_masked[row] == 0 are written as 0 when given.
 void launch_recenter_with_sums(const float* trans, const float* sums, float* out, int B, int L, cudaStream_t stream,
                                const uint8_t* zero_masked = nullptr);
+// flags[b, i] = 1 for every row of a sample without a valid residue (flash_ipa.cpp:156-158)
+void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cudaStream_t stream);
 // Subtract each sample's translation centroid (exact: the layer is invariant to it).
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream);

@@ -519,6 +519,16 @@ __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat1
 }
 
 // One block per sample: subtract the centroid of the valid residues' translations.
+// fully_masked flags (proj/src/flash_ipa.cpp:156-158): every row of a sample without a valid
+// residue is flagged (its output is all zeros); one block per sample.
+__global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* __restrict__ flags, int L) {
+    const int b = blockIdx.x;
+    int any = 0;
+    for (int i = threadIdx.x; i < L && !any; i += blockDim.x) any = mask == nullptr || mask[int64_t(b) * L + i] != 0;
+    any = __syncthreads_or(any);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) flags[int64_t(b) * L + i] = any ? 0 : 1;
+}
+
 __global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
                                 float* __restrict__ out, int L) {
     __shared__ float red[4][32];
@@ -707,6 +717,10 @@ void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, in
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
     f32_to_bf16_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, rows, cols, ld_out);
+}
+
+void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cudaStream_t stream) {
+    fully_masked_kernel<<<B, 256, 0, stream>>>(mask, flags, L);
 }
 
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,

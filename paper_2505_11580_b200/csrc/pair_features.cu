@@ -3,8 +3,9 @@
 //   knn_distogram        proj/src/pair_features.cpp:10-64
 //   positional_encoding  proj/src/pair_features.cpp:66-81
 //   build_factors        proj/src/pair_features.cpp:83-97 (two linears; tcgen05 GEMM here)
-// Neighbour selection is integer work and must match the reference exactly: distances are formed
-// in float64 with the reference's operation order (no FMA contraction: __dmul_rn/__dadd_rn, a
+// Neighbour selection is integer work and must match the reference exactly: translations stay in
+// the caller's precision (float64 for the reference's f64 API: no rounding before the distance),
+// distances are formed in float64 with the reference's operation order (no FMA contraction: __dmul_rn/__dadd_rn, a
 // correctly rounded sqrt), ordered lexicographically by (distance, index) -- the reference's
 // partial_sort of (distance, index) pairs gives the lower-index tie-break.  One warp per residue:
 // each lane keeps a sorted top-k of its strided candidates in shared memory, then k rounds of a
@@ -28,9 +29,10 @@ __device__ __forceinline__ bool lex_less(double da, int ia, double db, int ib) {
     return da < db || (da == db && ia < ib);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) knn_distogram_kernel(const float* __restrict__ trans, int B, int L,
+template <class T, class O>
+__global__ void __launch_bounds__(kWarps * 32) knn_distogram_kernel(const T* __restrict__ trans, int B, int L,
                                                                     KnnSpec spec, const double* __restrict__ freq,
-                                                                    float* __restrict__ out) {
+                                                                    O* __restrict__ out) {
     extern __shared__ __align__(8) unsigned char smraw[];
     const int k = spec.k;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(kWarps * 32) knn_distogram_kernel(const float*
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
     if (row >= static_cast<int64_t>(B) * L) return;
     const int b = static_cast<int>(row / L), i = static_cast<int>(row % L);
-    const float* t = trans + static_cast<int64_t>(b) * L * 3;
+    const T* t = trans + static_cast<int64_t>(b) * L * 3;
     const double xi = t[i * 3], yi = t[i * 3 + 1], zi = t[i * 3 + 2];
 
     // lane-local sorted top-k of candidates j = lane, lane + 32, ...
@@ -63,8 +65,8 @@ __global__ void __launch_bounds__(kWarps * 32) knn_distogram_kernel(const float*
     }
     // k rounds of warp arg-min over the lane heads
     const int width = spec.n_bins + spec.pe_dim;
-    float* orow = out + row * static_cast<int64_t>(k) * width;
-    for (int e = lane; e < k * width; e += 32) orow[e] = 0.f;
+    O* orow = out + row * static_cast<int64_t>(k) * width;
+    for (int e = lane; e < k * width; e += 32) orow[e] = O(0);
     __syncwarp();
     const double bin_width = (spec.d_max - spec.d_min) / static_cast<double>(spec.n_bins);
     int head = 0;
@@ -90,14 +92,14 @@ __global__ void __launch_bounds__(kWarps * 32) knn_distogram_kernel(const float*
             rel = rel > 0.0 ? rel : 0.0;
             const double last = static_cast<double>(spec.n_bins - 1);
             const int bin = rel >= last ? spec.n_bins - 1 : static_cast<int>(rel);
-            orow[n * width + bin] = 1.f;
+            orow[n * width + bin] = O(1);
         }
         const double x = static_cast<double>(bi - i);
         for (int p = lane; p < spec.pe_dim / 2; p += 32) {
             double sv, cv;
             sincos(x * freq[p], &sv, &cv);
-            orow[n * width + spec.n_bins + 2 * p] = static_cast<float>(sv);
-            orow[n * width + spec.n_bins + 2 * p + 1] = static_cast<float>(cv);
+            orow[n * width + spec.n_bins + 2 * p] = static_cast<O>(sv);
+            orow[n * width + spec.n_bins + 2 * p + 1] = static_cast<O>(cv);
         }
     }
 }
@@ -119,15 +121,26 @@ void launch_transpose_to_bf16(const float* w, int K, int N, __nv_bfloat16* wt, i
 
 size_t knn_smem_bytes(const KnnSpec& spec) { return size_t(kWarps) * 32 * spec.k * (sizeof(double) + sizeof(int)); }
 
-void launch_knn_distogram(const float* trans, int B, int L, const KnnSpec& spec, const double* d_freq, float* out,
-                          cudaStream_t stream) {
+template <class T, class O>
+void launch_knn_impl(const T* trans, int B, int L, const KnnSpec& spec, const double* d_freq, O* out,
+                     cudaStream_t stream) {
     const size_t smem = knn_smem_bytes(spec);
     if (smem > 200 * 1024) throw std::invalid_argument("knn_distogram: k too large for the GPU kernel");
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(knn_distogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    auto kern = knn_distogram_kernel<T, O>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int64_t rows = int64_t(B) * L;
-    knn_distogram_kernel<<<static_cast<unsigned>((rows + kWarps - 1) / kWarps), kWarps * 32, smem, stream>>>(
-        trans, B, L, spec, d_freq, out);
+    kern<<<static_cast<unsigned>((rows + kWarps - 1) / kWarps), kWarps * 32, smem, stream>>>(trans, B, L, spec,
+                                                                                            d_freq, out);
+}
+
+void launch_knn_distogram(const float* trans, int B, int L, const KnnSpec& spec, const double* d_freq, float* out,
+                          cudaStream_t stream) {
+    launch_knn_impl(trans, B, L, spec, d_freq, out, stream);
+}
+
+void launch_knn_distogram(const double* trans, int B, int L, const KnnSpec& spec, const double* d_freq, double* out,
+                          cudaStream_t stream) {
+    launch_knn_impl(trans, B, L, spec, d_freq, out, stream);
 }
 
 }  // namespace fipa_b200

@@ -23,10 +23,13 @@ void validate_knn(std::int64_t B, std::int64_t L, const KnnSpec& s) {
     if (s.pe_dim % 2 != 0 || s.pe_dim < 0) throw ValueError("positional encoding width must be even");
 }
 
-void knn_distogram(std::int64_t B, std::int64_t L, const float* trans, const KnnSpec& spec, float* out,
-                   cudaStream_t stream) {
+namespace {
+template <class T, class O>
+void knn_distogram_impl(std::int64_t B, std::int64_t L, const T* trans, const KnnSpec& spec, O* out,
+                        cudaStream_t stream) {
     validate_knn(B, L, spec);
     if (trans == nullptr || out == nullptr) throw ValueError("null pointer");
+    // frequencies as the reference forms them (std::pow on the host, pair_features.cpp:73-75)
     std::vector<double> freq(std::max(1, spec.pe_dim / 2));
     for (int p = 0; p < spec.pe_dim / 2; ++p)
         freq[p] = std::pow(10000.0, -static_cast<double>(2 * p) / static_cast<double>(spec.pe_dim));
@@ -36,6 +39,17 @@ void knn_distogram(std::int64_t B, std::int64_t L, const float* trans, const Knn
     launch_knn_distogram(trans, int(B), int(L), spec, d_freq, out, stream);
     cuda_check(cudaGetLastError(), "knn_distogram launch");
     cuda_check(cudaFreeAsync(d_freq, stream), "cudaFreeAsync");
+}
+}  // namespace
+
+void knn_distogram(std::int64_t B, std::int64_t L, const float* trans, const KnnSpec& spec, float* out,
+                   cudaStream_t stream) {
+    knn_distogram_impl(B, L, trans, spec, out, stream);
+}
+
+void knn_distogram(std::int64_t B, std::int64_t L, const double* trans, const KnnSpec& spec, double* out,
+                   cudaStream_t stream) {
+    knn_distogram_impl(B, L, trans, spec, out, stream);
 }
 
 std::size_t build_factors_workspace(std::int64_t rows, std::size_t f, std::size_t n) {
@@ -100,17 +114,16 @@ std::vector<float> to_f32(const double* x, std::size_t n) {
 }
 }  // namespace
 
+// The reference's f64 API: float64 translations copied as they are and float64 features back --
+// neighbour choice and bins bit-exact with proj/src/pair_features.cpp:29-45.
 void knn_distogram_host(std::int64_t B, std::int64_t L, const double* trans, const KnnSpec& spec, double* out) {
     validate_knn(B, L, spec);
     if (trans == nullptr || out == nullptr) throw ValueError("null pointer");
     const std::size_t n_in = std::size_t(B) * L * 3, n_out = std::size_t(B) * L * spec.k * (spec.n_bins + spec.pe_dim);
-    const auto t32 = to_f32(trans, n_in);
-    DevBuf dt(n_in * 4), dout(n_out * 4);
-    cuda_check(cudaMemcpy(dt.p, t32.data(), n_in * 4, cudaMemcpyHostToDevice), "H2D");
-    knn_distogram(B, L, dt.as<float>(), spec, dout.as<float>(), nullptr);
-    std::vector<float> h(n_out);
-    cuda_check(cudaMemcpy(h.data(), dout.p, n_out * 4, cudaMemcpyDeviceToHost), "D2H");
-    for (std::size_t i = 0; i < n_out; ++i) out[i] = h[i];
+    DevBuf dt(n_in * 8), dout(n_out * 8);
+    cuda_check(cudaMemcpy(dt.p, trans, n_in * 8, cudaMemcpyHostToDevice), "H2D");
+    knn_distogram(B, L, dt.as<double>(), spec, dout.as<double>(), nullptr);
+    cuda_check(cudaMemcpy(out, dout.p, n_out * 8, cudaMemcpyDeviceToHost), "D2H");
 }
 
 void build_factors_host(std::int64_t rows, std::size_t f, const double* features, std::size_t r, std::size_t d_z,

@@ -90,7 +90,7 @@ def report_to_json(report: RunReport) -> str:
                    for c in report.checks],
         "notes": list(report.notes),
     }
-    return json.dumps(j, indent=2) + "\n"
+    return json.dumps(j, indent=2, sort_keys=True) + "\n"  # nlohmann::json: keys sorted, dump(2)
 
 
 def emit_report(report: RunReport, fmt: str, path: str = "-") -> None:
@@ -276,7 +276,7 @@ def load_config(path: str = "") -> BenchConfig:
 def config_to_json(cfg: BenchConfig) -> str:
     j = {"model": dataclasses.asdict(cfg.model), "distogram": dataclasses.asdict(cfg.distogram),
          "bench": {k: getattr(cfg, k) for k in _BENCH_KEYS}}
-    return json.dumps(j, separators=(",", ":"))
+    return json.dumps(j, separators=(",", ":"), sort_keys=True)  # nlohmann::json dump(): compact, keys sorted
 
 
 def run_fit(csv_path: str, metric: str, cfg: BenchConfig | None = None) -> RunReport:

@@ -249,3 +249,15 @@ def test_forward_bench_config_all_rows(fipa):
     got, _, _ = gpu_forward_device(model, batch)
     ref, _ = emulated_backward(MAIN, w, batch, np.zeros((8, 1024, MAIN["d_in"])))
     assert rel_dev(ref, got) < BF16_TOL
+
+
+def test_fully_masked_flags(fipa):
+    """fully_masked (proj/src/flash_ipa.cpp:156-158): every row of a sample without a valid residue
+    is flagged; partially masked or unmasked samples are not."""
+    mask = np.ones((3, 70), dtype=bool)
+    mask[1, :] = False
+    mask[2, ::3] = False
+    f = fipa.fully_masked(mask)
+    assert f.shape == (3, 70) and f.dtype == bool
+    assert f[1].all() and not f[0].any() and not f[2].any()
+    assert not fipa.fully_masked(np.ones(5, bool)).any() and fipa.fully_masked(np.zeros(5, bool)).all()

@@ -18,7 +18,24 @@ def _line(n):
 
 
 def _cloud(n, seed, scale=6.0):
-    return np.random.default_rng(seed).standard_normal((n, 3)).astype(np.float32).astype(np.float64) * scale
+    """A float64 point cloud (NOT rounded to float32: the f64 API must keep every bit)."""
+    return np.random.default_rng(seed).standard_normal((n, 3)) * scale
+
+
+def _near_ties(n, seed):
+    """Shells of points whose distances to their centre differ by ~1e-12 A: they tie after a
+    float32 rounding, and the higher index is always the nearer one, so a rounded path picks the
+    wrong neighbour (lower-index tie-break) while the f64 reference does not."""
+    rng = np.random.default_rng(seed)
+    pts = [rng.standard_normal(3) * 8.0 for _ in range(n // 8)]
+    out = []
+    for c in pts:
+        out.append(c)
+        for m in range(7):
+            u = rng.standard_normal(3)
+            u /= np.linalg.norm(u)
+            out.append(c + u * (3.0 - 1e-12 * m))  # later points slightly closer
+    return np.asarray(out[:n])
 
 
 def test_oracle_matches_reference_knn_and_factors():
@@ -65,7 +82,33 @@ def test_input_validation_matches_reference(fipa):
 
 def _check_feats(ref, got, n_bins):
     assert np.array_equal(ref[..., :n_bins], got[..., :n_bins])  # neighbour choice + bins: exact
-    assert np.abs(ref[..., n_bins:] - got[..., n_bins:]).max() < 2e-7  # sinusoids: float32 rounding
+    # sinusoids: float64 on both sides (device sincos vs glibc: a few ulp); wrong neighbours would
+    # show as O(1) differences of the offset encoding
+    assert np.abs(ref[..., n_bins:] - got[..., n_bins:]).max() < 1e-12
+
+
+def test_near_tie_cloud_separates_f32_from_f64():
+    """The near-tie fixture really is a float32/float64 discriminator for the oracle."""
+    pts = _near_ties(64, 3)
+    exact = fo.knn_distogram(pts, k=6)
+    rounded = fo.knn_distogram(pts.astype(np.float32).astype(np.float64), k=6)
+    assert not np.array_equal(exact[..., 22:], rounded[..., 22:])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [11, 12])
+def test_gpu_knn_near_ties_bit_exact_vs_compiled_reference(fipa, seed):
+    """f64 clouds with engineered near-ties (distances 1e-12 apart): the GPU's neighbour indices and
+    bins equal the compiled reference's (oracle/_ref, proj/src/pair_features.cpp:29-45) bit for bit."""
+    from oracle import ref
+
+    pts = _near_ties(256, seed)
+    kw = dict(k=7, n_bins=16, d_min=2.0, d_max=4.0, pe_dim=8)
+    got = fipa.knn_distogram(pts, **kw)
+    want = ref.knn_distogram(pts, **kw) if ref.available() else fo.knn_distogram(pts, **kw)
+    _check_feats(want, got, kw["n_bins"])
+    got_b = fipa.knn_distogram(np.stack([pts, pts[::-1].copy()]), **kw)  # batched path, same rule
+    _check_feats(want, got_b[0], kw["n_bins"])
 
 
 @pytest.mark.gpu

@@ -130,3 +130,88 @@ def test_fit_command_and_scaling_checks(tmp_path):
     fit = rp.run_fit(str(p), "peak_bytes")
     assert [f.arm for f in fit.fits] == ["flash", "reference"]
     assert fit.fits[1].quadratic == pytest.approx(544.0, rel=1e-9)
+
+
+# ------------------------------------------------------------------ pinned to the compiled reference
+def _ref():
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("compiled reference not available (make -C oracle)")
+    return ref
+
+
+def _rich_report():
+    r = rp.RunReport(command="scaling", config_echo=rp.config_to_json(rp.load_config("")))
+    vals = [0.125, 1.0 / 3.0, 1e-9, 12345.678901234567, 2.0 ** -40, 7.0, 0.1 + 0.2]
+    r.records = [rp.RunRecord("flash" if i % 2 else "reference", 128 << i, 7 + i, "f32" if i % 3 else "f64",
+                              10 ** i + 3, v) for i, v in enumerate(vals)]
+    r.fits = [rp.FitSummary("flash", "peak_bytes", 1e-3, 2.5, 0.999),
+              rp.FitSummary("reference", "seconds", 3.25e-9, -1.5e-7, 1.0 / 7.0)]
+    r.checks = [rp.CheckOutcome("scaling/flash/quadratic-share", 0.001, 0.01, True),
+                rp.CheckOutcome("scaling/reference/r2", 0.5, 0.99, False)]
+    r.notes = ["reference arm skipped at L=8192: estimated peak exceeds budget", "second note"]
+    return r
+
+
+def test_report_text_byte_identical_to_reference():
+    """report_to_csv / report_to_json text equals the reference's (proj/src/model_io.cpp:200-243)
+    byte for byte: 17-digit CSV seconds, nlohmann's sorted keys and number forms."""
+    ref = _ref()
+    rep = _rich_report()
+    assert rp.report_to_csv(rep) == ref.report_text(rep, "csv")
+    assert rp.report_to_json(rep) == ref.report_text(rep, "json")
+
+
+def test_records_csv_parsed_identically(tmp_path):
+    """Our CSV parsed by the reference (model_io.cpp:260-306) and re-emitted is the same text; the
+    reference's CSV parsed by ours gives the same records."""
+    ref = _ref()
+    rep = _rich_report()
+    p = tmp_path / "r.csv"
+    p.write_text(rp.report_to_csv(rep))
+    assert ref.parse_records_csv_text(p) == rp.report_to_csv(rep)
+    p.write_text(ref.report_text(rep, "csv"))
+    assert rp.parse_records_csv(str(p)) == rep.records
+    for body in ("arm,length,seed,precision,peak_bytes,seconds\n", rp.CSV_HEADER + "\nflash,128,7,f64\n"):
+        p.write_text(body)
+        with pytest.raises(IOError):
+            ref.parse_records_csv_text(p)
+        with pytest.raises(IOError):
+            rp.parse_records_csv(str(p))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fit_polynomial_matches_reference(seed):
+    """fit_polynomial (proj/src/bench.cpp:103-149) on random designs, noisy and exact."""
+    ref = _ref()
+    rng = np.random.default_rng(seed)
+    Ls = np.sort(rng.choice([128, 256, 512, 1024, 2048, 4096, 8192, 16384], size=4 + seed % 4, replace=False))
+    a, b = rng.uniform(1e-6, 1e-2), rng.uniform(-1.0, 5.0)
+    ys = a * Ls ** 2 + b * Ls
+    if seed % 2:
+        ys = ys * (1 + 0.05 * rng.standard_normal(len(Ls)))
+    pts = list(zip(Ls.astype(float), ys))
+    want = ref.fit_polynomial(pts)
+    got = rp.fit_polynomial(pts)
+    for w_, g_ in zip(want, got):
+        assert abs(w_ - g_) <= 1e-12 * max(1.0, abs(w_))
+
+
+def test_fit_polynomial_degenerate_designs_match_reference():
+    ref = _ref()
+    for pts in ([(128.0, 1.0)], [(256.0, 1.0), (256.0, 2.0)], [(0.0, 1.0), (0.0, 3.0)]):
+        with pytest.raises(ArithmeticError):
+            ref.fit_polynomial(pts)
+        with pytest.raises(ArithmeticError):
+            rp.fit_polynomial(pts)
+
+
+def test_config_json_matches_reference(tmp_path):
+    """load_config + config_to_json (model_io.cpp:308-405): defaults and a partial file."""
+    ref = _ref()
+    assert rp.config_to_json(rp.load_config("")) == ref.config_json("")
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"model": {"d_in": 64, "heads": 4, "precision": "f32"},
+                             "distogram": {"k": 12}, "bench": {"lengths": [128, 256], "trials": 3}}))
+    assert rp.config_to_json(rp.load_config(str(p))) == ref.config_json(str(p))
