@@ -21,15 +21,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
-# Load order: torch's CUDA libraries (cuSPARSELt among them) initialise with static TLS and
-# crash at import if libfipa_b200.so -- which links the CUDA runtime statically and claims
-# glibc's optional static-TLS surplus -- was loaded first.  When torch is installed (the plumbing
-# for device memory, streams and torch.distributed), import it before the extension.
-try:
-    import torch  # noqa: F401
-except ImportError:
-    pass
-
+# No torch import: libfipa_b200.so links the CUDA runtime shared, so it loads in any order with
+# torch (or without it); torch is only the tests' / bench's plumbing for buffers and streams.
 try:
     from ._fipa_b200 import (Comm, Model, Trunk, build_factors, comm_unique_id,  # noqa: F401  (native, in-tree)
                              flash_attention, fully_masked, knn_distogram, naive_attention)

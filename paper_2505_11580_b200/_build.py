@@ -39,7 +39,16 @@ EXT_PATH = os.path.join(PKG, EXT_NAME)
 
 
 def _cxx():
-    return os.environ.get("CXX") or shutil.which("g++") or "g++"
+    # Prefer the system g++: it links libstdc++ dynamically.  A g++ that links it statically puts
+    # a second, exported libstdc++ inside the pybind module, and libraries loaded after it
+    # (torch's cuSPARSELt) then crash in their static constructors.
+    # (The image's CXX wrapper links parts of libstdc++ statically, so CXX is not honoured here;
+    # FIPA_CXX overrides.)
+    if os.environ.get("FIPA_CXX"):
+        return os.environ["FIPA_CXX"]
+    if os.access("/usr/bin/g++", os.X_OK):
+        return "/usr/bin/g++"
+    return shutil.which("g++") or "g++"
 
 
 def _stale(target, deps):
@@ -81,7 +90,10 @@ def build_native(verbose=False):
         objs = list(ex.map(_compile, CU_SOURCES + CXX_SOURCES))
     if _stale(LIB_PATH, objs):
         tmp = LIB_PATH + ".tmp"
-        _run([NVCC, *GENCODE, "-shared", "-o", tmp, *objs, "-Xlinker", "-soname=" + LIB_NAME, "-ldl"])
+        # CUDA runtime linked SHARED (rpath to the toolkit): a static cudart claims glibc's static-TLS
+        # surplus, which made torch's CUDA libraries fail to load after this library
+        _run([NVCC, *GENCODE, "-shared", "-cudart", "shared", "-o", tmp, *objs, "-Xlinker", "-soname=" + LIB_NAME,
+              "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64"), "-ldl"])
         os.replace(tmp, LIB_PATH)
     import pybind11
 

@@ -6,8 +6,9 @@ rows, the packed key/value rows are all-gathered rank-major over NCCL ([G][B*H][
 key j of the sequence = row j % L_local of shard j // L_local -- the layout the attention
 kernel's 5-D TMA maps read), and each rank returns the output rows of its block.  The
 translation centroid used for recentring is all-reduced (4 floats per sample).  The compute and
-the collectives run in libfipa_b200.so (fipa_layer_forward_sharded); torch.distributed is used
-here only to hand rank 0's NCCL unique id to the other ranks.
+the collectives run in libfipa_b200.so (fipa_layer_forward_sharded).  The only host-side exchange
+is rank 0's 128-byte NCCL unique id: any byte-broadcast callable can carry it (MPI, a key-value
+store, a file); torch.distributed is used only when no callable is given.
 """
 
 from __future__ import annotations
@@ -31,21 +32,35 @@ def key_location(j: int, L_local: int):
     return j // L_local, j % L_local
 
 
-def share_unique_id(uid: bytes | None, group=None) -> bytes:
-    """Broadcast rank 0's 128-byte NCCL unique id to every rank (any torch.distributed backend)."""
-    import torch.distributed as dist
+def share_unique_id(uid: bytes | None, group=None, broadcast=None) -> bytes:
+    """Broadcast rank 0's 128-byte NCCL unique id to every rank.
 
-    obj = [uid if dist.get_rank(group) == 0 else None]
-    dist.broadcast_object_list(obj, src=0, group=group)
-    if not isinstance(obj[0], (bytes, bytearray)) or len(obj[0]) != 128:
+    broadcast: optional callable(bytes | None) -> bytes that returns rank 0's payload on every
+    rank (rank 0 passes the id, the others None).  Without it, torch.distributed (any backend,
+    `group` or the default group) carries it."""
+    if broadcast is not None:
+        got = broadcast(uid)
+    else:
+        import torch.distributed as dist
+
+        obj = [uid if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        got = obj[0]
+    if not isinstance(got, (bytes, bytearray)) or len(got) != 128:
         raise RuntimeError("NCCL unique id exchange failed")
-    return bytes(obj[0])
+    return bytes(got)
 
 
-def make_comm(fipa, device: int, group=None):
-    """fipa.Comm over the ranks of the (initialised) default torch.distributed group."""
-    import torch.distributed as dist
+def make_comm(fipa, device: int, group=None, *, world: int | None = None, rank: int | None = None,
+              broadcast=None):
+    """fipa.Comm over `world` ranks.  With `broadcast` (see share_unique_id) the caller names world
+    and rank itself and torch is not needed; otherwise they come from the (initialised)
+    torch.distributed group."""
+    if broadcast is None:
+        import torch.distributed as dist
 
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    uid = share_unique_id(fipa.comm_unique_id() if rank == 0 else None, group)
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    elif world is None or rank is None:
+        raise ValueError("make_comm(broadcast=...) needs world and rank")
+    uid = share_unique_id(fipa.comm_unique_id() if rank == 0 else None, group, broadcast)
     return fipa.Comm(world, rank, uid, device)

@@ -102,3 +102,48 @@ def test_two_rank_gloo_sharded_plan_reproduces_unsharded_layer():
     for rank, err_layout, err_oracle in res:
         assert err_layout < 1e-12, (rank, err_layout)   # same layout arithmetic, sharded vs not
         assert err_oracle < 1e-3, (rank, err_oracle)    # vs the reference restatement (hi/lo split)
+
+
+def test_unique_id_exchange_without_torch():
+    """share_unique_id / make_comm take any byte-broadcast callable (no torch.distributed)."""
+    from paper_2505_11580_b200 import sharding
+
+    uid = bytes(range(128))
+    box = {}
+
+    def bcast(payload):  # a 'store': rank 0 writes, the others read
+        if payload is not None:
+            box["id"] = payload
+        return box["id"]
+
+    assert sharding.share_unique_id(uid, broadcast=bcast) == uid
+    assert sharding.share_unique_id(None, broadcast=bcast) == uid
+    with pytest.raises(RuntimeError):
+        sharding.share_unique_id(None, broadcast=lambda p: b"short")
+    with pytest.raises(ValueError):
+        sharding.make_comm(None, 0, broadcast=bcast)
+
+
+def test_product_imports_without_torch():
+    """The product package (pybind module + libfipa_b200.so) imports in a process where
+    `import torch` raises, and does not import torch on its own; torch still imports after it
+    (the CUDA runtime is linked shared, libstdc++ dynamically)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import builtins, sys\n"
+            "real = builtins.__import__\n"
+            "def imp(n, *a, **k):\n"
+            "    if n == 'torch' or n.startswith('torch.'): raise ImportError('torch blocked')\n"
+            "    return real(n, *a, **k)\n"
+            "builtins.__import__ = imp\n"
+            "import paper_2505_11580_b200 as f\n"
+            "assert 'torch' not in sys.modules\n"
+            "from paper_2505_11580_b200 import sharding, report\n"
+            "print(f.Model(seed=1).config['d_in'])\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "32", r.stderr
+    code2 = "import sys, paper_2505_11580_b200\nassert 'torch' not in sys.modules\nimport torch\nprint('ok')\n"
+    r = subprocess.run([sys.executable, "-c", code2], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
