@@ -25,7 +25,8 @@
  * Differences from the reference, all additive: a leading batch axis B (each sample is an
  * independent reference call with its own mask), caller-owned device buffers + a CUDA stream,
  * and a precision switch: FIPA_PREC_BF16 runs the tcgen05 tensor-core path (bf16 operands, fp32
- * accumulation), FIPA_PREC_F32 the fp32 SIMT path.  There is no CPU fallback: without a
+ * accumulation), FIPA_PREC_F32 / F64 the fp32-accuracy path, also on the tcgen05 tensor cores
+ * (3xTF32: kind::tf32 MMAs over hi/lo operand splits).  There is no CPU fallback: without a
  * B200 every compute entry point returns FIPA_ERR_CUDA.
  *
  * Threading: a layer handle may be used from several threads on distinct streams for
@@ -50,8 +51,8 @@ extern "C" {
 #define FIPA_ERR_OTHER 9
 
 #define FIPA_PREC_BF16 0 /* tcgen05 path: bf16 operands, fp32 accumulation; f64 master weights */
-#define FIPA_PREC_F32 1  /* fp32 SIMT path; master weights rounded to f32 (reference "f32")    */
-#define FIPA_PREC_F64 2  /* reference "f64" models: f64 master weights, fp32 SIMT compute     */
+#define FIPA_PREC_F32 1  /* fp32-accuracy path (3xTF32 tensor cores); master weights rounded to f32 */
+#define FIPA_PREC_F64 2  /* reference "f64" models: f64 master weights, fp32-accuracy compute      */
 
 /* Hyper-parameters (IpaConfig).  Names follow the reference: d_in = c_s, d_z = c_z,
  * c = c_hidden, n_query = qk-points, n_value = v-points, rank = z_factor_rank. */
@@ -321,10 +322,13 @@ int fipa_layer_forward_launches(const fipa_layer* layer);
  *   bwd_ds     materialised-dS backward: -1 automatic (L <= 2048, dS <= 1 GiB), 0 off, 1 on
  *              within that cap (FIPA_BWD_DS)
  *   bwd_ring   attention-backward ring plan {nst1, nst2, nab, kb1}, zeros = automatic (FIPA_BWD_RING)
- *   pass_ring  two-pass attention rings {kb, kst, vkeys, vst}, zeros = automatic (FIPA_PASS_RING) */
+ *   pass_ring  two-pass attention rings {kb, kst, vkeys, vst}, zeros = automatic (FIPA_PASS_RING)
+ *   f32_tc     1: FIPA_PREC_F32/F64 run on the tensor cores (3xTF32 projections, attention and
+ *              output projection); 0: the fp32 CUDA-core kernels (FIPA_F32_TC=0) */
 typedef struct fipa_tuning {
     int32_t attn_impl, fused_pack, bwd_ds;
     int32_t bwd_ring[4], pass_ring[4];
+    int32_t f32_tc;
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

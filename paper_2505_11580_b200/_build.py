@@ -28,7 +28,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_tc.cu", "pack.cu", "attn_fwd_tc.cu", "attn_fwd_2sm.cu", "attn_fwd_pass.cu", "dense.cu", "simt_f32.cu", "attn_bwd.cu",
-              "bwd.cu", "pair_features.cu", "proj_pack.cu"]
+              "bwd.cu", "pair_features.cu", "proj_pack.cu", "attn_fwd_f32tc.cu"]
 CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp", "trunk.cpp", "producer.cpp"]
 HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp", "trunk.hpp", "producer.hpp"]
 

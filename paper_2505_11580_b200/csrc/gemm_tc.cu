@@ -3,7 +3,8 @@
 //   warp 0      : TMA producer (one elected lane)
 //   warp 1      : TMEM allocator + MMA issuer (one elected lane)
 //   warps 2..5  : epilogue, TMEM -> registers -> global (warp w owns TMEM lanes 32*(w%4)..)
-// One 128 x BN output tile per CTA.  Serves the projection GEMM (reference
+// One 128 x BN output tile per CTA.  TF32 = true: fp32 operands, tcgen05.mma kind::tf32 (the
+// fp32 path; 3xTF32 accuracy comes from K-concatenated hi/lo operands, see launch_gemm_tf32x3).  Serves the projection GEMM (reference
 // project_inputs, proj/src/ipa.cpp:201-217 -> linear, proj/src/tensor.cpp:292-317), the
 // output projection (proj/src/flash_ipa.cpp:212) and the backward GEMMs.
 #include <cuda_runtime.h>
@@ -21,18 +22,18 @@ namespace fipa_b200 {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BN>
+template <int BN, bool TF32 = false>
 struct GemmCfg {
+    static constexpr int BK = TF32 ? 32 : 64;  // K elements per stage: one 128-byte swizzle row
     // Output staging buffers per epilogue warp: 2 keep up once the epilogue math is branch-free
     // (tools/gemm_bench.cu: 4 buffers at the cost of ring stages measured no faster on the
     // short-K shapes and 13% slower on a square 8192^3 product).
     static constexpr int kStages = BN == 256 ? 4 : 6;
     static constexpr int kCBuf = 2;
-    static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kABytes = BM * 128;
+    static constexpr int kBBytes = BN * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStageC = 4 * kCBuf * 32 * 128;  // fp32 output staging: 4 warps x kCBuf x (32 rows x 128 B)
     static constexpr int kSmem = kStages * kStageBytes + kStageC + 1024 /*align*/ + 256 /*barriers*/;
@@ -68,12 +69,14 @@ __device__ long long g_gemm_trace[2][8][24];  // [epilogue warp 2 | MMA warp][un
 // Persistent: each CTA walks work units u = blockIdx.x, += gridDim.x over (split, m-tile, n-tile).
 // The smem ring runs continuously across units; the accumulator is double-buffered in TMEM
 // (2 x BN columns) so the epilogue warps drain unit u while the tensor pipe computes unit u+1.
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB,
                      const __grid_constant__ CUtensorMap mapC, EpiParams p) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, TF32>;
+    constexpr int BK = Cfg::BK;
+    static_assert(!TF32 || (!A_MN && !B_MN), "tf32 GEMM: K-major operands only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -160,12 +163,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The whole warp runs the loop and one elected lane issues (warp-uniform descriptors in
         // uniform registers; a lane-0-only loop paid ~45 cycles of R2UR per MMA, which left the
         // N=128 MMAs issue-bound); descriptors advance by 64-bit adds of (byte offset >> 4).
-        constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+        constexpr uint32_t idesc = TF32 ? ptx::idesc_tf32(BM, BN, A_MN, B_MN) : ptx::idesc_bf16(BM, BN, A_MN, B_MN);
         const uint32_t tiles_u32 = ptx::smem_u32(tiles);
         const uint64_t da0 = A_MN ? ptx::sw128_desc(tiles_u32, 64 * 128, 1024) : ptx::sw128_desc(tiles_u32, 16, 1024);
         const uint64_t db0 = B_MN ? ptx::sw128_desc(tiles_u32 + Cfg::kABytes, 64 * 128, 1024)
                                   : ptx::sw128_desc(tiles_u32 + Cfg::kABytes, 16, 1024);
-        constexpr uint64_t kStepA = A_MN ? (2048 >> 4) : (32 >> 4);  // one 16-deep K step
+        constexpr uint64_t kStepA = A_MN ? (2048 >> 4) : (32 >> 4);  // one MMA K step (16 bf16 / 8 tf32 = 32 B)
         constexpr uint64_t kStepB = B_MN ? (2048 >> 4) : (32 >> 4);
         int it = 0, lu = 0;  // k-block counter, local unit counter
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++lu) {
@@ -184,8 +187,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (ptx::elect_one()) {
                     const uint64_t so = static_cast<uint64_t>((s * Cfg::kStageBytes) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        ptx::mma_ss(acc, da0 + so + kk * kStepA, db0 + so + kk * kStepB, idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if constexpr (TF32)
+                            ptx::mma_ss_tf32(acc, da0 + so + kk * kStepA, db0 + so + kk * kStepB, idesc, (kb | kk) != 0);
+                        else
+                            ptx::mma_ss(acc, da0 + so + kk * kStepA, db0 + so + kk * kStepB, idesc, (kb | kk) != 0);
+                    }
                     ptx::mma_commit(&empty[s]);
                 }
                 __syncwarp();
@@ -339,9 +346,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) ptx::tmem_dealloc(tmem, kTmemCols);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool TF32 = false>
 void launch_impl(const GemmArgs& a, cudaStream_t stream) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, TF32>;
+    constexpr int BK = Cfg::BK;
     // TMA maps: K-major operands are [rows=M|N, cols=K] with box {64, rows-per-tile};
     // MN-major operands are [rows=K, cols=M|N] with box {64, BK}.
     // TMA maps (dim 2 = batch, dense stacks): K-major operands are [rows=M|N, cols=K] with box
@@ -351,12 +359,18 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
     // tile's columns) come in as ONE 4-D box {64, BK, tile/64 blocks} per stage
     const bool a_blk = A_MN && a.lda % 64 == 0 && a.lda >= a.M;
     const bool b_blk = B_MN && a.ldb % 64 == 0 && a.ldb >= a.N;
-    const CUtensorMap mapA = a_blk  ? make_map_blocks_bf16(a.A, a.K, nb, a.lda, BK, BM / 64)
-                             : A_MN ? make_map_3d_bf16(a.A, a.M, a.K, nb, a.lda, 64, BK)
-                                    : make_map_3d_bf16(a.A, a.K, a.M, nb, a.lda, 64, BM);
-    const CUtensorMap mapB = b_blk  ? make_map_blocks_bf16(a.B, a.K, nb, a.ldb, BK, BN / 64)
-                             : B_MN ? make_map_3d_bf16(a.B, a.N, a.K, nb, a.ldb, 64, BK)
-                                    : make_map_3d_bf16(a.B, a.K, a.N, nb, a.ldb, 64, BN);
+    CUtensorMap mapA, mapB;
+    if constexpr (TF32) {
+        mapA = make_map_3d_f32(a.A, a.K, a.M, nb, a.lda, 32, BM);
+        mapB = make_map_3d_f32(a.B, a.K, a.N, nb, a.ldb, 32, BN);
+    } else {
+        mapA = a_blk  ? make_map_blocks_bf16(a.A, a.K, nb, a.lda, BK, BM / 64)
+               : A_MN ? make_map_3d_bf16(a.A, a.M, a.K, nb, a.lda, 64, BK)
+                      : make_map_3d_bf16(a.A, a.K, a.M, nb, a.lda, 64, BM);
+        mapB = b_blk  ? make_map_blocks_bf16(a.B, a.K, nb, a.ldb, BK, BN / 64)
+               : B_MN ? make_map_3d_bf16(a.B, a.N, a.K, nb, a.ldb, 64, BK)
+                      : make_map_3d_bf16(a.B, a.K, a.N, nb, a.ldb, 64, BN);
+    }
     const bool tma_c = !a.out_bf16 && !a.accumulate && a.split_k <= 1 && (a.ldc * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
     const int bh = std::max(1, a.batch_h);
@@ -372,7 +386,7 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
         const uint32_t cb[4] = {32, 1, 32, 1};
         mapC = make_map_4d_f32_strided(a.C, cd, cs, cb);
     }
-    auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
+    auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, TF32>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);  // per device
     const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k) * static_cast<int>(nb);
     const int sms = device_sm_count();
@@ -381,6 +395,32 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+// fp32 GEMM on the tensor cores at ~fp32 accuracy ("3xTF32"): the caller passes K-concatenated
+// operands A' = [A_hi | A_hi | A_lo] and B'^T = [B_hi | B_lo | B_hi] (split3 layout, each part
+// `K` columns), so one kind::tf32 product over K' = 3K sums A_hi B_hi + A_hi B_lo + A_lo B_hi
+// (dropped: A_lo B_lo ~ 2^-22 relative).  Operands fp32, K-major, row strides multiples of 4.
+void launch_gemm_tf32(const GemmF32Args& a, cudaStream_t stream) {
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0) return;
+    if ((a.lda * 4) % 16 != 0 || (a.ldb * 4) % 16 != 0 || (a.ldc * 4) % 16 != 0)
+        throw std::invalid_argument("tf32 gemm: row strides must be multiples of 4 elements");
+    GemmArgs g;
+    g.A = reinterpret_cast<const __nv_bfloat16*>(a.A);
+    g.B = reinterpret_cast<const __nv_bfloat16*>(a.B);
+    g.C = a.C;
+    g.lda = a.lda;
+    g.ldb = a.ldb;
+    g.ldc = a.ldc;
+    g.M = a.M;
+    g.N = a.N;
+    g.K = a.K;
+    g.bias = a.bias;
+    g.row_mask = a.row_mask;
+    if (a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512))
+        launch_impl<256, false, false, true>(g, stream);
+    else
+        launch_impl<128, false, false, true>(g, stream);
+}
 
 void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return;

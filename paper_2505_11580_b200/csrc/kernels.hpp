@@ -41,6 +41,24 @@ struct GemmArgs {
 };
 void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 
+// C[M,N] = A[M,K] . B[N,K]^T (+ bias) with masked rows zeroed, fp32 operands (K-major, row
+// strides lda / ldb), tcgen05 kind::tf32.  For fp32 accuracy pass split3 operands (K = 3 parts).
+struct GemmF32Args {
+    const float* A = nullptr;
+    const float* B = nullptr;
+    float* C = nullptr;
+    int64_t lda = 0, ldb = 0, ldc = 0;
+    int M = 0, N = 0, K = 0;
+    const float* bias = nullptr;
+    const uint8_t* row_mask = nullptr;
+};
+void launch_gemm_tf32(const GemmF32Args& args, cudaStream_t stream);
+// split3: out[r, part*ld_part + c] = part_sel(in[r, c]) for parts p = 0, 1, 2, where bit p of
+// lo_mask selects lo(x) = x - tf32(x) instead of hi(x) = tf32(x); columns c in [cols, ld_part)
+// are written as 0.  planar = true writes part p to out + p * plane instead (row stride ld_part).
+void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,
+                   int lo_mask, int nparts, cudaStream_t stream, int64_t plane = 0);
+
 // ------------------------------------------------------- FlashIPA layer
 // Sizes of one layer configuration (host side, shared with the kernels).
 struct LayerDims {
@@ -268,6 +286,19 @@ struct AttnF32Args {
     int B, L;
 };
 void launch_attn_fwd_f32(const LayerDims& d, const AttnF32Args& a, cudaStream_t stream);
+// fp32-accuracy attention on the tensor cores (attn_fwd_f32tc.cu, "3xTF32"): q/k/v_hat split into
+// tf32 hi and lo planes ([B*H, L, dqk_pad] / [B*H, L, dv_pad] each, launch_split3 planar).
+struct AttnF32TcArgs {
+    const float *q_hi, *q_lo, *k_hi, *k_lo, *v_hi, *v_lo;
+    const float* z1;
+    const float* rot;
+    const float* trans;
+    float* feat;  // [BL, feat_ld] fp32
+    float* lse;
+    int B, L;
+};
+bool attn_fwd_f32tc_supported(const LayerDims& d);
+void launch_attn_fwd_f32tc(const LayerDims& d, const AttnF32TcArgs& a, cudaStream_t stream);
 
 // ------------------------------------------------ quadratic-memory arms (dense.cu)
 // Dense IPA forward (reference_forward, proj/src/ipa.cpp:244-310), fp32: materialises the pair

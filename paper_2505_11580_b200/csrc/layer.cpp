@@ -139,6 +139,7 @@ Tuning Tuning::from_env() {
     }
     if (const char* e = std::getenv("FIPA_FUSED_PACK")) t.fused_pack = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_BWD_DS")) t.bwd_ds = std::atoi(e) != 0 ? 1 : 0;
+    if (const char* e = std::getenv("FIPA_F32_TC")) t.f32_tc = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3]);
     if (const char* e = std::getenv("FIPA_PASS_RING"))
@@ -417,11 +418,13 @@ void FlashIpaLayer::release_device() {
     for (void* p : {static_cast<void*>(d_wproj_t_), static_cast<void*>(d_wout_t_), static_cast<void*>(d_wheads_),
                     static_cast<void*>(d_wproj_), static_cast<void*>(d_wout_),
                     static_cast<void*>(d_bout_), static_cast<void*>(d_head_g_),
-                    static_cast<void*>(d_wl_bias_), static_cast<void*>(d_bwd_scale_)}) {
+                    static_cast<void*>(d_wl_bias_), static_cast<void*>(d_bwd_scale_),
+                    static_cast<void*>(d_wproj_cat_), static_cast<void*>(d_wout_cat_)}) {
         if (p) cudaFree(p);
     }
     d_wproj_t_ = d_wout_t_ = d_wheads_ = nullptr;
     d_wproj_ = d_wout_ = d_bout_ = d_head_g_ = d_wl_bias_ = d_bwd_scale_ = nullptr;
+    d_wproj_cat_ = d_wout_cat_ = nullptr;
 }
 
 void FlashIpaLayer::init_weights(std::uint64_t seed) {
@@ -508,6 +511,31 @@ void FlashIpaLayer::upload_weights() {
         std::vector<float> o(w_.w_out.begin(), w_.w_out.end());
         up(&d_wout_, o);
     }
+    if (f32_tensor_cores()) {
+        // 3xTF32 B operands (K-major): row n = [w_hi | w_lo | w_hi] over the K extent, zero padded;
+        // hi = tf32(w) (round to nearest, ties away, like cvt.rna), lo = w - hi rounded to fp32
+        auto tf32 = [](double w) {
+            const float f = static_cast<float>(w);
+            std::uint32_t u = std::bit_cast<std::uint32_t>(f);
+            if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+            return std::bit_cast<float>(u);
+        };
+        auto cat = [&](std::size_t rows, std::size_t K, std::size_t Kp, auto&& val) {
+            std::vector<float> v(rows * 3 * Kp, 0.f);
+            for (std::size_t r = 0; r < rows; ++r)
+                for (std::size_t k = 0; k < K; ++k) {
+                    const double w = val(r, k);
+                    const float hi = tf32(w), lo = static_cast<float>(w - static_cast<double>(hi));
+                    float* row = v.data() + r * 3 * Kp;
+                    row[k] = hi;
+                    row[Kp + k] = lo;
+                    row[2 * Kp + k] = hi;
+                }
+            return v;
+        };
+        up(&d_wproj_cat_, cat(np, din, std::size_t(din_p()), [&](std::size_t n, std::size_t k) { return wproj[k * np + n]; }));
+        up(&d_wout_cat_, cat(din, feat, std::size_t(feat_p()), [&](std::size_t n, std::size_t k) { return w_.w_out[k * din + n]; }));
+    }
     std::vector<float> bout(w_.b_out.begin(), w_.b_out.end());
     up(&d_bout_, bout);
     std::vector<float> g(H), wlb(H * cfg_.d_z);
@@ -544,6 +572,13 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     w.colbias = reinterpret_cast<float*>(take(BHL * 4));
     w.lse = reinterpret_cast<float*>(take(BHL * 4));
     w.feat = take(BL * d.feat_ld * el);
+    if (f32_tensor_cores()) {
+        w.s_cat = reinterpret_cast<float*>(take(BL * 3 * std::size_t(din_p()) * 4));
+        w.qs = reinterpret_cast<float*>(take(2 * BHL * d.dqk_pad * 4));
+        w.ks = reinterpret_cast<float*>(take(2 * BHL * d.dqk_pad * 4));
+        w.vs = reinterpret_cast<float*>(take(2 * BHL * d.dv_pad * 4));
+        w.feat_cat = reinterpret_cast<float*>(take(BL * 3 * std::size_t(feat_p()) * 4));
+    }
     if (train) {
         const std::size_t rdz = std::size_t(d.rank) * d.d_z;
         w.o_hat = reinterpret_cast<float*>(take(BHL * d.dv_pad * 4));
@@ -568,6 +603,10 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     }
     w.bytes = off;
     return w;
+}
+
+bool FlashIpaLayer::f32_tensor_cores() const {
+    return cfg_.precision == Precision::f32 && tuning_.f32_tc && attn_fwd_f32tc_supported(dims_);
 }
 
 bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L) const {
@@ -602,6 +641,9 @@ int FlashIpaLayer::launches_per_backward() const {
 }
 
 int FlashIpaLayer::launches_per_forward() const {
+    // fp32 tensor-core path: recenter, split s, projection GEMM, pack, split q/k/v, attention,
+    // split feat, output GEMM
+    if (f32_tensor_cores()) return 10;
     if (cfg_.precision != Precision::bf16) return 5;
     // recenter, cast, [fused projection+pack | projection GEMM, pack], attention, output GEMM
     return (proj_pack_supported(dims_) && tuning_.fused_pack) ? 5 : 6;
@@ -710,6 +752,21 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         g.N = d.n_proj;
         g.K = d.d_in;
         launch_gemm_bf16(g, stream);
+    } else if (f32_tensor_cores()) {
+        // 3xTF32: proj = [s_hi | s_hi | s_lo] . [W_hi | W_lo | W_hi]^T on the tensor cores
+        launch_split3(s, BL, d.d_in, d.d_in, ws.s_cat, din_p(), 3 * int64_t(din_p()), 0b100, 3, stream);
+        mark(2);
+        GemmF32Args g;
+        g.A = ws.s_cat;
+        g.lda = 3 * din_p();
+        g.B = d_wproj_cat_;
+        g.ldb = 3 * din_p();
+        g.C = ws.proj;
+        g.ldc = d.n_proj;
+        g.M = BL;
+        g.N = d.n_proj;
+        g.K = 3 * din_p();
+        launch_gemm_tf32(g, stream);
     } else {
         mark(2);
         launch_gemm_f32(s, d.d_in, d_wproj_, ws.proj, BL, d.n_proj, d.d_in, nullptr, nullptr, stream);
@@ -782,6 +839,46 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         g.bias = d_bout_;
         g.row_mask = mask;
         launch_gemm_bf16(g, stream);
+    } else if (f32_tensor_cores()) {
+        const int64_t BHL = int64_t(B) * d.heads * L;
+        const int64_t pq = BHL * d.dqk_pad, pv = BHL * d.dv_pad;
+        launch_split3(static_cast<const float*>(ws.qhat), BHL, d.dqk_pad, d.dqk_pad, ws.qs, d.dqk_pad, d.dqk_pad, 0b10, 2,
+                      stream, pq);
+        launch_split3(static_cast<const float*>(ws.khat), BHL, d.dqk_pad, d.dqk_pad, ws.ks, d.dqk_pad, d.dqk_pad, 0b10, 2,
+                      stream, pq);
+        launch_split3(static_cast<const float*>(ws.vhat), BHL, d.dv_pad, d.dv_pad, ws.vs, d.dv_pad, d.dv_pad, 0b10, 2,
+                      stream, pv);
+        AttnF32TcArgs aa{};
+        aa.q_hi = ws.qs;
+        aa.q_lo = ws.qs + pq;
+        aa.k_hi = ws.ks;
+        aa.k_lo = ws.ks + pq;
+        aa.v_hi = ws.vs;
+        aa.v_lo = ws.vs + pv;
+        aa.z1 = z1;
+        aa.rot = rot;
+        aa.trans = ws.trans_c;
+        aa.feat = static_cast<float*>(ws.feat);
+        aa.lse = ws.lse;
+        aa.B = int(B);
+        aa.L = int(L);
+        launch_attn_fwd_f32tc(d, aa, stream);
+        mark(5);
+        launch_split3(static_cast<const float*>(ws.feat), BL, d.feat, d.feat_ld, ws.feat_cat, feat_p(),
+                      3 * int64_t(feat_p()), 0b100, 3, stream);
+        GemmF32Args g;
+        g.A = ws.feat_cat;
+        g.lda = 3 * feat_p();
+        g.B = d_wout_cat_;
+        g.ldb = 3 * feat_p();
+        g.C = out;
+        g.ldc = d.d_in;
+        g.M = BL;
+        g.N = d.d_in;
+        g.K = 3 * feat_p();
+        g.bias = d_bout_;
+        g.row_mask = mask;
+        launch_gemm_tf32(g, stream);
     } else {
         AttnF32Args aa{};
         aa.qhat = static_cast<const float*>(ws.qhat);

@@ -67,6 +67,7 @@ struct Tuning {
                                   // 1 on (within the same cap)
     int bwd_ring[4] = {0, 0, 0, 0};   // FIPA_BWD_RING  "nst1,nst2,nab,kb1" (0 = automatic)
     int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
+    bool f32_tc = true;           // FIPA_F32_TC = 0: fp32 path on CUDA cores (SIMT reference kernels)
     static Tuning from_env();
 };
 
@@ -177,7 +178,10 @@ public:
     bool materialize_ds(std::int64_t B, std::int64_t L) const;
     const Tuning& tuning() const { return tuning_; }
     // Not thread-safe against concurrent calls on the same layer (like weight mutation).
-    void set_tuning(const Tuning& t) { tuning_ = t; }
+    void set_tuning(const Tuning& t) {
+        tuning_ = t;
+        dirty_ = true;  // the device weight copies depend on the kernel choice
+    }
     std::size_t num_weights() const;
     void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                   const float* rot, const float* trans, const std::uint8_t* mask, const float* dout,
@@ -237,8 +241,18 @@ public:
         __nv_bfloat16* ds = nullptr;       // [BH, L, ds_ld] materialised dS (short sequences, or null)
         int ds_ld = 0;
         float* dwproj = nullptr;           // [d_in, n_proj]
+        // fp32 path on the tensor cores (3xTF32): K-concatenated / planar hi-lo operands
+        float* s_cat = nullptr;            // [BL, 3 din_p]  s_hi | s_hi | s_lo
+        float* qs = nullptr;               // [2][BH L, dqk_pad]  q_hat hi / lo planes
+        float* ks = nullptr;
+        float* vs = nullptr;               // [2][BH L, dv_pad]
+        float* feat_cat = nullptr;         // [BL, 3 feat_p]  feat_hi | feat_hi | feat_lo
         std::size_t bytes = 0;
     };
+    // fp32 path: projections, attention and output projection on the tensor cores (3xTF32)
+    bool f32_tensor_cores() const;
+    int din_p() const { return (dims_.d_in + 31) / 32 * 32; }
+    int feat_p() const { return (dims_.feat + 31) / 32 * 32; }
     static constexpr int kAccLd = 448;
     int nproj_ld() const { return (dims_.n_proj + 7) / 8 * 8; }
     Workspace carve(void* base, std::int64_t B, std::int64_t L, bool train = false) const;
@@ -284,6 +298,8 @@ private:
     __nv_bfloat16* d_wout_t_ = nullptr;   // bf16 [d_in, feat]
     __nv_bfloat16* d_wheads_ = nullptr;   // bf16 [H * NH, d_in] head-major projection (fused path)
     float* d_wproj_ = nullptr;            // f32  [d_in, n_proj]
+    float* d_wproj_cat_ = nullptr;        // f32  [n_proj, 3 din_p]  W_hi | W_lo | W_hi (K-major, 3xTF32)
+    float* d_wout_cat_ = nullptr;         // f32  [d_in, 3 feat_p]   w_out^T hi | lo | hi
     float* d_wout_ = nullptr;             // f32  [feat, d_in]
     float* d_bout_ = nullptr;             // [d_in]
     float* d_head_g_ = nullptr;           // [H]

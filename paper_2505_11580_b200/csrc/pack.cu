@@ -519,6 +519,32 @@ __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat1
 }
 
 // One block per sample: subtract the centroid of the valid residues' translations.
+// 3xTF32 operand split (fp32 path): each element x becomes hi = tf32(x) and lo = x - hi (exact),
+// written into up to three K-concatenated parts (or planes) per row.
+__device__ __forceinline__ float tf32_round(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void split3_kernel(const float* __restrict__ in, int64_t rows, int cols, int64_t ld_in,
+                              float* __restrict__ out, int ld_part, int64_t ld_out, int lo_mask, int nparts,
+                              int64_t plane) {
+    const int64_t n = rows * ld_part;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / ld_part;
+        const int c = static_cast<int>(e - r * ld_part);
+        const float x = c < cols ? in[r * ld_in + c] : 0.f;
+        const float hi = tf32_round(x), lo = x - hi;
+        for (int p = 0; p < nparts; ++p) {
+            const float v = (lo_mask >> p) & 1 ? lo : hi;
+            if (plane) out[p * plane + r * ld_part + c] = v;
+            else out[r * ld_out + int64_t(p) * ld_part + c] = v;
+        }
+    }
+}
+
 // fully_masked flags (proj/src/flash_ipa.cpp:156-158): every row of a sample without a valid
 // residue is flagged (its output is all zeros); one block per sample.
 __global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* __restrict__ flags, int L) {
@@ -717,6 +743,15 @@ void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, in
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
     f32_to_bf16_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, rows, cols, ld_out);
+}
+
+void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,
+                   int lo_mask, int nparts, cudaStream_t stream, int64_t plane) {
+    const int64_t n = rows * ld_part;
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 16);
+    split3_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, rows, cols, ld_in, out, ld_part, ld_out,
+                                                                      lo_mask, nparts, plane);
 }
 
 void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cudaStream_t stream) {

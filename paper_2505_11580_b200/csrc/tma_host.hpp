@@ -48,6 +48,22 @@ inline CUtensorMap make_map_2d_bf16(const void* base, uint64_t rows, uint64_t co
     return m;
 }
 
+// fp32 tensor [d2, d1, d0] (d0 contiguous, rows of `ld` elements), box {box0, box1, 1},
+// SWIZZLE_128B (box0 = 32: one 128-byte row).
+inline CUtensorMap make_map_3d_f32(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld,
+                                   uint32_t box0, uint32_t box1) {
+    CUtensorMap m{};
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {ld * 4, ld * 4 * d1};
+    cuuint32_t box[3] = {box0, box1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled(3d f32) failed: " + std::to_string(int(r)));
+    return m;
+}
+
 // bf16 tensor [d2, d1, d0] (d0 contiguous, rows of `ld` elements), box {box0, box1, 1}.
 inline CUtensorMap make_map_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                                     uint64_t ld, uint32_t box0, uint32_t box1) {
