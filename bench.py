@@ -235,6 +235,8 @@ def run_reference(args, shape):
 
 
 def run_ours(args, shape):
+    if args.precision == "f32":
+        args.pass_ = "fwd"  # the fp32-accuracy path (3xTF32 tensor cores) is inference-only
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -482,7 +484,8 @@ def run_ours(args, shape):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic (reference input distribution), random-init weights",
-            "config": {"workload": f"FlashIPA layer {args.pass_}, B={B} L={L} per GPU (BASELINE cfg2)",
+            "config": {"workload": f"FlashIPA layer {args.pass_}, B={B} L={L} per GPU (BASELINE cfg2)" +
+                                   (" at fp32 accuracy (3xTF32 tensor cores)" if args.precision == "f32" else ""),
                        "pass": args.pass_, "model": "FlashIPA layer", "global_batch": B * world, "seq_len": L,
                        "shape": shape, "parallelism": (f"dp{world} (samples sharded, weight-gradient all-reduce)" if train and world > 1
                                        else f"dp{world} (independent samples)"),

@@ -16,8 +16,9 @@
 //   P_j  = 2^(S_j - m) in fp32 by the softmax warps (lazy rescale: the running max moves only
 //          when it grows by more than 2^8), split into P_hi | P_lo in shared memory
 //          (K-major, 128 rows x 64 keys each).
-//   O   += P_j . V_hat_j      three chains P_hi V_hi + P_lo V_hi + P_hi V_lo, V streamed in
-//          128-column chunks (hi and lo planes, MN-major), N = 128, 128, 128, 48 -> TMEM [0, 432)
+//   O   += P_j . V_hat_j      three chains P_hi V_hi + P_lo V_hi + P_hi V_lo, V^T streamed in
+//          128-column chunks (hi and lo planes, K-major: keys contiguous), N = 128, 128, 128, 48
+//          -> TMEM [0, 432)
 // The tensor pipe runs S_{j+1} while the softmax warps turn S_j into P_j.  Epilogue: the same
 // split / pair contraction / inverse frame / norms as the bf16 kernels, fp32 features staged in
 // shared memory and written with coalesced stores.
@@ -48,7 +49,7 @@ constexpr int kQChunk = BM * 128;  // 32 fp32 columns x 128 rows
 constexpr int kKChunk = BN * 128;  // 32 fp32 columns x 64 keys
 constexpr int kQKStage = 2 * kQChunk + 2 * kKChunk;  // q_hi | q_lo | k_hi | k_lo
 constexpr int kVNc = 128;                            // value columns per V chunk
-constexpr int kVStage = BN * kVNc * 4;               // 64 keys x 128 fp32 (4 blocks of 32 columns)
+constexpr int kVStage = BN * kVNc * 4;               // 128 value columns x 64 keys: 2 atoms of 32 keys
 constexpr int kPBytes = BM * BN * 4;                 // one P plane: 2 atoms of 128 rows x 128 B
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -157,16 +158,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int it = 0;
             for (int j = 0; j < ntiles; ++j) {
                 for (int nc = 0; nc < nvc; ++nc) {
-                    const int ncols = min(kVNc, p.dv_mma - nc * kVNc);
-                    const int nblk = (ncols + 31) / 32;
                     for (int plane = 0; plane < 2; ++plane, ++it) {
                         const int s = it % kVStages;
                         if (it >= kVStages) ptx::mbar_wait(&bars->v_empty[s], ((it / kVStages) - 1) & 1);
                         uint8_t* st = sV + s * kVStage;
-                        ptx::mbar_expect_tx(&bars->v_full[s], nblk * BN * 128);
-                        for (int b = 0; b < nblk; ++b)
-                            ptx::tma_load_3d(st + b * (BN * 128), plane ? &mVl : &mVh, &bars->v_full[s],
-                                             nc * kVNc + b * 32, j * BN, bh);
+                        ptx::mbar_expect_tx(&bars->v_full[s], kVStage);
+                        for (int a = 0; a < 2; ++a)  // keys [32a, 32a + 32) x 128 value columns
+                            ptx::tma_load_3d(st + a * (kVNc * 128), plane ? &mVl : &mVh, &bars->v_full[s],
+                                             j * BN + 32 * a, nc * kVNc, bh);
                     }
                 }
             }
@@ -179,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t v_base = ptx::smem_u32(sV);
         const uint64_t d_qk = ptx::sw128_desc(qk_base, 16, 1024);
         const uint64_t d_p = ptx::sw128_desc(p_base, 16, 1024);
-        // MN-major V chunk: 32-column blocks of [64 keys x 128 B] (LBO), 8 keys per 1 KB atom (SBO)
-        const uint64_t d_v = ptx::sw128_desc(v_base, BN * 128, 1024);
+        // K-major V^T chunk: 128 value-column rows of 128 B (32 keys) per atom, atoms 16 KB apart
+        const uint64_t d_v = ptx::sw128_desc(v_base, 16, 1024);
         int it = 0, vit = 0;
         for (int j = 0; j <= ntiles; ++j) {
             if (j < ntiles) {
@@ -212,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 for (int nc = 0; nc < nvc; ++nc) {
                     const int ncols = min(kVNc, p.dv_mma - nc * kVNc);
-                    const uint32_t idesc_v = ptx::idesc_tf32(BM, ncols, false, true);
+                    const uint32_t idesc_v = ptx::idesc_tf32(BM, ncols, false, false);
                     const int sh = vit % kVStages, sl = (vit + 1) % kVStages;
                     ptx::mbar_wait(&bars->v_full[sh], (vit / kVStages) & 1);
                     ptx::mbar_wait(&bars->v_full[sl], ((vit + 1) / kVStages) & 1);
@@ -226,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // A (P, K-major): 8 keys = +32 B within a 32-key atom, atoms 16 KB apart
                             const uint64_t pa = d_p + static_cast<uint64_t>(((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4);
                             const uint64_t pl = pa + static_cast<uint64_t>(kPBytes >> 4);
-                            const uint64_t o = static_cast<uint64_t>((kk * 8 * 128) >> 4);  // 8 key rows of V
+                            const uint64_t o = static_cast<uint64_t>(((kk >> 2) * (kVNc * 128) + (kk & 3) * 32) >> 4);
                             const uint32_t first = (jj > 0 || kk > 0) ? 1u : 0u;
                             ptx::mma_ss_tf32(acc_col, pa, vh + o, idesc_v, first);
                             ptx::mma_ss_tf32(acc_col, pl, vh + o, idesc_v, 1u);
@@ -455,8 +454,9 @@ void launch_attn_fwd_f32tc(const LayerDims& d, const AttnF32TcArgs& a, cudaStrea
     const CUtensorMap mQl = make_map_3d_f32(a.q_lo, d.dqk_pad, a.L, BH, d.dqk_pad, 32, BM);
     const CUtensorMap mKh = make_map_3d_f32(a.k_hi, d.dqk_pad, a.L, BH, d.dqk_pad, 32, BN);
     const CUtensorMap mKl = make_map_3d_f32(a.k_lo, d.dqk_pad, a.L, BH, d.dqk_pad, 32, BN);
-    const CUtensorMap mVh = make_map_3d_f32(a.v_hi, d.dv_pad, a.L, BH, d.dv_pad, 32, BN);
-    const CUtensorMap mVl = make_map_3d_f32(a.v_lo, d.dv_pad, a.L, BH, d.dv_pad, 32, BN);
+    const uint64_t Lp = (static_cast<uint64_t>(a.L) + 3) / 4 * 4;
+    const CUtensorMap mVh = make_map_3d_f32(a.v_hi, a.L, d.dv_pad, BH, Lp, 32, kVNc);
+    const CUtensorMap mVl = make_map_3d_f32(a.v_lo, a.L, d.dv_pad, BH, Lp, 32, kVNc);
     constexpr Layout lay = smem_layout();
     const int smem = lay.total + 1024;
     static_assert(smem_layout().total + 1024 <= 232448, "3xTF32 attention: shared memory budget");

@@ -397,9 +397,10 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
 }  // namespace
 
 // fp32 GEMM on the tensor cores at ~fp32 accuracy ("3xTF32"): the caller passes K-concatenated
-// operands A' = [A_hi | A_hi | A_lo] and B'^T = [B_hi | B_lo | B_hi] (split3 layout, each part
-// `K` columns), so one kind::tf32 product over K' = 3K sums A_hi B_hi + A_hi B_lo + A_lo B_hi
-// (dropped: A_lo B_lo ~ 2^-22 relative).  Operands fp32, K-major, row strides multiples of 4.
+// operands, e.g. A' = [A_hi | A_lo | A_hi] and B'^T = [B_lo | B_hi | B_hi] (split3 layout, each part
+// `K` columns), so one kind::tf32 product over K' = 3K sums A_hi B_lo + A_lo B_hi + A_hi B_hi
+// (small cross terms first; dropped: A_lo B_lo ~ 2^-22 relative).  Operands fp32, K-major, row
+// strides multiples of 4.
 void launch_gemm_tf32(const GemmF32Args& a, cudaStream_t stream) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0) return;
     if ((a.lda * 4) % 16 != 0 || (a.ldb * 4) % 16 != 0 || (a.ldc * 4) % 16 != 0)

@@ -56,6 +56,8 @@ void launch_gemm_tf32(const GemmF32Args& args, cudaStream_t stream);
 // split3: out[r, part*ld_part + c] = part_sel(in[r, c]) for parts p = 0, 1, 2, where bit p of
 // lo_mask selects lo(x) = x - tf32(x) instead of hi(x) = tf32(x); columns c in [cols, ld_part)
 // are written as 0.  planar = true writes part p to out + p * plane instead (row stride ld_part).
+// hi/lo split with transpose: in [BH][L][D] -> out [2][BH][D][Lp] (planes `plane` floats apart)
+void launch_split_t(const float* in, int BH, int L, int D, float* out, int Lp, int64_t plane, cudaStream_t stream);
 void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,
                    int lo_mask, int nparts, cudaStream_t stream, int64_t plane = 0);
 
@@ -286,8 +288,9 @@ struct AttnF32Args {
     int B, L;
 };
 void launch_attn_fwd_f32(const LayerDims& d, const AttnF32Args& a, cudaStream_t stream);
-// fp32-accuracy attention on the tensor cores (attn_fwd_f32tc.cu, "3xTF32"): q/k/v_hat split into
-// tf32 hi and lo planes ([B*H, L, dqk_pad] / [B*H, L, dv_pad] each, launch_split3 planar).
+// fp32-accuracy attention on the tensor cores (attn_fwd_f32tc.cu, "3xTF32"): q/k_hat split into
+// tf32 hi and lo planes ([B*H, L, dqk_pad] each, launch_split3 planar), v_hat transposed into
+// [B*H, dv_pad, Lp] hi / lo planes (launch_split_t; Lp = L rounded up to 4).
 struct AttnF32TcArgs {
     const float *q_hi, *q_lo, *k_hi, *k_lo, *v_hi, *v_lo;
     const float* z1;

@@ -512,8 +512,9 @@ void FlashIpaLayer::upload_weights() {
         up(&d_wout_, o);
     }
     if (f32_tensor_cores()) {
-        // 3xTF32 B operands (K-major): row n = [w_hi | w_lo | w_hi] over the K extent, zero padded;
-        // hi = tf32(w) (round to nearest, ties away, like cvt.rna), lo = w - hi rounded to fp32
+        // 3xTF32 B operands (K-major): row n = [w_lo | w_hi | w_hi] over the K extent, zero padded,
+        // against A' = [a_hi | a_lo | a_hi]: the two small cross terms accumulate first, then the
+        // large hi.hi term.  hi = tf32(w) (round to nearest, ties away, like cvt.rna), lo = w - hi.
         auto tf32 = [](double w) {
             const float f = static_cast<float>(w);
             std::uint32_t u = std::bit_cast<std::uint32_t>(f);
@@ -527,8 +528,8 @@ void FlashIpaLayer::upload_weights() {
                     const double w = val(r, k);
                     const float hi = tf32(w), lo = static_cast<float>(w - static_cast<double>(hi));
                     float* row = v.data() + r * 3 * Kp;
-                    row[k] = hi;
-                    row[Kp + k] = lo;
+                    row[k] = lo;
+                    row[Kp + k] = hi;
                     row[2 * Kp + k] = hi;
                 }
             return v;
@@ -576,7 +577,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.s_cat = reinterpret_cast<float*>(take(BL * 3 * std::size_t(din_p()) * 4));
         w.qs = reinterpret_cast<float*>(take(2 * BHL * d.dqk_pad * 4));
         w.ks = reinterpret_cast<float*>(take(2 * BHL * d.dqk_pad * 4));
-        w.vs = reinterpret_cast<float*>(take(2 * BHL * d.dv_pad * 4));
+        w.vs = reinterpret_cast<float*>(take(2 * std::size_t(B) * d.heads * d.dv_pad * round_up(std::size_t(L), 4) * 4));
         w.feat_cat = reinterpret_cast<float*>(take(BL * 3 * std::size_t(feat_p()) * 4));
     }
     if (train) {
@@ -753,8 +754,8 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         g.K = d.d_in;
         launch_gemm_bf16(g, stream);
     } else if (f32_tensor_cores()) {
-        // 3xTF32: proj = [s_hi | s_hi | s_lo] . [W_hi | W_lo | W_hi]^T on the tensor cores
-        launch_split3(s, BL, d.d_in, d.d_in, ws.s_cat, din_p(), 3 * int64_t(din_p()), 0b100, 3, stream);
+        // 3xTF32: proj = [s_hi | s_lo | s_hi] . [W_lo | W_hi | W_hi]^T on the tensor cores
+        launch_split3(s, BL, d.d_in, d.d_in, ws.s_cat, din_p(), 3 * int64_t(din_p()), 0b010, 3, stream);
         mark(2);
         GemmF32Args g;
         g.A = ws.s_cat;
@@ -841,13 +842,15 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         launch_gemm_bf16(g, stream);
     } else if (f32_tensor_cores()) {
         const int64_t BHL = int64_t(B) * d.heads * L;
-        const int64_t pq = BHL * d.dqk_pad, pv = BHL * d.dv_pad;
+        const int64_t pq = BHL * d.dqk_pad;
         launch_split3(static_cast<const float*>(ws.qhat), BHL, d.dqk_pad, d.dqk_pad, ws.qs, d.dqk_pad, d.dqk_pad, 0b10, 2,
                       stream, pq);
         launch_split3(static_cast<const float*>(ws.khat), BHL, d.dqk_pad, d.dqk_pad, ws.ks, d.dqk_pad, d.dqk_pad, 0b10, 2,
                       stream, pq);
-        launch_split3(static_cast<const float*>(ws.vhat), BHL, d.dv_pad, d.dv_pad, ws.vs, d.dv_pad, d.dv_pad, 0b10, 2,
-                      stream, pv);
+        const int Lp = int((L + 3) / 4 * 4);
+        const int64_t pv = int64_t(B) * d.heads * d.dv_pad * Lp;
+        launch_split_t(static_cast<const float*>(ws.vhat), int(B) * d.heads, int(L), d.dv_pad, ws.vs, Lp, pv, stream);
+        mark(4);  // the operand splits count with the pack stage; the attention stage is the kernel alone
         AttnF32TcArgs aa{};
         aa.q_hi = ws.qs;
         aa.q_lo = ws.qs + pq;
@@ -865,7 +868,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         launch_attn_fwd_f32tc(d, aa, stream);
         mark(5);
         launch_split3(static_cast<const float*>(ws.feat), BL, d.feat, d.feat_ld, ws.feat_cat, feat_p(),
-                      3 * int64_t(feat_p()), 0b100, 3, stream);
+                      3 * int64_t(feat_p()), 0b010, 3, stream);
         GemmF32Args g;
         g.A = ws.feat_cat;
         g.lda = 3 * feat_p();

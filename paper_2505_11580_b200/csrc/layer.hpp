@@ -242,11 +242,11 @@ public:
         int ds_ld = 0;
         float* dwproj = nullptr;           // [d_in, n_proj]
         // fp32 path on the tensor cores (3xTF32): K-concatenated / planar hi-lo operands
-        float* s_cat = nullptr;            // [BL, 3 din_p]  s_hi | s_hi | s_lo
+        float* s_cat = nullptr;            // [BL, 3 din_p]  s_hi | s_lo | s_hi
         float* qs = nullptr;               // [2][BH L, dqk_pad]  q_hat hi / lo planes
         float* ks = nullptr;
         float* vs = nullptr;               // [2][BH L, dv_pad]
-        float* feat_cat = nullptr;         // [BL, 3 feat_p]  feat_hi | feat_hi | feat_lo
+        float* feat_cat = nullptr;         // [BL, 3 feat_p]  feat_hi | feat_lo | feat_hi
         std::size_t bytes = 0;
     };
     // fp32 path: projections, attention and output projection on the tensor cores (3xTF32)
@@ -298,8 +298,8 @@ private:
     __nv_bfloat16* d_wout_t_ = nullptr;   // bf16 [d_in, feat]
     __nv_bfloat16* d_wheads_ = nullptr;   // bf16 [H * NH, d_in] head-major projection (fused path)
     float* d_wproj_ = nullptr;            // f32  [d_in, n_proj]
-    float* d_wproj_cat_ = nullptr;        // f32  [n_proj, 3 din_p]  W_hi | W_lo | W_hi (K-major, 3xTF32)
-    float* d_wout_cat_ = nullptr;         // f32  [d_in, 3 feat_p]   w_out^T hi | lo | hi
+    float* d_wproj_cat_ = nullptr;        // f32  [n_proj, 3 din_p]  W_lo | W_hi | W_hi (K-major, 3xTF32)
+    float* d_wout_cat_ = nullptr;         // f32  [d_in, 3 feat_p]   w_out^T lo | hi | hi
     float* d_wout_ = nullptr;             // f32  [feat, d_in]
     float* d_bout_ = nullptr;             // [d_in]
     float* d_head_g_ = nullptr;           // [H]

@@ -545,6 +545,32 @@ __global__ void split3_kernel(const float* __restrict__ in, int64_t rows, int co
     }
 }
 
+// Transposing hi/lo split of v_hat: in [BH][L][D] -> out planes [2][BH][D][Lp] (keys contiguous:
+// the K-major B operand of the 3xTF32 P.V products).  32 x 32 tiles through shared memory.
+__global__ void split_t_kernel(const float* __restrict__ in, int L, int D, float* __restrict__ out, int Lp,
+                               int64_t plane) {
+    __shared__ float tile[32][33];
+    const int bh = blockIdx.z;
+    const int l0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    const float* src = in + static_cast<int64_t>(bh) * L * D;
+    for (int r = ty; r < 32; r += 8) {
+        const int l = l0 + r, d = d0 + tx;
+        tile[r][tx] = (l < L && d < D) ? src[static_cast<int64_t>(l) * D + d] : 0.f;
+    }
+    __syncthreads();
+    float* dst = out + static_cast<int64_t>(bh) * D * Lp;
+    for (int r = ty; r < 32; r += 8) {
+        const int d = d0 + r, l = l0 + tx;
+        if (d < D && l < Lp) {
+            const float x = tile[tx][r];
+            const float hi = tf32_round(x);
+            dst[static_cast<int64_t>(d) * Lp + l] = hi;
+            dst[plane + static_cast<int64_t>(d) * Lp + l] = x - hi;
+        }
+    }
+}
+
 // fully_masked flags (proj/src/flash_ipa.cpp:156-158): every row of a sample without a valid
 // residue is flagged (its output is all zeros); one block per sample.
 __global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* __restrict__ flags, int L) {
@@ -752,6 +778,11 @@ void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 16);
     split3_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, rows, cols, ld_in, out, ld_part, ld_out,
                                                                       lo_mask, nparts, plane);
+}
+
+void launch_split_t(const float* in, int BH, int L, int D, float* out, int Lp, int64_t plane, cudaStream_t stream) {
+    dim3 grid((Lp + 31) / 32, (D + 31) / 32, BH);
+    split_t_kernel<<<grid, 256, 0, stream>>>(in, L, D, out, Lp, plane);
 }
 
 void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cudaStream_t stream) {
