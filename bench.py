@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-attn-long", action="store_true", help="skip the L=4096 / L=16384 attention timings")
     ap.add_argument("--cpu-sample-L", type=int, default=0, help="residues per CPU sample (default L)")
     ap.add_argument("--pass", dest="pass_", choices=["fwd+bwd", "fwd"], default="fwd+bwd")
     ap.add_argument("--trunk", type=int, default=0,
@@ -465,6 +466,51 @@ def run_ours(args, shape):
             "api": ("Model.flash_grad (float64 numpy in/out, every gradient copied back)" if train
                     else "Model.flash (float64 numpy in/out)")}
 
+    # Long-sequence attention (north-star target: >= 50% of bf16 peak at L >= 4096), timed in the
+    # same run with its own clock record: inference forward at B=2 L=4096 and B=1 L=16384, CUDA
+    # events around the attention kernel (the layer's stage timing) on the launch stream.
+    attn_long = None
+    if not args.no_attn_long and args.precision == "bf16":
+        attn_long = []
+        for Bl, Ll in ((2, 4096), (1, 16384)):
+            hl = synth_inputs(Bl, Ll, shape, seed=4321)
+            tl = {k: torch.from_numpy(v).to(dev) for k, v in hl.items()}
+            ol = torch.empty((Bl, Ll, shape["d_in"]), dtype=torch.float32, device=dev)
+            wl = model.workspace_size(Bl, Ll)
+            wsl = torch.empty(wl, dtype=torch.uint8, device=dev)
+            pl = {k: v.data_ptr() for k, v in tl.items()}
+
+            def fwd_l():
+                model.forward_device(Bl, Ll, pl["s"], pl["z1"], pl["z2"], pl["rot"], pl["trans"], pl["mask"],
+                                     ol.data_ptr(), wsl.data_ptr(), wl, stream.cuda_stream)
+
+            for _ in range(3):
+                fwd_l()
+            torch.cuda.synchronize()
+            model.set_timing(True)
+            reps = 10 if Ll <= 4096 else 5
+            att, tot = [], []
+            with ClockSampler(gpu_index) as clk_l:
+                for _ in range(reps):
+                    flush.zero_()
+                    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a_.record(stream)
+                    fwd_l()
+                    b_.record(stream)
+                    b_.synchronize()
+                    att.append(model.stage_times()[4])
+                    tot.append(a_.elapsed_time(b_))
+            model.set_timing(False)
+            att_ms, tot_ms = float(np.median(att)), float(np.median(tot))
+            fl = attn_flops(shape, Bl, Ll)
+            peak_l, _, kind_l = load_peaks()
+            attn_long.append({"B": Bl, "L": Ll, "attn_ms": att_ms, "layer_fwd_ms": tot_ms,
+                              "attn_tflops": fl / (att_ms / 1e3) / 1e12, "frac": fl / (att_ms / 1e3) / 1e12 / peak_l,
+                              "peak": peak_l, "peak_kind": f"{kind_l} burst bf16",
+                              "residues_per_s": Bl * Ll / (tot_ms / 1e3), "reps": reps, "clocks": clk_l.summary()})
+            del tl, ol, wsl
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -492,9 +538,11 @@ def run_ours(args, shape):
                        "l2": "flushed (256 MiB write) before every timed step"},
             "attn_tflops": achieved,
             "attn_bwd_tflops": achieved_bwd,
+            "attn_long": attn_long,
             "stage_ms": stage_ms,
-            "roofline": roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus,
-                                       peak_kind, traffic, ds_mode=ds_mode(B, L, shape["heads"])),
+            "roofline": (roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus,
+                                        peak_kind, traffic, ds_mode=ds_mode(B, L, shape["heads"]))
+                         if args.precision == "bf16" else roofline_f32(achieved, flops, peak, peak_kind)),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (model.forward_launches() + (model.backward_launches() if train else 0)) * args.steps,
@@ -504,6 +552,18 @@ def run_ours(args, shape):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def roofline_f32(achieved, flops, peak_bf16, peak_kind):
+    """fp32-accuracy path: the 3xTF32 attention kernel against the dense TF32 peak (half the bf16
+    rate: the measured bf16 peak / 2).  It issues 4 kind::tf32 products per useful product, so the
+    tensor pipe sees 4x the algorithmic FLOPs; its limiter is the streamed fp32 Q/K operands (L2)."""
+    peak = peak_bf16 / 2.0
+    return {"bound": "tensor", "kernel": "attn_fwd_f32tc_kernel (3xTF32: 4 kind::tf32 products per useful product)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+            "issued_frac": (4 * achieved / peak) if achieved else None,
+            "peak_kind": f"dense TF32 = {peak_kind} bf16 burst / 2", "traffic": None,
+            "algorithmic": f"2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per launch (useful)"}
 
 
 def ds_mode(B, L, H):

@@ -108,11 +108,16 @@ int fipa_fully_masked(int64_t B, int64_t L, const uint8_t* mask, uint8_t* flags,
 /* Same over host buffers (synchronous, current device). */
 int fipa_fully_masked_host(int64_t B, int64_t L, const uint8_t* mask, uint8_t* flags);
 
-/* Same forward over HOST float64 buffers (the reference / Python calling convention): copies in,
- * runs on an internal stream, copies out, synchronises. */
+/* Same forward over HOST float64 buffers (the reference / Python calling convention), synchronous.
+ * Pipelined over the batch: chunks of whole samples; the float64 <-> float32 conversion (host
+ * cores), the copies (two copy streams) and the kernels of neighbouring chunks overlap. */
 int fipa_layer_forward_host(fipa_layer* layer, int64_t B, int64_t L, const double* s,
                             const double* z1, const double* z2, const double* rot,
                             const double* trans, const uint8_t* mask, double* out);
+
+/* Same over HOST float32 buffers (additive: no float64 round trip; float32 out). */
+int fipa_layer_forward_host_f32(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                                const float* z2, const float* rot, const float* trans, const uint8_t* mask, float* out);
 
 /* ------------------------------------------------------------ quadratic-memory arm (f3)
  * The reference's dense forward (reference_forward, src/ipa.cpp:244-310; Python Model.reference,
@@ -180,6 +185,11 @@ int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L, const double* 
                          const double* z2, const double* rot, const double* trans, const uint8_t* mask,
                          const double* dout, double* out, double* ds, double* dz1, double* dz2,
                          double* drot, double* dtrans, double* dweights);
+/* Same over HOST float32 buffers (additive: no float64 round trip). */
+int fipa_layer_grad_host_f32(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
+                             const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                             const float* dout, float* out, float* ds, float* dz1, float* dz2, float* drot,
+                             float* dtrans, float* dweights);
 /* Byte offsets of the training intermediates in a train workspace, -1 when absent:
  *   0 o_hat (f32 [B,L,H,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
  *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B,L,H,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])

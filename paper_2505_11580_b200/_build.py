@@ -29,7 +29,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_tc.cu", "pack.cu", "attn_fwd_tc.cu", "attn_fwd_2sm.cu", "attn_fwd_pass.cu", "dense.cu", "simt_f32.cu", "attn_bwd.cu",
               "bwd.cu", "pair_features.cu", "proj_pack.cu", "attn_fwd_f32tc.cu"]
-CXX_SOURCES = ["layer.cpp", "capi.cpp", "comm.cpp", "trunk.cpp", "producer.cpp"]
+CXX_SOURCES = ["layer.cpp", "host_path.cpp", "capi.cpp", "comm.cpp", "trunk.cpp", "producer.cpp"]
 HEADERS = ["ptx.cuh", "kernels.hpp", "layer.hpp", "tma_host.hpp", "trunk.hpp", "producer.hpp"]
 
 LIB_NAME = "libfipa_b200.so"

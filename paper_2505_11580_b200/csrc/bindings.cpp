@@ -19,6 +19,18 @@ namespace py = pybind11;
 namespace {
 
 using DArr = py::array_t<double, py::array::c_style | py::array::forcecast>;
+using FArr = py::array_t<float, py::array::c_style | py::array::forcecast>;
+
+// Additive float32 host API: when every array argument is a float32 numpy array the host path
+// skips the float64 round trip (float32 in, float32 out); anything else takes the reference's
+// float64 convention (proj/python/bindings.cpp:26-45).
+bool all_f32(std::initializer_list<py::handle> xs) {
+    for (py::handle h : xs) {
+        if (!py::isinstance<py::array>(h)) return false;
+        if (!py::reinterpret_borrow<py::array>(h).dtype().is(py::dtype::of<float>())) return false;
+    }
+    return true;
+}
 
 struct FipaValueError : std::runtime_error {
     using std::runtime_error::runtime_error;
@@ -171,18 +183,20 @@ public:
     // Unbatched [L, ...] inputs return [L, d_in]; a leading batch axis [B, L, ...] is accepted
     // additively (mask then [B][L]).  Tiling/thread arguments are accepted and ignored: the
     // GPU result does not depend on them (reference guarantee, attention_kernel.hpp:34-37).
-    py::array_t<double> flash(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
-                              const DArr& translations, const py::object& mask, size_t tile_rows,
-                              size_t tile_cols, int threads) {
+    py::array flash(const py::object& s, const py::object& z1, const py::object& z2, const py::object& rotations,
+                    const py::object& translations, const py::object& mask, size_t tile_rows, size_t tile_cols,
+                    int threads) {
         if (tile_rows == 0 || tile_cols == 0) throw FipaValueError("tile sizes must be positive");
         (void)threads;
-        return run_host(s, z1, z2, rotations, translations, mask, false);
+        if (all_f32({s, z1, z2, rotations, translations}))
+            return run_host<float>(FArr(s), FArr(z1), FArr(z2), FArr(rotations), FArr(translations), mask, false);
+        return run_host<double>(DArr(s), DArr(z1), DArr(z2), DArr(rotations), DArr(translations), mask, false);
     }
 
     // Quadratic-memory forward (python/bindings.cpp:187-189 `reference`), on the GPU in fp32.
-    py::array_t<double> reference(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
-                                  const DArr& translations, const py::object& mask) {
-        return run_host(s, z1, z2, rotations, translations, mask, true);
+    py::array reference(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
+                        const DArr& translations, const py::object& mask) {
+        return run_host<double>(s, z1, z2, rotations, translations, mask, true);
     }
     size_t reference_workspace_size(int64_t B, int64_t L) const {
         return fipa_layer_reference_workspace_size(layer_, B, L);
@@ -202,8 +216,14 @@ public:
         check(rc);
     }
 
-    py::array_t<double> run_host(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
-                                 const DArr& translations, const py::object& mask, bool dense) {
+    template <class T>
+    py::array run_host(const py::array_t<T, py::array::c_style | py::array::forcecast>& s,
+                       const py::array_t<T, py::array::c_style | py::array::forcecast>& z1,
+                       const py::array_t<T, py::array::c_style | py::array::forcecast>& z2,
+                       const py::array_t<T, py::array::c_style | py::array::forcecast>& rotations,
+                       const py::array_t<T, py::array::c_style | py::array::forcecast>& translations,
+                       const py::object& mask, bool dense) {
+        using Arr = py::array_t<T, py::array::c_style | py::array::forcecast>;
         const bool batched = s.ndim() == 3;
         if (s.ndim() != 2 && s.ndim() != 3)
             throw FipaValueError("single representation must be [L, d_in] or [B, L, d_in]");
@@ -214,7 +234,7 @@ public:
         if (batched && s.shape(0) < 1) throw FipaValueError("batch must be >= 1");
         if (s.shape(o + 1) != int64_t(cfg_.d_in))
             throw FipaValueError("single representation must be [L, " + std::to_string(cfg_.d_in) + "]");
-        auto lead_ok = [&](const DArr& a, int nd) {
+        auto lead_ok = [&](const Arr& a, int nd) {
             if (a.ndim() != nd + o) return false;
             if (batched && a.shape(0) != B) return false;
             return a.shape(o) == L;
@@ -223,7 +243,7 @@ public:
             throw FipaValueError("rotations must have shape [L, 3, 3]");
         if (!lead_ok(translations, 2) || translations.shape(o + 1) != 3)
             throw FipaValueError("translations must have shape [L, 3]");
-        for (const DArr* z : {&z1, &z2}) {
+        for (const Arr* z : {&z1, &z2}) {
             if (!lead_ok(*z, 3) || z->shape(o + 1) != int64_t(cfg_.rank) ||
                 z->shape(o + 2) != int64_t(cfg_.d_z))
                 throw FipaValueError("factor shapes disagree with the configuration");
@@ -239,15 +259,20 @@ public:
         }
         std::vector<py::ssize_t> shape = batched ? std::vector<py::ssize_t>{B, L, (py::ssize_t)cfg_.d_in}
                                                  : std::vector<py::ssize_t>{L, (py::ssize_t)cfg_.d_in};
-        py::array_t<double> out(shape);
-        double* op = out.mutable_data();
+        py::array_t<T> out(shape);
+        T* op = out.mutable_data();
         int rc;
         {
             py::gil_scoped_release nogil;
-            rc = dense ? fipa_layer_reference_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
-                                                   translations.data(), mp, op)
-                       : fipa_layer_forward_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+            if constexpr (std::is_same_v<T, float>) {
+                rc = fipa_layer_forward_host_f32(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
                                                  translations.data(), mp, op);
+            } else {
+                rc = dense ? fipa_layer_reference_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                                       translations.data(), mp, op)
+                           : fipa_layer_forward_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                                     translations.data(), mp, op);
+            }
         }
         check(rc);
         return out;
@@ -449,8 +474,21 @@ public:
     // flash_grad(s, z1, z2, rotations, translations, dout, mask=None) -> (out, grads)
     // Forward + backward of sum(out * dout) through the host-buffer C ABI; grads is a dict with
     // s, z1, z2, rotations, translations and every weight tensor (reference names).
-    py::tuple flash_grad(const DArr& s, const DArr& z1, const DArr& z2, const DArr& rotations,
-                         const DArr& translations, const DArr& dout, const py::object& mask) {
+    py::tuple flash_grad(const py::object& s, const py::object& z1, const py::object& z2,
+                         const py::object& rotations, const py::object& translations, const py::object& dout,
+                         const py::object& mask) {
+        if (all_f32({s, z1, z2, rotations, translations, dout}))
+            return grad_host<float>(FArr(s), FArr(z1), FArr(z2), FArr(rotations), FArr(translations), FArr(dout), mask);
+        return grad_host<double>(DArr(s), DArr(z1), DArr(z2), DArr(rotations), DArr(translations), DArr(dout), mask);
+    }
+    template <class T>
+    py::tuple grad_host(const py::array_t<T, py::array::c_style | py::array::forcecast>& s,
+                        const py::array_t<T, py::array::c_style | py::array::forcecast>& z1,
+                        const py::array_t<T, py::array::c_style | py::array::forcecast>& z2,
+                        const py::array_t<T, py::array::c_style | py::array::forcecast>& rotations,
+                        const py::array_t<T, py::array::c_style | py::array::forcecast>& translations,
+                        const py::array_t<T, py::array::c_style | py::array::forcecast>& dout, const py::object& mask) {
+        using Arr = py::array_t<T, py::array::c_style | py::array::forcecast>;
         const bool batched = s.ndim() == 3;
         if (s.ndim() != 2 && s.ndim() != 3)
             throw FipaValueError("single representation must be [L, d_in] or [B, L, d_in]");
@@ -470,21 +508,28 @@ public:
             for (auto& v : m) v = v ? 1 : 0;
             mp = m.data();
         }
-        auto like = [](const DArr& a) {
-            return py::array_t<double>(std::vector<py::ssize_t>(a.shape(), a.shape() + a.ndim()));
+        auto like = [](const Arr& a) {
+            return py::array_t<T>(std::vector<py::ssize_t>(a.shape(), a.shape() + a.ndim()));
         };
-        py::array_t<double> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
-                            gt = like(translations);
+        py::array_t<T> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
+                       gt = like(translations);
         const uint64_t nw = fipa_layer_num_weights(layer_);
-        py::array_t<double> gw(static_cast<py::ssize_t>(nw));  // weight grads land here directly
-        double* gwp = gw.mutable_data();
+        py::array_t<T> gw(static_cast<py::ssize_t>(nw));  // weight grads land here directly
+        T* gwp = gw.mutable_data();
         int rc;
         {
             py::gil_scoped_release nogil;
-            rc = fipa_layer_grad_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
-                                      translations.data(), mp, dout.data(), out.mutable_data(), gs.mutable_data(),
-                                      gz1.mutable_data(), gz2.mutable_data(), gr.mutable_data(), gt.mutable_data(),
-                                      gwp);
+            if constexpr (std::is_same_v<T, float>) {
+                rc = fipa_layer_grad_host_f32(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                              translations.data(), mp, dout.data(), out.mutable_data(),
+                                              gs.mutable_data(), gz1.mutable_data(), gz2.mutable_data(),
+                                              gr.mutable_data(), gt.mutable_data(), gwp);
+            } else {
+                rc = fipa_layer_grad_host(layer_, B, L, s.data(), z1.data(), z2.data(), rotations.data(),
+                                          translations.data(), mp, dout.data(), out.mutable_data(), gs.mutable_data(),
+                                          gz1.mutable_data(), gz2.mutable_data(), gr.mutable_data(), gt.mutable_data(),
+                                          gwp);
+            }
         }
         check(rc);
         py::dict g;

@@ -438,6 +438,24 @@ int fipa_layer_backward(fipa_layer* layer, int64_t B, int64_t L_, const float* s
     });
 }
 
+int fipa_layer_forward_host_f32(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                                const float* z2, const float* rot, const float* trans, const uint8_t* mask, float* out) {
+    return guarded([&] {
+        if (!s || !z1 || !z2 || !rot || !trans || !out) throw fipa_b200::ValueError("null input/output pointer");
+        L(layer).forward_host_f32(B, L_, s, z1, z2, rot, trans, mask, out);
+    });
+}
+
+int fipa_layer_grad_host_f32(fipa_layer* layer, int64_t B, int64_t L_, const float* s, const float* z1,
+                             const float* z2, const float* rot, const float* trans, const uint8_t* mask,
+                             const float* dout, float* out, float* ds, float* dz1, float* dz2, float* drot,
+                             float* dtrans, float* dweights) {
+    return guarded([&] {
+        if (!s || !z1 || !z2 || !rot || !trans || !dout) throw fipa_b200::ValueError("null input pointer");
+        L(layer).grad_host_f32(B, L_, s, z1, z2, rot, trans, mask, dout, out, ds, dz1, dz2, drot, dtrans, dweights);
+    });
+}
+
 int fipa_layer_grad_host(fipa_layer* layer, int64_t B, int64_t L_, const double* s, const double* z1,
                          const double* z2, const double* rot, const double* trans, const uint8_t* mask,
                          const double* dout, double* out, double* ds, double* dz1, double* dz2,

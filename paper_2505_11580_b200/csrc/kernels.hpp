@@ -234,6 +234,8 @@ void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const Scat
                               cudaStream_t stream);
 // Translation gradient through the per-sample recentring: dt = mask*(dt_c - mean_valid(dt_c)).
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream);
+// acc[i] += x[i]
+void launch_add_inplace(float* acc, const float* x, int64_t n, cudaStream_t stream);
 // out[i] = in[i] * scale[i % period]
 void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream);
 

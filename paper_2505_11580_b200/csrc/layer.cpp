@@ -39,32 +39,6 @@ std::string cat(P&&... parts) {
 
 std::size_t round_up(std::size_t x, std::size_t m) { return (x + m - 1) / m * m; }
 
-// Host-side float64 <-> float32 conversion of the host-buffer entry points, split over the host
-// cores (the reference API is float64; the conversion is the dominant cost of the host path).
-template <class F>
-void parallel_chunks(std::size_t n, F&& f) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned T = std::min<unsigned>(16, hw);
-    if (n < (std::size_t(1) << 16) || T == 1) {
-        f(std::size_t(0), n);
-        return;
-    }
-    std::vector<std::thread> th;
-    const std::size_t per = (n + T - 1) / T;
-    for (unsigned t = 0; t < T; ++t) {
-        const std::size_t a = t * per, b = std::min(n, a + per);
-        if (a < b) th.emplace_back([&f, a, b] { f(a, b); });
-    }
-    for (auto& x : th) x.join();
-}
-
-template <class D, class S>
-void convert(D* dst, const S* src, std::size_t n) {
-    parallel_chunks(n, [dst, src](std::size_t a, std::size_t b) {
-        for (std::size_t i = a; i < b; ++i) dst[i] = static_cast<D>(src[i]);
-    });
-}
-
 // Inference attention kernel: the CTA-pair kernel where its budget allows, the two-pass pair
 // kernel for wider lifted rows (rank 3-4), else the single-CTA kernel.  Tuning::attn forces an
 // alternative (A/B checks); the single-CTA kernel does not read sharded keys, so a sharded
@@ -403,14 +377,10 @@ FlashIpaLayer::FlashIpaLayer(const Config& cfg) : cfg_(cfg) {
 
 FlashIpaLayer::~FlashIpaLayer() {
     release_device();
-    if (h_stage_) cudaFreeHost(h_stage_);
-    if (d_stage_) cudaFree(d_stage_);
-    if (own_stream_) cudaStreamDestroy(own_stream_);
+    release_host_pipe();
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : evb_)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : d2h_ev_)
         if (e) cudaEventDestroy(e);
 }
 
@@ -905,76 +875,6 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
     cuda_check(cudaGetLastError(), "kernel launch");
 }
 
-void FlashIpaLayer::forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
-                                 const double* z2, const double* rot, const double* trans,
-                                 const std::uint8_t* mask, double* out) {
-    run_host(B, L, s, z1, z2, rot, trans, mask, out, false);
-}
-
-void FlashIpaLayer::reference_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
-                                   const double* z2, const double* rot, const double* trans,
-                                   const std::uint8_t* mask, double* out) {
-    run_host(B, L, s, z1, z2, rot, trans, mask, out, true);
-}
-
-// Host buffers in, host buffers out (the reference calling convention): threaded float64 -> float32
-// conversion overlapped with the per-tensor copies, one device pass, copy back.
-void FlashIpaLayer::run_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
-                             const double* z2, const double* rot, const double* trans,
-                             const std::uint8_t* mask, double* out, bool dense) {
-    REQUIRE(B >= 1, "batch must be >= 1");
-    REQUIRE(L >= 1, "empty frame set");
-    std::lock_guard<std::mutex> host_lock(host_mu_);  // one staging set per layer
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-    if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");
-    const std::size_t BL = std::size_t(B) * L;
-    const std::size_t rdz = cfg_.rank * cfg_.d_z;
-    const std::size_t n_s = BL * cfg_.d_in, n_z = BL * rdz, n_r = BL * 9, n_t = BL * 3;
-    const std::size_t n_in = n_s + 2 * n_z + n_r + n_t, n_out = BL * cfg_.d_in;
-    const std::size_t io_bytes = round_up((n_in + n_out) * 4 + BL, 256);
-    const std::size_t ws_bytes = dense ? reference_workspace_size(B, L) : workspace_size(B, L);
-    if (h_stage_bytes_ < io_bytes) {
-        if (h_stage_) cudaFreeHost(h_stage_);
-        h_stage_ = nullptr;
-        cuda_check(cudaMallocHost(&h_stage_, io_bytes), "cudaMallocHost");
-        h_stage_bytes_ = io_bytes;
-    }
-    if (d_stage_bytes_ < io_bytes + ws_bytes) {
-        if (d_stage_) cudaFree(d_stage_);
-        d_stage_ = nullptr;
-        cuda_check(cudaMalloc(&d_stage_, io_bytes + ws_bytes), "cudaMalloc");
-        d_stage_bytes_ = io_bytes + ws_bytes;
-    }
-    float* h = static_cast<float*>(h_stage_);
-    float* dbase = static_cast<float*>(d_stage_);
-    std::size_t o = 0;
-    for (auto [src, n] : {std::pair{s, n_s}, std::pair{z1, n_z}, std::pair{z2, n_z}, std::pair{rot, n_r},
-                          std::pair{trans, n_t}}) {
-        convert(h + o, src, n);  // the copy of this tensor overlaps the conversion of the next
-        cuda_check(cudaMemcpyAsync(dbase + o, h + o, n * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
-        o += n;
-    }
-    std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
-    if (mask) std::memcpy(hmask, mask, BL);
-    std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
-    if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
-    void* ws = static_cast<char*>(d_stage_) + io_bytes;
-    if (dense) {
-        reference_forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
-                          dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
-                          own_stream_);
-    } else {
-        forward(B, L, dbase, dbase + n_s, dbase + n_s + n_z, dbase + n_s + 2 * n_z,
-                dbase + n_s + 2 * n_z + n_r, mask ? dmask : nullptr, dbase + n_in, ws, ws_bytes,
-                own_stream_);
-    }
-    cuda_check(cudaMemcpyAsync(h + n_in, dbase + n_in, n_out * 4, cudaMemcpyDeviceToHost, own_stream_),
-               "D2H");
-    cuda_check(cudaStreamSynchronize(own_stream_), "forward");
-    convert(out, h + n_in, n_out);
-}
-
-
 // ------------------------------------------------------------ quadratic-memory arm
 namespace {
 struct DenseLayout {
@@ -1052,22 +952,6 @@ void FlashIpaLayer::reference_forward(std::int64_t B, std::int64_t L, const floa
     a.out = out;
     launch_dense_ipa(dims_, a, stream);
     cuda_check(cudaGetLastError(), "kernel launch");
-}
-
-void FlashIpaLayer::ensure_staging(std::size_t host_bytes, std::size_t dev_bytes) {
-    if (!own_stream_) cuda_check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "stream");
-    if (h_stage_bytes_ < host_bytes) {
-        if (h_stage_) cudaFreeHost(h_stage_);
-        h_stage_ = nullptr;
-        cuda_check(cudaMallocHost(&h_stage_, host_bytes), "cudaMallocHost");
-        h_stage_bytes_ = host_bytes;
-    }
-    if (d_stage_bytes_ < dev_bytes) {
-        if (d_stage_) cudaFree(d_stage_);
-        d_stage_ = nullptr;
-        cuda_check(cudaMalloc(&d_stage_, dev_bytes), "cudaMalloc");
-        d_stage_bytes_ = dev_bytes;
-    }
 }
 
 // Backward of the layer (no reference counterpart: proj/SPEC.md:8).  Order of work:
@@ -1301,71 +1185,6 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
     }  // stage 3
     if (timing_) bwd_timed_once_ = true;
     cuda_check(cudaGetLastError(), "backward launch");
-}
-
-void FlashIpaLayer::grad_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,
-                              const double* z2, const double* rot, const double* trans,
-                              const std::uint8_t* mask, const double* dout, double* out, double* ds,
-                              double* dz1, double* dz2, double* drot, double* dtrans, double* dweights) {
-    REQUIRE(B >= 1, "batch must be >= 1");
-    REQUIRE(L >= 1, "empty frame set");
-    std::lock_guard<std::mutex> host_lock(host_mu_);  // one staging set per layer
-    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-    const std::size_t BL = std::size_t(B) * L;
-    const std::size_t rdz = cfg_.rank * cfg_.d_z;
-    const std::size_t n_s = BL * cfg_.d_in, n_z = BL * rdz, n_r = BL * 9, n_t = BL * 3;
-    const std::size_t n_in = n_s + 2 * n_z + n_r + n_t + n_s /*dout*/;
-    const std::size_t n_grad = n_s + 2 * n_z + n_r + n_t + num_weights();
-    const std::size_t n_out = n_s + n_grad;
-    const std::size_t io_bytes = round_up((n_in + n_out) * 4 + BL, 256);
-    const std::size_t ws_bytes = train_workspace_size(B, L);
-    ensure_staging(io_bytes, io_bytes + ws_bytes);
-    float* h = static_cast<float*>(h_stage_);
-    float* dbase = static_cast<float*>(d_stage_);
-    std::size_t o = 0;
-    for (auto [src, n] : {std::pair{s, n_s}, std::pair{z1, n_z}, std::pair{z2, n_z}, std::pair{rot, n_r},
-                          std::pair{trans, n_t}, std::pair{dout, n_s}}) {
-        convert(h + o, src, n);  // the copy of this tensor overlaps the conversion of the next
-        cuda_check(cudaMemcpyAsync(dbase + o, h + o, n * 4, cudaMemcpyHostToDevice, own_stream_), "H2D");
-        o += n;
-    }
-    std::uint8_t* hmask = reinterpret_cast<std::uint8_t*>(h + n_in + n_out);
-    if (mask) std::memcpy(hmask, mask, BL);
-    std::uint8_t* dmask = reinterpret_cast<std::uint8_t*>(dbase + n_in + n_out);
-    if (mask) cuda_check(cudaMemcpyAsync(dmask, hmask, BL, cudaMemcpyHostToDevice, own_stream_), "H2D");
-    void* ws = static_cast<char*>(d_stage_) + io_bytes;
-    const float* di = dbase;
-    float* dout_d = dbase + n_in;  // out, then grads
-    const float *d_s = di, *d_z1 = di + n_s, *d_z2 = d_z1 + n_z, *d_rot = d_z2 + n_z, *d_t = d_rot + n_r,
-                *d_dout = d_t + n_t;
-    float* g_s = dout_d + n_s;
-    float* g_z1 = g_s + n_s;
-    float* g_z2 = g_z1 + n_z;
-    float* g_rot = g_z2 + n_z;
-    float* g_t = g_rot + n_r;
-    float* g_w = g_t + n_t;
-    forward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, dout_d, ws, ws_bytes, own_stream_, true);
-    backward(B, L, d_s, d_z1, d_z2, d_rot, d_t, mask ? dmask : nullptr, d_dout, g_s, g_z1, g_z2, g_rot, g_t,
-             g_w, ws, ws_bytes, own_stream_);
-    // Per-tensor device->host copies, each followed by an event, so the float64 conversion of one
-    // output overlaps the transfer of the next.
-    const float* r = h + n_in;
-    const std::size_t offs[8] = {0, n_s, 2 * n_s, 2 * n_s + n_z, 2 * n_s + 2 * n_z, 2 * n_s + 2 * n_z + n_r,
-                                 2 * n_s + 2 * n_z + n_r + n_t, n_out};
-    double* dsts[7] = {out, ds, dz1, dz2, drot, dtrans, dweights};
-    if (!d2h_ev_[0])
-        for (auto& e : d2h_ev_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    for (int k = 0; k < 7; ++k) {
-        const std::size_t n = offs[k + 1] - offs[k];
-        if (dsts[k] != nullptr && n > 0)
-            cuda_check(cudaMemcpyAsync(h + n_in + offs[k], dout_d + offs[k], n * 4, cudaMemcpyDeviceToHost, own_stream_),
-                       "D2H");
-        cuda_check(cudaEventRecord(d2h_ev_[k], own_stream_), "event");
-    }
-    for (int k = 0; k < 7; ++k) {
-        cuda_check(cudaEventSynchronize(d2h_ev_[k]), "grad");
-        if (dsts[k] != nullptr) convert(dsts[k], r + offs[k], offs[k + 1] - offs[k]);
-    }
 }
 
 }  // namespace fipa_b200

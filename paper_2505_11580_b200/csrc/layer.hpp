@@ -188,10 +188,17 @@ public:
                   float* ds, float* dz1, float* dz2, float* drot, float* dtrans, float* dweights,
                   void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
                   const BwdShard* shard = nullptr);
+    // Host-buffer entry points (host_path.cpp): pipelined over the batch, float64 (reference
+    // convention) or float32 arrays.
     void grad_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
                    const double* rot, const double* trans, const std::uint8_t* mask, const double* dout,
                    double* out, double* ds, double* dz1, double* dz2, double* drot, double* dtrans,
                    double* dweights);
+    void grad_host_f32(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                       const float* rot, const float* trans, const std::uint8_t* mask, const float* dout, float* out,
+                       float* ds, float* dz1, float* dz2, float* drot, float* dtrans, float* dweights);
+    void forward_host_f32(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                          const float* rot, const float* trans, const std::uint8_t* mask, float* out);
     bool backward_supported() const;
     int launches_per_backward() const;
 
@@ -308,17 +315,20 @@ private:
     float k_scale_ = 0.f;
     bool dirty_ = true;
     std::mutex upload_mu_;
-    // host-path staging (forward_host / reference_host / grad_host), guarded by host_mu_: the
-    // host entry points release the GIL and may be called concurrently on one layer
+    // host-path pipeline (host_path.cpp: pinned / device slots, copy + compute streams), guarded
+    // by host_mu_: the host entry points release the GIL and may be called concurrently on one layer
     std::mutex host_mu_;
-    void* h_stage_ = nullptr;
-    std::size_t h_stage_bytes_ = 0;
-    void* d_stage_ = nullptr;
-    std::size_t d_stage_bytes_ = 0;
-    void ensure_staging(std::size_t host_bytes, std::size_t dev_bytes);
-    void run_host(std::int64_t B, std::int64_t L, const double* s, const double* z1, const double* z2,
-                  const double* rot, const double* trans, const std::uint8_t* mask, double* out, bool dense);
-    cudaStream_t own_stream_ = nullptr;
+    struct HostPipe;
+    HostPipe* pipe_ = nullptr;
+    HostPipe& host_pipe();
+    void release_host_pipe();
+    template <class T, class O>
+    void host_forward(std::int64_t B, std::int64_t L, const T* s, const T* z1, const T* z2, const T* rot,
+                      const T* trans, const std::uint8_t* mask, O* out, bool dense);
+    template <class T, class O>
+    void host_grad(std::int64_t B, std::int64_t L, const T* s, const T* z1, const T* z2, const T* rot,
+                   const T* trans, const std::uint8_t* mask, const T* dout, O* out, O* ds, O* dz1, O* dz2,
+                   O* drot, O* dtrans, O* dweights);
     // timing
     bool timing_ = false;
     static constexpr int kStages = 6;
@@ -329,7 +339,6 @@ public:
     std::vector<float> bwd_stage_times() const;
 private:
     cudaEvent_t evb_[kBwdStages + 1] = {};
-    cudaEvent_t d2h_ev_[7] = {};
     bool bwd_timed_once_ = false;
     bool timed_once_ = false;
 };

@@ -571,6 +571,12 @@ __global__ void split_t_kernel(const float* __restrict__ in, int L, int D, float
     }
 }
 
+__global__ void add_inplace_kernel(float* __restrict__ acc, const float* __restrict__ x, int64_t n) {
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        acc[e] += x[e];
+}
+
 // fully_masked flags (proj/src/flash_ipa.cpp:156-158): every row of a sample without a valid
 // residue is flagged (its output is all zeros); one block per sample.
 __global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* __restrict__ flags, int L) {
@@ -783,6 +789,12 @@ void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float
 void launch_split_t(const float* in, int BH, int L, int D, float* out, int Lp, int64_t plane, cudaStream_t stream) {
     dim3 grid((Lp + 31) / 32, (D + 31) / 32, BH);
     split_t_kernel<<<grid, 256, 0, stream>>>(in, L, D, out, Lp, plane);
+}
+
+void launch_add_inplace(float* acc, const float* x, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8);
+    add_inplace_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(acc, x, n);
 }
 
 void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cudaStream_t stream) {

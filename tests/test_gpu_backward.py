@@ -202,3 +202,28 @@ def test_backward_L4096_streaming_dq(fipa):
     model = _model(fipa, MAIN, 0)
     assert model.tuning()["bwd_ds"] == -1
     _check_large(fipa, 1, 4096, seed=4096, mask_frac=0.05)
+
+
+def test_host_paths_pipelined_and_float32(fipa):
+    """The host entry points cut the batch into chunks (4 chunks here) pipelined over copy and compute
+    streams; results equal the device path.  float32 arrays take the additive float32 path (float32
+    out) with the same numbers."""
+    model = _model(fipa, MAIN, 14)
+    B, L = 8, 256
+    batch = make_batch(MAIN, B, L, seed=14, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(2).standard_normal((B, L, MAIN["d_in"]))
+    out_d, g_d, _, _ = gpu_train_device(model, batch, dout)
+    args = [batch[k] for k in ("s", "z1", "z2", "rot", "trans")]
+    out_h = model.flash(*args, mask=batch["mask"])
+    assert out_h.dtype == np.float64 and rel_dev(out_d, out_h) < 1e-6
+    out_g, g_h = model.flash_grad(*args, dout, mask=batch["mask"])
+    assert rel_dev(out_d, out_g) < 1e-6
+    for n, m in (("s", "s"), ("z2", "z2"), ("rot", "rotations"), ("trans", "translations"), ("w_k", "w_k"),
+                 ("w_bias", "w_bias"), ("w_out", "w_out"), ("b_out", "b_out")):
+        assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
+    a32 = [a.astype(np.float32) for a in args]
+    out_32 = model.flash(*a32, mask=batch["mask"])
+    assert out_32.dtype == np.float32 and rel_dev(out_h, out_32) < 1e-6
+    o32, g32 = model.flash_grad(*a32, dout.astype(np.float32), mask=batch["mask"])
+    assert o32.dtype == np.float32 and g32["s"].dtype == np.float32
+    assert rel_dev(g_h["s"], g32["s"]) < 1e-5 and rel_dev(g_h["w_q"], g32["w_q"]) < 1e-5
