@@ -331,7 +331,8 @@ int fipa_layer_forward_launches(const fipa_layer* layer);
  *   fused_pack 1: fused projection + pack kernel (FIPA_FUSED_PACK=0 -> GEMM + pack kernel)
  *   bwd_ds     materialised-dS backward: -1 automatic (L <= 2048, dS <= 1 GiB), 0 off, 1 on
  *              within that cap (FIPA_BWD_DS)
- *   bwd_ring   attention-backward ring plan {nst1, nst2, nab, kb1}, zeros = automatic (FIPA_BWD_RING)
+ *   bwd_ring   attention-backward ring plan {nst1, nst2, nab, kb1}, zeros = automatic, and
+ *   bwd_slice  its B2 slice rows (16 / 32, 0 = any) (FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]")
  *   pass_ring  two-pass attention rings {kb, kst, vkeys, vst}, zeros = automatic (FIPA_PASS_RING)
  *   f32_tc     1: FIPA_PREC_F32/F64 run on the tensor cores (3xTF32 projections, attention and
  *              output projection); 0: the fp32 CUDA-core kernels (FIPA_F32_TC=0) */
@@ -339,6 +340,7 @@ typedef struct fipa_tuning {
     int32_t attn_impl, fused_pack, bwd_ds;
     int32_t bwd_ring[4], pass_ring[4];
     int32_t f32_tc;
+    int32_t bwd_slice;
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

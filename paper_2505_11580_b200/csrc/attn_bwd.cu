@@ -52,8 +52,9 @@ constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
 constexpr int kMaxStages1 = 3;  // B1 ring: whole 32-row tile halves, or groups of KB1 column blocks
 constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
-constexpr int kSlice = 16;
-constexpr int kSliceBox = kSlice * 128;
+// B2 slices of 16 or 32 rows (template SL): TMA throughput per SM grows with the box size
+// (profiles/r1_tma_microbench.txt: 2 KB boxes ~20 B/clk, 4 KB ~40 B/clk), so 32-row slices halve
+// the number of boxes per tile at the same ring bytes.
 constexpr uint32_t kXCol = 448;
 constexpr float kL2E = 1.4426950408889634f;
 
@@ -75,6 +76,7 @@ struct BwdParams {
     int kb1;           // column blocks per B1 stage (= nb1: whole tiles)
     int nst1;          // B1 ring depth (1 or 2)
     int nab;           // P / dS exchange buffers (2 or 3)
+    int slice;         // B2 slice rows (16 or 32)
     const float* lse;  // [BH, L] natural-log LSE of the forward
     const float* Dvec; // [BH, L] rowsum(dO_hat * O_hat)
     float* acc_out[2]; // [BH, L, acc_ld] fp32 (null = none)
@@ -159,12 +161,13 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
 
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
-template <bool KV, int kStages1, int NST2, int NAB, int KB1>
+template <bool KV, int kStages1, int NST2, int NAB, int KB1, int SL>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
                     const __grid_constant__ CUtensorMap b1D, const __grid_constant__ CUtensorMap b2D,
                     const __grid_constant__ CUtensorMap mapDS, BwdParams p) {
+    constexpr int kSlice = SL, kSliceBox = SL * 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -593,51 +596,55 @@ RoleDims make_role(int k1, int n2) {
 }
 
 // Ring plan: the stationary tile (128 rows x all column blocks) and the two P/dS buffers are
-// fixed; whole 32-row B1 tile halves (1 or 2 stages) and 16-row B2 slices (compile-time depth)
-// share the rest: dQ kernel (2, 6 x 4 KB), dK/dV kernel (1, 6 x 8 KB).  Whole-tile B1 stages
-// measured faster than column-block groups (dK/dV 0.406 vs 0.439 ms at B=8 L=1024, same-box A/B).
+// fixed; whole 32-row B1 tile halves (1 or 2 stages) and B2 slices of 16 or 32 rows
+// (compile-time depth) share the rest.  Whole-tile B1 stages measured faster than column-block
+// groups (dK/dV 0.406 vs 0.439 ms at B=8 L=1024, same-box A/B).
 void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     int nb1 = std::max(p.role[0].nb1, p.role[1].nb1);
     int nb2 = std::max(p.role[0].nba + p.role[0].nbb, p.role[1].nba + p.role[1].nbb);
     p.stat_bytes = nb1 * BM * 128;
     p.kb1 = nb1;
     p.b1_stage = nb1 * 32 * 128;
-    p.b2_stage = std::max(nb2, 1) * kSliceBox;
-    int forced[4] = {0, 0, 0, 0};  // AttnBwdArgs::ring (Tuning::bwd_ring): tuning experiments
+    int forced[5] = {0, 0, 0, 0, 0};  // AttnBwdArgs::ring (Tuning::bwd_ring): tuning experiments
     if (ring != nullptr)
-        for (int i = 0; i < 4; ++i) forced[i] = ring[i];
-    // (B1 stages, B2 stages, exchange buffers), preferred first.  Measured (B=8 L=1024, same box):
-    // dK/dV kernel (1,6,2) 0.392 ms vs (1,4,3) 0.397; dQ kernel (1,4,3) 0.349 vs (2,6,2) 0.358.
-    // (kb1 = 0: whole-tile B1 stages)
-    const int plans_kv[][4] = {{2, 6, 2, 0}, {1, 6, 2, 0}, {2, 3, 2, 0}, {2, 2, 2, 0}, {1, 4, 3, 0}, {1, 6, 3, 0},
-                               {3, 4, 2, 4}};
-    const int plans_q[][4] = {{1, 4, 3, 0}, {2, 6, 2, 0}, {1, 6, 2, 0}, {2, 3, 2, 0}, {2, 2, 2, 0}, {1, 6, 3, 0},
-                              {3, 4, 2, 4}};
+        for (int i = 0; i < 5; ++i) forced[i] = ring[i];
+    // (B1 stages, B2 stages, exchange buffers, kb1, B2 slice rows), preferred first.  Measured
+    // (B=8 L=1024, same box): dK/dV kernel (1,6,2,-,16) 0.392 ms vs (1,4,3,-,16) 0.397; dQ kernel
+    // (1,4,3,-,16) 0.349 vs (2,6,2,-,16) 0.358.  (kb1 = 0: whole-tile B1 stages)
+    const int plans_kv[][5] = {{1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
+                               {2, 2, 2, 0, 16}, {1, 4, 3, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
+                               {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
+    const int plans_q[][5] = {{1, 4, 3, 0, 16}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
+                              {2, 2, 2, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16}, {1, 3, 2, 0, 32},
+                              {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
     const auto& plans = kv ? plans_kv : plans_q;
     for (int pass = 0; pass < 2; ++pass) {
         for (const auto& pl : plans) {
             if (pass == 0 && forced[0] > 0 &&
-                (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2] || pl[3] != forced[3]))
+                (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2] || pl[3] != forced[3] ||
+                 (forced[4] > 0 && pl[4] != forced[4])))
                 continue;
             if (pass == 0 && forced[0] == 0) break;
             p.nst1 = pl[0];
             p.nst2 = pl[1];
             p.nab = pl[2];
             p.kb1 = pl[3] ? pl[3] : nb1;
+            p.slice = pl[4];
             p.b1_stage = p.kb1 * 32 * 128;
+            p.b2_stage = std::max(nb2, 1) * p.slice * 128;
             if (smem_layout(p).total + 1024 <= 232448) return;
         }
     }
     throw std::invalid_argument("attention backward: no ring plan fits shared memory");
 }
 
-template <bool KV, int NS1, int NST2, int NAB, int KB1 = 0>
+template <bool KV, int NS1, int NST2, int NAB, int KB1 = 0, int SL = 16>
 void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
                   cudaStream_t stream) {
     const Layout lay = smem_layout(p);
     const int smem = lay.total + 1024;
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
-    auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB, KB1>;
+    auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB, KB1, SL>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
@@ -647,7 +654,12 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
 template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
-    if (p.kb1 == 4 && p.nst1 == 3) {
+    if (p.slice == 32) {
+        if (p.nab == 3) launch_depth<KV, 1, 2, 3, 0, 32>(d, a, p, maps, stream);
+        else if (p.nst1 == 2 && p.nst2 == 3) launch_depth<KV, 2, 3, 2, 0, 32>(d, a, p, maps, stream);
+        else if (p.nst1 == 2) launch_depth<KV, 2, 2, 2, 0, 32>(d, a, p, maps, stream);
+        else launch_depth<KV, 1, 3, 2, 0, 32>(d, a, p, maps, stream);
+    } else if (p.kb1 == 4 && p.nst1 == 3) {
         launch_depth<KV, 3, 4, 2, 4>(d, a, p, maps, stream);
     } else if (p.nab == 3) {
         if (p.nst2 == 4) launch_depth<KV, 1, 4, 3>(d, a, p, maps, stream);
@@ -699,9 +711,9 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         return sharded(x) ? make_map_blocks_bf16_sharded(x, kc, BH, G, ld_of(x), 32, kb)
                           : make_map_blocks_bf16(x, chunk_of(x), BH, ld_of(x), 32, kb);
     };
-    auto slice = [&](const void* x) {
-        return sharded(x) ? make_map_4d_bf16_sharded(x, ld_of(x), kc, BH, G, 64, kSlice)
-                          : make_map_3d_bf16(x, ld_of(x), chunk_of(x), BH, ld_of(x), 64, kSlice);
+    auto slice = [&](const void* x, int sl) {
+        return sharded(x) ? make_map_4d_bf16_sharded(x, ld_of(x), kc, BH, G, 64, sl)
+                          : make_map_3d_bf16(x, ld_of(x), chunk_of(x), BH, ld_of(x), 64, sl);
     };
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
@@ -725,8 +737,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < a.L))
             throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= L, % 8");
         const CUtensorMap m0 = stat(a.khat, nqk);
-        const CUtensorMap maps[7] = {m0, tile(a.qhat, p.kb1), slice(a.dohat),
-                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat),
+        const CUtensorMap maps[7] = {m0, tile(a.qhat, p.kb1), slice(a.dohat, p.slice),
+                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat, p.slice),
                                      p.ds_store ? make_map_3d_bf16(a.ds, a.L, a.L, BH, a.ds_ld, 64, BM) : m0};
         launch<true>(d, a, p, maps, stream);
     }
@@ -780,8 +792,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
         const CUtensorMap q0map = stat(a.qhat, nqk);
-        const CUtensorMap maps[7] = {q0map, tile(a.khat, p.kb1), slice(a.khat),
-                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat), q0map};
+        const CUtensorMap maps[7] = {q0map, tile(a.khat, p.kb1), slice(a.khat, p.slice),
+                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat, p.slice), q0map};
         launch<false>(d, a, p, maps, stream);
     }
 }

@@ -558,7 +558,9 @@ public:
         d["attn_impl"] = attn[t.attn_impl];
         d["fused_pack"] = t.fused_pack != 0;
         d["bwd_ds"] = t.bwd_ds;
-        d["bwd_ring"] = std::vector<int>(t.bwd_ring, t.bwd_ring + 4);
+        std::vector<int> ring(t.bwd_ring, t.bwd_ring + 4);
+        ring.push_back(t.bwd_slice);
+        d["bwd_ring"] = ring;
         d["pass_ring"] = std::vector<int>(t.pass_ring, t.pass_ring + 4);
         d["f32_tc"] = t.f32_tc != 0;
         return d;
@@ -579,14 +581,15 @@ public:
         if (!fused_pack.is_none()) t.fused_pack = fused_pack.cast<bool>() ? 1 : 0;
         if (!bwd_ds.is_none()) t.bwd_ds = bwd_ds.cast<int>();
         if (!f32_tc.is_none()) t.f32_tc = f32_tc.cast<bool>() ? 1 : 0;
-        auto ring = [](py::object o, int32_t* dst) {
+        auto ring = [](py::object o, int32_t* dst, int32_t* extra) {
             if (o.is_none()) return;
             const auto v = o.cast<std::vector<int>>();
-            if (v.size() != 4) throw py::value_error("ring plans have 4 entries");
+            if (v.size() != 4 && !(extra && v.size() == 5)) throw py::value_error("ring plans have 4 entries (5 with the slice)");
             for (int i = 0; i < 4; ++i) dst[i] = v[i];
+            if (extra) *extra = v.size() == 5 ? v[4] : 0;
         };
-        ring(bwd_ring, t.bwd_ring);
-        ring(pass_ring, t.pass_ring);
+        ring(bwd_ring, t.bwd_ring, &t.bwd_slice);
+        ring(pass_ring, t.pass_ring, nullptr);
         check(fipa_layer_set_tuning(layer_, &t));
     }
     std::vector<float> stage_times() const {

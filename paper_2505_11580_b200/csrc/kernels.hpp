@@ -174,7 +174,7 @@ struct AttnBwdArgs {
     // stores its dS tiles there and dQ becomes one batched GEMM dS^T . K_hat (which & 2).
     __nv_bfloat16* ds = nullptr;
     int ds_ld = 0;
-    int ring[4] = {0, 0, 0, 0};  // forced ring plan (nst1, nst2, nab, kb1), 0 = automatic
+    int ring[5] = {0, 0, 0, 0, 0};  // forced ring plan (nst1, nst2, nab, kb1, slice rows), 0 = automatic
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both

@@ -115,7 +115,8 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_BWD_DS")) t.bwd_ds = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("FIPA_F32_TC")) t.f32_tc = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_BWD_RING"))
-        std::sscanf(e, "%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3]);
+        std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
+                    &t.bwd_ring[4]);
     if (const char* e = std::getenv("FIPA_PASS_RING"))
         std::sscanf(e, "%d,%d,%d,%d", &t.pass_ring[0], &t.pass_ring[1], &t.pass_ring[2], &t.pass_ring[3]);
     return t;
@@ -1073,7 +1074,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         a.acc_ld = kAccLd;
         a.B = int(B);
         a.L = int(L);
-        for (int i = 0; i < 4; ++i) a.ring[i] = tuning_.bwd_ring[i];
+        for (int i = 0; i < 5; ++i) a.ring[i] = tuning_.bwd_ring[i];
         if (shard != nullptr) {  // local queries against all G shards' keys; partial dK / dV
             a.khat = static_cast<const __nv_bfloat16*>(shard->k_all);
             a.vhat = static_cast<const __nv_bfloat16*>(shard->v_all);

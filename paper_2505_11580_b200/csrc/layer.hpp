@@ -65,7 +65,7 @@ struct Tuning {
     bool fused_pack = true;       // FIPA_FUSED_PACK = 0: projection GEMM + separate pack kernel
     int bwd_ds = -1;              // FIPA_BWD_DS: -1 automatic (L <= 2048 and dS <= 1 GiB), 0 off,
                                   // 1 on (within the same cap)
-    int bwd_ring[4] = {0, 0, 0, 0};   // FIPA_BWD_RING  "nst1,nst2,nab,kb1" (0 = automatic)
+    int bwd_ring[5] = {0, 0, 0, 0, 0};  // FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]" (0 = automatic)
     int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
     bool f32_tc = true;           // FIPA_F32_TC = 0: fp32 path on CUDA cores (SIMT reference kernels)
     static Tuning from_env();
