@@ -609,14 +609,15 @@ void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     if (ring != nullptr)
         for (int i = 0; i < 5; ++i) forced[i] = ring[i];
     // (B1 stages, B2 stages, exchange buffers, kb1, B2 slice rows), preferred first.  Measured
-    // (B=8 L=1024, same box): dK/dV kernel (1,6,2,-,16) 0.392 ms vs (1,4,3,-,16) 0.397; dQ kernel
-    // (1,4,3,-,16) 0.349 vs (2,6,2,-,16) 0.358.  (kb1 = 0: whole-tile B1 stages)
+    // (B=8 L=1024, same box, tools/bwd_ab.py): dK/dV kernel (1,3,2,-,32) 0.385 ms vs (1,6,2,-,16)
+    // 0.395 vs (1,4,3,-,16) 0.397; dQ kernel (1,2,3,-,32) 0.336 vs (1,4,3,-,16) 0.349 vs
+    // (2,6,2,-,16) 0.358.  (kb1 = 0: whole-tile B1 stages)
     const int plans_kv[][5] = {{1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
                                {2, 2, 2, 0, 16}, {1, 4, 3, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
                                {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
-    const int plans_q[][5] = {{1, 4, 3, 0, 16}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
-                              {2, 2, 2, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16}, {1, 3, 2, 0, 32},
-                              {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
+    const int plans_q[][5] = {{1, 2, 3, 0, 32}, {1, 4, 3, 0, 16}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16},
+                              {2, 3, 2, 0, 16}, {2, 2, 2, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
+                              {1, 3, 2, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
     const auto& plans = kv ? plans_kv : plans_q;
     for (int pass = 0; pass < 2; ++pass) {
         for (const auto& pl : plans) {
