@@ -61,50 +61,33 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-// Persistent blocks walk residues (b, i) = blockIdx.x, += gridDim.x; warp w handles heads w, w+8,
-// ...  The residue's dfeat row and its H saved O_hat rows arrive by bulk copies into one of two
-// buffers: the copy for the NEXT residue is issued before the current one is processed, so the
-// HBM latency overlaps the arithmetic (one block per residue had ~4 residues in flight per SM and
-// ran at ~35% of HBM bandwidth).  dO_hat rows go straight to global (16-byte stores); cross-head
-// sums (dz1, frames) go through per-warp slices.
-__global__ void __launch_bounds__(256, 3) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
+// One block per residue (b, i), warp w handles heads w, w+8, ...  The residue's dfeat row and the
+// H saved O_hat rows arrive by bulk copies; dO_hat rows are assembled in shared memory and
+// written with 16-byte stores; cross-head sums (dz1, frames) go through per-warp slices.
+__global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z, Nv = d.n_value;
     const int nw = blockDim.x >> 5;
-    const int buf_floats = d.feat_ld / 2 + H * d.dv_pad;  // dfeat row (bf16) | H O_hat rows (f32)
-    float* s_buf = sm;                              // 2 x buf_floats
-    float* s_z1 = s_buf + 2 * buf_floats;           // rdz
+    __nv_bfloat16* s_df = reinterpret_cast<__nv_bfloat16*>(sm);  // feat_ld   dfeat row (bf16)
+    float* s_o = sm + d.feat_ld / 2;                // H x dv_pad  O_hat rows (feat_ld % 8 == 0)
+    float* s_z1 = s_o + H * d.dv_pad;               // rdz
     float* s_pair = s_z1 + ((rdz + 3) & ~3);        // nw x rdz   per-warp dz1 partials
     float* s_geo = s_pair + nw * rdz;               // nw x 12    per-warp dR (9) | dt (3)
     float* s_dopt = s_geo + nw * 12;                // nw x 3*Nv
     __nv_bfloat16* s_out = reinterpret_cast<__nv_bfloat16*>(
         (reinterpret_cast<uintptr_t>(s_dopt + nw * 3 * Nv) + 15) & ~uintptr_t(15));  // H x dv_pad
-    uint64_t* bar = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(s_out + H * d.dv_pad) + 15) & ~uintptr_t(15));  // [2]
-    const int64_t BL = static_cast<int64_t>(a.B) * a.L;
-    const uint32_t df_bytes = d.feat_ld * 2, o_bytes = d.dv_pad * 4;
-    auto issue = [&](int64_t r, int k) {  // thread 0: bulk copies of residue r into buffer k
-        float* bb = s_buf + k * buf_floats;
-        ptx::fence_proxy_async_smem();  // the buffer's previous generic reads precede the async writes
-        ptx::mbar_expect_tx(&bar[k], df_bytes + H * o_bytes);
-        bulk_g2s(bb, a.dfeat + r * d.feat_ld, df_bytes, &bar[k]);
-        bulk_g2s(bb + d.feat_ld / 2, a.ohat + r * H * d.dv_pad, H * o_bytes, &bar[k]);  // residue-major O_hat
-    };
-    if (threadIdx.x == 0) {
-        ptx::mbar_init(&bar[0], 1);
-        ptx::mbar_init(&bar[1], 1);
-        ptx::fence_mbar_init();
-        if (static_cast<int64_t>(blockIdx.x) < BL) issue(blockIdx.x, 0);
-    }
-    __syncthreads();
-    int it = 0;
-    for (int64_t row = blockIdx.x; row < BL; row += gridDim.x, ++it) {
-    const int kb = it & 1;
-    if (threadIdx.x == 0 && row + gridDim.x < BL) issue(row + gridDim.x, kb ^ 1);  // prefetch the next residue
-    const __nv_bfloat16* s_df = reinterpret_cast<const __nv_bfloat16*>(s_buf + kb * buf_floats);
-    const float* s_o = s_buf + kb * buf_floats + d.feat_ld / 2;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_out + H * d.dv_pad);
+    const int64_t row = blockIdx.x;
     const int b = static_cast<int>(row / a.L), i = static_cast<int>(row % a.L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::fence_mbar_init();
+        const uint32_t df_bytes = d.feat_ld * 2, o_bytes = d.dv_pad * 4;
+        ptx::mbar_expect_tx(bar, df_bytes + H * o_bytes);
+        bulk_g2s(s_df, a.dfeat + row * d.feat_ld, df_bytes, bar);
+        bulk_g2s(s_o, a.ohat + row * H * d.dv_pad, H * o_bytes, bar);  // residue-major O_hat rows
+    }
     for (int e = threadIdx.x; e < rdz; e += blockDim.x) s_z1[e] = a.z1[row * rdz + e];
     // s_pair needs no clearing when every warp owns exactly one head (its slice is overwritten)
     const bool one_head = H <= nw;
@@ -116,7 +99,7 @@ __global__ void __launch_bounds__(256, 3) bwd_prep_kernel(LayerDims d, BwdPrepAr
 #pragma unroll
     for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
     __syncthreads();
-    ptx::mbar_wait(&bar[kb], (it >> 1) & 1);
+    ptx::mbar_wait(bar, 0);
 
     const int vpair = c + rdz, vpts = vpair + 6, vend = vpts + 3 * Nv;
     float* dopt_s = s_dopt + warp * 3 * Nv;
@@ -255,8 +238,6 @@ __global__ void __launch_bounds__(256, 3) bwd_prep_kernel(LayerDims d, BwdPrepAr
         for (int w = 0; w < nw; ++w) acc += s_geo[w * 12 + threadIdx.x];
         a.geo_epi[row * 12 + threadIdx.x] = acc;
     }
-    __syncthreads();  // buffers and scratch free for the next residue
-    }  // residues
 }
 
 constexpr int kUnpackRows = 8;
@@ -721,15 +702,11 @@ void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stre
     const int rdz = d.rank * d.d_z;
     if (d.feat_ld % 8 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
         throw std::invalid_argument("bwd_prep: row strides must be multiples of 16 bytes");
-    const size_t smem = sizeof(float) * (2 * (d.feat_ld / 2 + d.heads * d.dv_pad) + ((rdz + 3) & ~3) +
+    const size_t smem = sizeof(float) * (d.feat_ld + d.heads * d.dv_pad + ((rdz + 3) & ~3) +
                                          8 * (rdz + 12 + 3 * d.n_value)) +
-                        16 + 2 * size_t(d.heads) * d.dv_pad + 16 + 2 * sizeof(uint64_t) + 16;
+                        16 + 2 * size_t(d.heads) * d.dv_pad + 16;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    const int64_t BL = int64_t(a.B) * a.L;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bwd_prep_kernel, 256, smem);
-    const int64_t grid = std::min<int64_t>(BL, int64_t(device_sm_count()) * std::max(1, per_sm));
-    bwd_prep_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(d, a);
+    bwd_prep_kernel<<<static_cast<unsigned>(int64_t(a.B) * a.L), 256, smem, stream>>>(d, a);
 }
 
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
