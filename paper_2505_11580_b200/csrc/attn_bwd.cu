@@ -50,7 +50,7 @@ namespace {
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
 constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
-constexpr int kMaxStages1 = 3;  // B1 ring: whole 32-row tile halves, or groups of KB1 column blocks
+constexpr int kMaxStages1 = 6;  // B1 ring: whole 32-row tile halves, or groups of KB1 column blocks
 constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
 // B2 slices of 16 or 32 rows (template SL): TMA throughput per SM grows with the box size
 // (profiles/r1_tma_microbench.txt: 2 KB boxes ~20 B/clk, 4 KB ~40 B/clk), so 32-row slices halve
@@ -609,15 +609,20 @@ void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     if (ring != nullptr)
         for (int i = 0; i < 5; ++i) forced[i] = ring[i];
     // (B1 stages, B2 stages, exchange buffers, kb1, B2 slice rows), preferred first.  Measured
-    // (B=8 L=1024, same box, tools/bwd_ab.py): dK/dV kernel (1,3,2,-,32) 0.385 ms vs (1,6,2,-,16)
-    // 0.395 vs (1,4,3,-,16) 0.397; dQ kernel (1,2,3,-,32) 0.336 vs (1,4,3,-,16) 0.349 vs
-    // (2,6,2,-,16) 0.358.  (kb1 = 0: whole-tile B1 stages)
-    const int plans_kv[][5] = {{1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
+    // (B=8 L=1024, same box, tools/bwd_ab.py): dK/dV kernel (3,2,2,4,32) 0.369 ms vs (2,3,2,4,32)
+    // 0.373 vs (4,2,2,3,32) 0.378 vs (1,3,2,0,32) 0.385 vs (1,6,2,0,16) 0.395 vs (6,2,2,2,32) 0.400;
+    // dQ kernel (1,2,3,0,32) 0.336 vs (1,4,3,0,16) 0.349 vs (2,6,2,0,16) 0.358.  The trace
+    // (tools/attn_bwd_trace.cu) shows the critical loop MMA1(j) -> B1(j+1) TMA (~1.4k cycles under
+    // load) -> MMA1(j+1): B1 in 4-block groups over 3 stages lets the next tile's first group land
+    // while MMA1(j) runs.  (kb1 = 0: whole-tile B1 stages)
+    const int plans_kv[][5] = {{3, 2, 2, 4, 32}, {1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
                                {2, 2, 2, 0, 16}, {1, 4, 3, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
-                               {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
+                               {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}, {3, 2, 2, 4, 32},
+                               {2, 3, 2, 4, 32}, {4, 2, 2, 3, 32}, {6, 2, 2, 2, 32}, {4, 4, 2, 3, 16}};
     const int plans_q[][5] = {{1, 2, 3, 0, 32}, {1, 4, 3, 0, 16}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16},
                               {2, 3, 2, 0, 16}, {2, 2, 2, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
-                              {1, 3, 2, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}};
+                              {1, 3, 2, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}, {3, 2, 2, 4, 32},
+                              {2, 3, 2, 4, 32}, {4, 2, 2, 3, 32}, {6, 2, 2, 2, 32}, {4, 4, 2, 3, 16}};
     const auto& plans = kv ? plans_kv : plans_q;
     for (int pass = 0; pass < 2; ++pass) {
         for (const auto& pl : plans) {
@@ -656,12 +661,18 @@ template <bool KV>
 void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
             cudaStream_t stream) {
     if (p.slice == 32) {
-        if (p.nab == 3) launch_depth<KV, 1, 2, 3, 0, 32>(d, a, p, maps, stream);
+        if (p.kb1 == 4 && p.nst1 == 3) launch_depth<KV, 3, 2, 2, 4, 32>(d, a, p, maps, stream);
+        else if (p.kb1 == 3 && p.nst1 == 4) launch_depth<KV, 4, 2, 2, 3, 32>(d, a, p, maps, stream);
+        else if (p.kb1 == 2 && p.nst1 == 6) launch_depth<KV, 6, 2, 2, 2, 32>(d, a, p, maps, stream);
+        else if (p.kb1 == 4 && p.nst1 == 2) launch_depth<KV, 2, 3, 2, 4, 32>(d, a, p, maps, stream);
+        else if (p.nab == 3) launch_depth<KV, 1, 2, 3, 0, 32>(d, a, p, maps, stream);
         else if (p.nst1 == 2 && p.nst2 == 3) launch_depth<KV, 2, 3, 2, 0, 32>(d, a, p, maps, stream);
         else if (p.nst1 == 2) launch_depth<KV, 2, 2, 2, 0, 32>(d, a, p, maps, stream);
         else launch_depth<KV, 1, 3, 2, 0, 32>(d, a, p, maps, stream);
     } else if (p.kb1 == 4 && p.nst1 == 3) {
         launch_depth<KV, 3, 4, 2, 4>(d, a, p, maps, stream);
+    } else if (p.kb1 == 3 && p.nst1 == 4) {
+        launch_depth<KV, 4, 4, 2, 3>(d, a, p, maps, stream);
     } else if (p.nab == 3) {
         if (p.nst2 == 4) launch_depth<KV, 1, 4, 3>(d, a, p, maps, stream);
         else launch_depth<KV, 1, 6, 3>(d, a, p, maps, stream);

@@ -34,6 +34,11 @@ int main(int argc, char** argv) {
     cudaMemcpy(lse, hl.data(), BH * L * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(D, hl.data(), BH * L * 4, cudaMemcpyHostToDevice);
     AttnBwdArgs a{q, k, v, dO, lse, D, acc, acc + BH * L * 448, acc + 2 * BH * L * 448, 448, B, L};
+    if (argc > 4 && atoi(argv[4]) == 1) {  // materialised dS (the default path at L <= 2048)
+        a.ds_ld = (L + 63) / 64 * 64;
+        cudaMalloc(&a.ds, BH * L * size_t(a.ds_ld) * 2);
+    }
+    if (argc > 5) sscanf(argv[5], "%d,%d,%d,%d,%d", &a.ring[0], &a.ring[1], &a.ring[2], &a.ring[3], &a.ring[4]);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -52,11 +57,12 @@ int main(int argc, char** argv) {
     auto T = [&](int cta, int w, int ev, int j) { return t[((cta * 12 + w) * 16 + ev) * 64 + j]; };
     const long long t0 = T(0, 1, 0, 0);
     const int nt = (L + 63) / 64;
+    const int spt = (argc > 5 && a.ring[4] == 16) ? 4 : 2;  // B2 slices per tile
     for (int cta : {0, 2}) {
-        printf("leader cta%d: tile xfree_ok mma1_issue a_full_ok(mma2 issue) b2_last_full | b1_issue b2_issue(4j)\n", cta);
+        printf("leader cta%d: tile xfree_ok mma1_issue a_full_ok(mma2 issue) b2_last_full | b1_issue b2_issue(first slice of tile j)\n", cta);
         for (int j = 0; j < nt && j < 64; ++j)
             printf("  %3d %8lld %8lld %8lld %8lld | %8lld %8lld\n", j, T(cta,1,2,j)-t0, T(cta,1,0,j)-t0, T(cta,1,1,j)-t0,
-                   T(cta,1,13,j)-t0, T(cta,0,11,j)-t0, T(cta,10,12,4*j)-t0);
+                   T(cta,1,13,j)-t0, T(cta,0,11,j)-t0, T(cta,10,12,spt*j)-t0);
     }
     printf("P cta0 w2: tile x_full p_done mma2done_ok pin_free_ok\n");
     for (int j = 0; j < nt && j < 64; ++j)
