@@ -335,12 +335,16 @@ int fipa_layer_forward_launches(const fipa_layer* layer);
  *   bwd_slice  its B2 slice rows (16 / 32, 0 = any) (FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]")
  *   pass_ring  two-pass attention rings {kb, kst, vkeys, vst}, zeros = automatic (FIPA_PASS_RING)
  *   f32_tc     1: FIPA_PREC_F32/F64 run on the tensor cores (3xTF32 projections, attention and
- *              output projection); 0: the fp32 CUDA-core kernels (FIPA_F32_TC=0) */
+ *              output projection); 0: the fp32 CUDA-core kernels (FIPA_F32_TC=0)
+ *   graphs     1: the device entry points (forward, training forward, backward) replay a CUDA graph
+ *              captured on their first call with the same shapes and buffers; 0: kernel-by-kernel
+ *              launches (FIPA_GRAPHS=0) */
 typedef struct fipa_tuning {
     int32_t attn_impl, fused_pack, bwd_ds;
     int32_t bwd_ring[4], pass_ring[4];
     int32_t f32_tc;
     int32_t bwd_slice;
+    int32_t graphs;
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

@@ -623,9 +623,11 @@ void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
                               {2, 3, 2, 0, 16}, {2, 2, 2, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
                               {1, 3, 2, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}, {3, 2, 2, 4, 32},
                               {2, 3, 2, 4, 32}, {4, 2, 2, 3, 32}, {6, 2, 2, 2, 32}, {4, 4, 2, 3, 16}};
-    const auto& plans = kv ? plans_kv : plans_q;
+    const int(*plans)[5] = kv ? plans_kv : plans_q;
+    const int nplans = kv ? int(sizeof(plans_kv) / sizeof(plans_kv[0])) : int(sizeof(plans_q) / sizeof(plans_q[0]));
     for (int pass = 0; pass < 2; ++pass) {
-        for (const auto& pl : plans) {
+        for (int pi = 0; pi < nplans; ++pi) {
+            const int* pl = plans[pi];
             if (pass == 0 && forced[0] > 0 &&
                 (pl[0] != forced[0] || pl[1] != forced[1] || pl[2] != forced[2] || pl[3] != forced[3] ||
                  (forced[4] > 0 && pl[4] != forced[4])))

@@ -341,7 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qi = q0 + row;
         const bool ok = qi < p.L;
         if (ok) p.lse[static_cast<int64_t>(bh) * p.L + qi] = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
-        // all MMAs are done: the Q/K ring is free for the fp32 feature staging [128][seg | 1]
+        // all MMAs are done: the operand rings are free for the fp32 feature staging [128][seg | 1]
+        // (the barrier makes every softmax thread's last P store precede the staging writes without
+        // relying on the o_full chain alone)
+        named_bar_sync(1, 128);
         const int sst = p.seg | 1;
         float* frow = reinterpret_cast<float*>(smem) + row * sst;
         const int H = p.H, b = bh / H, h = bh - b * H;

@@ -376,6 +376,7 @@ int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
         out->bwd_ds = t.bwd_ds;
         out->f32_tc = t.f32_tc ? 1 : 0;
         out->bwd_slice = t.bwd_ring[4];
+        out->graphs = t.graphs ? 1 : 0;
         for (int i = 0; i < 4; ++i) {
             out->bwd_ring[i] = t.bwd_ring[i];
             out->pass_ring[i] = t.pass_ring[i];
@@ -394,6 +395,7 @@ int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in) {
         t.bwd_ds = in->bwd_ds;
         t.f32_tc = in->f32_tc != 0;
         t.bwd_ring[4] = in->bwd_slice;
+        t.graphs = in->graphs != 0;
         for (int i = 0; i < 4; ++i) {
             t.bwd_ring[i] = in->bwd_ring[i];
             t.pass_ring[i] = in->pass_ring[i];

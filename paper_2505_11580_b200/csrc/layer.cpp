@@ -10,6 +10,7 @@
 #include <cstring>
 #include <fstream>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <numbers>
 #include <sstream>
@@ -114,6 +115,7 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_FUSED_PACK")) t.fused_pack = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_BWD_DS")) t.bwd_ds = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("FIPA_F32_TC")) t.f32_tc = std::string(e) != "0";
+    if (const char* e = std::getenv("FIPA_GRAPHS")) t.graphs = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
                     &t.bwd_ring[4]);
@@ -379,6 +381,8 @@ FlashIpaLayer::FlashIpaLayer(const Config& cfg) : cfg_(cfg) {
 FlashIpaLayer::~FlashIpaLayer() {
     release_device();
     release_host_pipe();
+    clear_graphs();
+    if (capture_stream_) cudaStreamDestroy(capture_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : evb_)
@@ -423,6 +427,7 @@ void FlashIpaLayer::load(const std::string& path) {
 // (w_q | w_k | w_v | w_qp | w_kp | w_vp), output projection, per-head scalars.
 void FlashIpaLayer::upload_weights() {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    clear_graphs();  // captured graphs hold the old device weight pointers
     release_device();
     const LayerDims& d = dims_;
     const std::size_t din = cfg_.d_in, np = d.n_proj, feat = d.feat, H = cfg_.heads;
@@ -651,11 +656,88 @@ std::vector<float> FlashIpaLayer::stage_times() const {
     return out;
 }
 
+bool FlashIpaLayer::GraphKey::operator<(const GraphKey& o) const {
+    return std::tie(kind, B, L, ptrs, ws_bytes) < std::tie(o.kind, o.B, o.L, o.ptrs, o.ws_bytes);
+}
+
+void FlashIpaLayer::clear_graphs() {
+    std::lock_guard<std::mutex> lk(graph_mu_);
+    for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+    graphs_.clear();
+    graph_order_.clear();
+}
+
+// Replays the graph captured for `key` on `stream` (capturing it first); false when graphs do not
+// apply (then the caller launches kernel by kernel).
+template <class F>
+bool FlashIpaLayer::run_graph(const GraphKey& key, cudaStream_t stream, F&& launch) {
+    if (!tuning_.graphs || timing_) return false;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return false;  // the caller is capturing its own graph: launch into it directly
+    }
+    std::lock_guard<std::mutex> lk(graph_mu_);
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+        if (!capture_stream_)
+            cuda_check(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            launch(capture_stream_);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(capture_stream_, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            throw;
+        }
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamEndCapture(capture_stream_, &graph), "end capture");
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(e, "graph instantiate");
+        if (graph_order_.size() >= 32) {  // bounded cache: drop the oldest
+            auto old = graphs_.find(graph_order_.front());
+            if (old != graphs_.end()) {
+                cudaGraphExecDestroy(old->second);
+                graphs_.erase(old);
+            }
+            graph_order_.erase(graph_order_.begin());
+        }
+        it = graphs_.emplace(key, exec).first;
+        graph_order_.push_back(key);
+    }
+    cuda_check(cudaGraphLaunch(it->second, stream), "graph launch");
+    return true;
+}
+
 void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, const float* z1,
                             const float* z2, const float* rot, const float* trans,
                             const std::uint8_t* mask, float* out, void* workspace,
                             std::size_t workspace_bytes, cudaStream_t stream, bool train,
                             const ShardStage* shard) {
+    if (shard == nullptr && B >= 1 && L >= 1 && s && z1 && z2 && rot && trans && out && workspace) {
+        cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+        if (dirty_) {
+            std::lock_guard<std::mutex> lk(upload_mu_);
+            if (dirty_) upload_weights();
+        }
+        GraphKey key{train ? 1 : 0, B, L, {s, z1, z2, rot, trans, mask, out, workspace}, workspace_bytes};
+        if (run_graph(key, stream, [&](cudaStream_t cs) {
+                forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train, nullptr);
+            }))
+            return;
+    }
+    forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, stream, train, shard);
+}
+
+void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                 const float* z2, const float* rot, const float* trans,
+                                 const std::uint8_t* mask, float* out, void* workspace,
+                                 std::size_t workspace_bytes, cudaStream_t stream, bool train,
+                                 const ShardStage* shard) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
@@ -964,6 +1046,26 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
                              const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
                              float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
                              std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard) {
+    if (shard == nullptr && !dirty_ && B >= 1 && L >= 1 && s && z1 && z2 && rot && trans && dout && ds && dz1 &&
+        dz2 && dweights && workspace && backward_supported()) {
+        cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+        GraphKey key{2, B, L, {s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace},
+                     workspace_bytes};
+        if (run_graph(key, stream, [&](cudaStream_t cs) {
+                backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
+                              workspace, workspace_bytes, cs, nullptr);
+            }))
+            return;
+    }
+    backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+                  workspace_bytes, stream, shard);
+}
+
+void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                  const float* z2, const float* rot, const float* trans,
+                                  const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
+                                  float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
+                                  std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && dout && ds && dz1 && dz2 && dweights,

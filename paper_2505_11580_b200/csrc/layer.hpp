@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <map>
 #include <cstdint>
 #include <mutex>
 #include <stdexcept>
@@ -68,6 +69,8 @@ struct Tuning {
     int bwd_ring[5] = {0, 0, 0, 0, 0};  // FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]" (0 = automatic)
     int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
     bool f32_tc = true;           // FIPA_F32_TC = 0: fp32 path on CUDA cores (SIMT reference kernels)
+    bool graphs = true;           // FIPA_GRAPHS = 0: launch kernel by kernel instead of replaying a
+                                  // captured CUDA graph per (call kind, shapes, buffers)
     static Tuning from_env();
 };
 
@@ -180,7 +183,7 @@ public:
     // Not thread-safe against concurrent calls on the same layer (like weight mutation).
     void set_tuning(const Tuning& t) {
         tuning_ = t;
-        dirty_ = true;  // the device weight copies depend on the kernel choice
+        dirty_ = true;  // the device weight copies (and captured graphs) depend on the kernel choice
     }
     std::size_t num_weights() const;
     void backward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
@@ -294,6 +297,31 @@ public:
 private:
     void upload_weights();
     void release_device();
+    // CUDA-graph replay of the device entry points (forward / training forward / backward): the
+    // first call with a given (kind, B, L, buffers) captures the launch sequence on a private stream,
+    // later calls replay it on the caller's stream (one launch instead of ~20; no per-kernel host
+    // work such as TMA descriptor encoding).  Cleared whenever the device weights are re-uploaded.
+    struct GraphKey {
+        int kind;
+        std::int64_t B, L;
+        std::array<const void*, 16> ptrs;
+        std::size_t ws_bytes;
+        bool operator<(const GraphKey& o) const;
+    };
+    std::map<GraphKey, cudaGraphExec_t> graphs_;
+    std::vector<GraphKey> graph_order_;
+    std::mutex graph_mu_;
+    cudaStream_t capture_stream_ = nullptr;
+    void clear_graphs();
+    template <class F>
+    bool run_graph(const GraphKey& key, cudaStream_t stream, F&& launch);
+    void forward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                      const float* rot, const float* trans, const std::uint8_t* mask, float* out, void* workspace,
+                      std::size_t workspace_bytes, cudaStream_t stream, bool train, const ShardStage* shard);
+    void backward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                       const float* rot, const float* trans, const std::uint8_t* mask, const float* dout, float* ds,
+                       float* dz1, float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
+                       std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard);
 
     Config cfg_;
     LayerDims dims_{};
