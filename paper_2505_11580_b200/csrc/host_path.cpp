@@ -197,7 +197,8 @@ void FlashIpaLayer::release_host_pipe() {
 namespace {
 // Samples per chunk: at least ~2k residues per chunk (smaller batches leave the GPU idle) and,
 // when B allows, four or more chunks so the conversions and copies overlap the kernels.
-std::int64_t chunk_samples(std::int64_t B, std::int64_t L) {
+std::int64_t chunk_samples(std::int64_t B, std::int64_t L, int forced) {
+    if (forced > 0) return std::min<std::int64_t>(B, forced);
     const std::int64_t by_size = std::max<std::int64_t>(1, (2048 + L - 1) / L);
     const std::int64_t by_count = std::max<std::int64_t>(1, B / 4);
     return std::min(B, std::max<std::int64_t>(1, std::min(by_size, by_count)));
@@ -213,7 +214,7 @@ void FlashIpaLayer::host_forward(std::int64_t B, std::int64_t L, const T* s, con
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     HostPipe& hp = host_pipe();
     const std::size_t din = cfg_.d_in, rdz = cfg_.rank * cfg_.d_z;
-    const std::int64_t nb = chunk_samples(B, L);
+    const std::int64_t nb = chunk_samples(B, L, tuning_.host_chunk);
     const std::size_t R = std::size_t(nb) * L;  // residues per chunk (max)
     // slot layout (floats): s | z1 | z2 | rot | trans | out | mask bytes
     const std::size_t o_s = 0, o_z1 = R * din, o_z2 = o_z1 + R * rdz, o_r = o_z2 + R * rdz, o_t = o_r + R * 9,
@@ -278,7 +279,7 @@ void FlashIpaLayer::host_grad(std::int64_t B, std::int64_t L, const T* s, const 
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     HostPipe& hp = host_pipe();
     const std::size_t din = cfg_.d_in, rdz = cfg_.rank * cfg_.d_z, nw = num_weights();
-    const std::int64_t nb = chunk_samples(B, L);
+    const std::int64_t nb = chunk_samples(B, L, tuning_.host_chunk);
     const std::size_t R = std::size_t(nb) * L;
     // slot (floats): inputs s | z1 | z2 | rot | trans | dout, outputs out | ds | dz1 | dz2 | drot | dtrans, mask
     const std::size_t sz_in[6] = {R * din, R * rdz, R * rdz, R * 9, R * 3, R * din};

@@ -116,6 +116,7 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_BWD_DS")) t.bwd_ds = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("FIPA_F32_TC")) t.f32_tc = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_GRAPHS")) t.graphs = std::string(e) != "0";
+    if (const char* e = std::getenv("FIPA_HOST_CHUNK")) t.host_chunk = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
                     &t.bwd_ring[4]);

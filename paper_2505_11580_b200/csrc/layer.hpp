@@ -69,6 +69,7 @@ struct Tuning {
     int bwd_ring[5] = {0, 0, 0, 0, 0};  // FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]" (0 = automatic)
     int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
     bool f32_tc = true;           // FIPA_F32_TC = 0: fp32 path on CUDA cores (SIMT reference kernels)
+    int host_chunk = 0;           // FIPA_HOST_CHUNK: samples per chunk of the host-buffer pipeline (0 = auto)
     bool graphs = true;           // FIPA_GRAPHS = 0: launch kernel by kernel instead of replaying a
                                   // captured CUDA graph per (call kind, shapes, buffers)
     static Tuning from_env();
