@@ -447,12 +447,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int u = 0; u < 2; ++u) {
                         const int k = 2 * cc + u;
                         const float x = __uint_as_float(xr[k]);
-                        // half of the exponentials on the FMA pipe (ptx::ex2_poly), half on the SFU
                         if (KV) {
-                            pv[u] = u ? ptx::ex2_poly(x - cv[k]) : ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
+                            pv[u] = ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
                         } else {
-                            const float e = u ? ptx::ex2_poly(x - row_v) : ptx::ex2(x - row_v);
-                            pv[u] = c0 + k < p.Lcol ? e : 0.f;
+                            pv[u] = c0 + k < p.Lcol ? ptx::ex2(x - row_v) : 0.f;
                         }
                     }
                     pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);

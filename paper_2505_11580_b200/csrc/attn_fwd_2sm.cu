@@ -763,9 +763,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int cc = 0; cc < 16; ++cc) {
-                // half of the exponentials on the SFU, half on the FMA pipe (ptx::ex2_poly)
                 const float p0 = ptx::ex2(x[2 * cc] - mm);
-                const float p1 = ptx::ex2_poly(x[2 * cc + 1] - mm);
+                const float p1 = ptx::ex2(x[2 * cc + 1] - mm);
                 ls[cc & 3] += p0 + p1;
                 pk[cc] = ptx::pack_bf16x2(p0, p1);
             }

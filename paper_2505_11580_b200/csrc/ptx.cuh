@@ -204,20 +204,6 @@ __device__ __forceinline__ uint32_t mapa(const void* local, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// 2^x on the FMA / ALU pipes (x <= 0): x = n + f with n = floor(x) taken from the low mantissa
-// bits of x + 1.5*2^23 (round-down add), 2^f from a cubic minimax polynomial (max relative error
-// 8.6e-5, far below bf16's 3.9e-3), 2^n added to the exponent field.  The softmax kernels compute
-// half of their exponentials this way so the SFU (MUFU.EX2) is not the only pipe doing them.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -125.0f);
-    const float j = __fadd_rd(x, 12582912.0f);
-    const float n = j - 12582912.0f;
-    const float f = x - n;
-    float p = fmaf(0.0770652f, f, 0.227647f);
-    p = fmaf(p, f, 0.69511634f);
-    p = fmaf(p, f, 1.0f);
-    return __int_as_float(__float_as_int(p) + ((__float_as_int(j) - 0x4B400000) << 23));
-}
 // Remote arrive with the default (CTA-scope release) semantics -- the CUTLASS ClusterBarrier
 // form; paired with fence.proxy.async it hands shared-memory operands to the peer's MMA without
 // the GPU-scope membar that .release.cluster compiles to.
