@@ -106,6 +106,7 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.b1 = l.abuf + p.nab * BM * 128;  // P (P pair) / received-P-then-dS (dS pair) exchange buffers
     l.b2 = l.b1 + p.nst1 * p.b1_stage;
     l.bars = l.b2 + p.nst2 * p.b2_stage;
+    if (l.bars < 8 * 8192) l.bars = 8 * 8192;  // the epilogue's staging boxes (8 warps x 8 KB) from offset 0
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
 }
@@ -118,7 +119,26 @@ __device__ long long g_bwd_trace[4 * 12 * 16 * 64];  // [cta][warp][event][tile]
         if (blockIdx.x < 4 && blockIdx.y == 0 && (j) < 64)                                               \
             g_bwd_trace[((blockIdx.x * 12 + ptx::warp_id()) * 16 + (ev)) * 64 + (j)] = clock64();        \
     } while (0)
+// Whole-grid spans: globaltimer (ns) of every CTA's start, epilogue start and end, and its SM.
+__device__ unsigned long long g_bwd_span[4 * 65536];
+__device__ __forceinline__ void bwd_span(int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned id = blockIdx.y * gridDim.x + blockIdx.x;
+    if (id < 65536) {
+        g_bwd_span[4 * id + k] = t;
+        if (k == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_bwd_span[4 * id + 3] = sm;
+        }
+    }
+}
+#define BSPAN(k) bwd_span(k)
 #else
+#define BSPAN(k) \
+    do {         \
+    } while (0)
 #define BTRACE(ev, j) \
     do {              \
     } while (0)
@@ -166,7 +186,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
                     const __grid_constant__ CUtensorMap b1D, const __grid_constant__ CUtensorMap b2D,
-                    const __grid_constant__ CUtensorMap mapDS, BwdParams p) {
+                    const __grid_constant__ CUtensorMap mapDS, const __grid_constant__ CUtensorMap accP,
+                    const __grid_constant__ CUtensorMap accD, BwdParams p) {
     constexpr int kSlice = SL, kSliceBox = SL * 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -195,6 +216,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const CUtensorMap* mB2 = role ? &b2D : &b2P;
 
     if (warp == 0 && lane == 0) {
+        BSPAN(0);
         ptx::tma_prefetch(mStat);
         ptx::tma_prefetch(mB1);
         if (has_mma2) ptx::tma_prefetch(mB2);
@@ -542,45 +564,57 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             if (ntiles > 0) ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(ntiles - 1) % NAB], crank - 2u));
         }
         // ------------------------------------------------------------- epilogue
-        float* out = p.acc_out[role];
-        if (has_mma2 && out != nullptr) {
+        // The accumulator rows leave through TMA tensor stores: each warp stages 32 rows x 32
+        // columns (128-byte swizzled, 4 KB, double-buffered in the now idle stationary-tile
+        // region) and stores the box into the rank-major [G][B][chunk][H][acc_ld] accumulator
+        // (5-D map, columns clipped at the role's n2).  Per-thread float4 stores of a row each
+        // (rows 14 KB apart) had left half of every sector unused and ran the epilogue at ~2 TB/s
+        // across the grid (14 us of a 44 us CTA lifetime, tools/attn_bwd_trace.cu spans).
+        if (has_mma2 && p.acc_out[role] != nullptr) {
             ptx::mbar_wait(&bars->acc_full, 0);
             ptx::tc_fence_after();
-            const int n16 = rd.n2 / 16;
-            const int lo = half ? (n16 + 1) / 2 : 0, hi = half ? n16 : (n16 + 1) / 2;
-            // residue-major [B, L, H, acc_ld]: the H rows of a residue are contiguous for bwd_unpack
+            if (warp == 2 && lane == 0) BSPAN(1);
+            // staging overwrites the exchange buffers for small widths: warp 2's wait on the last
+            // dS store (above) precedes this barrier
+            named_bar_sync(1, 256);
+            const int n32 = (rd.n2 + 31) / 32;
+            const int lo = half ? (n32 + 1) / 2 : 0, hi = half ? n32 : (n32 + 1) / 2;
             const int bb = bh / p.H, hh = bh - bb * p.H;
-            // rank-major [G][B][chunk][H][acc_ld] (G = 1 unsharded: residue-major [B, L, H, acc_ld])
-            const int rr = grow < p.Lrow ? grow : 0;
-            const int g = rr / p.stat_chunk, gi = rr - g * p.stat_chunk;
-            float* orow = out + (((static_cast<int64_t>(g) * p.B + bb) * p.stat_chunk + gi) * p.H + hh) * p.acc_ld +
-                          p.acc_col0[role];
-            // four TMEM loads in flight per wait (one round trip costs ~0.5k cycles)
-            for (int ch0 = lo; ch0 < hi; ch0 += 4) {
-                uint32_t o[4][16];
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (ch0 + k < hi) ptx::tmem_ld16(tl + 16 * (ch0 + k), o[k]);
+            const int wrow0 = r0 + quad * 32;  // first row of this warp's boxes
+            const bool store_rows = wrow0 < p.Lrow;
+            const int g = store_rows ? wrow0 / p.stat_chunk : 0, gi = wrow0 - g * p.stat_chunk;
+            uint8_t* stage = smem + sw * 8192;  // two 4 KB boxes per warp
+            const CUtensorMap* mAcc = role ? &accD : &accP;
+            for (int cb = lo; cb < hi; ++cb) {
+                const int nb = (cb - lo) & 1;
+                uint8_t* box = stage + nb * 4096;
+                uint32_t o[2][16];
+                ptx::tmem_ld16(tl + 32 * cb, o[0]);
+                ptx::tmem_ld16(tl + 32 * cb + 16, o[1]);
                 ptx::tmem_wait_ld();
-                if (grow < p.Lrow) {
+                if (cb - lo >= 2 && lane == 0) ptx::bulk_wait_group_read<1>();  // box nb's previous store read
+                __syncwarp();
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (ch0 + k < hi) {
-                            float4* dst = reinterpret_cast<float4*>(orow + 16 * (ch0 + k));
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                dst[q] = make_float4(__uint_as_float(o[k][4 * q]), __uint_as_float(o[k][4 * q + 1]),
-                                                     __uint_as_float(o[k][4 * q + 2]), __uint_as_float(o[k][4 * q + 3]));
-                        }
-                    }
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t* w = &o[k >> 2][(k & 3) * 4];
+                    *reinterpret_cast<uint4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && store_rows) {
+                    ptx::tma_store_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
+                    ptx::bulk_commit_group();
                 }
             }
+            if (lane == 0) ptx::bulk_wait_group_read<0>();
         }
     }
 
     ptx::tc_fence_before();
     ptx::cluster_sync();
     if (warp == 1) ptx::tmem_dealloc_2sm(tmem, 512);
+    if (warp == 0 && lane == 0) BSPAN(2);
 }
 
 RoleDims make_role(int k1, int n2) {
@@ -656,7 +690,8 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int clusters = (p.Lrow + 255) / 256;
     dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
-    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
+    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
+                                           maps[8], p);
 }
 
 template <bool KV>
@@ -702,6 +737,16 @@ bool attn_bwd_supported(const LayerDims& d) {
         return false;
     }
     return smem_layout(p).total + 1024 <= 232448;
+}
+
+// Accumulator output map for one role: rank-major [G][B][chunk][H][acc_ld] fp32 from column col0,
+// n2 columns wide (clipped), boxes of 32 columns x 32 rows.
+CUtensorMap acc_map(float* out, int col0, int n2, int H, int chunk, int B, int G, int acc_ld) {
+    const uint64_t row = uint64_t(acc_ld) * 4;
+    const uint64_t dims[5] = {uint64_t(n2), uint64_t(H), uint64_t(chunk), uint64_t(B), uint64_t(G)};
+    const uint64_t strides[4] = {row, row * H, row * H * chunk, row * H * chunk * B};
+    const uint32_t box[5] = {32, 1, 32, 1, 1};
+    return make_map_5d_f32_strided(out + col0, dims, strides, box);
 }
 
 void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream, int which) {
@@ -751,9 +796,11 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < a.L))
             throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= L, % 8");
         const CUtensorMap m0 = stat(a.khat, nqk);
-        const CUtensorMap maps[7] = {m0, tile(a.qhat, p.kb1), slice(a.dohat, p.slice),
-                                     stat(a.vhat, nv),  tile(a.dohat, p.kb1), slice(a.qhat, p.slice),
-                                     p.ds_store ? make_map_3d_bf16(a.ds, a.L, a.L, BH, a.ds_ld, 64, BM) : m0};
+        const CUtensorMap maps[9] = {
+            m0, tile(a.qhat, p.kb1), slice(a.dohat, p.slice), stat(a.vhat, nv), tile(a.dohat, p.kb1),
+            slice(a.qhat, p.slice), p.ds_store ? make_map_3d_bf16(a.ds, a.L, a.L, BH, a.ds_ld, 64, BM) : m0,
+            a.dv_acc ? acc_map(a.dv_acc, 0, p.role[0].n2, d.heads, kc, a.B, G, a.acc_ld) : m0,
+            a.dk_acc ? acc_map(a.dk_acc, 0, p.role[1].n2, d.heads, kc, a.B, G, a.acc_ld) : m0};
         launch<true>(d, a, p, maps, stream);
     }
     if ((which & 2) && a.ds != nullptr) {
@@ -806,8 +853,10 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
         const CUtensorMap q0map = stat(a.qhat, nqk);
-        const CUtensorMap maps[7] = {q0map, tile(a.khat, p.kb1), slice(a.khat, p.slice),
-                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat, p.slice), q0map};
+        const CUtensorMap maps[9] = {q0map, tile(a.khat, p.kb1), slice(a.khat, p.slice),
+                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat, p.slice), q0map,
+                                     acc_map(a.dq_acc, 0, nq0, d.heads, a.L, a.B, 1, a.acc_ld),
+                                     acc_map(a.dq_acc, nq0, d.dqk_mma - nq0, d.heads, a.L, a.B, 1, a.acc_ld)};
         launch<false>(d, a, p, maps, stream);
     }
 }
