@@ -240,6 +240,134 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
     }
 }
 
+// Compile-time-shaped prep (c = d_z = 128, rank 1-2, 12 value points: every BASELINE training
+// config): one WARP per residue looping over its heads, lanes across columns.  The generic kernel
+// above (block per residue, warp per head, runtime-shaped loops) ran issue bound -- 9.1k warp
+// instructions per residue, a third of them index arithmetic, plus per-head cross-warp reductions
+// through shared memory (ncu: 74% issue slots busy, DRAM 28%).  Here the pair-factor row z1, the
+// dz1 partial sums and the frame gradient stay in registers across the heads, every global access
+// is a coalesced 8/16-byte lane access, and the only cross-lane work per head is D (one warp sum)
+// and the translation-column sum of the point gradients.
+template <int C, int DZ, int RANK, int NV, int DVPAD>
+__global__ void __launch_bounds__(256, 3) bwd_prep_warp_kernel(LayerDims d, BwdPrepArgs a) {
+    constexpr int RDZ = RANK * DZ, VPAIR = C + RDZ, VPTS = VPAIR + 6, VEND = VPTS + 3 * NV, TAIL = DVPAD - VPAIR;
+    constexpr int SEG = DZ + C + 4 * NV;
+    static_assert(C % 128 == 0 && DZ % 128 == 0 && TAIL % 64 == 0 && VEND <= DVPAD && NV <= 32, "prep shape");
+    __shared__ float s_pt[8][3 * NV];  // per-warp point gradients of the current head
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = int64_t(blockIdx.x) * 8 + warp;
+    if (row >= int64_t(a.B) * a.L) return;  // no block-level synchronisation below
+    const int b = static_cast<int>(row / a.L), i = static_cast<int>(row - int64_t(b) * a.L);
+    const int H = d.heads;
+    float R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(a.rot + row * 9 + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = __ldg(a.trans_c + row * 3 + k);
+    float4 z1v[RDZ / 128], dz1[RDZ / 128];
+#pragma unroll
+    for (int k = 0; k < RDZ / 128; ++k) {
+        z1v[k] = __ldg(reinterpret_cast<const float4*>(a.z1 + row * RDZ + 128 * k) + lane);
+        dz1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float dR[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, dt[3] = {0.f, 0.f, 0.f};
+    float* spt = s_pt[warp];
+#pragma unroll 1
+    for (int h = 0; h < H; ++h) {
+        const float* o = a.ohat + (row * H + h) * DVPAD;
+        const __nv_bfloat16* df = a.dfeat + row * d.feat_ld + h * SEG;
+        // all of the head's loads first (one memory latency per head)
+        float4 os[C / 128], op[RDZ / 128], dv[C / 128], dp[DZ / 128];
+        float2 ot[TAIL / 64];
+#pragma unroll
+        for (int k = 0; k < C / 128; ++k) {
+            os[k] = __ldg(reinterpret_cast<const float4*>(o + 128 * k) + lane);
+            dv[k] = ld4_bf16(df + DZ + 128 * k + 4 * lane);
+        }
+#pragma unroll
+        for (int k = 0; k < RDZ / 128; ++k) op[k] = __ldg(reinterpret_cast<const float4*>(o + C + 128 * k) + lane);
+#pragma unroll
+        for (int k = 0; k < DZ / 128; ++k) dp[k] = ld4_bf16(df + 128 * k + 4 * lane);
+#pragma unroll
+        for (int k = 0; k < TAIL / 64; ++k) ot[k] = __ldg(reinterpret_cast<const float2*>(o + VPAIR + 64 * k) + lane);
+        // value points: lane p < NV.  y = global point - t; loc = R^T y; the feature block holds
+        // loc (3) and |loc| (1) per point; ds = R dl is the gradient of the global point.
+        float ds[3] = {0.f, 0.f, 0.f};
+        if (lane < NV) {
+            const int p = lane;
+            float y[3], loc[3], dl[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) y[x] = __ldg(o + VPTS + 3 * p + x) + __ldg(o + VPAIR + x) + __ldg(o + VPAIR + 3 + x) - t[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) loc[x] = R[x] * y[0] + R[3 + x] * y[1] + R[6 + x] * y[2];
+            const float nrm = sqrtf(loc[0] * loc[0] + loc[1] * loc[1] + loc[2] * loc[2]);
+            const float sc = nrm > 0.f ? __bfloat162float(df[DZ + C + 3 * NV + p]) / nrm : 0.f;
+#pragma unroll
+            for (int x = 0; x < 3; ++x) dl[x] = __bfloat162float(df[DZ + C + 3 * p + x]) + sc * loc[x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                ds[x] = R[3 * x] * dl[0] + R[3 * x + 1] * dl[1] + R[3 * x + 2] * dl[2];
+                spt[3 * p + x] = bfr(ds[x]);
+                dt[x] -= ds[x];
+            }
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                for (int aa = 0; aa < 3; ++aa) dR[3 * bb + aa] += y[bb] * dl[aa];
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x) ds[x] = bfr(warp_sum(ds[x]));  // translation hi and lo columns
+        __syncwarp();
+        __nv_bfloat16* gout = a.dohat + ((int64_t(b) * H + h) * a.L + i) * DVPAD;
+        float Dp = 0.f;
+#pragma unroll
+        for (int k = 0; k < C / 128; ++k) {
+            Dp += dv[k].x * os[k].x + dv[k].y * os[k].y + dv[k].z * os[k].z + dv[k].w * os[k].w;
+            *reinterpret_cast<uint2*>(gout + 128 * k + 4 * lane) =
+                make_uint2(ptx_pack(dv[k].x, dv[k].y), ptx_pack(dv[k].z, dv[k].w));
+        }
+#pragma unroll
+        for (int k = 0; k < RDZ / 128; ++k) {  // pair block rho = k / (DZ / 128): d(pair) repeats per rank
+            const float4 dpc = dp[k % (DZ / 128)], zz = z1v[k], ov = op[k];
+            const float v0 = bfr(zz.x * dpc.x), v1 = bfr(zz.y * dpc.y), v2 = bfr(zz.z * dpc.z), v3 = bfr(zz.w * dpc.w);
+            Dp += v0 * ov.x + v1 * ov.y + v2 * ov.z + v3 * ov.w;
+            dz1[k].x += ov.x * dpc.x;
+            dz1[k].y += ov.y * dpc.y;
+            dz1[k].z += ov.z * dpc.z;
+            dz1[k].w += ov.w * dpc.w;
+            *reinterpret_cast<uint2*>(gout + C + 128 * k + 4 * lane) = make_uint2(ptx_pack(v0, v1), ptx_pack(v2, v3));
+        }
+#pragma unroll
+        for (int k = 0; k < TAIL / 64; ++k) {
+            float v[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int col = VPAIR + 64 * k + 2 * lane + u;
+                const int x = (col - VPAIR) % 3;
+                v[u] = col < VPTS ? (x == 0 ? ds[0] : (x == 1 ? ds[1] : ds[2])) : col < VEND ? spt[col - VPTS] : 0.f;
+            }
+            // padding columns of O_hat are never written: keep them out of D
+            const int col0 = VPAIR + 64 * k + 2 * lane;
+            if (col0 < VEND) Dp += v[0] * ot[k].x;
+            if (col0 + 1 < VEND) Dp += v[1] * ot[k].y;
+            *reinterpret_cast<uint32_t*>(gout + col0) = ptx_pack(v[0], v[1]);
+        }
+        Dp = warp_sum(Dp);
+        if (lane == 0) a.Dvec[(int64_t(b) * H + h) * a.L + i] = Dp;
+        __syncwarp();  // spt reused by the next head
+    }
+#pragma unroll
+    for (int k = 0; k < RDZ / 128; ++k) reinterpret_cast<float4*>(a.dz1_epi + row * RDZ + 128 * k)[lane] = dz1[k];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) dR[k] = warp_sum(dR[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dt[k] = warp_sum(dt[k]);
+    float gv = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) gv = lane == k ? (k < 9 ? dR[k] : dt[k - 9]) : gv;  // no indexed (local) array
+    if (lane < 12) a.geo_epi[row * 12 + lane] = gv;
+}
+
 constexpr int kUnpackRows = 8;
 constexpr int kUnpackMaxH = 16;
 
@@ -700,6 +828,16 @@ __global__ void scale_vec_kernel(const float* in, const float* scale, int period
 
 void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stream) {
     const int rdz = d.rank * d.d_z;
+    const int64_t BL = int64_t(a.B) * a.L;
+    const bool aligned = d.feat_ld % 4 == 0 && d.seg % 4 == 0;
+    if (aligned && d.c == 128 && d.d_z == 128 && d.n_value == 12 && d.rank == 2 && d.dv_pad == 448) {
+        bwd_prep_warp_kernel<128, 128, 2, 12, 448><<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
+        return;
+    }
+    if (aligned && d.c == 128 && d.d_z == 128 && d.n_value == 12 && d.rank == 1 && d.dv_pad == 320) {
+        bwd_prep_warp_kernel<128, 128, 1, 12, 320><<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
+        return;
+    }
     if (d.feat_ld % 8 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
         throw std::invalid_argument("bwd_prep: row strides must be multiples of 16 bytes");
     const size_t smem = sizeof(float) * (d.feat_ld + d.heads * d.dv_pad + ((rdz + 3) & ~3) +
