@@ -345,6 +345,7 @@ typedef struct fipa_tuning {
     int32_t f32_tc;
     int32_t bwd_slice;
     int32_t graphs;
+    int32_t micro; /* bf16 device calls: interleaved sample chunks on forked streams (1 = one chain) */
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

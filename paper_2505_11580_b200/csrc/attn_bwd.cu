@@ -119,26 +119,7 @@ __device__ long long g_bwd_trace[4 * 12 * 16 * 64];  // [cta][warp][event][tile]
         if (blockIdx.x < 4 && blockIdx.y == 0 && (j) < 64)                                               \
             g_bwd_trace[((blockIdx.x * 12 + ptx::warp_id()) * 16 + (ev)) * 64 + (j)] = clock64();        \
     } while (0)
-// Whole-grid spans: globaltimer (ns) of every CTA's start, epilogue start and end, and its SM.
-__device__ unsigned long long g_bwd_span[4 * 65536];
-__device__ __forceinline__ void bwd_span(int k) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned id = blockIdx.y * gridDim.x + blockIdx.x;
-    if (id < 65536) {
-        g_bwd_span[4 * id + k] = t;
-        if (k == 0) {
-            unsigned sm;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            g_bwd_span[4 * id + 3] = sm;
-        }
-    }
-}
-#define BSPAN(k) bwd_span(k)
 #else
-#define BSPAN(k) \
-    do {         \
-    } while (0)
 #define BTRACE(ev, j) \
     do {              \
     } while (0)
@@ -216,7 +197,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const CUtensorMap* mB2 = role ? &b2D : &b2P;
 
     if (warp == 0 && lane == 0) {
-        BSPAN(0);
+        span_mark(0);
         ptx::tma_prefetch(mStat);
         ptx::tma_prefetch(mB1);
         if (has_mma2) ptx::tma_prefetch(mB2);
@@ -573,7 +554,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         if (has_mma2 && p.acc_out[role] != nullptr) {
             ptx::mbar_wait(&bars->acc_full, 0);
             ptx::tc_fence_after();
-            if (warp == 2 && lane == 0) BSPAN(1);
+            if (warp == 2 && lane == 0) span_mark(1);
             // staging overwrites the exchange buffers for small widths: warp 2's wait on the last
             // dS store (above) precedes this barrier
             named_bar_sync(1, 256);
@@ -614,7 +595,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     ptx::cluster_sync();
     if (warp == 1) ptx::tmem_dealloc_2sm(tmem, 512);
-    if (warp == 0 && lane == 0) BSPAN(2);
+    if (warp == 0 && lane == 0) span_mark(2);
 }
 
 RoleDims make_role(int k1, int n2) {

@@ -575,6 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tma_prefetch(&mapF);
             ptx::tma_prefetch(&mapFP);
         }
+        span_mark(0);
         ptx::mbar_init(&bars->q_full, 1);
         for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(&bars->k_full[s], 1);
@@ -823,6 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ptx::mbar_wait(&bars->o_full, 0);
         if (lane == 0) FIPA_TRACE(9, 0);
+        if (warp == 2 && lane == 0) span_mark(1);
         ptx::tc_fence_after();
         const float inv_l = l > 0.f ? 1.0f / l : 0.f;
         const int qi = q0 + row;
@@ -887,6 +889,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     ptx::cluster_sync();
     if (warp == 1) ptx::tmem_dealloc_2sm(tmem, 512);
+    if (warp == 0 && lane == 0) span_mark(2);
 }
 
 }  // namespace

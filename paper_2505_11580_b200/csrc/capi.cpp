@@ -377,6 +377,7 @@ int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
         out->f32_tc = t.f32_tc ? 1 : 0;
         out->bwd_slice = t.bwd_ring[4];
         out->graphs = t.graphs ? 1 : 0;
+        out->micro = t.micro;
         for (int i = 0; i < 4; ++i) {
             out->bwd_ring[i] = t.bwd_ring[i];
             out->pass_ring[i] = t.pass_ring[i];
@@ -389,7 +390,9 @@ int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in) {
         if (layer == nullptr || in == nullptr) throw fipa_b200::ValueError("null layer or tuning");
         if (in->attn_impl < 0 || in->attn_impl > 3) throw fipa_b200::ValueError("tuning: attn_impl must be 0..3");
         if (in->bwd_ds < -1 || in->bwd_ds > 1) throw fipa_b200::ValueError("tuning: bwd_ds must be -1, 0 or 1");
-        fipa_b200::Tuning t;
+        if (in->micro < 1 || in->micro > 4) throw fipa_b200::ValueError("tuning: micro must be 1..4");
+        fipa_b200::Tuning t = L(layer).tuning();  // fields not in fipa_tuning (host_chunk) kept
+        t.micro = in->micro;
         t.attn = static_cast<fipa_b200::Tuning::Attn>(in->attn_impl);
         t.fused_pack = in->fused_pack != 0;
         t.bwd_ds = in->bwd_ds;

@@ -117,6 +117,7 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_F32_TC")) t.f32_tc = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_GRAPHS")) t.graphs = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_HOST_CHUNK")) t.host_chunk = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("FIPA_MICRO")) t.micro = std::min(4, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
                     &t.bwd_ring[4]);
@@ -384,6 +385,11 @@ FlashIpaLayer::~FlashIpaLayer() {
     release_host_pipe();
     clear_graphs();
     if (capture_stream_) cudaStreamDestroy(capture_stream_);
+    for (auto& st : side_streams_)
+        if (st) cudaStreamDestroy(st);
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    for (auto& e : join_ev_)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : evb_)
@@ -583,6 +589,41 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
     return w;
 }
 
+FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b0, std::int64_t L) const {
+    const LayerDims& d = dims_;
+    const std::size_t n = std::size_t(b0) * L, H = d.heads, rdz = std::size_t(d.rank) * d.d_z;
+    const std::size_t el = cfg_.precision == Precision::bf16 ? 2 : 4;
+    auto adv = [](auto* p, std::size_t bytes) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        return p == nullptr ? p : reinterpret_cast<T*>(reinterpret_cast<char*>(p) + bytes);
+    };
+    Workspace v = w;
+    v.trans_c = adv(w.trans_c, n * 3 * 4);
+    v.s_bf16 = adv(w.s_bf16, n * d.din_ld * 2);
+    v.proj = adv(w.proj, n * d.n_proj * 4);
+    v.qhat = adv(static_cast<char*>(w.qhat), n * H * d.dqk_pad * el);
+    v.khat = adv(static_cast<char*>(w.khat), n * H * d.dqk_pad * el);
+    v.vhat = adv(static_cast<char*>(w.vhat), n * H * d.dv_pad * el);
+    v.colbias = adv(w.colbias, n * H * 4);
+    v.lse = adv(w.lse, n * H * 4);
+    v.feat = adv(static_cast<char*>(w.feat), n * d.feat_ld * el);
+    v.o_hat = adv(w.o_hat, n * H * d.dv_pad * 4);
+    v.dout_bf16 = adv(w.dout_bf16, n * d.din_ld * 2);
+    v.dfeat = adv(w.dfeat, n * d.feat_ld * 2);
+    v.do_hat = adv(w.do_hat, n * H * d.dv_pad * 2);
+    v.Dvec = adv(w.Dvec, n * H * 4);
+    v.dq_acc = adv(w.dq_acc, n * H * kAccLd * 4);
+    v.dk_acc = adv(w.dk_acc, n * H * kAccLd * 4);
+    v.dv_acc = adv(w.dv_acc, n * H * kAccLd * 4);
+    v.dproj = adv(w.dproj, n * nproj_ld() * 2);
+    v.dz1_epi = adv(w.dz1_epi, n * rdz * 4);
+    v.geo_epi = adv(w.geo_epi, n * 12 * 4);
+    v.dt_c = adv(w.dt_c, n * 3 * 4);
+    v.dg_rows = adv(w.dg_rows, n * H * 4);
+    v.ds = adv(w.ds, n * H * std::size_t(w.ds_ld) * 2);
+    return v;  // red / dwproj: shared accumulators; the fp32-path planes are not sliced (bf16 only)
+}
+
 bool FlashIpaLayer::f32_tensor_cores() const {
     return cfg_.precision == Precision::f32 && tuning_.f32_tc && attn_fwd_f32tc_supported(dims_);
 }
@@ -727,7 +768,11 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         }
         GraphKey key{train ? 1 : 0, B, L, {s, z1, z2, rot, trans, mask, out, workspace}, workspace_bytes};
         if (run_graph(key, stream, [&](cudaStream_t cs) {
-                forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train, nullptr);
+                if (micro_chunks(B, L) > 1)
+                    forward_micro(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train);
+                else
+                    forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train,
+                                 nullptr);
             }))
             return;
     }
@@ -738,7 +783,7 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
                                  const float* z2, const float* rot, const float* trans,
                                  const std::uint8_t* mask, float* out, void* workspace,
                                  std::size_t workspace_bytes, cudaStream_t stream, bool train,
-                                 const ShardStage* shard) {
+                                 const ShardStage* shard, const Workspace* view) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
@@ -748,8 +793,8 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
             "query-row sharding needs precision='bf16'");
     const bool do_pack = shard == nullptr || shard->stage == 1;
     const bool do_attend = shard == nullptr || shard->stage == 2;
-    const Workspace ws = carve(workspace, B, L, train);
-    REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "workspace too small: need ",
+    const Workspace ws = view ? *view : carve(workspace, B, L, train);
+    REQUIRE(view != nullptr || (workspace != nullptr && workspace_bytes >= ws.bytes), "workspace too small: need ",
             ws.bytes, " bytes, got ", workspace_bytes);
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     if (dirty_) {
@@ -1053,8 +1098,12 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         GraphKey key{2, B, L, {s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace},
                      workspace_bytes};
         if (run_graph(key, stream, [&](cudaStream_t cs) {
-                backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
-                              workspace, workspace_bytes, cs, nullptr);
+                if (micro_chunks(B, L) > 1)
+                    backward_micro(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
+                                   workspace, workspace_bytes, cs);
+                else
+                    backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
+                                  workspace, workspace_bytes, cs, nullptr);
             }))
             return;
     }
@@ -1066,13 +1115,17 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
                                   const float* z2, const float* rot, const float* trans,
                                   const std::uint8_t* mask, const float* dout, float* ds, float* dz1,
                                   float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
-                                  std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard) {
+                                  std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard,
+                                  const Workspace* view, int parts) {
     REQUIRE(B >= 1, "batch must be >= 1");
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && dout && ds && dz1 && dz2 && dweights,
             "null input/output pointer");
     REQUIRE(backward_supported(), "backward needs precision='bf16' and lifted widths <= 448");
-    const Workspace ws = carve(workspace, B, L, true);
+    const Workspace ws = view ? *view : carve(workspace, B, L, true);
+    // chunks of a micro-batched call accumulate the weight gradients concurrently: atomic GEMM
+    // epilogues (split-K >= 2), accumulators zeroed once (part 1) and scattered once (part 4)
+    const bool chunked = parts != 7;
     REQUIRE(workspace != nullptr && workspace_bytes >= ws.bytes, "train workspace too small: need ",
             ws.bytes, " bytes, got ", workspace_bytes);
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -1106,10 +1159,12 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     const bool st2 = shard == nullptr || shard->stage == 2;
     const bool st3 = shard == nullptr || shard->stage == 3;
     mark(0);
-    if (st1) {
+    if (st1 && (parts & 1)) {
     cuda_check(cudaMemsetAsync(dw_out, 0, (woff[10] - woff[8]) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.red, 0, (H + std::size_t(H) * d.d_z) * 4, stream), "memset");
     cuda_check(cudaMemsetAsync(ws.dwproj, 0, std::size_t(d.d_in) * d.n_proj * 4, stream), "memset");
+    }
+    if (st1 && (parts & 2)) {
 
     launch_bwd_dout(dout, mask, ws.dout_bf16, d.din_ld, db_out, BL, d.d_in, stream);
     mark(1);
@@ -1143,7 +1198,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         g.N = d.d_in;
         g.K = BL;
         const int tiles = ((d.feat + 127) / 128) * ((d.d_in + 127) / 128);
-        g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
+        g.split_k = std::max(chunked ? 2 : 1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
         launch_gemm_bf16(g, stream);
     }
     mark(3);
@@ -1195,7 +1250,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     }
     mark(6);
     }  // stage 1
-    if (st2) {
+    if (st2 && (parts & 2)) {
     {
         BwdUnpackArgs a{};
         a.dq_acc = ws.dq_acc;
@@ -1227,7 +1282,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     mark(7);
     if (shard != nullptr) launch_centroid_sums(ws.dt_c, mask, shard->dt_sums, int(B), int(L), stream);
     }  // stage 2
-    if (st3) {
+    if (st3 && (parts & 2)) {
     if (dtrans != nullptr) {
         if (shard != nullptr) {  // dt = mask (dt_c - mean over the valid rows of ALL shards)
             launch_recenter_with_sums(ws.dt_c, shard->dt_sums, dtrans, int(B), int(L), stream,
@@ -1267,10 +1322,12 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         g.K = BL;
         const int bn = (d.n_proj >= 2048) ? 256 : 128;
         const int tiles = ((d.d_in + 127) / 128) * ((d.n_proj + bn - 1) / bn);
-        g.split_k = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
+        g.split_k = std::max(chunked ? 2 : 1, std::min(148 / std::max(tiles, 1), std::max(1, BL / 512)));
         launch_gemm_bf16(g, stream);
     }
     mark(10);
+    }
+    if (st3 && (parts & 4)) {
     {  // scatter the fused projection gradient into w_q .. w_vp (one kernel)
         ScatterCols seg{};
         int col0 = 0;
@@ -1289,6 +1346,81 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     }  // stage 3
     if (timing_) bwd_timed_once_ = true;
     cuda_check(cudaGetLastError(), "backward launch");
+}
+
+// ------------------------------------------------------------ micro-batched capture
+int FlashIpaLayer::micro_chunks(std::int64_t B, std::int64_t L) const {
+    if (tuning_.micro < 2 || timing_ || cfg_.precision != Precision::bf16 || B < 2) return 1;
+    // each chunk's weight-gradient GEMMs run split-K >= 2 over K = (B / chunks) * L
+    if ((B / 2) * L < 256) return 1;
+    return int(std::min<std::int64_t>(tuning_.micro, B));
+}
+
+void FlashIpaLayer::ensure_side_streams() {
+    for (auto& st : side_streams_)
+        if (!st) cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    if (!fork_ev_) cuda_check(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
+    for (auto& e : join_ev_)
+        if (!e) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+}
+
+void FlashIpaLayer::forward_micro(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                  const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                                  float* out, void* workspace, std::size_t workspace_bytes, cudaStream_t stream,
+                                  bool train) {
+    const Workspace full = carve(workspace, B, L, train);
+    REQUIRE(workspace != nullptr && workspace_bytes >= full.bytes, "workspace too small: need ", full.bytes,
+            " bytes, got ", workspace_bytes);
+    ensure_side_streams();
+    const int n = micro_chunks(B, L);
+    const std::size_t rdz = std::size_t(dims_.rank) * dims_.d_z, din = dims_.d_in;
+    cuda_check(cudaEventRecord(fork_ev_, stream), "event record");
+    for (int c = 0; c < n; ++c) {
+        const std::int64_t b0 = B * c / n, nb = B * (c + 1) / n - b0;
+        const std::size_t r = std::size_t(b0) * L;
+        cudaStream_t st = c == 0 ? stream : side_streams_[c - 1];
+        if (c > 0) cuda_check(cudaStreamWaitEvent(st, fork_ev_, 0), "stream wait");
+        const Workspace v = slice(full, b0, L);
+        forward_impl(nb, L, s + r * din, z1 + r * rdz, z2 + r * rdz, rot + r * 9, trans + r * 3,
+                     mask ? mask + r : nullptr, out + r * din, workspace, workspace_bytes, st, train, nullptr, &v);
+    }
+    for (int c = 1; c < n; ++c) {
+        cuda_check(cudaEventRecord(join_ev_[c - 1], side_streams_[c - 1]), "event record");
+        cuda_check(cudaStreamWaitEvent(stream, join_ev_[c - 1], 0), "stream wait");
+    }
+}
+
+void FlashIpaLayer::backward_micro(std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                   const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                                   const float* dout, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
+                                   float* dweights, void* workspace, std::size_t workspace_bytes,
+                                   cudaStream_t stream) {
+    const Workspace full = carve(workspace, B, L, true);
+    REQUIRE(workspace != nullptr && workspace_bytes >= full.bytes, "train workspace too small: need ", full.bytes,
+            " bytes, got ", workspace_bytes);
+    ensure_side_streams();
+    const int n = micro_chunks(B, L);
+    const std::size_t rdz = std::size_t(dims_.rank) * dims_.d_z, din = dims_.d_in;
+    backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+                  workspace_bytes, stream, nullptr, &full, 1);
+    cuda_check(cudaEventRecord(fork_ev_, stream), "event record");
+    for (int c = 0; c < n; ++c) {
+        const std::int64_t b0 = B * c / n, nb = B * (c + 1) / n - b0;
+        const std::size_t r = std::size_t(b0) * L;
+        cudaStream_t st = c == 0 ? stream : side_streams_[c - 1];
+        if (c > 0) cuda_check(cudaStreamWaitEvent(st, fork_ev_, 0), "stream wait");
+        const Workspace v = slice(full, b0, L);
+        backward_impl(nb, L, s + r * din, z1 + r * rdz, z2 + r * rdz, rot + r * 9, trans + r * 3,
+                      mask ? mask + r : nullptr, dout + r * din, ds + r * din, dz1 + r * rdz, dz2 + r * rdz,
+                      drot ? drot + r * 9 : nullptr, dtrans ? dtrans + r * 3 : nullptr, dweights, workspace,
+                      workspace_bytes, st, nullptr, &v, 2);
+    }
+    for (int c = 1; c < n; ++c) {
+        cuda_check(cudaEventRecord(join_ev_[c - 1], side_streams_[c - 1]), "event record");
+        cuda_check(cudaStreamWaitEvent(stream, join_ev_[c - 1], 0), "stream wait");
+    }
+    backward_impl(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
+                  workspace_bytes, stream, nullptr, &full, 4);
 }
 
 }  // namespace fipa_b200

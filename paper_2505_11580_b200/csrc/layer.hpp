@@ -72,6 +72,8 @@ struct Tuning {
     int host_chunk = 0;           // FIPA_HOST_CHUNK: samples per chunk of the host-buffer pipeline (0 = auto)
     bool graphs = true;           // FIPA_GRAPHS = 0: launch kernel by kernel instead of replaying a
                                   // captured CUDA graph per (call kind, shapes, buffers)
+    int micro = 2;                // FIPA_MICRO: bf16 device calls captured as this many interleaved
+                                  // sample chunks on forked streams (1 = one chain)
     static Tuning from_env();
 };
 
@@ -267,6 +269,9 @@ public:
     static constexpr int kAccLd = 448;
     int nproj_ld() const { return (dims_.n_proj + 7) / 8 * 8; }
     Workspace carve(void* base, std::int64_t B, std::int64_t L, bool train = false) const;
+    // The same workspace seen from sample b0 on (every per-sample buffer advanced; the shared
+    // weight-gradient accumulators `red` / `dwproj` unchanged).
+    Workspace slice(const Workspace& w, std::int64_t b0, std::int64_t L) const;
 
     // Query-row sharded forward (comm.cpp): this rank holds residues [rank*L, (rank+1)*L) of B
     // sequences of comm.world()*L residues; out receives its rows.  L % 64 == 0 when world > 1.
@@ -318,11 +323,29 @@ private:
     bool run_graph(const GraphKey& key, cudaStream_t stream, F&& launch);
     void forward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                       const float* rot, const float* trans, const std::uint8_t* mask, float* out, void* workspace,
-                      std::size_t workspace_bytes, cudaStream_t stream, bool train, const ShardStage* shard);
+                      std::size_t workspace_bytes, cudaStream_t stream, bool train, const ShardStage* shard,
+                      const Workspace* view = nullptr);
+    // parts: 1 = zero the weight-gradient accumulators, 2 = per-sample work (weight gradients
+    // accumulated atomically), 4 = scatter / scale the accumulators into dweights
     void backward_impl(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                        const float* rot, const float* trans, const std::uint8_t* mask, const float* dout, float* ds,
                        float* dz1, float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
-                       std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard);
+                       std::size_t workspace_bytes, cudaStream_t stream, const BwdShard* shard,
+                       const Workspace* view = nullptr, int parts = 7);
+    // Micro-batched capture: the B samples split into tuning_.micro chunks whose kernel chains run on
+    // forked streams (the graph holds parallel branches), so each kernel's tail wave and launch ramp
+    // overlap the other chain's kernels.  Same workspace (sample-sliced views), same results.
+    int micro_chunks(std::int64_t B, std::int64_t L) const;
+    void forward_micro(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                       const float* rot, const float* trans, const std::uint8_t* mask, float* out, void* workspace,
+                       std::size_t workspace_bytes, cudaStream_t stream, bool train);
+    void backward_micro(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
+                        const float* rot, const float* trans, const std::uint8_t* mask, const float* dout, float* ds,
+                        float* dz1, float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
+                        std::size_t workspace_bytes, cudaStream_t stream);
+    cudaStream_t side_streams_[3] = {};
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[3] = {};
+    void ensure_side_streams();
 
     Config cfg_;
     LayerDims dims_{};

@@ -406,4 +406,25 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 }  // namespace ptx
+// Whole-grid span trace (tools only, -DFIPA_SPAN_TRACE): globaltimer (ns) of each CTA's start (0),
+// epilogue start (1) and end (2), and its SM (3); summarised by tools/span_summary.hpp.
+#ifdef FIPA_SPAN_TRACE
+__device__ unsigned long long g_span[4 * 65536];
+__device__ __forceinline__ void span_mark(int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (id < 65536) {
+        g_span[4 * id + k] = t;
+        if (k == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_span[4 * id + 3] = sm;
+        }
+    }
+}
+#else
+__device__ __forceinline__ void span_mark(int) {}
+#endif
+
 }  // namespace fipa_b200

@@ -2,12 +2,14 @@
 // north-star shape, random lifted rows.  Build: see tools/README (nvcc -gencode
 // arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2505_11580_b200/csrc).
 #define FIPA_ATTN_BWD_TRACE 1
+#define FIPA_SPAN_TRACE 1
 #include "../paper_2505_11580_b200/csrc/attn_bwd.cu"
 
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include <algorithm>
+
+#include "span_summary.hpp"
 
 using namespace fipa_b200;
 
@@ -71,44 +73,6 @@ int main(int argc, char** argv) {
     printf("dS cta2 w2: tile x_full pin_full_ok a_full_arrive\n");
     for (int j = 0; j < nt && j < 64; ++j)
         printf("  %3d %8lld %8lld %8lld\n", j, T(2,2,3,j)-t0, T(2,2,9,j)-t0, T(2,2,10,j)-t0);
-    // whole-grid spans of the last launch: concurrency, lifetime, epilogue share
-    {
-        const int nc = 4 * ((L + 255) / 256) * int(BH);
-        std::vector<unsigned long long> sp(4 * 65536);
-        cudaMemcpyFromSymbol(sp.data(), g_bwd_span, sp.size() * sizeof(unsigned long long));
-        unsigned long long t_min = ~0ull, t_max = 0;
-        double life = 0, epi = 0, loop = 0;
-        int n = 0;
-        for (int c = 0; c < nc && c < 65536; ++c) {
-            const unsigned long long a0 = sp[4 * c], a1 = sp[4 * c + 1], a2 = sp[4 * c + 2];
-            if (!a0 || !a2) continue;
-            t_min = std::min(t_min, a0);
-            t_max = std::max(t_max, a2);
-            life += double(a2 - a0);
-            if (a1) { epi += double(a2 - a1); loop += double(a1 - a0); }
-            ++n;
-        }
-        // max concurrency: sweep over start/end events
-        std::vector<std::pair<unsigned long long, int>> ev;
-        for (int c = 0; c < nc && c < 65536; ++c)
-            if (sp[4 * c] && sp[4 * c + 2]) { ev.push_back({sp[4 * c], 1}); ev.push_back({sp[4 * c + 2], -1}); }
-        std::sort(ev.begin(), ev.end());
-        int cur = 0, mx = 0;
-        for (auto& e : ev) { cur += e.second; mx = std::max(mx, cur); }
-        printf("grid: %d CTAs, span %.1f us, max concurrent CTAs %d, mean lifetime %.2f us "
-               "(start->epilogue %.2f, epilogue %.2f), ideal waves %.2f\n",
-               n, (t_max - t_min) / 1e3, mx, life / n / 1e3, loop / n / 1e3, epi / n / 1e3, double(n) / mx);
-        int ncl = 0;
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(4 * ((L + 255) / 256), unsigned(BH));
-        cfg.blockDim = dim3(352);
-        cfg.dynamicSmemBytes = 227 * 1024;
-        cudaLaunchAttribute at{};
-        at.id = cudaLaunchAttributeClusterDimension;
-        at.val.clusterDim.x = 4; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
-        cfg.attrs = &at; cfg.numAttrs = 1;
-        cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, attn_bwd_kernel<true, 3, 2, 2, 4, 32>, &cfg);
-        printf("cudaOccupancyMaxActiveClusters(4 CTAs, 227 KB): %d (%s)\n", ncl, cudaGetErrorString(e));
-    }
+    span_summary("attn_bwd", 4 * ((L + 255) / 256) * int(BH));
     return 0;
 }

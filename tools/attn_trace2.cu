@@ -2,11 +2,14 @@
 // shape.  Events (SM clock): QK first-block ready, PV first-stage ready, softmax S ready,
 // softmax PV(j-1) done, softmax P published, K/V load issue, MMA s_free / p_full observed.
 #define FIPA_ATTN_TRACE 1
+#define FIPA_SPAN_TRACE 1
 #include "../paper_2505_11580_b200/csrc/attn_fwd_2sm.cu"
 
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+
+#include "span_summary.hpp"
 
 using namespace fipa_b200;
 
@@ -78,6 +81,7 @@ int main(int argc, char** argv) {
                 printf("  %3d %8lld %8lld %8lld %8lld %8lld %8lld\n", j, T(cta,w,2,j)-t0, T(cta,w,12,j)-t0,
                        T(cta,w,13,j)-t0, j ? T(cta,w,3,j)-t0 : 0, T(cta,w,14,j)-t0, T(cta,w,4,j)-t0);
         }
+    span_summary("attn_fwd_2sm", 2 * ((L + 255) / 256) * int(BH));
     printf("o_full %lld  end %lld\n", T(0,2,9,0)-t0, T(0,2,9,1)-t0);
     for (int cta = 0; cta < 2; ++cta)
         for (int w = 2; w < 10; ++w)
