@@ -107,6 +107,8 @@ struct ProjPackArgs {
     const __nv_bfloat16* w_heads;  // [H * NH, din_ld]
     const float* z1;
     const float* z2;
+    const __nv_bfloat16* z1q;      // [BL, r d_z] bf16(log2(e) z1)  (launch_cast_inputs)
+    const __nv_bfloat16* z2b;      // [BL, r d_z] bf16(z2)
     const float* rot;
     const float* trans;            // recentred
     const uint8_t* mask;
@@ -257,6 +259,10 @@ void launch_transpose_to_bf16(const float* w, int K, int N, __nv_bfloat16* wt, i
 // Row-wise fp32 -> bf16 conversion (s input, dOut, ...).
 void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t stream);
 // Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
+// s -> bf16 [rows, din_ld] plus the pair-factor blocks bf16(log2(e) z1), bf16(z2) of proj_pack.
+bool cast_inputs_supported(int d_in, int din_ld, int rdz);
+void launch_cast_inputs(const float* s, __nv_bfloat16* s_bf16, int d_in, int din_ld, const float* z1, const float* z2,
+                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream);
 void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
                            cudaStream_t stream);
 // Trunk step: s += ipa_out; backbone update of the frames (rot [rows,9], trans [rows,3]) in place.

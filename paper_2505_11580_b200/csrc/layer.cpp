@@ -548,7 +548,11 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         return p;
     };
     w.trans_c = reinterpret_cast<float*>(take(BL * 3 * 4));
-    if (cfg_.precision == Precision::bf16) w.s_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
+    if (cfg_.precision == Precision::bf16) {
+        w.s_bf16 = reinterpret_cast<__nv_bfloat16*>(take(BL * d.din_ld * 2));
+        w.z1q = reinterpret_cast<__nv_bfloat16*>(take(BL * std::size_t(d.rank) * d.d_z * 2));
+        w.z2b = reinterpret_cast<__nv_bfloat16*>(take(BL * std::size_t(d.rank) * d.d_z * 2));
+    }
     w.proj = reinterpret_cast<float*>(take(BL * d.n_proj * 4));
     w.qhat = take(BHL * d.dqk_pad * el);
     w.khat = take(BHL * d.dqk_pad * el);
@@ -600,6 +604,8 @@ FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b
     Workspace v = w;
     v.trans_c = adv(w.trans_c, n * 3 * 4);
     v.s_bf16 = adv(w.s_bf16, n * d.din_ld * 2);
+    v.z1q = adv(w.z1q, n * rdz * 2);
+    v.z2b = adv(w.z2b, n * rdz * 2);
     v.proj = adv(w.proj, n * d.n_proj * 4);
     v.qhat = adv(static_cast<char*>(w.qhat), n * H * d.dqk_pad * el);
     v.khat = adv(static_cast<char*>(w.khat), n * H * d.dqk_pad * el);
@@ -815,13 +821,15 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
     mark(1);
     if (do_pack && d_wheads_ != nullptr && tuning_.fused_pack) {
         // fused projection GEMM + frame application + packing (proj_pack.cu)
-        launch_f32_to_bf16_2d(s, ws.s_bf16, BL, d.d_in, d.din_ld, stream);
+        launch_cast_inputs(s, ws.s_bf16, d.d_in, d.din_ld, z1, z2, ws.z1q, ws.z2b, d.rank * d.d_z, BL, stream);
         mark(2);
         ProjPackArgs pp{};
         pp.s_bf16 = ws.s_bf16;
         pp.w_heads = d_wheads_;
         pp.z1 = z1;
         pp.z2 = z2;
+        pp.z1q = ws.z1q;
+        pp.z2b = ws.z2b;
         pp.rot = rot;
         pp.trans = ws.trans_c;
         pp.mask = mask;

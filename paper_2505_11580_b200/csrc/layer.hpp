@@ -230,6 +230,8 @@ public:
         float* trans_c = nullptr;
         __nv_bfloat16* s_bf16 = nullptr;
         float* proj = nullptr;
+        __nv_bfloat16* z1q = nullptr;      // [BL, r d_z] bf16(log2(e) z1)  (fused projection + pack)
+        __nv_bfloat16* z2b = nullptr;      // [BL, r d_z] bf16(z2)
         void* qhat = nullptr;
         void* khat = nullptr;
         void* vhat = nullptr;

@@ -36,6 +36,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "ptx.cuh"
 
 namespace fipa_b200 {
 
@@ -518,6 +519,43 @@ __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat1
     }
 }
 
+// Inputs of the fused projection + pack kernel in one pass: s -> bf16 rows of din_ld, and the
+// head-independent pair-factor column blocks of the lifted rows, bf16(log2(e) z1) (q_hat) and
+// bf16(z2) (v_hat; k_hat scales it per head), so proj_pack copies them instead of converting the
+// fp32 rows once per head and tensor.  float4 loads, 8-byte stores; thread = 4 columns.
+__global__ void cast_inputs_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ s_bf16, int d_in,
+                                   int din_ld, const float* __restrict__ z1, const float* __restrict__ z2,
+                                   __nv_bfloat16* __restrict__ z1q, __nv_bfloat16* __restrict__ z2b, int rdz,
+                                   int64_t rows) {
+    const int q_s = (d_in + 3) / 4, q_z = rdz / 4;
+    const bool vec_s = d_in % 4 == 0;
+    const int64_t n_s = rows * q_s, n = n_s + 2 * rows * q_z;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const float* src;
+        __nv_bfloat16* dst;
+        float sc = 1.f;
+        if (e < n_s) {
+            const int64_t r = e / q_s;
+            const int c4 = int(e - r * q_s);
+            src = s + r * d_in + 4 * c4;
+            dst = s_bf16 + r * din_ld + 4 * c4;
+            if (!vec_s) {  // unaligned rows: element-wise
+                for (int k = 0; k < 4 && 4 * c4 + k < d_in; ++k) dst[k] = __float2bfloat16_rn(src[k]);
+                continue;
+            }
+        } else {
+            const int64_t f = e - n_s;
+            const bool second = f >= rows * q_z;
+            const int64_t g = second ? f - rows * q_z : f;
+            src = (second ? z2 : z1) + 4 * g;
+            dst = (second ? z2b : z1q) + 4 * g;
+            sc = second ? 1.f : 1.4426950408889634f;
+        }
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        *reinterpret_cast<uint2*>(dst) = make_uint2(ptx::pack_bf16x2(sc * v.x, sc * v.y), ptx::pack_bf16x2(sc * v.z, sc * v.w));
+    }
+}
+
 // One block per sample: subtract the centroid of the valid residues' translations.
 // 3xTF32 operand split (fp32 path): each element x becomes hi = tf32(x) and lo = x - hi (exact),
 // written into up to three K-concatenated parts (or planes) per row.
@@ -775,6 +813,19 @@ void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, in
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
     f32_to_bf16_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(in, out, rows, cols, ld_out);
+}
+
+bool cast_inputs_supported(int, int din_ld, int rdz) { return din_ld % 4 == 0 && rdz % 4 == 0; }
+
+void launch_cast_inputs(const float* s, __nv_bfloat16* s_bf16, int d_in, int din_ld, const float* z1, const float* z2,
+                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream) {
+    if (!cast_inputs_supported(d_in, din_ld, rdz)) throw std::invalid_argument("cast_inputs: widths must be multiples of 4");
+    if (din_ld > d_in) cudaMemsetAsync(s_bf16, 0, size_t(rows) * din_ld * 2, stream);  // padding columns
+    const int64_t n = rows * (d_in / 4 + 2 * (rdz / 4));
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8);
+    cast_inputs_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(s, s_bf16, d_in, din_ld, z1, z2, z1q, z2b,
+                                                                          rdz, rows);
 }
 
 void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,

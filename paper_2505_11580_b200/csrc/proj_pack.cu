@@ -39,6 +39,8 @@ struct PPParams {
     int write_points;  // training: raw point columns into proj for the backward
     const float* z1;
     const float* z2;
+    const __nv_bfloat16* z1q;  // bf16(log2(e) z1): q_hat pair block, copied
+    const __nv_bfloat16* z2b;  // bf16(z2): v_hat pair block copied, k_hat's scaled per head
     const float* rot;
     const float* trans;  // recentred
     const uint8_t* mask;
@@ -76,6 +78,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                  ::"l"(reinterpret_cast<uint64_t>(map)), "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+// 16-byte asynchronous global -> shared copy (L2 only) and its completion wait
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
@@ -154,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = ptx::warp_id(), lane = ptx::lane_id();
     const int m0 = blockIdx.x * BM, h = blockIdx.y;
     if (warp == 0 && lane == 0) {
+        span_mark(0);
         ptx::tma_prefetch(&mapA);
         ptx::tma_prefetch(&mapB);
         for (int s = 0; s < kStages; ++s) {
@@ -189,12 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // epilogue warps go on building the next tensor while the previous one drains
                 // (issuing from the epilogue warps stalled them ~5k cycles per tensor on the
                 // store queue)
+                // tensor order q (tile 0), v (tile 1), k (tile 0 again: its pair block is v's, scaled)
                 for (int tsel = 0; tsel < 3; ++tsel) {
-                    const int tb = tsel & 1;
+                    const int tb = tsel & 1, T = tsel == 0 ? 0 : tsel == 1 ? 2 : 1;
                     ptx::mbar_wait(&tile_ready[tb], (tsel >> 1) & 1);
                     const uint8_t* tile = tiles + tb * tile_bytes;
-                    const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
-                    const CUtensorMap* map = tsel == 0 ? &mapQ : tsel == 1 ? &mapK : &mapV;
+                    const int width = T < 2 ? p.dqk_pad : p.dv_pad;
+                    const CUtensorMap* map = T == 0 ? &mapQ : T == 1 ? &mapK : &mapV;
                     // 32-row chunks never straddle two samples (L % 32 == 0)
                     for (int ch = 0; ch < BM / 32; ++ch) {
                         const int rr = m0 + ch * 32;
@@ -204,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_store_3d(map, tile + blk * (BM * 128) + ch * 32 * 128, blk * 64, ci, cb_ * p.H + h);
                     }
                     bulk_commit();
-                    if (tsel == 1) {
-                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // tensor 0 read
+                    if (tsel == 0) {
+                        bulk_wait_read0();  // tile 0 read by the q stores: free for k
                         ptx::mbar_arrive(tile_free);
                     }
                 }
@@ -254,10 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 3; ++k) t[k] = __ldg(p.trans + int64_t(rowc) * 3 + k);
         const bool valid = p.mask == nullptr || p.mask[rowc] != 0;
         const float g = p.head_g[h];
-        {  // warm L2 with this row's pair factors (phase B reads them) while the GEMM runs
-            const char* z1r = reinterpret_cast<const char*>(p.z1 + int64_t(rowc) * rdz);
-            const char* z2r = reinterpret_cast<const char*>(p.z2 + int64_t(rowc) * rdz);
-            for (int o = 128 * half; o < rdz * 4; o += 256) {
+        {  // warm L2 with this row's bf16 pair factors (phase B copies them) while the GEMM runs
+            const char* z1r = reinterpret_cast<const char*>(p.z1q + int64_t(rowc) * rdz);
+            const char* z2r = reinterpret_cast<const char*>(p.z2b + int64_t(rowc) * rdz);
+            for (int o = 128 * half; o < rdz * 2; o += 256) {
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(z1r + o));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(z2r + o));
             }
@@ -266,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(done, 0);
         ptx::tc_fence_after();
         PPTRACE(1);
+        if (warp == 2 && lane == 0) span_mark(1);
 
         // points: frame-rotated (geometry half only); the raw copies into proj (training) go out
         // after the three tensors
@@ -307,8 +317,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         // derived from TMEM and the frame.  Phase B (warp-cooperative, lanes across columns): the
         // pair-factor columns, straight from coalesced z1 / z2 row loads.
         const float* wbh = p.wl_bias + h * p.dz;
+        // head-independent pair block (q_hat: bf16(log2 e z1), v_hat: bf16(z2)) -> staging tile
+        // columns [col0, col0 + rdz): 16-byte cp.async per (row, 8 columns), a warp per row
+        // segment (coalesced 512 B), all 4096 copies of the tile in flight at once
+        const int etid = threadIdx.x - 64;
+        auto copy_pair = [&](uint8_t* tile, const __nv_bfloat16* src, int col0) {
+            const int nch = rdz / 8;
+            auto one = [&](int rr, int j) {
+                const int grow = m0 + rr < p.M ? m0 + rr : p.M - 1;
+                const int col = col0 + 8 * j;
+                cp_async16(tile + (col >> 6) * (BM * 128) + rr * 128 + ((((col & 63) >> 3) ^ (rr & 7)) << 4),
+                           src + int64_t(grow) * rdz + 8 * j);
+            };
+            if (nch == 32) {  // rank 2 x d_z 128: lane = 16-byte chunk, warp = row (no division)
+                for (int rr = etid >> 5; rr < BM; rr += 8) one(rr, etid & 31);
+            } else {
+                for (int e = etid; e < BM * nch; e += 256) one(e / nch, e % nch);
+            }
+        };
         PPTRACE(2);
         for (int tsel = 0; tsel < 3; ++tsel) {
+            // T: 0 = q_hat (tile 0), 2 = v_hat (tile 1), 1 = k_hat (tile 0 once the q stores read it)
+            const int T = tsel == 0 ? 0 : tsel == 1 ? 2 : 1;
             uint8_t* tile = tiles + (tsel & 1) * tile_bytes;
             PPTRACE(3 + 4 * tsel);
             if (tsel == 2) {
@@ -319,11 +349,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     named_sync(1, 256);
                 }
             }
-            const int width = tsel < 2 ? p.dqk_pad : p.dv_pad;
+            const int width = T < 2 ? p.dqk_pad : p.dv_pad;
+            if (T == 0) copy_pair(tile, p.z1q, zq);
+            if (T == 2) copy_pair(tile, p.z2b, c);
             float v8[8];
             // ---- phase A, half 0: [0, c) scalar channels from TMEM, 16 per load
-            const float sc = tsel == 0 ? kL2E : tsel == 1 ? p.k_scale : 1.f;
-            const int tcol = tsel == 0 ? cq : tsel == 1 ? ck : cv;
+            const float sc = T == 0 ? kL2E : T == 1 ? p.k_scale : 1.f;
+            const int tcol = T == 0 ? cq : T == 1 ? ck : cv;
             if (half == 0 && c % 32 == 0) {
                 // two TMEM loads in flight per wait (each round trip costs ~0.5k cycles; four
                 // spill at this kernel's 168-register cap)
@@ -356,11 +388,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (half == 0) {
-            } else if (tsel < 2) {
+            } else if (T < 2) {
                 // rotated points, the 21 translation / bias columns and the zq padding
-                const float gs = tsel == 0 ? kL2E : g;
-                const float* pts = tsel == 0 ? rq : rk;
-                // translation / bias column e of the [g0, zq) block (q_hat if tsel == 0, else k_hat)
+                const float gs = T == 0 ? kL2E : g;
+                const float* pts = T == 0 ? rq : rk;
+                // translation / bias column e of the [g0, zq) block (q_hat if T == 0, else k_hat)
                 auto tcolv = [&](int e) -> float {
                     const int x = e % 3;
                     float qv, kv;
@@ -379,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         qv = 0.f;
                         kv = e == 20 ? 1.0f : 0.f;
                     }
-                    return tsel == 0 ? qv : kv;
+                    return T == 0 ? qv : kv;
                 };
                 if (3 * Nq == 3 * kMaxQ && c % 8 == 0 && zq - g0 == 24 && p.dqk_used % 8 == 0) {
                     // 16-byte stores: 3 point chunks, 3 translation chunks, the pad chunks
@@ -433,41 +465,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             PPTRACE(4 + 4 * tsel);
-            // ---- phase B: pair factors, warp covers rows quad*32 + half*16 .. +16, lane = 8-column chunk
-            {
-                const float* zsrc = tsel == 0 ? p.z1 : p.z2;
-                const int zcol = tsel == 2 ? c : zq;
+            // ---- phase B: pair factors.  q / v: the copies issued above; k: bf16(w_l w_bias[h] z2),
+            // warp covers rows quad*32 + half*16 .. +16, lane = 8-column chunk, 16 rows in flight
+            if (T == 1) {
+                // k_hat pair block = w_l w_bias[h] (.) bf16(z2): scaled from v_hat's block in tile 1
+                // (every thread's copies into it completed before this barrier)
+                named_sync(1, 256);
+                const uint8_t* vt = tiles + tile_bytes;
                 const int nchunk = rdz / 8;
                 for (int j = lane; j < nchunk; j += 32) {
                     float wm[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        wm[e] = tsel == 0 ? kL2E : tsel == 1 ? __ldg(wbh + (8 * j + e) % p.dz) : 1.f;
-                    // 8 rows of loads in flight per lane before any use
-                    for (int rb = 16 * half; rb < 16 * half + 16; rb += 8) {
-                        float4 za[8][2];
+                    for (int e = 0; e < 8; ++e) wm[e] = __ldg(wbh + (8 * j + e) % p.dz);
+                    const int col = c + 8 * j;
+#pragma unroll 4
+                    for (int u = 0; u < 16; ++u) {
+                        const int rr = quad * 32 + 16 * half + u;
+                        const uint4 za = *reinterpret_cast<const uint4*>(
+                            vt + (col >> 6) * (BM * 128) + rr * 128 + ((((col & 63) >> 3) ^ (rr & 7)) << 4));
+                        const uint32_t w4[4] = {za.x, za.y, za.z, za.w};
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            int grow = m0 + quad * 32 + rb + u;
-                            grow = grow < p.M ? grow : p.M - 1;
-                            const float* zr = zsrc + int64_t(grow) * rdz + 8 * j;
-                            za[u][0] = __ldg(reinterpret_cast<const float4*>(zr));
-                            za[u][1] = __ldg(reinterpret_cast<const float4*>(zr + 4));
+                        for (int e = 0; e < 4; ++e) {
+                            v8[2 * e] = wm[2 * e] * __uint_as_float(w4[e] << 16);
+                            v8[2 * e + 1] = wm[2 * e + 1] * __uint_as_float(w4[e] & 0xffff0000u);
                         }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            v8[0] = wm[0] * za[u][0].x;
-                            v8[1] = wm[1] * za[u][0].y;
-                            v8[2] = wm[2] * za[u][0].z;
-                            v8[3] = wm[3] * za[u][0].w;
-                            v8[4] = wm[4] * za[u][1].x;
-                            v8[5] = wm[5] * za[u][1].y;
-                            v8[6] = wm[6] * za[u][1].z;
-                            v8[7] = wm[7] * za[u][1].w;
-                            stage_put8(tile, quad * 32 + rb + u, zcol + 8 * j, v8);
-                        }
+                        stage_put8(tile, rr, zq + 8 * j, v8);
                     }
                 }
+            } else {
+                cp_async_wait_all();
             }
             PPTRACE(5 + 4 * tsel);
             if (p.chunk_ok) {
@@ -481,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (!p.chunk_ok && ok && half == 0) {
                 // generic shapes: each thread copies its own row (16-byte chunks, un-swizzled)
-                __nv_bfloat16* dst = (tsel == 0 ? p.qhat : tsel == 1 ? p.khat : p.vhat) + hrow * width;
+                __nv_bfloat16* dst = (T == 0 ? p.qhat : T == 1 ? p.khat : p.vhat) + hrow * width;
                 for (int ch8 = 0; ch8 < width / 8; ++ch8) {
                     const uint8_t* src = tile + (ch8 >> 3) * (BM * 128) + r * 128 + (((ch8 & 7) ^ (r & 7)) << 4);
                     reinterpret_cast<uint4*>(dst)[ch8] = *reinterpret_cast<const uint4*>(src);
@@ -508,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+    if (warp == 0 && lane == 0) span_mark(2);
 }
 
 }  // namespace
@@ -526,6 +553,7 @@ int proj_pack_head_width(const LayerDims& d) { return (3 * d.c + 6 * d.n_query +
 
 void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t stream) {
     if (!proj_pack_supported(d)) throw std::invalid_argument("fused projection+pack: unsupported shape");
+    if (a.z1q == nullptr || a.z2b == nullptr) throw std::invalid_argument("fused projection+pack: bf16 pair factors missing");
     PPParams p{};
     p.M = a.B * a.L;
     p.L = a.L;
@@ -549,6 +577,8 @@ void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t st
     p.write_points = a.write_points ? 1 : 0;
     p.z1 = a.z1;
     p.z2 = a.z2;
+    p.z1q = a.z1q;
+    p.z2b = a.z2b;
     p.rot = a.rot;
     p.trans = a.trans;
     p.mask = a.mask;

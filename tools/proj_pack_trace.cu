@@ -2,14 +2,18 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2505_11580_b200/csrc
 //        -o tools/proj_pack_trace_bin tools/proj_pack_trace.cu
 #define FIPA_PP_TRACE 1
+#define FIPA_SPAN_TRACE 1
 #include "../paper_2505_11580_b200/csrc/proj_pack.cu"
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
+
+#include "span_summary.hpp"
 
 using namespace fipa_b200;
 
-int main() {
+int main(int argc, char** argv) {
     const int B = 8, L = 1024, H = 8, din = 256;
     LayerDims d{};
     d.d_in = din; d.d_z = 128; d.heads = H; d.c = 128; d.n_query = 8; d.n_value = 12; d.rank = 2;
@@ -34,6 +38,13 @@ int main() {
     float* z = (float*)dalloc(hz.size() * 4);
     cudaMemcpy(z, hz.data(), hz.size() * 4, cudaMemcpyHostToDevice);
     a.z1 = z; a.z2 = z;
+    {
+        std::vector<__nv_bfloat16> hzb(hz.size());
+        for (size_t i = 0; i < hz.size(); ++i) hzb[i] = __float2bfloat16(hz[i]);
+        __nv_bfloat16* zb = (__nv_bfloat16*)dalloc(hzb.size() * 2);
+        cudaMemcpy(zb, hzb.data(), hzb.size() * 2, cudaMemcpyHostToDevice);
+        a.z1q = zb; a.z2b = zb;
+    }
     float* rot = (float*)dalloc(hr.size() * 4);
     cudaMemcpy(rot, hr.data(), hr.size() * 4, cudaMemcpyHostToDevice);
     float* tr = (float*)dalloc(ht.size() * 4);
@@ -49,6 +60,7 @@ int main() {
     a.khat = (__nv_bfloat16*)dalloc(BL * H * 448 * 2);
     a.vhat = (__nv_bfloat16*)dalloc(BL * H * 448 * 2);
     a.B = B; a.L = L;
+    a.write_points = argc > 1 && atoi(argv[1]) != 0;  // training forward
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int i = 0; i < 3; ++i) launch_proj_pack(d, a, 0);
     cudaEventRecord(e0);
@@ -67,5 +79,6 @@ int main() {
         for (int ev = 0; ev < 16; ++ev) if (t[w * 16 + ev]) printf(" %s=%lld", names[ev], t[w * 16 + ev] - t0);
         printf("\n");
     }
+    span_summary("proj_pack", (B * L / 128) * H);
     return 0;
 }
