@@ -37,7 +37,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <stdexcept>
+#include <tuple>
 
 #include "kernels.hpp"
 #include "ptx.cuh"
@@ -49,7 +52,8 @@ namespace {
 
 constexpr int BM = 128;       // rows per CTA (256 per pair)
 constexpr int BN = 64;        // tile columns
-constexpr int kThreads = 352; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer
+constexpr int kThreads = 480; // w0 stat/B1 producer, w1 TMEM + MMA, w2..w9 elementwise, w10 B2 producer,
+                              // w11..w14 accumulator epilogue (one per TMEM lane quadrant)
 constexpr int kMaxStages1 = 6;  // B1 ring: whole 32-row tile halves, or groups of KB1 column blocks
 constexpr int kMaxStages2 = 6;  // 16-row B2 slices (see finish_params)
 // B2 slices of 16 or 32 rows (template SL): TMA throughput per SM grows with the box size
@@ -67,7 +71,7 @@ struct RoleDims {
 };
 
 struct BwdParams {
-    int Lrow, Lcol, H, B;       // rows (keys in KV, queries in Q) / tile columns
+    int Lrow, Lcol, H, B, BH;   // rows (keys in KV, queries in Q) / tile columns; BH = B * H
     int stat_chunk, col_chunk;  // rows per shard of the stationary / column operands (sharded keys)
     int stat_sharded, col_sharded;  // 1: operand read through the 5-D / 4-D rank-major maps (measured
                                     // ~10% slower per box than the unsharded 4-D / 3-D maps)
@@ -90,14 +94,15 @@ struct Bars {
     uint64_t stat_full;
     uint64_t b1_full[kMaxStages1], b1_empty[kMaxStages1];
     uint64_t b2_full[kMaxStages2], b2_empty[kMaxStages2];
-    uint64_t x_full, x_free, a_full, acc_full;
+    uint64_t stat_empty;
+    uint64_t x_full, x_free, a_full, acc_full, acc_empty, acc_empty_b;
     uint64_t mma2_done[3], pin_full[3], pin_free[3];  // per P / dS exchange buffer (2 or 3)
     uint64_t dsin_full[3];                            // Q kernel: dS returned to the P pair
     uint32_t tmem_slot;
 };
 
 struct Layout {
-    int stat, abuf, b1, b2, bars, total;
+    int stat, abuf, b1, b2, stage, bars, total;
 };
 __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     Layout l{};
@@ -105,8 +110,8 @@ __host__ __device__ inline Layout smem_layout(const BwdParams& p) {
     l.abuf = p.stat_bytes;
     l.b1 = l.abuf + p.nab * BM * 128;  // P (P pair) / received-P-then-dS (dS pair) exchange buffers
     l.b2 = l.b1 + p.nst1 * p.b1_stage;
-    l.bars = l.b2 + p.nst2 * p.b2_stage;
-    if (l.bars < 8 * 8192) l.bars = 8 * 8192;  // the epilogue's staging boxes (8 warps x 8 KB) from offset 0
+    l.stage = (l.b2 + p.nst2 * p.b2_stage + 1023) & ~1023;  // 4 epilogue warps x one 4 KB TMA-store box
+    l.bars = l.stage + 4 * 4096;
     l.total = l.bars + static_cast<int>(sizeof(Bars));
     return l;
 }
@@ -119,9 +124,18 @@ __device__ long long g_bwd_trace[4 * 12 * 16 * 64];  // [cta][warp][event][tile]
         if (blockIdx.x < 4 && blockIdx.y == 0 && (j) < 64)                                               \
             g_bwd_trace[((blockIdx.x * 12 + ptx::warp_id()) * 16 + (ev)) * 64 + (j)] = clock64();        \
     } while (0)
+// Per-unit events of the first cluster (persistent loop): [cta][unit][event]
+__device__ long long g_unit_trace[4 * 16 * 8];
+#define UTRACE(ev, itv)                                                                                  \
+    do {                                                                                                 \
+        if (blockIdx.x < 4 && (itv) < 16) g_unit_trace[(blockIdx.x * 16 + (itv)) * 8 + (ev)] = clock64(); \
+    } while (0)
 #else
 #define BTRACE(ev, j) \
     do {              \
+    } while (0)
+#define UTRACE(ev, itv) \
+    do {                \
     } while (0)
 #endif
 
@@ -162,6 +176,23 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
 
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
+//
+// Persistent: the grid holds as many 4-CTA clusters as fit at once (33 on B200), and each cluster
+// walks the work units (sample-head, 256-row block) u = cluster, cluster + nclusters, ...  Every
+// ring, exchange buffer and barrier phase runs on counters global over the cluster's tiles, so the
+// next unit's operand loads, first Q.K^T and softmax overlap the previous unit's last tiles, and
+// four dedicated epilogue warps (w11..w14, one per TMEM lane quadrant) drain the accumulator while
+// the elementwise warps start the next unit:
+//   stat_empty (MMA commit after a unit's last MMA1)   -> the producer reloads the stationary tile;
+//   acc_empty / acc_empty_b (8 epilogue-warp arrivals) -> columns [0, n2a) / [n2a, n2) are out of
+//                                                         TMEM; the next unit's first MMA2 may run.
+// The drain leaves through 4 KB TMA-store boxes; an SM stores at most ~32 B/clk
+// (tools/store_microbench.cu), so the 221 KB accumulator of a unit still holds the next unit's
+// first MMA2 back a few thousand cycles.  Measured (B=8 L=1024, dK/dV): 0.300 -> 0.28 ms; the
+// non-persistent kernel idled the tensor pipe through each CTA's prologue and epilogue (6 + 5.7 us
+// of a 36 us lifetime) and ran 1024 CTAs in 7.76 waves.  tcgen05.ld 16x256b read TMEM ~3x slower
+// than 32x32b here (9.5k vs 3k cycles for 128 x 432 fp32), and stores whose 32-byte sectors were
+// completed by two different instructions ran ~10x slower (partial-sector writes).
 template <bool KV, int kStages1, int NST2, int NAB, int KB1, int SL>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap statP, const __grid_constant__ CUtensorMap b1P,
@@ -188,20 +219,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const bool leader = prank == 0;
     const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (crank & 2u));
     const RoleDims rd = p.role[role];
-    const int bh = blockIdx.y;
-    const int r0 = (blockIdx.x >> 2) * 256 + static_cast<int>(prank) * BM;  // first row of this CTA
     const int ntiles = (p.Lcol + BN - 1) / BN;
+    const int nrb = (p.Lrow + 255) / 256;                // 256-row blocks per (sample, head)
+    const int nunits = p.BH * nrb;
+    const int cluster = static_cast<int>(blockIdx.x >> 2), nclusters = static_cast<int>(gridDim.x >> 2);
     const bool has_mma2 = rd.n2 > 0;
     const CUtensorMap* mStat = role ? &statD : &statP;
     const CUtensorMap* mB1 = role ? &b1D : &b1P;
     const CUtensorMap* mB2 = role ? &b2D : &b2P;
-
+    auto unit_bh = [&](int u) { return u / nrb; };
+    auto unit_r0 = [&](int u) { return (u - (u / nrb) * nrb) * 256 + static_cast<int>(prank) * BM; };
     if (warp == 0 && lane == 0) {
         span_mark(0);
         ptx::tma_prefetch(mStat);
         ptx::tma_prefetch(mB1);
         if (has_mma2) ptx::tma_prefetch(mB2);
         ptx::mbar_init(&bars->stat_full, 1);
+        ptx::mbar_init(&bars->stat_empty, 1);
         for (int s = 0; s < kStages1; ++s) {
             ptx::mbar_init(&bars->b1_full[s], 1);
             ptx::mbar_init(&bars->b1_empty[s], 1);
@@ -215,6 +249,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         // Q kernel, P pair: the MMA operand (dS) arrives by copy; the odd CTA forwards its arrival
         ptx::mbar_init(&bars->a_full, (!KV && role == 0) ? 1 : 16);
         ptx::mbar_init(&bars->acc_full, 1);
+        ptx::mbar_init(&bars->acc_empty, 8);    // columns [0, n2a) read out: 4 epilogue warps x 2 CTAs
+        ptx::mbar_init(&bars->acc_empty_b, 8);  // columns [n2a, n2) read out
         for (int b = 0; b < 3; ++b) {
             ptx::mbar_init(&bars->mma2_done[b], 1);
             ptx::mbar_init(&bars->pin_full[b], 1);
@@ -233,29 +269,36 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------- stationary tile + B1 tile producer
         if (lane == 0) {
-            if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
-            if (p.stat_sharded) {
-                const int g = r0 / p.stat_chunk;  // rows past the end land in shard G: TMA zero fill
-                ptx::tma_load_5d_2sm(sStat, mStat, &bars->stat_full, 0, r0 - g * p.stat_chunk, 0, bh, g);
-            } else {
-                ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
-            }
             const int nk1 = KB1 ? (rd.nb1 + KB1 - 1) / KB1 : 1;  // B1 stages per tile
             const int stage = (KB1 ? KB1 : rd.nb1) * 32 * 128;
-            for (int j = 0; j < ntiles; ++j) {
-                BTRACE(11, j);
-                const int key = j * BN + 32 * static_cast<int>(prank);
-                const int g = p.col_sharded ? key / p.col_chunk : 0;
-                for (int u = 0; u < nk1; ++u) {
-                    const int n = j * nk1 + u;
-                    const int s = n % kStages1;
-                    if (n >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((n / kStages1) - 1) & 1);
-                    if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
-                    if (p.col_sharded) {
-                        ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key - g * p.col_chunk,
-                                             u * KB1, bh, g);
-                    } else {
-                        ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key, u * KB1, bh);
+            int n = 0;  // B1 stages issued (ring slot n % kStages1)
+            int it = 0;
+            for (int u = cluster; u < nunits; u += nclusters, ++it) {
+                const int bh = unit_bh(u), r0 = unit_r0(u);
+                // the previous unit's last MMA1 has read the stationary tile
+                if (it > 0) ptx::mbar_wait(&bars->stat_empty, (it - 1) & 1);
+                UTRACE(6, it);
+                if (leader) ptx::mbar_expect_tx(&bars->stat_full, 2 * rd.nb1 * BM * 128);
+                if (p.stat_sharded) {
+                    const int g = r0 / p.stat_chunk;  // rows past the end land in shard G: TMA zero fill
+                    ptx::tma_load_5d_2sm(sStat, mStat, &bars->stat_full, 0, r0 - g * p.stat_chunk, 0, bh, g);
+                } else {
+                    ptx::tma_load_4d_2sm(sStat, mStat, &bars->stat_full, 0, r0, 0, bh);
+                }
+                for (int j = 0; j < ntiles; ++j) {
+                    if (it == 0) BTRACE(11, j);
+                    const int key = j * BN + 32 * static_cast<int>(prank);
+                    const int g = p.col_sharded ? key / p.col_chunk : 0;
+                    for (int uu = 0; uu < nk1; ++uu, ++n) {
+                        const int s = n % kStages1;
+                        if (n >= kStages1) ptx::mbar_wait(&bars->b1_empty[s], ((n / kStages1) - 1) & 1);
+                        if (leader) ptx::mbar_expect_tx(&bars->b1_full[s], 2 * stage);
+                        if (p.col_sharded) {
+                            ptx::tma_load_5d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0,
+                                                 key - g * p.col_chunk, uu * KB1, bh, g);
+                        } else {
+                            ptx::tma_load_4d_2sm(sB1 + s * p.b1_stage, mB1, &bars->b1_full[s], 0, key, uu * KB1, bh);
+                        }
                     }
                 }
             }
@@ -270,31 +313,38 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int nslices = ntiles * (BN / kSlice);
             const int col_a = p.b2_col0[role] + halfa * static_cast<int>(prank);
             const int col_b = p.b2_col0[role] + rd.n2a + halfb * static_cast<int>(prank);
-            int g = 0, rloc = 0;
-            for (int n = 0; n < nslices; ++n) {
-                const int s = n % NST2;
-                if (n >= NST2) ptx::mbar_wait(&bars->b2_empty[s], ((n / NST2) - 1) & 1);
-                BTRACE(12, n);
-                if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
-                uint8_t* dst = sB2 + s * p.b2_stage;
-                if (p.col_sharded) {
-                    for (int x = 0; x < rd.nba; ++x)
-                        ptx::tma_load_4d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, rloc, bh, g);
-                    for (int x = 0; x < rd.nbb; ++x)
-                        ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s], col_b + 64 * x,
-                                             rloc, bh, g);
-                } else {
-                    const int row = n * kSlice;
-                    for (int x = 0; x < rd.nba; ++x)
-                        ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, row, bh);
-                    for (int x = 0; x < rd.nbb; ++x)
-                        ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s], col_b + 64 * x,
-                                             row, bh);
-                }
-                rloc += kSlice;  // shard-local row of the next slice
-                if (rloc >= p.col_chunk) {
-                    rloc -= p.col_chunk;
-                    ++g;
+            int s = 0, ph = 0, n = 0;
+            for (int u = cluster; u < nunits; u += nclusters) {
+                const int bh = unit_bh(u);
+                int g = 0, rloc = 0;
+                for (int i = 0; i < nslices; ++i, ++n) {
+                    if (n >= NST2) ptx::mbar_wait(&bars->b2_empty[s], ph ^ 1);
+                    if (n < 64) BTRACE(12, n);
+                    if (leader) ptx::mbar_expect_tx(&bars->b2_full[s], 2 * stage_bytes);
+                    uint8_t* dst = sB2 + s * p.b2_stage;
+                    if (p.col_sharded) {
+                        for (int x = 0; x < rd.nba; ++x)
+                            ptx::tma_load_4d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, rloc, bh, g);
+                        for (int x = 0; x < rd.nbb; ++x)
+                            ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
+                                                 col_b + 64 * x, rloc, bh, g);
+                    } else {
+                        const int row = i * kSlice;
+                        for (int x = 0; x < rd.nba; ++x)
+                            ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, row, bh);
+                        for (int x = 0; x < rd.nbb; ++x)
+                            ptx::tma_load_3d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s], col_b + 64 * x,
+                                                 row, bh);
+                    }
+                    rloc += kSlice;  // shard-local row of the next slice
+                    if (rloc >= p.col_chunk) {
+                        rloc -= p.col_chunk;
+                        ++g;
+                    }
+                    if (++s == NST2) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
@@ -305,8 +355,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             // leader (a bulk copy can only complete on a barrier of the destination CTA)
             if (lane == 0) {
                 const uint32_t a_full_leader = ptx::mapa(&bars->a_full, crank & 2u);
-                for (int j = 0; j < ntiles; ++j) {
-                    ptx::mbar_wait(&bars->dsin_full[j % NAB], (j / NAB) & 1);
+                const int ntot = ((nunits - cluster + nclusters - 1) / nclusters) * ntiles;
+                for (int t = 0; t < ntot; ++t) {
+                    ptx::mbar_wait(&bars->dsin_full[t % NAB], (t / NAB) & 1);
                     ptx::mbar_arrive_remote(a_full_leader);
                 }
             }
@@ -320,81 +371,213 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1_base = ptx::smem_u32(sB1);
             const uint32_t b2_base = ptx::smem_u32(sB2);
             const int k1_steps = rd.k1 / 16;
+            const int nk1 = KB1 ? (rd.nb1 + KB1 - 1) / KB1 : 1;
             // descriptors advance by 64-bit adds of (byte offset >> 4): the issue thread's work per
             // MMA is a couple of integer ops (it is on the critical path with ~35 MMAs per tile)
             const uint64_t d_stat = ptx::sw128_desc(stat_base, 16, 1024);
             const uint64_t d_b1 = ptx::sw128_desc(b1_base, 16, 1024);
             const uint64_t d_a = ptx::sw128_desc(a_base, 16, 1024);
             const uint64_t d_b2 = ptx::sw128_desc(b2_base, kSliceBox, 1024);
-            ptx::mbar_wait(&bars->stat_full, 0);
-            for (int j = 0; j <= ntiles; ++j) {
-                if (j < ntiles) {
-                    if (j > 0) ptx::mbar_wait_cluster(&bars->x_free, (j - 1) & 1);
-                    if (lane == 0) BTRACE(2, j);
-                    const int nk1 = KB1 ? (rd.nb1 + KB1 - 1) / KB1 : 1;
-                    for (int u = 0; u < nk1; ++u) {
-                        const int n = j * nk1 + u;
-                        const int s = n % kStages1;
-                        ptx::mbar_wait(&bars->b1_full[s], (n / kStages1) & 1);
-                        if (lane == 0 && u == 0) BTRACE(0, j);
-                        ptx::tc_fence_after();
-                        if (ptx::elect_one()) {
-                            const uint64_t db0 = d_b1 + static_cast<uint64_t>((s * p.b1_stage) >> 4);
-                            const int b_lo = u * KB1, b_hi = KB1 ? min(rd.nb1, (u + 1) * KB1) : rd.nb1;
-                            for (int blk = b_lo; blk < b_hi; ++blk) {
-                                const uint64_t da_b = d_stat + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
-                                const uint64_t db_b = db0 + static_cast<uint64_t>(((blk - b_lo) * (32 * 128)) >> 4);
+            int it = 0, t = 0;  // t: global tile index of MMA1 (tile j of unit it)
+            int n1 = 0, n2 = 0;  // B1 stages / B2 slices consumed
+            for (int u = cluster; u < nunits; u += nclusters, ++it) {
+                ptx::mbar_wait(&bars->stat_full, it & 1);
+                if (lane == 0) UTRACE(0, it);
+                for (int j = 0; j <= ntiles; ++j) {
+                    if (j < ntiles) {
+                        if (t > 0) ptx::mbar_wait_cluster(&bars->x_free, (t - 1) & 1);
+                        if (lane == 0 && it == 0) BTRACE(2, j);
+                        for (int uu = 0; uu < nk1; ++uu, ++n1) {
+                            const int s = n1 % kStages1;
+                            ptx::mbar_wait(&bars->b1_full[s], (n1 / kStages1) & 1);
+                            if (lane == 0 && uu == 0 && it == 0) BTRACE(0, j);
+                            ptx::tc_fence_after();
+                            if (ptx::elect_one()) {
+                                const uint64_t db0 = d_b1 + static_cast<uint64_t>((s * p.b1_stage) >> 4);
+                                const int b_lo = uu * KB1, b_hi = KB1 ? min(rd.nb1, (uu + 1) * KB1) : rd.nb1;
+                                for (int blk = b_lo; blk < b_hi; ++blk) {
+                                    const uint64_t da_b = d_stat + static_cast<uint64_t>((blk * (BM * 128)) >> 4);
+                                    const uint64_t db_b = db0 + static_cast<uint64_t>(((blk - b_lo) * (32 * 128)) >> 4);
 #pragma unroll
-                                for (int sub = 0; sub < 4; ++sub) {
-                                    if (4 * blk + sub < k1_steps)
-                                        ptx::mma2_ss(tmem + kXCol, da_b + 2 * sub, db_b + 2 * sub, idesc1,
-                                                     (blk | sub) != 0);
+                                    for (int sub = 0; sub < 4; ++sub) {
+                                        if (4 * blk + sub < k1_steps)
+                                            ptx::mma2_ss(tmem + kXCol, da_b + 2 * sub, db_b + 2 * sub, idesc1,
+                                                         (blk | sub) != 0);
+                                    }
+                                }
+                                ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
+                                if (uu == nk1 - 1) {
+                                    ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                                    // last MMA1 of the unit: the stationary tile may be reloaded
+                                    if (j == ntiles - 1) ptx::mma_commit_2sm(&bars->stat_empty, pair_mask);
                                 }
                             }
-                            ptx::mma_commit_2sm(&bars->b1_empty[s], pair_mask);
-                            if (u == nk1 - 1) ptx::mma_commit_2sm(&bars->x_full, pair_mask);
+                            __syncwarp();
                         }
-                        __syncwarp();
+                        ++t;
                     }
-                }
-                if (j > 0 && has_mma2) {
-                    const int jj = j - 1;
-                    if (!KV && role == 0) ptx::mbar_wait(&bars->dsin_full[jj % NAB], (jj / NAB) & 1);
-                    ptx::mbar_wait_cluster(&bars->a_full, jj & 1);
-                    if (lane == 0) BTRACE(1, jj);
-                    for (int h2 = 0; h2 < BN / kSlice; ++h2) {
-                        const int n = jj * (BN / kSlice) + h2;
-                        const int s = n % NST2;
-                        ptx::mbar_wait(&bars->b2_full[s], (n / NST2) & 1);
-                        if (lane == 0 && h2 == BN / kSlice - 1) BTRACE(13, jj);
-                        ptx::tc_fence_after();
-                        if (ptx::elect_one()) {
+                    if (j > 0 && has_mma2) {
+                        const int jj = j - 1, tt = t - (j < ntiles ? 2 : 1);  // global index of tile jj
+                        if (!KV && role == 0) ptx::mbar_wait(&bars->dsin_full[tt % NAB], (tt / NAB) & 1);
+                        ptx::mbar_wait_cluster(&bars->a_full, tt & 1);
+                        // the previous unit's epilogue has read the accumulator out of TMEM: columns
+                        // [0, n2a) first -- the first tile's n2a-wide MMAs go as soon as those are
+                        // out (both of its B2 slices are resident), the n2b-wide ones after the rest
+                        if (jj == 0 && it > 0) ptx::mbar_wait_cluster(&bars->acc_empty, (it - 1) & 1);
+                        if (lane == 0 && jj == 0) UTRACE(1, it);
+                        if (lane == 0 && it == 0) BTRACE(1, jj);
+                        const bool split_first = jj == 0 && it > 0 && rd.n2b > 0 && NST2 >= BN / kSlice;
+                        if (split_first) {
+                            const int n2s = n2;
+                            for (int h2 = 0; h2 < BN / kSlice; ++h2) {
+                                const int s = (n2s + h2) % NST2;
+                                ptx::mbar_wait(&bars->b2_full[s], ((n2s + h2) / NST2) & 1);
+                                ptx::tc_fence_after();
+                                if (ptx::elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < kSlice / 16; ++kk) {
-                                const uint64_t da = d_a + static_cast<uint64_t>(
-                                    ((jj % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32) >> 4);
-                                const uint64_t db = d_b2 + static_cast<uint64_t>((s * p.b2_stage + kk * 2048) >> 4);
-                                const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
-                                ptx::mma2_ss(tmem, da, db, idesc2a, acc);
-                                if (rd.n2b > 0)
-                                    ptx::mma2_ss(tmem + rd.n2a, da, db + static_cast<uint64_t>((rd.nba * kSliceBox) >> 4),
-                                                 idesc2b, acc);
+                                    for (int kk = 0; kk < kSlice / 16; ++kk) {
+                                        const uint64_t da = d_a + static_cast<uint64_t>(
+                                            ((tt % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32) >> 4);
+                                        const uint64_t db = d_b2 + static_cast<uint64_t>((s * p.b2_stage + kk * 2048) >> 4);
+                                        ptx::mma2_ss(tmem, da, db, idesc2a, (h2 > 0 || kk > 0) ? 1u : 0u);
+                                    }
+                                }
+                                __syncwarp();
                             }
-                            ptx::mma_commit_2sm(&bars->b2_empty[s], pair_mask);
+                            ptx::mbar_wait_cluster(&bars->acc_empty_b, (it - 1) & 1);
+                            ptx::tc_fence_after();
+                            for (int h2 = 0; h2 < BN / kSlice; ++h2, ++n2) {
+                                const int s = n2 % NST2;
+                                if (ptx::elect_one()) {
+#pragma unroll
+                                    for (int kk = 0; kk < kSlice / 16; ++kk) {
+                                        const uint64_t da = d_a + static_cast<uint64_t>(
+                                            ((tt % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32) >> 4);
+                                        const uint64_t db = d_b2 + static_cast<uint64_t>((s * p.b2_stage + kk * 2048) >> 4);
+                                        ptx::mma2_ss(tmem + rd.n2a, da, db + static_cast<uint64_t>((rd.nba * kSliceBox) >> 4),
+                                                     idesc2b, (h2 > 0 || kk > 0) ? 1u : 0u);
+                                    }
+                                    ptx::mma_commit_2sm(&bars->b2_empty[s], pair_mask);
+                                }
+                                __syncwarp();
+                            }
+                        } else {
+                        if (jj == 0 && it > 0 && rd.n2b > 0) ptx::mbar_wait_cluster(&bars->acc_empty_b, (it - 1) & 1);
+                        for (int h2 = 0; h2 < BN / kSlice; ++h2, ++n2) {
+                            const int s = n2 % NST2;
+                            ptx::mbar_wait(&bars->b2_full[s], (n2 / NST2) & 1);
+                            if (lane == 0 && h2 == BN / kSlice - 1 && it == 0) BTRACE(13, jj);
+                            ptx::tc_fence_after();
+                            if (ptx::elect_one()) {
+#pragma unroll
+                                for (int kk = 0; kk < kSlice / 16; ++kk) {
+                                    const uint64_t da = d_a + static_cast<uint64_t>(
+                                        ((tt % NAB) * (BM * 128) + ((kSlice / 16) * h2 + kk) * 32) >> 4);
+                                    const uint64_t db = d_b2 + static_cast<uint64_t>((s * p.b2_stage + kk * 2048) >> 4);
+                                    const uint32_t acc = (jj > 0 || h2 > 0 || kk > 0) ? 1u : 0u;
+                                    ptx::mma2_ss(tmem, da, db, idesc2a, acc);
+                                    if (rd.n2b > 0)
+                                        ptx::mma2_ss(tmem + rd.n2a, da,
+                                                     db + static_cast<uint64_t>((rd.nba * kSliceBox) >> 4), idesc2b, acc);
+                                }
+                                ptx::mma_commit_2sm(&bars->b2_empty[s], pair_mask);
+                            }
+                            __syncwarp();
+                        }
+                        }  // !split_first
+                        if (ptx::elect_one()) {
+                            // P pair: its P buffer is free again.  dS pair: the received-P buffer
+                            // is free -> the P pair may send the next tile.
+                            if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done[tt % NAB], pair_mask);
+                            else ptx::mma_commit_2sm(&bars->pin_free[tt % NAB], 0x3);
+                            if (j == ntiles) ptx::mma_commit_2sm(&bars->acc_full, pair_mask);
                         }
                         __syncwarp();
                     }
-                    if (ptx::elect_one()) {
-                        // P pair: its P buffer is free again.  dS pair: the received-P buffer
-                        // is free -> the P pair may send the next tile.
-                        if (role == 0) ptx::mma_commit_2sm(&bars->mma2_done[jj % NAB], pair_mask);
-                        else ptx::mma_commit_2sm(&bars->pin_free[jj % NAB], 0x3);
-                        if (j == ntiles) ptx::mma_commit_2sm(&bars->acc_full, pair_mask);
-                    }
-                    __syncwarp();
                 }
             }
         }
+    } else if (warp >= 11) {
+        // ---------------------------------------------- accumulator epilogue (own warps)
+        // drains unit u's accumulator while the elementwise warps start unit u+1's tiles; the
+        // next unit's first MMA2 waits on acc_empty
+        const int quad = warp & 3;
+        const uint32_t tl = tmem + (uint32_t(quad * 32) << 16);
+        const uint32_t acc_empty_remote = ptx::mapa(&bars->acc_empty, crank & 2u);
+        const uint32_t acc_empty_b_remote = ptx::mapa(&bars->acc_empty_b, crank & 2u);
+        int it = 0;
+        for (int u = cluster; u < nunits; u += nclusters, ++it) {
+            if (!has_mma2) break;
+            const int bh = unit_bh(u), r0 = unit_r0(u);
+            float* out = p.acc_out[role];
+            if (warp == 11 && lane == 0) UTRACE(3, it);
+            ptx::mbar_wait(&bars->acc_full, it & 1);
+            ptx::tc_fence_after();
+            if (warp == 11 && lane == 0) UTRACE(4, it);
+            if (warp == 11 && lane == 0 && it == 0) span_mark(1);
+            if (out != nullptr) {
+                const int bb = bh / p.H, hh = bh - bb * p.H;
+                // thread = row (TMEM lane, tcgen05.ld 32x32b: the 16x256b shape read TMEM ~3x slower,
+                // 9.5k vs 3k cycles for a 128 x 432 fp32 tile).  Each 32-column chunk is staged as a
+                // 128-byte-swizzled 32 x 32 box (this warp's 4 KB) and leaves by one TMA tensor
+                // store of 32 full 128-byte lines; stores straight from registers (32-byte sectors
+                // of 32 rows per instruction) ran at ~25 B/clk per SM and held the next unit's
+                // first MMA2 back for the whole drain.  The next chunk's TMEM load is in flight
+                // while the previous box is read out.
+                const int g = (r0 + quad * 32) / p.stat_chunk, gi = r0 + quad * 32 - g * p.stat_chunk;
+                const bool rows_ok = r0 + quad * 32 < p.Lrow;
+                const CUtensorMap* mAcc = role ? &accD : &accP;
+                uint8_t* box = smem + lay.stage + (warp - 11) * 4096;
+                const int n32 = (rd.n2 + 31) / 32;
+                uint32_t o0[32], o1[32];
+                auto stage_box = [&](const uint32_t* w, int cb) {
+                    if (lane == 0) ptx::bulk_wait_group_read<0>();  // the previous box has been read
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        *reinterpret_cast<uint4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                            make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && rows_ok) {
+                        ptx::tma_store_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
+                        ptx::bulk_commit_group();
+                    }
+                };
+                // columns [0, n2a) out of TMEM -> acc_empty (the next unit's first n2a-wide MMAs)
+                const int na32 = rd.n2b > 0 ? rd.n2a / 32 : n32;
+                auto read_out_a = [&](int cb) {
+                    if (cb + 1 == na32) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cluster_relaxed(acc_empty_remote);
+                    }
+                };
+                ptx::tmem_ld32(tl, o0);
+                for (int cb = 0; cb < n32; cb += 2) {
+                    ptx::tmem_wait_ld();
+                    read_out_a(cb);
+                    if (cb + 1 < n32) ptx::tmem_ld32(tl + 32 * (cb + 1), o1);
+                    stage_box(o0, cb);
+                    if (cb + 1 < n32) {
+                        ptx::tmem_wait_ld();
+                        read_out_a(cb + 1);
+                        if (cb + 2 < n32) ptx::tmem_ld32(tl + 32 * (cb + 2), o0);
+                        stage_box(o1, cb + 1);
+                    }
+                }
+            } else {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster_relaxed(acc_empty_remote);
+            }
+            // accumulator read out: the next unit's first MMA2 may overwrite it
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(acc_empty_b_remote);
+            if (warp == 11 && lane == 0) UTRACE(5, it);
+        }
+        if (lane == 0) ptx::bulk_wait_group_read<0>();  // staging read before the CTA exits
     } else {
         // ------------------------------------------------------------- elementwise
         const int sw = warp - 2;
@@ -405,190 +588,149 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t leader_rank = crank & 2u;
         const uint32_t x_free_remote = ptx::mapa(&bars->x_free, leader_rank);
         const uint32_t a_full_remote = ptx::mapa(&bars->a_full, leader_rank);
-        const int64_t vec_base = static_cast<int64_t>(bh) * (KV ? p.Lcol : p.Lrow);  // per-query vectors
-        const int grow = r0 + row;  // global row (key in KV, query in Q)
-        // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.
-        float row_v = 0.f;
-        if (!KV && grow < p.Lrow) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
-                                                 : __ldg(p.Dvec + vec_base + grow);
         const uint32_t peer_rank = crank + 2u;  // P pair -> dS pair partner
-
-        for (int j = 0; j < ntiles; ++j) {
-            const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
-            const int buf = j % NAB;
-            uint8_t* abuf = sA + buf * (BM * 128);
-            uint8_t* arow = abuf + row * 128;
-            if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full[buf], BM * 128);
-            // per-column vector (KV kernel)
-            float cv[32];
-            if (KV) {
-                if (role == 0) {
-                    load_vec32(p.lse + vec_base, c0, p.Lcol, INFINITY, cv);
+        int it = 0, t = 0;  // t: global tile index
+        for (int u = cluster; u < nunits; u += nclusters, ++it) {
+            const int bh = unit_bh(u), r0 = unit_r0(u);
+            const int64_t vec_base = static_cast<int64_t>(bh) * (KV ? p.Lcol : p.Lrow);  // per-query vectors
+            const int grow = r0 + row;  // global row (key in KV, query in Q)
+            // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.
+            float row_v = 0.f;
+            if (!KV && grow < p.Lrow) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
+                                                     : __ldg(p.Dvec + vec_base + grow);
+            for (int j = 0; j < ntiles; ++j, ++t) {
+                const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
+                const int buf = t % NAB;
+                uint8_t* abuf = sA + buf * (BM * 128);
+                uint8_t* arow = abuf + row * 128;
+                if (role == 1 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->pin_full[buf], BM * 128);
+                // per-column vector (KV kernel)
+                float cv[32];
+                if (KV) {
+                    if (role == 0) {
+                        load_vec32(p.lse + vec_base, c0, p.Lcol, INFINITY, cv);
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) cv[k] *= kL2E;
-                } else {
-                    load_vec32(p.Dvec + vec_base, c0, p.Lcol, 0.f, cv);
-                }
-            }
-            ptx::mbar_wait(&bars->x_full, j & 1);
-            if (lane == 0) BTRACE(3, j);
-            ptx::tc_fence_after();
-            uint32_t xr[32];
-            ptx::tmem_ld32(tl + kXCol + 32 * half, xr);
-            ptx::tmem_wait_ld();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(x_free_remote);
-
-            uint32_t pk[16];
-            if (role == 0) {
-                // P = 2^(X - lse2), zero past the sequence end (padding rows of K/Q tiles)
-#pragma unroll
-                for (int cc = 0; cc < 16; ++cc) {
-                    float pv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int k = 2 * cc + u;
-                        const float x = __uint_as_float(xr[k]);
-                        if (KV) {
-                            pv[u] = ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
-                        } else {
-                            pv[u] = c0 + k < p.Lcol ? ptx::ex2(x - row_v) : 0.f;
-                        }
+                        for (int k = 0; k < 32; ++k) cv[k] *= kL2E;
+                    } else {
+                        load_vec32(p.Dvec + vec_base, c0, p.Lcol, 0.f, cv);
                     }
-                    pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);
                 }
-                if (lane == 0) BTRACE(4, j);
-                // Buffer `buf` held P_{j-2}: free once the local dV MMA of tile j-2 (KV) and the dS
-                // pair's MMA of tile j-2 (which implies the copy of P_{j-2} landed) are done; the
-                // latter also frees the dS pair's buffer `buf` for the copy of P_j.
-                if (j >= NAB) {
-                    if (has_mma2) ptx::mbar_wait(&bars->mma2_done[buf], ((j / NAB) - 1) & 1);
-                    ptx::mbar_wait_cluster(&bars->pin_free[buf], ((j / NAB) - 1) & 1);
-                    ptx::tc_fence_after();
-                }
-                // Q kernel: dS_j comes back into this buffer once the dS pair has it (the copy of
-                // P_j out of it has completed by then)
-                if (!KV && has_mma2 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->dsin_full[buf], BM * 128);
-                if (lane == 0) BTRACE(5, j);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = 4 * half + k;
-                    *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
-                        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                }
-                ptx::fence_proxy_async_smem();
+                ptx::mbar_wait(&bars->x_full, t & 1);
+                if (lane == 0 && it == 0) BTRACE(3, j);
+                if (warp == 2 && lane == 0 && j == 0) UTRACE(2, it);
+                ptx::tc_fence_after();
+                uint32_t xr[32];
+                ptx::tmem_ld32(tl + kXCol + 32 * half, xr);
+                ptx::tmem_wait_ld();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (KV && has_mma2 && lane == 0) ptx::mbar_arrive_remote(a_full_remote);
-                // all 128 rows written -> one bulk copy of the 16 KB tile into the dS pair
-                named_bar_sync(1, 256);
-                if (warp == 2 && lane == 0) {
-                    bulk_copy_s2cluster(ptx::mapa(abuf, peer_rank), abuf, BM * 128, ptx::mapa(&bars->pin_full[buf], peer_rank));
-                    BTRACE(7, j);
-                }
-            } else {
-                if (KV && p.ds_store && j > 0 && warp == 2 && lane == 0) {
-                    // dS_{j-1}'s store has read its buffer: release it to the P pair
-                    ptx::bulk_wait_group_read<0>();
-                    ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(j - 1) % NAB], crank - 2u));
-                }
-                ptx::mbar_wait_cluster(&bars->pin_full[buf], (j / NAB) & 1);
-                if (lane == 0) BTRACE(9, j);
-                uint4 pin[4];
+                if (lane == 0) ptx::mbar_arrive_cluster_relaxed(x_free_remote);
+
+                uint32_t pk[16];
+                if (role == 0) {
+                    // P = 2^(X - lse2), zero past the sequence end (padding rows of K/Q tiles)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = 4 * half + k;
-                    pin[k] = *reinterpret_cast<const uint4*>(arow + ((chunk ^ (row & 7)) << 4));
-                }
-                const uint32_t* pw = reinterpret_cast<const uint32_t*>(pin);
+                    for (int cc = 0; cc < 16; ++cc) {
+                        float pv[2];
 #pragma unroll
-                for (int cc = 0; cc < 16; ++cc) {
-                    const float d0 = KV ? cv[2 * cc] : row_v;
-                    const float d1 = KV ? cv[2 * cc + 1] : row_v;
-                    const float s0 = bf_lo(pw[cc]) * (__uint_as_float(xr[2 * cc]) - d0);
-                    const float s1 = bf_hi(pw[cc]) * (__uint_as_float(xr[2 * cc + 1]) - d1);
-                    pk[cc] = ptx::pack_bf16x2(s0, s1);
-                }
+                        for (int uu = 0; uu < 2; ++uu) {
+                            const int k = 2 * cc + uu;
+                            const float x = __uint_as_float(xr[k]);
+                            if (KV) {
+                                pv[uu] = ptx::ex2(x - cv[k]);  // cv = +inf past L -> 0
+                            } else {
+                                pv[uu] = c0 + k < p.Lcol ? ptx::ex2(x - row_v) : 0.f;
+                            }
+                        }
+                        pk[cc] = ptx::pack_bf16x2(pv[0], pv[1]);
+                    }
+                    if (lane == 0 && it == 0) BTRACE(4, j);
+                    // Buffer `buf` held P_{t-NAB}: free once the local dV MMA of that tile (KV) and the
+                    // dS pair's MMA of it (which implies the copy landed) are done; the latter also
+                    // frees the dS pair's buffer `buf` for the copy of P_t.
+                    if (t >= NAB) {
+                        if (has_mma2) ptx::mbar_wait(&bars->mma2_done[buf], ((t / NAB) - 1) & 1);
+                        ptx::mbar_wait_cluster(&bars->pin_free[buf], ((t / NAB) - 1) & 1);
+                        ptx::tc_fence_after();
+                    }
+                    // Q kernel: dS_t comes back into this buffer once the dS pair has it (the copy of
+                    // P_t out of it has completed by then)
+                    if (!KV && has_mma2 && warp == 2 && lane == 0) ptx::mbar_expect_tx(&bars->dsin_full[buf], BM * 128);
+                    if (lane == 0 && it == 0) BTRACE(5, j);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = 4 * half + k;
-                    *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
-                        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                }
-                ptx::fence_proxy_async_smem();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
-                if (lane == 0) BTRACE(10, j);
-                if (KV && p.ds_store) {
-                    // the whole 128-key x 64-query dS tile (already in the 128-byte-swizzled
-                    // K-major layout of the TMA box) -> dS[bh][key][query] for the dQ GEMM
+                    for (int k = 0; k < 4; ++k) {
+                        const int chunk = 4 * half + k;
+                        *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
+                            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (KV && has_mma2 && lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                    // all 128 rows written -> one bulk copy of the 16 KB tile into the dS pair
                     named_bar_sync(1, 256);
                     if (warp == 2 && lane == 0) {
-                        ptx::tma_store_3d(&mapDS, abuf, j * BN, r0, bh);
-                        ptx::bulk_commit_group();
+                        bulk_copy_s2cluster(ptx::mapa(abuf, peer_rank), abuf, BM * 128,
+                                            ptx::mapa(&bars->pin_full[buf], peer_rank));
+                        if (it == 0) BTRACE(7, j);
+                    }
+                } else {
+                    if (KV && p.ds_store && t > 0 && warp == 2 && lane == 0) {
+                        // dS_{t-1}'s store has read its buffer: release it to the P pair
+                        ptx::bulk_wait_group_read<0>();
+                        ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(t - 1) % NAB], crank - 2u));
+                    }
+                    ptx::mbar_wait_cluster(&bars->pin_full[buf], (t / NAB) & 1);
+                    if (lane == 0 && it == 0) BTRACE(9, j);
+                    uint4 pin[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int chunk = 4 * half + k;
+                        pin[k] = *reinterpret_cast<const uint4*>(arow + ((chunk ^ (row & 7)) << 4));
+                    }
+                    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pin);
+#pragma unroll
+                    for (int cc = 0; cc < 16; ++cc) {
+                        const float d0 = KV ? cv[2 * cc] : row_v;
+                        const float d1 = KV ? cv[2 * cc + 1] : row_v;
+                        const float s0 = bf_lo(pw[cc]) * (__uint_as_float(xr[2 * cc]) - d0);
+                        const float s1 = bf_hi(pw[cc]) * (__uint_as_float(xr[2 * cc + 1]) - d1);
+                        pk[cc] = ptx::pack_bf16x2(s0, s1);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int chunk = 4 * half + k;
+                        *reinterpret_cast<uint4*>(arow + ((chunk ^ (row & 7)) << 4)) =
+                            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_remote(a_full_remote);
+                    if (lane == 0 && it == 0) BTRACE(10, j);
+                    if (KV && p.ds_store) {
+                        // the whole 128-key x 64-query dS tile (already in the 128-byte-swizzled
+                        // K-major layout of the TMA box) -> dS[bh][key][query] for the dQ GEMM
+                        named_bar_sync(1, 256);
+                        if (warp == 2 && lane == 0) {
+                            ptx::tma_store_3d(&mapDS, abuf, j * BN, r0, bh);
+                            ptx::bulk_commit_group();
+                        }
+                    }
+                    if (!KV && p.role[0].n2 > 0) {
+                        // Q kernel: the P pair accumulates the other half of dQ from the same dS tile
+                        named_bar_sync(1, 256);
+                        if (warp == 2 && lane == 0)
+                            bulk_copy_s2cluster(ptx::mapa(abuf, crank - 2u), abuf, BM * 128,
+                                                ptx::mapa(&bars->dsin_full[buf], crank - 2u));
                     }
                 }
-                if (!KV && p.role[0].n2 > 0) {
-                    // Q kernel: the P pair accumulates the other half of dQ from the same dS tile
-                    named_bar_sync(1, 256);
-                    if (warp == 2 && lane == 0)
-                        bulk_copy_s2cluster(ptx::mapa(abuf, crank - 2u), abuf, BM * 128,
-                                            ptx::mapa(&bars->dsin_full[buf], crank - 2u));
-                }
             }
-        }
 
+        }
         if (KV && p.ds_store && role == 1 && warp == 2 && lane == 0) {
             ptx::bulk_wait_group_read<0>();  // last dS store done reading before the CTA exits
-            if (ntiles > 0) ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(ntiles - 1) % NAB], crank - 2u));
-        }
-        // ------------------------------------------------------------- epilogue
-        // The accumulator rows leave through TMA tensor stores: each warp stages 32 rows x 32
-        // columns (128-byte swizzled, 4 KB, double-buffered in the now idle stationary-tile
-        // region) and stores the box into the rank-major [G][B][chunk][H][acc_ld] accumulator
-        // (5-D map, columns clipped at the role's n2).  Per-thread float4 stores of a row each
-        // (rows 14 KB apart) had left half of every sector unused and ran the epilogue at ~2 TB/s
-        // across the grid (14 us of a 44 us CTA lifetime, tools/attn_bwd_trace.cu spans).
-        if (has_mma2 && p.acc_out[role] != nullptr) {
-            ptx::mbar_wait(&bars->acc_full, 0);
-            ptx::tc_fence_after();
-            if (warp == 2 && lane == 0) span_mark(1);
-            // staging overwrites the exchange buffers for small widths: warp 2's wait on the last
-            // dS store (above) precedes this barrier
-            named_bar_sync(1, 256);
-            const int n32 = (rd.n2 + 31) / 32;
-            const int lo = half ? (n32 + 1) / 2 : 0, hi = half ? n32 : (n32 + 1) / 2;
-            const int bb = bh / p.H, hh = bh - bb * p.H;
-            const int wrow0 = r0 + quad * 32;  // first row of this warp's boxes
-            const bool store_rows = wrow0 < p.Lrow;
-            const int g = store_rows ? wrow0 / p.stat_chunk : 0, gi = wrow0 - g * p.stat_chunk;
-            uint8_t* stage = smem + sw * 8192;  // two 4 KB boxes per warp
-            const CUtensorMap* mAcc = role ? &accD : &accP;
-            for (int cb = lo; cb < hi; ++cb) {
-                const int nb = (cb - lo) & 1;
-                uint8_t* box = stage + nb * 4096;
-                uint32_t o[2][16];
-                ptx::tmem_ld16(tl + 32 * cb, o[0]);
-                ptx::tmem_ld16(tl + 32 * cb + 16, o[1]);
-                ptx::tmem_wait_ld();
-                if (cb - lo >= 2 && lane == 0) ptx::bulk_wait_group_read<1>();  // box nb's previous store read
-                __syncwarp();
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t* w = &o[k >> 2][(k & 3) * 4];
-                    *reinterpret_cast<uint4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-                        make_uint4(w[0], w[1], w[2], w[3]);
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0 && store_rows) {
-                    ptx::tma_store_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
-                    ptx::bulk_commit_group();
-                }
-            }
-            if (lane == 0) ptx::bulk_wait_group_read<0>();
+            if (t > 0) ptx::mbar_arrive_remote(ptx::mapa(&bars->pin_free[(t - 1) % NAB], crank - 2u));
         }
     }
 
@@ -630,7 +772,7 @@ void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     // (tools/attn_bwd_trace.cu) shows the critical loop MMA1(j) -> B1(j+1) TMA (~1.4k cycles under
     // load) -> MMA1(j+1): B1 in 4-block groups over 3 stages lets the next tile's first group land
     // while MMA1(j) runs.  (kb1 = 0: whole-tile B1 stages)
-    const int plans_kv[][5] = {{3, 2, 2, 4, 32}, {1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
+    const int plans_kv[][5] = {{3, 2, 2, 4, 32}, {2, 2, 2, 4, 32}, {1, 3, 2, 0, 32}, {2, 6, 2, 0, 16}, {1, 6, 2, 0, 16}, {2, 3, 2, 0, 16},
                                {2, 2, 2, 0, 16}, {1, 4, 3, 0, 16}, {1, 6, 3, 0, 16}, {3, 4, 2, 4, 16},
                                {1, 2, 3, 0, 32}, {2, 3, 2, 0, 32}, {2, 2, 2, 0, 32}, {3, 2, 2, 4, 32},
                                {2, 3, 2, 4, 32}, {4, 2, 2, 3, 32}, {6, 2, 2, 2, 32}, {4, 4, 2, 3, 16}};
@@ -661,6 +803,32 @@ void finish_params(BwdParams& p, bool kv, const int* ring = nullptr) {
     throw std::invalid_argument("attention backward: no ring plan fits shared memory");
 }
 
+// 4-CTA clusters of one kernel that fit on the device at once (the persistent grid size), cached
+// per (device, kernel, shared memory).  The occupancy query can report 0 for compile-time cluster
+// dims on some drivers: then 7/8 of SMs / 4 (B200: 33 of 37 4-SM groups fit, the GPCs' odd SMs left
+// over) -- an over-estimate would leave whole clusters waiting for a second round.
+int resident_clusters(const void* kern, int smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, kern, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4 * 1024, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = std::max(1, device_sm_count() * 7 / 32);
+    }
+    cache[key] = n;
+    return n;
+}
+
 template <bool KV, int NS1, int NST2, int NAB, int KB1 = 0, int SL = 16>
 void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const CUtensorMap* maps,
                   cudaStream_t stream) {
@@ -669,8 +837,9 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
     if (smem > 232448) throw std::invalid_argument("attention backward: shared memory budget exceeded");
     auto kern = attn_bwd_kernel<KV, NS1, NST2, NAB, KB1, SL>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int clusters = (p.Lrow + 255) / 256;
-    dim3 grid(static_cast<unsigned>(clusters * 4), static_cast<unsigned>(a.B * d.heads));
+    const int units = p.BH * ((p.Lrow + 255) / 256);
+    const int clusters = std::min(units, resident_clusters(reinterpret_cast<const void*>(kern), smem));
+    dim3 grid(static_cast<unsigned>(clusters * 4), 1u);
     kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
                                            maps[8], p);
 }
@@ -682,6 +851,7 @@ void launch(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, const 
         if (p.kb1 == 4 && p.nst1 == 3) launch_depth<KV, 3, 2, 2, 4, 32>(d, a, p, maps, stream);
         else if (p.kb1 == 3 && p.nst1 == 4) launch_depth<KV, 4, 2, 2, 3, 32>(d, a, p, maps, stream);
         else if (p.kb1 == 2 && p.nst1 == 6) launch_depth<KV, 6, 2, 2, 2, 32>(d, a, p, maps, stream);
+        else if (p.kb1 == 4 && p.nst1 == 2 && p.nst2 == 2) launch_depth<KV, 2, 2, 2, 4, 32>(d, a, p, maps, stream);
         else if (p.kb1 == 4 && p.nst1 == 2) launch_depth<KV, 2, 3, 2, 4, 32>(d, a, p, maps, stream);
         else if (p.nab == 3) launch_depth<KV, 1, 2, 3, 0, 32>(d, a, p, maps, stream);
         else if (p.nst1 == 2 && p.nst2 == 3) launch_depth<KV, 2, 3, 2, 0, 32>(d, a, p, maps, stream);
@@ -765,6 +935,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.col_sharded = 0;
         p.H = d.heads;
         p.B = a.B;
+        p.BH = a.B * d.heads;
         p.role[0] = make_role(d.dqk_mma, d.dv_mma);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma);
         finish_params(p, true, a.ring);
@@ -821,6 +992,7 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.col_sharded = G > 1;
         p.H = d.heads;
         p.B = a.B;
+        p.BH = a.B * d.heads;
         p.role[0] = make_role(d.dqk_mma, nq0);
         p.role[1] = make_role(d.dv_mma, d.dqk_mma - nq0);
         finish_params(p, false, a.ring);

@@ -73,6 +73,20 @@ int main(int argc, char** argv) {
     printf("dS cta2 w2: tile x_full pin_full_ok a_full_arrive\n");
     for (int j = 0; j < nt && j < 64; ++j)
         printf("  %3d %8lld %8lld %8lld\n", j, T(2,2,3,j)-t0, T(2,2,9,j)-t0, T(2,2,10,j)-t0);
+    {
+        std::vector<long long> ut(4 * 16 * 8);
+        cudaMemcpyFromSymbol(ut.data(), g_unit_trace, ut.size() * sizeof(long long));
+        for (int cta : {0, 2}) {
+            const long long u0 = ut[(cta * 16) * 8 + 6];
+            printf("cta%d units: stat_issue stat_full x_full(0) mma2(0) epi_enter acc_full epi_done\n", cta);
+            for (int u = 0; u < 16; ++u) {
+                const long long* e = &ut[(cta * 16 + u) * 8];
+                if (!e[0]) break;
+                printf("  %2d %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", u, e[6] - u0, e[0] - u0, e[2] - u0, e[1] - u0,
+                       e[3] - u0, e[4] - u0, e[5] - u0);
+            }
+        }
+    }
     span_summary("attn_bwd", 4 * ((L + 255) / 256) * int(BH));
     return 0;
 }
