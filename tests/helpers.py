@@ -179,6 +179,39 @@ def emulated_backward(shape, w, batch, dout):
     return np.stack(outs), grads
 
 
+def emulated_forward(cfg, w, s, z1, z2, rot, trans, mask):
+    """Oracle-equivalent layer forward of one sample at large L (tests/bwd_emulation.py with
+    EXACT_SPLIT: the lifted-row restatement of fipa_oracle.flash_ipa_forward, query-blocked)."""
+    import bwd_emulation as be
+
+    mask = np.asarray(mask, bool)
+    if not mask.any():
+        return np.zeros_like(s)
+    prev = be.EXACT_SPLIT
+    be.EXACT_SPLIT = True
+    try:
+        trans_c = trans - trans[mask].mean(0)
+        pk = be.pack(cfg, w, s, z1, z2, rot, trans_c, mask)
+        o_hat, _ = be.attention(pk["q_hat"], pk["k_hat"], pk["v_hat"], s.shape[0])
+        feat, _ = be.epilogue(cfg, o_hat, z1, rot, trans_c)
+    finally:
+        be.EXACT_SPLIT = prev
+    out = feat @ w["w_out"] + w["b_out"]
+    return np.where(mask[:, None], out, 0.0)
+
+
+def emulated_trunk(cfg, layers, backbones, s, z1, z2, rot, trans, mask, layer_input=None):
+    """fipa_oracle.trunk_forward over emulated_forward; layer_input (e.g. round_bf16) is applied
+    to s where each layer reads it (the device casts a layer's input to bf16 for its projection
+    GEMM; the residual stream stays fp32)."""
+    mask = np.asarray(mask, bool)
+    for w, bb in zip(layers, backbones):
+        x = layer_input(s) if layer_input is not None else s
+        s = s + emulated_forward(cfg, w, x, z1, z2, rot, trans, mask)
+        rot, trans = fo.backbone_update(s, rot, trans, mask, bb)
+    return s, rot, trans
+
+
 def gpu_train_device(model, batch, dout):
     """forward_train + backward through the C ABI over torch-owned device buffers.
     Returns (out, grads, workspace, layouts)."""
