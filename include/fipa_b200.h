@@ -346,6 +346,7 @@ typedef struct fipa_tuning {
     int32_t bwd_slice;
     int32_t graphs;
     int32_t micro; /* bf16 device calls: interleaved sample chunks on forked streams (1 = one chain) */
+    int32_t shard_chunks; /* query-row sharding: head chunks of the overlapped K/V gather (0 auto, 1 off) */
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

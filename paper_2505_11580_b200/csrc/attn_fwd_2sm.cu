@@ -64,6 +64,7 @@ struct Attn2Params {
     float* o_save;  // [BH, L, dv_pad] normalised O_hat (fp32) for the backward, or null
     int dv_pad;
     int feat_tma;  // feature blocks written by per-warp TMA stores (fast epilogue shapes)
+    int h0, hc;    // head sub-range [h0, h0 + hc) of every sample (grid.y = B * hc); hc = H: all
 };
 
 struct Bars {
@@ -561,7 +562,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int lane = ptx::lane_id();
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
-    const int bh = blockIdx.y;
+    // (sample, head) of this CTA pair: a head sub-range lets query-row sharding start the heads whose
+    // gathered keys have landed while the rest are still on the wire (comm.cpp)
+    const int bh = static_cast<int>(blockIdx.y / p.hc) * p.H + p.h0 + static_cast<int>(blockIdx.y % p.hc);
     const int q0 = blockIdx.x * BM;
     const int ntiles = (p.Lk + BN - 1) / BN;
     const int qk_steps = p.dqk_mma / 16;
@@ -930,6 +933,9 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     p.lse = a.lse;
     p.o_save = a.o_save;
     p.dv_pad = d.dv_pad;
+    p.h0 = a.hc > 0 ? a.h0 : 0;
+    p.hc = a.hc > 0 ? a.hc : d.heads;
+    if (p.h0 < 0 || p.h0 + p.hc > d.heads) throw std::invalid_argument("attention: head range out of bounds");
     const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
     const CUtensorMap mapQ = make_map_blocks_bf16(a.qhat, a.L, BH, d.dqk_pad, BM, p.n_qkb);
     p.Lk = a.Lk > 0 ? a.Lk : a.L;
@@ -956,7 +962,7 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
                                  : mapV;
     cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int qtiles = (a.L + BM - 1) / BM;
-    dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(BH));
+    dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(a.B * p.hc));
     // fast epilogue with per-warp TMA feature stores: c = d_z = 128, rank 1-2, z1 staged,
     // even n_value (points block a whole number of 16-byte chunks), 16-byte aligned rows
     p.feat_tma = (d.c == 128 && d.d_z == 128 && (d.rank == 1 || d.rank == 2) && p.z1_tma && d.n_value % 2 == 0 &&

@@ -565,11 +565,13 @@ public:
         d["f32_tc"] = t.f32_tc != 0;
         d["graphs"] = t.graphs != 0;
         d["micro"] = t.micro;
+        d["shard_chunks"] = t.shard_chunks;
         return d;
     }
     // Keyword-wise update of the layer's tuning knobs (fipa_layer_set_tuning); None keeps a value.
     void set_tuning(py::object attn_impl, py::object fused_pack, py::object bwd_ds, py::object bwd_ring,
-                    py::object pass_ring, py::object f32_tc, py::object graphs, py::object micro) {
+                    py::object pass_ring, py::object f32_tc, py::object graphs, py::object micro,
+                    py::object shard_chunks) {
         fipa_tuning t{};
         check(fipa_layer_get_tuning(layer_, &t));
         if (!attn_impl.is_none()) {
@@ -585,6 +587,7 @@ public:
         if (!f32_tc.is_none()) t.f32_tc = f32_tc.cast<bool>() ? 1 : 0;
         if (!graphs.is_none()) t.graphs = graphs.cast<bool>() ? 1 : 0;
         if (!micro.is_none()) t.micro = micro.cast<int>();
+        if (!shard_chunks.is_none()) t.shard_chunks = shard_chunks.cast<int>();
         auto ring = [](py::object o, int32_t* dst, int32_t* extra) {
             if (o.is_none()) return;
             const auto v = o.cast<std::vector<int>>();
@@ -863,7 +866,8 @@ PYBIND11_MODULE(_fipa_b200, m) {
         .def("tuning", &Model::tuning)
         .def("set_tuning", &Model::set_tuning, py::arg("attn_impl") = py::none(), py::arg("fused_pack") = py::none(),
              py::arg("bwd_ds") = py::none(), py::arg("bwd_ring") = py::none(), py::arg("pass_ring") = py::none(),
-             py::arg("f32_tc") = py::none(), py::arg("graphs") = py::none(), py::arg("micro") = py::none())
+             py::arg("f32_tc") = py::none(), py::arg("graphs") = py::none(), py::arg("micro") = py::none(),
+             py::arg("shard_chunks") = py::none())
         .def("stage_times", &Model::stage_times)
         .def("bwd_stage_times", &Model::bwd_stage_times)
         .def_property_readonly("precision", &Model::precision)

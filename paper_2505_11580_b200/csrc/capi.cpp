@@ -378,6 +378,7 @@ int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
         out->bwd_slice = t.bwd_ring[4];
         out->graphs = t.graphs ? 1 : 0;
         out->micro = t.micro;
+        out->shard_chunks = t.shard_chunks;
         for (int i = 0; i < 4; ++i) {
             out->bwd_ring[i] = t.bwd_ring[i];
             out->pass_ring[i] = t.pass_ring[i];
@@ -393,6 +394,8 @@ int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in) {
         if (in->micro < 1 || in->micro > 4) throw fipa_b200::ValueError("tuning: micro must be 1..4");
         fipa_b200::Tuning t = L(layer).tuning();  // fields not in fipa_tuning (host_chunk) kept
         t.micro = in->micro;
+        if (in->shard_chunks < 0 || in->shard_chunks > 7) throw fipa_b200::ValueError("tuning: shard_chunks must be 0..7");
+        t.shard_chunks = in->shard_chunks;
         t.attn = static_cast<fipa_b200::Tuning::Attn>(in->attn_impl);
         t.fused_pack = in->fused_pack != 0;
         t.bwd_ds = in->bwd_ds;

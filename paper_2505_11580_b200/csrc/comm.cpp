@@ -11,10 +11,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
 
+#include "kernels.hpp"
 #include "layer.hpp"
 
 namespace fipa_b200 {
@@ -32,6 +34,11 @@ struct NcclApi {
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                   cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    // point-to-point (optional: the overlapped gather falls back to one all-gather without them)
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -55,6 +62,10 @@ const NcclApi& nccl() {
         api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
         api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
         if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.AllReduce ||
             !api.ReduceScatter) {
             err = "NCCL library lacks required symbols";
@@ -108,6 +119,36 @@ void Comm::all_gather_bytes(const void* send, void* recv, std::size_t bytes, cud
                "ncclAllGather");
 }
 
+bool Comm::has_p2p() const {
+    const auto& a = nccl();
+    return a.Send && a.Recv && a.GroupStart && a.GroupEnd;
+}
+
+void Comm::all_gather_pieces(const void* send, void* recv, std::size_t piece, int pieces, std::size_t stride,
+                             std::size_t rank_stride, cudaStream_t stream) {
+    const auto& a = nccl();
+    const char* src = static_cast<const char*>(send);
+    char* dst = static_cast<char*>(recv);
+    // own blocks: device copies; peers: one grouped send / recv per block and peer
+    for (int k = 0; k < pieces; ++k)
+        cuda_check(cudaMemcpyAsync(dst + std::size_t(rank_) * rank_stride + k * stride, src + k * stride, piece,
+                                   cudaMemcpyDeviceToDevice, stream),
+                   "gather copy");
+    if (world_ == 1) return;
+    if (!has_p2p()) throw CommError("NCCL point-to-point symbols unavailable");
+    auto comm = static_cast<ncclComm_t>(comm_);
+    nccl_check(a.GroupStart(), "ncclGroupStart");
+    for (int g = 0; g < world_; ++g) {
+        if (g == rank_) continue;
+        for (int k = 0; k < pieces; ++k) {
+            nccl_check(a.Send(src + k * stride, piece, ncclUint8, g, comm, stream), "ncclSend");
+            nccl_check(a.Recv(dst + std::size_t(g) * rank_stride + k * stride, piece, ncclUint8, g, comm, stream),
+                       "ncclRecv");
+        }
+    }
+    nccl_check(a.GroupEnd(), "ncclGroupEnd");
+}
+
 void Comm::reduce_scatter_sum_f32(const float* send, float* recv, std::size_t n, cudaStream_t stream) {
     nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), stream),
                "ncclReduceScatter");
@@ -144,6 +185,70 @@ std::size_t FlashIpaLayer::sharded_train_workspace_size(std::int64_t B, std::int
     return carve_sharded(nullptr, B, L, groups, true).bytes;
 }
 
+// Stage 2 of the sharded forward with the K/V all-gather overlapped: the packed rows go out in head
+// chunks on a side stream (grouped send / recv straight into the [G][B*H][L][pad] gathered layout)
+// and the attention of chunk c starts as soon as its keys have landed, while chunks c+1.. are on
+// the wire; the output projection follows the last chunk.  One chunk (or no point-to-point NCCL,
+// or a non-pair attention kernel): one all-gather of each tensor, then the attention.
+void FlashIpaLayer::gather_and_attend(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                                      const float* z2, const float* rot, const float* trans,
+                                      const std::uint8_t* mask, float* out, void* workspace,
+                                      const ShardedWorkspace& ws, bool train, cudaStream_t stream) {
+    const int G = comm.world(), H = dims_.heads;
+    // automatic: nothing to overlap at world 1; otherwise as many chunks (4 or 2) as keep each
+    // chunk's attention launch >= ~6 waves of CTAs (4 chunks of B=8 L=1024 cost 50% in quantisation)
+    int chunks = tuning_.shard_chunks;
+    if (chunks == 0) {
+        chunks = 1;
+        const std::int64_t ctas = B * ((L + 127) / 128);  // per head
+        for (int c : {4, 2})
+            if (G > 1 && H % c == 0 && ctas * (H / c) >= 6 * device_sm_count()) {
+                chunks = c;
+                break;
+            }
+    }
+    chunks = std::min(chunks, 7);  // comm_ev_[0..6] per chunk
+    const bool pair = train || attention_impl_for_sharding();
+    if (H % chunks != 0 || !pair || (G > 1 && !comm.has_p2p())) chunks = 1;
+    ShardStage st;
+    st.k_all = ws.k_all;
+    st.v_all = ws.v_all;
+    st.groups = G;
+    if (chunks == 1) {
+        comm.all_gather_bytes(ws.local.khat, ws.k_all, ws.kv_bytes, stream);
+        comm.all_gather_bytes(ws.local.vhat, ws.v_all, ws.v_bytes, stream);
+        st.stage = 2;
+        forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, train, &st);
+        return;
+    }
+    ensure_side_streams();
+    for (auto& e : comm_ev_)
+        if (!e) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cudaStream_t cs = side_streams_[0];
+    const int hc = H / chunks;
+    const std::size_t krow = std::size_t(dims_.dqk_pad) * 2, vrow = std::size_t(dims_.dv_pad) * 2;
+    cuda_check(cudaEventRecord(comm_ev_[7], stream), "event record");  // packed rows complete
+    cuda_check(cudaStreamWaitEvent(cs, comm_ev_[7], 0), "stream wait");
+    for (int c = 0; c < chunks; ++c) {
+        const std::size_t ko = std::size_t(c) * hc * L * krow, vo = std::size_t(c) * hc * L * vrow;
+        comm.all_gather_pieces(static_cast<const char*>(ws.local.khat) + ko, static_cast<char*>(ws.k_all) + ko,
+                               hc * L * krow, int(B), std::size_t(H) * L * krow, ws.kv_bytes, cs);
+        comm.all_gather_pieces(static_cast<const char*>(ws.local.vhat) + vo, static_cast<char*>(ws.v_all) + vo,
+                               hc * L * vrow, int(B), std::size_t(H) * L * vrow, ws.v_bytes, cs);
+        cuda_check(cudaEventRecord(comm_ev_[c], cs), "event record");
+    }
+    st.stage = 2;
+    for (int c = 0; c < chunks; ++c) {
+        cuda_check(cudaStreamWaitEvent(stream, comm_ev_[c], 0), "stream wait");
+        st.h0 = c * hc;
+        st.hc = hc;
+        forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, train, &st);
+    }
+    st.stage = 3;
+    st.hc = 0;
+    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, train, &st);
+}
+
 // Sharded training step.  Forward as forward_sharded with the training buffers (fp32 O_hat, lse)
 // kept; the gathered k_hat / v_hat stay in the workspace for the backward.
 void FlashIpaLayer::forward_train_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s,
@@ -161,13 +266,7 @@ void FlashIpaLayer::forward_train_sharded(Comm& comm, std::int64_t B, std::int64
     st.stage = 1;
     st.sums = ws.sums;
     forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, true, &st);
-    comm.all_gather_bytes(ws.local.khat, ws.k_all, ws.kv_bytes, stream);
-    comm.all_gather_bytes(ws.local.vhat, ws.v_all, ws.v_bytes, stream);
-    st.stage = 2;
-    st.k_all = ws.k_all;
-    st.v_all = ws.v_all;
-    st.groups = G;
-    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, true, &st);
+    gather_and_attend(comm, B, L, s, z1, z2, rot, trans, mask, out, workspace, ws, true, stream);
 }
 
 // Backward of the sharded step: the three BwdShard stages joined by a reduce-scatter of the partial
@@ -189,11 +288,22 @@ void FlashIpaLayer::backward_sharded(Comm& comm, std::int64_t B, std::int64_t L,
     sh.dk_part = ws.dk_part;
     sh.dv_part = ws.dv_part;
     sh.stage = 1;
+    // the reduce-scatter of the partial key gradients runs on a side stream as soon as the dK/dV
+    // kernel is done, overlapping the dQ kernel (which neither reads nor writes them)
+    ensure_side_streams();
+    for (auto& e : comm_ev_)
+        if (!e) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cudaStream_t cs = side_streams_[0];
+    sh.kv_done = comm_ev_[5];
     backward(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
              ws.local.bytes, stream, &sh);
+    sh.kv_done = nullptr;
     const std::size_t n = std::size_t(B) * L * dims_.heads * kAccLd;
-    comm.reduce_scatter_sum_f32(ws.dk_part, ws.local.dk_acc, n, stream);
-    comm.reduce_scatter_sum_f32(ws.dv_part, ws.local.dv_acc, n, stream);
+    cuda_check(cudaStreamWaitEvent(cs, comm_ev_[5], 0), "stream wait");
+    comm.reduce_scatter_sum_f32(ws.dk_part, ws.local.dk_acc, n, cs);
+    comm.reduce_scatter_sum_f32(ws.dv_part, ws.local.dv_acc, n, cs);
+    cuda_check(cudaEventRecord(comm_ev_[6], cs), "event record");
+    cuda_check(cudaStreamWaitEvent(stream, comm_ev_[6], 0), "stream wait");
     sh.stage = 2;
     sh.dk_own = ws.local.dk_acc;
     sh.dv_own = ws.local.dv_acc;
@@ -226,13 +336,7 @@ void FlashIpaLayer::forward_sharded(Comm& comm, std::int64_t B, std::int64_t L, 
     st.stage = 1;
     st.sums = ws.sums;
     forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, false, &st);
-    comm.all_gather_bytes(ws.local.khat, ws.k_all, ws.kv_bytes, stream);
-    comm.all_gather_bytes(ws.local.vhat, ws.v_all, ws.v_bytes, stream);
-    st.stage = 2;
-    st.k_all = ws.k_all;
-    st.v_all = ws.v_all;
-    st.groups = G;
-    forward(B, L, s, z1, z2, rot, trans, mask, out, workspace, ws.local.bytes, stream, false, &st);
+    gather_and_attend(comm, B, L, s, z1, z2, rot, trans, mask, out, workspace, ws, false, stream);
 }
 
 }  // namespace fipa_b200

@@ -143,6 +143,7 @@ struct AttnArgs {
     // [kgroups][B*H][kchunk][pad] (shard g = keys g*kchunk ..).  0 = unsharded (Lk = L).
     int Lk = 0, kchunk = 0;
     int pass_ring[4] = {0, 0, 0, 0};  // two-pass kernel: forced ring (kb, kst, vkeys, vst), 0 = automatic
+    int h0 = 0, hc = 0;  // CTA-pair kernel: heads [h0, h0 + hc) of every sample only (hc = 0: all)
 };
 // tcgen05 attention forward with the K4 epilogue fused (split / pair contraction /
 // inverse frame / norms) writing bf16 features.

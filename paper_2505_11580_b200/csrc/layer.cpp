@@ -118,6 +118,7 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_GRAPHS")) t.graphs = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_HOST_CHUNK")) t.host_chunk = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FIPA_MICRO")) t.micro = std::min(4, std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("FIPA_SHARD_CHUNKS")) t.shard_chunks = std::min(8, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
                     &t.bwd_ring[4]);
@@ -798,7 +799,10 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
     REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && bf16_attention_supported(dims_)),
             "query-row sharding needs precision='bf16'");
     const bool do_pack = shard == nullptr || shard->stage == 1;
-    const bool do_attend = shard == nullptr || shard->stage == 2;
+    const bool do_attend = shard == nullptr || shard->stage == 2 || shard->stage == 3;
+    // stage 2 with a head range (hc > 0): that chunk's attention only; stage 3: the output GEMM
+    const bool attn_part = shard == nullptr || shard->stage == 2;
+    const bool out_part = shard == nullptr || shard->stage == 3 || (shard->stage == 2 && shard->hc == 0);
     const Workspace ws = view ? *view : carve(workspace, B, L, train);
     REQUIRE(view != nullptr || (workspace != nullptr && workspace_bytes >= ws.bytes), "workspace too small: need ",
             ws.bytes, " bytes, got ", workspace_bytes);
@@ -905,6 +909,7 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
         return;
     }
     if (cfg_.precision == Precision::bf16) {
+        if (attn_part) {
         AttnArgs aa{};
         aa.qhat = static_cast<const __nv_bfloat16*>(ws.qhat);
         aa.khat = static_cast<const __nv_bfloat16*>(ws.khat);
@@ -926,6 +931,11 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
         }
         for (int i = 0; i < 4; ++i) aa.pass_ring[i] = tuning_.pass_ring[i];
         const AttnImpl impl = train ? AttnImpl::pair : attention_impl(d, tuning_.attn, shard != nullptr);
+        if (shard != nullptr && shard->hc > 0) {
+            REQUIRE(impl == AttnImpl::pair, "head-chunked sharded attention needs the CTA-pair kernel");
+            aa.h0 = shard->h0;
+            aa.hc = shard->hc;
+        }
         if (impl == AttnImpl::pair) {
             launch_attn_fwd_2sm(d, aa, stream);
         } else if (impl == AttnImpl::pass) {
@@ -934,6 +944,8 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
             launch_attn_fwd_tc(d, aa, stream);
         }
         mark(5);
+        }
+        if (out_part) {
         GemmArgs g;
         g.A = static_cast<const __nv_bfloat16*>(ws.feat);
         g.lda = d.feat_ld;
@@ -947,6 +959,7 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
         g.bias = d_bout_;
         g.row_mask = mask;
         launch_gemm_bf16(g, stream);
+        }
     } else if (f32_tensor_cores()) {
         const int64_t BHL = int64_t(B) * d.heads * L;
         const int64_t pq = BHL * d.dqk_pad;
@@ -1253,6 +1266,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
             a.ds_ld = ws.ds_ld;
         }
         launch_attn_bwd(d, a, stream, 1);
+        if (shard != nullptr && shard->kv_done != nullptr) cuda_check(cudaEventRecord(shard->kv_done, stream), "event");
         mark(5);
         launch_attn_bwd(d, a, stream, 2);
     }
@@ -1354,6 +1368,10 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     }  // stage 3
     if (timing_) bwd_timed_once_ = true;
     cuda_check(cudaGetLastError(), "backward launch");
+}
+
+bool FlashIpaLayer::attention_impl_for_sharding() const {
+    return attention_impl(dims_, tuning_.attn, true) == AttnImpl::pair;
 }
 
 // ------------------------------------------------------------ micro-batched capture

@@ -74,6 +74,8 @@ struct Tuning {
                                   // captured CUDA graph per (call kind, shapes, buffers)
     int micro = 2;                // FIPA_MICRO: bf16 device calls captured as this many interleaved
                                   // sample chunks on forked streams (1 = one chain)
+    int shard_chunks = 0;         // FIPA_SHARD_CHUNKS: head chunks of the overlapped K/V all-gather of
+                                  // query-row sharding (0 = automatic: 4, or 2; 1 = one all-gather)
     static Tuning from_env();
 };
 
@@ -111,6 +113,12 @@ public:
     int rank() const { return rank_; }
     void all_reduce_sum_f32(float* buf, std::size_t n, cudaStream_t stream);
     void all_gather_bytes(const void* send, void* recv, std::size_t bytes, cudaStream_t stream);
+    // All-gather of `pieces` equal blocks of `piece` bytes at send + k * stride into recv laid out as
+    // [world][...] with rank blocks rank_stride bytes apart (same offsets): grouped send / recv, so a
+    // head chunk of the packed rows lands in place in the standard gathered layout.
+    bool has_p2p() const;
+    void all_gather_pieces(const void* send, void* recv, std::size_t piece, int pieces, std::size_t stride,
+                           std::size_t rank_stride, cudaStream_t stream);
     // recv[n] = sum over ranks of send[rank_ * n .. ], send holding world() blocks of n floats
     void reduce_scatter_sum_f32(const float* send, float* recv, std::size_t n, cudaStream_t stream);
 
@@ -129,6 +137,9 @@ struct ShardStage {
     const void* k_all = nullptr;   // stage 2
     const void* v_all = nullptr;
     int groups = 1;
+    // stage 2 split over head chunks (gather / attention overlap): hc > 0 runs the attention of
+    // heads [h0, h0 + hc) only, and stage 3 the output projection after the last chunk
+    int h0 = 0, hc = 0;
 };
 
 // Stage of the query-row-sharded backward (rank r owns residues [r L, (r+1) L) of G L):
@@ -142,6 +153,8 @@ struct ShardStage {
 //   -- caller: all-reduce the weight gradients
 struct BwdShard {
     int stage = 1;
+    cudaEvent_t kv_done = nullptr;  // stage 1: recorded once the partial dK/dV are complete (the
+                                    // reduce-scatter may start while the dQ kernel runs)
     int groups = 1;
     const void* k_all = nullptr;  // gathered k_hat / v_hat [G][B*H][L][pad] (stage 1)
     const void* v_all = nullptr;
@@ -298,6 +311,10 @@ public:
                           const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
                           const float* dout, float* ds, float* dz1, float* dz2, float* drot, float* dtrans,
                           float* dweights, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
+    void gather_and_attend(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
+                           const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
+                           float* out, void* workspace, const ShardedWorkspace& ws, bool train, cudaStream_t stream);
+    bool attention_impl_for_sharding() const;
     void forward_sharded(Comm& comm, std::int64_t B, std::int64_t L, const float* s, const float* z1,
                          const float* z2, const float* rot, const float* trans, const std::uint8_t* mask,
                          float* out, void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
@@ -346,6 +363,7 @@ private:
                         float* dz1, float* dz2, float* drot, float* dtrans, float* dweights, void* workspace,
                         std::size_t workspace_bytes, cudaStream_t stream);
     cudaStream_t side_streams_[3] = {};
+    cudaEvent_t comm_ev_[8] = {};  // query-row sharding: per-chunk gather completion, kv_done, rs_done
     cudaEvent_t fork_ev_ = nullptr, join_ev_[3] = {};
     void ensure_side_streams();
 

@@ -92,6 +92,30 @@ def test_nccl_world1_sharded_forward_equals_forward(fipa):
     assert rel_dev(ref_gpu, out.cpu().numpy().astype(np.float64)) < 1e-3
 
 
+@pytest.mark.parametrize("chunks", [2, 4])
+def test_nccl_world1_overlapped_gather_equals_single_gather(fipa, chunks):
+    """The head-chunked gather / attention overlap (K/V rows sent in head chunks on a side stream,
+    attention of chunk c launched once its keys landed, output GEMM after the last) gives the same
+    output, bit for bit, as one all-gather followed by one attention launch."""
+    model = fipa.Model(**MAIN, precision="bf16", seed=6, enforce_head_cap=False)
+    B, L = 2, 256
+    batch = make_batch(MAIN, B, L, seed=61, mask_frac=0.1, bf16=True)
+    t = _dev(batch)
+    comm = fipa.Comm(1, 0, fipa.comm_unique_id(), 0)
+    outs = {}
+    for c in (1, chunks):
+        model.set_tuning(shard_chunks=c)
+        assert model.tuning()["shard_chunks"] == c
+        ws = torch.zeros(model.sharded_workspace_size(B, L, 1), dtype=torch.uint8, device="cuda")
+        out = torch.empty((B, L, MAIN["d_in"]), dtype=torch.float32, device="cuda")
+        model.forward_sharded_device(comm, B, L, t["s"].data_ptr(), t["z1"].data_ptr(), t["z2"].data_ptr(),
+                                     t["rot"].data_ptr(), t["trans"].data_ptr(), t["mask"].data_ptr(),
+                                     out.data_ptr(), ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs[c] = out.cpu().numpy()
+    assert np.array_equal(outs[1], outs[chunks])
+
+
 @pytest.mark.parametrize("n", [256, 1024])
 def test_emulated_sharded_training_matches_unsharded(fipa, n):
     """Query-row-sharded training step for G=2 ranks emulated on one GPU through the

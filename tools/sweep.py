@@ -6,7 +6,8 @@ whole layer time), and the device memory the call needs (workspace bytes + input
 show memory linear in L.  Every rank runs the bf16 tcgen05 path: rank 1-2 the CTA-pair kernel,
 rank 3-4 (lifted widths 560-704) the two-pass CTA-pair kernel (attn_fwd_pass.cu).
 
-    python tools/sweep.py --out profiles/r1_sweep.json
+    python tools/sweep.py --out profiles/r2_sweep.json   (each row carries the SM clocks sampled
+    during its timed reps)
 """
 
 import argparse
@@ -42,15 +43,23 @@ def run(shape, precision, B, L, reps=5):
 
     for _ in range(2):
         step()
+    # enough reps that the clock sampler sees the timed region (>= ~30 ms in total)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    step()
+    b.record(st)
+    b.synchronize()
+    reps = max(reps, min(400, int(30.0 / max(a.elapsed_time(b), 1e-3))))
     times = []
-    for _ in range(reps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        step()
-        b.record(st)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
+    with bench.ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            step()
+            b.record(st)
+            b.synchronize()
+            times.append(a.elapsed_time(b))
     ms = float(np.median(times))
     ok = bool(torch.isfinite(out).all().item())
     io = sum(v.numel() * v.element_size() for v in t.values()) + out.numel() * 4
@@ -58,12 +67,13 @@ def run(shape, precision, B, L, reps=5):
             "residues_per_s": B * L / (ms / 1e3),
             "attn_equiv_tflops": bench.attn_flops(shape, B, L) / (ms / 1e3) / 1e12,
             "workspace_bytes": nbytes, "device_bytes_total": nbytes + io,
-            "bytes_per_residue": (nbytes + io) / (B * L), "finite": ok}
+            "bytes_per_residue": (nbytes + io) / (B * L), "finite": ok, "clocks": clk.summary(),
+            "l2": "flushed (256 MiB write) before every rep"}
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_sweep.json"))
     ap.add_argument("--maxL", type=int, default=65536)
     ap.add_argument("--minL", type=int, default=256)
     ap.add_argument("--ranks", default="1,2,3,4")
