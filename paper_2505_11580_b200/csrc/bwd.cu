@@ -773,6 +773,40 @@ __global__ void scatter_proj_grad_kernel(const float* __restrict__ src, int d_in
     }
 }
 
+// The backward's last launch: the fused projection-weight gradient scattered into w_q .. w_vp
+// (one block per source row, float4 when every segment is 4-aligned) plus the two tiny scalings
+// d(w_bias) = w_l . d(w_l w_bias) and d(gamma_raw) = w_l w_c sigmoid(gamma_raw) . dg (the last
+// block) -- one launch instead of three latency-bound ones.
+__global__ void finish_weight_grads_kernel(const float* __restrict__ src, int d_in, int n_proj, ScatterCols seg,
+                                           float* __restrict__ dst, int vec4, const float* __restrict__ red,
+                                           const float* __restrict__ scale, int H, int dz, float* __restrict__ dw_bias,
+                                           float* __restrict__ dgamma) {
+    const int r = blockIdx.x;
+    if (r == d_in) {  // d(w_bias) [H, dz] and d(gamma_raw) [H]
+        for (int e = threadIdx.x; e < H * dz; e += blockDim.x) dw_bias[e] = red[H + e] * scale[H];
+        for (int e = threadIdx.x; e < H; e += blockDim.x) dgamma[e] = red[e] * scale[e];
+        return;
+    }
+    const float* srow = src + static_cast<int64_t>(r) * n_proj;
+    if (vec4) {
+        for (int c = 4 * threadIdx.x; c < n_proj; c += 4 * blockDim.x) {
+            int i = 0;
+#pragma unroll
+            for (int k = 1; k < 6; ++k) i += c >= seg.col0[k] ? 1 : 0;
+            const int cc = c - seg.col0[i];
+            *reinterpret_cast<float4*>(dst + seg.dst_off[i] + static_cast<int64_t>(r) * seg.width[i] + cc) =
+                *reinterpret_cast<const float4*>(srow + c);
+        }
+        return;
+    }
+    for (int c = threadIdx.x; c < n_proj; c += blockDim.x) {
+        int i = 0;
+#pragma unroll
+        for (int k = 1; k < 6; ++k) i += c >= seg.col0[k] ? 1 : 0;
+        dst[seg.dst_off[i] + static_cast<int64_t>(r) * seg.width[i] + (c - seg.col0[i])] = srow[c];
+    }
+}
+
 __global__ void bwd_recenter_kernel(const float* __restrict__ dtc, const uint8_t* __restrict__ mask,
                                     float* __restrict__ dt, int L) {
     __shared__ float red[4][32];
@@ -871,6 +905,15 @@ void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out,
 void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
                               cudaStream_t stream) {
     scatter_proj_grad_kernel<<<static_cast<unsigned>(d_in), 256, 0, stream>>>(src, d_in, n_proj, seg, dst);
+}
+
+void launch_finish_weight_grads(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
+                                const float* red, const float* scale, int H, int dz, float* dw_bias, float* dgamma,
+                                cudaStream_t stream) {
+    bool vec4 = n_proj % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    for (int i = 0; i < 6; ++i) vec4 = vec4 && seg.col0[i] % 4 == 0 && seg.width[i] % 4 == 0 && seg.dst_off[i] % 4 == 0;
+    finish_weight_grads_kernel<<<static_cast<unsigned>(d_in + 1), 256, 0, stream>>>(src, d_in, n_proj, seg, dst, vec4 ? 1 : 0,
+                                                                                    red, scale, H, dz, dw_bias, dgamma);
 }
 
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {

@@ -235,6 +235,10 @@ struct ScatterCols {
 };
 void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
                               cudaStream_t stream);
+// scatter + d(w_bias) = red[H..] * scale[H], d(gamma_raw) = red[..H] * scale[..H] in one launch
+void launch_finish_weight_grads(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
+                                const float* red, const float* scale, int H, int dz, float* dw_bias, float* dgamma,
+                                cudaStream_t stream);
 // Translation gradient through the per-sample recentring: dt = mask*(dt_c - mean_valid(dt_c)).
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream);
 // acc[i] += x[i]

@@ -1360,10 +1360,9 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
             col0 += seg.width[i];
         }
         seg.dst_off[6] = std::int64_t(woff[6]);
-        launch_scatter_proj_grad(ws.dwproj, d.d_in, d.n_proj, seg, dweights, stream);
+        launch_finish_weight_grads(ws.dwproj, d.d_in, d.n_proj, seg, dweights, ws.red, d_bwd_scale_, H, d.d_z, dw_bias,
+                                   dgamma, stream);
     }
-    launch_scale_vec(ws.red + H, d_bwd_scale_ + H, 1, dw_bias, H * d.d_z, stream);
-    launch_scale_vec(ws.red, d_bwd_scale_, H, dgamma, H, stream);
     mark(11);
     }  // stage 3
     if (timing_) bwd_timed_once_ = true;
