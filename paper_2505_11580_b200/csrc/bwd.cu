@@ -386,20 +386,16 @@ constexpr int kUnpackMaxH = 16;
 //                          dz2 = sum_h (w_l w_bias[h, e % d_z] ln2 dk[zq+e] + dv[c+e]),
 //                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials);
 //                          dg += sum of dg_rows over the block's residues.
-__global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
-    // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
-    // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
-    // heads with one warp reduction; per-head dgamma terms go through shared memory.
-    __shared__ float s_dg[8][kUnpackMaxH];
+// The geometry of one residue (warp-wide; lanes over (head, point) tasks): frame-applied point
+// gradients -> dproj point columns, dR / dt summed over the heads -> drot, dt_c, per-head dgamma
+// terms -> dg_rows.  s_dg: this warp's kUnpackMaxH floats of shared memory.
+__device__ __forceinline__ void unpack_geo_row(const LayerDims& d, const BwdUnpackArgs& a, int64_t row, int lane,
+                                               float* s_dg) {
     const int H = d.heads, c = d.c, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int off_qp = 3 * H * c, off_kp = off_qp + H * Nq * 3, off_vp = off_kp + H * Nq * 3;
     const int g0 = c + 3 * Nq, vpair = c + rdz;
-    const int64_t BL = static_cast<int64_t>(a.B) * a.L;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (lane < kUnpackMaxH) s_dg[warp][lane] = 0.f;
+    if (lane < kUnpackMaxH) s_dg[lane] = 0.f;
     __syncwarp();
-    if (row >= BL) return;
     const int64_t acc_h = a.acc_ld;
     const float* qrow = a.dq_acc + row * H * acc_h;
     const float* krow = a.dk_acc + row * H * acc_h;
@@ -466,7 +462,7 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
 #pragma unroll
             for (int y = 0; y < 3; ++y) dR[3 * x + y] += dB[x] * kp[y];
         }
-        atomicAdd(&s_dg[warp][h], dgh);
+        atomicAdd(&s_dg[h], dgh);
     }
     // ---- value points
     for (int task = lane; task < H * Nv; task += 32) {
@@ -510,7 +506,18 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
         }
     }
     __syncwarp();
-    if (lane < H) a.dg_rows[row * H + lane] = s_dg[warp][lane];
+    if (lane < H) a.dg_rows[row * H + lane] = s_dg[lane];
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
+    // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
+    // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
+    // heads with one warp reduction; per-head dgamma terms go through shared memory.
+    __shared__ float s_dg[8][kUnpackMaxH];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (row < static_cast<int64_t>(a.B) * a.L) unpack_geo_row(d, a, row, lane, s_dg[warp]);
 }
 
 __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
@@ -608,6 +615,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         finish_row(row_begin + rr, L0);
         if (rr + 1 < nrows) finish_row(row_begin + rr + 1, L1);
     }
+
     for (int rr = 0; !fast && rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
         const float* qrow = a.dq_acc + row * H * acc_h;
@@ -886,6 +894,8 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     if (d.heads > kUnpackMaxH) throw std::invalid_argument("bwd_unpack: at most 16 heads");
     if (d.n_query > 32 || d.n_value > 32) throw std::invalid_argument("bwd_unpack: at most 32 points per head");
     const int64_t BL = int64_t(a.B) * a.L;
+    // (running the geometry inside the streaming kernel's group loop measured slower: 0.134 vs
+    // 0.114 ms -- it serialises behind the streaming loads and spills at the 128-register cap)
     bwd_unpack_geo_kernel<<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
