@@ -3,6 +3,7 @@
 // are made from here; numpy arrays are accepted as float64 (other dtypes cast) and results come
 // back as float64, like the reference (bindings.cpp:26-45).
 #include <pybind11/numpy.h>
+#include <sys/mman.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
@@ -15,6 +16,17 @@
 #include "../../include/fipa_b200.h"
 
 namespace py = pybind11;
+
+namespace {
+// Fresh output arrays are first touched by the host pipeline's conversion threads: ask for
+// transparent huge pages (THP "madvise" mode on the GPU boxes) so a 68 MB gradient set costs tens
+// of 2 MB faults instead of ~17k 4 KB ones (measured ~7 ms per 68 MB, tools/host_path_probe.py).
+void hugepage_hint(void* p, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p), huge = uintptr_t(2) << 20;
+    const uintptr_t lo = (a + huge - 1) & ~(huge - 1), hi = (a + bytes) & ~(huge - 1);
+    if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+}
+}  // namespace
 
 namespace {
 
@@ -261,6 +273,7 @@ public:
                                                  : std::vector<py::ssize_t>{L, (py::ssize_t)cfg_.d_in};
         py::array_t<T> out(shape);
         T* op = out.mutable_data();
+        hugepage_hint(op, size_t(out.size()) * sizeof(T));
         int rc;
         {
             py::gil_scoped_release nogil;
@@ -513,6 +526,7 @@ public:
         };
         py::array_t<T> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
                        gt = like(translations);
+        for (auto* a : {&out, &gs, &gz1, &gz2}) hugepage_hint(a->mutable_data(), size_t(a->size()) * sizeof(T));
         const uint64_t nw = fipa_layer_num_weights(layer_);
         py::array_t<T> gw(static_cast<py::ssize_t>(nw));  // weight grads land here directly
         T* gwp = gw.mutable_data();
