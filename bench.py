@@ -504,10 +504,50 @@ def run_ours(args, shape):
             att_ms, tot_ms = float(np.median(att)), float(np.median(tot))
             fl = attn_flops(shape, Bl, Ll)
             peak_l, _, kind_l = load_peaks()
-            attn_long.append({"B": Bl, "L": Ll, "attn_ms": att_ms, "layer_fwd_ms": tot_ms,
-                              "attn_tflops": fl / (att_ms / 1e3) / 1e12, "frac": fl / (att_ms / 1e3) / 1e12 / peak_l,
-                              "peak": peak_l, "peak_kind": f"{kind_l} burst bf16",
-                              "residues_per_s": Bl * Ll / (tot_ms / 1e3), "reps": reps, "clocks": clk_l.summary()})
+            entry = {"B": Bl, "L": Ll, "attn_ms": att_ms, "layer_fwd_ms": tot_ms,
+                     "attn_tflops": fl / (att_ms / 1e3) / 1e12, "frac": fl / (att_ms / 1e3) / 1e12 / peak_l,
+                     "peak": peak_l, "peak_kind": f"{kind_l} burst bf16",
+                     "residues_per_s": Bl * Ll / (tot_ms / 1e3), "reps": reps, "clocks": clk_l.summary()}
+            if train:
+                # attention backward at the same size (training forward + backward, stage events
+                # around the dK/dV kernel and the dQ GEMM / streaming dQ kernel)
+                del wsl
+                wtl = model.train_workspace_size(Bl, Ll)
+                wsl = torch.empty(wtl, dtype=torch.uint8, device=dev)
+                dol = torch.randn((Bl, Ll, shape["d_in"]), dtype=torch.float32, device=dev)
+                gl = {k: torch.empty_like(v) for k, v in tl.items() if k != "mask"}
+                gwl = torch.empty(model.num_weights(), dtype=torch.float32, device=dev)
+
+                def train_l():
+                    model.forward_train_device(Bl, Ll, pl["s"], pl["z1"], pl["z2"], pl["rot"], pl["trans"],
+                                               pl["mask"], ol.data_ptr(), wsl.data_ptr(), wtl, stream.cuda_stream)
+                    model.backward_device(Bl, Ll, pl["s"], pl["z1"], pl["z2"], pl["rot"], pl["trans"], pl["mask"],
+                                          dol.data_ptr(), gl["s"].data_ptr(), gl["z1"].data_ptr(),
+                                          gl["z2"].data_ptr(), gl["rot"].data_ptr(), gl["trans"].data_ptr(),
+                                          gwl.data_ptr(), wsl.data_ptr(), wtl, stream.cuda_stream)
+
+                for _ in range(2):
+                    train_l()
+                torch.cuda.synchronize()
+                model.set_timing(True)
+                bt = []
+                with ClockSampler(gpu_index) as clk_b:
+                    for _ in range(max(3, reps // 2)):
+                        flush.zero_()
+                        train_l()
+                        torch.cuda.synchronize()
+                        bs = model.bwd_stage_times()
+                        bt.append(bs[4] + bs[5])
+                model.set_timing(False)
+                bms = float(np.median(bt))
+                bfl = attn_bwd_flops(shape, Bl, Ll)
+                entry.update({"attn_bwd_ms": bms, "attn_bwd_tflops": bfl / (bms / 1e3) / 1e12,
+                              "attn_bwd_frac": bfl / (bms / 1e3) / 1e12 / peak_l,
+                              "attn_bwd_dq": "GEMM over the materialised dS" if ds_mode(Bl, Ll, shape["heads"])
+                              else "streaming dQ kernel (linear memory)",
+                              "attn_bwd_clocks": clk_b.summary()})
+                del dol, gl, gwl
+            attn_long.append(entry)
             del tl, ol, wsl
         torch.cuda.empty_cache()
 
@@ -568,7 +608,7 @@ def roofline_f32(achieved, flops, peak_bf16, peak_kind):
 
 def ds_mode(B, L, H):
     """Whether the backward materialises dS (layer.hpp FlashIpaLayer::materialize_ds)."""
-    if L > 2048 or B * H * L * ((L + 63) // 64 * 64) * 2 > (1 << 30):
+    if L > 8192 or B * H * L * ((L + 63) // 64 * 64) * 2 > (2 << 30):
         return False
     return os.environ.get("FIPA_BWD_DS", "1") != "0"
 

@@ -329,7 +329,7 @@ int fipa_layer_forward_launches(const fipa_layer* layer);
  *   attn_impl  inference attention kernel: 0 automatic, 1 CTA pair, 2 two-pass, 3 single CTA
  *              (FIPA_ATTN_IMPL = pair | pass | 1sm; a sharded forward never takes 3)
  *   fused_pack 1: fused projection + pack kernel (FIPA_FUSED_PACK=0 -> GEMM + pack kernel)
- *   bwd_ds     materialised-dS backward: -1 automatic (L <= 2048, dS <= 1 GiB), 0 off, 1 on
+ *   bwd_ds     materialised-dS backward: -1 automatic (L <= 8192, dS <= 2 GiB), 0 off, 1 on
  *              within that cap (FIPA_BWD_DS)
  *   bwd_ring   attention-backward ring plan {nst1, nst2, nab, kb1}, zeros = automatic, and
  *   bwd_slice  its B2 slice rows (16 / 32, 0 = any) (FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]")

@@ -636,8 +636,11 @@ bool FlashIpaLayer::f32_tensor_cores() const {
 }
 
 bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L) const {
+    // dS costs B*H*L^2*2 bytes of workspace (quadratic in L): used up to L = 8192 and 2 GiB, where
+    // the dQ GEMM over it is ~3x faster than the streaming dQ kernel's recompute of S, P and dP
+    // (B=2 L=4096: 0.29 vs 0.98 ms); longer sequences keep linear memory with the streaming kernel
     const double bytes = double(B) * dims_.heads * double(L) * double((L + 63) / 64 * 64) * 2.0;
-    if (L > 2048 || bytes > double(1u << 30)) return false;
+    if (L > 8192 || bytes > double(2u << 30)) return false;
     return tuning_.bwd_ds != 0;
 }
 

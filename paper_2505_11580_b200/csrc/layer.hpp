@@ -64,7 +64,7 @@ struct Tuning {
     enum class Attn { automatic = 0, pair = 1, pass = 2, one_sm = 3 };
     Attn attn = Attn::automatic;  // FIPA_ATTN_IMPL = pair | pass | 1sm (inference forward only)
     bool fused_pack = true;       // FIPA_FUSED_PACK = 0: projection GEMM + separate pack kernel
-    int bwd_ds = -1;              // FIPA_BWD_DS: -1 automatic (L <= 2048 and dS <= 1 GiB), 0 off,
+    int bwd_ds = -1;              // FIPA_BWD_DS: -1 automatic (L <= 8192 and dS <= 2 GiB), 0 off,
                                   // 1 on (within the same cap)
     int bwd_ring[5] = {0, 0, 0, 0, 0};  // FIPA_BWD_RING "nst1,nst2,nab,kb1[,slice]" (0 = automatic)
     int pass_ring[4] = {0, 0, 0, 0};  // FIPA_PASS_RING "kb,kst,vkeys,vst"  (0 = automatic)
@@ -193,7 +193,7 @@ public:
     std::size_t train_workspace_size(std::int64_t B, std::int64_t L) const;
     // Short-sequence backward: the dK/dV kernel also writes dS (bf16, B*H*L^2*2 bytes of the
     // training workspace) and dQ is one batched GEMM instead of a second attention pass.  Used
-    // for L <= 2048 and at most 1 GiB of dS; Tuning::bwd_ds = 0 / 1 forces it off / on (within that cap).
+    // for L <= 8192 and at most 2 GiB of dS; Tuning::bwd_ds = 0 / 1 forces it off / on (within that cap).
     bool materialize_ds(std::int64_t B, std::int64_t L) const;
     const Tuning& tuning() const { return tuning_; }
     // Not thread-safe against concurrent calls on the same layer (like weight mutation).
