@@ -607,10 +607,14 @@ def roofline_f32(achieved, flops, peak_bf16, peak_kind):
 
 
 def ds_mode(B, L, H):
-    """Whether the backward materialises dS (layer.hpp FlashIpaLayer::materialize_ds)."""
-    if L > 8192 or B * H * L * ((L + 63) // 64 * 64) * 2 > (2 << 30):
+    """Whether the backward materialises dS (layer.cpp FlashIpaLayer::ds_chunk): the whole matrix up
+    to L = 8192 / 2 GiB, else in query chunks within 2 GiB (at least 256 columns)."""
+    if os.environ.get("FIPA_BWD_DS", "1") == "0":
         return False
-    return os.environ.get("FIPA_BWD_DS", "1") != "0"
+    per_col, cap = B * H * L * 2, int(os.environ.get("FIPA_DS_CAP_MB", "2048")) << 20
+    if L <= 8192 and per_col * ((L + 63) // 64 * 64) <= cap:
+        return True
+    return cap // per_col // 256 * 256 >= 256
 
 
 def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak, peak_sus, peak_kind, traffic,

@@ -347,6 +347,7 @@ typedef struct fipa_tuning {
     int32_t graphs;
     int32_t micro; /* bf16 device calls: interleaved sample chunks on forked streams (1 = one chain) */
     int32_t shard_chunks; /* query-row sharding: head chunks of the overlapped K/V gather (0 auto, 1 off) */
+    int32_t ds_cap_mb;    /* materialised-dS workspace cap in MiB (query chunks beyond it); default 2048 */
 } fipa_tuning;
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out);
 int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in);

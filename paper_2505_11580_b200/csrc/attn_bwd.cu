@@ -72,6 +72,8 @@ struct RoleDims {
 
 struct BwdParams {
     int Lrow, Lcol, H, B, BH;   // rows (keys in KV, queries in Q) / tile columns; BH = B * H
+    int col0, ncol;             // tile columns [col0, col0 + ncol) of this launch (query chunks, KV kernel)
+    int acc_add;                // accumulators reduced into (TMA add) instead of stored: later chunks
     int stat_chunk, col_chunk;  // rows per shard of the stationary / column operands (sharded keys)
     int stat_sharded, col_sharded;  // 1: operand read through the 5-D / 4-D rank-major maps (measured
                                     // ~10% slower per box than the unsharded 4-D / 3-D maps)
@@ -174,6 +176,16 @@ __device__ __forceinline__ void load_vec32(const float* base, int q, int L, floa
     }
 }
 
+// TMA tensor reduction store (fp32 add into global): later query chunks of the materialised-dS
+// backward add their partial dK / dV to the accumulators the first chunk stored
+__device__ __forceinline__ void tma_reduce_add_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                                  int c4) {
+    asm volatile("cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                   "r"(c4)
+                 : "memory");
+}
+
 // NST2: depth of the B2 ring, a compile-time constant -- the slice refill sits on the critical path
 // and a runtime ring index measured ~8% slower (same-box A/B at B=8 L=1024).
 //
@@ -219,7 +231,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const bool leader = prank == 0;
     const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (crank & 2u));
     const RoleDims rd = p.role[role];
-    const int ntiles = (p.Lcol + BN - 1) / BN;
+    const int ntiles = (p.ncol + BN - 1) / BN;
     const int nrb = (p.Lrow + 255) / 256;                // 256-row blocks per (sample, head)
     const int nunits = p.BH * nrb;
     const int cluster = static_cast<int>(blockIdx.x >> 2), nclusters = static_cast<int>(gridDim.x >> 2);
@@ -287,7 +299,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 for (int j = 0; j < ntiles; ++j) {
                     if (it == 0) BTRACE(11, j);
-                    const int key = j * BN + 32 * static_cast<int>(prank);
+                    const int key = p.col0 + j * BN + 32 * static_cast<int>(prank);
                     const int g = p.col_sharded ? key / p.col_chunk : 0;
                     for (int uu = 0; uu < nk1; ++uu, ++n) {
                         const int s = n % kStages1;
@@ -329,7 +341,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                             ptx::tma_load_4d_2sm(dst + (rd.nba + x) * kSliceBox, mB2, &bars->b2_full[s],
                                                  col_b + 64 * x, rloc, bh, g);
                     } else {
-                        const int row = i * kSlice;
+                        const int row = p.col0 + i * kSlice;
                         for (int x = 0; x < rd.nba; ++x)
                             ptx::tma_load_3d_2sm(dst + x * kSliceBox, mB2, &bars->b2_full[s], col_a + 64 * x, row, bh);
                         for (int x = 0; x < rd.nbb; ++x)
@@ -540,7 +552,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && rows_ok) {
-                        ptx::tma_store_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
+                        if (p.acc_add)
+                            tma_reduce_add_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
+                        else
+                            ptx::tma_store_5d(mAcc, box, 32 * cb, hh, gi, bb, g);
                         ptx::bulk_commit_group();
                     }
                 };
@@ -599,7 +614,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             if (!KV && grow < p.Lrow) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
                                                      : __ldg(p.Dvec + vec_base + grow);
             for (int j = 0; j < ntiles; ++j, ++t) {
-                const int c0 = j * BN + 32 * half;  // first tile column of this thread's half
+                const int c0 = p.col0 + j * BN + 32 * half;  // first tile column of this thread's half
                 const int buf = t % NAB;
                 uint8_t* abuf = sA + buf * (BM * 128);
                 uint8_t* arow = abuf + row * 128;
@@ -928,7 +943,12 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
     if (which & 1) {  // KV kernel: P pair K_hat/Q_hat/dO_hat -> dV ; dS pair V_hat/dO_hat/Q_hat -> dK
         BwdParams p{};
         p.Lrow = Lk;  // rows = keys (all shards)
-        p.Lcol = a.L; // tile columns = local queries
+        p.Lcol = a.L; // tile columns = local queries (this launch: [q0, q0 + qn))
+        p.col0 = a.q0;
+        p.ncol = a.qn > 0 ? a.qn : a.L - a.q0;
+        p.acc_add = a.acc_add;
+        if (p.col0 < 0 || p.col0 + p.ncol > a.L || (a.qn > 0 && a.q0 % BN != 0))
+            throw std::invalid_argument("attention backward: query chunk out of range or not 64-aligned");
         p.stat_chunk = kc;
         p.col_chunk = a.L;
         p.stat_sharded = G > 1;
@@ -945,12 +965,13 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.acc_out[1] = a.dk_acc;
         p.acc_ld = a.acc_ld;
         p.ds_store = a.ds != nullptr ? 1 : 0;
-        if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < a.L))
-            throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= L, % 8");
+        if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < p.ncol))
+            throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= chunk, % 8");
+        if (p.acc_add && G > 1) throw std::invalid_argument("attention backward: chunked accumulation is unsharded only");
         const CUtensorMap m0 = stat(a.khat, nqk);
         const CUtensorMap maps[9] = {
             m0, tile(a.qhat, p.kb1), slice(a.dohat, p.slice), stat(a.vhat, nv), tile(a.dohat, p.kb1),
-            slice(a.qhat, p.slice), p.ds_store ? make_map_3d_bf16(a.ds, a.L, a.L, BH, a.ds_ld, 64, BM) : m0,
+            slice(a.qhat, p.slice), p.ds_store ? make_map_3d_bf16(a.ds, p.ncol, a.L, BH, a.ds_ld, 64, BM) : m0,
             a.dv_acc ? acc_map(a.dv_acc, 0, p.role[0].n2, d.heads, kc, a.B, G, a.acc_ld) : m0,
             a.dk_acc ? acc_map(a.dk_acc, 0, p.role[1].n2, d.heads, kc, a.B, G, a.acc_ld) : m0};
         launch<true>(d, a, p, maps, stream);
@@ -960,17 +981,18 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         // one batched tcgen05 GEMM (both operands MN-major) straight into the residue-major
         // [B, L, H, acc_ld] accumulator -- no second pass over S, dP and the softmax
         GemmArgs g{};
+        const int qn = a.qn > 0 ? a.qn : a.L - a.q0;
         g.A = a.ds;
         g.lda = a.ds_ld;
         g.a_mn_major = true;
         g.B = a.khat;
         g.ldb = d.dqk_pad;
         g.b_mn_major = true;
-        g.C = a.dq_acc;
+        g.C = a.dq_acc + int64_t(a.q0) * d.heads * a.acc_ld;  // this chunk's query rows
         g.ldc = int64_t(d.heads) * a.acc_ld;
         g.ldc_h = a.acc_ld;
         g.ldc_b = int64_t(a.L) * d.heads * a.acc_ld;
-        g.M = a.L;
+        g.M = qn;
         g.N = d.dqk_mma;
         g.K = a.L;
         g.batch = static_cast<int>(BH);
@@ -986,6 +1008,8 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         BwdParams p{};
         p.Lrow = a.L;  // rows = local queries
         p.Lcol = Lk;   // tile columns = keys (all shards)
+        p.col0 = 0;
+        p.ncol = Lk;
         p.stat_chunk = a.L;
         p.col_chunk = kc;
         p.stat_sharded = 0;

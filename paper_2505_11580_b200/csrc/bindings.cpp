@@ -580,12 +580,13 @@ public:
         d["graphs"] = t.graphs != 0;
         d["micro"] = t.micro;
         d["shard_chunks"] = t.shard_chunks;
+        d["ds_cap_mb"] = t.ds_cap_mb;
         return d;
     }
     // Keyword-wise update of the layer's tuning knobs (fipa_layer_set_tuning); None keeps a value.
     void set_tuning(py::object attn_impl, py::object fused_pack, py::object bwd_ds, py::object bwd_ring,
                     py::object pass_ring, py::object f32_tc, py::object graphs, py::object micro,
-                    py::object shard_chunks) {
+                    py::object shard_chunks, py::object ds_cap_mb) {
         fipa_tuning t{};
         check(fipa_layer_get_tuning(layer_, &t));
         if (!attn_impl.is_none()) {
@@ -602,6 +603,7 @@ public:
         if (!graphs.is_none()) t.graphs = graphs.cast<bool>() ? 1 : 0;
         if (!micro.is_none()) t.micro = micro.cast<int>();
         if (!shard_chunks.is_none()) t.shard_chunks = shard_chunks.cast<int>();
+        if (!ds_cap_mb.is_none()) t.ds_cap_mb = ds_cap_mb.cast<int>();
         auto ring = [](py::object o, int32_t* dst, int32_t* extra) {
             if (o.is_none()) return;
             const auto v = o.cast<std::vector<int>>();
@@ -881,7 +883,7 @@ PYBIND11_MODULE(_fipa_b200, m) {
         .def("set_tuning", &Model::set_tuning, py::arg("attn_impl") = py::none(), py::arg("fused_pack") = py::none(),
              py::arg("bwd_ds") = py::none(), py::arg("bwd_ring") = py::none(), py::arg("pass_ring") = py::none(),
              py::arg("f32_tc") = py::none(), py::arg("graphs") = py::none(), py::arg("micro") = py::none(),
-             py::arg("shard_chunks") = py::none())
+             py::arg("shard_chunks") = py::none(), py::arg("ds_cap_mb") = py::none())
         .def("stage_times", &Model::stage_times)
         .def("bwd_stage_times", &Model::bwd_stage_times)
         .def_property_readonly("precision", &Model::precision)

@@ -379,6 +379,7 @@ int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
         out->graphs = t.graphs ? 1 : 0;
         out->micro = t.micro;
         out->shard_chunks = t.shard_chunks;
+        out->ds_cap_mb = t.ds_cap_mb;
         for (int i = 0; i < 4; ++i) {
             out->bwd_ring[i] = t.bwd_ring[i];
             out->pass_ring[i] = t.pass_ring[i];
@@ -396,6 +397,8 @@ int fipa_layer_set_tuning(fipa_layer* layer, const fipa_tuning* in) {
         t.micro = in->micro;
         if (in->shard_chunks < 0 || in->shard_chunks > 7) throw fipa_b200::ValueError("tuning: shard_chunks must be 0..7");
         t.shard_chunks = in->shard_chunks;
+        if (in->ds_cap_mb < 1) throw fipa_b200::ValueError("tuning: ds_cap_mb must be >= 1");
+        t.ds_cap_mb = in->ds_cap_mb;
         t.attn = static_cast<fipa_b200::Tuning::Attn>(in->attn_impl);
         t.fused_pack = in->fused_pack != 0;
         t.bwd_ds = in->bwd_ds;

@@ -177,6 +177,11 @@ struct AttnBwdArgs {
     // stores its dS tiles there and dQ becomes one batched GEMM dS^T . K_hat (which & 2).
     __nv_bfloat16* ds = nullptr;
     int ds_ld = 0;
+    // Query chunk of a materialised-dS backward too long for one dS buffer: the dK/dV kernel runs
+    // over queries [q0, q0 + qn) (dS [B*H][L keys][ds_ld] holds that chunk's columns; acc_add: the
+    // chunk's partial dK / dV are added to the accumulators -- every chunk after the first), and the
+    // dQ GEMM writes those query rows.  qn = 0: all queries.
+    int q0 = 0, qn = 0, acc_add = 0;
     int ring[5] = {0, 0, 0, 0, 0};  // forced ring plan (nst1, nst2, nab, kb1, slice rows), 0 = automatic
 };
 bool attn_bwd_supported(const LayerDims& d);

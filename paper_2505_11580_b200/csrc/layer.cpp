@@ -118,6 +118,7 @@ Tuning Tuning::from_env() {
     if (const char* e = std::getenv("FIPA_GRAPHS")) t.graphs = std::string(e) != "0";
     if (const char* e = std::getenv("FIPA_HOST_CHUNK")) t.host_chunk = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FIPA_MICRO")) t.micro = std::min(4, std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("FIPA_DS_CAP_MB")) t.ds_cap_mb = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FIPA_SHARD_CHUNKS")) t.shard_chunks = std::min(8, std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("FIPA_BWD_RING"))
         std::sscanf(e, "%d,%d,%d,%d,%d", &t.bwd_ring[0], &t.bwd_ring[1], &t.bwd_ring[2], &t.bwd_ring[3],
@@ -585,8 +586,8 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
         w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
-        if (materialize_ds(B, L)) {
-            w.ds_ld = static_cast<int>(round_up(static_cast<std::size_t>(L), 64));  // whole 64-column blocks
+        if (const std::int64_t qc = ds_chunk(B, L)) {
+            w.ds_ld = static_cast<int>(qc);  // whole 64-column blocks: all queries, or a query chunk
             w.ds = reinterpret_cast<__nv_bfloat16*>(take(BHL * w.ds_ld * 2));
         }
     }
@@ -635,13 +636,21 @@ bool FlashIpaLayer::f32_tensor_cores() const {
     return cfg_.precision == Precision::f32 && tuning_.f32_tc && attn_fwd_f32tc_supported(dims_);
 }
 
-bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L) const {
-    // dS costs B*H*L^2*2 bytes of workspace (quadratic in L): used up to L = 8192 and 2 GiB, where
-    // the dQ GEMM over it is ~3x faster than the streaming dQ kernel's recompute of S, P and dP
-    // (B=2 L=4096: 0.29 vs 0.98 ms); longer sequences keep linear memory with the streaming kernel
-    const double bytes = double(B) * dims_.heads * double(L) * double((L + 63) / 64 * 64) * 2.0;
-    if (L > 8192 || bytes > double(2u << 30)) return false;
-    return tuning_.bwd_ds != 0;
+bool FlashIpaLayer::materialize_ds(std::int64_t B, std::int64_t L) const { return ds_chunk(B, L) > 0; }
+
+// Query columns of dS held at once by the materialised-dS backward (0: streaming dQ kernel).  dS is
+// B*H*L*cols*2 bytes: the whole [L keys x L queries] matrix up to L = 8192 and 2 GiB, where the dQ GEMM
+// over it is ~3x faster than the streaming kernel's recompute of S, P and dP (B=2 L=4096: 0.29 vs
+// 0.98 ms); beyond, query chunks of a multiple of 256 columns within the same 2 GiB (the dK/dV kernel
+// runs once per chunk, later chunks adding their partial dK / dV by TMA reduction), so the workspace
+// stays linear in L.
+std::int64_t FlashIpaLayer::ds_chunk(std::int64_t B, std::int64_t L) const {
+    if (tuning_.bwd_ds == 0) return 0;
+    const double cap = double(tuning_.ds_cap_mb) * double(1 << 20), per_col = double(B) * dims_.heads * double(L) * 2.0;
+    const std::int64_t full = (L + 63) / 64 * 64;
+    if (L <= 8192 && per_col * double(full) <= cap) return full;
+    const std::int64_t qc = std::int64_t(cap / per_col) / 256 * 256;
+    return qc >= 256 ? std::min(qc, full) : 0;
 }
 
 std::size_t FlashIpaLayer::workspace_size(std::int64_t B, std::int64_t L) const {
@@ -1268,10 +1277,22 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
             a.ds = ws.ds;
             a.ds_ld = ws.ds_ld;
         }
+        if (shard == nullptr && ws.ds != nullptr && ws.ds_ld < L) {
+            // query-chunked materialised dS: dK/dV kernel + dQ GEMM per chunk of ds_ld queries
+            for (int q0 = 0; q0 < int(L); q0 += ws.ds_ld) {
+                a.q0 = q0;
+                a.qn = std::min<int>(ws.ds_ld, int(L) - q0);
+                a.acc_add = q0 > 0 ? 1 : 0;
+                launch_attn_bwd(d, a, stream, 1);
+                launch_attn_bwd(d, a, stream, 2);
+            }
+            mark(5);
+        } else {
         launch_attn_bwd(d, a, stream, 1);
         if (shard != nullptr && shard->kv_done != nullptr) cuda_check(cudaEventRecord(shard->kv_done, stream), "event");
         mark(5);
         launch_attn_bwd(d, a, stream, 2);
+        }
     }
     mark(6);
     }  // stage 1

@@ -74,6 +74,8 @@ struct Tuning {
                                   // captured CUDA graph per (call kind, shapes, buffers)
     int micro = 2;                // FIPA_MICRO: bf16 device calls captured as this many interleaved
                                   // sample chunks on forked streams (1 = one chain)
+    int ds_cap_mb = 2048;         // FIPA_DS_CAP_MB: workspace cap of the materialised dS (query-chunked
+                                  // beyond it; at least 256 columns per chunk, else the streaming kernel)
     int shard_chunks = 0;         // FIPA_SHARD_CHUNKS: head chunks of the overlapped K/V all-gather of
                                   // query-row sharding (0 = automatic: 4, or 2; 1 = one all-gather)
     static Tuning from_env();
@@ -195,6 +197,7 @@ public:
     // training workspace) and dQ is one batched GEMM instead of a second attention pass.  Used
     // for L <= 8192 and at most 2 GiB of dS; Tuning::bwd_ds = 0 / 1 forces it off / on (within that cap).
     bool materialize_ds(std::int64_t B, std::int64_t L) const;
+    std::int64_t ds_chunk(std::int64_t B, std::int64_t L) const;
     const Tuning& tuning() const { return tuning_; }
     // Not thread-safe against concurrent calls on the same layer (like weight mutation).
     void set_tuning(const Tuning& t) {

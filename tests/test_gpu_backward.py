@@ -177,7 +177,7 @@ def test_flash_grad_host_api_matches_device(fipa):
         assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
 
 
-def _check_large(fipa, B, L, seed, mask_frac, bwd_ds=None, oracle_samples=()):
+def _check_large(fipa, B, L, seed, mask_frac, bwd_ds=None, oracle_samples=(), ds_cap_mb=None):
     """Large-L parity: forward output and all 15 gradients against the oracle-equivalent blocked
     emulation (helpers.emulated_backward: EXACT_SPLIT lifted restatement of the oracle backward,
     equal to it within 1e-14), plus the dense f64 oracle itself on `oracle_samples` (per-sample
@@ -187,6 +187,8 @@ def _check_large(fipa, B, L, seed, mask_frac, bwd_ds=None, oracle_samples=()):
     model = _model(fipa, MAIN, seed)
     if bwd_ds is not None:
         model.set_tuning(bwd_ds=bwd_ds)
+    if ds_cap_mb is not None:
+        model.set_tuning(ds_cap_mb=ds_cap_mb)
     w = oracle_weights_for(model, "bf16")
     batch = make_batch(MAIN, B, L, seed=seed, mask_frac=mask_frac, bf16=True)
     dout = np.random.default_rng(seed + 1).standard_normal((B, L, MAIN["d_in"]))
@@ -214,16 +216,36 @@ def test_backward_bench_config(fipa):
 
 @pytest.mark.parametrize("ds", [0, 1])
 def test_backward_L2048(fipa, ds):
-    """L = 2048, the largest materialised-dS length, and the streaming dQ kernel at the same size."""
+    """L = 2048 through the materialised-dS path and the streaming dQ kernel."""
     _check_large(fipa, 1, 2048, seed=2048, mask_frac=0.1, bwd_ds=ds)
 
 
-def test_backward_L4096_streaming_dq(fipa):
-    """L = 4096: beyond the materialised-dS cap, so the streaming dQ attention kernel runs (the
-    path every L > 2048 and all sharded training takes)."""
-    model = _model(fipa, MAIN, 0)
-    assert model.tuning()["bwd_ds"] == -1
-    _check_large(fipa, 1, 4096, seed=4096, mask_frac=0.05)
+@pytest.mark.parametrize("ds", [0, 1])
+def test_backward_L4096(fipa, ds):
+    """L = 4096: the materialised-dS path (the default up to L = 8192 / 2 GiB of dS) and the
+    streaming dQ attention kernel (the path of every sharded training step)."""
+    _check_large(fipa, 1, 4096, seed=4096, mask_frac=0.05, bwd_ds=ds)
+
+
+@pytest.mark.parametrize("cap_mb", [8, 20])
+def test_backward_query_chunked_ds(fipa, cap_mb):
+    """Query-chunked materialised dS (the default beyond L = 8192 or 2 GiB, forced here with a small
+    cap: 256- / 512-column chunks at B=2 L=1024): dK/dV accumulated over the chunks by TMA reduction,
+    dQ one GEMM per chunk -- against the oracle-equivalent checker, and against the single-buffer
+    path far inside the gate (fp32 summation order differs)."""
+    errs = _check_large(fipa, 2, 1024, seed=77, mask_frac=0.1, ds_cap_mb=cap_mb)
+    model = _model(fipa, MAIN, 77)
+    batch = make_batch(MAIN, 2, 1024, seed=77, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(78).standard_normal((2, 1024, MAIN["d_in"]))
+    _, g_full, _, _ = gpu_train_device(model, batch, dout)
+    model.set_tuning(ds_cap_mb=cap_mb)
+    assert model.tuning()["ds_cap_mb"] == cap_mb
+    _, g_chunk, _, _ = gpu_train_device(model, batch, dout)
+    for n in GRADS:
+        # fp32 summation order of dK / dV differs; a bf16 rounding of dproj that flips moves the input
+        # gradients by ~1e-4 relative -- far inside the 2e-2 gate both paths pass above
+        assert rel_dev(g_full[n], g_chunk[n]) < 1e-3, n
+    assert errs
 
 
 def test_host_paths_pipelined_and_float32(fipa):
