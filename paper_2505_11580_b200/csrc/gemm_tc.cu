@@ -30,10 +30,12 @@ struct GemmCfg {
     // Output staging buffers per epilogue warp: 2 keep up once the epilogue math is branch-free
     // (tools/gemm_bench.cu: 4 buffers at the cost of ring stages measured no faster on the
     // short-K shapes and 13% slower on a square 8192^3 product).
-    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kStages = BN > 128 ? 4 : 6;
     static constexpr int kCBuf = 2;
     static constexpr int kABytes = BM * 128;
-    static constexpr int kBBytes = BN * 128;
+    // B rows of whole 64-element (128-byte) blocks: BN = 224 stages four blocks, the MMA reads 3.5
+    static constexpr int kBBlocks = (BN + 63) / 64;
+    static constexpr int kBBytes = kBBlocks * 64 * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStageC = 4 * kCBuf * 32 * 128;  // fp32 output staging: 4 warps x kCBuf x (32 rows x 128 B)
     static constexpr int kSmem = kStages * kStageBytes + kStageC + 1024 /*align*/ + 256 /*barriers*/;
@@ -104,7 +106,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         kb0 = static_cast<int>((int64_t(nk_all) * z) / p.split_k);
         nk = static_cast<int>((int64_t(nk_all) * (z + 1)) / p.split_k) - kb0;
     };
-    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    // power-of-two allocation covering the double-buffered accumulator (2 x 224 -> 512)
+    constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&mapA);
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (B_MN && p.b_blk) {
                         ptx::tma_load_4d(sb, &mapB, &full[s], 0, kc, n0 / 64, zb);
                     } else if (B_MN) {
-                        for (int nb = 0; nb < BN / 64; ++nb)
+                        for (int nb = 0; nb < Cfg::kBBlocks; ++nb)
                             ptx::tma_load_3d(sb + nb * 64 * 128, &mapB, &full[s], n0 + nb * 64, kc, zb);
                     } else {
                         ptx::tma_load_3d(sb, &mapB, &full[s], kc, n0, zb);
@@ -358,7 +361,7 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
     // MN-major operands whose row stride is a whole number of 64-column blocks (and covers the
     // tile's columns) come in as ONE 4-D box {64, BK, tile/64 blocks} per stage
     const bool a_blk = A_MN && a.lda % 64 == 0 && a.lda >= a.M;
-    const bool b_blk = B_MN && a.ldb % 64 == 0 && a.ldb >= a.N;
+    const bool b_blk = B_MN && BN % 64 == 0 && a.ldb % 64 == 0 && a.ldb >= a.N;
     CUtensorMap mapA, mapB;
     if constexpr (TF32) {
         mapA = make_map_3d_f32(a.A, a.K, a.M, nb, a.lda, 32, BM);
@@ -437,9 +440,11 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
                         (reinterpret_cast<uintptr_t>(a.C) & 15) != 0))
         throw std::invalid_argument("gemm: batched products write plain, 16-byte aligned fp32 C");
     // 256-wide tiles halve the shared-memory traffic per MMA (A is re-read per N tile); batched
-    // products with N in (256, 512] (dQ: N = 432) cover N with two of them
-    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512) || (a.batch > 1 && a.N > 256 && a.N <= 512);
+    // products with N in (256, 512] (dQ: N = 432) cover N with two of them.  (Two 224-wide tiles
+    // compute 448 instead of 512 columns but measured slower: dQ 0.073 -> 0.076 ms at B=8 L=1024,
+    // their B operand needs four 3-D TMA boxes per stage instead of one 4-D box.)
     const int sel = (a.a_mn_major ? 1 : 0) | (a.b_mn_major ? 2 : 0);
+    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512) || (a.batch > 1 && a.N > 256 && a.N <= 512);
     if (wide) {
         switch (sel) {
             case 0: return launch_impl<256, false, false>(a, stream);
