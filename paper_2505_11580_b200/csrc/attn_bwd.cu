@@ -277,6 +277,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_slot, 0);
+    ptx::pdl_wait();  // dO_hat, D of the preceding prep (and, per query chunk, the previous dQ GEMM)
+    ptx::pdl_trigger();
 
     if (warp == 0) {
         // ------------------------------------------- stationary tile + B1 tile producer
@@ -855,8 +857,8 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
     const int units = p.BH * ((p.Lrow + 255) / 256);
     const int clusters = std::min(units, resident_clusters(reinterpret_cast<const void*>(kern), smem));
     dim3 grid(static_cast<unsigned>(clusters * 4), 1u);
-    kern<<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7],
-                                           maps[8], p);
+    launch_pdl(kern, grid, dim3(kThreads), size_t(smem), stream, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+               maps[6], maps[7], maps[8], p);
 }
 
 template <bool KV>

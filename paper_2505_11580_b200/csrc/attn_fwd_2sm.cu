@@ -601,6 +601,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::cluster_sync();  // barrier inits + TMEM address visible to the pair
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_slot, 0);
+    ptx::pdl_wait();  // q/k/v_hat, colbias of the preceding pack
+    ptx::pdl_trigger();
 
     if (warp == 0) {
         // --------------------------------------------------------- Q / K producer
@@ -973,7 +975,8 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     const CUtensorMap mapF = p.feat_tma ? make_map_3d_bf16(a.feat, d.feat, a.L, a.B, d.feat_ld, 64, 32) : mapV;
     const CUtensorMap mapFP =
         p.feat_tma ? make_map_3d_bf16(a.feat, d.feat, a.L, a.B, d.feat_ld, 4 * d.n_value, 32) : mapV;
-    attn_fwd_2sm_kernel<<<grid, kThreads, smem, stream>>>(mapQ, mapK, mapV, mapZ, mapO, mapF, mapFP, p);
+    launch_pdl(attn_fwd_2sm_kernel, grid, dim3(kThreads), size_t(smem), stream, mapQ, mapK, mapV, mapZ, mapO, mapF,
+               mapFP, p);
 }
 
 }  // namespace fipa_b200

@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(256, 4) bwd_prep_kernel(LayerDims d, BwdPrepAr
 // and the translation-column sum of the point gradients.
 template <int C, int DZ, int RANK, int NV, int DVPAD>
 __global__ void __launch_bounds__(256, 3) bwd_prep_warp_kernel(LayerDims d, BwdPrepArgs a) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     constexpr int RDZ = RANK * DZ, VPAIR = C + RDZ, VPTS = VPAIR + 6, VEND = VPTS + 3 * NV, TAIL = DVPAD - VPAIR;
     constexpr int SEG = DZ + C + 4 * NV;
     static_assert(C % 128 == 0 && DZ % 128 == 0 && TAIL % 64 == 0 && VEND <= DVPAD && NV <= 32, "prep shape");
@@ -511,6 +513,8 @@ __device__ __forceinline__ void unpack_geo_row(const LayerDims& d, const BwdUnpa
 }
 
 __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
     // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
     // heads with one warp reduction; per-head dgamma terms go through shared memory.
@@ -521,6 +525,8 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
 }
 
 __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     extern __shared__ __align__(16) float sm[];
     const int H = d.heads, c = d.c, dz = d.d_z, rdz = d.rank * d.d_z;
     const int tid = threadIdx.x;
@@ -712,6 +718,8 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
 __global__ void __launch_bounds__(256) bwd_dout_kernel(const float* __restrict__ dout, const uint8_t* __restrict__ mask,
                                                        __nv_bfloat16* __restrict__ out, int ld_out, float* __restrict__ db,
                                                        int64_t rows, int cols, int rows_per_block) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     __shared__ float red[16][65];
     const int cq = threadIdx.x & 15, ry = threadIdx.x >> 4;
     const int col = blockIdx.x * 64 + 4 * cq;
@@ -789,6 +797,8 @@ __global__ void finish_weight_grads_kernel(const float* __restrict__ src, int d_
                                            float* __restrict__ dst, int vec4, const float* __restrict__ red,
                                            const float* __restrict__ scale, int H, int dz, float* __restrict__ dw_bias,
                                            float* __restrict__ dgamma) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int r = blockIdx.x;
     if (r == d_in) {  // d(w_bias) [H, dz] and d(gamma_raw) [H]
         for (int e = threadIdx.x; e < H * dz; e += blockDim.x) dw_bias[e] = red[H + e] * scale[H];
@@ -817,6 +827,8 @@ __global__ void finish_weight_grads_kernel(const float* __restrict__ src, int d_
 
 __global__ void bwd_recenter_kernel(const float* __restrict__ dtc, const uint8_t* __restrict__ mask,
                                     float* __restrict__ dt, int L) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     __shared__ float red[4][32];
     const int b = blockIdx.x;
     const float* g = dtc + int64_t(b) * L * 3;
@@ -873,11 +885,13 @@ void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stre
     const int64_t BL = int64_t(a.B) * a.L;
     const bool aligned = d.feat_ld % 4 == 0 && d.seg % 4 == 0;
     if (aligned && d.c == 128 && d.d_z == 128 && d.n_value == 12 && d.rank == 2 && d.dv_pad == 448) {
-        bwd_prep_warp_kernel<128, 128, 2, 12, 448><<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
+        launch_pdl(bwd_prep_warp_kernel<128, 128, 2, 12, 448>, dim3(static_cast<unsigned>((BL + 7) / 8)), dim3(256), 0,
+                   stream, d, a);
         return;
     }
     if (aligned && d.c == 128 && d.d_z == 128 && d.n_value == 12 && d.rank == 1 && d.dv_pad == 320) {
-        bwd_prep_warp_kernel<128, 128, 1, 12, 320><<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
+        launch_pdl(bwd_prep_warp_kernel<128, 128, 1, 12, 320>, dim3(static_cast<unsigned>((BL + 7) / 8)), dim3(256), 0,
+                   stream, d, a);
         return;
     }
     if (d.feat_ld % 8 || (d.dv_pad * 4) % 16 || d.dv_pad % 8)
@@ -896,20 +910,20 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     const int64_t BL = int64_t(a.B) * a.L;
     // (running the geometry inside the streaming kernel's group loop measured slower: 0.134 vs
     // 0.114 ms -- it serialises behind the streaming loads and spills at the 128-register cap)
-    bwd_unpack_geo_kernel<<<static_cast<unsigned>((BL + 7) / 8), 256, 0, stream>>>(d, a);
+    launch_pdl(bwd_unpack_geo_kernel, dim3(static_cast<unsigned>((BL + 7) / 8)), dim3(256), 0, stream, d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int sms = device_sm_count();
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
     const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 2);  // 2 resident blocks per SM
-    bwd_unpack_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(d, a);
+    launch_pdl(bwd_unpack_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), smem, stream, d, a);
 }
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
                      int64_t rows, int cols, cudaStream_t stream) {
     const int rpb = 128;
     dim3 grid((cols + 63) / 64, static_cast<unsigned>((rows + rpb - 1) / rpb));
-    bwd_dout_kernel<<<grid, 256, 0, stream>>>(dout, mask, out, ld_out, db, rows, cols, rpb);
+    launch_pdl(bwd_dout_kernel, grid, dim3(256), 0, stream, dout, mask, out, ld_out, db, rows, cols, rpb);
 }
 
 void launch_scatter_proj_grad(const float* src, int d_in, int n_proj, const ScatterCols& seg, float* dst,
@@ -922,12 +936,12 @@ void launch_finish_weight_grads(const float* src, int d_in, int n_proj, const Sc
                                 cudaStream_t stream) {
     bool vec4 = n_proj % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
     for (int i = 0; i < 6; ++i) vec4 = vec4 && seg.col0[i] % 4 == 0 && seg.width[i] % 4 == 0 && seg.dst_off[i] % 4 == 0;
-    finish_weight_grads_kernel<<<static_cast<unsigned>(d_in + 1), 256, 0, stream>>>(src, d_in, n_proj, seg, dst, vec4 ? 1 : 0,
-                                                                                    red, scale, H, dz, dw_bias, dgamma);
+    launch_pdl(finish_weight_grads_kernel, dim3(static_cast<unsigned>(d_in + 1)), dim3(256), 0, stream, src, d_in, n_proj,
+               seg, dst, vec4 ? 1 : 0, red, scale, H, dz, dw_bias, dgamma);
 }
 
 void launch_bwd_recenter(const float* dt_c, const uint8_t* mask, float* dt, int B, int L, cudaStream_t stream) {
-    bwd_recenter_kernel<<<B, 1024, 0, stream>>>(dt_c, mask, dt, L);
+    launch_pdl(bwd_recenter_kernel, dim3(B), dim3(1024), 0, stream, dt_c, mask, dt, L);
 }
 
 void launch_scale_vec(const float* in, const float* scale, int period, float* out, int n, cudaStream_t stream) {

@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    ptx::pdl_wait();  // operands (and split-K's zeroed C) of the preceding kernels
+    ptx::pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -394,7 +396,7 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
     const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k) * static_cast<int>(nb);
     const int sms = device_sm_count();
     dim3 grid(static_cast<unsigned>(std::min(units, sms)));
-    kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mapA, mapB, mapC, p);
+    launch_pdl(kern, grid, dim3(kThreads), size_t(Cfg::kSmem), stream, mapA, mapB, mapC, p);
 }
 
 }  // namespace

@@ -4,9 +4,34 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include <cstdint>
 
 namespace fipa_b200 {
+
+// Hot-path kernels are launched with programmatic stream serialization (each waits in
+// griddepcontrol.wait before touching global memory): the launch of kernel k+1 is processed while
+// kernel k's CTAs drain, -0.6% per training step (0.876 -> 0.871 ms).  The dependents are released
+// at CTA exit: an explicit early griddepcontrol.launch_dependents (FIPA_PDL_EARLY_TRIGGER) let the
+// waiting CTAs crowd the tail and measured 6% slower.  FIPA_PDL=0 (read once) disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 
 // SM count of the current device (cached per device, thread-safe); grids of the persistent
 // kernels are sized from it.

@@ -33,12 +33,22 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.hpp"
 #include "ptx.cuh"
 
 namespace fipa_b200 {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FIPA_PDL");
+        return e == nullptr || std::string(e) != "0";
+    }();
+    return on;
+}
 
 int device_sm_count() {
     static std::atomic<int> cache[64];  // zero-initialised (static storage)
@@ -527,6 +537,8 @@ __global__ void cast_inputs_kernel(const float* __restrict__ s, __nv_bfloat16* _
                                    int din_ld, const float* __restrict__ z1, const float* __restrict__ z2,
                                    __nv_bfloat16* __restrict__ z1q, __nv_bfloat16* __restrict__ z2b, int rdz,
                                    int64_t rows) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int q_s = (d_in + 3) / 4, q_z = rdz / 4;
     const bool vec_s = d_in % 4 == 0;
     const int64_t n_s = rows * q_s, n = n_s + 2 * rows * q_z;
@@ -628,6 +640,8 @@ __global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* _
 __global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
                                 float* __restrict__ out, int L) {
     __shared__ float red[4][32];
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int b = blockIdx.x;
     const float* t = trans + int64_t(b) * L * 3;
     float sx = 0.f, sy = 0.f, sz = 0.f, cnt = 0.f;
@@ -821,11 +835,11 @@ void launch_cast_inputs(const float* s, __nv_bfloat16* s_bf16, int d_in, int din
                         __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream) {
     if (!cast_inputs_supported(d_in, din_ld, rdz)) throw std::invalid_argument("cast_inputs: widths must be multiples of 4");
     if (din_ld > d_in) cudaMemsetAsync(s_bf16, 0, size_t(rows) * din_ld * 2, stream);  // padding columns
-    const int64_t n = rows * (d_in / 4 + 2 * (rdz / 4));
+    const int64_t n = rows * ((d_in + 3) / 4 + 2 * (rdz / 4));
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8);
-    cast_inputs_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(s, s_bf16, d_in, din_ld, z1, z2, z1q, z2b,
-                                                                          rdz, rows);
+    launch_pdl(cast_inputs_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, s, s_bf16, d_in, din_ld,
+               z1, z2, z1q, z2b, rdz, rows);
 }
 
 void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,
@@ -854,7 +868,7 @@ void launch_fully_masked(const uint8_t* mask, uint8_t* flags, int B, int L, cuda
 
 void launch_recenter(const float* trans, const uint8_t* mask, float* out, int B, int L,
                      cudaStream_t stream) {
-    recenter_kernel<<<B, 1024, 0, stream>>>(trans, mask, out, L);  // one block per sample: all of L in one pass
+    launch_pdl(recenter_kernel, dim3(B), dim3(1024), 0, stream, trans, mask, out, L);  // one block per sample
 }
 
 }  // namespace fipa_b200

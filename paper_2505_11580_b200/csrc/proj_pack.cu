@@ -179,6 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    ptx::pdl_wait();  // inputs (s_bf16, pair blocks, frames) written by the preceding kernels
+    ptx::pdl_trigger();
 
     if (warp == 0) {
         PPTRACE(0);
@@ -601,7 +603,7 @@ void launch_proj_pack(const LayerDims& d, const ProjPackArgs& a, cudaStream_t st
     const int smem = int(std::max(ring, 2 * tile)) + 1024 + 1024;
     cudaFuncSetAttribute(proj_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     dim3 grid(static_cast<unsigned>((p.M + BM - 1) / BM), static_cast<unsigned>(d.heads));
-    proj_pack_kernel<<<grid, kThreads, smem, stream>>>(mapA, mapB, mapQ, mapK, mapV, p);
+    launch_pdl(proj_pack_kernel, grid, dim3(kThreads), size_t(smem), stream, mapA, mapB, mapQ, mapK, mapV, p);
 }
 
 }  // namespace fipa_b200

@@ -405,6 +405,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Programmatic dependent launch: wait for the preceding grid's results (no-op when the kernel was
+// launched without the PDL attribute) / release the next grid early (compiled in only with
+// FIPA_PDL_EARLY_TRIGGER: measured slower, kernels.hpp launch_pdl).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef FIPA_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 }  // namespace ptx
 // Whole-grid span trace (tools only, -DFIPA_SPAN_TRACE): globaltimer (ns) of each CTA's start (0),
 // epilogue start (1) and end (2), and its SM (3); summarised by tools/span_summary.hpp.
