@@ -27,6 +27,11 @@ if which in ("all", "bwd"):
     for ds in (1, 0):
         m.set_tuning(bwd_ds=ds)
         gpu_train_device(m, batch, dout)
+    # query-chunked dS (two 256-query chunks: TMA-reduction accumulators) and the micro-batched capture
+    b2 = make_batch(MAIN, 2, 512, seed=2, mask_frac=0.1, bf16=True)
+    d2 = np.random.default_rng(1).standard_normal((2, 512, MAIN["d_in"]))
+    m.set_tuning(bwd_ds=-1, ds_cap_mb=4, micro=2)
+    gpu_train_device(m, b2, d2)
     print("bwd ok", flush=True)
 if which in ("all", "f32"):
     m = fipa.Model(**MAIN, precision="f32", seed=0, enforce_head_cap=False)
