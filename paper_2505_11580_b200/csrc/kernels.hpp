@@ -296,8 +296,11 @@ void launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStre
 // Same for a [rows, cols] matrix written with row stride ld_out (pad columns left untouched).
 // s -> bf16 [rows, din_ld] plus the pair-factor blocks bf16(log2(e) z1), bf16(z2) of proj_pack.
 bool cast_inputs_supported(int d_in, int din_ld, int rdz);
+// (trans != null: the same launch also recentres the B samples' translations into trans_c)
 void launch_cast_inputs(const float* s, __nv_bfloat16* s_bf16, int d_in, int din_ld, const float* z1, const float* z2,
-                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream);
+                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream,
+                        const float* trans = nullptr, const uint8_t* mask = nullptr, float* trans_c = nullptr,
+                        int B = 0, int L = 0);
 void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, int cols, int ld_out,
                            cudaStream_t stream);
 // Trunk step: s += ipa_out; backbone update of the frames (rot [rows,9], trans [rows,3]) in place.

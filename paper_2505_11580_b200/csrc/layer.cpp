@@ -673,9 +673,10 @@ bool FlashIpaLayer::backward_supported() const {
 }
 
 int FlashIpaLayer::launches_per_backward() const {
-    // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, attn Q, unpack (geometry + streaming),
-    // recenter, ds GEMM, dW_proj GEMM, scatter, two scale kernels (memsets are not kernels of ours)
-    return 14;
+    // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, dQ (GEMM or attention kernel), unpack
+    // (geometry + streaming), recenter, ds GEMM, dW_proj GEMM, finish (scatter + scalings); memsets
+    // are not kernels of ours; a query-chunked dS adds two launches per further chunk
+    return 12;
 }
 
 int FlashIpaLayer::launches_per_forward() const {
@@ -683,8 +684,9 @@ int FlashIpaLayer::launches_per_forward() const {
     // split feat, output GEMM
     if (f32_tensor_cores()) return 10;
     if (cfg_.precision != Precision::bf16) return 5;
-    // recenter, cast, [fused projection+pack | projection GEMM, pack], attention, output GEMM
-    return (proj_pack_supported(dims_) && tuning_.fused_pack) ? 5 : 6;
+    // fused: cast (+ recentre), projection+pack, attention, output GEMM; else recenter, cast,
+    // projection GEMM, pack, attention, output GEMM
+    return (proj_pack_supported(dims_) && tuning_.fused_pack) ? 4 : 6;
 }
 
 void FlashIpaLayer::set_timing(bool on) {
@@ -829,15 +831,18 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
         if (timing_) cuda_check(cudaEventRecord(ev_[i], stream), "cudaEventRecord");
     };
     mark(0);
-    if (shard == nullptr) {
+    const bool fused = do_pack && d_wheads_ != nullptr && tuning_.fused_pack;
+    if (shard == nullptr && !fused) {
         launch_recenter(trans, mask, ws.trans_c, int(B), int(L), stream);
-    } else if (do_pack) {
+    } else if (shard != nullptr && do_pack) {
         launch_recenter_with_sums(trans, shard->sums, ws.trans_c, int(B), int(L), stream);
     }
     mark(1);
-    if (do_pack && d_wheads_ != nullptr && tuning_.fused_pack) {
-        // fused projection GEMM + frame application + packing (proj_pack.cu)
-        launch_cast_inputs(s, ws.s_bf16, d.d_in, d.din_ld, z1, z2, ws.z1q, ws.z2b, d.rank * d.d_z, BL, stream);
+    if (fused) {
+        // fused projection GEMM + frame application + packing (proj_pack.cu); the input cast
+        // also recentres the translations (unsharded)
+        launch_cast_inputs(s, ws.s_bf16, d.d_in, d.din_ld, z1, z2, ws.z1q, ws.z2b, d.rank * d.d_z, BL, stream,
+                           shard == nullptr ? trans : nullptr, mask, ws.trans_c, int(B), int(L));
         mark(2);
         ProjPackArgs pp{};
         pp.s_bf16 = ws.s_bf16;

@@ -529,6 +529,59 @@ __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat1
     }
 }
 
+// Block-wide: translations of sample b minus the centroid of its valid residues.
+__device__ __forceinline__ void recenter_sample(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
+                                                float* __restrict__ out, int L, int b) {
+    __shared__ float red[4][32];
+    const float* t = trans + int64_t(b) * L * 3;
+    float sx = 0.f, sy = 0.f, sz = 0.f, cnt = 0.f;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const bool ok = mask == nullptr || mask[int64_t(b) * L + i] != 0;
+        if (ok) {
+            sx += t[i * 3 + 0];
+            sy += t[i * 3 + 1];
+            sz += t[i * 3 + 2];
+            cnt += 1.f;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[0][w] = sx;
+        red[1][w] = sy;
+        red[2][w] = sz;
+        red[3][w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int nw = blockDim.x >> 5;
+        float v[4];
+        for (int k = 0; k < 4; ++k) {
+            v[k] = l < nw ? red[k][l] : 0.f;
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        }
+        if (l == 0) {
+            const float n = v[3] > 0.f ? v[3] : 1.f;
+            red[0][0] = v[0] / n;
+            red[1][0] = v[1] / n;
+            red[2][0] = v[2] / n;
+        }
+    }
+    __syncthreads();
+    const float cx = red[0][0], cy = red[1][0], cz = red[2][0];
+    float* o = out + int64_t(b) * L * 3;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        o[i * 3 + 0] = t[i * 3 + 0] - cx;
+        o[i * 3 + 1] = t[i * 3 + 1] - cy;
+        o[i * 3 + 2] = t[i * 3 + 2] - cz;
+    }
+}
+
 // Inputs of the fused projection + pack kernel in one pass: s -> bf16 rows of din_ld, and the
 // head-independent pair-factor column blocks of the lifted rows, bf16(log2(e) z1) (q_hat) and
 // bf16(z2) (v_hat; k_hat scales it per head), so proj_pack copies them instead of converting the
@@ -536,9 +589,12 @@ __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ in, __nv_bfloat1
 __global__ void cast_inputs_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ s_bf16, int d_in,
                                    int din_ld, const float* __restrict__ z1, const float* __restrict__ z2,
                                    __nv_bfloat16* __restrict__ z1q, __nv_bfloat16* __restrict__ z2b, int rdz,
-                                   int64_t rows) {
+                                   int64_t rows, const float* __restrict__ trans, const uint8_t* __restrict__ mask,
+                                   float* __restrict__ trans_c, int L, int nrec) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    // the first nrec blocks also recentre one sample's translations each (one launch instead of two)
+    if (static_cast<int>(blockIdx.x) < nrec) recenter_sample(trans, mask, trans_c, L, blockIdx.x);
     const int q_s = (d_in + 3) / 4, q_z = rdz / 4;
     const bool vec_s = d_in % 4 == 0;
     const int64_t n_s = rows * q_s, n = n_s + 2 * rows * q_z;
@@ -637,59 +693,12 @@ __global__ void fully_masked_kernel(const uint8_t* __restrict__ mask, uint8_t* _
     for (int i = threadIdx.x; i < L; i += blockDim.x) flags[int64_t(b) * L + i] = any ? 0 : 1;
 }
 
+
 __global__ void recenter_kernel(const float* __restrict__ trans, const uint8_t* __restrict__ mask,
                                 float* __restrict__ out, int L) {
-    __shared__ float red[4][32];
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    const int b = blockIdx.x;
-    const float* t = trans + int64_t(b) * L * 3;
-    float sx = 0.f, sy = 0.f, sz = 0.f, cnt = 0.f;
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        const bool ok = mask == nullptr || mask[int64_t(b) * L + i] != 0;
-        if (ok) {
-            sx += t[i * 3 + 0];
-            sy += t[i * 3 + 1];
-            sz += t[i * 3 + 2];
-            cnt += 1.f;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        sz += __shfl_xor_sync(0xffffffffu, sz, o);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        red[0][w] = sx;
-        red[1][w] = sy;
-        red[2][w] = sz;
-        red[3][w] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const int nw = blockDim.x >> 5;
-        float v[4];
-        for (int k = 0; k < 4; ++k) {
-            v[k] = l < nw ? red[k][l] : 0.f;
-            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-        }
-        if (l == 0) {
-            const float n = v[3] > 0.f ? v[3] : 1.f;
-            red[0][0] = v[0] / n;
-            red[1][0] = v[1] / n;
-            red[2][0] = v[2] / n;
-        }
-    }
-    __syncthreads();
-    const float cx = red[0][0], cy = red[1][0], cz = red[2][0];
-    float* o = out + int64_t(b) * L * 3;
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        o[i * 3 + 0] = t[i * 3 + 0] - cx;
-        o[i * 3 + 1] = t[i * 3 + 1] - cy;
-        o[i * 3 + 2] = t[i * 3 + 2] - cz;
-    }
+    recenter_sample(trans, mask, out, L, blockIdx.x);
 }
 
 // Query-row sharding: per-sample partial sums {sum x, sum y, sum z, count} of the valid local
@@ -832,14 +841,16 @@ void launch_f32_to_bf16_2d(const float* in, __nv_bfloat16* out, int64_t rows, in
 bool cast_inputs_supported(int, int din_ld, int rdz) { return din_ld % 4 == 0 && rdz % 4 == 0; }
 
 void launch_cast_inputs(const float* s, __nv_bfloat16* s_bf16, int d_in, int din_ld, const float* z1, const float* z2,
-                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream) {
+                        __nv_bfloat16* z1q, __nv_bfloat16* z2b, int rdz, int64_t rows, cudaStream_t stream,
+                        const float* trans, const uint8_t* mask, float* trans_c, int B, int L) {
     if (!cast_inputs_supported(d_in, din_ld, rdz)) throw std::invalid_argument("cast_inputs: widths must be multiples of 4");
     if (din_ld > d_in) cudaMemsetAsync(s_bf16, 0, size_t(rows) * din_ld * 2, stream);  // padding columns
     const int64_t n = rows * ((d_in + 3) / 4 + 2 * (rdz / 4));
     if (n <= 0) return;
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8);
+    const int nrec = trans != nullptr ? B : 0;
+    const int64_t blocks = std::max<int64_t>(nrec, std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));
     launch_pdl(cast_inputs_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, s, s_bf16, d_in, din_ld,
-               z1, z2, z1q, z2b, rdz, rows);
+               z1, z2, z1q, z2b, rdz, rows, trans, mask, trans_c, L, nrec);
 }
 
 void launch_split3(const float* in, int64_t rows, int cols, int64_t ld_in, float* out, int ld_part, int64_t ld_out,
