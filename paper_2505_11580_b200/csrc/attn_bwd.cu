@@ -611,9 +611,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             const int bh = unit_bh(u), r0 = unit_r0(u);
             const int64_t vec_base = static_cast<int64_t>(bh) * (KV ? p.Lcol : p.Lrow);  // per-query vectors
             const int grow = r0 + row;  // global row (key in KV, query in Q)
-            // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.
+            // Per-row vector (Q kernel): lse2 for the P pair, D for the dS pair.  lse2 = lse * log2(e)
+            // is rounded on its own (__fmul_rn, never contracted into the ex2 argument) in both
+            // kernels, so the two dQ paths see bitwise-equal P and dS (the contraction otherwise
+            // follows register allocation: measured 2e-4 drift between the paths).
             float row_v = 0.f;
-            if (!KV && grow < p.Lrow) row_v = role == 0 ? __ldg(p.lse + vec_base + grow) * kL2E
+            if (!KV && grow < p.Lrow) row_v = role == 0 ? __fmul_rn(__ldg(p.lse + vec_base + grow), kL2E)
                                                      : __ldg(p.Dvec + vec_base + grow);
             for (int j = 0; j < ntiles; ++j, ++t) {
                 const int c0 = p.col0 + j * BN + 32 * half;  // first tile column of this thread's half
@@ -627,7 +630,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     if (role == 0) {
                         load_vec32(p.lse + vec_base, c0, p.Lcol, INFINITY, cv);
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) cv[k] *= kL2E;
+                        for (int k = 0; k < 32; ++k) cv[k] = __fmul_rn(cv[k], kL2E);
                     } else {
                         load_vec32(p.Dvec + vec_base, c0, p.Lcol, 0.f, cv);
                     }
