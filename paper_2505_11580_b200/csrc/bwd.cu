@@ -30,6 +30,7 @@ namespace fipa_b200 {
 namespace {
 
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kL2E = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t ptx_pack(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -917,6 +918,72 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
     const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 2);  // 2 resident blocks per SM
     launch_pdl(bwd_unpack_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), smem, stream, d, a);
+}
+
+// Streaming row kernels of the materialised backward: one block per (sample, head, query) row, 8
+// columns per thread and step (two float4 / one uint4 per operand).  Same rounding as the fused
+// kernels: lse2 = __fmul_rn(lse, log2 e), P = ex2(S - lse2) rounded to bf16, dS = P (dP - D).
+__global__ void __launch_bounds__(256) dense_softmax_kernel(const float* __restrict__ S, int ld,
+                                                            const float* __restrict__ lse, int L,
+                                                            __nv_bfloat16* __restrict__ P) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t row = blockIdx.x;
+    const float l = __ldg(lse + row);
+    const bool none = !(l > -INFINITY);
+    const float l2 = none ? 0.f : __fmul_rn(l, kL2E);
+    const float* s = S + row * ld;
+    __nv_bfloat16* p = P + row * ld;
+    for (int c = threadIdx.x * 8; c < L; c += blockDim.x * 8) {
+        const float4 a = *reinterpret_cast<const float4*>(s + c);
+        const float4 b = *reinterpret_cast<const float4*>(s + c + 4);
+        const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = none ? 0u : ptx::pack_bf16x2(ptx::ex2(x[2 * k] - l2), ptx::ex2(x[2 * k + 1] - l2));
+        *reinterpret_cast<uint4*>(p + c) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256) dense_ds_kernel(const __nv_bfloat16* __restrict__ P,
+                                                       const float* __restrict__ dP, int ld,
+                                                       const float* __restrict__ Dvec, int L,
+                                                       __nv_bfloat16* __restrict__ dS) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t row = blockIdx.x;
+    const float D = __ldg(Dvec + row);
+    const __nv_bfloat16* p = P + row * ld;
+    const float* g = dP + row * ld;
+    __nv_bfloat16* o = dS + row * ld;
+    for (int c = threadIdx.x * 8; c < L; c += blockDim.x * 8) {
+        const uint4 pw = *reinterpret_cast<const uint4*>(p + c);
+        const float4 a = *reinterpret_cast<const float4*>(g + c);
+        const float4 b = *reinterpret_cast<const float4*>(g + c + 4);
+        const uint32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
+        const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = ptx::pack_bf16x2(__uint_as_float(pv[k] << 16) * (x[2 * k] - D),
+                                    __uint_as_float(pv[k] & 0xFFFF0000u) * (x[2 * k + 1] - D));
+        *reinterpret_cast<uint4*>(o + c) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+void launch_dense_softmax(const float* S, int ld, const float* lse, int64_t rows, int L, __nv_bfloat16* P,
+                          cudaStream_t stream) {
+    if (ld % 8 != 0 || ld < L) throw std::invalid_argument("dense softmax: row stride must be >= L and % 8");
+    launch_pdl(dense_softmax_kernel, dim3(static_cast<unsigned>(rows)), dim3(std::min(256, (L + 7) / 8 + 31) / 32 * 32),
+               0, stream, S, ld, lse, L, P);
+}
+
+void launch_dense_ds(const __nv_bfloat16* P, const float* dP, int ld, const float* Dvec, int64_t rows, int L,
+                     __nv_bfloat16* dS, cudaStream_t stream) {
+    if (ld % 8 != 0 || ld < L) throw std::invalid_argument("dense dS: row stride must be >= L and % 8");
+    launch_pdl(dense_ds_kernel, dim3(static_cast<unsigned>(rows)), dim3(std::min(256, (L + 7) / 8 + 31) / 32 * 32), 0,
+               stream, P, dP, ld, Dvec, L, dS);
 }
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,

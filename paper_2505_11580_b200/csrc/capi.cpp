@@ -493,7 +493,7 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
     offsets[6] = off(w.dproj);
     offsets[7] = off(w.dfeat);
     if (dims != nullptr) {
-        dims[0] = fipa_b200::FlashIpaLayer::kAccLd;
+        dims[0] = layer->impl->acc_ld();
         dims[1] = layer->impl->nproj_ld();
         dims[2] = layer->impl->dims().feat_ld;
     }

@@ -172,7 +172,7 @@ FlashIpaLayer::ShardedWorkspace FlashIpaLayer::carve_sharded(void* base, std::in
     w.v_all = take(w.v_bytes * groups);
     w.sums = reinterpret_cast<float*>(take(std::size_t(B) * 4 * 4));
     if (train) {
-        const std::size_t part = std::size_t(groups) * BHL * kAccLd * 4;
+        const std::size_t part = std::size_t(groups) * BHL * acc_ld() * 4;
         w.dk_part = reinterpret_cast<float*>(take(part));
         w.dv_part = reinterpret_cast<float*>(take(part));
         w.dt_sums = reinterpret_cast<float*>(take(std::size_t(B) * 4 * 4));
@@ -298,7 +298,7 @@ void FlashIpaLayer::backward_sharded(Comm& comm, std::int64_t B, std::int64_t L,
     backward(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace,
              ws.local.bytes, stream, &sh);
     sh.kv_done = nullptr;
-    const std::size_t n = std::size_t(B) * L * dims_.heads * kAccLd;
+    const std::size_t n = std::size_t(B) * L * dims_.heads * acc_ld();
     cuda_check(cudaStreamWaitEvent(cs, comm_ev_[5], 0), "stream wait");
     comm.reduce_scatter_sum_f32(ws.dk_part, ws.local.dk_acc, n, cs);
     comm.reduce_scatter_sum_f32(ws.dv_part, ws.local.dv_acc, n, cs);

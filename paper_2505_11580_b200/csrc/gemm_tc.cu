@@ -814,7 +814,7 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
     // (FIPA_PAIR_GEMM=2 also routes wide single products -- dfeat: N = 2432, K = 256 -- to pairs:
     // no gain measured there, the short-K product is epilogue-bound)
     const bool pair_wide = pair_gemm_mode() >= 2 && a.batch <= 1 && a.split_k <= 1 && a.N >= 2048 && a.M >= 4096;
-    if (pair_gemm_enabled() && ((a.batch > 1 && a.N > 256 && a.N <= 512 && a.M >= 256) || pair_wide)) {
+    if (pair_gemm_enabled() && ((a.batch > 1 && a.N > 256 && a.M >= 256) || pair_wide)) {
         // batched dQ (and wide single products): 256 x 256 tiles over CTA pairs (half the B operand
         // bytes per SM)
         switch (sel) {
@@ -824,7 +824,7 @@ void launch_gemm_bf16(const GemmArgs& a, cudaStream_t stream) {
             default: return launch_impl2<256, true, true>(a, stream);
         }
     }
-    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512) || (a.batch > 1 && a.N > 256 && a.N <= 512);
+    const bool wide = a.N >= 2048 || (a.N % 256 == 0 && a.N >= 512) || (a.batch > 1 && a.N > 256);
     if (wide) {
         switch (sel) {
             case 0: return launch_impl<256, false, false>(a, stream);

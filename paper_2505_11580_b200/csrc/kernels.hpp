@@ -253,6 +253,13 @@ struct BwdUnpackArgs {
     int B, L;
 };
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream);
+// Materialised attention backward (FlashIpaLayer::dense_attention_backward), rows of length L with
+// stride ld (a multiple of 8): P = bf16(2^(S - lse * log2 e)) (0 for a row whose lse is -inf: no
+// valid key); dS = bf16(P (dP - D)).
+void launch_dense_softmax(const float* S, int ld, const float* lse, int64_t rows, int L, __nv_bfloat16* P,
+                          cudaStream_t stream);
+void launch_dense_ds(const __nv_bfloat16* P, const float* dP, int ld, const float* Dvec, int64_t rows, int L,
+                     __nv_bfloat16* dS, cudaStream_t stream);
 
 // dOut with masked rows zeroed -> bf16 [BL, ld_out]; db[d_in] += column sums (zero db first).
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,

@@ -576,9 +576,9 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dfeat = reinterpret_cast<__nv_bfloat16*>(take(BL * d.feat_ld * 2));
         w.do_hat = reinterpret_cast<__nv_bfloat16*>(take(BHL * d.dv_pad * 2));
         w.Dvec = reinterpret_cast<float*>(take(BHL * 4));
-        w.dq_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
-        w.dk_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
-        w.dv_acc = reinterpret_cast<float*>(take(BHL * kAccLd * 4));
+        w.dq_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
+        w.dk_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
+        w.dv_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
         w.dproj = reinterpret_cast<__nv_bfloat16*>(take(BL * nproj_ld() * 2));
         w.dz1_epi = reinterpret_cast<float*>(take(BL * rdz * 4));
         w.geo_epi = reinterpret_cast<float*>(take(BL * 12 * 4));
@@ -586,7 +586,20 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
         w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
-        if (const std::int64_t qc = ds_chunk(B, L)) {
+        if (dense_backward()) {
+            // materialised S / dP (fp32) and P / dS (bf16) for as many whole samples as fit the
+            // dS budget (Tuning::ds_cap_mb), at least one
+            w.att_ld = static_cast<int>(round_up(std::size_t(L), 64));
+            const double per_sample = double(d.heads) * double(L) * double(w.att_ld) * 12.0;
+            const double cap = double(tuning_.ds_cap_mb) * double(1 << 20);
+            w.att_samples = static_cast<int>(std::max<std::int64_t>(
+                1, std::min<std::int64_t>(B, static_cast<std::int64_t>(cap / per_sample))));
+            const std::size_t n = std::size_t(w.att_samples) * d.heads * L * w.att_ld;
+            w.att_s = reinterpret_cast<float*>(take(n * 4));
+            w.att_dp = reinterpret_cast<float*>(take(n * 4));
+            w.att_p = reinterpret_cast<__nv_bfloat16*>(take(n * 2));
+            w.att_ds = reinterpret_cast<__nv_bfloat16*>(take(n * 2));
+        } else if (const std::int64_t qc = ds_chunk(B, L)) {
             w.ds_ld = static_cast<int>(qc);  // whole 64-column blocks: all queries, or a query chunk
             w.ds = reinterpret_cast<__nv_bfloat16*>(take(BHL * w.ds_ld * 2));
         }
@@ -620,9 +633,9 @@ FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b
     v.dfeat = adv(w.dfeat, n * d.feat_ld * 2);
     v.do_hat = adv(w.do_hat, n * H * d.dv_pad * 2);
     v.Dvec = adv(w.Dvec, n * H * 4);
-    v.dq_acc = adv(w.dq_acc, n * H * kAccLd * 4);
-    v.dk_acc = adv(w.dk_acc, n * H * kAccLd * 4);
-    v.dv_acc = adv(w.dv_acc, n * H * kAccLd * 4);
+    v.dq_acc = adv(w.dq_acc, n * H * acc_ld() * 4);
+    v.dk_acc = adv(w.dk_acc, n * H * acc_ld() * 4);
+    v.dv_acc = adv(w.dv_acc, n * H * acc_ld() * 4);
     v.dproj = adv(w.dproj, n * nproj_ld() * 2);
     v.dz1_epi = adv(w.dz1_epi, n * rdz * 4);
     v.geo_epi = adv(w.geo_epi, n * 12 * 4);
@@ -667,10 +680,17 @@ std::size_t FlashIpaLayer::num_weights() const {
     return n;
 }
 
-bool FlashIpaLayer::backward_supported() const {
+bool FlashIpaLayer::fused_backward_supported() const {
     return cfg_.precision == Precision::bf16 && attn_fwd_2sm_supported(dims_) && attn_bwd_supported(dims_) &&
            dims_.n_value <= 32 && dims_.n_query <= 32;
 }
+
+bool FlashIpaLayer::dense_backward() const {
+    return cfg_.precision == Precision::bf16 && !fused_backward_supported() && bf16_attention_supported(dims_) &&
+           dims_.n_value <= 32 && dims_.n_query <= 32 && dims_.heads <= 16;
+}
+
+bool FlashIpaLayer::backward_supported() const { return fused_backward_supported() || dense_backward(); }
 
 int FlashIpaLayer::launches_per_backward() const {
     // dout cast, dfeat GEMM, dW_out GEMM, prep, attn KV, dQ (GEMM or attention kernel), unpack
@@ -789,7 +809,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         }
         GraphKey key{train ? 1 : 0, B, L, {s, z1, z2, rot, trans, mask, out, workspace}, workspace_bytes};
         if (run_graph(key, stream, [&](cudaStream_t cs) {
-                if (micro_chunks(B, L) > 1)
+                if (micro_chunks(B, L) > 1 && !(train && dense_backward()))
                     forward_micro(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train);
                 else
                     forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train,
@@ -809,7 +829,7 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && out, "null input/output pointer");
     REQUIRE(!train || backward_supported(),
-            "training (forward_train/backward) needs precision='bf16' and lifted widths <= 448");
+            "training (forward_train/backward) needs precision='bf16'");
     REQUIRE(shard == nullptr || (cfg_.precision == Precision::bf16 && bf16_attention_supported(dims_)),
             "query-row sharding needs precision='bf16'");
     const bool do_pack = shard == nullptr || shard->stage == 1;
@@ -937,7 +957,8 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
         aa.trans = ws.trans_c;
         aa.feat = static_cast<__nv_bfloat16*>(ws.feat);
         aa.lse = ws.lse;
-        aa.o_save = train ? ws.o_hat : nullptr;
+        // (the materialised backward recomputes O_hat from P and V_hat)
+        aa.o_save = train && !dense_backward() ? ws.o_hat : nullptr;
         aa.B = int(B);
         aa.L = int(L);
         if (shard != nullptr) {  // keys = all shards' rows, gathered [G][B*H][L][pad]
@@ -947,7 +968,8 @@ void FlashIpaLayer::forward_impl(std::int64_t B, std::int64_t L, const float* s,
             aa.kchunk = int(L);
         }
         for (int i = 0; i < 4; ++i) aa.pass_ring[i] = tuning_.pass_ring[i];
-        const AttnImpl impl = train ? AttnImpl::pair : attention_impl(d, tuning_.attn, shard != nullptr);
+        const AttnImpl impl = train && !dense_backward() ? AttnImpl::pair
+                                                         : attention_impl(d, tuning_.attn, shard != nullptr);
         if (shard != nullptr && shard->hc > 0) {
             REQUIRE(impl == AttnImpl::pair, "head-chunked sharded attention needs the CTA-pair kernel");
             aa.h0 = shard->h0;
@@ -1136,7 +1158,7 @@ void FlashIpaLayer::backward(std::int64_t B, std::int64_t L, const float* s, con
         GraphKey key{2, B, L, {s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights, workspace},
                      workspace_bytes};
         if (run_graph(key, stream, [&](cudaStream_t cs) {
-                if (micro_chunks(B, L) > 1)
+                if (micro_chunks(B, L) > 1 && !dense_backward())
                     backward_micro(B, L, s, z1, z2, rot, trans, mask, dout, ds, dz1, dz2, drot, dtrans, dweights,
                                    workspace, workspace_bytes, cs);
                 else
@@ -1159,7 +1181,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
     REQUIRE(L >= 1, "empty frame set");
     REQUIRE(s && z1 && z2 && rot && trans && dout && ds && dz1 && dz2 && dweights,
             "null input/output pointer");
-    REQUIRE(backward_supported(), "backward needs precision='bf16' and lifted widths <= 448");
+    REQUIRE(backward_supported(), "backward needs precision='bf16'");
     const Workspace ws = view ? *view : carve(workspace, B, L, true);
     // chunks of a micro-batched call accumulate the weight gradients concurrently: atomic GEMM
     // epilogues (split-K >= 2), accumulators zeroed once (part 1) and scattered once (part 4)
@@ -1240,6 +1262,12 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         launch_gemm_bf16(g, stream);
     }
     mark(3);
+    if (dense_backward()) {
+        REQUIRE(shard == nullptr, "query-row sharded training needs the fused attention backward (lifted widths <= 448)");
+        dense_attention_backward(B, L, z1, rot, ws, stream);
+        mark(4);
+        mark(5);
+    } else {
     {
         BwdPrepArgs a{};
         a.dfeat = ws.dfeat;
@@ -1267,7 +1295,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         a.dq_acc = ws.dq_acc;
         a.dk_acc = ws.dk_acc;
         a.dv_acc = ws.dv_acc;
-        a.acc_ld = kAccLd;
+        a.acc_ld = acc_ld();
         a.B = int(B);
         a.L = int(L);
         for (int i = 0; i < 5; ++i) a.ring[i] = tuning_.bwd_ring[i];
@@ -1299,6 +1327,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         launch_attn_bwd(d, a, stream, 2);
         }
     }
+    }  // fused
     mark(6);
     }  // stage 1
     if (st2 && (parts & 2)) {
@@ -1307,7 +1336,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         a.dq_acc = ws.dq_acc;
         a.dk_acc = shard ? shard->dk_own : ws.dk_acc;
         a.dv_acc = shard ? shard->dv_own : ws.dv_acc;
-        a.acc_ld = kAccLd;
+        a.acc_ld = acc_ld();
         a.proj = ws.proj;
         a.rot = rot;
         a.trans_c = ws.trans_c;
@@ -1403,6 +1432,82 @@ bool FlashIpaLayer::attention_impl_for_sharding() const {
 }
 
 // ------------------------------------------------------------ micro-batched capture
+// Materialised attention backward for lifted rows wider than the fused kernels hold (z_factor_rank
+// 3-4: D_qk / D_v up to ~700; attn_bwd.cu needs the 128 x D stationary tile in shared memory and the
+// 128 x D accumulator next to S in TMEM).  Per group of att_samples whole samples, every product is
+// one batched tcgen05 GEMM over the (sample, head) pairs and the softmax algebra is two streaming
+// kernels -- the same arithmetic as the fused kernels (S in log2 units from the lifted rows, P
+// rounded to bf16, dS = P (dP - D) rounded to bf16, fp32 accumulation), with [L, L] intermediates:
+//   S = Q_hat K_hat^T ; P = 2^(S - lse2) ; O_hat = P V_hat (the training forward of these widths
+//   saves no O_hat) ; prep (dO_hat, D, epilogue gradients) ; dP = dO_hat V_hat^T ;
+//   dS = P (dP - D) ; dV = P^T dO_hat ; dK = dS^T Q_hat ; dQ = dS K_hat
+// Workspace: 12 bytes per (sample, head, query, key) of one group -- quadratic in L, unlike the
+// fused path (Tuning::ds_cap_mb bounds the group, one sample at least).
+void FlashIpaLayer::dense_attention_backward(std::int64_t B, std::int64_t L, const float* z1, const float* rot,
+                                             const Workspace& ws, cudaStream_t stream) {
+    const LayerDims& d = dims_;
+    const int H = d.heads, ld = ws.att_ld, acc = acc_ld(), Li = int(L);
+    const std::int64_t rdz = std::int64_t(d.rank) * d.d_z;
+    auto bf = [](const void* p) { return static_cast<const __nv_bfloat16*>(p); };
+    for (std::int64_t b0 = 0; b0 < B; b0 += ws.att_samples) {
+        const int nb = int(std::min<std::int64_t>(ws.att_samples, B - b0));
+        const Workspace v = slice(ws, b0, L);
+        const int Z = nb * H;
+        // batched product over the group's (sample, head) pairs; C either [Z][L][ld] (square
+        // intermediates) or the residue-major [nb, L, H, width] rows
+        auto product = [&](const void* A, int64_t lda, bool a_mn, const void* Bm, int64_t ldb, bool b_mn, float* C,
+                           bool residue_major, int width, int N, int K) {
+            GemmArgs g;
+            g.A = bf(A);
+            g.lda = lda;
+            g.a_mn_major = a_mn;
+            g.B = bf(Bm);
+            g.ldb = ldb;
+            g.b_mn_major = b_mn;
+            g.C = C;
+            if (residue_major) {
+                g.ldc = int64_t(H) * width;
+                g.ldc_h = width;
+                g.ldc_b = int64_t(L) * H * width;
+                g.batch_h = H;
+            } else {
+                g.ldc = ld;
+                g.ldc_h = ld;
+                g.ldc_b = int64_t(L) * ld;
+                g.batch_h = 1;
+            }
+            g.M = Li;
+            g.N = N;
+            g.K = K;
+            g.batch = Z;
+            launch_gemm_bf16(g, stream);
+        };
+        product(v.qhat, d.dqk_pad, false, v.khat, d.dqk_pad, false, ws.att_s, false, 0, Li, d.dqk_pad);  // S
+        launch_dense_softmax(ws.att_s, ld, v.lse, int64_t(Z) * L, Li, ws.att_p, stream);                // P
+        product(ws.att_p, ld, false, v.vhat, d.dv_pad, true, v.o_hat, true, d.dv_pad, d.dv_pad, Li);      // O_hat
+        {
+            BwdPrepArgs a{};
+            a.dfeat = v.dfeat;
+            a.ohat = v.o_hat;
+            a.z1 = z1 + b0 * L * rdz;
+            a.rot = rot + b0 * L * 9;
+            a.trans_c = v.trans_c;
+            a.dohat = v.do_hat;
+            a.Dvec = v.Dvec;
+            a.dz1_epi = v.dz1_epi;
+            a.geo_epi = v.geo_epi;
+            a.B = nb;
+            a.L = Li;
+            launch_bwd_prep(d, a, stream);
+        }
+        product(v.do_hat, d.dv_pad, false, v.vhat, d.dv_pad, false, ws.att_dp, false, 0, Li, d.dv_pad);  // dP
+        launch_dense_ds(ws.att_p, ws.att_dp, ld, v.Dvec, int64_t(Z) * L, Li, ws.att_ds, stream);           // dS
+        product(ws.att_p, ld, true, v.do_hat, d.dv_pad, true, v.dv_acc, true, acc, d.dv_mma, Li);          // dV
+        product(ws.att_ds, ld, true, v.qhat, d.dqk_pad, true, v.dk_acc, true, acc, d.dqk_mma, Li);         // dK
+        product(ws.att_ds, ld, false, v.khat, d.dqk_pad, true, v.dq_acc, true, acc, d.dqk_mma, Li);        // dQ
+    }
+}
+
 int FlashIpaLayer::micro_chunks(std::int64_t B, std::int64_t L) const {
     if (tuning_.micro < 2 || timing_ || cfg_.precision != Precision::bf16 || B < 2) return 1;
     // each chunk's weight-gradient GEMMs run split-K >= 2 over K = (B / chunks) * L

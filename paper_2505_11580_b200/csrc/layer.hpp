@@ -222,6 +222,10 @@ public:
     void forward_host_f32(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                           const float* rot, const float* trans, const std::uint8_t* mask, float* out);
     bool backward_supported() const;
+    // The fused tcgen05 attention backward (attn_bwd.cu: lifted widths <= 448, rank <= 2) or, for
+    // wider lifted rows (z_factor_rank 3-4), the materialised backward (dense_attention_backward).
+    bool fused_backward_supported() const;
+    bool dense_backward() const;
     int launches_per_backward() const;
 
 
@@ -278,13 +282,20 @@ public:
         float* ks = nullptr;
         float* vs = nullptr;               // [2][BH L, dv_pad]
         float* feat_cat = nullptr;         // [BL, 3 feat_p]  feat_hi | feat_lo | feat_hi
+        // materialised attention backward (wide lifted rows), att_samples samples at a time:
+        float* att_s = nullptr;            // [att_samples H, L, att_ld] S (log2 units), fp32
+        float* att_dp = nullptr;           // [att_samples H, L, att_ld] dP, fp32
+        __nv_bfloat16* att_p = nullptr;    // [att_samples H, L, att_ld] P
+        __nv_bfloat16* att_ds = nullptr;   // [att_samples H, L, att_ld] dS
+        int att_ld = 0, att_samples = 0;
         std::size_t bytes = 0;
     };
     // fp32 path: projections, attention and output projection on the tensor cores (3xTF32)
     bool f32_tensor_cores() const;
     int din_p() const { return (dims_.d_in + 31) / 32 * 32; }
     int feat_p() const { return (dims_.feat + 31) / 32 * 32; }
-    static constexpr int kAccLd = 448;
+    // row stride of the fp32 dQ / dK / dV accumulators ([B, L, H, acc_ld]): 448 up to rank 2
+    int acc_ld() const { return std::max(448, (std::max(dims_.dqk_mma, dims_.dv_mma) + 31) / 32 * 32); }
     int nproj_ld() const { return (dims_.n_proj + 7) / 8 * 8; }
     Workspace carve(void* base, std::int64_t B, std::int64_t L, bool train = false) const;
     // The same workspace seen from sample b0 on (every per-sample buffer advanced; the shared
@@ -358,6 +369,10 @@ private:
     // forked streams (the graph holds parallel branches), so each kernel's tail wave and launch ramp
     // overlap the other chain's kernels.  Same workspace (sample-sliced views), same results.
     int micro_chunks(std::int64_t B, std::int64_t L) const;
+    // dK / dV / dQ by materialised per-(sample, head) products (tcgen05 GEMMs) for the lifted
+    // widths the fused kernels do not hold; recomputes O_hat and runs prep on the way
+    void dense_attention_backward(std::int64_t B, std::int64_t L, const float* z1, const float* rot,
+                                  const Workspace& ws, cudaStream_t stream);
     void forward_micro(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
                        const float* rot, const float* trans, const std::uint8_t* mask, float* out, void* workspace,
                        std::size_t workspace_bytes, cudaStream_t stream, bool train);

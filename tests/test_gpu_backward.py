@@ -95,6 +95,29 @@ def test_micro_batched_capture_matches_one_chain(fipa):
         assert rel_dev(ref[n], res[2][1][n]) < BF16_TOL, n
 
 
+@pytest.mark.parametrize("rank,B,L", [(3, 2, 200), (4, 2, 320), (3, 1, 257)])
+def test_backward_wide_lifted_rows(fipa, rank, B, L):
+    """z_factor_rank 3-4 (lifted widths 576-704, wider than the fused attention backward holds):
+    the materialised backward (batched tcgen05 GEMMs over the (sample, head) pairs) against the
+    oracle at the same 2e-2 gate as every other training shape."""
+    _check(fipa, dict(MAIN, rank=rank), B, L, seed=40 + rank + L, mask_frac=0.1)
+
+
+def test_backward_wide_sample_groups(fipa):
+    """The materialised backward in groups of one sample (a 1 MB intermediate budget forces
+    att_samples = 1) gives the same gradients as one group of all samples."""
+    shape = dict(MAIN, rank=3)
+    model = _model(fipa, shape, 5)
+    batch = make_batch(shape, 3, 192, seed=5, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(5).standard_normal((3, 192, shape["d_in"]))
+    got = {}
+    for cap in (2048, 1):
+        model.set_tuning(ds_cap_mb=cap)
+        got[cap] = gpu_train_device(model, batch, dout)[1]
+    for n in GRADS:
+        assert rel_dev(got[2048][n], got[1][n]) < 1e-5, n
+
+
 def test_backward_tiny_shape(fipa):
     _check(fipa, TINY, 3, 37, seed=3, mask_frac=0.2)
 
