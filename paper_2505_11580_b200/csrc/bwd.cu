@@ -379,7 +379,7 @@ constexpr int kUnpackMaxH = 16;
 //  bwd_unpack_geo_kernel   block = 8 residues, one warp per residue with lanes over (head, point)
 //                          tasks: frame-applied point gradients -> dproj point columns; dR, dt
 //                          summed over the residue's heads by one warp reduction -> drot, dt_c;
-//                          per-residue dgamma terms -> dg_rows [BL, H] (via shared memory).
+//                          dgamma terms summed over the block's residues in shared memory -> dg.
 //                          (launch bounds 256 x 4 cap it at 64 registers; ptxas -v: no spills)
 //  bwd_unpack_kernel       block streams kUnpackRows residues; every accumulator column of the
 //                          scalar and pair blocks is read by exactly one thread with coalesced
@@ -387,11 +387,12 @@ constexpr int kUnpackMaxH = 16;
 //                          scalar q | k (x w_l/sqrt(c) ln2) | v -> bf16 pairs of the dproj row;
 //                          pair e: dz1 = dz1_epi + sum_h dq[zq+e],
 //                          dz2 = sum_h (w_l w_bias[h, e % d_z] ln2 dk[zq+e] + dv[c+e]),
-//                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials);
-//                          dg += sum of dg_rows over the block's residues.
+//                          d(w_l w_bias)[h, e % d_z] += ln2 dk[zq+e] z2[e] (register partials).
+// The two write disjoint outputs.  (Forking the geometry kernel onto a side stream beside the
+// streaming one: unpack 0.109 -> 0.100 ms in one chain, but the micro-batched step 0.860 -> 0.874.)
 // The geometry of one residue (warp-wide; lanes over (head, point) tasks): frame-applied point
 // gradients -> dproj point columns, dR / dt summed over the heads -> drot, dt_c, per-head dgamma
-// terms -> dg_rows.  s_dg: this warp's kUnpackMaxH floats of shared memory.
+// terms -> s_dg (this warp's kUnpackMaxH floats of shared memory).
 __device__ __forceinline__ void unpack_geo_row(const LayerDims& d, const BwdUnpackArgs& a, int64_t row, int lane,
                                                float* s_dg) {
     const int H = d.heads, c = d.c, rdz = d.rank * d.d_z, Nq = d.n_query, Nv = d.n_value;
@@ -508,9 +509,6 @@ __device__ __forceinline__ void unpack_geo_row(const LayerDims& d, const BwdUnpa
             a.dt_c[row * 3 + lane - 9] = v;
         }
     }
-    __syncwarp();
-    if (lane < H) a.dg_rows[row * H + lane] = s_dg[lane];
-    __syncwarp();
 }
 
 __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, BwdUnpackArgs a) {
@@ -519,10 +517,21 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
     // One warp per residue; lanes run over (head, point) tasks so every lane works (the per-head
     // form left 20 of 32 lanes idle and was issue bound).  dR / dt are summed over the residue's
     // heads with one warp reduction; per-head dgamma terms go through shared memory.
+    // The block's 8 residues' dgamma terms are summed here (one atomic per head and block), so the
+    // streaming kernel does not depend on this one and the two run concurrently.
     __shared__ float s_dg[8][kUnpackMaxH];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (lane < kUnpackMaxH) s_dg[warp][lane] = 0.f;
+    __syncwarp();
     if (row < static_cast<int64_t>(a.B) * a.L) unpack_geo_row(d, a, row, lane, s_dg[warp]);
+    __syncthreads();
+    if (threadIdx.x < d.heads) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += s_dg[w][threadIdx.x];
+        atomicAdd(&a.dg[threadIdx.x], acc);
+    }
 }
 
 __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
@@ -703,13 +712,6 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     }
     __syncthreads();
     for (int e = tid; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
-    if (tid < H) {
-        float acc = 0.f;
-        for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x)
-            for (int64_t row = grp * kUnpackRows; row < BL && row < (grp + 1) * kUnpackRows; ++row)
-                acc += a.dg_rows[row * H + tid];
-        atomicAdd(&a.dg[tid], acc);
-    }
 }
 
 // dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 64 columns x 128 rows:

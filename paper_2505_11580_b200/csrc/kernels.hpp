@@ -248,7 +248,6 @@ struct BwdUnpackArgs {
     float* drot;            // [BL, 9] or null
     float* dt_c;            // [BL, 3] gradient w.r.t. the recentred translations
     float* dg;              // [H]     accumulated (zero first): dL/d(gamma_h w_l w_c)
-    float* dg_rows;         // [BL, H] scratch: per-residue dgamma terms
     float* dwlb;            // [H, d_z] accumulated (zero first): dL/d(w_l w_bias)
     int B, L;
 };

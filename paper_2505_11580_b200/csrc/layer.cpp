@@ -585,7 +585,6 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dt_c = reinterpret_cast<float*>(take(BL * 3 * 4));
         w.red = reinterpret_cast<float*>(take((d.heads + d.heads * std::size_t(d.d_z)) * 4));
         w.dwproj = reinterpret_cast<float*>(take(std::size_t(d.d_in) * d.n_proj * 4));
-        w.dg_rows = reinterpret_cast<float*>(take(BL * d.heads * 4));
         if (dense_backward()) {
             // materialised S / dP (fp32) and P / dS (bf16) for as many whole samples as fit the
             // dS budget (Tuning::ds_cap_mb), at least one
@@ -640,7 +639,6 @@ FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b
     v.dz1_epi = adv(w.dz1_epi, n * rdz * 4);
     v.geo_epi = adv(w.geo_epi, n * 12 * 4);
     v.dt_c = adv(w.dt_c, n * 3 * 4);
-    v.dg_rows = adv(w.dg_rows, n * H * 4);
     v.ds = adv(w.ds, n * H * std::size_t(w.ds_ld) * 2);
     return v;  // red / dwproj: shared accumulators; the fp32-path planes are not sliced (bf16 only)
 }
@@ -1353,7 +1351,6 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         a.drot = drot;
         a.dt_c = ws.dt_c;
         a.dg = ws.red;
-        a.dg_rows = ws.dg_rows;
         a.dwlb = ws.red + H;
         a.B = int(B);
         a.L = int(L);

@@ -272,7 +272,6 @@ public:
         float* geo_epi = nullptr;          // [BL, 12] dR | dt of the output epilogue
         float* dt_c = nullptr;             // [BL, 3]
         float* red = nullptr;              // [H + H d_z]  d(g) | d(w_l w_bias)
-        float* dg_rows = nullptr;          // [BL, H] per-residue dgamma terms (unpack scratch)
         __nv_bfloat16* ds = nullptr;       // [BH, L, ds_ld] materialised dS (short sequences, or null)
         int ds_ld = 0;
         float* dwproj = nullptr;           // [d_in, n_proj]
