@@ -41,7 +41,7 @@ METRIC = "FlashIPA layer residues/sec & attn TFLOP/s vs bf16 peak, L=1k-64k, 1-8
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--B", type=int, default=8)
@@ -410,7 +410,9 @@ def run_ours(args, shape):
                 hout[slot].copy_(douts[slot], non_blocking=True)
                 read[slot].record(rs)
 
-        n_e2e = max(3, min(args.steps, 20))
+        # every timed step copies its own inputs; only the first one's H2D cannot overlap a
+        # previous step (pipeline fill, amortised over the run like a training loop's first batch)
+        n_e2e = max(3, args.steps)
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
