@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     for (int e = tid; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
 }
 
-// dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 64 columns x 128 rows:
+// dOut with masked rows zeroed -> bf16, plus column sums (db_out).  Block = 64 columns x 32 rows:
 // 16 threads cover a row's 64 columns with float4 loads (256 B contiguous), 16 row lanes stride the
 // rows with all their loads independent; column partials reduced in shared memory, one atomic per
 // column and block.
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(256) bwd_dout_kernel(const float* __restrict__
     const bool vec = col + 4 <= cols && (cols & 3) == 0 && (ld_out & 3) == 0;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     if (col < cols) {
-#pragma unroll 4
+#pragma unroll
         for (int64_t r = r0 + ry; r < r1; r += 16) {
             const bool ok = mask == nullptr || mask[r] != 0;
             float v[4];
@@ -990,7 +990,7 @@ void launch_dense_ds(const __nv_bfloat16* P, const float* dP, int ld, const floa
 
 void launch_bwd_dout(const float* dout, const uint8_t* mask, __nv_bfloat16* out, int ld_out, float* db,
                      int64_t rows, int cols, cudaStream_t stream) {
-    const int rpb = 128;
+    const int rpb = 32;  // 2 rows per thread: 4x the blocks of 128-row tiles, loads all in flight
     dim3 grid((cols + 63) / 64, static_cast<unsigned>((rows + rpb - 1) / rpb));
     launch_pdl(bwd_dout_kernel, grid, dim3(256), 0, stream, dout, mask, out, ld_out, db, rows, cols, rpb);
 }
