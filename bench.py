@@ -639,8 +639,9 @@ def roofline_entry(train, stage_ms, achieved, achieved_bwd, flops, bflops, peak,
                 bwd_traffic = json.load(f).get("dram_bytes_per_backward")
         except Exception:
             bwd_traffic = None
-    # dQ path: layer.hpp FlashIpaLayer::materialize_ds (L <= 2048, dS <= 1 GiB, FIPA_BWD_DS override)
-    kernel = ("attn_bwd_kernel<true> (dK/dV, stores dS) + batched dQ GEMM gemm_bf16_kernel<256,MN,MN>"
+    # dQ path: layer.cpp FlashIpaLayer::ds_chunk (materialised dS up to L = 8192 within ds_cap_mb,
+    # query chunks beyond; FIPA_BWD_DS override); the batched dQ GEMM runs on CTA pairs
+    kernel = ("attn_bwd_kernel<true> (dK/dV, stores dS) + batched dQ GEMM gemm2_bf16_kernel<256,MN,MN>"
               if ds_mode else "attn_bwd_kernel<true> + attn_bwd_kernel<false> (dK/dV + dQ)")
     return {"bound": "tensor", "kernel": kernel,
             "achieved": achieved_bwd, "peak": peak, "unit": "TFLOP/s", "frac": achieved_bwd / peak,

@@ -13,10 +13,10 @@ python bench.py --shard rows --B 1 --L 32768 --no-cpu-baseline > $O/bench_cfg4_r
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-attn-long > $O/launches_raw.csv 2>> $O/bench.err
 FIPA_MICRO=1 ncu --set full --clock-control none --import-source on \
-    -k regex:"attn_|gemm_bf16|proj_pack|bwd_|cast_inputs|recenter|finish" -c 18 -o $O/step_full \
+    -k regex:"attn_|gemm|proj_pack|bwd_|cast_inputs|recenter|finish" -c 20 -o $O/step_full \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-attn-long > $O/ncu_full.log 2>&1
 python tools/ncu_summary.py $O/step_full.ncu-rep \
-    "FIPA_MICRO=1 ncu --set full --clock-control none --import-source on -k regex:\"attn_|gemm_bf16|proj_pack|bwd_|cast_inputs|recenter|finish\" -c 18 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-attn-long" \
-    "B=8 L=1024 north-star shape, one fwd+bwd training step (first 18 matching launches)" > $O/step_ncu_summary.json
+    "FIPA_MICRO=1 ncu --set full --clock-control none --import-source on -k regex:\"attn_|gemm|proj_pack|bwd_|cast_inputs|recenter|finish\" -c 20 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-attn-long" \
+    "B=8 L=1024 north-star shape, one fwd+bwd training step (first 20 matching launches)" > $O/step_ncu_summary.json
 python tools/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1
 ls -la $O
