@@ -200,6 +200,20 @@ def test_flash_grad_host_api_matches_device(fipa):
         assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
 
 
+def test_flash_grad_host_api_wide_rank(fipa):
+    """The reference calling convention (float64 host arrays) over the materialised backward."""
+    shape = dict(MAIN, rank=4)
+    model = _model(fipa, shape, 14)
+    batch = make_batch(shape, 2, 96, seed=14, mask_frac=0.1, bf16=True)
+    dout = np.random.default_rng(2).standard_normal((2, 96, shape["d_in"]))
+    out_d, g_d, _, _ = gpu_train_device(model, batch, dout)
+    out_h, g_h = model.flash_grad(batch["s"], batch["z1"], batch["z2"], batch["rot"], batch["trans"], dout,
+                                  mask=batch["mask"])
+    assert rel_dev(out_d, out_h) < 1e-6
+    for n, m in (("s", "s"), ("z2", "z2"), ("rot", "rotations"), ("w_k", "w_k"), ("w_bias", "w_bias")):
+        assert rel_dev(g_d[n], g_h[m]) < 1e-5, n
+
+
 def _check_large(fipa, B, L, seed, mask_frac, bwd_ds=None, oracle_samples=(), ds_cap_mb=None):
     """Large-L parity: forward output and all 15 gradients against the oracle-equivalent blocked
     emulation (helpers.emulated_backward: EXACT_SPLIT lifted restatement of the oracle backward,
