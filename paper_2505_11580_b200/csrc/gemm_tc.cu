@@ -71,6 +71,7 @@ struct EpiParams {
     const uint8_t* row_mask;
     int batch, batch_h;  // batched products (see GemmArgs)
     int a_blk, b_blk;    // MN-major operand loaded as ONE 4-D box of 64-column blocks (ld % 64 == 0)
+    bool tma_c16 = false;  // plain bf16 C: two 32-column chunks per 32 x 64 box, TMA stores
 };
 
 #ifdef FIPA_GEMM_TRACE
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_wait_ld();
                 if (warp == 2 && lane == 0) GTRACE(0, lu, 2 + 2 * (c0 / 32));
                 const int col0 = n0 + c0;
-                if (p.tma_c) {
+                if (p.tma_c || p.tma_c16) {
                     // warp-collective path: rows past M are clipped by the TMA store; nk == 0 (an
                     // empty split) cannot occur without split-K
                     if (col0 >= p.N || m0 + quad * 32 >= p.M) continue;
@@ -294,6 +295,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (zero_row) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+                }
+                if (p.tma_c16) {
+                    // bf16 C: chunk pairs fill one 128-byte line per row of a 32 x 64 box (stores
+                    // from registers wrote each 32-byte sector in two 16-byte halves from two
+                    // instructions: partial-sector writes)
+                    const int hsel = (c0 >> 5) & 1;
+                    uint8_t* sb = my_stage + (nstore % Cfg::kCBuf) * (32 * 128);
+                    if (hsel == 0) {
+                        if (nstore >= Cfg::kCBuf && lane == 0) ptx::bulk_wait_group_read<Cfg::kCBuf - 1>();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        *reinterpret_cast<uint4*>(sb + lane * 128 + (((4 * hsel + q) ^ (lane & 7)) << 4)) = w;
+                    }
+                    if (hsel == 1 || col0 + 32 >= p.N) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC, sb, col0 - 32 * hsel, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                        ++nstore;
+                    }
+                    continue;
                 }
                 if (p.tma_c) {
                     // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
@@ -527,7 +558,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::tmem_wait_ld();
                 if (warp == 2 && lane == 0) GTRACE(0, lu, 2 + 2 * (c0 / 32));
                 const int col0 = n0 + c0;
-                if (p.tma_c) {
+                if (p.tma_c || p.tma_c16) {
                     // warp-collective path: rows past M are clipped by the TMA store; nk == 0 (an
                     // empty split) cannot occur without split-K
                     if (col0 >= p.N || m0 + quad * 32 >= p.M) continue;
@@ -574,6 +605,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (zero_row) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+                }
+                if (p.tma_c16) {
+                    // bf16 C: chunk pairs fill one 128-byte line per row of a 32 x 64 box (stores
+                    // from registers wrote each 32-byte sector in two 16-byte halves from two
+                    // instructions: partial-sector writes)
+                    const int hsel = (c0 >> 5) & 1;
+                    uint8_t* sb = my_stage + (nstore % Cfg::kCBuf) * (32 * 128);
+                    if (hsel == 0) {
+                        if (nstore >= Cfg::kCBuf && lane == 0) ptx::bulk_wait_group_read<Cfg::kCBuf - 1>();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        *reinterpret_cast<uint4*>(sb + lane * 128 + (((4 * hsel + q) ^ (lane & 7)) << 4)) = w;
+                    }
+                    if (hsel == 1 || col0 + 32 >= p.N) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC, sb, col0 - 32 * hsel, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                        ++nstore;
+                    }
+                    continue;
                 }
                 if (p.tma_c) {
                     // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
@@ -680,6 +741,16 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
                 a.row_mask, static_cast<int>(nb), bh, a_blk ? 1 : 0, b_blk ? 1 : 0};
     // C as [batch / batch_h][M][batch_h][N]: box {32 cols, 1, 32 rows, 1} (the 2-D 32 x 32 box)
     CUtensorMap mapC = mapA;
+    // plain bf16 C (single product): 32 x 64 boxes
+    p.tma_c16 = a.out_bf16 && !a.accumulate && a.split_k <= 1 && nb == 1 && (a.ldc * 2) % 16 == 0 &&
+                (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+    if (p.tma_c16) {
+        const uint64_t cd[4] = {static_cast<uint64_t>(a.N), 1, static_cast<uint64_t>(a.M), 1};
+        const uint64_t cs[3] = {static_cast<uint64_t>(a.ldc) * 2, static_cast<uint64_t>(a.ldc) * 2,
+                                static_cast<uint64_t>(a.M) * a.ldc * 2};
+        const uint32_t cb[4] = {64, 1, 32, 1};
+        mapC = make_map_4d_bf16_strided(a.C, cd, cs, cb);
+    }
     if (tma_c) {
         const uint64_t cd[4] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(bh), static_cast<uint64_t>(a.M),
                                 nb / bh};
@@ -738,6 +809,16 @@ void launch_impl2(const GemmArgs& a, cudaStream_t stream) {
     EpiParams p{a.C, a.ldc, a.M, a.N, a.K, a.out_bf16, a.accumulate, tma_c, std::max(1, a.split_k), a.alpha, a.bias,
                 a.row_mask, static_cast<int>(nb), bh, a_blk ? 1 : 0, b_blk ? 1 : 0};
     CUtensorMap mapC = mapA;
+    // plain bf16 C (single product): 32 x 64 boxes
+    p.tma_c16 = a.out_bf16 && !a.accumulate && a.split_k <= 1 && nb == 1 && (a.ldc * 2) % 16 == 0 &&
+                (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+    if (p.tma_c16) {
+        const uint64_t cd[4] = {static_cast<uint64_t>(a.N), 1, static_cast<uint64_t>(a.M), 1};
+        const uint64_t cs[3] = {static_cast<uint64_t>(a.ldc) * 2, static_cast<uint64_t>(a.ldc) * 2,
+                                static_cast<uint64_t>(a.M) * a.ldc * 2};
+        const uint32_t cb[4] = {64, 1, 32, 1};
+        mapC = make_map_4d_bf16_strided(a.C, cd, cs, cb);
+    }
     if (tma_c) {
         const uint64_t cd[4] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(bh), static_cast<uint64_t>(a.M),
                                 nb / bh};

@@ -209,6 +209,24 @@ inline CUtensorMap make_map_4d_f32_strided(const void* base, const uint64_t dims
     return m;
 }
 
+// bf16 4-D tensor with explicit byte strides of dims 1..3, box {box0 (64: one 128-byte row), ...},
+// SWIZZLE_128B.
+inline CUtensorMap make_map_4d_bf16_strided(const void* base, const uint64_t dims_in[4], const uint64_t strides_in[3],
+                                            const uint32_t box_in[4]) {
+    CUtensorMap m{};
+    cuuint64_t dims[4] = {dims_in[0], dims_in[1], dims_in[2], dims_in[3]};
+    cuuint64_t strides[3] = {strides_in[0], strides_in[1], strides_in[2]};
+    cuuint32_t box[4] = {box_in[0], box_in[1], box_in[2], box_in[3]};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(4d bf16 strided) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 // fp32 5-D tensor with explicit byte strides of dims 1..4, box {box0..box4}, SWIZZLE_128B
 // (box0 * 4 == 128: one 128-byte row per box row).
 inline CUtensorMap make_map_5d_f32_strided(const void* base, const uint64_t dims_in[5], const uint64_t strides_in[4],
