@@ -50,6 +50,16 @@ Trunk::Trunk(const Config& cfg, int n_layers, std::uint64_t seed) : cfg_(cfg) {
 
 Trunk::~Trunk() {
     if (d_bb_) cudaFree(d_bb_);
+    if (side_) cudaStreamDestroy(side_);
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    if (join_ev_) cudaEventDestroy(join_ev_);
+}
+
+int Trunk::chains(std::int64_t B) const { return B >= 2 && layers_[0]->tuning().micro >= 2 ? 2 : 1; }
+
+std::size_t Trunk::chain_bytes(std::int64_t nb, std::int64_t L) const {
+    const std::size_t io = (std::size_t(nb) * L * cfg_.d_in * 4 + 255) / 256 * 256;
+    return (io + layers_[0]->workspace_size(nb, L) + 255) / 256 * 256;
 }
 
 void Trunk::set_backbone(int l, const double* w, const double* b) {
@@ -74,8 +84,10 @@ void Trunk::upload() {
 }
 
 std::size_t Trunk::workspace_size(std::int64_t B, std::int64_t L) const {
-    const std::size_t io = (std::size_t(B) * L * cfg_.d_in * 4 + 255) / 256 * 256;
-    return io + layers_[0]->workspace_size(B, L);
+    const int n = chains(B);
+    std::size_t total = 0;
+    for (int c = 0; c < n; ++c) total += chain_bytes(B * (c + 1) / n - B * c / n, L);
+    return total;
 }
 
 void Trunk::forward(std::int64_t B, std::int64_t L, const float* s, const float* z1, const float* z2,
@@ -86,19 +98,42 @@ void Trunk::forward(std::int64_t B, std::int64_t L, const float* s, const float*
     const std::size_t need = workspace_size(B, L);
     if (workspace == nullptr || workspace_bytes < need) throw ValueError("trunk workspace too small");
     if (dirty_) upload();
-    const std::size_t BL = std::size_t(B) * L;
-    const std::size_t io = (BL * cfg_.d_in * 4 + 255) / 256 * 256;
-    float* ipa_out = static_cast<float*>(workspace);
-    void* lws = static_cast<char*>(workspace) + io;
-    if (s_out != s) cuda_check(cudaMemcpyAsync(s_out, s, BL * cfg_.d_in * 4, cudaMemcpyDeviceToDevice, stream), "copy");
+    const std::size_t BL = std::size_t(B) * L, din = cfg_.d_in, rdz = std::size_t(cfg_.rank) * cfg_.d_z;
+    if (s_out != s) cuda_check(cudaMemcpyAsync(s_out, s, BL * din * 4, cudaMemcpyDeviceToDevice, stream), "copy");
     if (rot_out != rot) cuda_check(cudaMemcpyAsync(rot_out, rot, BL * 9 * 4, cudaMemcpyDeviceToDevice, stream), "copy");
     if (trans_out != trans)
         cuda_check(cudaMemcpyAsync(trans_out, trans, BL * 3 * 4, cudaMemcpyDeviceToDevice, stream), "copy");
+    const int n = chains(B);
+    if (n > 1) {
+        if (!side_) {
+            cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "stream");
+            cuda_check(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming), "event");
+        }
+        cuda_check(cudaEventRecord(fork_ev_, stream), "event record");
+        cuda_check(cudaStreamWaitEvent(side_, fork_ev_, 0), "stream wait");
+    }
     const std::size_t per = cfg_.d_in * 6 + 6;
-    for (int l = 0; l < n_layers(); ++l) {
-        layers_[l]->forward(B, L, s_out, z1, z2, rot_out, trans_out, mask, ipa_out, lws, workspace_bytes - io, stream);
-        launch_trunk_update(s_out, ipa_out, d_bb_ + l * per, d_bb_ + l * per + cfg_.d_in * 6, rot_out, trans_out,
-                            mask, static_cast<std::int64_t>(BL), int(cfg_.d_in), stream);
+    char* base = static_cast<char*>(workspace);
+    for (int c = 0; c < n; ++c) {
+        const std::int64_t b0 = B * c / n, nb = B * (c + 1) / n - b0;
+        const std::size_t r = std::size_t(b0) * L, rows = std::size_t(nb) * L;
+        const std::size_t io = (rows * din * 4 + 255) / 256 * 256, bytes = chain_bytes(nb, L);
+        cudaStream_t st = c == 0 ? stream : side_;
+        float* ipa_out = reinterpret_cast<float*>(base);
+        void* lws = base + io;
+        for (int l = 0; l < n_layers(); ++l) {
+            layers_[l]->forward(nb, L, s_out + r * din, z1 + r * rdz, z2 + r * rdz, rot_out + r * 9, trans_out + r * 3,
+                                mask ? mask + r : nullptr, ipa_out, lws, bytes - io, st);
+            launch_trunk_update(s_out + r * din, ipa_out, d_bb_ + l * per, d_bb_ + l * per + cfg_.d_in * 6,
+                                rot_out + r * 9, trans_out + r * 3, mask ? mask + r : nullptr,
+                                static_cast<std::int64_t>(rows), int(cfg_.d_in), st);
+        }
+        base += bytes;
+    }
+    if (n > 1) {
+        cuda_check(cudaEventRecord(join_ev_, side_), "event record");
+        cuda_check(cudaStreamWaitEvent(stream, join_ev_, 0), "stream wait");
     }
     cuda_check(cudaGetLastError(), "trunk launch");
 }

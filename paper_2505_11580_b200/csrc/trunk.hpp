@@ -32,6 +32,13 @@ public:
 
 private:
     void upload();
+    // Samples are independent through the whole trunk: with the layers' micro-batching on (B >= 2)
+    // they run as two sample chains on forked streams with no join between layers, so one chain's
+    // layer boundary (GPU drain + frame update) overlaps the other chain's kernels.
+    int chains(std::int64_t B) const;
+    std::size_t chain_bytes(std::int64_t nb, std::int64_t L) const;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
     Config cfg_;
     std::vector<std::unique_ptr<FlashIpaLayer>> layers_;
     std::vector<Backbone> bb_;
