@@ -163,7 +163,8 @@ int fipa_layer_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, i
 /* ---------------------------------------------------------------------------- training
  * Training forward: identical outputs to fipa_layer_forward, but over a workspace of
  * fipa_layer_train_workspace_size bytes in which it keeps what fipa_layer_backward needs (the
- * normalised attention output).  FIPA_PREC_BF16 only (tcgen05 path); lifted widths <= 448. */
+ * normalised attention output).  FIPA_PREC_BF16 only (tcgen05 path; z_factor_rank 3-4 through the
+ * materialised backward, whose workspace grows with L^2). */
 size_t fipa_layer_train_workspace_size(const fipa_layer* layer, int64_t B, int64_t L);
 int fipa_layer_forward_train(fipa_layer* layer, int64_t B, int64_t L, const float* s, const float* z1,
                              const float* z2, const float* rot, const float* trans, const uint8_t* mask,
