@@ -191,11 +191,15 @@ int fipa_layer_grad_host_f32(fipa_layer* layer, int64_t B, int64_t L, const floa
                              const float* z2, const float* rot, const float* trans, const uint8_t* mask,
                              const float* dout, float* out, float* ds, float* dz1, float* dz2, float* drot,
                              float* dtrans, float* dweights);
-/* Byte offsets of the training intermediates in a train workspace, -1 when absent:
+/* Byte offsets of the training intermediates in a train workspace (offsets[FIPA_TRAIN_LAYOUT_SLOTS]),
+ * -1 when absent:
  *   0 o_hat (f32 [B,L,H,dv_pad])  1 do_hat (bf16 [B*H,L,dv_pad])  2 D (f32 [B*H,L])
  *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B,L,H,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
- *   7 dfeat (bf16 [B*L,feat_ld]).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.  Returns 8.
- * Every slot is present in a train workspace (none is -1). */
+ *   7 dfeat (bf16 [B*L,feat_ld])  8 dk16 9 dv16 (bf16 [B,L,H,acc_ld]: the fused backward's bf16
+ *   dK / dV, every column; dk_acc / dv_acc then hold only the 32-column chunks with point /
+ *   translation columns.  -1 for z_factor_rank 3-4).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.
+ *   Returns FIPA_TRAIN_LAYOUT_SLOTS. */
+#define FIPA_TRAIN_LAYOUT_SLOTS 10
 int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
                                       int64_t* dims);
 int fipa_layer_backward_launches(const fipa_layer* layer);

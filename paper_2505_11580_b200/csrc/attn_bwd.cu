@@ -90,6 +90,8 @@ struct BwdParams {
     int acc_col0[2];   // first accumulator column each pair writes (dQ split over the pairs)
     int b2_col0[2];    // first B2 column each pair streams
     int ds_store;      // KV kernel: dS tiles also written to global [BH][Lk][ds_ld] (bf16) for dQ
+    int acc16;         // KV kernel: accumulators leave as bf16 (accP16 / accD16), plus fp32 for the
+    uint32_t f32_chunks[2];  // 32-column chunks flagged here (per role: point / translation columns)
 };
 
 struct Bars {
@@ -211,7 +213,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap b2P, const __grid_constant__ CUtensorMap statD,
                     const __grid_constant__ CUtensorMap b1D, const __grid_constant__ CUtensorMap b2D,
                     const __grid_constant__ CUtensorMap mapDS, const __grid_constant__ CUtensorMap accP,
-                    const __grid_constant__ CUtensorMap accD, BwdParams p) {
+                    const __grid_constant__ CUtensorMap accD, const __grid_constant__ CUtensorMap accP16,
+                    const __grid_constant__ CUtensorMap accD16, BwdParams p) {
     constexpr int kSlice = SL, kSliceBox = SL * 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -571,6 +574,44 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 };
                 ptx::tmem_ld32(tl, o0);
+                if (p.acc16) {
+                    // chunk pairs -> one 32 x 64 bf16 box (128-byte lines); the chunks holding point /
+                    // translation columns also leave in fp32
+                    const CUtensorMap* mAcc16 = role ? &accD16 : &accP16;
+                    const uint32_t f32m = p.f32_chunks[role];
+                    for (int cb = 0; cb < n32; cb += 2) {
+                        const bool has1 = cb + 1 < n32;
+                        ptx::tmem_wait_ld();
+                        read_out_a(cb);
+                        if (has1) {
+                            ptx::tmem_ld32(tl + 32 * (cb + 1), o1);
+                            ptx::tmem_wait_ld();
+                            read_out_a(cb + 1);
+                        }
+                        if (lane == 0) ptx::bulk_wait_group_read<0>();
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t* w = k < 4 ? o0 + 8 * k : o1 + 8 * (k - 4);
+                            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                            if (k < 4 || has1)
+                                q = make_uint4(ptx::pack_bf16x2(__uint_as_float(w[0]), __uint_as_float(w[1])),
+                                               ptx::pack_bf16x2(__uint_as_float(w[2]), __uint_as_float(w[3])),
+                                               ptx::pack_bf16x2(__uint_as_float(w[4]), __uint_as_float(w[5])),
+                                               ptx::pack_bf16x2(__uint_as_float(w[6]), __uint_as_float(w[7])));
+                            *reinterpret_cast<uint4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) = q;
+                        }
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0 && rows_ok) {
+                            ptx::tma_store_5d(mAcc16, box, 32 * cb, hh, gi, bb, g);
+                            ptx::bulk_commit_group();
+                        }
+                        if ((f32m >> cb) & 1u) stage_box(o0, cb);
+                        if (has1 && ((f32m >> (cb + 1)) & 1u)) stage_box(o1, cb + 1);
+                        if (cb + 2 < n32) ptx::tmem_ld32(tl + 32 * (cb + 2), o0);
+                    }
+                } else
                 for (int cb = 0; cb < n32; cb += 2) {
                     ptx::tmem_wait_ld();
                     read_out_a(cb);
@@ -861,7 +902,7 @@ void launch_depth(const LayerDims& d, const AttnBwdArgs& a, const BwdParams& p, 
     const int clusters = std::min(units, resident_clusters(reinterpret_cast<const void*>(kern), smem));
     dim3 grid(static_cast<unsigned>(clusters * 4), 1u);
     launch_pdl(kern, grid, dim3(kThreads), size_t(smem), stream, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-               maps[6], maps[7], maps[8], p);
+               maps[6], maps[7], maps[8], maps[9], maps[10], p);
 }
 
 template <bool KV>
@@ -920,6 +961,23 @@ CUtensorMap acc_map(float* out, int col0, int n2, int H, int chunk, int B, int G
     return make_map_5d_f32_strided(out + col0, dims, strides, box);
 }
 
+// bf16 copy of the same accumulator: boxes of 64 columns x 32 rows.
+CUtensorMap acc_map16(__nv_bfloat16* out, int n2, int H, int chunk, int B, int G, int acc_ld) {
+    const uint64_t row = uint64_t(acc_ld) * 2;
+    const uint64_t dims[5] = {uint64_t(n2), uint64_t(H), uint64_t(chunk), uint64_t(B), uint64_t(G)};
+    const uint64_t strides[4] = {row, row * H, row * H * chunk, row * H * chunk * B};
+    const uint32_t box[5] = {64, 1, 32, 1, 1};
+    return make_map_5d_bf16_strided(out, dims, strides, box);
+}
+
+// 32-column chunks of [0, n) that intersect columns [lo, hi)
+uint32_t chunk_mask(int lo, int hi, int n) {
+    uint32_t m = 0;
+    for (int k = 0; 32 * k < n && k < 32; ++k)
+        if (32 * k < hi && 32 * k + 32 > lo) m |= 1u << k;
+    return m;
+}
+
 void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stream, int which) {
     if (!attn_bwd_supported(d)) throw std::invalid_argument("tcgen05 attention backward: unsupported widths");
     const uint64_t BH = static_cast<uint64_t>(a.B) * d.heads;
@@ -970,15 +1028,22 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.acc_out[1] = a.dk_acc;
         p.acc_ld = a.acc_ld;
         p.ds_store = a.ds != nullptr ? 1 : 0;
+        // bf16 accumulators (unsharded, whole-query launches): fp32 kept for the chunks holding the
+        // point / translation columns -- dV: [c + r d_z, dv_used), dK: [c, zq)
+        p.acc16 = a.dk16 != nullptr && a.dv16 != nullptr && !p.acc_add && G == 1 && a.acc_ld % 8 == 0;
+        p.f32_chunks[0] = p.acc16 ? chunk_mask(d.c + d.rank * d.d_z, d.dv_used, p.role[0].n2) : 0xFFFFFFFFu;
+        p.f32_chunks[1] = p.acc16 ? chunk_mask(d.c, d.zq, p.role[1].n2) : 0xFFFFFFFFu;
         if (p.ds_store && (G > 1 || a.ds_ld % 8 != 0 || a.ds_ld < p.ncol))
             throw std::invalid_argument("attention backward: materialised dS needs unsharded keys, ds_ld >= chunk, % 8");
         if (p.acc_add && G > 1) throw std::invalid_argument("attention backward: chunked accumulation is unsharded only");
         const CUtensorMap m0 = stat(a.khat, nqk);
-        const CUtensorMap maps[9] = {
+        const CUtensorMap maps[11] = {
             m0, tile(a.qhat, p.kb1), slice(a.dohat, p.slice), stat(a.vhat, nv), tile(a.dohat, p.kb1),
             slice(a.qhat, p.slice), p.ds_store ? make_map_3d_bf16(a.ds, p.ncol, a.L, BH, a.ds_ld, 64, BM) : m0,
             a.dv_acc ? acc_map(a.dv_acc, 0, p.role[0].n2, d.heads, kc, a.B, G, a.acc_ld) : m0,
-            a.dk_acc ? acc_map(a.dk_acc, 0, p.role[1].n2, d.heads, kc, a.B, G, a.acc_ld) : m0};
+            a.dk_acc ? acc_map(a.dk_acc, 0, p.role[1].n2, d.heads, kc, a.B, G, a.acc_ld) : m0,
+            p.acc16 ? acc_map16(a.dv16, p.role[0].n2, d.heads, kc, a.B, G, a.acc_ld) : m0,
+            p.acc16 ? acc_map16(a.dk16, p.role[1].n2, d.heads, kc, a.B, G, a.acc_ld) : m0};
         launch<true>(d, a, p, maps, stream);
     }
     if ((which & 2) && a.ds != nullptr) {
@@ -1035,10 +1100,11 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         p.b2_col0[1] = nq0;
         p.acc_ld = a.acc_ld;
         const CUtensorMap q0map = stat(a.qhat, nqk);
-        const CUtensorMap maps[9] = {q0map, tile(a.khat, p.kb1), slice(a.khat, p.slice),
-                                     stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat, p.slice), q0map,
-                                     acc_map(a.dq_acc, 0, nq0, d.heads, a.L, a.B, 1, a.acc_ld),
-                                     acc_map(a.dq_acc, nq0, d.dqk_mma - nq0, d.heads, a.L, a.B, 1, a.acc_ld)};
+        const CUtensorMap maps[11] = {q0map, tile(a.khat, p.kb1), slice(a.khat, p.slice),
+                                      stat(a.dohat, nv), tile(a.vhat, p.kb1),  slice(a.khat, p.slice), q0map,
+                                      acc_map(a.dq_acc, 0, nq0, d.heads, a.L, a.B, 1, a.acc_ld),
+                                      acc_map(a.dq_acc, nq0, d.dqk_mma - nq0, d.heads, a.L, a.B, 1, a.acc_ld), q0map,
+                                      q0map};
         launch<false>(d, a, p, maps, stream);
     }
 }

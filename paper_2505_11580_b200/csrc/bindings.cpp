@@ -480,9 +480,11 @@ public:
         check(rc);
     }
     py::tuple train_workspace_layout(int64_t B, int64_t L) const {
-        int64_t off[8], dims[3];
-        if (fipa_layer_train_workspace_layout(layer_, B, L, off, dims) != 8) throw FipaValueError("invalid batch shape");
-        return py::make_tuple(std::vector<int64_t>(off, off + 8), std::vector<int64_t>(dims, dims + 3));
+        int64_t off[FIPA_TRAIN_LAYOUT_SLOTS], dims[3];
+        if (fipa_layer_train_workspace_layout(layer_, B, L, off, dims) != FIPA_TRAIN_LAYOUT_SLOTS)
+            throw FipaValueError("invalid batch shape");
+        return py::make_tuple(std::vector<int64_t>(off, off + FIPA_TRAIN_LAYOUT_SLOTS),
+                              std::vector<int64_t>(dims, dims + 3));
     }
     // flash_grad(s, z1, z2, rotations, translations, dout, mask=None) -> (out, grads)
     // Forward + backward of sum(out * dout) through the host-buffer C ABI; grads is a dict with

@@ -534,6 +534,30 @@ __global__ void __launch_bounds__(256, 4) bwd_unpack_geo_kernel(LayerDims d, Bwd
     }
 }
 
+// Accumulator element i from the bf16 copy (H16: scalar / pair columns of dK, dV) or fp32.
+template <bool H16>
+__device__ __forceinline__ float acc_at(const float* f, const __nv_bfloat16* b, int64_t i) {
+    if constexpr (H16) return __bfloat162float(b[i]);
+    else return __ldg(f + i);
+}
+// Scalar-column pair (even element i) of accumulator tsel (0 dQ, 1 dK, 2 dV): dQ always fp32.
+template <bool H16>
+__device__ __forceinline__ float2 acc2_sel(const BwdUnpackArgs& a, int tsel, int64_t i) {
+    if constexpr (H16) {
+        if (tsel != 0) {
+            const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>((tsel == 1 ? a.dk16 : a.dv16) + i));
+            return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+        }
+        return __ldg(reinterpret_cast<const float2*>(a.dq_acc + i));
+    } else {
+        return __ldg(reinterpret_cast<const float2*>((tsel == 0 ? a.dq_acc : (tsel == 1 ? a.dk_acc : a.dv_acc)) + i));
+    }
+}
+
+// FAST: H <= 8 heads, one pair column per thread, the row's scalar columns in kBatchF float2 per
+// thread (every training config); the general form otherwise.  (Two instantiations so the fast
+// loop's register budget holds only its 8 head partials: spills there cost ~2x.)
+template <bool ACC16, bool FAST>
 __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
@@ -555,46 +579,63 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         s_wlb[e] = a.wl_bias[e];
     }
     __syncthreads();
-    float pw[kUnpackMaxH];  // this thread's d(w_l w_bias) partials over the block's residues
+    constexpr int kPw = FAST ? 8 : kUnpackMaxH;
+    float pw[kPw];  // this thread's d(w_l w_bias) partials over the block's residues
 #pragma unroll
-    for (int h = 0; h < kUnpackMaxH; ++h) pw[h] = 0.f;
+    for (int h = 0; h < kPw; ++h) pw[h] = 0.f;
 
     // Fast path (H <= 8, one pair column per thread, a row's scalar columns in kBatchF float2 per
     // thread): ALL of a row's loads -- 24 pair-column loads and the scalar float2 loads -- are
     // issued before any use, so each row costs one memory latency instead of two.
-    constexpr int kBatchF = 6;
-    const bool fast = H <= 8 && reg_dwlb && pairs && rdz == static_cast<int>(blockDim.x) &&
-                      3 * H * half_c <= kBatchF * static_cast<int>(blockDim.x);
+    constexpr int kBatchF = 6;  // (unpack_fast() on the host selects FAST)
     // persistent: groups of kUnpackRows residues strided over a grid of (SMs x resident blocks)
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t row_begin = grp * kUnpackRows;
     const int nrows = static_cast<int>(BL - row_begin < kUnpackRows ? BL - row_begin : kUnpackRows);
+    // raw loaded bits, converted only at use (a conversion right after a load would wait for it
+    // and serialise the row's loads: measured 2x on the bf16 copies)
     struct RowLoads {
-        float qq[8], kq[8], vq[8];
-        float2 v[kBatchF];
+        float qq[8];
+        uint32_t kq[8], vq[8];  // fp32 bits, or a bf16 in the low half (ACC16)
+        uint2 v[kBatchF];       // fp32 pair, or a bf16 pair in .x (ACC16, dK / dV columns)
         float z2v, s1;
     };
+    auto raw16 = [](const __nv_bfloat16* b, int64_t i) -> uint32_t {
+        return __ldg(reinterpret_cast<const unsigned short*>(b + i));
+    };
+    auto as_f = [](uint32_t r) { return ACC16 ? __uint_as_float(r << 16) : __uint_as_float(r); };
     const int total = 3 * H * half_c;
     auto load_row = [&](int64_t row, RowLoads& L) {
-        const float* qrow = a.dq_acc + row * H * acc_h;
-        const float* krow = a.dk_acc + row * H * acc_h;
-        const float* vrow = a.dv_acc + row * H * acc_h;
+        const int64_t base = row * H * acc_h;
         L.z2v = __ldg(a.z2 + row * rdz + tid);
         L.s1 = __ldg(a.dz1_epi + row * rdz + tid);
+        const float* qp = a.dq_acc + base + zq + tid;
+        const int64_t ko = base + zq + tid, vo = base + c + tid;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int h = min(u, H - 1);
-            L.qq[u] = __ldg(qrow + h * acc_h + zq + tid);
-            L.kq[u] = __ldg(krow + h * acc_h + zq + tid);
-            L.vq[u] = __ldg(vrow + h * acc_h + c + tid);
+            L.qq[u] = __ldg(qp + h * acc_h);
+            if constexpr (ACC16) {
+                L.kq[u] = raw16(a.dk16, ko + h * acc_h);
+                L.vq[u] = raw16(a.dv16, vo + h * acc_h);
+            } else {
+                L.kq[u] = __float_as_uint(__ldg(a.dk_acc + ko + h * acc_h));
+                L.vq[u] = __float_as_uint(__ldg(a.dv_acc + vo + h * acc_h));
+            }
         }
 #pragma unroll
         for (int u = 0; u < kBatchF; ++u) {
             const int idx = min(tid + u * static_cast<int>(blockDim.x), total - 1);
             const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
             const int h = rem / half_c, cc = 2 * (rem - h * half_c);
-            const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
-            L.v[u] = __ldg(reinterpret_cast<const float2*>(src));
+            const int64_t i = base + h * acc_h + cc;
+            if (ACC16 && tsel != 0) {
+                L.v[u].x = __ldg(reinterpret_cast<const unsigned int*>((tsel == 1 ? a.dk16 : a.dv16) + i));
+                L.v[u].y = 0u;
+            } else {
+                L.v[u] = __ldg(reinterpret_cast<const uint2*>(
+                    (tsel == 0 ? a.dq_acc : (tsel == 1 ? a.dk_acc : a.dv_acc)) + i));
+            }
         }
     };
     auto finish_row = [&](int64_t row, const RowLoads& L) {
@@ -603,9 +644,9 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (u < H) {
-                const float k2 = kLn2 * L.kq[u];
+                const float k2 = kLn2 * as_f(L.kq[u]);
                 s1 += L.qq[u];
-                s2 += s_wlb[u * dz + dd] * k2 + L.vq[u];
+                s2 += s_wlb[u * dz + dd] * k2 + as_f(L.vq[u]);
                 pw[u] = fmaf(k2, L.z2v, pw[u]);
             }
         }
@@ -617,14 +658,24 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
             const int idx = tid + u * static_cast<int>(blockDim.x);
             if (idx < total) {
                 // dproj column of the same (tensor, head, channel pair): idx * 2 in [q | k | v] order
-                const float sc = idx >= H * half_c && idx < 2 * H * half_c ? kscale : 1.f;
-                *reinterpret_cast<uint32_t*>(dp + 2 * idx) = ptx_pack(L.v[u].x * sc, L.v[u].y * sc);
+                const bool kcol = idx >= H * half_c && idx < 2 * H * half_c;
+                const float sc = kcol ? kscale : 1.f;
+                float vx, vy;
+                if (ACC16 && idx >= H * half_c) {  // dK / dV: a bf16 pair
+                    vx = __uint_as_float(L.v[u].x << 16);
+                    vy = __uint_as_float(L.v[u].x & 0xFFFF0000u);
+                } else {
+                    vx = __uint_as_float(L.v[u].x);
+                    vy = __uint_as_float(L.v[u].y);
+                }
+                *reinterpret_cast<uint32_t*>(dp + 2 * idx) = ptx_pack(vx * sc, vy * sc);
             }
         }
         for (int x = d.n_proj + tid; x < a.nproj_ld; x += blockDim.x) dp[x] = __float2bfloat16_rn(0.f);
     };
     // two residues' loads in flight per thread before either is used
-    for (int rr = 0; fast && rr < nrows; rr += 2) {
+    if constexpr (FAST)
+    for (int rr = 0; rr < nrows; rr += 2) {
         RowLoads L0, L1;
         load_row(row_begin + rr, L0);
         if (rr + 1 < nrows) load_row(row_begin + rr + 1, L1);
@@ -632,11 +683,10 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         if (rr + 1 < nrows) finish_row(row_begin + rr + 1, L1);
     }
 
-    for (int rr = 0; !fast && rr < nrows; ++rr) {
+    if constexpr (!FAST)
+    for (int rr = 0; rr < nrows; ++rr) {
         const int64_t row = row_begin + rr;
-        const float* qrow = a.dq_acc + row * H * acc_h;
-        const float* krow = a.dk_acc + row * H * acc_h;
-        const float* vrow = a.dv_acc + row * H * acc_h;
+        const int64_t rbase = row * H * acc_h;
         __nv_bfloat16* dp = a.dproj + row * a.nproj_ld;
         // ---- pair columns
         for (int e = tid; e < rdz; e += blockDim.x) {
@@ -650,9 +700,9 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int h = min(h0 + u, H - 1);
-                    qq[u] = __ldg(qrow + h * acc_h + zq + e);
-                    kq[u] = __ldg(krow + h * acc_h + zq + e);
-                    vq[u] = __ldg(vrow + h * acc_h + c + e);
+                    qq[u] = __ldg(a.dq_acc + rbase + h * acc_h + zq + e);
+                    kq[u] = acc_at<ACC16>(a.dk_acc, a.dk16, rbase + h * acc_h + zq + e);
+                    vq[u] = acc_at<ACC16>(a.dv_acc, a.dv16, rbase + h * acc_h + c + e);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -661,7 +711,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
                         const float k2 = kLn2 * kq[u];
                         s1 += qq[u];
                         s2 += s_wlb[h * dz + dd] * k2 + vq[u];
-                        if (reg_dwlb) pw[u + h0] = fmaf(k2, z2v, pw[u + h0]);
+                        if (reg_dwlb) pw[(u + h0) % kPw] = fmaf(k2, z2v, pw[(u + h0) % kPw]);
                         else atomicAdd(&s_dwlb[h * dz + dd], k2 * z2v);
                     }
                 }
@@ -681,8 +731,8 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
                     const int idx = min(base + u * static_cast<int>(blockDim.x), total - 1);
                     const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
                     const int h = rem / half_c, cc = 2 * (rem - h * half_c);
-                    const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
-                    v[u] = __ldg(reinterpret_cast<const float2*>(src));
+                    const int64_t i = rbase + h * acc_h + cc;
+                    v[u] = acc2_sel<ACC16>(a, tsel, i);
                     dst[u] = tsel * H * c + h * c + cc;
                     if (tsel == 1) {
                         v[u].x *= kscale;
@@ -698,8 +748,10 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
             for (int idx = tid; idx < 3 * H * c; idx += blockDim.x) {
                 const int tsel = idx / (H * c), rem = idx - tsel * (H * c);
                 const int h = rem / c, cc = rem - h * c;
-                const float* src = (tsel == 0 ? qrow : (tsel == 1 ? krow : vrow)) + h * acc_h + cc;
-                dp[tsel * H * c + h * c + cc] = __float2bfloat16_rn(__ldg(src) * (tsel == 1 ? kscale : 1.f));
+                const int64_t i = rbase + h * acc_h + cc;
+                const float x = tsel == 0 ? __ldg(a.dq_acc + i)
+                                          : (tsel == 1 ? acc_at<ACC16>(a.dk_acc, a.dk16, i) : acc_at<ACC16>(a.dv_acc, a.dv16, i));
+                dp[tsel * H * c + h * c + cc] = __float2bfloat16_rn(x * (tsel == 1 ? kscale : 1.f));
             }
         }
         for (int e = d.n_proj + tid; e < a.nproj_ld; e += blockDim.x) dp[e] = __float2bfloat16_rn(0.f);
@@ -708,7 +760,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     if (reg_dwlb && tid < rdz) {
 #pragma unroll
         for (int h = 0; h < kUnpackMaxH; ++h)
-            if (h < H) atomicAdd(&s_dwlb[h * dz + tid % dz], pw[h]);
+            if (h < H && h < kPw) atomicAdd(&s_dwlb[h * dz + tid % dz], pw[h]);
     }
     __syncthreads();
     for (int e = tid; e < H * dz; e += blockDim.x) atomicAdd(&a.dwlb[e], s_dwlb[e]);
@@ -906,6 +958,13 @@ void launch_bwd_prep(const LayerDims& d, const BwdPrepArgs& a, cudaStream_t stre
     bwd_prep_kernel<<<static_cast<unsigned>(int64_t(a.B) * a.L), 256, smem, stream>>>(d, a);
 }
 
+// The streaming kernel's fast form (see bwd_unpack_kernel): 256 threads, one pair column each.
+bool unpack_fast(const LayerDims& d, int acc_ld, int nproj_ld) {
+    const int rdz = d.rank * d.d_z;
+    const bool pairs = d.c % 2 == 0 && acc_ld % 2 == 0 && nproj_ld % 2 == 0;
+    return d.heads <= 8 && pairs && rdz == 256 && 3 * d.heads * (d.c / 2) <= 6 * 256;
+}
+
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream) {
     if (std::max(d.dqk_used, d.dv_used) > a.acc_ld) throw std::invalid_argument("bwd_unpack: accumulator stride");
     if (d.heads > kUnpackMaxH) throw std::invalid_argument("bwd_unpack: at most 16 heads");
@@ -915,11 +974,15 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     // 0.114 ms -- it serialises behind the streaming loads and spills at the 128-register cap)
     launch_pdl(bwd_unpack_geo_kernel, dim3(static_cast<unsigned>((BL + 7) / 8)), dim3(256), 0, stream, d, a);
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(bwd_unpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if ((a.dk16 == nullptr) != (a.dv16 == nullptr)) throw std::invalid_argument("bwd_unpack: dk16 and dv16 go together");
+    const bool fast = unpack_fast(d, a.acc_ld, a.nproj_ld);
+    auto kern = a.dk16 != nullptr ? (fast ? bwd_unpack_kernel<true, true> : bwd_unpack_kernel<true, false>)
+                                  : (fast ? bwd_unpack_kernel<false, true> : bwd_unpack_kernel<false, false>);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int sms = device_sm_count();
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;
     const int64_t grid = std::min<int64_t>(groups, int64_t(sms) * 2);  // 2 resident blocks per SM
-    launch_pdl(bwd_unpack_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), smem, stream, d, a);
+    launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(256), smem, stream, d, a);
 }
 
 // Streaming row kernels of the materialised backward: one block per (sample, head, query) row, 8

@@ -492,12 +492,14 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
     offsets[5] = off(w.dv_acc);
     offsets[6] = off(w.dproj);
     offsets[7] = off(w.dfeat);
+    offsets[8] = w.dk16 ? off(w.dk16) : -1;
+    offsets[9] = w.dv16 ? off(w.dv16) : -1;
     if (dims != nullptr) {
         dims[0] = layer->impl->acc_ld();
         dims[1] = layer->impl->nproj_ld();
         dims[2] = layer->impl->dims().feat_ld;
     }
-    return 8;
+    return FIPA_TRAIN_LAYOUT_SLOTS;
 }
 
 int fipa_layer_bwd_stage_times(const fipa_layer* layer, float* ms, int n) {

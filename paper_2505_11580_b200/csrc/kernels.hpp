@@ -208,6 +208,12 @@ struct AttnBwdArgs {
     // dQ GEMM writes those query rows.  qn = 0: all queries.
     int q0 = 0, qn = 0, acc_add = 0;
     int ring[5] = {0, 0, 0, 0, 0};  // forced ring plan (nst1, nst2, nab, kb1, slice rows), 0 = automatic
+    // Optional bf16 copies of dK / dV ([B, L, H, acc_ld], unsharded whole-query launches only):
+    // every accumulator column also leaves as bf16 (half the drain bytes of the scalar and pair
+    // columns, which bwd_unpack reads from here); dk_acc / dv_acc then receive only the 32-column
+    // chunks that hold point / translation columns (cancellation-sensitive, kept fp32).
+    __nv_bfloat16* dk16 = nullptr;
+    __nv_bfloat16* dv16 = nullptr;
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both
@@ -250,6 +256,10 @@ struct BwdUnpackArgs {
     float* dg;              // [H]     accumulated (zero first): dL/d(gamma_h w_l w_c)
     float* dwlb;            // [H, d_z] accumulated (zero first): dL/d(w_l w_bias)
     int B, L;
+    // bf16 dK / dV (AttnBwdArgs::dk16 / dv16): the scalar and pair columns are read from there
+    // (null: from dk_acc / dv_acc); the geometry columns always come from the fp32 accumulators
+    const __nv_bfloat16* dk16 = nullptr;
+    const __nv_bfloat16* dv16 = nullptr;
 };
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream);
 // Materialised attention backward (FlashIpaLayer::dense_attention_backward), rows of length L with

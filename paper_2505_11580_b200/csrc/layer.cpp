@@ -45,6 +45,14 @@ std::size_t round_up(std::size_t x, std::size_t m) { return (x + m - 1) / m * m;
 // alternative (A/B checks); the single-CTA kernel does not read sharded keys, so a sharded
 // forward never takes it.
 enum class AttnImpl { pair, pass, one_sm };
+// bf16 dK / dV hand-off to the unpack (AttnBwdArgs::dk16); FIPA_BF16_ACC=0 keeps them fp32 (A/B)
+bool bf16_acc_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FIPA_BF16_ACC");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
 AttnImpl attention_impl(const LayerDims& d, Tuning::Attn forced, bool sharded) {
     if (forced == Tuning::Attn::one_sm && !sharded) return AttnImpl::one_sm;
     if (forced == Tuning::Attn::pass && attn_fwd_pass_supported(d)) return AttnImpl::pass;
@@ -579,6 +587,10 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         w.dq_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
         w.dk_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
         w.dv_acc = reinterpret_cast<float*>(take(BHL * acc_ld() * 4));
+        if (!dense_backward()) {
+            w.dk16 = reinterpret_cast<__nv_bfloat16*>(take(BHL * acc_ld() * 2));
+            w.dv16 = reinterpret_cast<__nv_bfloat16*>(take(BHL * acc_ld() * 2));
+        }
         w.dproj = reinterpret_cast<__nv_bfloat16*>(take(BL * nproj_ld() * 2));
         w.dz1_epi = reinterpret_cast<float*>(take(BL * rdz * 4));
         w.geo_epi = reinterpret_cast<float*>(take(BL * 12 * 4));
@@ -635,6 +647,8 @@ FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b
     v.dq_acc = adv(w.dq_acc, n * H * acc_ld() * 4);
     v.dk_acc = adv(w.dk_acc, n * H * acc_ld() * 4);
     v.dv_acc = adv(w.dv_acc, n * H * acc_ld() * 4);
+    v.dk16 = adv(w.dk16, n * H * acc_ld() * 2);
+    v.dv16 = adv(w.dv16, n * H * acc_ld() * 2);
     v.dproj = adv(w.dproj, n * nproj_ld() * 2);
     v.dz1_epi = adv(w.dz1_epi, n * rdz * 4);
     v.geo_epi = adv(w.geo_epi, n * 12 * 4);
@@ -1308,6 +1322,13 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
             a.ds = ws.ds;
             a.ds_ld = ws.ds_ld;
         }
+        // bf16 dK / dV copies for the unpack (unsharded whole-query launches; the query-chunked
+        // dS accumulates by TMA reduction, the sharded one reduce-scatters fp32 partials)
+        const bool acc16 = bf16_acc_enabled() && shard == nullptr && ws.dk16 != nullptr && !(ws.ds != nullptr && ws.ds_ld < L);
+        if (acc16) {
+            a.dk16 = ws.dk16;
+            a.dv16 = ws.dv16;
+        }
         if (shard == nullptr && ws.ds != nullptr && ws.ds_ld < L) {
             // query-chunked materialised dS: dK/dV kernel + dQ GEMM per chunk of ds_ld queries
             for (int q0 = 0; q0 < int(L); q0 += ws.ds_ld) {
@@ -1335,6 +1356,11 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         a.dk_acc = shard ? shard->dk_own : ws.dk_acc;
         a.dv_acc = shard ? shard->dv_own : ws.dv_acc;
         a.acc_ld = acc_ld();
+        if (bf16_acc_enabled() && shard == nullptr && ws.dk16 != nullptr && !(ws.ds != nullptr && ws.ds_ld < L) &&
+            !dense_backward()) {
+            a.dk16 = ws.dk16;  // written by the dK/dV kernel above (same condition)
+            a.dv16 = ws.dv16;
+        }
         a.proj = ws.proj;
         a.rot = rot;
         a.trans_c = ws.trans_c;

@@ -267,6 +267,8 @@ public:
         float* dq_acc = nullptr;           // [BH, L, acc_ld]
         float* dk_acc = nullptr;
         float* dv_acc = nullptr;
+        __nv_bfloat16* dk16 = nullptr;     // [BH, L, acc_ld] bf16 dK / dV (fused backward: scalar and
+        __nv_bfloat16* dv16 = nullptr;     // pair columns; dk_acc / dv_acc keep the geometry chunks)
         __nv_bfloat16* dproj = nullptr;    // [BL, nproj_ld]
         float* dz1_epi = nullptr;          // [BL, r d_z]
         float* geo_epi = nullptr;          // [BL, 12] dR | dt of the output epilogue

@@ -227,6 +227,27 @@ inline CUtensorMap make_map_4d_bf16_strided(const void* base, const uint64_t dim
     return m;
 }
 
+// bf16 5-D tensor with explicit byte strides of dims 1..4, box {box0 (64: one 128-byte row), ...},
+// SWIZZLE_128B.
+inline CUtensorMap make_map_5d_bf16_strided(const void* base, const uint64_t dims_in[5], const uint64_t strides_in[4],
+                                            const uint32_t box_in[5]) {
+    CUtensorMap m{};
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    for (int i = 0; i < 5; ++i) {
+        dims[i] = dims_in[i];
+        box[i] = box_in[i];
+    }
+    for (int i = 0; i < 4; ++i) strides[i] = strides_in[i];
+    CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        throw std::runtime_error("cuTensorMapEncodeTiled(5d bf16 strided) failed: " + std::to_string(int(r)));
+    }
+    return m;
+}
+
 // fp32 5-D tensor with explicit byte strides of dims 1..4, box {box0..box4}, SWIZZLE_128B
 // (box0 * 4 == 128: one 128-byte row per box row).
 inline CUtensorMap make_map_5d_f32_strided(const void* base, const uint64_t dims_in[5], const uint64_t strides_in[4],

@@ -182,9 +182,20 @@ def test_attention_backward_stage_parity(fipa, ds):
     assert rel_dev(lse_ref, lse) < 1e-3
     assert rel_dev((do * o).sum(-1), D) < 1e-3
     dq_r, dk_r, dv_r = be.attention_backward(q, k, v, lse, do, D)
+    # dQ in fp32; dK / dV: every column in the bf16 copies (slots 8, 9), the 32-column chunks with
+    # point / translation columns also in fp32 (dK: [c, zq), dV: [c + r d_z, dv_used))
+    c, zq, rdz = shape["c"], 176, shape["rank"] * shape["d_z"]
+    geo = {"dk": (c, zq), "dv": (c + rdz, c + rdz + 6 + 3 * shape["n_value"])}
     for name, idx, ref in (("dq", 3, dq_r), ("dk", 4, dk_r), ("dv", 5, dv_r)):
         got = ws_view(ws, toff[idx], H * L * acc_ld, "f32").reshape(L, H, acc_ld).transpose(1, 0, 2)
-        assert rel_dev(ref[..., :432], got[..., :432]) < 1e-2, name
+        if name == "dq":
+            assert rel_dev(ref[..., :432], got[..., :432]) < 1e-2, name
+            continue
+        g16 = ws_view(ws, toff[idx + 4], H * L * acc_ld, "bf16").reshape(L, H, acc_ld).transpose(1, 0, 2)
+        assert rel_dev(ref[..., :432], g16[..., :432]) < 1e-2, name
+        lo, hi = geo[name]
+        lo32, hi32 = lo // 32 * 32, (hi + 31) // 32 * 32
+        assert rel_dev(ref[..., lo32:hi32], got[..., lo32:hi32]) < 1e-2, name + " geometry chunks"
 
 
 def test_flash_grad_host_api_matches_device(fipa):
@@ -279,9 +290,10 @@ def test_backward_query_chunked_ds(fipa, cap_mb):
     assert model.tuning()["ds_cap_mb"] == cap_mb
     _, g_chunk, _, _ = gpu_train_device(model, batch, dout)
     for n in GRADS:
-        # fp32 summation order of dK / dV differs; a bf16 rounding of dproj that flips moves the input
-        # gradients by ~1e-4 relative -- far inside the 2e-2 gate both paths pass above
-        assert rel_dev(g_full[n], g_chunk[n]) < 1e-3, n
+        # the single-buffer path hands dK / dV to the unpack as bf16 (scalar and pair columns), the
+        # chunked one accumulates them in fp32 by TMA reduction: 2^-9-relative roundings (and fp32
+        # summation order) apart, ~1e-3 on the gradients -- far inside the 2e-2 gate both pass above
+        assert rel_dev(g_full[n], g_chunk[n]) < 4e-3, n
     assert errs
 
 
