@@ -197,9 +197,10 @@ int fipa_layer_grad_host_f32(fipa_layer* layer, int64_t B, int64_t L, const floa
  *   3 dq_acc 4 dk_acc 5 dv_acc (f32 [B,L,H,acc_ld])  6 dproj (bf16 [B*L,nproj_ld])
  *   7 dfeat (bf16 [B*L,feat_ld])  8 dk16 9 dv16 (bf16 [B,L,H,acc_ld]: the fused backward's bf16
  *   dK / dV, every column; dk_acc / dv_acc then hold only the 32-column chunks with point /
- *   translation columns.  -1 for z_factor_rank 3-4).  dims[3] receives {acc_ld, nproj_ld, feat_ld}.
- *   Returns FIPA_TRAIN_LAYOUT_SLOTS. */
-#define FIPA_TRAIN_LAYOUT_SLOTS 10
+ *   translation columns.  -1 for z_factor_rank 3-4)  10 dq16 (likewise for dQ when it comes from
+ *   the materialised-dS GEMM; the streaming dQ kernel writes dq_acc whole).  dims[3] receives
+ *   {acc_ld, nproj_ld, feat_ld}.  Returns FIPA_TRAIN_LAYOUT_SLOTS. */
+#define FIPA_TRAIN_LAYOUT_SLOTS 11
 int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_t L, int64_t* offsets,
                                       int64_t* dims);
 int fipa_layer_backward_launches(const fipa_layer* layer);

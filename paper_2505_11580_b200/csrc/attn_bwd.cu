@@ -1067,6 +1067,10 @@ void launch_attn_bwd(const LayerDims& d, const AttnBwdArgs& a, cudaStream_t stre
         g.K = a.L;
         g.batch = static_cast<int>(BH);
         g.batch_h = d.heads;
+        if (a.dq16 != nullptr) {  // bf16 copy for the unpack; fp32 only for the point / translation chunks
+            g.C16 = a.dq16 + int64_t(a.q0) * d.heads * a.acc_ld;
+            g.c16_f32_chunks = chunk_mask(d.c, d.zq, d.dqk_mma);
+        }
         launch_gemm_bf16(g, stream);
         which &= ~2;
     }

@@ -540,24 +540,22 @@ __device__ __forceinline__ float acc_at(const float* f, const __nv_bfloat16* b, 
     if constexpr (H16) return __bfloat162float(b[i]);
     else return __ldg(f + i);
 }
-// Scalar-column pair (even element i) of accumulator tsel (0 dQ, 1 dK, 2 dV): dQ always fp32.
-template <bool H16>
+// Scalar-column pair (even element i) of accumulator tsel (0 dQ, 1 dK, 2 dV), from the bf16
+// copies where they exist (Q16: dQ, H16: dK / dV).
+template <bool H16, bool Q16>
 __device__ __forceinline__ float2 acc2_sel(const BwdUnpackArgs& a, int tsel, int64_t i) {
-    if constexpr (H16) {
-        if (tsel != 0) {
-            const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>((tsel == 1 ? a.dk16 : a.dv16) + i));
-            return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
-        }
-        return __ldg(reinterpret_cast<const float2*>(a.dq_acc + i));
-    } else {
-        return __ldg(reinterpret_cast<const float2*>((tsel == 0 ? a.dq_acc : (tsel == 1 ? a.dk_acc : a.dv_acc)) + i));
+    if ((tsel == 0 && Q16) || (tsel != 0 && H16)) {
+        const __nv_bfloat16* b = tsel == 0 ? a.dq16 : (tsel == 1 ? a.dk16 : a.dv16);
+        const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(b + i));
+        return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
     }
+    return __ldg(reinterpret_cast<const float2*>((tsel == 0 ? a.dq_acc : (tsel == 1 ? a.dk_acc : a.dv_acc)) + i));
 }
 
 // FAST: H <= 8 heads, one pair column per thread, the row's scalar columns in kBatchF float2 per
 // thread (every training config); the general form otherwise.  (Two instantiations so the fast
 // loop's register budget holds only its 8 head partials: spills there cost ~2x.)
-template <bool ACC16, bool FAST>
+template <bool ACC16, bool Q16, bool FAST>
 __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpackArgs a) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
@@ -595,26 +593,26 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
     // raw loaded bits, converted only at use (a conversion right after a load would wait for it
     // and serialise the row's loads: measured 2x on the bf16 copies)
     struct RowLoads {
-        float qq[8];
-        uint32_t kq[8], vq[8];  // fp32 bits, or a bf16 in the low half (ACC16)
-        uint2 v[kBatchF];       // fp32 pair, or a bf16 pair in .x (ACC16, dK / dV columns)
+        uint32_t qq[8], kq[8], vq[8];  // fp32 bits, or a bf16 in the low half (Q16 / ACC16)
+        uint2 v[kBatchF];              // fp32 pair, or a bf16 pair in .x
         float z2v, s1;
     };
     auto raw16 = [](const __nv_bfloat16* b, int64_t i) -> uint32_t {
         return __ldg(reinterpret_cast<const unsigned short*>(b + i));
     };
     auto as_f = [](uint32_t r) { return ACC16 ? __uint_as_float(r << 16) : __uint_as_float(r); };
+    auto as_fq = [](uint32_t r) { return Q16 ? __uint_as_float(r << 16) : __uint_as_float(r); };
     const int total = 3 * H * half_c;
     auto load_row = [&](int64_t row, RowLoads& L) {
         const int64_t base = row * H * acc_h;
         L.z2v = __ldg(a.z2 + row * rdz + tid);
         L.s1 = __ldg(a.dz1_epi + row * rdz + tid);
-        const float* qp = a.dq_acc + base + zq + tid;
         const int64_t ko = base + zq + tid, vo = base + c + tid;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int h = min(u, H - 1);
-            L.qq[u] = __ldg(qp + h * acc_h);
+            if constexpr (Q16) L.qq[u] = raw16(a.dq16, ko + h * acc_h);
+            else L.qq[u] = __float_as_uint(__ldg(a.dq_acc + ko + h * acc_h));
             if constexpr (ACC16) {
                 L.kq[u] = raw16(a.dk16, ko + h * acc_h);
                 L.vq[u] = raw16(a.dv16, vo + h * acc_h);
@@ -629,8 +627,9 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
             const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
             const int h = rem / half_c, cc = 2 * (rem - h * half_c);
             const int64_t i = base + h * acc_h + cc;
-            if (ACC16 && tsel != 0) {
-                L.v[u].x = __ldg(reinterpret_cast<const unsigned int*>((tsel == 1 ? a.dk16 : a.dv16) + i));
+            if ((ACC16 && tsel != 0) || (Q16 && tsel == 0)) {
+                L.v[u].x = __ldg(reinterpret_cast<const unsigned int*>(
+                    (tsel == 0 ? a.dq16 : (tsel == 1 ? a.dk16 : a.dv16)) + i));
                 L.v[u].y = 0u;
             } else {
                 L.v[u] = __ldg(reinterpret_cast<const uint2*>(
@@ -645,7 +644,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
         for (int u = 0; u < 8; ++u) {
             if (u < H) {
                 const float k2 = kLn2 * as_f(L.kq[u]);
-                s1 += L.qq[u];
+                s1 += as_fq(L.qq[u]);
                 s2 += s_wlb[u * dz + dd] * k2 + as_f(L.vq[u]);
                 pw[u] = fmaf(k2, L.z2v, pw[u]);
             }
@@ -661,7 +660,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
                 const bool kcol = idx >= H * half_c && idx < 2 * H * half_c;
                 const float sc = kcol ? kscale : 1.f;
                 float vx, vy;
-                if (ACC16 && idx >= H * half_c) {  // dK / dV: a bf16 pair
+                if (idx >= H * half_c ? ACC16 : Q16) {  // a bf16 pair
                     vx = __uint_as_float(L.v[u].x << 16);
                     vy = __uint_as_float(L.v[u].x & 0xFFFF0000u);
                 } else {
@@ -700,7 +699,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int h = min(h0 + u, H - 1);
-                    qq[u] = __ldg(a.dq_acc + rbase + h * acc_h + zq + e);
+                    qq[u] = acc_at<Q16>(a.dq_acc, a.dq16, rbase + h * acc_h + zq + e);
                     kq[u] = acc_at<ACC16>(a.dk_acc, a.dk16, rbase + h * acc_h + zq + e);
                     vq[u] = acc_at<ACC16>(a.dv_acc, a.dv16, rbase + h * acc_h + c + e);
                 }
@@ -732,7 +731,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
                     const int tsel = idx / (H * half_c), rem = idx - tsel * (H * half_c);
                     const int h = rem / half_c, cc = 2 * (rem - h * half_c);
                     const int64_t i = rbase + h * acc_h + cc;
-                    v[u] = acc2_sel<ACC16>(a, tsel, i);
+                    v[u] = acc2_sel<ACC16, Q16>(a, tsel, i);
                     dst[u] = tsel * H * c + h * c + cc;
                     if (tsel == 1) {
                         v[u].x *= kscale;
@@ -749,7 +748,7 @@ __global__ void __launch_bounds__(256, 2) bwd_unpack_kernel(LayerDims d, BwdUnpa
                 const int tsel = idx / (H * c), rem = idx - tsel * (H * c);
                 const int h = rem / c, cc = rem - h * c;
                 const int64_t i = rbase + h * acc_h + cc;
-                const float x = tsel == 0 ? __ldg(a.dq_acc + i)
+                const float x = tsel == 0 ? acc_at<Q16>(a.dq_acc, a.dq16, i)
                                           : (tsel == 1 ? acc_at<ACC16>(a.dk_acc, a.dk16, i) : acc_at<ACC16>(a.dv_acc, a.dv16, i));
                 dp[tsel * H * c + h * c + cc] = __float2bfloat16_rn(x * (tsel == 1 ? kscale : 1.f));
             }
@@ -976,8 +975,12 @@ void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t 
     const size_t smem = sizeof(float) * 2 * size_t(d.heads) * d.d_z;
     if ((a.dk16 == nullptr) != (a.dv16 == nullptr)) throw std::invalid_argument("bwd_unpack: dk16 and dv16 go together");
     const bool fast = unpack_fast(d, a.acc_ld, a.nproj_ld);
-    auto kern = a.dk16 != nullptr ? (fast ? bwd_unpack_kernel<true, true> : bwd_unpack_kernel<true, false>)
-                                  : (fast ? bwd_unpack_kernel<false, true> : bwd_unpack_kernel<false, false>);
+    using K = void (*)(LayerDims, BwdUnpackArgs);
+    const K kerns[8] = {bwd_unpack_kernel<false, false, false>, bwd_unpack_kernel<false, false, true>,
+                        bwd_unpack_kernel<false, true, false>,  bwd_unpack_kernel<false, true, true>,
+                        bwd_unpack_kernel<true, false, false>,  bwd_unpack_kernel<true, false, true>,
+                        bwd_unpack_kernel<true, true, false>,   bwd_unpack_kernel<true, true, true>};
+    const K kern = kerns[(a.dk16 != nullptr ? 4 : 0) + (a.dq16 != nullptr ? 2 : 0) + (fast ? 1 : 0)];
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     const int sms = device_sm_count();
     const int64_t groups = (BL + kUnpackRows - 1) / kUnpackRows;

@@ -494,6 +494,7 @@ int fipa_layer_train_workspace_layout(const fipa_layer* layer, int64_t B, int64_
     offsets[7] = off(w.dfeat);
     offsets[8] = w.dk16 ? off(w.dk16) : -1;
     offsets[9] = w.dv16 ? off(w.dv16) : -1;
+    offsets[10] = w.dq16 ? off(w.dq16) : -1;
     if (dims != nullptr) {
         dims[0] = layer->impl->acc_ld();
         dims[1] = layer->impl->nproj_ld();

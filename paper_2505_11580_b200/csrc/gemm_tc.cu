@@ -72,6 +72,8 @@ struct EpiParams {
     int batch, batch_h;  // batched products (see GemmArgs)
     int a_blk, b_blk;    // MN-major operand loaded as ONE 4-D box of 64-column blocks (ld % 64 == 0)
     bool tma_c16 = false;  // plain bf16 C: two 32-column chunks per 32 x 64 box, TMA stores
+    bool c16_split = false;      // batched fp32 C with a bf16 copy (GemmArgs::C16)
+    uint32_t c16_f32_chunks = 0;  // chunks also written in fp32
 };
 
 #ifdef FIPA_GEMM_TRACE
@@ -93,7 +95,8 @@ template <int BN, bool A_MN, bool B_MN, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB,
-                     const __grid_constant__ CUtensorMap mapC, EpiParams p) {
+                     const __grid_constant__ CUtensorMap mapC,
+                     const __grid_constant__ CUtensorMap mapC16, EpiParams p) {
     using Cfg = GemmCfg<BN, TF32>;
     constexpr int BK = Cfg::BK;
     static_assert(!TF32 || (!A_MN && !B_MN), "tf32 GEMM: K-major operands only");
@@ -326,6 +329,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     continue;
                 }
+                if (p.c16_split) {
+                    // bf16 copy of every chunk pair (buffer 0, stored after the odd chunk) and fp32
+                    // boxes of the flagged chunks (buffer 1); explicit waits order the two buffers
+                    const int hsel = (c0 >> 5) & 1;
+                    uint8_t* b16 = my_stage;
+                    uint8_t* b32 = my_stage + 32 * 128;
+                    if (hsel == 0) {
+                        if (lane == 0) ptx::bulk_wait_group_read<0>();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        *reinterpret_cast<uint4*>(b16 + lane * 128 + (((4 * hsel + q) ^ (lane & 7)) << 4)) = w;
+                    }
+                    if (hsel == 1 || col0 + 32 >= p.N) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC16, b16, col0 - 32 * hsel, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                    }
+                    if ((col0 >> 5) < 32 && ((p.c16_f32_chunks >> (col0 >> 5)) & 1u)) {
+                        if (hsel == 1) {  // buffer 1's previous fp32 box (chunk c0 - 32) has been read
+                            if (lane == 0) ptx::bulk_wait_group_read<1>();
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<float4*>(b32 + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC, b32, col0, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                    }
+                    continue;
+                }
                 if (p.tma_c) {
                     // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
                     uint8_t* sb = my_stage + (nstore % Cfg::kCBuf) * (32 * 128);
@@ -408,7 +456,8 @@ template <int BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB,
-                      const __grid_constant__ CUtensorMap mapC, EpiParams p) {
+                      const __grid_constant__ CUtensorMap mapC,
+                     const __grid_constant__ CUtensorMap mapC16, EpiParams p) {
     using Cfg = GemmCfg2<BN>;
     constexpr int BK = Cfg::BK;
     extern __shared__ uint8_t smem_raw[];
@@ -636,6 +685,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     continue;
                 }
+                if (p.c16_split) {
+                    // bf16 copy of every chunk pair (buffer 0, stored after the odd chunk) and fp32
+                    // boxes of the flagged chunks (buffer 1); explicit waits order the two buffers
+                    const int hsel = (c0 >> 5) & 1;
+                    uint8_t* b16 = my_stage;
+                    uint8_t* b32 = my_stage + 32 * 128;
+                    if (hsel == 0) {
+                        if (lane == 0) ptx::bulk_wait_group_read<0>();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 w;
+                        w.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        w.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        w.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        w.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        *reinterpret_cast<uint4*>(b16 + lane * 128 + (((4 * hsel + q) ^ (lane & 7)) << 4)) = w;
+                    }
+                    if (hsel == 1 || col0 + 32 >= p.N) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC16, b16, col0 - 32 * hsel, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                    }
+                    if ((col0 >> 5) < 32 && ((p.c16_f32_chunks >> (col0 >> 5)) & 1u)) {
+                        if (hsel == 1) {  // buffer 1's previous fp32 box (chunk c0 - 32) has been read
+                            if (lane == 0) ptx::bulk_wait_group_read<1>();
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<float4*>(b32 + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_4d(&mapC, b32, col0, zh, m0 + quad * 32, zo);
+                            ptx::bulk_commit_group();
+                        }
+                    }
+                    continue;
+                }
                 if (p.tma_c) {
                     // this warp's 32 rows x 32 columns -> swizzled staging -> one TMA store
                     uint8_t* sb = my_stage + (nstore % Cfg::kCBuf) * (32 * 128);
@@ -759,12 +853,24 @@ void launch_impl(const GemmArgs& a, cudaStream_t stream) {
         const uint32_t cb[4] = {32, 1, 32, 1};
         mapC = make_map_4d_f32_strided(a.C, cd, cs, cb);
     }
+    CUtensorMap mapC16 = mapC;
+    if (a.C16 != nullptr) {
+        if (!tma_c || nb <= 1) throw std::invalid_argument("gemm: the bf16 copy of C is for batched fp32 products");
+        p.c16_split = true;
+        p.c16_f32_chunks = a.c16_f32_chunks;
+        const uint64_t cd[4] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(bh), static_cast<uint64_t>(a.M),
+                                nb / bh};
+        const uint64_t cs[3] = {static_cast<uint64_t>(a.ldc_h) * 2, static_cast<uint64_t>(a.ldc) * 2,
+                                static_cast<uint64_t>(a.ldc_b) * 2};
+        const uint32_t cb[4] = {64, 1, 32, 1};
+        mapC16 = make_map_4d_bf16_strided(a.C16, cd, cs, cb);
+    }
     auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, TF32>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);  // per device
     const int units = ((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * std::max(1, a.split_k) * static_cast<int>(nb);
     const int sms = device_sm_count();
     dim3 grid(static_cast<unsigned>(std::min(units, sms)));
-    launch_pdl(kern, grid, dim3(kThreads), size_t(Cfg::kSmem), stream, mapA, mapB, mapC, p);
+    launch_pdl(kern, grid, dim3(kThreads), size_t(Cfg::kSmem), stream, mapA, mapB, mapC, mapC16, p);
 }
 
 // CTA pairs of a kernel resident at once (persistent grid size), cached per (device, kernel).
@@ -827,13 +933,25 @@ void launch_impl2(const GemmArgs& a, cudaStream_t stream) {
         const uint32_t cb[4] = {32, 1, 32, 1};
         mapC = make_map_4d_f32_strided(a.C, cd, cs, cb);
     }
+    CUtensorMap mapC16 = mapC;
+    if (a.C16 != nullptr) {
+        if (!tma_c || nb <= 1) throw std::invalid_argument("gemm: the bf16 copy of C is for batched fp32 products");
+        p.c16_split = true;
+        p.c16_f32_chunks = a.c16_f32_chunks;
+        const uint64_t cd[4] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(bh), static_cast<uint64_t>(a.M),
+                                nb / bh};
+        const uint64_t cs[3] = {static_cast<uint64_t>(a.ldc_h) * 2, static_cast<uint64_t>(a.ldc) * 2,
+                                static_cast<uint64_t>(a.ldc_b) * 2};
+        const uint32_t cb[4] = {64, 1, 32, 1};
+        mapC16 = make_map_4d_bf16_strided(a.C16, cd, cs, cb);
+    }
     auto kern = gemm2_bf16_kernel<BN, A_MN, B_MN>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     const int units = ((a.N + BN - 1) / BN) * ((a.M + 2 * BM - 1) / (2 * BM)) * std::max(1, a.split_k) *
                       static_cast<int>(nb);
     const int pairs = std::min(units, resident_pairs(reinterpret_cast<const void*>(kern), Cfg::kSmem));
     launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kThreads), size_t(Cfg::kSmem), stream, mapA, mapB,
-               mapC, p);
+               mapC, mapC16, p);
 }
 
 }  // namespace

@@ -63,6 +63,10 @@ struct GemmArgs {
     // (plain fp32 C only: no accumulate / split-K / row mask)
     int batch = 1, batch_h = 1;
     int64_t ldc_h = 0, ldc_b = 0;
+    // Batched fp32 C only: also write every column as bf16 to C16 (same element strides), and to
+    // C only the 32-column chunks flagged in c16_f32_chunks (bit k: columns [32k, 32k + 32))
+    __nv_bfloat16* C16 = nullptr;
+    uint32_t c16_f32_chunks = 0;
 };
 void launch_gemm_bf16(const GemmArgs& args, cudaStream_t stream);
 
@@ -214,6 +218,7 @@ struct AttnBwdArgs {
     // chunks that hold point / translation columns (cancellation-sensitive, kept fp32).
     __nv_bfloat16* dk16 = nullptr;
     __nv_bfloat16* dv16 = nullptr;
+    __nv_bfloat16* dq16 = nullptr;  // same for dQ from the materialised-dS GEMM (its epilogue)
 };
 bool attn_bwd_supported(const LayerDims& d);
 // which: 1 = dK/dV kernel, 2 = dQ kernel, 3 = both
@@ -260,6 +265,7 @@ struct BwdUnpackArgs {
     // (null: from dk_acc / dv_acc); the geometry columns always come from the fp32 accumulators
     const __nv_bfloat16* dk16 = nullptr;
     const __nv_bfloat16* dv16 = nullptr;
+    const __nv_bfloat16* dq16 = nullptr;  // (independent of dk16 / dv16: the streaming dQ kernel is fp32)
 };
 void launch_bwd_unpack(const LayerDims& d, const BwdUnpackArgs& a, cudaStream_t stream);
 // Materialised attention backward (FlashIpaLayer::dense_attention_backward), rows of length L with

@@ -590,6 +590,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::carve(void* base, std::int64_t B, std::i
         if (!dense_backward()) {
             w.dk16 = reinterpret_cast<__nv_bfloat16*>(take(BHL * acc_ld() * 2));
             w.dv16 = reinterpret_cast<__nv_bfloat16*>(take(BHL * acc_ld() * 2));
+            w.dq16 = reinterpret_cast<__nv_bfloat16*>(take(BHL * acc_ld() * 2));
         }
         w.dproj = reinterpret_cast<__nv_bfloat16*>(take(BL * nproj_ld() * 2));
         w.dz1_epi = reinterpret_cast<float*>(take(BL * rdz * 4));
@@ -649,6 +650,7 @@ FlashIpaLayer::Workspace FlashIpaLayer::slice(const Workspace& w, std::int64_t b
     v.dv_acc = adv(w.dv_acc, n * H * acc_ld() * 4);
     v.dk16 = adv(w.dk16, n * H * acc_ld() * 2);
     v.dv16 = adv(w.dv16, n * H * acc_ld() * 2);
+    v.dq16 = adv(w.dq16, n * H * acc_ld() * 2);
     v.dproj = adv(w.dproj, n * nproj_ld() * 2);
     v.dz1_epi = adv(w.dz1_epi, n * rdz * 4);
     v.geo_epi = adv(w.geo_epi, n * 12 * 4);
@@ -1328,6 +1330,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
         if (acc16) {
             a.dk16 = ws.dk16;
             a.dv16 = ws.dv16;
+            if (ws.ds != nullptr) a.dq16 = ws.dq16;  // dQ by the GEMM over the stored dS
         }
         if (shard == nullptr && ws.ds != nullptr && ws.ds_ld < L) {
             // query-chunked materialised dS: dK/dV kernel + dQ GEMM per chunk of ds_ld queries
@@ -1360,6 +1363,7 @@ void FlashIpaLayer::backward_impl(std::int64_t B, std::int64_t L, const float* s
             !dense_backward()) {
             a.dk16 = ws.dk16;  // written by the dK/dV kernel above (same condition)
             a.dv16 = ws.dv16;
+            if (ws.ds != nullptr) a.dq16 = ws.dq16;
         }
         a.proj = ws.proj;
         a.rot = rot;

@@ -269,6 +269,7 @@ public:
         float* dv_acc = nullptr;
         __nv_bfloat16* dk16 = nullptr;     // [BH, L, acc_ld] bf16 dK / dV (fused backward: scalar and
         __nv_bfloat16* dv16 = nullptr;     // pair columns; dk_acc / dv_acc keep the geometry chunks)
+        __nv_bfloat16* dq16 = nullptr;     // likewise for dQ from the materialised-dS GEMM
         __nv_bfloat16* dproj = nullptr;    // [BL, nproj_ld]
         float* dz1_epi = nullptr;          // [BL, r d_z]
         float* geo_epi = nullptr;          // [BL, 12] dR | dt of the output epilogue

@@ -60,8 +60,9 @@ def test_backward_both_dq_paths(fipa, ds):
 
 
 def test_dq_paths_agree(fipa):
-    """Same dS values either way (same formula, same bf16 rounding); only the fp32 summation
-    order of dQ differs, so the gradients agree far inside the oracle gate."""
+    """Same dS values either way (same formula, same bf16 rounding); the fp32 summation order of
+    dQ differs, and the GEMM path hands dQ's scalar and pair columns to the unpack in bf16 while the
+    streaming kernel keeps fp32 -- 2^-9-relative roundings, far inside the oracle gate."""
     model = _model(fipa, MAIN, 13)
     batch = make_batch(MAIN, 2, 320, seed=13, mask_frac=0.1, bf16=True)
     dout = np.random.default_rng(13).standard_normal((2, 320, MAIN["d_in"]))
@@ -70,7 +71,7 @@ def test_dq_paths_agree(fipa):
         model.set_tuning(bwd_ds=ds)
         _, got[ds], _, _ = gpu_train_device(model, batch, dout)
     for n in GRADS:
-        assert rel_dev(got[0][n], got[1][n]) < 1e-4, n
+        assert rel_dev(got[0][n], got[1][n]) < 4e-3, n
 
 
 def test_micro_batched_capture_matches_one_chain(fipa):
@@ -186,12 +187,16 @@ def test_attention_backward_stage_parity(fipa, ds):
     # point / translation columns also in fp32 (dK: [c, zq), dV: [c + r d_z, dv_used))
     c, zq, rdz = shape["c"], 176, shape["rank"] * shape["d_z"]
     geo = {"dk": (c, zq), "dv": (c + rdz, c + rdz + 6 + 3 * shape["n_value"])}
+    # (dQ: the streaming kernel (ds = 0) writes fp32 whole; the materialised-dS GEMM a bf16 copy,
+    # slot 10, plus the same fp32 geometry chunks as dK)
+    geo["dq"] = geo["dk"]
     for name, idx, ref in (("dq", 3, dq_r), ("dk", 4, dk_r), ("dv", 5, dv_r)):
         got = ws_view(ws, toff[idx], H * L * acc_ld, "f32").reshape(L, H, acc_ld).transpose(1, 0, 2)
-        if name == "dq":
+        if name == "dq" and ds == 0:
             assert rel_dev(ref[..., :432], got[..., :432]) < 1e-2, name
             continue
-        g16 = ws_view(ws, toff[idx + 4], H * L * acc_ld, "bf16").reshape(L, H, acc_ld).transpose(1, 0, 2)
+        slot16 = {"dq": 10, "dk": 8, "dv": 9}[name]
+        g16 = ws_view(ws, toff[slot16], H * L * acc_ld, "bf16").reshape(L, H, acc_ld).transpose(1, 0, 2)
         assert rel_dev(ref[..., :432], g16[..., :432]) < 1e-2, name
         lo, hi = geo[name]
         lo32, hi32 = lo // 32 * 32, (hi + 31) // 32 * 32
