@@ -7,6 +7,7 @@ using namespace fipa_b200;
 int main(int argc, char** argv) {
     const int M = argc > 1 ? atoi(argv[1]) : 8192, N = argc > 2 ? atoi(argv[2]) : 2048, K = argc > 3 ? atoi(argv[3]) : 512;
     const int bf16out = argc > 4 ? atoi(argv[4]) : 0;
+    const int b_mn = argc > 5 ? atoi(argv[5]) : 0;  // 1: B stored [K][N] (MN-major)
     __nv_bfloat16 *A, *B;
     float* C;
     cudaMalloc(&A, size_t(M) * K * 2);
@@ -15,9 +16,21 @@ int main(int argc, char** argv) {
     cudaMemset(A, 0, size_t(M) * K * 2);
     cudaMemset(B, 0, size_t(N) * K * 2);
     GemmArgs g;
-    g.A = A; g.B = B; g.C = C; g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = K; g.ldc = N; g.out_bf16 = bf16out;
+    g.A = A; g.B = B; g.C = C; g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = b_mn ? N : K; g.ldc = N; g.out_bf16 = bf16out;
+    g.b_mn_major = b_mn != 0;
     for (int i = 0; i < 5; ++i) launch_gemm_bf16(g, 0);
     cudaDeviceSynchronize();
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int i = 0; i < 20; ++i) launch_gemm_bf16(g, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("M=%d N=%d K=%d bf16out=%d b_mn=%d: %.4f ms per launch, %.1f TFLOP/s\n", M, N, K, bf16out, b_mn, ms / 20,
+           2.0 * M * N * K / (ms / 20 * 1e-3) / 1e12);
     long long t[2][8][24];
     cudaMemcpyFromSymbol(t, g_gemm_trace, sizeof(t));
     const long long t0 = t[1][0][0];
