@@ -32,7 +32,17 @@ if which in ("all", "bwd"):
     d2 = np.random.default_rng(1).standard_normal((2, 512, MAIN["d_in"]))
     m.set_tuning(bwd_ds=-1, ds_cap_mb=4, micro=2)
     gpu_train_device(m, b2, d2)
+    # whole-query materialised dS with the micro-batched capture (bf16 dQ / dK / dV hand-off)
+    m.set_tuning(ds_cap_mb=2048)
+    gpu_train_device(m, b2, d2)
     print("bwd ok", flush=True)
+if which in ("all", "wide"):
+    # z_factor_rank 3: the materialised backward (batched GEMMs + streaming softmax kernels)
+    r3 = dict(MAIN, rank=3)
+    m = fipa.Model(**r3, precision="bf16", seed=0, enforce_head_cap=False)
+    b3 = make_batch(r3, 2, 192, seed=5, mask_frac=0.1, bf16=True)
+    gpu_train_device(m, b3, np.random.default_rng(5).standard_normal((2, 192, r3["d_in"])))
+    print("wide ok", flush=True)
 if which in ("all", "f32"):
     m = fipa.Model(**MAIN, precision="f32", seed=0, enforce_head_cap=False)
     gpu_forward_device(m, batch)
