@@ -8,6 +8,10 @@
 #include <pybind11/stl.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <new>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -18,13 +22,65 @@
 namespace py = pybind11;
 
 namespace {
-// Fresh output arrays are first touched by the host pipeline's conversion threads: ask for
-// transparent huge pages (THP "madvise" mode on the GPU boxes) so a 68 MB gradient set costs tens
-// of 2 MB faults instead of ~17k 4 KB ones (measured ~7 ms per 68 MB, tools/host_path_probe.py).
-void hugepage_hint(void* p, size_t bytes) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p), huge = uintptr_t(2) << 20;
-    const uintptr_t lo = (a + huge - 1) & ~(huge - 1), hi = (a + bytes) & ~(huge - 1);
-    if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+// Large output arrays of the host entry points come from a recycling pool of 2 MB-aligned buffers,
+// handed back when Python frees the array: the allocator otherwise maps fresh pages for each
+// call's outputs and the first touch costs ~7 ms per 68 MB gradient set (the float64 flash_grad
+// measured 14 ms per call at B=8 L=1024 against 8 ms with recycled pages).  Bounded: at most
+// kMaxHeld bytes wait in the pool.
+class HostBufPool {
+public:
+    static HostBufPool& get() {
+        static HostBufPool* pool = new HostBufPool();  // never destroyed: arrays may outlive statics
+        return *pool;
+    }
+    void* take(size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = free_.find(bytes);
+            if (it != free_.end() && !it->second.empty()) {
+                void* p = it->second.back();
+                it->second.pop_back();
+                held_ -= bytes;
+                return p;
+            }
+        }
+        void* p = std::aligned_alloc(size_t(2) << 20, bytes);
+        if (p == nullptr) throw std::bad_alloc();
+        madvise(p, bytes, MADV_HUGEPAGE);
+        return p;
+    }
+    void give(void* p, size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (held_ + bytes > kMaxHeld) {
+            std::free(p);
+            return;
+        }
+        free_[bytes].push_back(p);
+        held_ += bytes;
+    }
+
+private:
+    static constexpr size_t kMaxHeld = size_t(1) << 30;
+    std::mutex mu_;
+    std::map<size_t, std::vector<void*>> free_;
+    size_t held_ = 0;
+};
+
+// C-contiguous output array: pooled when >= 1 MB, a plain numpy allocation otherwise.
+template <class T>
+py::array_t<T> host_out(const std::vector<py::ssize_t>& shape) {
+    size_t n = 1;
+    for (auto d : shape) n *= size_t(d);
+    if (n * sizeof(T) < (size_t(1) << 20)) return py::array_t<T>(shape);
+    const size_t huge = size_t(2) << 20, bytes = (n * sizeof(T) + huge - 1) / huge * huge;
+    void* p = HostBufPool::get().take(bytes);
+    auto* info = new std::pair<void*, size_t>(p, bytes);
+    py::capsule owner(info, [](void* v) {
+        auto* i = static_cast<std::pair<void*, size_t>*>(v);
+        HostBufPool::get().give(i->first, i->second);
+        delete i;
+    });
+    return py::array_t<T>(shape, static_cast<T*>(p), owner);
 }
 }  // namespace
 
@@ -271,9 +327,8 @@ public:
         }
         std::vector<py::ssize_t> shape = batched ? std::vector<py::ssize_t>{B, L, (py::ssize_t)cfg_.d_in}
                                                  : std::vector<py::ssize_t>{L, (py::ssize_t)cfg_.d_in};
-        py::array_t<T> out(shape);
+        py::array_t<T> out = host_out<T>(shape);
         T* op = out.mutable_data();
-        hugepage_hint(op, size_t(out.size()) * sizeof(T));
         int rc;
         {
             py::gil_scoped_release nogil;
@@ -523,12 +578,9 @@ public:
             for (auto& v : m) v = v ? 1 : 0;
             mp = m.data();
         }
-        auto like = [](const Arr& a) {
-            return py::array_t<T>(std::vector<py::ssize_t>(a.shape(), a.shape() + a.ndim()));
-        };
+        auto like = [](const Arr& a) { return host_out<T>(std::vector<py::ssize_t>(a.shape(), a.shape() + a.ndim())); };
         py::array_t<T> out = like(s), gs = like(s), gz1 = like(z1), gz2 = like(z2), gr = like(rotations),
                        gt = like(translations);
-        for (auto* a : {&out, &gs, &gz1, &gz2}) hugepage_hint(a->mutable_data(), size_t(a->size()) * sizeof(T));
         const uint64_t nw = fipa_layer_num_weights(layer_);
         py::array_t<T> gw(static_cast<py::ssize_t>(nw));  // weight grads land here directly
         T* gwp = gw.mutable_data();
