@@ -42,6 +42,10 @@ int main(int argc, char** argv) {
         cudaMalloc(&a.ds, BH * L * size_t(a.ds_ld) * 2);
     }
     if (argc > 5) sscanf(argv[5], "%d,%d,%d,%d,%d", &a.ring[0], &a.ring[1], &a.ring[2], &a.ring[3], &a.ring[4]);
+    if (!(argc > 6 && atoi(argv[6]) == 0)) {  // bf16 dK / dV hand-off (the layer's default)
+        cudaMalloc(&a.dk16, BH * L * 448 * 2);
+        cudaMalloc(&a.dv16, BH * L * 448 * 2);
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
