@@ -137,6 +137,25 @@ def test_workspace_layout_is_consistent(fipa):
     assert off32[1] == -1  # no bf16 cast buffer on the fp32 path
 
 
+def test_train_workspace_layout_slots(fipa):
+    """Training layout: 11 slots; the fused backward's bf16 dQ / dK / dV copies (slots 8-10) exist
+    at rank 2 and are absent (-1) for the materialised rank 3-4 backward, whose accumulator stride
+    widens with the lifted rows."""
+    m = fipa.Model(**MAIN, precision="bf16", enforce_head_cap=False)
+    off, dims = m.train_workspace_layout(2, 512)
+    assert len(off) == 11 and dims[0] == 448
+    assert all(o >= 0 for o in off)
+    assert len(set(off)) == 11 and all(o % 256 == 0 for o in off)
+    assert m.train_workspace_size(2, 512) > max(off)
+    m3 = fipa.Model(**dict(MAIN, rank=3), precision="bf16", enforce_head_cap=False)
+    off3, dims3 = m3.train_workspace_layout(2, 512)
+    assert off3[8:] == [-1, -1, -1] and dims3[0] >= 576
+    # the materialised backward's [L, L] intermediates (12 bytes per head, query, key): quadratic in
+    # L per sample group -- f(2L) - 2 f(L) = 2 * 12 H L^2 for the quadratic part
+    excess = m3.train_workspace_size(1, 1024) - 2 * m3.train_workspace_size(1, 512)
+    assert abs(excess - 2 * 12 * MAIN["heads"] * 512 ** 2) < 0.1 * 2 * 12 * MAIN["heads"] * 512 ** 2  # (- constant buffers)
+
+
 def test_quadratic_arm_workspace_is_quadratic_and_flash_linear(fipa):
     """Memory model of the two arms (reference bench.cpp:151-155 estimate_reference_bytes and the
     paper's Fig. 2): the dense arm's workspace grows as (d_z + H) L^2, the flash workspace as L."""
