@@ -22,11 +22,14 @@ def _dev(batch):
     return t
 
 
-@pytest.mark.parametrize("G,B,rank", [(2, 1, 2), (4, 2, 2), (2, 1, 3)])
-def test_emulated_shards_match_unsharded_forward(fipa, G, B, rank):
+@pytest.mark.parametrize("G,B,rank,n_local", [(2, 1, 2, 128), (4, 2, 2, 128), (2, 1, 3, 128), (8, 1, 2, 2048)])
+def test_emulated_shards_match_unsharded_forward(fipa, G, B, rank, n_local):
+    """G query-row shards through the C-ABI blocks (centroid sums -> pack -> rank-major gather ->
+    attend) against the unsharded forward; up to L = 16384 over 8 shards (the cfg4 regime; the
+    oracle comparison only at the small sizes)."""
     shape = dict(MAIN, rank=rank)  # rank 3: the two-pass attention kernel reads the sharded keys
     model = fipa.Model(**shape, precision="bf16", seed=3, enforce_head_cap=False)
-    L = 128 * G
+    L = n_local * G
     batch = make_batch(shape, B, L, seed=31, mask_frac=0.1, bf16=True)
     ref_gpu, _, _ = gpu_forward_device(model, batch)
     t = _dev(batch)
@@ -62,8 +65,9 @@ def test_emulated_shards_match_unsharded_forward(fipa, G, B, rank):
     torch.cuda.synchronize()
     got = torch.cat(outs, 1).cpu().numpy().astype(np.float64)
     assert rel_dev(ref_gpu, got) < 1e-3  # only the centroid's summation order differs
-    ref = oracle_forward(shape, oracle_weights_for(model, "bf16"), batch)
-    assert rel_dev(ref, got) < BF16_TOL
+    if L <= 1024:
+        ref = oracle_forward(shape, oracle_weights_for(model, "bf16"), batch)
+        assert rel_dev(ref, got) < BF16_TOL
 
 
 def test_nccl_world1_gradient_all_reduce_is_identity(fipa):
