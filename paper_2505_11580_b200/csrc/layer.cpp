@@ -823,7 +823,7 @@ void FlashIpaLayer::forward(std::int64_t B, std::int64_t L, const float* s, cons
         }
         GraphKey key{train ? 1 : 0, B, L, {s, z1, z2, rot, trans, mask, out, workspace}, workspace_bytes};
         if (run_graph(key, stream, [&](cudaStream_t cs) {
-                if (micro_chunks(B, L, train) > 1 && !(train && dense_backward()))
+                if (micro_chunks(B, L, true) > 1 && !(train && dense_backward()))
                     forward_micro(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train);
                 else
                     forward_impl(B, L, s, z1, z2, rot, trans, mask, out, workspace, workspace_bytes, cs, train,
@@ -1535,11 +1535,11 @@ void FlashIpaLayer::dense_attention_backward(std::int64_t B, std::int64_t L, con
     }
 }
 
-int FlashIpaLayer::micro_chunks(std::int64_t B, std::int64_t L, bool train) const {
+int FlashIpaLayer::micro_chunks(std::int64_t B, std::int64_t L, bool forward) const {
     if (tuning_.micro < 2 || timing_ || cfg_.precision != Precision::bf16 || B < 2) return 1;
     // each chunk's weight-gradient GEMMs run split-K >= 2 over K = (B / chunks) * L
     if ((B / 2) * L < 256) return 1;
-    int n = int(std::min<std::int64_t>(train ? tuning_.micro : std::max(tuning_.micro, 4), B));
+    int n = int(std::min<std::int64_t>(forward ? std::max(tuning_.micro, 4) : tuning_.micro, B));
     n = std::min(n, int(sizeof(side_streams_) / sizeof(side_streams_[0])) + 1);
     while (n > 2 && (B / n) * L < 256) --n;  // chunks of at least 256 residues
     return n;
@@ -1561,7 +1561,7 @@ void FlashIpaLayer::forward_micro(std::int64_t B, std::int64_t L, const float* s
     REQUIRE(workspace != nullptr && workspace_bytes >= full.bytes, "workspace too small: need ", full.bytes,
             " bytes, got ", workspace_bytes);
     ensure_side_streams();
-    const int n = micro_chunks(B, L, train);
+    const int n = micro_chunks(B, L, true);
     const std::size_t rdz = std::size_t(dims_.rank) * dims_.d_z, din = dims_.d_in;
     cuda_check(cudaEventRecord(fork_ev_, stream), "event record");
     for (int c = 0; c < n; ++c) {
