@@ -587,7 +587,7 @@ def run_ours(args, shape):
                          if args.precision == "bf16" else roofline_f32(achieved, flops, peak, peak_kind)),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (model.forward_launches() + (model.backward_launches() if train else 0)) * args.steps,
+            "gpu_launches": model.step_launches(B, L, train) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -809,7 +809,7 @@ def run_trunk(args, shape):
                          "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
                          "algorithmic": f"layers*2*B*H*L^2*(D_qk+D_v) = {flops:.4g} FLOP per step"},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": trunk.forward_launches() * args.steps, "clocks": clk.summary(),
+            "gpu_launches": trunk.step_launches(B, L) * args.steps, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

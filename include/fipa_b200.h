@@ -300,6 +300,8 @@ int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L, const float* s, 
                        const float* rot, const float* trans, const uint8_t* mask, float* s_out, float* rot_out,
                        float* trans_out, void* workspace, size_t workspace_bytes, void* stream);
 int fipa_trunk_forward_launches(const fipa_trunk* trunk);
+/* Kernels of one fipa_trunk_forward at (B, L), sample chains and micro-batch chains included. */
+int fipa_trunk_step_launches(const fipa_trunk* trunk, int64_t B, int64_t L);
 
 /* ----------------------------------------------------------- pair-factor producer (§8 f2)
  * knn_distogram (proj/src/pair_features.cpp:10-64): translations [B,L,3] -> features
@@ -325,8 +327,13 @@ int fipa_build_factors(int64_t rows, uint64_t f, const float* features, uint64_t
 int fipa_build_factors_host(int64_t rows, uint64_t f, const double* features, uint64_t r, uint64_t d_z,
                             const double* w1, const double* w2, double* z1, double* z2, int precision);
 
-/* Number of kernels fipa_layer_forward launches per call for this configuration. */
+/* Number of kernels fipa_layer_forward launches per call for this configuration (one sample
+ * chain). */
 int fipa_layer_forward_launches(const fipa_layer* layer);
+/* Kernels of one device call at (B, L) with the layer's tuning, micro-batch chains included:
+ * train = 0 the forward, 1 the training forward + backward (the measured step; CUPTI counts of
+ * tools/count_launches.py agree: 16 and 39 at B=8 L=1024). */
+int fipa_layer_step_launches(const fipa_layer* layer, int64_t B, int64_t L, int train);
 
 /* Kernel-selection / tuning knobs of a layer.  Fixed per layer: seeded once at creation from
  * the FIPA_* environment variables named below (A/B experiments; defaults = the measured-best

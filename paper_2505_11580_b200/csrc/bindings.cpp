@@ -412,6 +412,9 @@ public:
     }
 
     int forward_launches() const { return fipa_layer_forward_launches(layer_); }
+    int step_launches(int64_t B, int64_t L, bool train) const {
+        return fipa_layer_step_launches(layer_, B, L, train ? 1 : 0);
+    }
     int backward_launches() const { return fipa_layer_backward_launches(layer_); }
     size_t sharded_workspace_size(int64_t B, int64_t L, int world) const {
         return fipa_layer_sharded_workspace_size(layer_, B, L, world);
@@ -753,6 +756,7 @@ public:
         check(rc);
     }
     int forward_launches() const { return fipa_trunk_forward_launches(trunk_); }
+    int step_launches(int64_t B, int64_t L) const { return fipa_trunk_step_launches(trunk_, B, L); }
 
 private:
     fipa_config cfg_{};
@@ -890,6 +894,7 @@ PYBIND11_MODULE(_fipa_b200, m) {
              py::arg("out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
         .def("workspace_layout", &Model::workspace_layout, py::arg("B"), py::arg("L"))
         .def("forward_launches", &Model::forward_launches)
+        .def("step_launches", &Model::step_launches, py::arg("B"), py::arg("L"), py::arg("train"))
         .def("backward_launches", &Model::backward_launches)
         .def("sharded_workspace_size", &Model::sharded_workspace_size, py::arg("B"), py::arg("L"), py::arg("world"))
         .def("forward_sharded_device", &Model::forward_sharded_device, py::arg("comm"), py::arg("B"), py::arg("L"),
@@ -956,5 +961,6 @@ PYBIND11_MODULE(_fipa_b200, m) {
         .def("forward_device", &Trunk::forward_device, py::arg("B"), py::arg("L"), py::arg("s"), py::arg("z1"),
              py::arg("z2"), py::arg("rot"), py::arg("trans"), py::arg("mask"), py::arg("s_out"), py::arg("rot_out"),
              py::arg("trans_out"), py::arg("workspace"), py::arg("workspace_bytes"), py::arg("stream"))
-        .def("forward_launches", &Trunk::forward_launches);
+        .def("forward_launches", &Trunk::forward_launches)
+        .def("step_launches", &Trunk::step_launches, py::arg("B"), py::arg("L"));
 }

@@ -367,6 +367,10 @@ int fipa_layer_forward_launches(const fipa_layer* layer) {
     return layer ? layer->impl->launches_per_forward() : 0;
 }
 
+int fipa_layer_step_launches(const fipa_layer* layer, int64_t B, int64_t L_, int train) {
+    return layer && B >= 1 && L_ >= 1 ? layer->impl->step_launches(B, L_, train != 0) : 0;
+}
+
 int fipa_layer_get_tuning(const fipa_layer* layer, fipa_tuning* out) {
     return guarded([&] {
         if (layer == nullptr || out == nullptr) throw fipa_b200::ValueError("null layer or tuning");
@@ -739,6 +743,9 @@ int fipa_trunk_forward(fipa_trunk* trunk, int64_t B, int64_t L_, const float* s,
 }
 
 int fipa_trunk_forward_launches(const fipa_trunk* trunk) { return trunk ? trunk->impl.launches_per_forward() : 0; }
+int fipa_trunk_step_launches(const fipa_trunk* trunk, int64_t B, int64_t L) {
+    return trunk && B >= 1 && L >= 1 ? trunk->impl.step_launches(B, L) : 0;
+}
 
 }  // extern "C"
 

@@ -713,6 +713,19 @@ int FlashIpaLayer::launches_per_backward() const {
     return 12;
 }
 
+int FlashIpaLayer::step_launches(std::int64_t B, std::int64_t L, bool train) const {
+    // the captured graphs run micro_chunks(...) sample chains (forward_micro / backward_micro): every
+    // chain launches the per-call kernels; the backward's finish kernel runs once after the join
+    const bool graphs = tuning_.graphs && !timing_;
+    const int nf = graphs && !(train && dense_backward()) ? micro_chunks(B, L, true) : 1;
+    int n = nf * launches_per_forward();
+    if (train) {
+        const int nb = graphs && !dense_backward() ? micro_chunks(B, L) : 1;
+        n += nb > 1 ? nb * (launches_per_backward() - 1) + 1 : launches_per_backward();
+    }
+    return n;
+}
+
 int FlashIpaLayer::launches_per_forward() const {
     // fp32 tensor-core path: recenter, split s, projection GEMM, pack, split q/k/v, attention,
     // split feat, output GEMM

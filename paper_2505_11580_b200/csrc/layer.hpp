@@ -227,6 +227,8 @@ public:
     bool fused_backward_supported() const;
     bool dense_backward() const;
     int launches_per_backward() const;
+    // kernels of one device call (graph replay with its micro-batch chains) at (B, L)
+    int step_launches(std::int64_t B, std::int64_t L, bool train) const;
 
 
     void forward_host(std::int64_t B, std::int64_t L, const double* s, const double* z1,

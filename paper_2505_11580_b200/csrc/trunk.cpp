@@ -140,4 +140,12 @@ void Trunk::forward(std::int64_t B, std::int64_t L, const float* s, const float*
 
 int Trunk::launches_per_forward() const { return n_layers() * (layers_[0]->launches_per_forward() + 1); }
 
+int Trunk::step_launches(std::int64_t B, std::int64_t L) const {
+    const int n = chains(B);
+    int total = 0;
+    for (int c = 0; c < n; ++c)
+        total += n_layers() * (layers_[0]->step_launches(B * (c + 1) / n - B * c / n, L, false) + 1);
+    return total;
+}
+
 }  // namespace fipa_b200

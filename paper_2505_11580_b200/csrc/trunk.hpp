@@ -29,6 +29,7 @@ public:
                  const float* trans, const std::uint8_t* mask, float* s_out, float* rot_out, float* trans_out,
                  void* workspace, std::size_t workspace_bytes, cudaStream_t stream);
     int launches_per_forward() const;
+    int step_launches(std::int64_t B, std::int64_t L) const;  // chains included
 
 private:
     void upload();
