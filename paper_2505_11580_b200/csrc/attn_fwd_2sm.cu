@@ -959,9 +959,16 @@ void launch_attn_fwd_2sm(const LayerDims& d, const AttnArgs& a, cudaStream_t str
     const int smem = lay.total + 1024;
     if (a.o_save != nullptr && d.dv_pad % 32 != 0)
         throw std::invalid_argument("attention: O_hat rows must be a multiple of 32 floats");
-    const CUtensorMap mapO = a.o_save != nullptr
-                                 ? make_map_4d_f32(a.o_save, d.dv_pad, d.heads, a.L, a.B, 32, 1, BM, 1)
-                                 : mapV;
+    // O_hat rows keep the dv_pad stride; the map stops at dv_used, so the padding columns of the
+    // last 32-column chunk are not written (prep keeps them out of D)
+    CUtensorMap mapO = mapV;
+    if (a.o_save != nullptr) {
+        const uint64_t od[4] = {uint64_t(d.dv_used), uint64_t(d.heads), uint64_t(a.L), uint64_t(a.B)};
+        const uint64_t os[3] = {uint64_t(d.dv_pad) * 4, uint64_t(d.dv_pad) * d.heads * 4,
+                                uint64_t(d.dv_pad) * d.heads * a.L * 4};
+        const uint32_t ob[4] = {32, 1, BM, 1};
+        mapO = make_map_4d_f32_strided(a.o_save, od, os, ob);
+    }
     cudaFuncSetAttribute(attn_fwd_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int qtiles = (a.L + BM - 1) / BM;
     dim3 grid(static_cast<unsigned>((qtiles + 1) / 2 * 2), static_cast<unsigned>(a.B * p.hc));
