@@ -96,6 +96,13 @@ def test_micro_batched_capture_matches_one_chain(fipa):
         assert rel_dev(ref[n], res[2][1][n]) < BF16_TOL, n
 
 
+@pytest.mark.parametrize("L", [200, 1024])
+def test_backward_rank1(fipa, L):
+    """z_factor_rank 1 (lifted widths 304 / 298: the fused kernels with narrower rows, prep's rank-1
+    warp kernel, the general unpack form, rank-1 bf16 hand-off chunk masks) against the oracle."""
+    _check(fipa, dict(MAIN, rank=1), 2, L, seed=60 + L, mask_frac=0.1)
+
+
 @pytest.mark.parametrize("rank,B,L", [(3, 2, 200), (4, 2, 320), (3, 1, 257)])
 def test_backward_wide_lifted_rows(fipa, rank, B, L):
     """z_factor_rank 3-4 (lifted widths 576-704, wider than the fused attention backward holds):
