@@ -103,6 +103,13 @@ def test_backward_rank1(fipa, L):
     _check(fipa, dict(MAIN, rank=1), 2, L, seed=60 + L, mask_frac=0.1)
 
 
+def test_backward_sixteen_heads(fipa):
+    """16 heads with narrower channels (the unpack's general form: more than 8 heads per residue,
+    d(w_l w_bias) partials for 16 heads; the generic prep) against the oracle."""
+    _check(fipa, dict(d_in=128, d_z=64, heads=16, c=64, n_query=4, n_value=8, rank=2), 2, 256, seed=71,
+           mask_frac=0.1)
+
+
 @pytest.mark.parametrize("rank,B,L", [(3, 2, 200), (4, 2, 320), (3, 1, 257)])
 def test_backward_wide_lifted_rows(fipa, rank, B, L):
     """z_factor_rank 3-4 (lifted widths 576-704, wider than the fused attention backward holds):
